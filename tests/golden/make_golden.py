@@ -1,0 +1,157 @@
+"""Generate golden input/output vectors by running the REAL reference package.
+
+Run in the build container only (it needs /root/reference, which does not
+exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+The fixtures it writes (``tests/golden/*.npz``) are committed; the tests read
+only the fixtures.  Inputs are seeded (Philox) and, for the cases the bf16
+GPU path consumes, rounded to bf16-representable float32 values so the same
+numbers can be fed to the device exactly.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round float32 to the nearest bf16 (ties to even), returned as float32."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)) << np.uint32(16)
+    return r.view(np.float32)
+
+
+def main() -> None:
+    sys.path.insert(0, REF_SRC)
+    import flashblock as fb  # the real reference
+    from flashblock.attention import CacheEntry
+
+    rng = np.random.Generator(np.random.Philox(20261017))
+    out: dict[str, np.ndarray] = {}
+    meta: dict[str, dict] = {}
+
+    # -- attention_partial / streamed / merge, fp64 and fp32, ragged sizes --
+    cases = [
+        ("p0", 4, 20, 8, np.float64, 64),
+        ("p1", 3, 50, 8, np.float64, 17),
+        ("p2", 5, 0, 8, np.float64, 64),      # empty sentinel
+        ("p3", 7, 1, 16, np.float32, 64),     # single key
+        ("p4", 33, 257, 64, np.float32, 512),
+        ("p5", 128, 384, 128, np.float32, 512),
+        ("p6", 16, 129, 128, np.float64, 64),
+    ]
+    for name, nq, n, d, dt, tile in cases:
+        q = rng.standard_normal((nq, d)).astype(dt)
+        k = rng.standard_normal((n, d)).astype(dt)
+        v = rng.standard_normal((n, d)).astype(dt)
+        if dt == np.float32:
+            q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
+        p = fb.attention_partial(q, k, v, tile_size=tile)
+        out.update({f"{name}_q": q, f"{name}_k": k, f"{name}_v": v,
+                    f"{name}_out": p.out, f"{name}_lse": p.lognorm})
+        meta[name] = {"nq": nq, "n": n, "d": d, "dtype": np.dtype(dt).name, "tile": tile}
+
+    # streamed + merge at several boundaries (incl. 0 and n)
+    q = rng.standard_normal((6, 32))
+    k = rng.standard_normal((40, 32))
+    v = rng.standard_normal((40, 32))
+    out.update({"s_q": q, "s_k": k, "s_v": v})
+    for b in (0, 1, 17, 39, 40):
+        e, i = fb.attention_streamed(q, k, v, b)
+        out[f"s_b{b}_ext_out"] = e.out
+        out[f"s_b{b}_ext_lse"] = e.lognorm
+        out[f"s_b{b}_int_out"] = i.out
+        out[f"s_b{b}_int_lse"] = i.lognorm
+        out[f"s_b{b}_merged"] = fb.merge_partials(e, i)
+
+    # combine with one side empty / both sides partially empty rows
+    a = fb.attention_partial(q, k[:10], v[:10])
+    bpart = fb.attention_partial(q, k[10:], v[10:])
+    lse_a = a.lognorm.copy()
+    lse_a[[1, 4]] = -np.inf
+    out_a = a.out.copy()
+    out_a[[1, 4]] = 0.0
+    lse_b = bpart.lognorm.copy()
+    lse_b[[4, 5]] = -np.inf
+    out_b = bpart.out.copy()
+    out_b[[4, 5]] = 0.0
+    c = fb.combine_partials(fb.AttnPartial(out_a, lse_a), fb.AttnPartial(out_b, lse_b))
+    out.update({"c_a_out": out_a, "c_a_lse": lse_a, "c_b_out": out_b, "c_b_lse": lse_b,
+                "c_out": c.out, "c_lse": c.lognorm})
+
+    # reuse: cached external from q0, drifted q1
+    q0 = bf16_round(rng.standard_normal((64, 64)).astype(np.float32))
+    kk = bf16_round(rng.standard_normal((300, 64)).astype(np.float32))
+    vv = bf16_round(rng.standard_normal((300, 64)).astype(np.float32))
+    q1 = bf16_round((q0 + 0.3 * rng.standard_normal(q0.shape)).astype(np.float32))
+    ext, _ = fb.attention_streamed(q0, kk, vv, 268)
+    entry = CacheEntry(partial=ext, step_created=0, block_id=0)
+    ro, ri = fb.attention_with_reuse(q1, entry, kk[268:], vv[268:])
+    out.update({"r_q0": q0, "r_q1": q1, "r_k": kk, "r_v": vv, "r_ext_out": ext.out,
+                "r_ext_lse": ext.lognorm, "r_out": ro, "r_int_out": ri.out,
+                "r_int_lse": ri.lognorm})
+
+    # -- sparse: masks over densities, planted blocks, residual outputs --
+    for name, nq, n_ext, n_in, d, kbs, planted in [
+        ("m0", 4, 64, 8, 8, 16, None),
+        ("m1", 8, 160, 8, 16, 16, None),
+        ("m2", 32, 1000, 32, 64, 16, [3, 17, 40]),
+        ("m3", 128, 2048, 32, 128, 16, [5, 77, 100, 127]),
+    ]:
+        qq = bf16_round(rng.standard_normal((nq, d)).astype(np.float32))
+        keys = bf16_round(rng.standard_normal((n_ext + n_in, d)).astype(np.float32))
+        vals = bf16_round(rng.standard_normal((n_ext + n_in, d)).astype(np.float32))
+        if planted:
+            for blk in planted:
+                keys[blk * kbs:(blk + 1) * kbs] += bf16_round(
+                    (qq.mean(axis=0) * 0.6).astype(np.float32))
+            keys = bf16_round(keys)
+        out.update({f"{name}_q": qq, f"{name}_k": keys, f"{name}_v": vals})
+        dens = [0.05, 0.1, 0.2, 0.3, 0.5, 1.0]
+        for di, dn in enumerate(dens):
+            mask = fb.build_sparse_mask(qq, keys, n_ext, dn, kbs, block_id=3)
+            out[f"{name}_d{di}_sel"] = mask.selected
+            o1, res = fb.sparse_attention_with_residual(qq, mask, keys, vals, None)
+            out[f"{name}_d{di}_out1"] = o1
+            out[f"{name}_d{di}_res_out"] = res.out
+            out[f"{name}_d{di}_res_lse"] = res.lognorm
+            q2 = bf16_round((qq + 0.05 * np.random.Generator(np.random.Philox(di)).standard_normal(qq.shape)).astype(np.float32))
+            o2, _ = fb.sparse_attention_with_residual(
+                q2, mask, keys, vals, CacheEntry(partial=res, step_created=0, block_id=3))
+            out[f"{name}_d{di}_q2"] = q2
+            out[f"{name}_d{di}_out2"] = o2
+        meta[name] = {"nq": nq, "n_ext": n_ext, "n_in": n_in, "d": d, "kbs": kbs,
+                      "densities": dens}
+
+    # -- policy: decisions straight from the reference simulator --
+    sched_cases = []
+    for (bs, steps, per, tau) in [(32, 32, 1, 2), (32, 16, 2, 2), (8, 8, 1, 1),
+                                  (8, 8, 3, 2), (32, 32, 0, 2), (16, 10, 2, 3)]:
+        model = fb.SyntheticModel(fb.ModelConfig(num_layers=1, num_heads=2, head_dim=8, seed=1))
+        run = fb.run_sequence(model, 16, 1, bs, steps, fb.ReuseConfig(tau=tau),
+                              seed=2, unmask_per_step=per)
+        sched_cases.append({
+            "block_size": bs, "steps": steps, "per_step": per, "tau": tau,
+            "schedule": fb.unmask_schedule(bs, steps, per),
+            "decisions": [t.decision for t in run.traces],
+            "updated": [t.updated_tokens for t in run.traces],
+        })
+    meta["schedules"] = sched_cases
+
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+    with open(os.path.join(HERE, "golden_meta.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("wrote", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
