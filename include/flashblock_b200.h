@@ -1,0 +1,190 @@
+/*
+ * flashblock_b200.h -- C ABI of the B200 (sm_100a) FlashBlock attention hot path.
+ *
+ * The reference (flashblock 0.1.0, /root/reference/pkg/src/flashblock) exposes
+ * this path as synchronous numpy functions, one (layer, head) at a time.  This
+ * library is the device-side replacement: every entry point below is
+ * asynchronous on the given CUDA stream, takes caller-owned DEVICE pointers
+ * with the layouts stated here, never synchronises the host, and returns an
+ * fb_status.  fb_last_error() gives a human-readable message for the calling
+ * thread.  Entry points are CUDA-graph capturable (no allocation, no sync).
+ *
+ * Layout model ("groups").  One call processes `groups` independent pairs of
+ * (query block, key/value slab):
+ *
+ *   queries  q  + g * q_rows * head_dim            [q_rows, head_dim] row-major
+ *   keys     k  + g * kv_rows_cap * head_dim       rows [key_begin, key_end)
+ *   values   v  + g * kv_rows_cap * head_dim       same rows as keys
+ *   partial  o  + g * q_rows * head_dim            [q_rows, head_dim]
+ *   lognorm  lse+ g * q_rows                       [q_rows]
+ *
+ * GQA stacking: with Q laid out [batch, Hq, B, d] and the KV cache
+ * [batch, Hkv, N_cap, d], groups = batch*Hkv and q_rows = (Hq/Hkv)*B -- the
+ * G query heads sharing a kv head are one contiguous [G*B, d] matrix.  Every
+ * hot-path function is row-independent, so this is exactly the reference
+ * applied to the stacked query matrix ("GQA mapping").
+ *
+ * Precision modes (fb_dtype of the inputs):
+ *   FB_F64  : q,k,v double; scores/statistics double; partial out double,
+ *             lognorm double.                     (reference float64 path)
+ *   FB_F32  : q,k,v float; scores float, statistics and accumulation double
+ *             (attention.py:158-174); partial out float, lognorm double.
+ *   FB_BF16 : q,k,v bf16; tcgen05 tensor cores, fp32 accumulate; partial out
+ *             float, lognorm float (natural log).
+ * The "partial types" of a mode are (out, lognorm) as listed.
+ * An empty key group yields the sentinel out = 0, lognorm = -inf
+ * (attention.py:77-82).
+ */
+#ifndef FLASHBLOCK_B200_H
+#define FLASHBLOCK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FB_API __attribute__((visibility("default")))
+#else
+#define FB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fb_status {
+  FB_OK = 0,
+  FB_ERR_SHAPE = 1,       /* -> ShapeError          (linalg.py:28)            */
+  FB_ERR_BOUNDS = 2,      /* -> BoundsError         (kv_cache.py:26)          */
+  FB_ERR_DEGENERATE = 3,  /* -> DegenerateInputError (attention.py:52)        */
+  FB_ERR_REUSE = 4,       /* -> ReusePreconditionError (attention.py:56)      */
+  FB_ERR_STALE = 5,       /* -> StalenessError      (sparse.py:43)            */
+  FB_ERR_CUDA = 6,        /* CUDA runtime / launch failure                    */
+  FB_ERR_VALUE = 7,       /* -> ValueError (bad density, tile, block size)    */
+  FB_ERR_UNSUPPORTED = 8  /* shape/dtype combination not built                */
+} fb_status;
+
+typedef enum fb_dtype { FB_F64 = 0, FB_F32 = 1, FB_BF16 = 2 } fb_dtype;
+
+/* Message for the last non-OK status returned on this host thread. */
+FB_API const char* fb_last_error(void);
+/* Library version string, e.g. "fb200 0.1.0 sm_100a". */
+FB_API const char* fb_version(void);
+
+/* Bytes of scratch fb_attention_partial may use for split-KV partials at this
+ * shape (0 if it will not split).  Passing less makes it split less. */
+FB_API size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
+                                  int64_t head_dim, int64_t n_keys);
+
+/* K1 -- block-external partial ("refresh").
+ * Replaces attention_partial (attention.py:136-182) and the external half of
+ * attention_streamed (attention.py:185-204, call at :202); batched over groups.
+ * Streams keys [key_begin, key_end) of every slab once; writes the normalised
+ * partial (o_out, lse_out) in the mode's partial types.  key_begin==key_end
+ * writes the empty sentinel.  BF16 with head_dim in {64,128} runs the
+ * TMA + tcgen05/TMEM kernel; other shapes run the SIMT kernel. */
+FB_API int fb_attention_partial(int dtype, const void* q, const void* k, const void* v,
+                         int64_t groups, int64_t q_rows, int64_t head_dim,
+                         int64_t kv_rows_cap, int64_t key_begin, int64_t key_end,
+                         double scale, void* o_out, void* lse_out,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* K2 -- cached step: block-internal partial fused with the log-space merge
+ * against the cached external partial.
+ * Replaces attention_with_reuse (attention.py:295-321) = attention_partial on
+ * the internal keys (:320) + merge_partials (:321, :236-245).  Never receives
+ * the KV cache.  k_in/v_in: [groups, n_in, head_dim] (slab stride n_in).
+ * o_ext/lse_ext: partial types of the mode.  out: out_dtype (FB_F64 for F64,
+ * FB_F32 for F32; FB_F32 or FB_BF16 for BF16).  Optional (NULL to skip):
+ * lse_merged (lognorm type), o_int/lse_int (the internal partial, partial
+ * types), empty_rows (device int32 counter incremented once per row with no
+ * keys on either side; the caller raises DegenerateInputError if > 0). */
+FB_API int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_in,
+                      int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_in,
+                      double scale, const void* o_ext, const void* lse_ext,
+                      void* out, int out_dtype, void* lse_merged,
+                      void* o_int, void* lse_int, int32_t* empty_rows, void* stream);
+
+/* K3 -- P-way log-space combine of partials over disjoint key groups.
+ * Replaces combine_partials (attention.py:207-233) / merge_partials (:236-245)
+ * and is the split-KV merge (one partial per shard).  o_parts[p], lse_parts[p]
+ * are host arrays of device pointers (partial types of the mode), each
+ * [rows, head_dim] / [rows].  Rows empty on one side pass through bitwise;
+ * rows empty everywhere stay empty and bump *empty_rows when given.
+ * Outputs: o_out in out_dtype (partial out type, or FB_BF16 in BF16 mode),
+ * lse_out (lognorm type, may be NULL).  1 <= n_parts <= 16. */
+FB_API int fb_combine(int dtype, int n_parts, const void* const* o_parts,
+               const void* const* lse_parts, int64_t rows, int64_t head_dim,
+               void* o_out, int out_dtype, void* lse_out, int32_t* empty_rows,
+               void* stream);
+
+/* K4 -- full recompute over [committed | current block] keys, normalised
+ * output.  Replaces attention_streamed(boundary=committed) + merge_partials
+ * (simulator.py:424-429) and attention_dense for the GPU baseline.  Runs K1
+ * over the cache into (o_ext_scratch, lse_ext_scratch) then K2; those scratch
+ * buffers (partial types, [groups, q_rows, (head_dim)]) also receive the
+ * refreshed external partial, so a refresh step is exactly this call. */
+FB_API int fb_full_attention(int dtype, const void* q, const void* k, const void* v,
+                      int64_t groups, int64_t q_rows, int64_t head_dim,
+                      int64_t kv_rows_cap, int64_t n_ext,
+                      const void* k_in, const void* v_in, int64_t n_in, double scale,
+                      void* o_ext_scratch, void* lse_ext_scratch,
+                      void* out, int out_dtype, int32_t* empty_rows,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* K5 -- sparse block scoring.  Replaces the score/softmax/mass stage of
+ * build_sparse_mask (sparse.py:117-125): softmax over ALL keys (external
+ * [0,n_ext) from the cache plus the n_in current-block keys), probability
+ * mass per external key block of key_block_size rows summed over the q_rows
+ * rows of the group.  mass: double [groups, ceil(n_ext/kbs)].  Scores are
+ * formed in double for FB_F64/FB_F32 (as the reference) and in float from
+ * bf16 products for FB_BF16; masses always accumulate in double. */
+FB_API int fb_block_mass(int dtype, const void* q, const void* k, const void* k_in,
+                  int64_t groups, int64_t q_rows, int64_t head_dim,
+                  int64_t kv_rows_cap, int64_t n_ext, int64_t n_in,
+                  int64_t key_block_size, double scale, double* mass,
+                  void* workspace, size_t workspace_bytes, void* stream);
+FB_API size_t fb_block_mass_workspace_bytes(int64_t groups, int64_t q_rows);
+
+/* K6 -- stable top-k block selection.  Replaces sparse.py:126-128: order by
+ * (mass desc, index asc), keep `budget`, emit ascending.  selected: int32
+ * [groups, budget].  budget must be min(nb, max(1, ceil(density*n_ext/kbs)))
+ * (fb_mask_budget computes it exactly as the reference, in double). */
+FB_API int fb_topk_blocks(const double* mass, int64_t groups, int64_t num_blocks,
+                   int64_t budget, int32_t* selected, void* stream);
+FB_API int64_t fb_mask_budget(int64_t n_ext, double density, int64_t key_block_size);
+
+/* K7 -- sparse first step, exact partition (sparse.py:166-175): selected
+ * partial over the selected external blocks PLUS all n_in current-block keys,
+ * residual partial over the unselected external keys; both written (partial
+ * types), plus the merged output (out_dtype).  selected: int32 [groups, n_sel]
+ * ascending block ids of key_block_size rows (tail block clipped at n_ext). */
+FB_API int fb_sparse_partitioned(int dtype, const void* q, const void* k, const void* v,
+                          const void* k_in, const void* v_in,
+                          int64_t groups, int64_t q_rows, int64_t head_dim,
+                          int64_t kv_rows_cap, int64_t n_ext, int64_t n_in,
+                          const int32_t* selected, int64_t n_sel,
+                          int64_t key_block_size, double scale,
+                          void* o_sel, void* lse_sel, void* o_res, void* lse_res,
+                          void* out, int out_dtype, int32_t* empty_rows, void* stream);
+
+/* K8 -- later sparse steps (sparse.py:177-183): attend the selected external
+ * blocks (gathered straight from the cache by block index, no copy) plus the
+ * current block, and merge the cached residual in the epilogue.  o_res may be
+ * NULL for the renormalised sparse-only baseline (sparse.py:317-322). */
+FB_API int fb_sparse_attend_merge(int dtype, const void* q, const void* k, const void* v,
+                           const void* k_in, const void* v_in,
+                           int64_t groups, int64_t q_rows, int64_t head_dim,
+                           int64_t kv_rows_cap, int64_t n_ext, int64_t n_in,
+                           const int32_t* selected, int64_t n_sel,
+                           int64_t key_block_size, double scale,
+                           const void* o_res, const void* lse_res,
+                           void* out, int out_dtype, int32_t* empty_rows, void* stream);
+
+/* Count of kernel launches issued by this library since load (for bench). */
+FB_API int64_t fb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASHBLOCK_B200_H */

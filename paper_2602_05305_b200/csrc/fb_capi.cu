@@ -1,0 +1,534 @@
+// extern "C" entry points (include/flashblock_b200.h): validation, precision
+// dispatch, split-KV planning.  No host synchronisation, no allocation.
+#include "fb_kernels.cuh"
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <type_traits>
+
+namespace fb {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return FB_OK;
+}
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- split planning
+
+struct SplitPlan {
+  int splits;
+  int64_t per_split;  // keys per split
+};
+
+// SIMT: aim for ~2 waves of 4-warp CTAs; at least 256 keys per split.
+static SplitPlan plan_simt(int64_t groups, int64_t q_rows, int64_t n, size_t ws_bytes,
+                           size_t bytes_per_split) {
+  const int64_t ctas = groups * ((q_rows + 15) / 16);
+  int64_t want = (2 * (int64_t)num_sms() * 4 + ctas - 1) / std::max<int64_t>(ctas, 1);
+  want = std::min<int64_t>(want, (n + 255) / 256);
+  want = std::min<int64_t>(want, 1024);
+  if (bytes_per_split > 0) want = std::min<int64_t>(want, (int64_t)(ws_bytes / bytes_per_split));
+  want = std::max<int64_t>(want, 1);
+  int64_t per = (n + want - 1) / want;
+  per = (per + 31) / 32 * 32;
+  const int splits = (int)((n + per - 1) / per);
+  return {splits, per};
+}
+
+// tcgen05: one 128-key tile granularity, one CTA per SM (TMEM + smem bound).
+static SplitPlan plan_sm100(int64_t groups, int64_t q_rows, int64_t n, size_t ws_bytes,
+                            size_t bytes_per_split) {
+  const int64_t items = groups * ((q_rows + 127) / 128);
+  const int64_t tiles = (n + 127) / 128;
+  int64_t want = std::max<int64_t>(1, (int64_t)num_sms() / std::max<int64_t>(items, 1));
+  want = std::min<int64_t>(want, tiles);
+  if (bytes_per_split > 0 && want > 1)
+    want = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(ws_bytes / bytes_per_split)));
+  const int64_t tiles_per = (tiles + want - 1) / want;
+  const int splits = (int)((tiles + tiles_per - 1) / tiles_per);
+  return {splits, tiles_per * 128};
+}
+
+template <typename Mode>
+static size_t split_bytes(int64_t rows, int64_t d) {
+  return (size_t)rows * (size_t)(d + 1) * sizeof(typename Mode::Ta) + 256;
+}
+
+template <typename Mode>
+static CombineList strided_list(void* ws, int splits, int64_t rows, int64_t d) {
+  CombineList L{};
+  L.n = splits;
+  L.strided = true;
+  L.o[0] = ws;
+  L.l[0] = reinterpret_cast<typename Mode::Ta*>(ws) + (size_t)splits * rows * d;
+  L.o_stride = rows * d;
+  L.l_stride = rows;
+  return L;
+}
+
+// Partial over a key map into (o_out, lse_out) of the mode's partial types.
+template <typename Mode, typename Map>
+static int partial_any(const typename Mode::Tin* q, const Map& map, int64_t groups, int64_t q_rows,
+                       int64_t d, int64_t n, double scale, typename Mode::To* o_out,
+                       typename Mode::Tl* lse_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  using Ta = typename Mode::Ta;
+  const int64_t rows = groups * q_rows;
+  const size_t per = split_bytes<Mode>(rows, d);
+  SplitPlan p = plan_simt(groups, q_rows, n, ws ? ws_bytes : 0, per);
+  constexpr bool direct_ok = std::is_same<Ta, typename Mode::To>::value &&
+                             std::is_same<Ta, typename Mode::Tl>::value;
+  MergeOut<Mode> none{};
+  if (p.splits == 1 && direct_ok) {
+    return launch_partial_simt<Mode, false, false>(q, map, groups, q_rows, d, p.per_split, 1, scale,
+                                                   reinterpret_cast<Ta*>(o_out),
+                                                   reinterpret_cast<typename Mode::Tl*>(lse_out),
+                                                   none, st);
+  }
+  if (ws == nullptr || ws_bytes < per * p.splits)
+    return fail(FB_ERR_VALUE, "workspace too small (query fb_partial_workspace_bytes)");
+  Ta* wo = reinterpret_cast<Ta*>(ws);
+  Ta* wl = wo + (size_t)p.splits * rows * d;
+  int rc = launch_partial_simt<Mode, false, false>(q, map, groups, q_rows, d, p.per_split, p.splits,
+                                                   scale, wo, reinterpret_cast<typename Mode::Tl*>(wl),
+                                                   none, st);
+  if (rc) return rc;
+  return launch_combine<Ta, Ta, Ta, typename Mode::To, typename Mode::Tl>(
+      strided_list<Mode>(ws, p.splits, rows, d), rows, d, o_out, lse_out, nullptr, st);
+}
+
+static int check_dtype(int dt) {
+  if (dt != FB_F64 && dt != FB_F32 && dt != FB_BF16) return fail(FB_ERR_VALUE, "unknown dtype");
+  return FB_OK;
+}
+
+template <typename Mode>
+static int attention_partial_t(const void* qv, const void* kv, const void* vv, int64_t groups,
+                               int64_t q_rows, int64_t d, int64_t cap, int64_t kb, int64_t ke,
+                               double scale, void* o_out, void* lse_out, void* ws, size_t ws_bytes,
+                               cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  auto* q = reinterpret_cast<const Tin*>(qv);
+  auto* k = reinterpret_cast<const Tin*>(kv);
+  auto* v = reinterpret_cast<const Tin*>(vv);
+  auto* o = reinterpret_cast<typename Mode::To*>(o_out);
+  auto* l = reinterpret_cast<typename Mode::Tl*>(lse_out);
+  const int64_t rows = groups * q_rows;
+  const int64_t n = ke - kb;
+  if (n == 0) return launch_fill_sentinel<typename Mode::To, typename Mode::Tl>(o, l, rows, d, st);
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (sm100_supported(d) && ke < (int64_t(1) << 31) && q_rows < (int64_t(1) << 31) &&
+        (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
+        (reinterpret_cast<uintptr_t>(v) % 16 == 0) && groups < 65536) {
+      const size_t per = (size_t)rows * (size_t)(d + 1) * sizeof(float) + 256;
+      SplitPlan p = plan_sm100(groups, q_rows, n, ws ? ws_bytes : 0, per);
+      if (p.splits == 1)
+        return launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, p.per_split, 1, scale,
+                                    o, l, st);
+      float* wo = reinterpret_cast<float*>(ws);
+      float* wl = wo + (size_t)p.splits * rows * d;
+      int rc = launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, p.per_split, p.splits,
+                                    scale, wo, wl, st);
+      if (rc) return rc;
+      return launch_combine<float, float, float, float, float>(
+          strided_list<ModeBF16>(ws, p.splits, rows, d), rows, d, o, l, nullptr, st);
+    }
+  }
+  RangeMap<Tin> map{k, v, cap * d, kb, ke, d};
+  return partial_any<Mode>(q, map, groups, q_rows, d, n, scale, o, l, ws, ws_bytes, st);
+}
+
+template <typename Mode>
+static int internal_merge_t(const void* qv, const void* kv, const void* vv, int64_t groups,
+                            int64_t q_rows, int64_t d, int64_t n_in, double scale,
+                            const void* o_ext, const void* lse_ext, void* out, bool out_bf16,
+                            void* lse_merged, void* o_int, void* lse_int, int32_t* empty,
+                            cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  MergeOut<Mode> mo{};
+  mo.o_ext = reinterpret_cast<const typename Mode::To*>(o_ext);
+  mo.lse_ext = reinterpret_cast<const typename Mode::Tl*>(lse_ext);
+  mo.out = out;
+  mo.out_bf16 = out_bf16;
+  mo.lse_merged = reinterpret_cast<typename Mode::Tl*>(lse_merged);
+  mo.o_int = reinterpret_cast<typename Mode::To*>(o_int);
+  mo.lse_int = reinterpret_cast<typename Mode::Tl*>(lse_int);
+  mo.empty_rows = empty;
+  RangeMap<Tin> map{reinterpret_cast<const Tin*>(kv), reinterpret_cast<const Tin*>(vv), n_in * d, 0,
+                    n_in, d};
+  const int64_t per = std::max<int64_t>(n_in, 1);
+  return launch_partial_simt<Mode, true, false>(reinterpret_cast<const Tin*>(qv), map, groups, q_rows,
+                                                d, per, 1, scale, nullptr, nullptr, mo, st);
+}
+
+template <typename Mode>
+static int combine_t(int n_parts, const void* const* o_parts, const void* const* lse_parts,
+                     int64_t rows, int64_t d, void* o_out, bool out_bf16, void* lse_out,
+                     int32_t* empty, cudaStream_t st) {
+  CombineList L{};
+  L.n = n_parts;
+  L.strided = false;
+  for (int i = 0; i < n_parts; ++i) {
+    L.o[i] = o_parts[i];
+    L.l[i] = lse_parts[i];
+  }
+  using To = typename Mode::To;
+  using Tl = typename Mode::Tl;
+  using Ta = typename Mode::Ta;
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (out_bf16)
+      return launch_combine<float, float, float, __nv_bfloat16, float>(
+          L, rows, d, reinterpret_cast<__nv_bfloat16*>(o_out), reinterpret_cast<float*>(lse_out),
+          empty, st);
+  }
+  return launch_combine<To, Tl, Ta, To, Tl>(L, rows, d, reinterpret_cast<To*>(o_out),
+                                            reinterpret_cast<Tl*>(lse_out), empty, st);
+}
+
+template <typename MaskMode>
+static int block_mass_t(const void* qv, const void* kv, const void* kin, int64_t groups,
+                        int64_t q_rows, int64_t d, int64_t cap, int64_t n_ext, int64_t n_in,
+                        int64_t kbs, double scale, double* mass, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  using Tin = typename MaskMode::Tin;
+  const int64_t rows = groups * q_rows;
+  double* row_lse = reinterpret_cast<double*>(ws);
+  void* rest = reinterpret_cast<char*>(ws) + align_up((size_t)rows * sizeof(double), 256);
+  const size_t rest_bytes = ws_bytes - align_up((size_t)rows * sizeof(double), 256);
+  ConcatMap<Tin> map{reinterpret_cast<const Tin*>(kv), nullptr, reinterpret_cast<const Tin*>(kin),
+                     nullptr, cap * d, n_ext, n_in, d};
+  const int64_t n = n_ext + n_in;
+  const size_t per = (size_t)rows * sizeof(double) + 256;
+  SplitPlan p = plan_simt(groups, q_rows, n, rest_bytes, per);
+  MergeOut<MaskMode> none{};
+  int rc;
+  if (p.splits == 1) {
+    rc = launch_partial_simt<MaskMode, false, true>(reinterpret_cast<const Tin*>(qv), map, groups,
+                                                    q_rows, d, p.per_split, 1, scale, nullptr,
+                                                    row_lse, none, st);
+  } else {
+    // lognorm-only split partials: [splits][rows] doubles, combined with d = 0 columns
+    double* wl = reinterpret_cast<double*>(rest);
+    rc = launch_partial_simt<MaskMode, false, true>(reinterpret_cast<const Tin*>(qv), map, groups,
+                                                    q_rows, d, p.per_split, p.splits, scale, nullptr,
+                                                    wl, none, st);
+    if (rc) return rc;
+    CombineList L{};
+    L.n = p.splits;
+    L.strided = true;
+    L.o[0] = wl;  // never read with head_dim 0
+    L.l[0] = wl;
+    L.o_stride = 0;
+    L.l_stride = rows;
+    rc = launch_combine<double, double, double, double, double>(L, rows, 0, nullptr, row_lse, nullptr, st);
+  }
+  if (rc) return rc;
+  return launch_block_mass<MaskMode>(reinterpret_cast<const Tin*>(qv), reinterpret_cast<const Tin*>(kv),
+                                     row_lse, groups, q_rows, d, cap * d, n_ext, kbs, scale, mass, st);
+}
+
+template <typename Mode>
+static int sparse_partitioned_t(const void* qv, const void* kv, const void* vv, const void* kin,
+                                const void* vin, int64_t groups, int64_t q_rows, int64_t d,
+                                int64_t cap, int64_t n_ext, int64_t n_in, const int32_t* sel,
+                                int64_t n_sel, int64_t kbs, double scale, void* o_sel, void* l_sel,
+                                void* o_res, void* l_res, void* out, bool out_bf16, int32_t* empty,
+                                cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  using To = typename Mode::To;
+  using Tl = typename Mode::Tl;
+  const Tin* q = reinterpret_cast<const Tin*>(qv);
+  const Tin* k = reinterpret_cast<const Tin*>(kv);
+  const Tin* v = reinterpret_cast<const Tin*>(vv);
+  // selected external blocks + every current-block key, fused with nothing
+  SelectedMap<Tin> smap{k, v, reinterpret_cast<const Tin*>(kin), reinterpret_cast<const Tin*>(vin),
+                        sel, n_sel, kbs, n_ext, n_in, cap * d, d};
+  MergeOut<Mode> mo{};
+  mo.o_ext = nullptr;
+  mo.lse_ext = nullptr;
+  mo.out = o_sel;
+  mo.out_bf16 = false;
+  mo.lse_merged = reinterpret_cast<Tl*>(l_sel);
+  int rc = launch_partial_simt<Mode, true, false>(q, smap, groups, q_rows, d, int64_t(1) << 40, 1,
+                                                  scale, nullptr, nullptr, mo, st);
+  if (rc) return rc;
+  // residual: the unselected external keys (partial, unmerged)
+  ResidualMap<Tin> rmap{k, v, sel, n_sel, kbs, n_ext, cap * d, d};
+  MergeOut<Mode> mr{};
+  mr.o_ext = nullptr;
+  mr.lse_ext = nullptr;
+  mr.out = o_res;
+  mr.out_bf16 = false;
+  mr.lse_merged = reinterpret_cast<Tl*>(l_res);
+  rc = launch_partial_simt<Mode, true, false>(q, rmap, groups, q_rows, d, int64_t(1) << 40, 1, scale,
+                                              nullptr, nullptr, mr, st);
+  if (rc) return rc;
+  if (out == nullptr) return FB_OK;
+  const void* op[2] = {o_sel, o_res};
+  const void* lp[2] = {l_sel, l_res};
+  return combine_t<Mode>(2, op, lp, groups * q_rows, d, out, out_bf16, nullptr, empty, st);
+}
+
+template <typename Mode>
+static int sparse_attend_t(const void* qv, const void* kv, const void* vv, const void* kin,
+                           const void* vin, int64_t groups, int64_t q_rows, int64_t d, int64_t cap,
+                           int64_t n_ext, int64_t n_in, const int32_t* sel, int64_t n_sel,
+                           int64_t kbs, double scale, const void* o_res, const void* l_res,
+                           void* out, bool out_bf16, int32_t* empty, cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  SelectedMap<Tin> smap{reinterpret_cast<const Tin*>(kv), reinterpret_cast<const Tin*>(vv),
+                        reinterpret_cast<const Tin*>(kin), reinterpret_cast<const Tin*>(vin),
+                        sel, n_sel, kbs, n_ext, n_in, cap * d, d};
+  MergeOut<Mode> mo{};
+  mo.o_ext = reinterpret_cast<const typename Mode::To*>(o_res);
+  mo.lse_ext = reinterpret_cast<const typename Mode::Tl*>(l_res);
+  mo.out = out;
+  mo.out_bf16 = out_bf16;
+  mo.empty_rows = empty;
+  return launch_partial_simt<Mode, true, false>(reinterpret_cast<const Tin*>(qv), smap, groups, q_rows,
+                                                d, int64_t(1) << 40, 1, scale, nullptr, nullptr, mo, st);
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+const char* fb_last_error(void) { return g_last_error.c_str(); }
+const char* fb_version(void) { return "fb200 0.1.0 sm_100a"; }
+int64_t fb_launch_count(void) { return g_launches.load(); }
+
+size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,
+                                  int64_t n_keys) {
+  if (groups <= 0 || q_rows <= 0 || n_keys <= 0) return 0;
+  const int64_t rows = groups * q_rows;
+  if (dtype == FB_BF16 && sm100_supported(head_dim)) {
+    const size_t per = (size_t)rows * (size_t)(head_dim + 1) * sizeof(float) + 256;
+    SplitPlan p = plan_sm100(groups, q_rows, n_keys, SIZE_MAX, per);
+    SplitPlan s = plan_simt(groups, q_rows, n_keys, SIZE_MAX, per);
+    return per * (size_t)std::max(p.splits, s.splits);
+  }
+  const size_t elem = dtype == FB_BF16 ? 4 : 8;
+  const size_t per = (size_t)rows * (size_t)(head_dim + 1) * elem + 256;
+  SplitPlan s = plan_simt(groups, q_rows, n_keys, SIZE_MAX, per);
+  return per * (size_t)s.splits;
+}
+
+int fb_attention_partial(int dtype, const void* q, const void* k, const void* v, int64_t groups,
+                         int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap, int64_t key_begin,
+                         int64_t key_end, double scale, void* o_out, void* lse_out, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0)
+    return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (!(0 <= key_begin && key_begin <= key_end && key_end <= kv_rows_cap))
+    return fail(FB_ERR_BOUNDS, "key range [" + std::to_string(key_begin) + ", " +
+                                   std::to_string(key_end) + ") outside [0, " +
+                                   std::to_string(kv_rows_cap) + "]");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return attention_partial_t<ModeF64>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, key_begin,
+                                          key_end, scale, o_out, lse_out, workspace, workspace_bytes, st);
+    case FB_F32:
+      return attention_partial_t<ModeF32>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, key_begin,
+                                          key_end, scale, o_out, lse_out, workspace, workspace_bytes, st);
+    default:
+      return attention_partial_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, key_begin,
+                                           key_end, scale, o_out, lse_out, workspace, workspace_bytes, st);
+  }
+}
+
+int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_in, int64_t groups,
+                      int64_t q_rows, int64_t head_dim, int64_t n_in, double scale,
+                      const void* o_ext, const void* lse_ext, void* out, int out_dtype,
+                      void* lse_merged, void* o_int, void* lse_int, int32_t* empty_rows,
+                      void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0)
+    return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      if (out_dtype != FB_F64) return fail(FB_ERR_VALUE, "F64 mode writes F64 output");
+      return internal_merge_t<ModeF64>(q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
+                                       lse_ext, out, false, lse_merged, o_int, lse_int, empty_rows, st);
+    case FB_F32:
+      if (out_dtype != FB_F32) return fail(FB_ERR_VALUE, "F32 mode writes F32 output");
+      return internal_merge_t<ModeF32>(q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
+                                       lse_ext, out, false, lse_merged, o_int, lse_int, empty_rows, st);
+    default:
+      if (out_dtype != FB_F32 && out_dtype != FB_BF16)
+        return fail(FB_ERR_VALUE, "BF16 mode writes F32 or BF16 output");
+      return internal_merge_t<ModeBF16>(q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
+                                        lse_ext, out, out_dtype == FB_BF16, lse_merged, o_int,
+                                        lse_int, empty_rows, st);
+  }
+}
+
+int fb_combine(int dtype, int n_parts, const void* const* o_parts, const void* const* lse_parts,
+               int64_t rows, int64_t head_dim, void* o_out, int out_dtype, void* lse_out,
+               int32_t* empty_rows, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (n_parts < 1 || n_parts > FB_MAX_PARTS) return fail(FB_ERR_VALUE, "n_parts must be in [1, 16]");
+  if (rows < 0 || head_dim < 1) return fail(FB_ERR_SHAPE, "negative rows or head_dim < 1");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return combine_t<ModeF64>(n_parts, o_parts, lse_parts, rows, head_dim, o_out, false, lse_out,
+                                empty_rows, st);
+    case FB_F32:
+      return combine_t<ModeF32>(n_parts, o_parts, lse_parts, rows, head_dim, o_out, false, lse_out,
+                                empty_rows, st);
+    default:
+      return combine_t<ModeBF16>(n_parts, o_parts, lse_parts, rows, head_dim, o_out,
+                                 out_dtype == FB_BF16, lse_out, empty_rows, st);
+  }
+}
+
+int fb_full_attention(int dtype, const void* q, const void* k, const void* v, int64_t groups,
+                      int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap, int64_t n_ext,
+                      const void* k_in, const void* v_in, int64_t n_in, double scale,
+                      void* o_ext_scratch, void* lse_ext_scratch, void* out, int out_dtype,
+                      int32_t* empty_rows, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = fb_attention_partial(dtype, q, k, v, groups, q_rows, head_dim, kv_rows_cap, 0, n_ext,
+                                scale, o_ext_scratch, lse_ext_scratch, workspace, workspace_bytes,
+                                stream);
+  if (rc) return rc;
+  return fb_internal_merge(dtype, q, k_in, v_in, groups, q_rows, head_dim, n_in, scale,
+                           o_ext_scratch, lse_ext_scratch, out, out_dtype, nullptr, nullptr, nullptr,
+                           empty_rows, stream);
+}
+
+// ---------------------------------------------------------------- sparse
+
+size_t fb_block_mass_workspace_bytes(int64_t groups, int64_t q_rows) {
+  // row lognorms (double) + split scratch for the lognorm pass
+  const int64_t rows = groups * q_rows;
+  const size_t per = (size_t)rows * sizeof(double) * 2 + 256;
+  return (size_t)rows * sizeof(double) + per * 1024;
+}
+
+int64_t fb_mask_budget(int64_t n_ext, double density, int64_t key_block_size) {
+  if (n_ext <= 0 || key_block_size < 1) return 0;
+  const int64_t nb = (n_ext + key_block_size - 1) / key_block_size;
+  const int64_t want = (int64_t)std::ceil(density * (double)n_ext / (double)key_block_size);
+  return std::min<int64_t>(nb, std::max<int64_t>(1, want));
+}
+
+int fb_block_mass(int dtype, const void* q, const void* k, const void* k_in, int64_t groups,
+                  int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap, int64_t n_ext, int64_t n_in,
+                  int64_t key_block_size, double scale, double* mass, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (key_block_size < 1) return fail(FB_ERR_VALUE, "key_block_size must be >= 1");
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0) return fail(FB_ERR_SHAPE, "bad extents");
+  if (n_ext < 0 || n_ext > kv_rows_cap) return fail(FB_ERR_VALUE, "n_ext outside [0, kv_rows_cap]");
+  if (groups == 0 || n_ext == 0) return FB_OK;
+  if (q_rows == 0) return fail(FB_ERR_SHAPE, "no query rows");
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  if (workspace == nullptr || workspace_bytes < (size_t)groups * q_rows * sizeof(double) + 512)
+    return fail(FB_ERR_VALUE, "workspace too small (fb_block_mass_workspace_bytes)");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return block_mass_t<ModeMaskF64>(q, k, k_in, groups, q_rows, head_dim, kv_rows_cap, n_ext, n_in,
+                                       key_block_size, scale, mass, workspace, workspace_bytes, st);
+    case FB_F32:
+      return block_mass_t<ModeMaskF32>(q, k, k_in, groups, q_rows, head_dim, kv_rows_cap, n_ext, n_in,
+                                       key_block_size, scale, mass, workspace, workspace_bytes, st);
+    default:
+      return block_mass_t<ModeMaskBF16>(q, k, k_in, groups, q_rows, head_dim, kv_rows_cap, n_ext,
+                                        n_in, key_block_size, scale, mass, workspace, workspace_bytes, st);
+  }
+}
+
+int fb_topk_blocks(const double* mass, int64_t groups, int64_t num_blocks, int64_t budget,
+                   int32_t* selected, void* stream) {
+  if (groups < 0 || num_blocks < 0 || budget < 0 || budget > num_blocks)
+    return fail(FB_ERR_VALUE, "need 0 <= budget <= num_blocks");
+  if (num_blocks > (int64_t(1) << 30)) return fail(FB_ERR_UNSUPPORTED, "too many blocks");
+  return launch_topk(mass, groups, num_blocks, budget, selected, nullptr, 0, as_stream(stream));
+}
+
+int fb_sparse_partitioned(int dtype, const void* q, const void* k, const void* v, const void* k_in,
+                          const void* v_in, int64_t groups, int64_t q_rows, int64_t head_dim,
+                          int64_t kv_rows_cap, int64_t n_ext, int64_t n_in, const int32_t* selected,
+                          int64_t n_sel, int64_t key_block_size, double scale, void* o_sel,
+                          void* lse_sel, void* o_res, void* lse_res, void* out, int out_dtype,
+                          int32_t* empty_rows, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (key_block_size < 1) return fail(FB_ERR_VALUE, "key_block_size must be >= 1");
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0 || n_sel < 0)
+    return fail(FB_ERR_SHAPE, "bad extents");
+  if (n_ext < 0 || n_ext > kv_rows_cap) return fail(FB_ERR_SHAPE, "key set smaller than the mask");
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return sparse_partitioned_t<ModeF64>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap,
+                                           n_ext, n_in, selected, n_sel, key_block_size, scale, o_sel,
+                                           lse_sel, o_res, lse_res, out, false, empty_rows, st);
+    case FB_F32:
+      return sparse_partitioned_t<ModeF32>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap,
+                                           n_ext, n_in, selected, n_sel, key_block_size, scale, o_sel,
+                                           lse_sel, o_res, lse_res, out, false, empty_rows, st);
+    default:
+      return sparse_partitioned_t<ModeBF16>(q, k, v, k_in, v_in, groups, q_rows, head_dim,
+                                            kv_rows_cap, n_ext, n_in, selected, n_sel, key_block_size,
+                                            scale, o_sel, lse_sel, o_res, lse_res, out,
+                                            out_dtype == FB_BF16, empty_rows, st);
+  }
+}
+
+int fb_sparse_attend_merge(int dtype, const void* q, const void* k, const void* v, const void* k_in,
+                           const void* v_in, int64_t groups, int64_t q_rows, int64_t head_dim,
+                           int64_t kv_rows_cap, int64_t n_ext, int64_t n_in, const int32_t* selected,
+                           int64_t n_sel, int64_t key_block_size, double scale, const void* o_res,
+                           const void* lse_res, void* out, int out_dtype, int32_t* empty_rows,
+                           void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (key_block_size < 1) return fail(FB_ERR_VALUE, "key_block_size must be >= 1");
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0 || n_sel < 0)
+    return fail(FB_ERR_SHAPE, "bad extents");
+  if (n_ext < 0 || n_ext > kv_rows_cap) return fail(FB_ERR_SHAPE, "key set smaller than the mask");
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  if ((o_res == nullptr) != (lse_res == nullptr)) return fail(FB_ERR_VALUE, "o_res/lse_res mismatch");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      if (out_dtype != FB_F64) return fail(FB_ERR_VALUE, "F64 mode writes F64 output");
+      return sparse_attend_t<ModeF64>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap, n_ext,
+                                      n_in, selected, n_sel, key_block_size, scale, o_res, lse_res,
+                                      out, false, empty_rows, st);
+    case FB_F32:
+      if (out_dtype != FB_F32) return fail(FB_ERR_VALUE, "F32 mode writes F32 output");
+      return sparse_attend_t<ModeF32>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap, n_ext,
+                                      n_in, selected, n_sel, key_block_size, scale, o_res, lse_res,
+                                      out, false, empty_rows, st);
+    default:
+      return sparse_attend_t<ModeBF16>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap,
+                                       n_ext, n_in, selected, n_sel, key_block_size, scale, o_res,
+                                       lse_res, out, out_dtype == FB_BF16, empty_rows, st);
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// Internal kernel-launch interface shared by the C-ABI layer and the kernels.
+#pragma once
+
+#include "fb_common.cuh"
+#include "fb_keymap.cuh"
+
+namespace fb {
+
+constexpr int FB_MAX_PARTS = 16;
+
+// Parts of a combine: a pointer list (API combine, split-KV shards) or a
+// strided workspace (intra-GPU split partials).
+struct CombineList {
+  const void* o[FB_MAX_PARTS];
+  const void* l[FB_MAX_PARTS];
+  int n;
+  bool strided;
+  int64_t o_stride, l_stride;  // elements between parts when strided
+};
+
+// K2 merge-epilogue operands: the cached external partial and the outputs.
+template <typename Mode>
+struct MergeOut {
+  const typename Mode::To* o_ext;  // [rows_total, d]
+  const typename Mode::Tl* lse_ext;
+  void* out;                       // To, or bf16 when out_bf16
+  bool out_bf16;
+  typename Mode::Tl* lse_merged;   // optional
+  typename Mode::To* o_int;        // optional internal partial
+  typename Mode::Tl* lse_int;
+  int32_t* empty_rows;             // optional
+};
+
+template <typename Mode, bool MERGE, bool NO_V, typename Map>
+int launch_partial_simt(const typename Mode::Tin* q, const Map& map, int64_t groups,
+                        int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
+                        double scale, typename Mode::Ta* po, typename Mode::Tl* pl,
+                        const MergeOut<Mode>& mo, cudaStream_t st);
+
+template <typename Tp, typename Tlp, typename Ta, typename To, typename Tlo>
+int launch_combine(const CombineList& list, int64_t rows, int64_t head_dim, To* o_out, Tlo* l_out,
+                   int32_t* empty_rows, cudaStream_t st);
+
+template <typename Mode>
+int launch_block_mass(const typename Mode::Tin* q, const typename Mode::Tin* k,
+                      const double* row_lse, int64_t groups, int64_t q_rows, int64_t head_dim,
+                      int64_t slab_stride, int64_t n_ext, int64_t kbs, double scale, double* mass,
+                      cudaStream_t st);
+int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, int32_t* selected,
+                void* scratch, size_t scratch_bytes, cudaStream_t st);
+
+template <typename To, typename Tl>
+int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStream_t st);
+
+// tcgen05 / TMA refresh kernel (bf16, head_dim 64 or 128).  Writes split
+// partials (fp32 out + fp32 natural-log lse) to (po, pl) slot
+// [split][g*q_rows + row]; returns FB_ERR_UNSUPPORTED if the shape is not
+// covered so the caller can route to the SIMT kernel.
+bool sm100_supported(int64_t head_dim);
+int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                         int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                         int64_t key_begin, int64_t key_end, int64_t keys_per_split, int splits,
+                         double scale, float* po, float* pl, cudaStream_t st);
+
+}  // namespace fb

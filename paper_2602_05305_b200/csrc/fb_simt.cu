@@ -1,0 +1,328 @@
+// SIMT kernels of the FlashBlock hot path: any head_dim, F64 / F32 / BF16.
+//
+//  * partial_simt     -- online-softmax partial over a key map, optionally
+//                        split along the keys (split-KV within the GPU) and
+//                        optionally fused with the log-space merge against a
+//                        cached partial (the K2 "internal + merge" epilogue).
+//  * combine_parts    -- P-way log-space merge (K3), sentinel aware.
+//  * fill_sentinel    -- the empty partial (out 0, lognorm -inf).
+//
+// Algorithm restated from the reference: tile-streamed softmax with running
+// max / normaliser / accumulator and exp(m_old - m_new) rescaling
+// (attention.py:156-182); merge weights exp(L - max L) (attention.py:207-233).
+// The score product runs in the mode's score type (the tensor dtype, as
+// attention.py:166); statistics and accumulation in the accumulate type.
+#include "fb_kernels.cuh"
+
+namespace fb {
+
+constexpr int SIMT_WARPS = 4;
+constexpr int SIMT_ROWS_PER_WARP = 4;
+constexpr int SIMT_ROWS = SIMT_WARPS * SIMT_ROWS_PER_WARP;  // query rows per CTA
+constexpr int SIMT_KT = 32;                                  // keys per tile (one per lane)
+
+template <int D, typename Ts, typename Ta>
+constexpr size_t simt_smem_bytes() {
+  return sizeof(Ts) * (SIMT_ROWS * D + SIMT_KT * (D + 1)) + sizeof(Ta) * SIMT_KT * D;
+}
+
+// grid: (ceil(q_rows/SIMT_ROWS), splits, groups); block: 32*SIMT_WARPS.
+// Split s of group g covers key ordinals [s*per_split, min((s+1)*per_split, count)).
+// Without MERGE the normalised partial goes to (po, pl) at slot
+// [s][g*q_rows + row]; with MERGE (splits == 1) it is merged with the cache.
+template <typename Mode, int D, bool MERGE, bool NO_V, typename Map>
+__global__ void __launch_bounds__(32 * SIMT_WARPS)
+partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, int64_t head_dim,
+             int64_t per_split, typename Mode::Ta scale, typename Mode::Ta* po,
+             typename Mode::Tl* pl, int64_t rows_total, MergeOut<Mode> mo) {
+  using Tin = typename Mode::Tin;
+  using Ts = typename Mode::Ts;
+  using Ta = typename Mode::Ta;
+  constexpr int C = D / 32;  // output columns per lane
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ts* qs = reinterpret_cast<Ts*>(smem_raw);           // [SIMT_ROWS][D]
+  Ts* ks = qs + SIMT_ROWS * D;                         // [KT][D+1]
+  Ta* vs = reinterpret_cast<Ta*>(ks + SIMT_KT * (D + 1));  // [KT][D]
+
+  const int64_t g = blockIdx.z;
+  const int split = blockIdx.y;
+  const int64_t row0 = (int64_t)blockIdx.x * SIMT_ROWS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int64_t n_keys = map.count(g);
+  const int64_t kb = min((int64_t)split * per_split, n_keys);
+  const int64_t ke = min(kb + per_split, n_keys);
+
+  // stage the CTA's query rows (zero-padded to D)
+  for (int i = threadIdx.x; i < SIMT_ROWS * D; i += blockDim.x) {
+    const int r = i / D, c = i % D;
+    const int64_t gr = row0 + r;
+    Ts val = 0;
+    if (gr < q_rows && c < head_dim) val = cvt<Ts>(q[(g * q_rows + gr) * head_dim + c]);
+    qs[i] = val;
+  }
+
+  Ta m[SIMT_ROWS_PER_WARP], l[SIMT_ROWS_PER_WARP], acc[SIMT_ROWS_PER_WARP][C];
+#pragma unroll
+  for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) {
+    m[i] = Num<Ta>::ninf();
+    l[i] = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[i][c] = 0;
+  }
+
+  for (int64_t t0 = kb; t0 < ke; t0 += SIMT_KT) {
+    __syncthreads();
+    // cooperative tile load: warp w loads rows w, w+4, ...
+    for (int j = warp; j < SIMT_KT; j += SIMT_WARPS) {
+      const int64_t t = t0 + j;
+      const Tin* kr = nullptr;
+      const Tin* vr = nullptr;
+      if (t < ke) map.row(g, t, kr, vr);
+      for (int c = lane; c < D; c += 32) {
+        Ts kv = 0;
+        Ta vv = 0;
+        if (kr != nullptr && c < head_dim) {
+          kv = cvt<Ts>(kr[c]);
+          if constexpr (!NO_V) vv = cvt<Ta>(vr[c]);
+        }
+        ks[j * (D + 1) + c] = kv;
+        if constexpr (!NO_V) vs[j * D + c] = vv;
+      }
+    }
+    __syncthreads();
+    const bool key_ok = (t0 + lane) < ke;
+
+    Ts s[SIMT_ROWS_PER_WARP];
+#pragma unroll
+    for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) s[i] = 0;
+    const Ts* krow = ks + lane * (D + 1);
+#pragma unroll 8
+    for (int c = 0; c < D; ++c) {
+      const Ts kc = krow[c];
+#pragma unroll
+      for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i)
+        s[i] += qs[(warp * SIMT_ROWS_PER_WARP + i) * D + c] * kc;
+    }
+#pragma unroll
+    for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) {
+      // scores in the tensor dtype, then widened (attention.py:166)
+      const Ta si = key_ok ? (Ta)(s[i] * (Ts)scale) : Num<Ta>::ninf();
+      const Ta m_new = fmax(m[i], warp_max(si));
+      const Ta alpha = Num<Ta>::exp_(m[i] - m_new);  // exp(-inf) = 0 for the first tile
+      const Ta p = key_ok ? Num<Ta>::exp_(si - m_new) : (Ta)0;
+      l[i] = l[i] * alpha + warp_sum(p);
+      if constexpr (!NO_V) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[i][c] *= alpha;
+        for (int j = 0; j < SIMT_KT; ++j) {
+          const Ta pj = __shfl_sync(0xffffffffu, p, j);
+          const Ta* vrow = vs + j * D + lane;
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[i][c] += pj * vrow[c * 32];
+        }
+      }
+      m[i] = m_new;
+    }
+  }
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) {
+    const int64_t gr = row0 + warp * SIMT_ROWS_PER_WARP + i;
+    if (gr >= q_rows) continue;
+    const int64_t rr = g * q_rows + gr;  // global row
+    const bool empty = (ke <= kb);
+    const Ta inv = empty ? (Ta)0 : (Ta)1 / l[i];
+    const Ta lse = empty ? Num<Ta>::ninf() : m[i] + Num<Ta>::log_(l[i]);
+    if constexpr (!MERGE) {
+      if constexpr (!NO_V) {
+        Ta* dst = po + ((int64_t)split * rows_total + rr) * head_dim;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const int col = lane + 32 * c;
+          if (col < head_dim) dst[col] = acc[i][c] * inv;
+        }
+      }
+      if (lane == 0) pl[(int64_t)split * rows_total + rr] = (typename Mode::Tl)lse;
+    } else {
+      using To = typename Mode::To;
+      using Tl = typename Mode::Tl;
+      // internal partial rounded to its stored type first, as the reference
+      // merges the partial it returns (attention.py:180, :320-321)
+      const Ta le = mo.lse_ext ? (Ta)mo.lse_ext[rr] : Num<Ta>::ninf();
+      const Ta li = (Ta)(Tl)lse;
+      const Ta mx = fmax(le, li);
+      const bool live = mx != Num<Ta>::ninf();
+      const Ta we = live ? Num<Ta>::exp_(le - mx) : (Ta)0;
+      const Ta wi = live ? Num<Ta>::exp_(li - mx) : (Ta)0;
+      const Ta z = we + wi;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int col = lane + 32 * c;
+        if (col >= head_dim) continue;
+        const To oi = (To)(acc[i][c] * inv);
+        if (mo.o_int) mo.o_int[rr * head_dim + col] = oi;
+        Ta val = 0;
+        if (live) {
+          const Ta oe = mo.o_ext ? (Ta)mo.o_ext[rr * head_dim + col] : (Ta)0;
+          val = (we * oe + wi * (Ta)oi) / z;
+        }
+        if (mo.out_bf16)
+          reinterpret_cast<__nv_bfloat16*>(mo.out)[rr * head_dim + col] = cvt<__nv_bfloat16>(val);
+        else
+          reinterpret_cast<To*>(mo.out)[rr * head_dim + col] = (To)val;
+      }
+      if (lane == 0) {
+        if (mo.lse_int) mo.lse_int[rr] = (Tl)lse;
+        if (mo.lse_merged) mo.lse_merged[rr] = live ? (Tl)(mx + Num<Ta>::log_(z)) : (Tl)Num<Ta>::ninf();
+        if (!live && mo.empty_rows) atomicAdd(mo.empty_rows, 1);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ combine
+
+// One warp per row.  Parts come either from a pointer list (API combine) or
+// from a strided workspace (split-KV partials).
+template <typename Tp, typename Tlp, typename Ta, typename To, typename Tlo>
+__global__ void combine_parts(CombineList list, int64_t rows, int64_t head_dim, To* o_out,
+                              Tlo* l_out, int32_t* empty_rows) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  auto optr = [&](int p) -> const Tp* {
+    return list.strided ? reinterpret_cast<const Tp*>(list.o[0]) + (int64_t)p * list.o_stride
+                        : reinterpret_cast<const Tp*>(list.o[p]);
+  };
+  auto lptr = [&](int p) -> const Tlp* {
+    return list.strided ? reinterpret_cast<const Tlp*>(list.l[0]) + (int64_t)p * list.l_stride
+                        : reinterpret_cast<const Tlp*>(list.l[p]);
+  };
+  Ta mx = Num<Ta>::ninf();
+  for (int p = 0; p < list.n; ++p) mx = fmax(mx, (Ta)lptr(p)[row]);
+  const bool live = mx != Num<Ta>::ninf();
+  Ta z = 0;
+  for (int p = 0; p < list.n; ++p) z += live ? Num<Ta>::exp_((Ta)lptr(p)[row] - mx) : (Ta)0;
+  for (int64_t c = lane; c < head_dim; c += 32) {
+    Ta num = 0;
+    if (live) {
+      for (int p = 0; p < list.n; ++p) {
+        const Ta w = Num<Ta>::exp_((Ta)lptr(p)[row] - mx);
+        num += w * (Ta)optr(p)[row * head_dim + c];
+      }
+      num = num / z;
+    }
+    o_out[row * head_dim + c] = cvt<To>(num);
+  }
+  if (lane == 0) {
+    if (l_out) l_out[row] = live ? (Tlo)(mx + Num<Ta>::log_(z)) : (Tlo)Num<Ta>::ninf();
+    if (!live && empty_rows) atomicAdd(empty_rows, 1);
+  }
+}
+
+template <typename To, typename Tl>
+__global__ void fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows * head_dim) o[i] = cvt<To>(0.0f);
+  if (l && i < rows) l[i] = (Tl)(-INFINITY);
+}
+
+// ------------------------------------------------------------------ launchers
+
+template <typename Mode, int D, bool MERGE, bool NO_V, typename Map>
+static int launch_partial_d(const typename Mode::Tin* q, const Map& map, int64_t groups,
+                            int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
+                            double scale, typename Mode::Ta* po, typename Mode::Tl* pl,
+                            const MergeOut<Mode>& mo, cudaStream_t st) {
+  constexpr size_t smem = simt_smem_bytes<D, typename Mode::Ts, typename Mode::Ta>();
+  auto kern = partial_simt<Mode, D, MERGE, NO_V, Map>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((q_rows + SIMT_ROWS - 1) / SIMT_ROWS), (unsigned)splits, (unsigned)groups);
+  kern<<<grid, 32 * SIMT_WARPS, smem, st>>>(q, map, q_rows, head_dim, per_split,
+                                            (typename Mode::Ta)scale, po, pl, groups * q_rows, mo);
+  count_launch();
+  return check_launch("partial_simt");
+}
+
+template <typename Mode, bool MERGE, bool NO_V, typename Map>
+int launch_partial_simt(const typename Mode::Tin* q, const Map& map, int64_t groups,
+                        int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
+                        double scale, typename Mode::Ta* po, typename Mode::Tl* pl,
+                        const MergeOut<Mode>& mo, cudaStream_t st) {
+  if (head_dim <= 32)
+    return launch_partial_d<Mode, 32, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+  if (head_dim <= 64)
+    return launch_partial_d<Mode, 64, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+  if (head_dim <= 128)
+    return launch_partial_d<Mode, 128, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+  if (head_dim <= 256)
+    return launch_partial_d<Mode, 256, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+  return fail(FB_ERR_UNSUPPORTED, "head_dim > 256 is not supported");
+}
+
+template <typename Tp, typename Tlp, typename Ta, typename To, typename Tlo>
+int launch_combine(const CombineList& list, int64_t rows, int64_t head_dim, To* o_out, Tlo* l_out,
+                   int32_t* empty_rows, cudaStream_t st) {
+  if (rows == 0) return FB_OK;
+  const int warps = 8;
+  const unsigned blocks = (unsigned)((rows + warps - 1) / warps);
+  combine_parts<Tp, Tlp, Ta, To, Tlo><<<blocks, 32 * warps, 0, st>>>(list, rows, head_dim, o_out,
+                                                                      l_out, empty_rows);
+  count_launch();
+  return check_launch("combine_parts");
+}
+
+template <typename To, typename Tl>
+int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStream_t st) {
+  const int64_t n = rows * head_dim > rows ? rows * head_dim : rows;
+  if (n == 0) return FB_OK;
+  fill_sentinel<To, Tl><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(o, l, rows, head_dim);
+  count_launch();
+  return check_launch("fill_sentinel");
+}
+
+// ------------------------------------------------------------------ instantiations
+
+#define FB_INST_PARTIAL(MODE, MERGE, MAP)                                                      \
+  template int launch_partial_simt<MODE, MERGE, false, MAP<MODE::Tin>>(                       \
+      const MODE::Tin*, const MAP<MODE::Tin>&, int64_t, int64_t, int64_t, int64_t, int, double, \
+      MODE::Ta*, MODE::Tl*, const MergeOut<MODE>&, cudaStream_t);
+
+#define FB_INST_MODE(MODE)                  \
+  FB_INST_PARTIAL(MODE, false, RangeMap)    \
+  FB_INST_PARTIAL(MODE, true, RangeMap)     \
+  FB_INST_PARTIAL(MODE, false, SelectedMap) \
+  FB_INST_PARTIAL(MODE, true, SelectedMap)  \
+  FB_INST_PARTIAL(MODE, false, ResidualMap) \
+  FB_INST_PARTIAL(MODE, true, ResidualMap)
+
+FB_INST_MODE(ModeF64)
+FB_INST_MODE(ModeF32)
+FB_INST_MODE(ModeBF16)
+
+// lognorm-only passes for the sparse mask (scores in double for F64/F32 inputs,
+// as sparse.py:117-118 widens before the product)
+template int launch_partial_simt<ModeMaskF64, false, true, ConcatMap<double>>(const double*, const ConcatMap<double>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF64>&, cudaStream_t);
+template int launch_partial_simt<ModeMaskF32, false, true, ConcatMap<float>>(const float*, const ConcatMap<float>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF32>&, cudaStream_t);
+template int launch_partial_simt<ModeMaskBF16, false, true, ConcatMap<__nv_bfloat16>>(const __nv_bfloat16*, const ConcatMap<__nv_bfloat16>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskBF16>&, cudaStream_t);
+
+// combine: (part out, part lse, accumulate, out, lse out)
+template int launch_combine<double, double, double, double, double>(const CombineList&, int64_t, int64_t, double*, double*, int32_t*, cudaStream_t);
+template int launch_combine<float, double, double, float, double>(const CombineList&, int64_t, int64_t, float*, double*, int32_t*, cudaStream_t);
+template int launch_combine<float, float, float, float, float>(const CombineList&, int64_t, int64_t, float*, float*, int32_t*, cudaStream_t);
+template int launch_combine<float, float, float, __nv_bfloat16, float>(const CombineList&, int64_t, int64_t, __nv_bfloat16*, float*, int32_t*, cudaStream_t);
+template int launch_combine<double, double, double, float, double>(const CombineList&, int64_t, int64_t, float*, double*, int32_t*, cudaStream_t);
+
+template int launch_fill_sentinel<double, double>(double*, double*, int64_t, int64_t, cudaStream_t);
+template int launch_fill_sentinel<float, double>(float*, double*, int64_t, int64_t, cudaStream_t);
+template int launch_fill_sentinel<float, float>(float*, float*, int64_t, int64_t, cudaStream_t);
+template int launch_fill_sentinel<__nv_bfloat16, float>(__nv_bfloat16*, float*, int64_t, int64_t, cudaStream_t);
+
+}  // namespace fb

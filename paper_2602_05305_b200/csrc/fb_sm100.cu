@@ -1,0 +1,360 @@
+// K1 -- block-external ("refresh") partial attention on sm_100a.
+//
+// Computes, per group g (a kv head of one sequence, its G query heads stacked
+// into 128-row query tiles) and per key split, the normalised online-softmax
+// partial over keys [kb, ke) of the slab -- the reference's attention_partial
+// over the committed context (attention.py:136-182, called at :202).  This is
+// the HBM-bound kernel: the KV cache is streamed exactly once.
+//
+// Structure (one CTA per (split, group, 128-row query tile); 256 threads):
+//   warp 0      TMA producer: Q tile once, then K/V 128-key tiles into a
+//               STAGES-deep ring (128B-swizzled boxes of 64 columns).
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T  (SS, tcgen05.mma into
+//               TMEM, double-buffered S), then O += P_{j-1} V_{j-1} with P
+//               read straight from TMEM (TS form) -- QK^T of tile j overlaps
+//               the softmax of tile j-1.
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O).
+//   warps 4..7  softmax: thread t owns query row t (TMEM lane t); reads S,
+//               keeps (max, sum) in registers, writes P (bf16) back over S,
+//               rescales O in TMEM only when the running max grows by more
+//               than 2^8 (exact: the same max is used for l and O), and
+//               finally normalises O and writes the fp32 partial and the
+//               natural-log lognorm.
+#include "fb_kernels.cuh"
+#include "fb_sm100_ptx.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+namespace fb {
+namespace sm100 {
+
+constexpr int BM = 128;       // query rows per tile (TMEM lanes)
+constexpr int BN = 128;       // keys per tile
+constexpr int THREADS = 256;
+constexpr int BOX_COLS = 64;  // 128-byte swizzle span in bf16
+constexpr uint32_t TMEM_COLS = 512;
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P stays <= 256
+
+template <int D>
+struct Cfg {
+  static constexpr int STAGES = D == 128 ? 3 : 6;
+  static constexpr int NBOX = D / BOX_COLS;
+  static constexpr uint32_t BOX_BYTES = BM * BOX_COLS * 2;  // 16 KB (128 rows x 128 B)
+  static constexpr uint32_t TILE_BYTES = NBOX * BOX_BYTES;  // one Q / K / V tile
+  static constexpr uint32_t OFF_Q = 0;
+  static constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
+  static constexpr uint32_t OFF_V = OFF_K + STAGES * TILE_BYTES;
+  static constexpr uint32_t OFF_BAR = OFF_V + STAGES * TILE_BYTES;
+  static constexpr uint32_t BAR_BYTES = 256;
+  static constexpr uint32_t SMEM = OFF_BAR + BAR_BYTES + 1024;  // + alignment slack
+  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O = 256;
+};
+
+struct Barriers {
+  uint64_t q_full;
+  uint64_t k_full[6], k_empty[6], v_full[6], v_empty[6];
+  uint64_t s_full[2], p_ready[2];
+  uint64_t pv_done, o_full;
+  uint32_t tmem_base;
+};
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+               const __grid_constant__ CUtensorMap tm_v, int q_rows, int m_tiles, int key_begin,
+               int key_end, int keys_per_split, float scale_log2, float* __restrict__ po,
+               float* __restrict__ pl, long long rows_total) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Barriers* bar = reinterpret_cast<Barriers*>(smem + C::OFF_BAR);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int split = blockIdx.x;
+  const int g = blockIdx.y / m_tiles;
+  const int mt = blockIdx.y % m_tiles;
+  const int kb = key_begin + split * keys_per_split;
+  const int ke = min(kb + keys_per_split, key_end);
+  const int n_tiles = (ke - kb + BN - 1) / BN;  // >= 1 (host guarantees kb < ke)
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+    ptx::mbar_init(&bar->q_full, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&bar->k_full[s], 1);
+      ptx::mbar_init(&bar->k_empty[s], 1);
+      ptx::mbar_init(&bar->v_full[s], 1);
+      ptx::mbar_init(&bar->v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&bar->s_full[b], 1);
+      ptx::mbar_init(&bar->p_ready[b], 128);
+    }
+    ptx::mbar_init(&bar->pv_done, 1);
+    ptx::mbar_init(&bar->o_full, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(&bar->tmem_base, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bar->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t keep = ptx::policy_evict_last();
+      const uint64_t stream = ptx::policy_evict_first();
+      ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
+      for (int b = 0; b < C::NBOX; ++b)
+        ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
+                         mt * BM, g, keep);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % C::STAGES;
+        const uint32_t ph = (j / C::STAGES) & 1;
+        const int row = kb + j * BN;
+        ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+        ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+        for (int b = 0; b < C::NBOX; ++b)
+          ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
+                           &bar->k_full[s], b * BOX_COLS, row, g, stream);
+        ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+        ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+        for (int b = 0; b < C::NBOX; ++b)
+          ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
+                           &bar->v_full[s], b * BOX_COLS, row, g, stream);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, BN, false);
+      constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
+      const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
+      ptx::mbar_wait(&bar->q_full, 0);
+      ptx::tc_fence_after();
+      for (int j = 0; j <= n_tiles; ++j) {
+        if (j < n_tiles) {
+          const int s = j % C::STAGES;
+          ptx::mbar_wait(&bar->k_full[s], (j / C::STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
+          const uint32_t d_s = tmem + ((j & 1) ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            // K-major SW128: 16-element K step = +32 B inside a 64-column box
+            const uint32_t off = (kk / 4) * C::BOX_BYTES + (kk % 4) * 32;
+            ptx::mma_ss(d_s, ptx::sdesc_sw128(q_base + off, 16, 1024),
+                        ptx::sdesc_sw128(k_base + off, 16, 1024), IDESC_S, kk > 0);
+          }
+          ptx::tc_commit(&bar->k_empty[s]);
+          ptx::tc_commit(&bar->s_full[j & 1]);
+        }
+        if (j > 0) {
+          const int jj = j - 1;
+          const int s = jj % C::STAGES;
+          ptx::mbar_wait(&bar->p_ready[jj & 1], (jj >> 1) & 1);
+          ptx::mbar_wait(&bar->v_full[s], (jj / C::STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V + s * C::TILE_BYTES);
+          const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
+            ptx::mma_ts(tmem + C::COL_O, p_tmem + kk * 8,
+                        ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
+                        (jj > 0 || kk > 0) ? 1u : 0u);
+          }
+          ptx::tc_commit(&bar->v_empty[s]);
+          ptx::tc_commit(&bar->pv_done);
+          if (j == n_tiles) ptx::tc_commit(&bar->o_full);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int wq = warp & 3;                       // TMEM lane quarter
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const int row = wq * 32 + lane;                // row inside the 128-row tile
+    float m_used = -INFINITY;                      // running max, log2-scaled
+    float l = 0.f;
+    uint32_t r[32];
+    float s[BN];
+    for (int j = 0; j < n_tiles; ++j) {
+      const uint32_t s_col = (j & 1) ? C::COL_S1 : C::COL_S0;
+      ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+      }
+      const int valid = ke - (kb + j * BN);
+      if (valid < BN) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+          if (i >= valid) s[i] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
+      const float m_new = fmaxf(m_used, mx * scale_log2);
+      const bool need = m_new > m_used + RESCALE_THRESHOLD;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = ptx::ex2(m_used - m_new);
+        if (j > 0) {
+          // O holds P_0..P_{j-1} V: wait for the last PV before touching it
+          ptx::mbar_wait(&bar->pv_done, (j - 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            const uint32_t a = tmem + lane_off + C::COL_O + c * 32;
+            ptx::tmem_ld32(a, r);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            ptx::tmem_st32(a, r);
+          }
+          ptx::tmem_wait_st();
+        }
+        l *= alpha;
+        m_used = m_new;
+      }
+      const float neg = -m_used;
+      float lsum = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = ptx::ex2(fmaf(s[c * 64 + 2 * i], scale_log2, neg));
+          const float p1 = ptx::ex2(fmaf(s[c * 64 + 2 * i + 1], scale_log2, neg));
+          lsum += p0 + p1;
+          r[i] = ptx::pack_bf16(p0, p1);
+        }
+        ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
+      }
+      l += lsum;
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&bar->p_ready[j & 1]);
+    }
+    // ------------------------------------------------------------ epilogue
+    ptx::mbar_wait(&bar->o_full, 0);
+    ptx::tc_fence_after();
+    const float inv = 1.f / l;
+    const float lse = (m_used + log2f(l)) * 0.69314718055994530942f;
+    const int grow = mt * BM + row;
+    const bool live = grow < q_rows;
+    const long long out_row = (long long)split * rows_total + (long long)g * q_rows + grow;
+    float* dst = po + out_row * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
+      ptx::tmem_wait_ld();
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 v4 = make_float4(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv,
+                                  __uint_as_float(r[i + 2]) * inv, __uint_as_float(r[i + 3]) * inv);
+          *reinterpret_cast<float4*>(dst + c * 32 + i) = v4;
+        }
+      }
+    }
+    if (live) pl[out_row] = lse;
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 view [dim2][dim1][D] with a 128-row x 64-col 128B-swizzled box.
+// Rows >= dim1 read as zero (TMA out-of-bounds fill), so slab tails are safe.
+static int make_map(CUtensorMap* map, const void* base, int64_t D, int64_t dim1,
+                    int64_t dim1_stride_rows, int64_t dim2) {
+  auto enc = get_encode();
+  if (!enc) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)dim1, (cuuint64_t)dim2};
+  cuuint64_t strides[2] = {(cuuint64_t)(D * 2), (cuuint64_t)(dim1_stride_rows * D * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)BOX_COLS, (cuuint32_t)BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return FB_OK;
+}
+
+}  // namespace sm100
+
+bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 128; }
+
+template <int D>
+static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                            int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
+                            int64_t key_end, int64_t keys_per_split, int splits, double scale,
+                            float* po, float* pl, cudaStream_t st) {
+  using C = sm100::Cfg<D>;
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = sm100::make_map(&mq, q, D, q_rows, q_rows, groups)) != FB_OK) return rc;
+  if ((rc = sm100::make_map(&mk, k, D, key_end, kv_rows_cap, groups)) != FB_OK) return rc;
+  if ((rc = sm100::make_map(&mv, v, D, key_end, kv_rows_cap, groups)) != FB_OK) return rc;
+  auto kern = sm100::refresh_kernel<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const int m_tiles = (int)((q_rows + sm100::BM - 1) / sm100::BM);
+  dim3 grid((unsigned)splits, (unsigned)(groups * m_tiles));
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  kern<<<grid, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, (int)q_rows, m_tiles, (int)key_begin,
+                                              (int)key_end, (int)keys_per_split, scale_log2, po, pl,
+                                              (long long)(groups * q_rows));
+  count_launch();
+  return check_launch("refresh_kernel(sm100)");
+}
+
+int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                         int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                         int64_t key_begin, int64_t key_end, int64_t keys_per_split, int splits,
+                         double scale, float* po, float* pl, cudaStream_t st) {
+  if (head_dim == 128)
+    return launch_refresh_d<128>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
+                                 keys_per_split, splits, scale, po, pl, st);
+  if (head_dim == 64)
+    return launch_refresh_d<64>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
+                                keys_per_split, splits, scale, po, pl, st);
+  return FB_ERR_UNSUPPORTED;
+}
+
+}  // namespace fb

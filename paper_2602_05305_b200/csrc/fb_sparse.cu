@@ -1,0 +1,196 @@
+// Sparse key-block selection: K5 block mass and K6 stable top-k.
+//
+// Reference: build_sparse_mask (sparse.py:83-136).  The softmax runs over ALL
+// keys passed -- the committed context [0, n_ext) plus the current block --
+// with per-row normalisation (linalg.py:52-65, used at sparse.py:119); the
+// mass of external block b is the sum of those probabilities over the block's
+// rows and over every query row (sparse.py:120-125); the budget is
+// min(nb, max(1, ceil(density*n_ext/kbs))) (sparse.py:126) and ranking is a
+// stable sort on -mass, i.e. ties go to the lower block index (sparse.py:127),
+// emitted ascending (sparse.py:128).
+//
+// Mass = sum_r sum_{t in b} exp(s_rt - lse_r), with lse_r the row log-sum-exp
+// over all keys (computed by the partial kernel in lognorm-only mode).  Block
+// sums use a fixed reduction order, so equal inputs give bit-equal masses and
+// the tie rule is exact.
+#include "fb_kernels.cuh"
+
+namespace fb {
+
+constexpr int MASS_WARPS = 8;
+
+// grid: (ceil(nb / MASS_WARPS), groups); block: 32*MASS_WARPS.
+// smem: K rows of the CTA's blocks [MASS_WARPS*kbs][d+1] in the score type.
+template <typename Mode>
+__global__ void __launch_bounds__(32 * MASS_WARPS)
+block_mass_kernel(const typename Mode::Tin* __restrict__ q, const typename Mode::Tin* __restrict__ k,
+                  const double* __restrict__ row_lse, int64_t q_rows, int64_t head_dim,
+                  int64_t slab_stride, int64_t n_ext, int64_t kbs, int64_t nb, double scale,
+                  double* __restrict__ mass) {
+  using Ts = typename Mode::Ts;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ts* ks = reinterpret_cast<Ts*>(smem_raw);
+  const int64_t g = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b0 = (int64_t)blockIdx.x * MASS_WARPS;
+  const int64_t ld = head_dim + 1;
+
+  // stage the keys of this CTA's blocks
+  const int64_t key0 = b0 * kbs;
+  const int64_t nkeys = min((int64_t)MASS_WARPS * kbs, n_ext - key0);
+  for (int64_t i = threadIdx.x; i < nkeys * head_dim; i += blockDim.x) {
+    const int64_t t = i / head_dim, c = i % head_dim;
+    ks[t * ld + c] = cvt<Ts>(k[g * slab_stride + (key0 + t) * head_dim + c]);
+  }
+  __syncthreads();
+
+  const int64_t b = b0 + warp;
+  if (b >= nb) return;
+  const int64_t lo = b * kbs;
+  const int64_t hi = min(lo + kbs, n_ext);
+  double acc = 0.0;
+  for (int64_t t = lo + lane; t < hi; t += 32) {
+    const Ts* kr = ks + (t - key0) * ld;
+    double part = 0.0;
+    for (int64_t r = 0; r < q_rows; ++r) {
+      const typename Mode::Tin* qr = q + (g * q_rows + r) * head_dim;
+      Ts s = 0;
+      for (int64_t c = 0; c < head_dim; ++c) s += cvt<Ts>(qr[c]) * kr[c];
+      part += exp((double)(s * (Ts)scale) - row_lse[g * q_rows + r]);
+    }
+    acc += part;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) mass[g * nb + b] = acc;
+}
+
+// ---------------------------------------------------------------- top-k
+
+// Orders (mass desc, index asc) -- a strict total order.
+__device__ __forceinline__ bool before(double ma, int ia, double mb, int ib) {
+  return ma > mb || (ma == mb && ia < ib);
+}
+
+// One CTA per group: bitonic sort of (mass, index) in shared memory, mark the
+// first `budget`, compact the marked indices in ascending order.
+__global__ void topk_bitonic_kernel(const double* __restrict__ mass, int64_t nb, int64_t budget,
+                                    int32_t* __restrict__ selected, int pow2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* key = reinterpret_cast<double*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + pow2);
+  int* flag = idx + pow2;  // nb + 1 ints (exclusive prefix scratch)
+  const int64_t g = blockIdx.x;
+  const double* m = mass + g * nb;
+  for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+    key[i] = i < nb ? m[i] : -INFINITY;
+    idx[i] = i < nb ? i : (int)(nb + i);  // padding sorts last
+  }
+  __syncthreads();
+  for (int size = 2; size <= pow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool asc = (i & size) == 0;  // "ascending" in the before() order
+          const bool swap = asc ? before(key[j], idx[j], key[i], idx[i])
+                                : before(key[i], idx[i], key[j], idx[j]);
+          if (swap) {
+            const double tk = key[i]; key[i] = key[j]; key[j] = tk;
+            const int ti = idx[i]; idx[i] = idx[j]; idx[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) flag[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < budget; i += blockDim.x) flag[idx[i]] = 1;
+  __syncthreads();
+  // ascending compaction: serial scan by warp 0 in 32-wide chunks
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int64_t c0 = 0; c0 < nb; c0 += 32) {
+      const int64_t i = c0 + lane;
+      const int f = i < nb ? flag[i] : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (f) selected[g * budget + base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+      base += __popc(bal);
+    }
+  }
+}
+
+// Fallback for very large nb: rank by counting (O(nb^2), exact).
+__global__ void topk_rank_kernel(const double* __restrict__ mass, int64_t nb, int64_t budget,
+                                 int32_t* __restrict__ selected, unsigned char* __restrict__ flag) {
+  const int64_t g = blockIdx.y;
+  const double* m = mass + g * nb;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const double mi = m[i];
+  int64_t rank = 0;
+  for (int64_t j = 0; j < nb; ++j) rank += before(m[j], (int)j, mi, (int)i) ? 1 : 0;
+  flag[g * nb + i] = rank < budget ? 1 : 0;
+}
+__global__ void compact_flags_kernel(const unsigned char* __restrict__ flag, int64_t nb,
+                                     int64_t budget, int32_t* __restrict__ selected) {
+  const int64_t g = blockIdx.x;
+  const int lane = threadIdx.x;
+  int base = 0;
+  for (int64_t c0 = 0; c0 < nb; c0 += 32) {
+    const int64_t i = c0 + lane;
+    const int f = i < nb ? flag[g * nb + i] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (f) selected[g * budget + base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+    base += __popc(bal);
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+
+template <typename Mode>
+int launch_block_mass(const typename Mode::Tin* q, const typename Mode::Tin* k,
+                      const double* row_lse, int64_t groups, int64_t q_rows, int64_t head_dim,
+                      int64_t slab_stride, int64_t n_ext, int64_t kbs, double scale, double* mass,
+                      cudaStream_t st) {
+  const int64_t nb = (n_ext + kbs - 1) / kbs;
+  if (nb == 0 || groups == 0) return FB_OK;
+  const size_t smem = sizeof(typename Mode::Ts) * (size_t)(MASS_WARPS * kbs) * (size_t)(head_dim + 1);
+  if (smem > 220 * 1024) return fail(FB_ERR_UNSUPPORTED, "key_block_size * head_dim too large for block_mass");
+  auto kern = block_mass_kernel<Mode>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)((nb + MASS_WARPS - 1) / MASS_WARPS), (unsigned)groups);
+  kern<<<grid, 32 * MASS_WARPS, smem, st>>>(q, k, row_lse, q_rows, head_dim, slab_stride, n_ext, kbs,
+                                            nb, scale, mass);
+  count_launch();
+  return check_launch("block_mass_kernel");
+}
+
+template int launch_block_mass<ModeMaskF64>(const double*, const double*, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, double, double*, cudaStream_t);
+template int launch_block_mass<ModeMaskF32>(const float*, const float*, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, double, double*, cudaStream_t);
+template int launch_block_mass<ModeMaskBF16>(const __nv_bfloat16*, const __nv_bfloat16*, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, double, double*, cudaStream_t);
+
+int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, int32_t* selected,
+                void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (groups == 0 || budget == 0) return FB_OK;
+  int pow2 = 1;
+  while (pow2 < nb) pow2 <<= 1;
+  const size_t smem = (size_t)pow2 * (sizeof(double) + sizeof(int)) + (size_t)(nb + 1) * sizeof(int);
+  if (smem <= 200 * 1024) {
+    cudaFuncSetAttribute(topk_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    topk_bitonic_kernel<<<(unsigned)groups, 1024, smem, st>>>(mass, nb, budget, selected, pow2);
+    count_launch();
+    return check_launch("topk_bitonic_kernel");
+  }
+  if (scratch == nullptr || scratch_bytes < (size_t)(groups * nb))
+    return fail(FB_ERR_VALUE, "top-k over this many blocks needs groups*num_blocks bytes of scratch");
+  unsigned char* flag = reinterpret_cast<unsigned char*>(scratch);
+  dim3 grid((unsigned)((nb + 255) / 256), (unsigned)groups);
+  topk_rank_kernel<<<grid, 256, 0, st>>>(mass, nb, budget, selected, flag);
+  compact_flags_kernel<<<(unsigned)groups, 32, 0, st>>>(flag, nb, budget, selected);
+  count_launch(2);
+  return check_launch("topk_rank_kernel");
+}
+
+}  // namespace fb

@@ -1,0 +1,343 @@
+"""Batched device API over the C ABI: torch tensors in, torch tensors out.
+
+Layouts (see include/flashblock_b200.h): a call processes ``groups`` pairs of
+(query block [q_rows, d], key/value slab [kv_rows_cap, d]).  For a GQA layer
+with Q [b, Hq, B, d] and a KV cache [b, Hkv, N_cap, d], use
+``gqa_view`` -- groups = b*Hkv, q_rows = (Hq/Hkv)*B.
+
+Every function here launches on the current torch CUDA stream and never
+synchronises the host unless ``check=True`` (which reads the degenerate-row
+counter back to raise ``DegenerateInputError`` like the reference).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .errors import DegenerateInputError, ShapeError
+
+_CODE = {torch.float64: _lib.FB_F64, torch.float32: _lib.FB_F32, torch.bfloat16: _lib.FB_BF16}
+# (partial out dtype, lognorm dtype) per mode
+PARTIAL_TYPES = {
+    _lib.FB_F64: (torch.float64, torch.float64),
+    _lib.FB_F32: (torch.float32, torch.float64),
+    _lib.FB_BF16: (torch.float32, torch.float32),
+}
+_OUT_CODE = {torch.float64: _lib.FB_F64, torch.float32: _lib.FB_F32, torch.bfloat16: _lib.FB_BF16}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _CODE[t.dtype]
+    except KeyError:
+        raise ShapeError(f"unsupported dtype {t.dtype}; expected float64, float32 or bfloat16")
+
+
+def mode_of_partial(out: torch.Tensor, lse: torch.Tensor) -> int:
+    key = (out.dtype, lse.dtype)
+    for code, types in PARTIAL_TYPES.items():
+        if types == key:
+            return code
+    raise ShapeError(f"partial dtypes {key} match no precision mode")
+
+
+def require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise RuntimeError("paper_2602_05305_b200 runs on CUDA tensors only (no CPU fallback)")
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+class _Workspace:
+    """Per-device scratch buffer for split-KV partials, grown on demand."""
+
+    def __init__(self):
+        self._bufs: dict[int, torch.Tensor] = {}
+
+    def get(self, device: torch.device, nbytes: int) -> torch.Tensor:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        buf = self._bufs.get(idx)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            self._bufs[idx] = buf
+        return buf
+
+
+WORKSPACE = _Workspace()
+
+
+def gqa_view(q: torch.Tensor, num_kv_heads: int) -> torch.Tensor:
+    """[b, Hq, B, d] -> [b*Hkv, (Hq/Hkv)*B, d] (no copy)."""
+    b, hq, blk, d = q.shape
+    if hq % num_kv_heads:
+        raise ShapeError(f"{hq} query heads not divisible by {num_kv_heads} kv heads")
+    return q.contiguous().view(b * num_kv_heads, (hq // num_kv_heads) * blk, d)
+
+
+def _as3(x: torch.Tensor, name: str) -> torch.Tensor:
+    if x.dim() == 2:
+        return x.unsqueeze(0)
+    if x.dim() == 3:
+        return x
+    if x.dim() == 4:
+        return x.reshape(x.shape[0] * x.shape[1], x.shape[2], x.shape[3])
+    raise ShapeError(f"{name} must be 2-, 3- or 4-D, got {x.dim()}-D")
+
+
+def _check_kv(q3, k3, v3):
+    if k3.shape != v3.shape:
+        raise ShapeError(f"keys {tuple(k3.shape)} and values {tuple(v3.shape)} differ")
+    if k3.shape[0] != q3.shape[0] or k3.shape[2] != q3.shape[2]:
+        raise ShapeError(f"queries {tuple(q3.shape)} do not match keys {tuple(k3.shape)}")
+    if not (q3.dtype == k3.dtype == v3.dtype):
+        raise ShapeError("q, k, v must share one dtype")
+
+
+def attention_partial(q, k, v, key_begin: int = 0, key_end: int | None = None,
+                      scale: float | None = None, out=None, lse=None):
+    """K1: normalised partial over slab rows [key_begin, key_end) for every group.
+
+    q [groups, q_rows, d] (or [q_rows, d]); k, v [groups, cap, d].
+    Returns (o, lse) in the mode's partial types.
+    """
+    q3, k3, v3 = _as3(q, "q"), _as3(k, "k"), _as3(v, "v")
+    require_cuda(q3, k3, v3)
+    _check_kv(q3, k3, v3)
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    groups, q_rows, d = q3.shape
+    cap = k3.shape[1]
+    key_end = cap if key_end is None else int(key_end)
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
+    if lse is None:
+        lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_partial_workspace_bytes(code, groups, q_rows, d, max(0, key_end - key_begin))
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_attention_partial", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
+              int(key_begin), key_end, scale, _p(out), _p(lse), _p(ws),
+              0 if ws is None else ws.numel(), _stream(q3))
+    return out, lse
+
+
+def _empty_counter(device):
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def _raise_if_empty(counter, what):
+    if counter is not None and int(counter.item()) > 0:
+        raise DegenerateInputError(f"{what}: some query rows have no keys on either side")
+
+
+def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
+                   out_dtype: torch.dtype | None = None, want_lse: bool = False,
+                   want_internal: bool = False, check: bool = False, out=None):
+    """K2: block-internal partial fused with the merge against the cached
+    external partial.  Returns out, or a tuple (out, lse_merged?, (o_int, lse_int)?)."""
+    q3, k3, v3 = _as3(q, "q"), _as3(k_in, "k_in"), _as3(v_in, "v_in")
+    require_cuda(q3, k3, v3, o_ext, lse_ext)
+    _check_kv(q3, k3, v3)
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    groups, q_rows, d = q3.shape
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    o_ext = o_ext.contiguous()
+    lse_ext = lse_ext.contiguous()
+    if o_ext.dtype != ot or lse_ext.dtype != lt or o_ext.numel() != groups * q_rows * d \
+            or lse_ext.numel() != groups * q_rows:
+        raise ShapeError("cached partial does not match the queries (shape or precision)")
+    if out_dtype is None:
+        out_dtype = ot
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
+    lse_m = torch.empty((groups, q_rows), dtype=lt, device=q3.device) if want_lse else None
+    o_int = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device) if want_internal else None
+    l_int = torch.empty((groups, q_rows), dtype=lt, device=q3.device) if want_internal else None
+    cnt = _empty_counter(q3.device) if check else None
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    _lib.call("fb_internal_merge", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
+              scale, _p(o_ext), _p(lse_ext), _p(out), _OUT_CODE[out.dtype], _p(lse_m), _p(o_int),
+              _p(l_int), _p(cnt), _stream(q3))
+    _raise_if_empty(cnt, "internal_merge")
+    if not (want_lse or want_internal):
+        return out
+    res = [out]
+    if want_lse:
+        res.append(lse_m)
+    if want_internal:
+        res.append((o_int, l_int))
+    return tuple(res)
+
+
+def combine(parts, out_dtype: torch.dtype | None = None, want_lse: bool = True,
+            check: bool = False):
+    """K3: log-space merge of partials [(o, lse), ...] over disjoint key groups."""
+    if not 1 <= len(parts) <= 16:
+        raise ValueError("combine takes 1..16 partials")
+    o0, l0 = parts[0]
+    require_cuda(o0, l0)
+    code = mode_of_partial(o0, l0)
+    os_, ls_ = [], []
+    for o, l in parts:
+        if o.shape != o0.shape or l.shape != l0.shape:
+            raise ShapeError(f"partial shapes differ: {tuple(o0.shape)} vs {tuple(o.shape)}")
+        if mode_of_partial(o, l) != code:
+            raise ShapeError("partials of different precision modes")
+        os_.append(o.contiguous())
+        ls_.append(l.contiguous())
+    d = o0.shape[-1]
+    rows = l0.numel()
+    ot, lt = PARTIAL_TYPES[code]
+    out_dtype = ot if out_dtype is None else out_dtype
+    out = torch.empty(o0.shape, dtype=out_dtype, device=o0.device)
+    lse = torch.empty(l0.shape, dtype=lt, device=o0.device) if want_lse else None
+    cnt = _empty_counter(o0.device) if check else None
+    _lib.call("fb_combine", code, len(parts), _lib.ptr_array([_p(o) for o in os_]),
+              _lib.ptr_array([_p(l) for l in ls_]), rows, d, _p(out), _OUT_CODE[out_dtype], _p(lse),
+              _p(cnt), _stream(o0))
+    _raise_if_empty(cnt, "combine")
+    return out, lse
+
+
+def full_attention(q, k, v, n_ext: int, k_in, v_in, scale: float | None = None,
+                   out_dtype: torch.dtype | None = None, o_ext=None, lse_ext=None,
+                   check: bool = False, out=None):
+    """K4 / refresh step: attention over [cache rows 0..n_ext) | current block],
+    normalised output; the refreshed external partial lands in (o_ext, lse_ext)."""
+    q3, k3, v3 = _as3(q, "q"), _as3(k, "k"), _as3(v, "v")
+    ki3, vi3 = _as3(k_in, "k_in").contiguous(), _as3(v_in, "v_in").contiguous()
+    require_cuda(q3, k3, v3, ki3, vi3)
+    _check_kv(q3, k3, v3)
+    _check_kv(q3, ki3, vi3)
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    groups, q_rows, d = q3.shape
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    if o_ext is None:
+        o_ext = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
+    if lse_ext is None:
+        lse_ext = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    out_dtype = ot if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
+    cnt = _empty_counter(q3.device) if check else None
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_partial_workspace_bytes(code, groups, q_rows, d, int(n_ext))
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_full_attention", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
+              int(n_ext), _p(ki3), _p(vi3), ki3.shape[1], scale, _p(o_ext), _p(lse_ext), _p(out),
+              _OUT_CODE[out.dtype], _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
+    _raise_if_empty(cnt, "full_attention")
+    return out, o_ext, lse_ext
+
+
+# ------------------------------------------------------------------ sparse
+
+
+def mask_budget(n_ext: int, density: float, key_block_size: int) -> int:
+    """min(nb, max(1, ceil(density*n_ext/kbs))) evaluated in double (sparse.py:126)."""
+    return int(_lib.load().fb_mask_budget(int(n_ext), float(density), int(key_block_size)))
+
+
+def block_mass(q, k, k_in, n_ext: int, key_block_size: int = 16, scale: float | None = None):
+    """K5: float64 softmax mass per external key block, summed over each group's rows."""
+    q3, k3, ki3 = _as3(q, "q").contiguous(), _as3(k, "k").contiguous(), _as3(k_in, "k_in").contiguous()
+    require_cuda(q3, k3, ki3)
+    groups, q_rows, d = q3.shape
+    if k3.shape[0] != groups or k3.shape[2] != d or ki3.shape[0] != groups or ki3.shape[2] != d:
+        raise ShapeError("q and keys must be 2-D with matching feature dim")
+    code = dtype_code(q3)
+    nb = -(-int(n_ext) // int(key_block_size))
+    mass = torch.empty((groups, nb), dtype=torch.float64, device=q3.device)
+    wsb = _lib.load().fb_block_mass_workspace_bytes(groups, q_rows)
+    ws = WORKSPACE.get(q3.device, wsb)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    _lib.call("fb_block_mass", code, _p(q3), _p(k3), _p(ki3), groups, q_rows, d, k3.shape[1],
+              int(n_ext), ki3.shape[1], int(key_block_size), scale, _p(mass), _p(ws), ws.numel(),
+              _stream(q3))
+    return mass
+
+
+def topk_blocks(mass: torch.Tensor, budget: int) -> torch.Tensor:
+    """K6: stable top-`budget` blocks per group (mass desc, index asc), ascending int32."""
+    require_cuda(mass)
+    m2 = mass.reshape(-1, mass.shape[-1]).contiguous()
+    sel = torch.empty((m2.shape[0], int(budget)), dtype=torch.int32, device=mass.device)
+    _lib.call("fb_topk_blocks", _p(m2), m2.shape[0], m2.shape[1], int(budget), _p(sel), _stream(m2))
+    return sel
+
+
+def sparse_partitioned(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
+                       key_block_size: int = 16, scale: float | None = None,
+                       out_dtype: torch.dtype | None = None, check: bool = False):
+    """K7: first sparse step -- (out, selected partial, residual partial)."""
+    q3, k3, v3 = _as3(q, "q").contiguous(), _as3(k, "k").contiguous(), _as3(v, "v").contiguous()
+    ki3, vi3 = _as3(k_in, "k_in").contiguous(), _as3(v_in, "v_in").contiguous()
+    require_cuda(q3, k3, v3, ki3, vi3, selected)
+    _check_kv(q3, k3, v3)
+    _check_kv(q3, ki3, vi3)
+    groups, q_rows, d = q3.shape
+    if k3.shape[1] < n_ext:
+        raise ShapeError(f"key set has {k3.shape[1]} rows but mask covers {n_ext} external keys")
+    sel = selected.reshape(groups, -1).to(torch.int32).contiguous()
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    mk = lambda: (torch.empty((groups, q_rows, d), dtype=ot, device=q3.device),
+                  torch.empty((groups, q_rows), dtype=lt, device=q3.device))
+    o_sel, l_sel = mk()
+    o_res, l_res = mk()
+    out_dtype = ot if out_dtype is None else out_dtype
+    out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
+    cnt = _empty_counter(q3.device) if check else None
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    _lib.call("fb_sparse_partitioned", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
+              q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
+              int(key_block_size), scale, _p(o_sel), _p(l_sel), _p(o_res), _p(l_res), _p(out),
+              _OUT_CODE[out_dtype], _p(cnt), _stream(q3))
+    _raise_if_empty(cnt, "sparse_partitioned")
+    return out, (o_sel, l_sel), (o_res, l_res)
+
+
+def sparse_attend_merge(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
+                        residual=None, key_block_size: int = 16, scale: float | None = None,
+                        out_dtype: torch.dtype | None = None, check: bool = False):
+    """K8: later sparse steps -- selected blocks + current block, merged with
+    the cached residual (or renormalised sparse-only when residual is None)."""
+    q3, k3, v3 = _as3(q, "q").contiguous(), _as3(k, "k").contiguous(), _as3(v, "v").contiguous()
+    ki3, vi3 = _as3(k_in, "k_in").contiguous(), _as3(v_in, "v_in").contiguous()
+    require_cuda(q3, k3, v3, ki3, vi3, selected)
+    _check_kv(q3, k3, v3)
+    _check_kv(q3, ki3, vi3)
+    groups, q_rows, d = q3.shape
+    if k3.shape[1] < n_ext:
+        raise ShapeError(f"key set has {k3.shape[1]} rows but mask covers {n_ext} external keys")
+    sel = selected.reshape(groups, -1).to(torch.int32).contiguous()
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    o_res = l_res = None
+    if residual is not None:
+        o_res, l_res = residual[0].contiguous(), residual[1].contiguous()
+        if (o_res.dtype, l_res.dtype) != (ot, lt):
+            raise ShapeError("residual precision does not match the queries")
+    out_dtype = ot if out_dtype is None else out_dtype
+    out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
+    cnt = _empty_counter(q3.device) if check else None
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    _lib.call("fb_sparse_attend_merge", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
+              q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
+              int(key_block_size), scale, _p(o_res), _p(l_res), _p(out), _OUT_CODE[out_dtype],
+              _p(cnt), _stream(q3))
+    _raise_if_empty(cnt, "sparse_attend_merge")
+    return out

@@ -1,0 +1,347 @@
+"""GPU parity: the B200 kernels against the golden vectors of the real
+reference and against the CPU oracle (tests/golden, oracle/).
+
+Tolerances (stated, per north_star):
+  * F64 mode     : 1e-12 absolute on outputs, 1e-10 on lognorms.
+  * F32 mode     : max|diff| <= 1e-4 * max|ref| (outputs), |dLSE| <= 1e-4 * max(1, |LSE|).
+  * BF16 mode    : max|diff| <= 1e-2 * max|ref| against the float64 oracle on
+                   bf16-exact inputs (mean reported in the assertion message);
+                   lognorm within 1e-3 absolute.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import flashblock_oracle as orc  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2602_05305_b200  # noqa: F401  (fails loudly if libfb200.so is missing)
+
+
+def fb():
+    import paper_2602_05305_b200 as m
+
+    return m
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = max(1e-30, float(np.max(np.abs(ref))))
+    return float(np.max(np.abs(got - ref))) / scale
+
+
+def bf16_exact(rng, shape, sigma=1.0):
+    x = torch.from_numpy((rng.standard_normal(shape) * sigma).astype(np.float32))
+    return x.to(torch.bfloat16)
+
+
+# ----------------------------------------------------------------- golden, mirror API
+
+
+@pytest.mark.parametrize("name", ["p0", "p1", "p2", "p3", "p4", "p5", "p6"])
+def test_partial_matches_reference_golden(golden, golden_meta, name):
+    m = golden_meta[name]
+    p = fb().attention_partial(golden[f"{name}_q"], golden[f"{name}_k"], golden[f"{name}_v"],
+                               tile_size=m["tile"])
+    ref_o, ref_l = golden[f"{name}_out"], golden[f"{name}_lse"]
+    assert p.out.dtype == ref_o.dtype and p.lognorm.dtype == np.float64
+    np.testing.assert_array_equal(np.isneginf(p.lognorm), np.isneginf(ref_l))
+    if m["dtype"] == "float64":
+        np.testing.assert_allclose(p.out, ref_o, atol=1e-12)
+        np.testing.assert_allclose(p.lognorm, ref_l, atol=1e-10)
+    else:
+        assert rel_err(p.out, ref_o) <= 1e-4
+        fin = np.isfinite(ref_l)
+        assert np.all(np.abs(p.lognorm[fin] - ref_l[fin]) <= 1e-4 * np.maximum(1, np.abs(ref_l[fin])))
+
+
+@pytest.mark.parametrize("b", [0, 1, 17, 39, 40])
+def test_streamed_and_merge_match_golden(golden, b):
+    e, i = fb().attention_streamed(golden["s_q"], golden["s_k"], golden["s_v"], b)
+    np.testing.assert_allclose(e.out, golden[f"s_b{b}_ext_out"], atol=1e-12)
+    np.testing.assert_allclose(i.out, golden[f"s_b{b}_int_out"], atol=1e-12)
+    np.testing.assert_array_equal(np.isneginf(e.lognorm), np.isneginf(golden[f"s_b{b}_ext_lse"]))
+    np.testing.assert_allclose(fb().merge_partials(e, i), golden[f"s_b{b}_merged"], atol=1e-12)
+
+
+def test_combine_empty_rows_pass_through_bitwise(golden):
+    A = fb().AttnPartial(golden["c_a_out"], golden["c_a_lse"])
+    B = fb().AttnPartial(golden["c_b_out"], golden["c_b_lse"])
+    c = fb().combine_partials(A, B)
+    live = np.isfinite(golden["c_lse"])
+    np.testing.assert_allclose(c.out, golden["c_out"], atol=1e-13)
+    np.testing.assert_array_equal(np.isneginf(c.lognorm), ~live)
+    # rows empty on one side pass through bit for bit (tests/test_attention.py:182-190 there)
+    one_side = np.isneginf(golden["c_a_lse"]) ^ np.isneginf(golden["c_b_lse"])
+    np.testing.assert_array_equal(c.out[one_side], golden["c_out"][one_side])
+    np.testing.assert_array_equal(c.lognorm[one_side], golden["c_lse"][one_side])
+
+
+def test_combine_symmetric_bitwise(rng):
+    q, k, v = rng.standard_normal((4, 8)), rng.standard_normal((30, 8)), rng.standard_normal((30, 8))
+    a = fb().attention_partial(q, k[:11], v[:11])
+    b = fb().attention_partial(q, k[11:], v[11:])
+    ab, ba = fb().combine_partials(a, b), fb().combine_partials(b, a)
+    assert (ab.out == ba.out).all() and (ab.lognorm == ba.lognorm).all()
+
+
+def test_merge_rejects_fully_empty_rows():
+    AP = fb().AttnPartial
+    with pytest.raises(fb().DegenerateInputError):
+        fb().merge_partials(AP.empty(2, 4), AP.empty(2, 4))
+
+
+def test_three_way_association(rng):
+    for _ in range(5):
+        q, k, v = rng.standard_normal((4, 8)), rng.standard_normal((30, 8)), rng.standard_normal((30, 8))
+        c1, c2 = sorted(rng.integers(0, 31, size=2))
+        p = [fb().attention_partial(q, k[a:b], v[a:b]) for a, b in ((0, c1), (c1, c2), (c2, 30))]
+        left = fb().combine_partials(fb().combine_partials(p[0], p[1]), p[2])
+        right = fb().combine_partials(p[0], fb().combine_partials(p[1], p[2]))
+        np.testing.assert_allclose(left.out, right.out, atol=1e-10)
+        np.testing.assert_allclose(left.out, orc.dense(q, k, v), atol=1e-10)
+
+
+def test_shift_stability_bitwise_on_lattice():
+    # reference tests/test_attention.py:242-263: +80 on every score must vanish
+    rng = np.random.Generator(np.random.Philox(99))
+    for _ in range(3):
+        n, nq, d = 48, 6, 16
+        boundary = int(rng.integers(0, n + 1))
+        q = (rng.integers(-128, 129, size=(nq, d)) / 64.0).astype(np.float32)
+        k = (rng.integers(-128, 129, size=(n, d)) / 64.0).astype(np.float32)
+        v = rng.standard_normal((n, d)).astype(np.float32)
+        k_aug = np.hstack([k, np.ones((n, 1), dtype=np.float32)])
+        v_aug = np.hstack([v, np.zeros((n, 1), dtype=np.float32)])
+        outs = []
+        for c in (0.0, 320.0):
+            q_aug = np.hstack([q, np.full((nq, 1), c, dtype=np.float32)])
+            e, i = fb().attention_streamed(q_aug, k_aug, v_aug, boundary, scale=0.25)
+            outs.append(fb().merge_partials(e, i))
+        assert (outs[0] == outs[1]).all()
+
+
+def test_reuse_matches_golden(golden):
+    entry = fb().CacheEntry(partial=fb().AttnPartial(golden["r_ext_out"], golden["r_ext_lse"]),
+                            step_created=0, block_id=0)
+    out, internal = fb().attention_with_reuse(golden["r_q1"], entry, golden["r_k"][268:],
+                                              golden["r_v"][268:])
+    assert rel_err(out, golden["r_out"]) <= 1e-4
+    assert rel_err(internal.out, golden["r_int_out"]) <= 1e-4
+    np.testing.assert_allclose(internal.lognorm, golden["r_int_lse"], atol=1e-4)
+
+
+def test_reuse_preconditions(rng):
+    q, k, v = rng.standard_normal((4, 8)), rng.standard_normal((40, 8)), rng.standard_normal((40, 8))
+    ext, _ = fb().attention_streamed(q, k, v, 32)
+    with pytest.raises(fb().ReusePreconditionError):
+        fb().attention_with_reuse(q, None, k[32:], v[32:])
+    with pytest.raises(fb().ReusePreconditionError):
+        fb().attention_with_reuse(q, fb().CacheEntry(ext, 0, valid=False), k[32:], v[32:])
+    with pytest.raises(fb().ReusePreconditionError):
+        fb().attention_with_reuse(q[:2], fb().CacheEntry(ext, 0), k[32:], v[32:])
+
+
+def test_reuse_with_same_queries_is_exact(rng):
+    q, k, v = rng.standard_normal((4, 8)), rng.standard_normal((40, 8)), rng.standard_normal((40, 8))
+    ext, _ = fb().attention_streamed(q, k, v, 32)
+    out, _ = fb().attention_with_reuse(q, fb().CacheEntry(ext, 0, 0), k[32:], v[32:])
+    np.testing.assert_allclose(out, orc.dense(q, k, v), atol=1e-12)
+
+
+def test_shape_and_bounds_errors(rng):
+    q, k, v = rng.standard_normal((4, 8)), rng.standard_normal((20, 8)), rng.standard_normal((20, 8))
+    with pytest.raises(fb().ShapeError):
+        fb().attention_partial(q, k[:, :4], v)
+    with pytest.raises(fb().ShapeError):
+        fb().attention_partial(q, k, v[:5])
+    with pytest.raises(fb().BoundsError):
+        fb().attention_streamed(q, k, v, 21)
+    with pytest.raises(ValueError):
+        fb().attention_partial(q, k, v, tile_size=0)
+    with pytest.raises(fb().DegenerateInputError):
+        fb().attention_dense(q, k[:0], v[:0])
+
+
+def test_dense_matches_oracle(rng):
+    q, k, v = rng.standard_normal((5, 16)), rng.standard_normal((77, 16)), rng.standard_normal((77, 16))
+    np.testing.assert_allclose(fb().attention_dense(q, k, v), orc.dense(q, k, v), atol=1e-12)
+    np.testing.assert_allclose(fb().attention_dense(q, k, v, scale=0.1), orc.dense(q, k, v, 0.1),
+                               atol=1e-12)
+
+
+# ----------------------------------------------------------------- bf16 tensor-core path
+
+
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("n", [1, 37, 128, 129, 300, 1000, 4096])
+def test_bf16_refresh_kernel_vs_oracle(rng, d, n):
+    from paper_2602_05305_b200 import kernels as K
+
+    groups, q_rows = 3, 128
+    q = bf16_exact(rng, (groups, q_rows, d))
+    k = bf16_exact(rng, (groups, n + 5, d))
+    v = bf16_exact(rng, (groups, n + 5, d))
+    o, l = K.attention_partial(q.cuda(), k.cuda(), v.cuda(), 2, n + 2)
+    o, l = o.cpu().numpy(), l.cpu().numpy()
+    for g in range(groups):
+        ref = orc.partial(q[g].float().numpy().astype(np.float64),
+                          k[g, 2:n + 2].float().numpy().astype(np.float64),
+                          v[g, 2:n + 2].float().numpy().astype(np.float64))
+        err = rel_err(o[g], ref.out)
+        assert err <= 1e-2, f"g={g} rel err {err:.3e}"
+        assert np.max(np.abs(l[g] - ref.lognorm)) <= 1e-3
+
+
+@pytest.mark.parametrize("q_rows", [32, 96, 200])
+def test_bf16_refresh_ragged_rows(rng, q_rows):
+    from paper_2602_05305_b200 import kernels as K
+
+    d, n = 128, 700
+    q = bf16_exact(rng, (2, q_rows, d))
+    k = bf16_exact(rng, (2, n, d))
+    v = bf16_exact(rng, (2, n, d))
+    o, l = K.attention_partial(q.cuda(), k.cuda(), v.cuda())
+    for g in range(2):
+        ref = orc.partial(q[g].double().numpy(), k[g].double().numpy(), v[g].double().numpy())
+        assert rel_err(o[g].cpu().numpy(), ref.out) <= 1e-2
+        assert np.max(np.abs(l[g].cpu().numpy() - ref.lognorm)) <= 1e-3
+
+
+def test_bf16_large_scores_stay_stable(rng):
+    # score std ~ 6 (sigma 2.5 on q and k): exercises the lazy O rescale
+    from paper_2602_05305_b200 import kernels as K
+
+    d, n = 128, 2048
+    q = bf16_exact(rng, (2, 128, d), 2.5)
+    k = bf16_exact(rng, (2, n, d), 2.5)
+    v = bf16_exact(rng, (2, n, d))
+    o, l = K.attention_partial(q.cuda(), k.cuda(), v.cuda())
+    for g in range(2):
+        ref = orc.partial(q[g].double().numpy(), k[g].double().numpy(), v[g].double().numpy())
+        assert rel_err(o[g].cpu().numpy(), ref.out) <= 1e-2
+        assert np.max(np.abs(l[g].cpu().numpy() - ref.lognorm)) <= 1e-3
+
+
+def test_bf16_refresh_c2_shape_split_invariance():
+    """C2 shape (8 groups x 128 rows, d=128, N=32768): the split-KV tcgen05
+    result equals the F32 SIMT kernel (an independent implementation) on the
+    same bf16-exact inputs, and K1 over [0,N) equals combine(K1 [0,a), K1 [a,N))."""
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    groups, rows, d, n = 8, 128, 128, 32768
+    q = torch.randn((groups, rows, d), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((groups, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((groups, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    o, l = K.attention_partial(q, k, v)
+    o32, l32 = K.attention_partial(q.float(), k.float(), v.float())
+    err = (o - o32).abs().max().item() / o32.abs().max().item()
+    assert err <= 1e-2, err
+    assert (l.double() - l32).abs().max().item() <= 1e-3
+    a = 12345
+    pa = K.attention_partial(q, k, v, 0, a)
+    pb = K.attention_partial(q, k, v, a, n)
+    oc, lc = K.combine([pa, pb])
+    assert (oc - o).abs().max().item() / o.abs().max().item() <= 2e-3
+    assert (lc - l).abs().max().item() <= 1e-4
+
+
+# ----------------------------------------------------------------- engine (GQA, batched)
+
+
+def test_engine_refresh_then_cached_matches_oracle(rng):
+    from paper_2602_05305_b200 import FlashBlockAttention
+
+    b, hq, hkv, B, d, n = 2, 8, 2, 32, 128, 1000
+    eng = FlashBlockAttention(1, b, hq, hkv, B, d, out_dtype=torch.float32)
+    q = bf16_exact(rng, (b, hq, B, d)).cuda()
+    kc = bf16_exact(rng, (b, hkv, n + 24, d)).cuda()
+    vc = bf16_exact(rng, (b, hkv, n + 24, d)).cuda()
+    ki = bf16_exact(rng, (b, hkv, B, d)).cuda()
+    vi = bf16_exact(rng, (b, hkv, B, d)).cuda()
+    out = eng.refresh(0, q, kc, vc, n, ki, vi)
+    q2 = (q.float() + 0.1 * torch.randn_like(q.float())).to(torch.bfloat16)
+    out2 = eng.cached(0, q2, ki, vi)
+    G = hq // hkv
+    for bi in range(b):
+        for h in range(hkv):
+            qs = q[bi, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            q2s = q2[bi, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            kk = np.concatenate([kc[bi, h, :n].double().cpu().numpy(), ki[bi, h].double().cpu().numpy()])
+            vv = np.concatenate([vc[bi, h, :n].double().cpu().numpy(), vi[bi, h].double().cpu().numpy()])
+            ref = orc.dense(qs, kk, vv)
+            got = out[bi, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            assert rel_err(got, ref) <= 1e-2
+            ext = orc.partial(qs, kk[:n], vv[:n])
+            ref2, _ = orc.with_reuse(q2s, ext, True, kk[n:], vv[n:])
+            got2 = out2[bi, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            assert rel_err(got2, ref2) <= 1e-2
+
+
+# ----------------------------------------------------------------- sparse
+
+
+@pytest.mark.parametrize("name", ["m0", "m1", "m2", "m3"])
+def test_sparse_mask_and_outputs_match_golden(golden, golden_meta, name):
+    m = golden_meta[name]
+    q, k, v = golden[f"{name}_q"], golden[f"{name}_k"], golden[f"{name}_v"]
+    for di, dn in enumerate(m["densities"]):
+        mask = fb().build_sparse_mask(q, k, m["n_ext"], dn, m["kbs"], block_id=3)
+        np.testing.assert_array_equal(mask.selected, golden[f"{name}_d{di}_sel"])  # exact
+        o1, res = fb().sparse_attention_with_residual(q, mask, k, v, None)
+        assert rel_err(o1, golden[f"{name}_d{di}_out1"]) <= 1e-4
+        if np.isfinite(golden[f"{name}_d{di}_res_lse"]).all():
+            assert rel_err(res.out, golden[f"{name}_d{di}_res_out"]) <= 1e-4
+        o2, _ = fb().sparse_attention_with_residual(
+            golden[f"{name}_d{di}_q2"], mask, k, v, fb().CacheEntry(res, 0, block_id=3))
+        assert rel_err(o2, golden[f"{name}_d{di}_out2"]) <= 1e-4
+
+
+def test_sparse_ties_budget_tail_and_staleness(rng):
+    q = np.ones((2, 4))
+    keys = np.ones((40, 4))
+    assert list(fb().build_sparse_mask(q, keys, 32, 0.5, 16).selected) == [0]
+    assert list(fb().build_sparse_mask(q, keys, 32, 1.0, 16).selected) == [0, 1]
+    q2 = rng.standard_normal((4, 8))
+    k2 = rng.standard_normal((168, 8))
+    for density, blocks in ((0.001, 1), (0.1, 1), (0.2, 2), (0.5, 5), (1.0, 10)):
+        assert fb().build_sparse_mask(q2, k2, 160, density, 16).selected.size == blocks
+    tail = fb().build_sparse_mask(q2, k2[:28], 20, 1.0, 16)
+    assert list(tail.selected) == [0, 1] and tail.realized_density == 1.0
+    assert fb().build_sparse_mask(q2, k2[:8], 0, 0.5, 16).selected.size == 0
+    mask = fb().build_sparse_mask(q2, k2[:72], 64, 0.25, 16, block_id=1)
+    _, res = fb().sparse_attention_with_residual(q2, mask, k2[:72], k2[:72])
+    with pytest.raises(fb().StalenessError):
+        fb().sparse_attention_with_residual(q2, mask, k2[:72], k2[:72], fb().CacheEntry(res, 0, 2))
+    with pytest.raises(fb().StalenessError):
+        fb().sparse_attention_with_residual(q2, mask, k2[:72], k2[:72],
+                                            fb().CacheEntry(res, 0, 1, valid=False))
+    with pytest.raises(fb().ShapeError):
+        fb().sparse_attention_with_residual(q2, mask, k2[:32], k2[:32])
+    for bad in (0.0, -0.2, 1.5):
+        with pytest.raises(ValueError):
+            fb().build_sparse_mask(q2, k2, 32, bad)
+
+
+def test_sparse_full_density_equals_dense_and_partition_exact(rng):
+    q, keys, values = rng.standard_normal((4, 8)), rng.standard_normal((72, 8)), rng.standard_normal((72, 8))
+    mask = fb().build_sparse_mask(q, keys, 64, 1.0, 16)
+    out, residual = fb().sparse_attention_with_residual(q, mask, keys, values)
+    np.testing.assert_allclose(out, orc.dense(q, keys, values), atol=1e-9)
+    assert residual.empty_rows().all()
+    for density in (0.1, 0.3, 0.7):
+        mask = fb().build_sparse_mask(q, keys, 64, density, 16)
+        out, residual = fb().sparse_attention_with_residual(q, mask, keys, values)
+        np.testing.assert_allclose(out, orc.dense(q, keys, values), atol=1e-10)
+        assert not residual.empty_rows().any()
