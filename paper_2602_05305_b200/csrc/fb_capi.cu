@@ -157,6 +157,17 @@ static int internal_merge_t(const void* qv, const void* kv, const void* vv, int6
                             void* lse_merged, void* o_int, void* lse_int, int32_t* empty,
                             cudaStream_t st) {
   using Tin = typename Mode::Tin;
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    if (sm100_k2_supported(d, n_in) && o_ext != nullptr && lse_ext != nullptr && a16(qv) &&
+        a16(kv) && a16(vv) && a16(o_ext) && a16(out) && a16(o_int) && groups * ((q_rows + 127) / 128) < (1LL << 31))
+      return launch_internal_merge_sm100(
+          reinterpret_cast<const __nv_bfloat16*>(qv), reinterpret_cast<const __nv_bfloat16*>(kv),
+          reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, n_in, scale,
+          reinterpret_cast<const float*>(o_ext), reinterpret_cast<const float*>(lse_ext), out,
+          out_bf16, reinterpret_cast<float*>(lse_merged), reinterpret_cast<float*>(o_int),
+          reinterpret_cast<float*>(lse_int), empty, st);
+  }
   MergeOut<Mode> mo{};
   mo.o_ext = reinterpret_cast<const typename Mode::To*>(o_ext);
   mo.lse_ext = reinterpret_cast<const typename Mode::Tl*>(lse_ext);

@@ -62,4 +62,11 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
                          int64_t key_begin, int64_t key_end, int64_t keys_per_split, int splits,
                          double scale, float* po, float* pl, cudaStream_t st);
 
+bool sm100_k2_supported(int64_t head_dim, int64_t n_in);
+int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,
+                                const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
+                                int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
+                                const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
+                                float* o_int, float* lse_int, int32_t* empty, cudaStream_t st);
+
 }  // namespace fb

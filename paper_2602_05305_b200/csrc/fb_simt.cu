@@ -26,24 +26,49 @@ constexpr size_t simt_smem_bytes() {
   return sizeof(Ts) * (SIMT_ROWS * D + SIMT_KT * (D + 1)) + sizeof(Ta) * SIMT_KT * D;
 }
 
+// Products that must round before they are summed (no FMA contraction), so a
+// two-way merge is bitwise symmetric like the reference's wa*A + wb*B.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// Element type -> 16-byte chunk unpacking into the score / accumulate types.
+template <typename Tin>
+struct Chunk {
+  static constexpr int E = 16 / sizeof(Tin);
+  template <typename To>
+  static __device__ __forceinline__ void unpack(const uint4& u, To* dst) {
+    const Tin* e = reinterpret_cast<const Tin*>(&u);
+#pragma unroll
+    for (int i = 0; i < E; ++i) dst[i] = cvt<To>(e[i]);
+  }
+};
+
 // grid: (ceil(q_rows/SIMT_ROWS), splits, groups); block: 32*SIMT_WARPS.
 // Split s of group g covers key ordinals [s*per_split, min((s+1)*per_split, count)).
 // Without MERGE the normalised partial goes to (po, pl) at slot
 // [s][g*q_rows + row]; with MERGE (splits == 1) it is merged with the cache.
+// `vec`: every row pointer is 16-byte aligned and head_dim*sizeof(Tin) % 16 == 0,
+// so tiles move as 16-byte chunks with all loads of a batch issued up front.
 template <typename Mode, int D, bool MERGE, bool NO_V, typename Map>
 __global__ void __launch_bounds__(32 * SIMT_WARPS)
 partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, int64_t head_dim,
              int64_t per_split, typename Mode::Ta scale, typename Mode::Ta* po,
-             typename Mode::Tl* pl, int64_t rows_total, MergeOut<Mode> mo) {
+             typename Mode::Tl* pl, int64_t rows_total, MergeOut<Mode> mo, bool vec) {
   using Tin = typename Mode::Tin;
   using Ts = typename Mode::Ts;
   using Ta = typename Mode::Ta;
+  using To = typename Mode::To;
+  using Tl = typename Mode::Tl;
   constexpr int C = D / 32;  // output columns per lane
+  constexpr int E = Chunk<Tin>::E;
+  constexpr int NT = 32 * SIMT_WARPS;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Ts* qs = reinterpret_cast<Ts*>(smem_raw);           // [SIMT_ROWS][D]
-  Ts* ks = qs + SIMT_ROWS * D;                         // [KT][D+1]
-  Ta* vs = reinterpret_cast<Ta*>(ks + SIMT_KT * (D + 1));  // [KT][D]
+  Ts* qs = reinterpret_cast<Ts*>(smem_raw);                // [SIMT_ROWS][D]
+  Ts* ks = qs + SIMT_ROWS * D;                              // [KT][D+1]
+  Ta* vs = reinterpret_cast<Ta*>(ks + SIMT_KT * (D + 1));   // [KT][D]
+  __shared__ const Tin* kptr[SIMT_KT];
+  __shared__ const Tin* vptr[SIMT_KT];
 
   const int64_t g = blockIdx.z;
   const int split = blockIdx.y;
@@ -54,13 +79,46 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
   const int64_t kb = min((int64_t)split * per_split, n_keys);
   const int64_t ke = min(kb + per_split, n_keys);
 
+  // merge operands first: their latency overlaps the tile loads
+  Ta oe[SIMT_ROWS_PER_WARP][C];
+  Ta le[SIMT_ROWS_PER_WARP];
+  if constexpr (MERGE) {
+#pragma unroll
+    for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) {
+      const int64_t gr = row0 + warp * SIMT_ROWS_PER_WARP + i;
+      const int64_t rr = g * q_rows + gr;
+      const bool ok = gr < q_rows && mo.lse_ext != nullptr;
+      le[i] = ok ? (Ta)mo.lse_ext[rr] : Num<Ta>::ninf();
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int col = lane + 32 * c;
+        oe[i][c] = (ok && col < head_dim) ? (Ta)mo.o_ext[rr * head_dim + col] : (Ta)0;
+      }
+    }
+  }
+
   // stage the CTA's query rows (zero-padded to D)
-  for (int i = threadIdx.x; i < SIMT_ROWS * D; i += blockDim.x) {
-    const int r = i / D, c = i % D;
-    const int64_t gr = row0 + r;
-    Ts val = 0;
-    if (gr < q_rows && c < head_dim) val = cvt<Ts>(q[(g * q_rows + gr) * head_dim + c]);
-    qs[i] = val;
+  const int cpr = (int)(head_dim / E);  // 16-byte chunks per row (vec path)
+  if (vec) {
+    for (int ci = threadIdx.x; ci < SIMT_ROWS * cpr; ci += NT) {
+      const int r = ci / cpr, cc = ci % cpr;
+      const int64_t gr = row0 + r;
+      uint4 u = make_uint4(0, 0, 0, 0);
+      if (gr < q_rows) u = *reinterpret_cast<const uint4*>(q + (g * q_rows + gr) * head_dim + cc * E);
+      Chunk<Tin>::unpack(u, qs + r * D + cc * E);
+    }
+    for (int i = threadIdx.x; i < SIMT_ROWS * (D - (int)head_dim); i += NT) {
+      const int r = i / (D - (int)head_dim), c = (int)head_dim + i % (D - (int)head_dim);
+      qs[r * D + c] = 0;
+    }
+  } else {
+    for (int i = threadIdx.x; i < SIMT_ROWS * D; i += NT) {
+      const int r = i / D, c = i % D;
+      const int64_t gr = row0 + r;
+      Ts val = 0;
+      if (gr < q_rows && c < head_dim) val = cvt<Ts>(q[(g * q_rows + gr) * head_dim + c]);
+      qs[i] = val;
+    }
   }
 
   Ta m[SIMT_ROWS_PER_WARP], l[SIMT_ROWS_PER_WARP], acc[SIMT_ROWS_PER_WARP][C];
@@ -73,22 +131,61 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
   }
 
   for (int64_t t0 = kb; t0 < ke; t0 += SIMT_KT) {
-    __syncthreads();
-    // cooperative tile load: warp w loads rows w, w+4, ...
-    for (int j = warp; j < SIMT_KT; j += SIMT_WARPS) {
-      const int64_t t = t0 + j;
+    __syncthreads();  // previous tile fully consumed
+    if (threadIdx.x < SIMT_KT) {
+      const int64_t t = t0 + threadIdx.x;
       const Tin* kr = nullptr;
       const Tin* vr = nullptr;
       if (t < ke) map.row(g, t, kr, vr);
-      for (int c = lane; c < D; c += 32) {
-        Ts kv = 0;
-        Ta vv = 0;
-        if (kr != nullptr && c < head_dim) {
-          kv = cvt<Ts>(kr[c]);
-          if constexpr (!NO_V) vv = cvt<Ta>(vr[c]);
+      kptr[threadIdx.x] = kr;
+      vptr[threadIdx.x] = vr;
+    }
+    __syncthreads();
+    if (vec) {
+      constexpr int NB = 4;  // chunks per thread per batch (per K and V)
+      for (int base = 0; base < SIMT_KT * cpr; base += NB * NT) {
+        uint4 ku[NB], vu[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int ci = base + b * NT + threadIdx.x;
+          ku[b] = vu[b] = make_uint4(0, 0, 0, 0);
+          if (ci < SIMT_KT * cpr) {
+            const int j = ci / cpr, cc = ci % cpr;
+            if (kptr[j] != nullptr) {
+              ku[b] = *reinterpret_cast<const uint4*>(kptr[j] + cc * E);
+              if constexpr (!NO_V) vu[b] = *reinterpret_cast<const uint4*>(vptr[j] + cc * E);
+            }
+          }
         }
-        ks[j * (D + 1) + c] = kv;
-        if constexpr (!NO_V) vs[j * D + c] = vv;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int ci = base + b * NT + threadIdx.x;
+          if (ci < SIMT_KT * cpr) {
+            const int j = ci / cpr, cc = ci % cpr;
+            Chunk<Tin>::unpack(ku[b], ks + j * (D + 1) + cc * E);
+            if constexpr (!NO_V) Chunk<Tin>::unpack(vu[b], vs + j * D + cc * E);
+          }
+        }
+      }
+      for (int i = threadIdx.x; i < SIMT_KT * (D - (int)head_dim); i += NT) {
+        const int j = i / (D - (int)head_dim), c = (int)head_dim + i % (D - (int)head_dim);
+        ks[j * (D + 1) + c] = 0;
+        if constexpr (!NO_V) vs[j * D + c] = 0;
+      }
+    } else {
+      for (int j = warp; j < SIMT_KT; j += SIMT_WARPS) {
+        const Tin* kr = kptr[j];
+        const Tin* vr = vptr[j];
+        for (int c = lane; c < D; c += 32) {
+          Ts kv = 0;
+          Ta vv = 0;
+          if (kr != nullptr && c < head_dim) {
+            kv = cvt<Ts>(kr[c]);
+            if constexpr (!NO_V) vv = cvt<Ta>(vr[c]);
+          }
+          ks[j * (D + 1) + c] = kv;
+          if constexpr (!NO_V) vs[j * D + c] = vv;
+        }
       }
     }
     __syncthreads();
@@ -116,6 +213,7 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
       if constexpr (!NO_V) {
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[i][c] *= alpha;
+#pragma unroll 8
         for (int j = 0; j < SIMT_KT; ++j) {
           const Ta pj = __shfl_sync(0xffffffffu, p, j);
           const Ta* vrow = vs + j * D + lane;
@@ -145,17 +243,14 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
           if (col < head_dim) dst[col] = acc[i][c] * inv;
         }
       }
-      if (lane == 0) pl[(int64_t)split * rows_total + rr] = (typename Mode::Tl)lse;
+      if (lane == 0) pl[(int64_t)split * rows_total + rr] = (Tl)lse;
     } else {
-      using To = typename Mode::To;
-      using Tl = typename Mode::Tl;
       // internal partial rounded to its stored type first, as the reference
       // merges the partial it returns (attention.py:180, :320-321)
-      const Ta le = mo.lse_ext ? (Ta)mo.lse_ext[rr] : Num<Ta>::ninf();
       const Ta li = (Ta)(Tl)lse;
-      const Ta mx = fmax(le, li);
+      const Ta mx = fmax(le[i], li);
       const bool live = mx != Num<Ta>::ninf();
-      const Ta we = live ? Num<Ta>::exp_(le - mx) : (Ta)0;
+      const Ta we = live ? Num<Ta>::exp_(le[i] - mx) : (Ta)0;
       const Ta wi = live ? Num<Ta>::exp_(li - mx) : (Ta)0;
       const Ta z = we + wi;
 #pragma unroll
@@ -165,10 +260,7 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
         const To oi = (To)(acc[i][c] * inv);
         if (mo.o_int) mo.o_int[rr * head_dim + col] = oi;
         Ta val = 0;
-        if (live) {
-          const Ta oe = mo.o_ext ? (Ta)mo.o_ext[rr * head_dim + col] : (Ta)0;
-          val = (we * oe + wi * (Ta)oi) / z;
-        }
+        if (live) val = (mul_rn(we, oe[i][c]) + mul_rn(wi, (Ta)oi)) / z;
         if (mo.out_bf16)
           reinterpret_cast<__nv_bfloat16*>(mo.out)[rr * head_dim + col] = cvt<__nv_bfloat16>(val);
         else
@@ -211,7 +303,7 @@ __global__ void combine_parts(CombineList list, int64_t rows, int64_t head_dim, 
     if (live) {
       for (int p = 0; p < list.n; ++p) {
         const Ta w = Num<Ta>::exp_((Ta)lptr(p)[row] - mx);
-        num += w * (Ta)optr(p)[row * head_dim + c];
+        num += mul_rn(w, (Ta)optr(p)[row * head_dim + c]);
       }
       num = num / z;
     }
@@ -232,6 +324,29 @@ __global__ void fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim) {
 
 // ------------------------------------------------------------------ launchers
 
+static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+template <typename T>
+static bool rows_ok(const T* q, int64_t d) {
+  return al16(q) && (d * (int64_t)sizeof(T)) % 16 == 0;
+}
+template <typename T>
+static bool map_vec_ok(const RangeMap<T>& m, const T* q, int64_t d) {
+  return rows_ok(q, d) && al16(m.k) && al16(m.v);
+}
+template <typename T>
+static bool map_vec_ok(const ConcatMap<T>& m, const T* q, int64_t d) {
+  return rows_ok(q, d) && al16(m.k) && al16(m.k_in) && (m.v == nullptr || al16(m.v)) &&
+         (m.v_in == nullptr || al16(m.v_in));
+}
+template <typename T>
+static bool map_vec_ok(const SelectedMap<T>& m, const T* q, int64_t d) {
+  return rows_ok(q, d) && al16(m.k) && al16(m.v) && al16(m.k_in) && al16(m.v_in);
+}
+template <typename T>
+static bool map_vec_ok(const ResidualMap<T>& m, const T* q, int64_t d) {
+  return rows_ok(q, d) && al16(m.k) && al16(m.v);
+}
+
 template <typename Mode, int D, bool MERGE, bool NO_V, typename Map>
 static int launch_partial_d(const typename Mode::Tin* q, const Map& map, int64_t groups,
                             int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
@@ -245,8 +360,10 @@ static int launch_partial_d(const typename Mode::Tin* q, const Map& map, int64_t
     attr_set = true;
   }
   dim3 grid((unsigned)((q_rows + SIMT_ROWS - 1) / SIMT_ROWS), (unsigned)splits, (unsigned)groups);
+  const bool vec = map_vec_ok(map, q, head_dim);
   kern<<<grid, 32 * SIMT_WARPS, smem, st>>>(q, map, q_rows, head_dim, per_split,
-                                            (typename Mode::Ta)scale, po, pl, groups * q_rows, mo);
+                                            (typename Mode::Ta)scale, po, pl, groups * q_rows, mo,
+                                            vec);
   count_launch();
   return check_launch("partial_simt");
 }

@@ -296,24 +296,29 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 3-D bf16 view [dim2][dim1][D] with a 128-row x 64-col 128B-swizzled box.
-// Rows >= dim1 read as zero (TMA out-of-bounds fill), so slab tails are safe.
-static int make_map(CUtensorMap* map, const void* base, int64_t D, int64_t dim1,
-                    int64_t dim1_stride_rows, int64_t dim2) {
-  auto enc = get_encode();
+}  // namespace sm100
+
+// 3-D view [dim2][dim1][inner] (element size 2 or 4 bytes) with a
+// box_rows x box_inner 128B-swizzled box.  Rows >= dim1 read as zero (TMA
+// out-of-bounds fill), so slab tails never leak uninitialised memory.
+int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t inner, int64_t dim1,
+                 int64_t dim1_stride_elems, int64_t dim2, int box_inner, int box_rows) {
+  auto enc = sm100::get_encode();
   if (!enc) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)dim1, (cuuint64_t)dim2};
-  cuuint64_t strides[2] = {(cuuint64_t)(D * 2), (cuuint64_t)(dim1_stride_rows * D * 2)};
-  cuuint32_t box[3] = {(cuuint32_t)BOX_COLS, (cuuint32_t)BM, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)dim1, (cuuint64_t)dim2};
+  cuuint64_t strides[2] = {(cuuint64_t)(inner * dtype_bytes),
+                           (cuuint64_t)(dim1_stride_elems * inner * dtype_bytes)};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUtensorMapDataType dt =
+      dtype_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUresult r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (r != CUDA_SUCCESS)
+    return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return FB_OK;
 }
-
-}  // namespace sm100
 
 bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 128; }
 
@@ -325,9 +330,9 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv;
   int rc;
-  if ((rc = sm100::make_map(&mq, q, D, q_rows, q_rows, groups)) != FB_OK) return rc;
-  if ((rc = sm100::make_map(&mk, k, D, key_end, kv_rows_cap, groups)) != FB_OK) return rc;
-  if ((rc = sm100::make_map(&mv, v, D, key_end, kv_rows_cap, groups)) != FB_OK) return rc;
+  if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100::BOX_COLS, sm100::BM))) return rc;
+  if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+  if ((rc = make_tmap_3d(&mv, v, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
   auto kern = sm100::refresh_kernel<D>;
   static bool attr = false;
   if (!attr) {

@@ -1,0 +1,311 @@
+// K2 -- cached step on sm_100a: block-internal attention fused with the
+// log-space merge against the cached external partial.
+//
+// Reference: attention_with_reuse (attention.py:295-321) = attention_partial
+// over the current block's keys (:320) + merge_partials with the cached
+// external partial (:321, :207-245).  The KV cache is not an argument.
+//
+// One CTA per (group, 128-row query tile), 192 threads:
+//   warps 0..3  softmax + merge epilogue, thread = query row = TMEM lane;
+//   warp 4      TMA (Q, K_in, V_in, and the fp32 O_ext tile, all 128B
+//               swizzled) and the tcgen05.mma issue (one thread).
+// S = Q K_in^T (N = NT <= 128 keys) lands in TMEM; P (bf16) overwrites S;
+// O = P V_in (TS MMA) lands in TMEM; the epilogue normalises O, merges it
+// with O_ext / LSE_ext in fp32 and writes bf16 (or fp32) output.  Two CTAs
+// fit per SM (TMEM NT+D <= 256 columns, ~115 KB smem).
+#include "fb_kernels.cuh"
+#include "fb_sm100_ptx.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace fb {
+namespace sm100k2 {
+
+constexpr int BM = 128;
+constexpr int THREADS = 192;
+constexpr int BOX = 64;  // bf16 columns per 128-byte swizzle span
+
+template <int D, int NT>
+struct Cfg {
+  static constexpr int NB = D / BOX;                    // 64-col boxes per bf16 row
+  static constexpr uint32_t QBOX = BM * 128;            // 16 KB
+  static constexpr uint32_t KBOX = NT * 128;            // NT rows x 128 B
+  static constexpr uint32_t OBOX = BM * 128;            // fp32: 32 cols x 128 rows
+  static constexpr int NOB = D / 32;                    // fp32 boxes of O_ext
+  static constexpr uint32_t OFF_Q = 0;
+  static constexpr uint32_t OFF_K = OFF_Q + NB * QBOX;
+  static constexpr uint32_t OFF_V = OFF_K + NB * KBOX;
+  static constexpr uint32_t OFF_O = OFF_V + NB * KBOX;
+  static constexpr uint32_t OFF_BAR = OFF_O + NOB * OBOX;
+  static constexpr uint32_t SMEM = OFF_BAR + 128 + 1024;
+  static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;  // P stores span >= 32 cols
+  static constexpr uint32_t TMEM_COLS = (COL_O + D) <= 128 ? 128 : (COL_O + D) <= 256 ? 256 : 512;
+  static constexpr uint32_t TX_QKV = NB * (QBOX + 2 * KBOX);
+};
+
+struct Bars {
+  uint64_t load_qkv, load_o, s_full, p_ready, o_full;
+  uint32_t tmem_base;
+};
+
+template <int D, int NT>
+__global__ void __launch_bounds__(THREADS, 2)
+internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                      const float* __restrict__ lse_ext, int q_rows, int m_tiles, int n_in,
+                      float scale_log2, void* __restrict__ out, int out_bf16,
+                      float* __restrict__ lse_merged, float* __restrict__ o_int,
+                      float* __restrict__ lse_int, int* __restrict__ empty_rows) {
+  using C = Cfg<D, NT>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bar = reinterpret_cast<Bars*>(smem + C::OFF_BAR);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x / m_tiles;
+  const int mt = blockIdx.x % m_tiles;
+
+  if (threadIdx.x == 128) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+    ptx::tma_prefetch_desc(&tm_o);
+    ptx::mbar_init(&bar->load_qkv, 1);
+    ptx::mbar_init(&bar->load_o, 1);
+    ptx::mbar_init(&bar->s_full, 1);
+    ptx::mbar_init(&bar->p_ready, 128);
+    ptx::mbar_init(&bar->o_full, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(&bar->tmem_base, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bar->tmem_base;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      ptx::mbar_expect_tx(&bar->load_qkv, C::TX_QKV);
+      for (int b = 0; b < C::NB; ++b) {
+        ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
+        ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
+        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, b * BOX, 0, g, pol);
+      }
+      ptx::mbar_expect_tx(&bar->load_o, C::NOB * C::OBOX);
+      for (int b = 0; b < C::NOB; ++b)
+        ptx::tma_load_3d(smem + C::OFF_O + b * C::OBOX, &tm_o, &bar->load_o, b * 32, mt * BM, g, pol);
+
+      constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
+      constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
+      ptx::mbar_wait(&bar->load_qkv, 0);
+      ptx::tc_fence_after();
+      const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
+      const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K);
+      const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        ptx::mma_ss(tmem + C::COL_S,
+                    ptx::sdesc_sw128(q_base + (kk / 4) * C::QBOX + (kk % 4) * 32, 16, 1024),
+                    ptx::sdesc_sw128(k_base + (kk / 4) * C::KBOX + (kk % 4) * 32, 16, 1024),
+                    IDESC_S, kk > 0);
+      }
+      ptx::tc_commit(&bar->s_full);
+      ptx::mbar_wait(&bar->p_ready, 0);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < NT / 16; ++kk) {
+        ptx::mma_ts(tmem + C::COL_O, tmem + C::COL_S + kk * 8,
+                    ptx::sdesc_sw128(v_base + kk * 2048, C::KBOX, 1024), IDESC_O, kk > 0);
+      }
+      ptx::tc_commit(&bar->o_full);
+    }
+  } else {
+    // ------------------------------------------------ softmax + merge epilogue
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const int row = warp * 32 + lane;
+    const int grow = mt * BM + row;
+    const bool live_row = grow < q_rows;
+    const long long rr = (long long)g * q_rows + grow;
+    const float le = live_row ? lse_ext[rr] : -INFINITY;  // natural log
+
+    uint32_t r[32];
+    float s[NT];
+    ptx::mbar_wait(&bar->s_full, 0);
+    ptx::tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < NT / 32 + (NT % 32 ? 1 : 0); ++c) {
+      if constexpr (NT >= 32) {
+        ptx::tmem_ld32(tmem + lane_off + C::COL_S + c * 32, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+      } else {
+        ptx::tmem_ld32(tmem + lane_off + C::COL_S, r);  // 16 valid columns, rest unused TMEM
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < NT; ++i) s[i] = __uint_as_float(r[i]);
+      }
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      if (i >= n_in) s[i] = -INFINITY;
+      mx = fmaxf(mx, s[i]);
+    }
+    const float m2 = mx * scale_log2;  // -inf when n_in == 0
+    const float neg = (n_in > 0) ? -m2 : 0.f;
+    float l = 0.f;
+#pragma unroll
+    for (int c = 0; c < (NT + 63) / 64; ++c) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = c * 64 + 2 * i;
+        float p0 = 0.f, p1 = 0.f;
+        if (j < NT) {
+          p0 = ptx::ex2(fmaf(s[j], scale_log2, neg));
+          p1 = ptx::ex2(fmaf(s[j + 1], scale_log2, neg));
+        }
+        l += p0 + p1;
+        r[i] = ptx::pack_bf16(p0, p1);
+      }
+      ptx::tmem_st32(tmem + lane_off + C::COL_S + c * 32, r);
+    }
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    ptx::mbar_arrive(&bar->p_ready);
+
+    // internal partial statistics (natural log), rounded as stored (fp32)
+    const bool has_int = n_in > 0;
+    const float li = has_int ? (m2 + log2f(l)) * 0.69314718055994530942f : -INFINITY;
+    const float inv = has_int ? 1.f / l : 0.f;
+    const float mm = fmaxf(le, li);
+    const bool live = mm != -INFINITY;
+    const float we = live ? __expf(le - mm) : 0.f;
+    const float wi = live ? __expf(li - mm) : 0.f;
+    const float z = we + wi;
+    const float iz = live ? 1.f / z : 0.f;
+
+    ptx::mbar_wait(&bar->load_o, 0);
+    ptx::mbar_wait(&bar->o_full, 0);
+    ptx::tc_fence_after();
+    const unsigned char* o_sm = smem + C::OFF_O;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
+      ptx::tmem_wait_ld();
+      // cached external row chunk c (fp32, 128B-swizzled box c): 8 x 16-byte pieces
+      float oe[32];
+      const unsigned char* brow = o_sm + c * C::OBOX + row * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v4 = *reinterpret_cast<const float4*>(brow + ((j ^ (row & 7)) * 16));
+        oe[4 * j] = v4.x; oe[4 * j + 1] = v4.y; oe[4 * j + 2] = v4.z; oe[4 * j + 3] = v4.w;
+      }
+      float val[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float oi = __uint_as_float(r[i]) * inv;
+        val[i] = live ? (__fmul_rn(we, oe[i]) + __fmul_rn(wi, oi)) * iz : 0.f;
+        r[i] = __float_as_uint(oi);
+      }
+      if (live_row) {
+        if (out_bf16) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * D + c * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]),
+                                ptx::pack_bf16(val[8 * j + 2], val[8 * j + 3]),
+                                ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]),
+                                ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
+        } else {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * D + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(val[4 * j], val[4 * j + 1], val[4 * j + 2], val[4 * j + 3]);
+        }
+        if (o_int) {
+          float4* di = reinterpret_cast<float4*>(o_int + rr * D + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            di[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+      }
+    }
+    if (live_row) {
+      if (lse_int) lse_int[rr] = li;
+      if (lse_merged) lse_merged[rr] = live ? mm + logf(z) : -INFINITY;
+      if (!live && empty_rows) atomicAdd(empty_rows, 1);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace sm100k2
+
+// host: tensor maps shared with the refresh kernel's encoder
+int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t inner, int64_t dim1,
+                 int64_t dim1_stride_elems, int64_t dim2, int box_inner, int box_rows);
+
+bool sm100_k2_supported(int64_t head_dim, int64_t n_in) {
+  return (head_dim == 128 || head_dim == 64) && n_in >= 0 && n_in <= 128;
+}
+
+template <int D, int NT>
+static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
+                     int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
+                     const float* lse_ext, void* out, bool out_bf16, float* lse_merged, float* o_int,
+                     float* lse_int, int32_t* empty, cudaStream_t st) {
+  using C = sm100k2::Cfg<D, NT>;
+  CUtensorMap mq, mk, mv, mo;
+  int rc;
+  if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
+  const int64_t nin_eff = n_in > 0 ? n_in : 1;  // zero-row maps are invalid; rows are masked
+  if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
+  if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
+  if ((rc = make_tmap_3d(&mo, o_ext, 4, D, q_rows, q_rows, groups, 32, sm100k2::BM))) return rc;
+  auto kern = sm100k2::internal_merge_kernel<D, NT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  kern<<<(unsigned)(groups * m_tiles), sm100k2::THREADS, C::SMEM, st>>>(
+      mq, mk, mv, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
+      lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty));
+  count_launch();
+  return check_launch("internal_merge_kernel(sm100)");
+}
+
+int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,
+                                const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
+                                int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
+                                const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
+                                float* o_int, float* lse_int, int32_t* empty, cudaStream_t st) {
+#define FB_K2(DD, NN)                                                                          \
+  return launch_k2<DD, NN>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext, out,  \
+                           out_bf16, lse_merged, o_int, lse_int, empty, st)
+  if (head_dim == 128) {
+    if (n_in <= 16) FB_K2(128, 16);
+    if (n_in <= 32) FB_K2(128, 32);
+    if (n_in <= 64) FB_K2(128, 64);
+    FB_K2(128, 128);
+  }
+  if (n_in <= 16) FB_K2(64, 16);
+  if (n_in <= 32) FB_K2(64, 32);
+  if (n_in <= 64) FB_K2(64, 64);
+  FB_K2(64, 128);
+#undef FB_K2
+}
+
+}  // namespace fb

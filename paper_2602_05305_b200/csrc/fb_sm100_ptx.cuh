@@ -39,12 +39,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Wait until the phase with the given parity has completed.  A pipeline
-// bug must not wedge the GPU: after ~2^31 polls (many seconds) trap, which
+// bug must not wedge the GPU: after ~2^26 polls (seconds) trap, which
 // surfaces as a launch failure instead of a hang.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++polls == 0x80000000u) __trap();
+    if (++polls == (1u << 26)) __trap();
   }
 }
 

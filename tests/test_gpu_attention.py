@@ -345,3 +345,39 @@ def test_sparse_full_density_equals_dense_and_partition_exact(rng):
         out, residual = fb().sparse_attention_with_residual(q, mask, keys, values)
         np.testing.assert_allclose(out, orc.dense(q, keys, values), atol=1e-10)
         assert not residual.empty_rows().any()
+
+
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("n_in", [0, 8, 16, 32, 50, 64, 128])
+@pytest.mark.parametrize("q_rows", [128, 96, 200])
+def test_bf16_cached_step_kernel_vs_oracle(rng, d, n_in, q_rows):
+    """K2 (tcgen05 internal partial + fused merge) against the oracle's
+    attention_with_reuse, including the internal partial it returns."""
+    from paper_2602_05305_b200 import kernels as K
+
+    groups, n_ext = 3, 300
+    q = bf16_exact(rng, (groups, q_rows, d))
+    k = bf16_exact(rng, (groups, n_ext + max(n_in, 1), d))
+    v = bf16_exact(rng, (groups, n_ext + max(n_in, 1), d))
+    qc, kc, vc = q.cuda(), k.cuda(), v.cuda()
+    o_ext, l_ext = K.attention_partial(qc, kc, vc, 0, n_ext)
+    ki = kc[:, n_ext:n_ext + n_in].contiguous()
+    vi = vc[:, n_ext:n_ext + n_in].contiguous()
+    out, lse_m, (o_int, l_int) = K.internal_merge(qc, ki, vi, o_ext, l_ext, out_dtype=torch.float32,
+                                                  want_lse=True, want_internal=True)
+    out_bf = K.internal_merge(qc, ki, vi, o_ext, l_ext, out_dtype=torch.bfloat16)
+    for g in range(groups):
+        qq = q[g].double().numpy()
+        kk, vv = k[g].double().numpy(), v[g].double().numpy()
+        ext = orc.Partial(o_ext[g].double().cpu().numpy(), l_ext[g].double().cpu().numpy())
+        ref, inner = orc.with_reuse(qq, ext, True, kk[n_ext:n_ext + n_in], vv[n_ext:n_ext + n_in])
+        assert rel_err(out[g].cpu().numpy(), ref) <= 1e-2
+        assert rel_err(out_bf[g].float().cpu().numpy(), ref) <= 1.5e-2
+        assert rel_err(o_int[g].cpu().numpy(), inner.out) <= 1e-2 if n_in else \
+            np.all(o_int[g].cpu().numpy() == 0)
+        if n_in:
+            assert np.max(np.abs(l_int[g].cpu().numpy() - inner.lognorm)) <= 1e-3
+            full = orc.combine(ext, inner)
+            assert np.max(np.abs(lse_m[g].cpu().numpy() - full.lognorm)) <= 1e-3
+        else:
+            assert np.isneginf(l_int[g].cpu().numpy()).all()
