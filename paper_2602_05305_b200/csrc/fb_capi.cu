@@ -48,20 +48,6 @@ static SplitPlan plan_simt(int64_t groups, int64_t q_rows, int64_t n, size_t ws_
   return {splits, per};
 }
 
-// tcgen05: one 128-key tile granularity, one CTA per SM (TMEM + smem bound).
-static SplitPlan plan_sm100(int64_t groups, int64_t q_rows, int64_t n, size_t ws_bytes,
-                            size_t bytes_per_split) {
-  const int64_t items = groups * ((q_rows + 127) / 128);
-  const int64_t tiles = (n + 127) / 128;
-  int64_t want = std::max<int64_t>(1, (int64_t)num_sms() / std::max<int64_t>(items, 1));
-  want = std::min<int64_t>(want, tiles);
-  if (bytes_per_split > 0 && want > 1)
-    want = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(ws_bytes / bytes_per_split)));
-  const int64_t tiles_per = (tiles + want - 1) / want;
-  const int splits = (int)((tiles + tiles_per - 1) / tiles_per);
-  return {splits, tiles_per * 128};
-}
-
 template <typename Mode>
 static size_t split_bytes(int64_t rows, int64_t d) {
   return (size_t)rows * (size_t)(d + 1) * sizeof(typename Mode::Ta) + 256;
@@ -132,18 +118,7 @@ static int attention_partial_t(const void* qv, const void* kv, const void* vv, i
     if (sm100_supported(d) && ke < (int64_t(1) << 31) && q_rows < (int64_t(1) << 31) &&
         (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
         (reinterpret_cast<uintptr_t>(v) % 16 == 0) && groups < 65536) {
-      const size_t per = (size_t)rows * (size_t)(d + 1) * sizeof(float) + 256;
-      SplitPlan p = plan_sm100(groups, q_rows, n, ws ? ws_bytes : 0, per);
-      if (p.splits == 1)
-        return launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, p.per_split, 1, scale,
-                                    o, l, st);
-      float* wo = reinterpret_cast<float*>(ws);
-      float* wl = wo + (size_t)p.splits * rows * d;
-      int rc = launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, p.per_split, p.splits,
-                                    scale, wo, wl, st);
-      if (rc) return rc;
-      return launch_combine<float, float, float, float, float>(
-          strided_list<ModeBF16>(ws, p.splits, rows, d), rows, d, o, l, nullptr, st);
+      return launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, scale, o, l, ws, ws_bytes, st);
     }
   }
   RangeMap<Tin> map{k, v, cap * d, kb, ke, d};
@@ -328,9 +303,9 @@ size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int
   const int64_t rows = groups * q_rows;
   if (dtype == FB_BF16 && sm100_supported(head_dim)) {
     const size_t per = (size_t)rows * (size_t)(head_dim + 1) * sizeof(float) + 256;
-    SplitPlan p = plan_sm100(groups, q_rows, n_keys, SIZE_MAX, per);
     SplitPlan s = plan_simt(groups, q_rows, n_keys, SIZE_MAX, per);
-    return per * (size_t)std::max(p.splits, s.splits);
+    return std::max(refresh_sm100_workspace_bytes(groups, q_rows, head_dim, n_keys),
+                    per * (size_t)s.splits);
   }
   const size_t elem = dtype == FB_BF16 ? 4 : 8;
   const size_t per = (size_t)rows * (size_t)(head_dim + 1) * elem + 256;

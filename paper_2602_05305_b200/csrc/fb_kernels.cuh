@@ -52,15 +52,17 @@ int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, 
 template <typename To, typename Tl>
 int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStream_t st);
 
-// tcgen05 / TMA refresh kernel (bf16, head_dim 64 or 128).  Writes split
-// partials (fp32 out + fp32 natural-log lse) to (po, pl) slot
-// [split][g*q_rows + row]; returns FB_ERR_UNSUPPORTED if the shape is not
-// covered so the caller can route to the SIMT kernel.
+// tcgen05 / TMA refresh kernel (bf16, head_dim 64 or 128): normalised fp32
+// partial + fp32 natural-log lse over keys [key_begin, key_end) of every
+// group, written to (o_out, lse_out).  Stream-K over all SMs; split partials
+// are merged in-kernel by the last CTA of each item (needs the workspace of
+// refresh_sm100_workspace_bytes; with less it runs one CTA per item).
 bool sm100_supported(int64_t head_dim);
+size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
-                         int64_t key_begin, int64_t key_end, int64_t keys_per_split, int splits,
-                         double scale, float* po, float* pl, cudaStream_t st);
+                         int64_t key_begin, int64_t key_end, double scale, float* o_out,
+                         float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st);
 
 bool sm100_k2_supported(int64_t head_dim, int64_t n_in);
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 
 namespace fb {
@@ -48,25 +49,45 @@ struct Cfg {
   static constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
   static constexpr uint32_t OFF_V = OFF_K + STAGES * TILE_BYTES;
   static constexpr uint32_t OFF_BAR = OFF_V + STAGES * TILE_BYTES;
-  static constexpr uint32_t BAR_BYTES = 256;
+  static constexpr uint32_t BAR_BYTES = 512;
   static constexpr uint32_t SMEM = OFF_BAR + BAR_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O = 256;
 };
 
 struct Barriers {
-  uint64_t q_full;
+  uint64_t q_full, q_empty;
   uint64_t k_full[6], k_empty[6], v_full[6], v_empty[6];
   uint64_t s_full[2], p_ready[2];
-  uint64_t pv_done, o_full;
+  uint64_t pv_done, o_full, o_empty;
   uint32_t tmem_base;
+  int last_flag;
 };
+
+// Stream-K schedule: the flattened (item, key tile) space of T tiles is cut
+// into gridDim.x equal contiguous ranges, one per CTA (one CTA per SM), so
+// every SM streams the same number of KV bytes whatever b*Hkv is.  A CTA's
+// range covers one or more "segments" (the part of one item inside it).
+struct Sched {
+  long long T;      // total tiles
+  int tpi;          // tiles per item
+  int m_tiles;      // 128-row query tiles per group
+  int maxseg;       // workspace slots per item
+  __device__ __forceinline__ long long start(int c) const { return (long long)c * T / gridDim.x; }
+  // largest c with start(c) <= x
+  __device__ __forceinline__ int cta_of(long long x) const {
+    return (int)(((x + 1) * gridDim.x - 1) / T);
+  }
+};
+
+static_assert(sizeof(Barriers) <= 512, "barrier block overflows its smem slot");
 
 template <int D>
 __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, int q_rows, int m_tiles, int key_begin,
-               int key_end, int keys_per_split, float scale_log2, float* __restrict__ po,
-               float* __restrict__ pl, long long rows_total) {
+               const __grid_constant__ CUtensorMap tm_v, Sched sc, int q_rows, int key_begin,
+               int key_end, float scale_log2, float* __restrict__ o_out,
+               float* __restrict__ lse_out, int* __restrict__ counters, float* __restrict__ ws_o,
+               float* __restrict__ ws_l) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -75,18 +96,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int split = blockIdx.x;
-  const int g = blockIdx.y / m_tiles;
-  const int mt = blockIdx.y % m_tiles;
-  const int kb = key_begin + split * keys_per_split;
-  const int ke = min(kb + keys_per_split, key_end);
-  const int n_tiles = (ke - kb + BN - 1) / BN;  // >= 1 (host guarantees kb < ke)
+  const long long t_begin = sc.start(blockIdx.x);
+  const long long t_end = sc.start(blockIdx.x + 1);
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
     ptx::mbar_init(&bar->q_full, 1);
+    ptx::mbar_init(&bar->q_empty, 1);
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&bar->k_full[s], 1);
       ptx::mbar_init(&bar->k_empty[s], 1);
@@ -99,6 +117,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
     ptx::mbar_init(&bar->pv_done, 1);
     ptx::mbar_init(&bar->o_full, 1);
+    ptx::mbar_init(&bar->o_empty, 128);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(&bar->tmem_base, TMEM_COLS);
@@ -112,24 +131,31 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     if (lane == 0) {
       const uint64_t keep = ptx::policy_evict_last();
       const uint64_t stream = ptx::policy_evict_first();
-      ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
-      for (int b = 0; b < C::NBOX; ++b)
-        ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
-                         mt * BM, g, keep);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j % C::STAGES;
-        const uint32_t ph = (j / C::STAGES) & 1;
-        const int row = kb + j * BN;
-        ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
-        ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+      int j = 0, seg = 0;
+      for (long long t = t_begin; t < t_end; ++seg) {
+        const int item = (int)(t / sc.tpi);
+        const long long seg_end = min(t_end, (long long)(item + 1) * sc.tpi);
+        const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+        if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
+        ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
         for (int b = 0; b < C::NBOX; ++b)
-          ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
-                           &bar->k_full[s], b * BOX_COLS, row, g, stream);
-        ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
-        ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-        for (int b = 0; b < C::NBOX; ++b)
-          ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
-                           &bar->v_full[s], b * BOX_COLS, row, g, stream);
+          ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
+                           mt * BM, g, keep);
+        for (; t < seg_end; ++t, ++j) {
+          const int s = j % C::STAGES;
+          const uint32_t ph = (j / C::STAGES) & 1;
+          const int row = key_begin + (int)(t - (long long)item * sc.tpi) * BN;
+          ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+          ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+          for (int b = 0; b < C::NBOX; ++b)
+            ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
+                             &bar->k_full[s], b * BOX_COLS, row, g, stream);
+          ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+          ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+          for (int b = 0; b < C::NBOX; ++b)
+            ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
+                             &bar->v_full[s], b * BOX_COLS, row, g, stream);
+        }
       }
     }
   } else if (warp == 1) {
@@ -138,44 +164,54 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, BN, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
-      ptx::mbar_wait(&bar->q_full, 0);
-      ptx::tc_fence_after();
-      for (int j = 0; j <= n_tiles; ++j) {
-        if (j < n_tiles) {
-          const int s = j % C::STAGES;
-          ptx::mbar_wait(&bar->k_full[s], (j / C::STAGES) & 1);
-          ptx::tc_fence_after();
-          const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
-          const uint32_t d_s = tmem + ((j & 1) ? C::COL_S1 : C::COL_S0);
+      int jg = 0, seg = 0;
+      for (long long t0 = t_begin; t0 < t_end; ++seg) {
+        const int item = (int)(t0 / sc.tpi);
+        const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+        ptx::mbar_wait(&bar->q_full, seg & 1);
+        ptx::tc_fence_after();
+        for (int t = 0; t <= n; ++t) {
+          if (t < n) {
+            const int j = jg + t;
+            const int s = j % C::STAGES;
+            ptx::mbar_wait(&bar->k_full[s], (j / C::STAGES) & 1);
+            ptx::tc_fence_after();
+            const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
+            const uint32_t d_s = tmem + ((j & 1) ? C::COL_S1 : C::COL_S0);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            // K-major SW128: 16-element K step = +32 B inside a 64-column box
-            const uint32_t off = (kk / 4) * C::BOX_BYTES + (kk % 4) * 32;
-            ptx::mma_ss(d_s, ptx::sdesc_sw128(q_base + off, 16, 1024),
-                        ptx::sdesc_sw128(k_base + off, 16, 1024), IDESC_S, kk > 0);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              // K-major SW128: a 16-element K step is +32 B inside a 64-column box
+              const uint32_t off = (kk / 4) * C::BOX_BYTES + (kk % 4) * 32;
+              ptx::mma_ss(d_s, ptx::sdesc_sw128(q_base + off, 16, 1024),
+                          ptx::sdesc_sw128(k_base + off, 16, 1024), IDESC_S, kk > 0);
+            }
+            ptx::tc_commit(&bar->k_empty[s]);
+            ptx::tc_commit(&bar->s_full[j & 1]);
+            if (t == n - 1) ptx::tc_commit(&bar->q_empty);  // Q no longer read
           }
-          ptx::tc_commit(&bar->k_empty[s]);
-          ptx::tc_commit(&bar->s_full[j & 1]);
-        }
-        if (j > 0) {
-          const int jj = j - 1;
-          const int s = jj % C::STAGES;
-          ptx::mbar_wait(&bar->p_ready[jj & 1], (jj >> 1) & 1);
-          ptx::mbar_wait(&bar->v_full[s], (jj / C::STAGES) & 1);
-          ptx::tc_fence_after();
-          const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V + s * C::TILE_BYTES);
-          const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
+          if (t > 0) {
+            const int jj = jg + t - 1;
+            const int s = jj % C::STAGES;
+            ptx::mbar_wait(&bar->p_ready[jj & 1], (jj >> 1) & 1);
+            ptx::mbar_wait(&bar->v_full[s], (jj / C::STAGES) & 1);
+            if (t == 1 && seg > 0) ptx::mbar_wait(&bar->o_empty, (seg - 1) & 1);  // O drained
+            ptx::tc_fence_after();
+            const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V + s * C::TILE_BYTES);
+            const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
-            ptx::mma_ts(tmem + C::COL_O, p_tmem + kk * 8,
-                        ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
-                        (jj > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
+              ptx::mma_ts(tmem + C::COL_O, p_tmem + kk * 8,
+                          ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
+                          (t > 1 || kk > 0) ? 1u : 0u);
+            }
+            ptx::tc_commit(&bar->v_empty[s]);
+            ptx::tc_commit(&bar->pv_done);
+            if (t == n) ptx::tc_commit(&bar->o_full);
           }
-          ptx::tc_commit(&bar->v_empty[s]);
-          ptx::tc_commit(&bar->pv_done);
-          if (j == n_tiles) ptx::tc_commit(&bar->o_full);
         }
+        jg += n;
+        t0 += n;
       }
     }
   } else if (warp >= 4) {
@@ -183,93 +219,153 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int wq = warp & 3;                       // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const int row = wq * 32 + lane;                // row inside the 128-row tile
-    float m_used = -INFINITY;                      // running max, log2-scaled
-    float l = 0.f;
     uint32_t r[32];
     float s[BN];
-    for (int j = 0; j < n_tiles; ++j) {
-      const uint32_t s_col = (j & 1) ? C::COL_S1 : C::COL_S0;
-      ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
-      ptx::tc_fence_after();
+    int jg = 0, seg = 0;
+    for (long long t0 = t_begin; t0 < t_end; ++seg) {
+      const int item = (int)(t0 / sc.tpi);
+      const int lt0 = (int)(t0 - (long long)item * sc.tpi);
+      const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+      const int kb = key_begin + lt0 * BN;
+      const int ke = min(kb + n * BN, key_end);
+      float m_used = -INFINITY;  // running max, log2-scaled
+      float l = 0.f;
+      for (int t = 0; t < n; ++t) {
+        const int j = jg + t;
+        const uint32_t s_col = (j & 1) ? C::COL_S1 : C::COL_S0;
+        ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
+        ptx::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, r);
-        ptx::tmem_wait_ld();
+        for (int c = 0; c < BN / 32; ++c) {
+          ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+          ptx::tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-      }
-      const int valid = ke - (kb + j * BN);
-      if (valid < BN) {
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+        }
+        const int valid = ke - (kb + t * BN);
+        if (valid < BN) {
 #pragma unroll
-        for (int i = 0; i < BN; ++i)
-          if (i >= valid) s[i] = -INFINITY;
-      }
-      float mx = s[0];
+          for (int i = 0; i < BN; ++i)
+            if (i >= valid) s[i] = -INFINITY;
+        }
+        float mx = s[0];
 #pragma unroll
-      for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
-      const float m_new = fmaxf(m_used, mx * scale_log2);
-      const bool need = m_new > m_used + RESCALE_THRESHOLD;
-      if (__any_sync(0xffffffffu, need)) {
-        const float alpha = ptx::ex2(m_used - m_new);
-        if (j > 0) {
-          // O holds P_0..P_{j-1} V: wait for the last PV before touching it
-          ptx::mbar_wait(&bar->pv_done, (j - 1) & 1);
-          ptx::tc_fence_after();
+        for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
+        const float m_new = fmaxf(m_used, mx * scale_log2);
+        const bool need = m_new > m_used + RESCALE_THRESHOLD;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = ptx::ex2(m_used - m_new);
+          if (t > 0) {
+            // O holds this segment's P V so far: wait for the last PV before touching it
+            ptx::mbar_wait(&bar->pv_done, (j - 1) & 1);
+            ptx::tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            const uint32_t a = tmem + lane_off + C::COL_O + c * 32;
-            ptx::tmem_ld32(a, r);
-            ptx::tmem_wait_ld();
+            for (int c = 0; c < D / 32; ++c) {
+              const uint32_t a = tmem + lane_off + C::COL_O + c * 32;
+              ptx::tmem_ld32(a, r);
+              ptx::tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            ptx::tmem_st32(a, r);
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              ptx::tmem_st32(a, r);
+            }
+            ptx::tmem_wait_st();
           }
-          ptx::tmem_wait_st();
+          l *= alpha;
+          m_used = m_new;
         }
-        l *= alpha;
-        m_used = m_new;
-      }
-      const float neg = -m_used;
-      float lsum = 0.f;
+        const float neg = -m_used;
+        float lsum = 0.f;
 #pragma unroll
-      for (int c = 0; c < BN / 64; ++c) {
+        for (int c = 0; c < BN / 64; ++c) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = ptx::ex2(fmaf(s[c * 64 + 2 * i], scale_log2, neg));
-          const float p1 = ptx::ex2(fmaf(s[c * 64 + 2 * i + 1], scale_log2, neg));
-          lsum += p0 + p1;
-          r[i] = ptx::pack_bf16(p0, p1);
+          for (int i = 0; i < 32; ++i) {
+            const float p0 = ptx::ex2(fmaf(s[c * 64 + 2 * i], scale_log2, neg));
+            const float p1 = ptx::ex2(fmaf(s[c * 64 + 2 * i + 1], scale_log2, neg));
+            lsum += p0 + p1;
+            r[i] = ptx::pack_bf16(p0, p1);
+          }
+          ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
         }
-        ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
+        l += lsum;
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&bar->p_ready[j & 1]);
       }
-      l += lsum;
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&bar->p_ready[j & 1]);
-    }
-    // ------------------------------------------------------------ epilogue
-    ptx::mbar_wait(&bar->o_full, 0);
-    ptx::tc_fence_after();
-    const float inv = 1.f / l;
-    const float lse = (m_used + log2f(l)) * 0.69314718055994530942f;
-    const int grow = mt * BM + row;
-    const bool live = grow < q_rows;
-    const long long out_row = (long long)split * rows_total + (long long)g * q_rows + grow;
-    float* dst = po + out_row * D;
+      jg += n;
+      t0 += n;
+
+      // ---------------------------------------------------------- segment epilogue
+      const int c_first = sc.cta_of((long long)item * sc.tpi);
+      const int nseg = sc.cta_of((long long)(item + 1) * sc.tpi - 1) - c_first + 1;
+      const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+      const int grow = mt * BM + row;
+      const bool live = grow < q_rows;
+      const long long orow = (long long)g * q_rows + grow;
+      const float inv = 1.f / l;
+      const float lse = (m_used + log2f(l)) * 0.69314718055994530942f;
+      float* dst;
+      if (nseg == 1) {
+        dst = live ? o_out + orow * D : nullptr;
+      } else {
+        const long long slot = ((long long)item * sc.maxseg + (blockIdx.x - c_first)) * BM + row;
+        dst = ws_o + slot * D;
+        ws_l[slot] = lse;
+      }
+      ptx::mbar_wait(&bar->o_full, seg & 1);
+      ptx::tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
-      ptx::tmem_wait_ld();
-      if (live) {
+      for (int c = 0; c < D / 32; ++c) {
+        ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
+        ptx::tmem_wait_ld();
+        if (dst != nullptr) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          float4 v4 = make_float4(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv,
-                                  __uint_as_float(r[i + 2]) * inv, __uint_as_float(r[i + 3]) * inv);
-          *reinterpret_cast<float4*>(dst + c * 32 + i) = v4;
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + c * 32 + i) =
+                make_float4(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv,
+                            __uint_as_float(r[i + 2]) * inv, __uint_as_float(r[i + 3]) * inv);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
+      if (nseg == 1) {
+        if (live) lse_out[orow] = lse;
+      } else {
+        // publish this split; the last split of the item merges all of them
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (row == 0) {
+          const int old = atomicAdd(counters + item, 1);
+          const int last = old == nseg - 1;
+          if (last) counters[item] = 0;  // self-reset for the next launch
+          bar->last_flag = last;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (bar->last_flag) {
+          __threadfence();
+          const long long base = (long long)item * sc.maxseg * BM + row;
+          float mmax = -INFINITY;
+          for (int k = 0; k < nseg; ++k) mmax = fmaxf(mmax, __ldcg(ws_l + base + (long long)k * BM));
+          float z = 0.f;
+          for (int k = 0; k < nseg; ++k) z += __expf(__ldcg(ws_l + base + (long long)k * BM) - mmax);
+          const float iz = 1.f / z;
+          if (live) {
+#pragma unroll 1
+            for (int c = 0; c < D / 4; ++c) {
+              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int k = 0; k < nseg; ++k) {
+                const long long sl = base + (long long)k * BM;
+                const float w = __expf(__ldcg(ws_l + sl) - mmax);
+                const float4 v4 = __ldcg(reinterpret_cast<const float4*>(ws_o + sl * D) + c);
+                acc.x += w * v4.x; acc.y += w * v4.y; acc.z += w * v4.z; acc.w += w * v4.w;
+              }
+              acc.x *= iz; acc.y *= iz; acc.z *= iz; acc.w *= iz;
+              reinterpret_cast<float4*>(o_out + orow * D)[c] = acc;
+            }
+            lse_out[orow] = mmax + logf(z);
+          }
         }
       }
     }
-    if (live) pl[out_row] = lse;
   }
 
   ptx::tc_fence_before();
@@ -322,11 +418,36 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t in
 
 bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 128; }
 
+struct RefreshPlan {
+  int ctas, maxseg, tpi, m_tiles;
+  long long T;
+  size_t counters_bytes, ws_bytes;
+};
+
+static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
+  RefreshPlan p{};
+  p.m_tiles = (int)((q_rows + sm100::BM - 1) / sm100::BM);
+  const long long items = groups * p.m_tiles;
+  p.tpi = (int)((n_keys + sm100::BN - 1) / sm100::BN);
+  p.T = items * p.tpi;
+  p.ctas = (int)std::min<long long>(num_sms(), p.T);
+  const long long per = p.T / p.ctas;  // >= 1
+  p.maxseg = (int)std::min<long long>(p.ctas, (p.tpi + per - 1) / per + 1);
+  p.counters_bytes = align_up((size_t)items * sizeof(int), 256);
+  p.ws_bytes = p.counters_bytes + (size_t)items * p.maxseg * sm100::BM * (head_dim + 1) * sizeof(float);
+  return p;
+}
+
+size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
+  if (n_keys <= 0 || groups <= 0 || q_rows <= 0) return 0;
+  return plan_refresh(groups, q_rows, head_dim, n_keys).ws_bytes;
+}
+
 template <int D>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
-                            int64_t key_end, int64_t keys_per_split, int splits, double scale,
-                            float* po, float* pl, cudaStream_t st) {
+                            int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
+                            size_t ws_bytes, cudaStream_t st) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv;
   int rc;
@@ -339,26 +460,43 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
-  const int m_tiles = (int)((q_rows + sm100::BM - 1) / sm100::BM);
-  dim3 grid((unsigned)splits, (unsigned)(groups * m_tiles));
+  RefreshPlan p = plan_refresh(groups, q_rows, D, key_end - key_begin);
+  const long long items = groups * p.m_tiles;
+  if (ws == nullptr || ws_bytes < p.ws_bytes) {
+    // no room for split partials: one CTA per whole item (no split, no workspace)
+    p.ctas = (int)items;
+    p.maxseg = 1;
+    ws = nullptr;
+  }
+  int* counters = nullptr;
+  float* ws_o = nullptr;
+  float* ws_l = nullptr;
+  if (ws != nullptr) {
+    counters = reinterpret_cast<int*>(ws);
+    ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + p.counters_bytes);
+    ws_l = ws_o + (size_t)items * p.maxseg * sm100::BM * D;
+    if (cudaMemsetAsync(counters, 0, (size_t)items * sizeof(int), st) != cudaSuccess)
+      return check_launch("refresh counters memset");
+  }
+  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  kern<<<grid, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, (int)q_rows, m_tiles, (int)key_begin,
-                                              (int)key_end, (int)keys_per_split, scale_log2, po, pl,
-                                              (long long)(groups * q_rows));
+  kern<<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, sc, (int)q_rows, (int)key_begin,
+                                                         (int)key_end, scale_log2, o_out, lse_out,
+                                                         counters, ws_o, ws_l);
   count_launch();
   return check_launch("refresh_kernel(sm100)");
 }
 
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
-                         int64_t key_begin, int64_t key_end, int64_t keys_per_split, int splits,
-                         double scale, float* po, float* pl, cudaStream_t st) {
+                         int64_t key_begin, int64_t key_end, double scale, float* o_out,
+                         float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (head_dim == 128)
-    return launch_refresh_d<128>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
-                                 keys_per_split, splits, scale, po, pl, st);
+    return launch_refresh_d<128>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
+                                 o_out, lse_out, ws, ws_bytes, st);
   if (head_dim == 64)
-    return launch_refresh_d<64>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
-                                keys_per_split, splits, scale, po, pl, st);
+    return launch_refresh_d<64>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
+                                o_out, lse_out, ws, ws_bytes, st);
   return FB_ERR_UNSUPPORTED;
 }
 
