@@ -5,7 +5,7 @@
 // over the current block's keys (:320) + merge_partials with the cached
 // external partial (:321, :207-245).  The KV cache is not an argument.
 //
-// One CTA per (group, 128-row query tile), 192 threads:
+// One CTA per (group, 128-row query tile), 160 threads:
 //   warps 0..3  softmax + merge epilogue, thread = query row = TMEM lane;
 //   warp 4      TMA (Q, K_in, V_in, and the fp32 O_ext tile, all 128B
 //               swizzled) and the tcgen05.mma issue (one thread).
@@ -23,7 +23,7 @@ namespace fb {
 namespace sm100k2 {
 
 constexpr int BM = 128;
-constexpr int THREADS = 192;
+constexpr int THREADS = 160;  // warps 0-3 softmax/epilogue, warp 4 TMA + MMA
 constexpr int BOX = 64;  // bf16 columns per 128-byte swizzle span
 
 template <int D, int NT>
@@ -121,7 +121,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       }
       ptx::tc_commit(&bar->o_full);
     }
-  } else {
+  } else if (warp < 4) {
     // ------------------------------------------------ softmax + merge epilogue
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const int row = warp * 32 + lane;
