@@ -349,17 +349,40 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           for (int k = 0; k < nseg; ++k) z += __expf(__ldcg(ws_l + base + (long long)k * BM) - mmax);
           const float iz = 1.f / z;
           if (live) {
+            // split partials are L2-resident; keep 16 float4 loads in flight per
+            // thread (two slots x 8 chunks) so the merge tail is a few round trips
 #pragma unroll 1
-            for (int c = 0; c < D / 4; ++c) {
-              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int k = 0; k < nseg; ++k) {
-                const long long sl = base + (long long)k * BM;
-                const float w = __expf(__ldcg(ws_l + sl) - mmax);
-                const float4 v4 = __ldcg(reinterpret_cast<const float4*>(ws_o + sl * D) + c);
-                acc.x += w * v4.x; acc.y += w * v4.y; acc.z += w * v4.z; acc.w += w * v4.w;
+            for (int cg = 0; cg < D / 32; ++cg) {
+              float4 acc[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+              for (int k = 0; k < nseg; k += 2) {
+                const long long sa = base + (long long)k * BM;
+                const bool two = k + 1 < nseg;
+                const long long sb = two ? sa + BM : sa;
+                const float4* pa = reinterpret_cast<const float4*>(ws_o + sa * D) + cg * 8;
+                const float4* pb = reinterpret_cast<const float4*>(ws_o + sb * D) + cg * 8;
+                float4 a[8], b[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  a[i] = __ldcg(pa + i);
+                  b[i] = __ldcg(pb + i);
+                }
+                const float wa = __expf(__ldcg(ws_l + sa) - mmax);
+                const float wb = two ? __expf(__ldcg(ws_l + sb) - mmax) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  acc[i].x += wa * a[i].x + wb * b[i].x;
+                  acc[i].y += wa * a[i].y + wb * b[i].y;
+                  acc[i].z += wa * a[i].z + wb * b[i].z;
+                  acc[i].w += wa * a[i].w + wb * b[i].w;
+                }
               }
-              acc.x *= iz; acc.y *= iz; acc.z *= iz; acc.w *= iz;
-              reinterpret_cast<float4*>(o_out + orow * D)[c] = acc;
+              float4* dstf = reinterpret_cast<float4*>(o_out + orow * D) + cg * 8;
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                dstf[i] = make_float4(acc[i].x * iz, acc[i].y * iz, acc[i].z * iz, acc[i].w * iz);
             }
             lse_out[orow] = mmax + logf(z);
           }

@@ -256,7 +256,8 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t in
                  int64_t dim1_stride_elems, int64_t dim2, int box_inner, int box_rows);
 
 bool sm100_k2_supported(int64_t head_dim, int64_t n_in) {
-  return (head_dim == 128 || head_dim == 64) && n_in >= 0 && n_in <= 128;
+  // n_in == 0 (no current-block keys) takes the SIMT path: there is nothing to load
+  return (head_dim == 128 || head_dim == 64) && n_in >= 1 && n_in <= 128;
 }
 
 template <int D, int NT>
