@@ -295,6 +295,8 @@ extern "C" {
 
 const char* fb_last_error(void) { return g_last_error.c_str(); }
 const char* fb_version(void) { return "fb200 0.1.0 sm_100a"; }
+// Diagnostics (not in the public header): per-CTA timestamps of the refresh kernel.
+FB_API void fb_debug_set_trace(void* device_buffer) { set_refresh_trace(device_buffer); }
 int64_t fb_launch_count(void) { return g_launches.load(); }
 
 size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,

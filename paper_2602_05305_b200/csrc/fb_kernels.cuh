@@ -58,6 +58,7 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 // are merged in-kernel by the last CTA of each item (needs the workspace of
 // refresh_sm100_workspace_bytes; with less it runs one CTA per item).
 bool sm100_supported(int64_t head_dim);
+void set_refresh_trace(void* p);
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,

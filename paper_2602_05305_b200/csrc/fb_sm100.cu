@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace fb {
@@ -60,7 +61,6 @@ struct Barriers {
   uint64_t s_full[2], p_ready[2];
   uint64_t pv_done, o_full, o_empty;
   uint32_t tmem_base;
-  int last_flag;
 };
 
 // Stream-K schedule: the flattened (item, key tile) space of T tiles is cut
@@ -86,8 +86,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, Sched sc, int q_rows, int key_begin,
                int key_end, float scale_log2, float* __restrict__ o_out,
-               float* __restrict__ lse_out, int* __restrict__ counters, float* __restrict__ ws_o,
-               float* __restrict__ ws_l) {
+               float* __restrict__ lse_out, float* __restrict__ ws_o,
+               float* __restrict__ ws_l, unsigned long long* __restrict__ trace) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -98,6 +98,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const int lane = threadIdx.x & 31;
   const long long t_begin = sc.start(blockIdx.x);
   const long long t_end = sc.start(blockIdx.x + 1);
+  // diagnostics (FB_REFRESH_TRACE): globaltimer at start / per-segment stream end / merge end
+  auto stamp = [&](int slot) {
+    if (trace != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      trace[blockIdx.x * 8 + slot] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tm_q);
@@ -293,6 +302,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       jg += n;
       t0 += n;
+      if (row == 0) stamp(1 + 2 * (seg & 1));
 
       // ---------------------------------------------------------- segment epilogue
       const int c_first = sc.cta_of((long long)item * sc.tpi);
@@ -327,67 +337,8 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
-      if (nseg == 1) {
-        if (live) lse_out[orow] = lse;
-      } else {
-        // publish this split; the last split of the item merges all of them
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (row == 0) {
-          const int old = atomicAdd(counters + item, 1);
-          const int last = old == nseg - 1;
-          if (last) counters[item] = 0;  // self-reset for the next launch
-          bar->last_flag = last;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (bar->last_flag) {
-          __threadfence();
-          const long long base = (long long)item * sc.maxseg * BM + row;
-          float mmax = -INFINITY;
-          for (int k = 0; k < nseg; ++k) mmax = fmaxf(mmax, __ldcg(ws_l + base + (long long)k * BM));
-          float z = 0.f;
-          for (int k = 0; k < nseg; ++k) z += __expf(__ldcg(ws_l + base + (long long)k * BM) - mmax);
-          const float iz = 1.f / z;
-          if (live) {
-            // split partials are L2-resident; keep 16 float4 loads in flight per
-            // thread (two slots x 8 chunks) so the merge tail is a few round trips
-#pragma unroll 1
-            for (int cg = 0; cg < D / 32; ++cg) {
-              float4 acc[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-              for (int k = 0; k < nseg; k += 2) {
-                const long long sa = base + (long long)k * BM;
-                const bool two = k + 1 < nseg;
-                const long long sb = two ? sa + BM : sa;
-                const float4* pa = reinterpret_cast<const float4*>(ws_o + sa * D) + cg * 8;
-                const float4* pb = reinterpret_cast<const float4*>(ws_o + sb * D) + cg * 8;
-                float4 a[8], b[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  a[i] = __ldcg(pa + i);
-                  b[i] = __ldcg(pb + i);
-                }
-                const float wa = __expf(__ldcg(ws_l + sa) - mmax);
-                const float wb = two ? __expf(__ldcg(ws_l + sb) - mmax) : 0.f;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  acc[i].x += wa * a[i].x + wb * b[i].x;
-                  acc[i].y += wa * a[i].y + wb * b[i].y;
-                  acc[i].z += wa * a[i].z + wb * b[i].z;
-                  acc[i].w += wa * a[i].w + wb * b[i].w;
-                }
-              }
-              float4* dstf = reinterpret_cast<float4*>(o_out + orow * D) + cg * 8;
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                dstf[i] = make_float4(acc[i].x * iz, acc[i].y * iz, acc[i].z * iz, acc[i].w * iz);
-            }
-            lse_out[orow] = mmax + logf(z);
-          }
-        }
-      }
+      if (nseg == 1 && live) lse_out[orow] = lse;
+      if (row == 0) stamp(2 + 2 * (seg & 1));
     }
   }
 
@@ -397,6 +348,48 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, TMEM_COLS);
   }
+}
+
+// Split merge for items covered by several CTAs: one warp per query row,
+// lanes over columns (coalesced 512 B per partial row); the partials are
+// merged in segment order, so the result does not depend on CTA timing.
+// Same log-space merge as K3 (attention.py:207-233).
+__global__ void __launch_bounds__(256)
+refresh_merge_kernel(Sched sc, int ctas, int q_rows, int D, const float* __restrict__ ws_o,
+                     const float* __restrict__ ws_l, float* __restrict__ o_out,
+                     float* __restrict__ lse_out) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // item*BM + row
+  const int lane = threadIdx.x & 31;
+  const long long item = gw / BM;
+  const int row = (int)(gw % BM);
+  if (item * sc.tpi >= sc.T) return;
+  auto cta_of = [&](long long x) { return (int)(((x + 1) * ctas - 1) / sc.T); };
+  const int c_first = cta_of(item * sc.tpi);
+  const int nseg = cta_of((item + 1) * sc.tpi - 1) - c_first + 1;
+  const int g = (int)(item / sc.m_tiles), mt = (int)(item % sc.m_tiles);
+  const int grow = mt * BM + row;
+  if (nseg == 1 || grow >= q_rows) return;
+  const long long base = item * sc.maxseg * BM + row;  // slot k at base + k*BM
+  float mx = -INFINITY;
+  for (int k = lane; k < nseg; k += 32) mx = fmaxf(mx, ws_l[base + (long long)k * BM]);
+  mx = warp_max(mx);
+  float z = 0.f;
+  for (int k = lane; k < nseg; k += 32) z += __expf(ws_l[base + (long long)k * BM] - mx);
+  z = warp_sum(z);
+  const float iz = 1.f / z;
+  const long long orow = (long long)g * q_rows + grow;
+  for (int c = lane * 4; c < D; c += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < nseg; ++k) {
+      const long long sl = base + (long long)k * BM;
+      const float w = __expf(ws_l[sl] - mx);
+      const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
+      acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+    }
+    *reinterpret_cast<float4*>(o_out + orow * D + c) =
+        make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
+  }
+  if (lane == 0) lse_out[orow] = mx + logf(z);
 }
 
 // ---------------------------------------------------------------- host side
@@ -441,10 +434,13 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t in
 
 bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 128; }
 
+// diagnostics: per-CTA globaltimer stamps (set through fb_debug_set_trace)
+static unsigned long long* g_trace = nullptr;
+
 struct RefreshPlan {
   int ctas, maxseg, tpi, m_tiles;
   long long T;
-  size_t counters_bytes, ws_bytes;
+  size_t ws_bytes;
 };
 
 static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
@@ -454,12 +450,17 @@ static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim
   p.tpi = (int)((n_keys + sm100::BN - 1) / sm100::BN);
   p.T = items * p.tpi;
   p.ctas = (int)std::min<long long>(num_sms(), p.T);
+  if (const char* e = getenv("FB_REFRESH_CTAS")) {  // diagnostics: force the CTA count
+    const long long want = atoll(e);
+    if (want > 0) p.ctas = (int)std::min<long long>(want, p.T);
+  }
   const long long per = p.T / p.ctas;  // >= 1
   p.maxseg = (int)std::min<long long>(p.ctas, (p.tpi + per - 1) / per + 1);
-  p.counters_bytes = align_up((size_t)items * sizeof(int), 256);
-  p.ws_bytes = p.counters_bytes + (size_t)items * p.maxseg * sm100::BM * (head_dim + 1) * sizeof(float);
+  p.ws_bytes = (size_t)items * p.maxseg * sm100::BM * (head_dim + 1) * sizeof(float);
   return p;
 }
+
+void set_refresh_trace(void* p) { g_trace = reinterpret_cast<unsigned long long*>(p); }
 
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
   if (n_keys <= 0 || groups <= 0 || q_rows <= 0) return 0;
@@ -491,23 +492,25 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     p.maxseg = 1;
     ws = nullptr;
   }
-  int* counters = nullptr;
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   if (ws != nullptr) {
-    counters = reinterpret_cast<int*>(ws);
-    ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + p.counters_bytes);
+    ws_o = reinterpret_cast<float*>(ws);
     ws_l = ws_o + (size_t)items * p.maxseg * sm100::BM * D;
-    if (cudaMemsetAsync(counters, 0, (size_t)items * sizeof(int), st) != cudaSuccess)
-      return check_launch("refresh counters memset");
   }
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   kern<<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, sc, (int)q_rows, (int)key_begin,
                                                          (int)key_end, scale_log2, o_out, lse_out,
-                                                         counters, ws_o, ws_l);
+                                                         ws_o, ws_l, g_trace);
   count_launch();
-  return check_launch("refresh_kernel(sm100)");
+  if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
+  if (p.T / p.ctas >= p.tpi && p.T % p.ctas == 0) return FB_OK;  // every item in one CTA
+  const long long warps = items * sm100::BM;
+  sm100::refresh_merge_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
+      sc, p.ctas, (int)q_rows, D, ws_o, ws_l, o_out, lse_out);
+  count_launch();
+  return check_launch("refresh_merge_kernel(sm100)");
 }
 
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
