@@ -315,23 +315,40 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     qg = [K.gqa_view(qs[l], HKV) for l in range(LAYERS)]
     kg = [kc[l].view(groups, cap, D) for l in range(LAYERS)]
     vg = [vc[l].view(groups, cap, D) for l in range(LAYERS)]
-    for l in range(4):
-        K.attention_partial(qg[l], kg[l], vg[l], 0, CTX, None, o_scr, l_scr)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for l in range(LAYERS):
-        K.attention_partial(qg[l], kg[l], vg[l], 0, CTX, None, o_scr, l_scr)
-    e1.record()
-    torch.cuda.synchronize()
-    k1_ms = e0.elapsed_time(e1) / LAYERS
-    # K2 (cached step) alone
-    e0.record()
-    for l in range(LAYERS):
-        eng.cached(l, qs[l], kis[l], vis[l], out=outs[l])
-    e1.record()
-    torch.cuda.synchronize()
-    k2_ms = e0.elapsed_time(e1) / LAYERS
+    # K1 and K2 timed alone, each as a CUDA graph of LAYERS back-to-back launches on
+    # distinct per-layer buffers (no host gaps, no L2 reuse), CUDA events on the
+    # replay stream
+    def graph_of(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        torch.cuda.synchronize()
+        return g
+
+    def k1_all():
+        for l in range(LAYERS):
+            K.attention_partial(qg[l], kg[l], vg[l], 0, CTX, None, o_scr, l_scr)
+
+    def k2_all():
+        for l in range(LAYERS):
+            eng.cached(l, qs[l], kis[l], vis[l], out=outs[l])
+
+    def time_graph(g, reps=3):
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()  # graphs replay on the current stream; events on the same stream
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    g_k1, g_k2 = graph_of(k1_all), graph_of(k2_all)
+    k1_ms = time_graph(g_k1) / LAYERS
+    k2_ms = time_graph(g_k2) / LAYERS
     k2_bytes = (b * HQ * BLK * D * 2 + 2 * b * HKV * BLK * D * 2 + b * HQ * BLK * D * 4
                 + b * HQ * BLK * 4 + b * HQ * BLK * D * 2)
 

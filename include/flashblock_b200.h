@@ -144,6 +144,11 @@ FB_API int fb_block_mass(int dtype, const void* q, const void* k, const void* k_
                   int64_t key_block_size, double scale, double* mass,
                   void* workspace, size_t workspace_bytes, void* stream);
 FB_API size_t fb_block_mass_workspace_bytes(int64_t groups, int64_t q_rows);
+/* Workspace for fb_block_mass at this exact shape (covers the tcgen05 path
+ * taken for BF16, head_dim 64/128, q_rows <= 128, key_block_size 16). */
+FB_API size_t fb_block_mass_workspace_bytes_ex(int dtype, int64_t groups, int64_t q_rows,
+                                               int64_t head_dim, int64_t n_ext, int64_t n_in,
+                                               int64_t key_block_size);
 
 /* K6 -- stable top-k block selection.  Replaces sparse.py:126-128: order by
  * (mass desc, index asc), keep `budget`, emit ascending.  selected: int32
@@ -165,7 +170,8 @@ FB_API int fb_sparse_partitioned(int dtype, const void* q, const void* k, const 
                           const int32_t* selected, int64_t n_sel,
                           int64_t key_block_size, double scale,
                           void* o_sel, void* lse_sel, void* o_res, void* lse_res,
-                          void* out, int out_dtype, int32_t* empty_rows, void* stream);
+                          void* out, int out_dtype, int32_t* empty_rows,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* K8 -- later sparse steps (sparse.py:177-183): attend the selected external
  * blocks (gathered straight from the cache by block index, no copy) plus the
@@ -178,7 +184,15 @@ FB_API int fb_sparse_attend_merge(int dtype, const void* q, const void* k, const
                            const int32_t* selected, int64_t n_sel,
                            int64_t key_block_size, double scale,
                            const void* o_res, const void* lse_res,
-                           void* out, int out_dtype, int32_t* empty_rows, void* stream);
+                           void* out, int out_dtype, int32_t* empty_rows,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Scratch for fb_sparse_partitioned / fb_sparse_attend_merge (BF16 tcgen05
+ * gather path: split partials, the residual block list, the temporary
+ * selected partial).  Other modes need none. */
+FB_API size_t fb_sparse_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
+                                        int64_t head_dim, int64_t n_ext, int64_t n_sel,
+                                        int64_t n_in, int64_t key_block_size);
 
 /* Count of kernel launches issued by this library since load (for bench). */
 FB_API int64_t fb_launch_count(void);

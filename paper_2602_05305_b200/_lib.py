@@ -37,12 +37,14 @@ SIGNATURES = {
     "fb_block_mass": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, i64, i64, dbl, vp, vp, sz,
                             vp]),
     "fb_block_mass_workspace_bytes": (sz, [i64, i64]),
+    "fb_block_mass_workspace_bytes_ex": (sz, [i32, i64, i64, i64, i64, i64, i64]),
     "fb_topk_blocks": (i32, [vp, i64, i64, i64, vp, vp]),
     "fb_mask_budget": (i64, [i64, dbl, i64]),
     "fb_sparse_partitioned": (i32, [i32, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp,
-                                    i64, i64, dbl, vp, vp, vp, vp, vp, i32, vp, vp]),
+                                    i64, i64, dbl, vp, vp, vp, vp, vp, i32, vp, vp, sz, vp]),
     "fb_sparse_attend_merge": (i32, [i32, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp,
-                                     i64, i64, dbl, vp, vp, vp, i32, vp, vp]),
+                                     i64, i64, dbl, vp, vp, vp, i32, vp, vp, sz, vp]),
+    "fb_sparse_workspace_bytes": (sz, [i32, i64, i64, i64, i64, i64, i64, i64]),
 }
 
 _lib = None

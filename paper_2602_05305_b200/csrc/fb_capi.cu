@@ -231,10 +231,45 @@ static int sparse_partitioned_t(const void* qv, const void* kv, const void* vv, 
                                 int64_t cap, int64_t n_ext, int64_t n_in, const int32_t* sel,
                                 int64_t n_sel, int64_t kbs, double scale, void* o_sel, void* l_sel,
                                 void* o_res, void* l_res, void* out, bool out_bf16, int32_t* empty,
-                                cudaStream_t st) {
+                                void* ws, size_t ws_bytes, cudaStream_t st) {
   using Tin = typename Mode::Tin;
   using To = typename Mode::To;
   using Tl = typename Mode::Tl;
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (sm100_supported(d) && kbs == 16 && n_ext < (int64_t(1) << 31) && ws != nullptr) {
+      const int64_t nb = (n_ext + kbs - 1) / kbs;
+      const int64_t n_res = nb - n_sel;
+      const size_t list_bytes = align_up((size_t)groups * std::max<int64_t>(n_res, 1) * 4, 256);
+      const size_t need = list_bytes + std::max(
+          gather_sm100_workspace_bytes(groups, q_rows, d, n_sel, n_in),
+          gather_sm100_workspace_bytes(groups, q_rows, d, n_res, 0));
+      if (ws_bytes >= need) {
+        int32_t* res_list = reinterpret_cast<int32_t*>(ws);
+        void* gws = reinterpret_cast<char*>(ws) + list_bytes;
+        int rc = launch_complement(sel, groups, n_sel, nb, res_list, st);
+        if (rc) return rc;
+        GatherSpec gsel{sel, n_sel, n_ext, n_in, reinterpret_cast<const __nv_bfloat16*>(kin),
+                        reinterpret_cast<const __nv_bfloat16*>(vin)};
+        rc = launch_gather_sm100(reinterpret_cast<const __nv_bfloat16*>(qv),
+                                 reinterpret_cast<const __nv_bfloat16*>(kv),
+                                 reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, cap,
+                                 gsel, scale, reinterpret_cast<float*>(o_sel),
+                                 reinterpret_cast<float*>(l_sel), gws, ws_bytes - list_bytes, st);
+        if (rc) return rc;
+        GatherSpec gres{res_list, n_res, n_ext, 0, nullptr, nullptr};
+        rc = launch_gather_sm100(reinterpret_cast<const __nv_bfloat16*>(qv),
+                                 reinterpret_cast<const __nv_bfloat16*>(kv),
+                                 reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, cap,
+                                 gres, scale, reinterpret_cast<float*>(o_res),
+                                 reinterpret_cast<float*>(l_res), gws, ws_bytes - list_bytes, st);
+        if (rc) return rc;
+        if (out == nullptr) return FB_OK;
+        const void* op[2] = {o_sel, o_res};
+        const void* lp[2] = {l_sel, l_res};
+        return combine_t<Mode>(2, op, lp, groups * q_rows, d, out, out_bf16, nullptr, empty, st);
+      }
+    }
+  }
   const Tin* q = reinterpret_cast<const Tin*>(qv);
   const Tin* k = reinterpret_cast<const Tin*>(kv);
   const Tin* v = reinterpret_cast<const Tin*>(vv);
@@ -272,8 +307,29 @@ static int sparse_attend_t(const void* qv, const void* kv, const void* vv, const
                            const void* vin, int64_t groups, int64_t q_rows, int64_t d, int64_t cap,
                            int64_t n_ext, int64_t n_in, const int32_t* sel, int64_t n_sel,
                            int64_t kbs, double scale, const void* o_res, const void* l_res,
-                           void* out, bool out_bf16, int32_t* empty, cudaStream_t st) {
+                           void* out, bool out_bf16, int32_t* empty, void* ws, size_t ws_bytes,
+                           cudaStream_t st) {
   using Tin = typename Mode::Tin;
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    const int64_t rows = groups * q_rows;
+    const size_t tmp_bytes = align_up((size_t)rows * (d + 1) * sizeof(float), 256);
+    if (sm100_supported(d) && kbs == 16 && n_ext < (int64_t(1) << 31) && ws != nullptr &&
+        ws_bytes >= tmp_bytes + gather_sm100_workspace_bytes(groups, q_rows, d, n_sel, n_in)) {
+      float* o_tmp = reinterpret_cast<float*>(ws);
+      float* l_tmp = o_tmp + (size_t)rows * d;
+      GatherSpec gsel{sel, n_sel, n_ext, n_in, reinterpret_cast<const __nv_bfloat16*>(kin),
+                      reinterpret_cast<const __nv_bfloat16*>(vin)};
+      int rc = launch_gather_sm100(reinterpret_cast<const __nv_bfloat16*>(qv),
+                                   reinterpret_cast<const __nv_bfloat16*>(kv),
+                                   reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d,
+                                   cap, gsel, scale, o_tmp, l_tmp,
+                                   reinterpret_cast<char*>(ws) + tmp_bytes, ws_bytes - tmp_bytes, st);
+      if (rc) return rc;
+      const void* op[2] = {o_tmp, o_res};
+      const void* lp[2] = {l_tmp, l_res};
+      return combine_t<Mode>(o_res ? 2 : 1, op, lp, rows, d, out, out_bf16, nullptr, empty, st);
+    }
+  }
   SelectedMap<Tin> smap{reinterpret_cast<const Tin*>(kv), reinterpret_cast<const Tin*>(vv),
                         reinterpret_cast<const Tin*>(kin), reinterpret_cast<const Tin*>(vin),
                         sel, n_sel, kbs, n_ext, n_in, cap * d, d};
@@ -413,6 +469,14 @@ size_t fb_block_mass_workspace_bytes(int64_t groups, int64_t q_rows) {
   return (size_t)rows * sizeof(double) + per * 1024;
 }
 
+size_t fb_block_mass_workspace_bytes_ex(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,
+                                        int64_t n_ext, int64_t n_in, int64_t kbs) {
+  size_t b = fb_block_mass_workspace_bytes(groups, q_rows);
+  if (dtype == FB_BF16 && score_sm100_supported(head_dim, q_rows, kbs))
+    b = std::max(b, score_sm100_workspace_bytes(groups, q_rows, n_ext, n_in));
+  return b;
+}
+
 int64_t fb_mask_budget(int64_t n_ext, double density, int64_t key_block_size) {
   if (n_ext <= 0 || key_block_size < 1) return 0;
   const int64_t nb = (n_ext + key_block_size - 1) / key_block_size;
@@ -434,6 +498,14 @@ int fb_block_mass(int dtype, const void* q, const void* k, const void* k_in, int
   if (workspace == nullptr || workspace_bytes < (size_t)groups * q_rows * sizeof(double) + 512)
     return fail(FB_ERR_VALUE, "workspace too small (fb_block_mass_workspace_bytes)");
   cudaStream_t st = as_stream(stream);
+  if (dtype == FB_BF16 && score_sm100_supported(head_dim, q_rows, key_block_size) &&
+      n_ext < (int64_t(1) << 31) &&
+      workspace_bytes >= score_sm100_workspace_bytes(groups, q_rows, n_ext, n_in))
+    return launch_score_sm100(reinterpret_cast<const __nv_bfloat16*>(q),
+                              reinterpret_cast<const __nv_bfloat16*>(k),
+                              reinterpret_cast<const __nv_bfloat16*>(k_in), groups, q_rows,
+                              head_dim, kv_rows_cap, n_ext, n_in, scale, mass, workspace,
+                              workspace_bytes, st);
   switch (dtype) {
     case FB_F64:
       return block_mass_t<ModeMaskF64>(q, k, k_in, groups, q_rows, head_dim, kv_rows_cap, n_ext, n_in,
@@ -445,6 +517,18 @@ int fb_block_mass(int dtype, const void* q, const void* k, const void* k_in, int
       return block_mass_t<ModeMaskBF16>(q, k, k_in, groups, q_rows, head_dim, kv_rows_cap, n_ext,
                                         n_in, key_block_size, scale, mass, workspace, workspace_bytes, st);
   }
+}
+
+size_t fb_sparse_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,
+                                 int64_t n_ext, int64_t n_sel, int64_t n_in, int64_t key_block_size) {
+  if (dtype != FB_BF16 || !sm100_supported(head_dim) || key_block_size != 16) return 0;
+  const int64_t nb = (n_ext + key_block_size - 1) / key_block_size;
+  const int64_t rows = groups * q_rows;
+  const size_t list_bytes = align_up((size_t)groups * std::max<int64_t>(nb - n_sel, 1) * 4, 256);
+  const size_t tmp_bytes = align_up((size_t)rows * (head_dim + 1) * sizeof(float), 256);
+  const size_t g1 = gather_sm100_workspace_bytes(groups, q_rows, head_dim, n_sel, n_in);
+  const size_t g2 = gather_sm100_workspace_bytes(groups, q_rows, head_dim, nb - n_sel, 0);
+  return std::max(list_bytes + std::max(g1, g2), tmp_bytes + g1) + 1024;
 }
 
 int fb_topk_blocks(const double* mass, int64_t groups, int64_t num_blocks, int64_t budget,
@@ -460,7 +544,8 @@ int fb_sparse_partitioned(int dtype, const void* q, const void* k, const void* v
                           int64_t kv_rows_cap, int64_t n_ext, int64_t n_in, const int32_t* selected,
                           int64_t n_sel, int64_t key_block_size, double scale, void* o_sel,
                           void* lse_sel, void* o_res, void* lse_res, void* out, int out_dtype,
-                          int32_t* empty_rows, void* stream) {
+                          int32_t* empty_rows, void* workspace, size_t workspace_bytes,
+                          void* stream) {
   if (int rc = check_dtype(dtype)) return rc;
   if (key_block_size < 1) return fail(FB_ERR_VALUE, "key_block_size must be >= 1");
   if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0 || n_sel < 0)
@@ -473,16 +558,17 @@ int fb_sparse_partitioned(int dtype, const void* q, const void* k, const void* v
     case FB_F64:
       return sparse_partitioned_t<ModeF64>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap,
                                            n_ext, n_in, selected, n_sel, key_block_size, scale, o_sel,
-                                           lse_sel, o_res, lse_res, out, false, empty_rows, st);
+                                           lse_sel, o_res, lse_res, out, false, empty_rows, workspace, workspace_bytes, st);
     case FB_F32:
       return sparse_partitioned_t<ModeF32>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap,
                                            n_ext, n_in, selected, n_sel, key_block_size, scale, o_sel,
-                                           lse_sel, o_res, lse_res, out, false, empty_rows, st);
+                                           lse_sel, o_res, lse_res, out, false, empty_rows, workspace, workspace_bytes, st);
     default:
       return sparse_partitioned_t<ModeBF16>(q, k, v, k_in, v_in, groups, q_rows, head_dim,
                                             kv_rows_cap, n_ext, n_in, selected, n_sel, key_block_size,
                                             scale, o_sel, lse_sel, o_res, lse_res, out,
-                                            out_dtype == FB_BF16, empty_rows, st);
+                                            out_dtype == FB_BF16, empty_rows, workspace,
+                                            workspace_bytes, st);
   }
 }
 
@@ -491,7 +577,7 @@ int fb_sparse_attend_merge(int dtype, const void* q, const void* k, const void* 
                            int64_t kv_rows_cap, int64_t n_ext, int64_t n_in, const int32_t* selected,
                            int64_t n_sel, int64_t key_block_size, double scale, const void* o_res,
                            const void* lse_res, void* out, int out_dtype, int32_t* empty_rows,
-                           void* stream) {
+                           void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_dtype(dtype)) return rc;
   if (key_block_size < 1) return fail(FB_ERR_VALUE, "key_block_size must be >= 1");
   if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0 || n_sel < 0)
@@ -506,16 +592,17 @@ int fb_sparse_attend_merge(int dtype, const void* q, const void* k, const void* 
       if (out_dtype != FB_F64) return fail(FB_ERR_VALUE, "F64 mode writes F64 output");
       return sparse_attend_t<ModeF64>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap, n_ext,
                                       n_in, selected, n_sel, key_block_size, scale, o_res, lse_res,
-                                      out, false, empty_rows, st);
+                                      out, false, empty_rows, workspace, workspace_bytes, st);
     case FB_F32:
       if (out_dtype != FB_F32) return fail(FB_ERR_VALUE, "F32 mode writes F32 output");
       return sparse_attend_t<ModeF32>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap, n_ext,
                                       n_in, selected, n_sel, key_block_size, scale, o_res, lse_res,
-                                      out, false, empty_rows, st);
+                                      out, false, empty_rows, workspace, workspace_bytes, st);
     default:
       return sparse_attend_t<ModeBF16>(q, k, v, k_in, v_in, groups, q_rows, head_dim, kv_rows_cap,
                                        n_ext, n_in, selected, n_sel, key_block_size, scale, o_res,
-                                       lse_res, out, out_dtype == FB_BF16, empty_rows, st);
+                                       lse_res, out, out_dtype == FB_BF16, empty_rows, workspace,
+                                       workspace_bytes, st);
   }
 }
 

@@ -46,6 +46,8 @@ int launch_block_mass(const typename Mode::Tin* q, const typename Mode::Tin* k,
                       const double* row_lse, int64_t groups, int64_t q_rows, int64_t head_dim,
                       int64_t slab_stride, int64_t n_ext, int64_t kbs, double scale, double* mass,
                       cudaStream_t st);
+int launch_complement(const int32_t* sel, int64_t groups, int64_t n_sel, int64_t nb, int32_t* out,
+                      cudaStream_t st);
 int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, int32_t* selected,
                 void* scratch, size_t scratch_bytes, cudaStream_t st);
 
@@ -64,6 +66,30 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
                          float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// Gathered variant (sparse K7/K8): keys = mask-selected 16-row blocks of the
+// cache (list [groups, n_list] of ascending block ids, rows clipped at n_ext)
+// followed by the n_in current-block rows of k_in / v_in ([groups, n_in, d]).
+struct GatherSpec {
+  const int32_t* list;
+  int64_t n_list, n_ext, n_in;
+  const __nv_bfloat16* k_in;
+  const __nv_bfloat16* v_in;
+};
+size_t gather_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim,
+                                    int64_t n_list, int64_t n_in);
+int launch_gather_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                        int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                        const GatherSpec& gs, double scale, float* o_out, float* lse_out, void* ws,
+                        size_t ws_bytes, cudaStream_t st);
+
+// K5 on the tensor cores (bf16, q_rows <= 128, kbs == 16): float64 block masses.
+bool score_sm100_supported(int64_t head_dim, int64_t q_rows, int64_t kbs);
+size_t score_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in);
+int launch_score_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* k_in,
+                       int64_t groups, int64_t q_rows, int64_t head_dim, int64_t cap, int64_t n_ext,
+                       int64_t n_in, double scale, double* mass, void* ws, size_t ws_bytes,
+                       cudaStream_t st);
 
 bool sm100_k2_supported(int64_t head_dim, int64_t n_in);
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,

@@ -81,10 +81,21 @@ struct Sched {
 
 static_assert(sizeof(Barriers) <= 512, "barrier block overflows its smem slot");
 
-template <int D>
+// Gathered key source (sparse K7/K8, sparse.py:167-183): an item's first
+// sel_tiles tiles are 8 mask-selected 16-key blocks each (read straight from
+// the cache by block index: one 16-row TMA box per block; missing entries
+// point past the slab end so TMA zero-fills them), followed by the current
+// block's keys from the k_in / v_in tensors in 128-row tiles.
+struct Gather {
+  const int32_t* list;  // [groups, n_list] ascending block ids
+  int n_list, n_ext, n_in, sel_tiles;
+};
+
+template <int D, bool GATHER>
 __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, Sched sc, int q_rows, int key_begin,
+               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ki,
+               const __grid_constant__ CUtensorMap tm_vi, Gather ga, Sched sc, int q_rows, int key_begin,
                int key_end, float scale_log2, float* __restrict__ o_out,
                float* __restrict__ lse_out, float* __restrict__ ws_o,
                float* __restrict__ ws_l, unsigned long long* __restrict__ trace) {
@@ -153,17 +164,53 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         for (; t < seg_end; ++t, ++j) {
           const int s = j % C::STAGES;
           const uint32_t ph = (j / C::STAGES) & 1;
-          const int row = key_begin + (int)(t - (long long)item * sc.tpi) * BN;
-          ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
-          ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-          for (int b = 0; b < C::NBOX; ++b)
-            ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
-                             &bar->k_full[s], b * BOX_COLS, row, g, stream);
-          ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
-          ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-          for (int b = 0; b < C::NBOX; ++b)
-            ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
-                             &bar->v_full[s], b * BOX_COLS, row, g, stream);
+          const int lt = (int)(t - (long long)item * sc.tpi);
+          if constexpr (!GATHER) {
+            const int row = key_begin + lt * BN;
+            ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+            ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+            for (int b = 0; b < C::NBOX; ++b)
+              ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
+                               &bar->k_full[s], b * BOX_COLS, row, g, stream);
+            ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+            ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+            for (int b = 0; b < C::NBOX; ++b)
+              ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
+                               &bar->v_full[s], b * BOX_COLS, row, g, stream);
+          } else if (lt < ga.sel_tiles) {
+            int rows[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int e = lt * 8 + i;
+              rows[i] = e < ga.n_list ? __ldg(ga.list + (long long)g * ga.n_list + e) * 16 : ga.n_ext;
+            }
+            ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+            ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+            for (int b = 0; b < C::NBOX; ++b)
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
+                                 &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], g, stream);
+            ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+            ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+            for (int b = 0; b < C::NBOX; ++b)
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
+                                 &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], g, stream);
+          } else {
+            const int row = (lt - ga.sel_tiles) * BN;
+            ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+            ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+            for (int b = 0; b < C::NBOX; ++b)
+              ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_ki,
+                               &bar->k_full[s], b * BOX_COLS, row, g, stream);
+            ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+            ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+            for (int b = 0; b < C::NBOX; ++b)
+              ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_vi,
+                               &bar->v_full[s], b * BOX_COLS, row, g, stream);
+          }
         }
       }
     }
@@ -251,11 +298,37 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
           for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
         }
-        const int valid = ke - (kb + t * BN);
-        if (valid < BN) {
+        if constexpr (!GATHER) {
+          const int valid = ke - (kb + t * BN);
+          if (valid < BN) {
 #pragma unroll
-          for (int i = 0; i < BN; ++i)
-            if (i >= valid) s[i] = -INFINITY;
+            for (int i = 0; i < BN; ++i)
+              if (i >= valid) s[i] = -INFINITY;
+          }
+        } else {
+          const int lt = lt0 + t;
+          if (lt < ga.sel_tiles) {
+            // per 16-key box: rows of the (possibly clipped tail / missing) block
+            int vr[8];
+            const int g_ = item / sc.m_tiles;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int e = lt * 8 + i;
+              vr[i] = e < ga.n_list
+                          ? min(16, ga.n_ext - __ldg(ga.list + (long long)g_ * ga.n_list + e) * 16)
+                          : 0;
+            }
+#pragma unroll
+            for (int i = 0; i < BN; ++i)
+              if ((i & 15) >= vr[i >> 4]) s[i] = -INFINITY;
+          } else {
+            const int valid = ga.n_in - (lt - ga.sel_tiles) * BN;
+            if (valid < BN) {
+#pragma unroll
+              for (int i = 0; i < BN; ++i)
+                if (i >= valid) s[i] = -INFINITY;
+            }
+          }
         }
         float mx = s[0];
 #pragma unroll
@@ -392,6 +465,245 @@ refresh_merge_kernel(Sched sc, int ctas, int q_rows, int D, const float* __restr
   if (lane == 0) lse_out[orow] = mx + logf(z);
 }
 
+// ---------------------------------------------------------------- K5 scoring
+//
+// Sparse block selection scores (sparse.py:117-125) on the tensor cores:
+//   LSE pass  : per query row, log2-domain log-sum-exp of the scaled scores over
+//               ALL keys (committed [0,n_ext) + current block [0,n_in)), as
+//               stream-K split partials merged by score_lse_merge_kernel;
+//   MASS pass : per external 16-key block, sum over the block's keys and over
+//               the tile's 128 query rows of exp2(s*c - lse2_row); rows reduce in
+//               double in a fixed order (bit-equal masses for equal inputs).
+// K tiles only (no V, no PV): Q + a 6-deep K ring in smem, S double-buffered
+// in TMEM, the softmax warps release each S buffer after reading it.
+template <int D>
+struct ScoreCfg {
+  static constexpr int STAGES = 6;
+  static constexpr int NBOX = D / BOX_COLS;
+  static constexpr uint32_t BOX_BYTES = BM * BOX_COLS * 2;
+  static constexpr uint32_t TILE_BYTES = NBOX * BOX_BYTES;
+  static constexpr uint32_t OFF_Q = 0;
+  static constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
+  static constexpr uint32_t OFF_BAR = OFF_K + STAGES * TILE_BYTES;
+  static constexpr uint32_t OFF_RED = OFF_BAR + 512;  // [2][4][8] doubles
+  static constexpr uint32_t SMEM = OFF_RED + 2 * 4 * 8 * 8 + 1024;
+};
+
+struct ScoreBars {
+  uint64_t q_full, q_empty;
+  uint64_t k_full[6], k_empty[6];
+  uint64_t s_full[2], s_free[2];
+  uint32_t tmem_base;
+};
+
+template <int D, bool MASS>
+__global__ void __launch_bounds__(THREADS, 1)
+score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+             const __grid_constant__ CUtensorMap tm_ki, Sched sc, int q_rows, int n_ext, int n_in,
+             int ext_tiles, float scale_log2, const float* __restrict__ lse2_in,
+             float* __restrict__ lse2_out, float* __restrict__ ws_l, double* __restrict__ mass,
+             int nb) {
+  using C = ScoreCfg<D>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  ScoreBars* bar = reinterpret_cast<ScoreBars*>(smem + C::OFF_BAR);
+  double* red = reinterpret_cast<double*>(smem + C::OFF_RED);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t_begin = sc.start(blockIdx.x), t_end = sc.start(blockIdx.x + 1);
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::mbar_init(&bar->q_full, 1);
+    ptx::mbar_init(&bar->q_empty, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&bar->k_full[s], 1);
+      ptx::mbar_init(&bar->k_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&bar->s_full[b], 1);
+      ptx::mbar_init(&bar->s_free[b], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(&bar->tmem_base, 256);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bar->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t keep = ptx::policy_evict_last(), stream = ptx::policy_evict_first();
+      int j = 0, seg = 0;
+      for (long long t = t_begin; t < t_end; ++seg) {
+        const int item = (int)(t / sc.tpi);
+        const long long seg_end = min(t_end, (long long)(item + 1) * sc.tpi);
+        const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+        if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
+        ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
+        for (int b = 0; b < C::NBOX; ++b)
+          ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
+                           mt * BM, g, keep);
+        for (; t < seg_end; ++t, ++j) {
+          const int s = j % C::STAGES;
+          const int lt = (int)(t - (long long)item * sc.tpi);
+          const bool ext = lt < ext_tiles;
+          const int row = ext ? lt * BN : (lt - ext_tiles) * BN;
+          ptx::mbar_wait(&bar->k_empty[s], ((j / C::STAGES) & 1) ^ 1);
+          ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+          for (int b = 0; b < C::NBOX; ++b)
+            ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES,
+                             ext ? &tm_k : &tm_ki, &bar->k_full[s], b * BOX_COLS, row, g, stream);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, BN, false);
+      const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
+      int j = 0, seg = 0;
+      for (long long t0 = t_begin; t0 < t_end; ++seg) {
+        const int item = (int)(t0 / sc.tpi);
+        const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+        ptx::mbar_wait(&bar->q_full, seg & 1);
+        ptx::tc_fence_after();
+        for (int t = 0; t < n; ++t, ++j) {
+          const int s = j % C::STAGES;
+          ptx::mbar_wait(&bar->k_full[s], (j / C::STAGES) & 1);
+          if (j >= 2) ptx::mbar_wait(&bar->s_free[j & 1], ((j >> 1) - 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * C::BOX_BYTES + (kk % 4) * 32;
+            ptx::mma_ss(tmem + (j & 1) * 128, ptx::sdesc_sw128(q_base + off, 16, 1024),
+                        ptx::sdesc_sw128(k_base + off, 16, 1024), IDESC_S, kk > 0);
+          }
+          ptx::tc_commit(&bar->k_empty[s]);
+          ptx::tc_commit(&bar->s_full[j & 1]);
+          if (t == n - 1) ptx::tc_commit(&bar->q_empty);
+        }
+        t0 += n;
+      }
+    }
+  } else if (warp >= 4) {
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const int row = wq * 32 + lane;
+    uint32_t r[32];
+    float s[BN];
+    int j = 0, seg = 0;
+    for (long long t0 = t_begin; t0 < t_end; ++seg) {
+      const int item = (int)(t0 / sc.tpi);
+      const int lt0 = (int)(t0 - (long long)item * sc.tpi);
+      const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+      const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+      const int grow = mt * BM + row;
+      const bool live = grow < q_rows;
+      const long long orow = (long long)g * q_rows + grow;
+      float m = -INFINITY, l = 0.f;
+      const float lse2 = MASS ? (live ? lse2_in[orow] : INFINITY) : 0.f;
+      for (int t = 0; t < n; ++t, ++j) {
+        const int lt = lt0 + t;
+        ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          ptx::tmem_ld32(tmem + lane_off + (j & 1) * 128 + c * 32, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&bar->s_free[j & 1]);
+        const bool ext = lt < ext_tiles;
+        const int valid = ext ? n_ext - lt * BN : n_in - (lt - ext_tiles) * BN;
+        if constexpr (!MASS) {
+          float mx = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < BN; ++i) {
+            if (i >= valid) s[i] = -INFINITY;
+            mx = fmaxf(mx, s[i]);
+          }
+          const float m_new = fmaxf(m, mx * scale_log2);
+          float acc = 0.f;
+#pragma unroll
+          for (int i = 0; i < BN; ++i) acc += ptx::ex2(fmaf(s[i], scale_log2, -m_new));
+          l = l * ptx::ex2(m - m_new) + acc;
+          m = m_new;
+        } else {
+          double bsum[BN / 16];
+#pragma unroll
+          for (int bi = 0; bi < BN / 16; ++bi) {
+            float a = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int c = bi * 16 + i;
+              a += (c < valid && live) ? ptx::ex2(fmaf(s[c], scale_log2, -lse2)) : 0.f;
+            }
+            double v = (double)a;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            bsum[bi] = v;
+          }
+          double* rb = red + (j & 1) * 32;
+          if (lane == 0) {
+#pragma unroll
+            for (int bi = 0; bi < BN / 16; ++bi) rb[wq * 8 + bi] = bsum[bi];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (wq == 0 && lane < BN / 16) {
+            const int blk = lt * (BN / 16) + lane;
+            if (blk < nb) {
+              const double tot = ((rb[lane] + rb[8 + lane]) + rb[16 + lane]) + rb[24 + lane];
+              mass[(long long)g * nb + blk] = tot;
+            }
+          }
+        }
+      }
+      t0 += n;
+      if constexpr (!MASS) {
+        const int c_first = sc.cta_of((long long)item * sc.tpi);
+        const int nseg = sc.cta_of((long long)(item + 1) * sc.tpi - 1) - c_first + 1;
+        const float lse = m + log2f(l);
+        if (nseg == 1) {
+          if (live) lse2_out[orow] = lse;
+        } else {
+          ws_l[((long long)item * sc.maxseg + (blockIdx.x - c_first)) * BM + row] = lse;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 256);
+  }
+}
+
+__global__ void score_lse_merge_kernel(Sched sc, int ctas, int q_rows, const float* __restrict__ ws_l,
+                                       float* __restrict__ lse2_out) {
+  const long long gr = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // item*BM + row
+  const long long item = gr / BM;
+  const int row = (int)(gr % BM);
+  if (item * sc.tpi >= sc.T) return;
+  auto cta_of = [&](long long x) { return (int)(((x + 1) * ctas - 1) / sc.T); };
+  const int c_first = cta_of(item * sc.tpi);
+  const int nseg = cta_of((item + 1) * sc.tpi - 1) - c_first + 1;
+  const int g = (int)(item / sc.m_tiles), mt = (int)(item % sc.m_tiles);
+  const int grow = mt * BM + row;
+  if (nseg == 1 || grow >= q_rows) return;
+  const long long base = item * sc.maxseg * BM + row;
+  float mx = -INFINITY;
+  for (int k = 0; k < nseg; ++k) mx = fmaxf(mx, ws_l[base + (long long)k * BM]);
+  float z = 0.f;
+  for (int k = 0; k < nseg; ++k) z += exp2f(ws_l[base + (long long)k * BM] - mx);
+  lse2_out[(long long)g * q_rows + grow] = mx + log2f(z);
+}
+
 // ---------------------------------------------------------------- host side
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -467,24 +779,49 @@ size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t hea
   return plan_refresh(groups, q_rows, head_dim, n_keys).ws_bytes;
 }
 
-template <int D>
+template <int D, bool GATHER>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
                             int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
-                            size_t ws_bytes, cudaStream_t st) {
+                            size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr) {
   using C = sm100::Cfg<D>;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
+  sm100::Gather ga{};
+  int64_t tiles;
   if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100::BOX_COLS, sm100::BM))) return rc;
-  if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
-  if ((rc = make_tmap_3d(&mv, v, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
-  auto kern = sm100::refresh_kernel<D>;
+  if constexpr (!GATHER) {
+    if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    if ((rc = make_tmap_3d(&mv, v, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    mki = mk;
+    mvi = mv;
+    tiles = (key_end - key_begin + sm100::BN - 1) / sm100::BN;
+  } else {
+    // cache rows [0, n_ext) in 16-row boxes; current block [0, n_in) in 128-row boxes
+    const int64_t n_ext_eff = gs->n_ext > 0 ? gs->n_ext : 1;
+    if ((rc = make_tmap_3d(&mk, k, 2, D, n_ext_eff, kv_rows_cap, groups, sm100::BOX_COLS, 16))) return rc;
+    if ((rc = make_tmap_3d(&mv, v, 2, D, n_ext_eff, kv_rows_cap, groups, sm100::BOX_COLS, 16))) return rc;
+    if (gs->n_in > 0) {
+      if ((rc = make_tmap_3d(&mki, gs->k_in, 2, D, gs->n_in, gs->n_in, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+      if ((rc = make_tmap_3d(&mvi, gs->v_in, 2, D, gs->n_in, gs->n_in, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    } else {
+      mki = mk;
+      mvi = mv;
+    }
+    ga.list = gs->list;
+    ga.n_list = (int)gs->n_list;
+    ga.n_ext = (int)gs->n_ext;
+    ga.n_in = (int)gs->n_in;
+    ga.sel_tiles = (int)((gs->n_list + 7) / 8);
+    tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
+  }
+  auto kern = sm100::refresh_kernel<D, GATHER>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
-  RefreshPlan p = plan_refresh(groups, q_rows, D, key_end - key_begin);
+  RefreshPlan p = plan_refresh(groups, q_rows, D, tiles * sm100::BN);
   const long long items = groups * p.m_tiles;
   if (ws == nullptr || ws_bytes < p.ws_bytes) {
     // no room for split partials: one CTA per whole item (no split, no workspace)
@@ -500,7 +837,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   }
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  kern<<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, sc, (int)q_rows, (int)key_begin,
+  kern<<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, mki, mvi, ga, sc, (int)q_rows, (int)key_begin,
                                                          (int)key_end, scale_log2, o_out, lse_out,
                                                          ws_o, ws_l, g_trace);
   count_launch();
@@ -518,11 +855,108 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
                          float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (head_dim == 128)
-    return launch_refresh_d<128>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
-                                 o_out, lse_out, ws, ws_bytes, st);
+    return launch_refresh_d<128, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
+                                        scale, o_out, lse_out, ws, ws_bytes, st);
   if (head_dim == 64)
-    return launch_refresh_d<64>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
-                                o_out, lse_out, ws, ws_bytes, st);
+    return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
+                                       scale, o_out, lse_out, ws, ws_bytes, st);
+  return FB_ERR_UNSUPPORTED;
+}
+
+size_t gather_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim,
+                                    int64_t n_list, int64_t n_in) {
+  const int64_t tiles = (n_list + 7) / 8 + (n_in + sm100::BN - 1) / sm100::BN;
+  if (tiles <= 0 || groups <= 0 || q_rows <= 0) return 0;
+  return plan_refresh(groups, q_rows, head_dim, tiles * sm100::BN).ws_bytes;
+}
+
+int launch_gather_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                        int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                        const GatherSpec& gs, double scale, float* o_out, float* lse_out, void* ws,
+                        size_t ws_bytes, cudaStream_t st) {
+  const int64_t tiles = (gs.n_list + 7) / 8 + (gs.n_in + sm100::BN - 1) / sm100::BN;
+  if (tiles == 0) return launch_fill_sentinel<float, float>(o_out, lse_out, groups * q_rows, head_dim, st);
+  if (head_dim == 128)
+    return launch_refresh_d<128, true>(q, k, v, groups, q_rows, kv_rows_cap, 0, 0, scale, o_out,
+                                       lse_out, ws, ws_bytes, st, &gs);
+  if (head_dim == 64)
+    return launch_refresh_d<64, true>(q, k, v, groups, q_rows, kv_rows_cap, 0, 0, scale, o_out,
+                                      lse_out, ws, ws_bytes, st, &gs);
+  return FB_ERR_UNSUPPORTED;
+}
+
+
+// K5 on sm_100a: q_rows <= 128 (one query tile per group), kbs == 16.
+bool score_sm100_supported(int64_t head_dim, int64_t q_rows, int64_t kbs) {
+  return (head_dim == 64 || head_dim == 128) && q_rows <= 128 && kbs == 16;
+}
+
+size_t score_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
+  const int64_t tiles = (n_ext + 127) / 128 + (n_in + 127) / 128;
+  const RefreshPlan p = plan_refresh(groups, q_rows, 0, tiles * 128);
+  return align_up((size_t)groups * q_rows * sizeof(float), 256) + p.ws_bytes;
+}
+
+template <int D>
+static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* k_in,
+                          int64_t groups, int64_t q_rows, int64_t cap, int64_t n_ext, int64_t n_in,
+                          double scale, double* mass, void* ws, size_t ws_bytes, cudaStream_t st) {
+  using C = sm100::ScoreCfg<D>;
+  CUtensorMap mq, mk, mki;
+  int rc;
+  if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100::BOX_COLS, sm100::BM))) return rc;
+  if ((rc = make_tmap_3d(&mk, k, 2, D, n_ext, cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+  if (n_in > 0) {
+    if ((rc = make_tmap_3d(&mki, k_in, 2, D, n_in, n_in, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+  } else {
+    mki = mk;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sm100::score_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(sm100::score_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const int ext_tiles = (int)((n_ext + 127) / 128);
+  const int in_tiles = (int)((n_in + 127) / 128);
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  const int64_t nb = (n_ext + 15) / 16;
+  float* lse2 = reinterpret_cast<float*>(ws);
+  const size_t lse_bytes = align_up((size_t)groups * q_rows * sizeof(float), 256);
+  float* ws_l = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + lse_bytes);
+  // LSE pass over ext + internal keys
+  RefreshPlan p = plan_refresh(groups, q_rows, 0, (int64_t)(ext_tiles + in_tiles) * 128);
+  if (ws_bytes < lse_bytes + p.ws_bytes) return fail(FB_ERR_VALUE, "score workspace too small");
+  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
+  sm100::score_kernel<D, false><<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(
+      mq, mk, mki, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2, nullptr, lse2, ws_l,
+      nullptr, (int)nb);
+  count_launch();
+  if ((rc = check_launch("score_kernel<lse>"))) return rc;
+  if (!(p.T / p.ctas >= p.tpi && p.T % p.ctas == 0)) {
+    const long long rows = groups * p.m_tiles * (long long)sm100::BM;
+    sm100::score_lse_merge_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(sc, p.ctas, (int)q_rows, ws_l, lse2);
+    count_launch();
+    if ((rc = check_launch("score_lse_merge_kernel"))) return rc;
+  }
+  // MASS pass over the external keys
+  RefreshPlan pm = plan_refresh(groups, q_rows, 0, (int64_t)ext_tiles * 128);
+  sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.maxseg};
+  sm100::score_kernel<D, true><<<(unsigned)pm.ctas, sm100::THREADS, C::SMEM, st>>>(
+      mq, mk, mki, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2, lse2, nullptr,
+      nullptr, mass, (int)nb);
+  count_launch();
+  return check_launch("score_kernel<mass>");
+}
+
+int launch_score_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* k_in,
+                       int64_t groups, int64_t q_rows, int64_t head_dim, int64_t cap, int64_t n_ext,
+                       int64_t n_in, double scale, double* mass, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+  if (head_dim == 128)
+    return launch_score_d<128>(q, k, k_in, groups, q_rows, cap, n_ext, n_in, scale, mass, ws, ws_bytes, st);
+  if (head_dim == 64)
+    return launch_score_d<64>(q, k, k_in, groups, q_rows, cap, n_ext, n_in, scale, mass, ws, ws_bytes, st);
   return FB_ERR_UNSUPPORTED;
 }
 

@@ -147,6 +147,34 @@ __global__ void compact_flags_kernel(const unsigned char* __restrict__ flag, int
   }
 }
 
+// Ascending list of the blocks NOT selected (the residual key set,
+// sparse.py:170): the u-th unselected block is u + |{selected < it}|, found
+// by a binary search over the ascending selection.
+__global__ void complement_kernel(const int32_t* __restrict__ sel, int64_t n_sel, int64_t nb,
+                                  int32_t* __restrict__ out) {
+  const int64_t g = blockIdx.y;
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_res = nb - n_sel;
+  if (u >= n_res) return;
+  const int32_t* s = sel + g * n_sel;
+  int64_t lo = 0, hi = n_sel;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)s[mid] - mid <= u) lo = mid + 1; else hi = mid;
+  }
+  out[g * n_res + u] = (int32_t)(u + lo);
+}
+
+int launch_complement(const int32_t* sel, int64_t groups, int64_t n_sel, int64_t nb, int32_t* out,
+                      cudaStream_t st) {
+  const int64_t n_res = nb - n_sel;
+  if (n_res <= 0 || groups == 0) return FB_OK;
+  dim3 grid((unsigned)((n_res + 255) / 256), (unsigned)groups);
+  complement_kernel<<<grid, 256, 0, st>>>(sel, n_sel, nb, out);
+  count_launch();
+  return check_launch("complement_kernel");
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <typename Mode>

@@ -261,7 +261,8 @@ def block_mass(q, k, k_in, n_ext: int, key_block_size: int = 16, scale: float | 
     code = dtype_code(q3)
     nb = -(-int(n_ext) // int(key_block_size))
     mass = torch.empty((groups, nb), dtype=torch.float64, device=q3.device)
-    wsb = _lib.load().fb_block_mass_workspace_bytes(groups, q_rows)
+    wsb = _lib.load().fb_block_mass_workspace_bytes_ex(code, groups, q_rows, d, int(n_ext),
+                                                       ki3.shape[1], int(key_block_size))
     ws = WORKSPACE.get(q3.device, wsb)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     _lib.call("fb_block_mass", code, _p(q3), _p(k3), _p(ki3), groups, q_rows, d, k3.shape[1],
@@ -302,10 +303,13 @@ def sparse_partitioned(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
     out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
     cnt = _empty_counter(q3.device) if check else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_sparse_workspace_bytes(code, groups, q_rows, d, int(n_ext), sel.shape[1],
+                                                ki3.shape[1], int(key_block_size))
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
     _lib.call("fb_sparse_partitioned", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
               q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
               int(key_block_size), scale, _p(o_sel), _p(l_sel), _p(o_res), _p(l_res), _p(out),
-              _OUT_CODE[out_dtype], _p(cnt), _stream(q3))
+              _OUT_CODE[out_dtype], _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
     _raise_if_empty(cnt, "sparse_partitioned")
     return out, (o_sel, l_sel), (o_res, l_res)
 
@@ -335,9 +339,12 @@ def sparse_attend_merge(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
     out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
     cnt = _empty_counter(q3.device) if check else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_sparse_workspace_bytes(code, groups, q_rows, d, int(n_ext), sel.shape[1],
+                                                ki3.shape[1], int(key_block_size))
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
     _lib.call("fb_sparse_attend_merge", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
               q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
               int(key_block_size), scale, _p(o_res), _p(l_res), _p(out), _OUT_CODE[out_dtype],
-              _p(cnt), _stream(q3))
+              _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
     _raise_if_empty(cnt, "sparse_attend_merge")
     return out

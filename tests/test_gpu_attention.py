@@ -404,3 +404,77 @@ def test_bf16_refresh_stream_k_segments(groups, q_rows, n):
     # run twice: the split counters must have reset themselves
     o2, l2 = K.attention_partial(q, k, v, 3, n + 3)
     assert torch.equal(o2, o) and torch.equal(l2, l)
+
+
+def _planted(rng, groups, q_rows, n_ext, n_in, d, planted):
+    q = bf16_exact(rng, (groups, q_rows, d))
+    k = rng.standard_normal((groups, n_ext + n_in, d)).astype(np.float32)
+    for g in range(groups):
+        for blk in planted:
+            k[g, blk * 16:(blk + 1) * 16] += 0.6 * q[g].float().numpy().mean(axis=0)
+    k = torch.from_numpy(k).to(torch.bfloat16)
+    v = bf16_exact(rng, (groups, n_ext + n_in, d))
+    return q, k, v
+
+
+@pytest.mark.parametrize("n_ext,n_in,q_rows", [(1000, 32, 128), (4101, 32, 128), (2048, 0, 96),
+                                               (300, 200, 128)])
+def test_bf16_block_mass_and_topk_vs_oracle(rng, n_ext, n_in, q_rows):
+    """K5 (tcgen05 LSE + mass passes) and K6 on bf16 inputs against the
+    float64 oracle (sparse.py:117-128); planted blocks make the selection
+    well separated, so the index sets must agree exactly."""
+    from paper_2602_05305_b200 import kernels as K
+
+    groups, d = 3, 128
+    planted = [1, 7, 20, 33]
+    q, k, v = _planted(rng, groups, q_rows, n_ext, n_in, d, planted)
+    qc, kc = q.cuda(), k.cuda()
+    kin = kc[:, n_ext:].contiguous()
+    mass = K.block_mass(qc, kc, kin, n_ext, 16).cpu().numpy()
+    nb = -(-n_ext // 16)
+    budget = K.mask_budget(n_ext, 0.02, 16)
+    sel = K.topk_blocks(torch.from_numpy(mass).cuda(), budget).cpu().numpy()
+    for g in range(groups):
+        ref = orc.block_mass(q[g].double().numpy(), k[g].double().numpy(), n_ext, 16)
+        assert mass.shape[1] == nb
+        assert np.max(np.abs(mass[g] - ref)) <= 1e-5 * np.max(ref) + 1e-9
+        want = orc.select_blocks(q[g].double().numpy(), k[g].double().numpy(), n_ext, 0.02, 16)
+        np.testing.assert_array_equal(sel[g], want)
+
+
+@pytest.mark.parametrize("n_ext,density", [(2000, 0.1), (4096, 0.3), (1000, 1.0), (130, 0.5)])
+def test_bf16_sparse_partitioned_and_cached_vs_oracle(rng, n_ext, density):
+    """K7 (gathered tcgen05 passes: selected+current block, residual) and K8
+    (gathered selected + current block fused with the cached residual)
+    against the oracle's sparse_attention_with_residual (sparse.py:139-183)."""
+    from paper_2602_05305_b200 import kernels as K
+
+    groups, q_rows, d, n_in = 2, 128, 128, 32
+    q, k, v = _planted(rng, groups, q_rows, n_ext, n_in, d, [0, 3])
+    qc, kc, vc = q.cuda(), k.cuda(), v.cuda()
+    kin, vin = kc[:, n_ext:].contiguous(), vc[:, n_ext:].contiguous()
+    sels = [orc.select_blocks(q[g].double().numpy(), k[g].double().numpy(), n_ext, density, 16)
+            for g in range(groups)]
+    sel = torch.from_numpy(np.stack(sels).astype(np.int32)).cuda()
+    out, (o_sel, l_sel), (o_res, l_res) = K.sparse_partitioned(qc, kc, vc, kin, vin, n_ext, sel,
+                                                               out_dtype=torch.float32)
+    q2 = (q.float() + 0.05 * torch.randn(q.shape, generator=torch.Generator().manual_seed(3))).to(torch.bfloat16)
+    out2 = K.sparse_attend_merge(q2.cuda(), kc, vc, kin, vin, n_ext, sel, (o_res, l_res),
+                                 out_dtype=torch.float32)
+    only = K.sparse_attend_merge(q2.cuda(), kc, vc, kin, vin, n_ext, sel, None, out_dtype=torch.float32)
+    for g in range(groups):
+        qq, kk, vv = q[g].double().numpy(), k[g].double().numpy(), v[g].double().numpy()
+        ref1, res, sel_p = orc.sparse_with_residual(qq, sels[g], 16, n_ext, kk, vv)
+        assert rel_err(out[g].cpu().numpy(), ref1) <= 1e-2
+        assert rel_err(out[g].cpu().numpy(), orc.dense(qq, kk, vv)) <= 1e-2  # exact partition
+        assert rel_err(o_sel[g].cpu().numpy(), sel_p.out) <= 1e-2
+        if np.isfinite(res.lognorm).all():
+            assert rel_err(o_res[g].cpu().numpy(), res.out) <= 1e-2
+            assert np.max(np.abs(l_res[g].cpu().numpy() - res.lognorm)) <= 1e-3
+        else:
+            assert np.isneginf(l_res[g].cpu().numpy()).all()
+        q2g = q2[g].double().numpy()
+        ref_res = orc.Partial(o_res[g].double().cpu().numpy(), l_res[g].double().cpu().numpy())
+        ref2, _, sel2 = orc.sparse_with_residual(q2g, sels[g], 16, n_ext, kk, vv, residual=ref_res)
+        assert rel_err(out2[g].cpu().numpy(), ref2) <= 1e-2
+        assert rel_err(only[g].cpu().numpy(), sel2.out) <= 1e-2
