@@ -102,7 +102,14 @@ FB_API int fb_internal_merge(int dtype, const void* q, const void* k_in, const v
                       int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_in,
                       double scale, const void* o_ext, const void* lse_ext,
                       void* out, int out_dtype, void* lse_merged,
-                      void* o_int, void* lse_int, int32_t* empty_rows, void* stream);
+                      void* o_int, void* lse_int, int32_t* empty_rows,
+                      void* workspace, size_t workspace_bytes, void* stream);
+/* Scratch fb_internal_merge needs at this shape: 0 for blocks of <= 128 keys
+ * (one fused tcgen05 kernel); large blocks (video chunks) run the stream-K
+ * tensor-core partial over the block's keys plus a K3 merge and need this
+ * much (without it they fall back to the SIMT kernel). */
+FB_API size_t fb_internal_merge_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
+                                                int64_t head_dim, int64_t n_in);
 
 /* K3 -- P-way log-space combine of partials over disjoint key groups.
  * Replaces combine_partials (attention.py:207-233) / merge_partials (:236-245)

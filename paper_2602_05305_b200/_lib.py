@@ -30,7 +30,8 @@ SIGNATURES = {
     "fb_attention_partial": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, i64, dbl, vp, vp,
                                    vp, sz, vp]),
     "fb_internal_merge": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, i32, vp,
-                                vp, vp, vp, vp]),
+                                vp, vp, vp, vp, sz, vp]),
+    "fb_internal_merge_workspace_bytes": (sz, [i32, i64, i64, i64, i64]),
     "fb_combine": (i32, [i32, i32, vp, vp, i64, i64, vp, i32, vp, vp, vp]),
     "fb_full_attention": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i64, dbl, vp,
                                 vp, vp, i32, vp, vp, sz, vp]),

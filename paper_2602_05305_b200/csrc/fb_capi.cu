@@ -397,11 +397,21 @@ int fb_attention_partial(int dtype, const void* q, const void* k, const void* v,
   }
 }
 
+size_t fb_internal_merge_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
+                                        int64_t head_dim, int64_t n_in) {
+  if (dtype != FB_BF16 || !sm100_supported(head_dim) || sm100_k2_supported(head_dim, n_in) ||
+      n_in <= 0)
+    return 0;
+  const int64_t rows = groups * q_rows;
+  return align_up((size_t)rows * (head_dim + 1) * sizeof(float), 256) +
+         refresh_sm100_workspace_bytes(groups, q_rows, head_dim, n_in);
+}
+
 int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_in, int64_t groups,
                       int64_t q_rows, int64_t head_dim, int64_t n_in, double scale,
                       const void* o_ext, const void* lse_ext, void* out, int out_dtype,
                       void* lse_merged, void* o_int, void* lse_int, int32_t* empty_rows,
-                      void* stream) {
+                      void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_dtype(dtype)) return rc;
   if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
@@ -420,6 +430,27 @@ int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_
     default:
       if (out_dtype != FB_F32 && out_dtype != FB_BF16)
         return fail(FB_ERR_VALUE, "BF16 mode writes F32 or BF16 output");
+      if (sm100_supported(head_dim) && !sm100_k2_supported(head_dim, n_in) && n_in > 0 &&
+          n_in < (int64_t(1) << 31) && workspace != nullptr &&
+          workspace_bytes >= fb_internal_merge_workspace_bytes(dtype, groups, q_rows, head_dim, n_in)) {
+        // large current block (video chunks, C5): tensor-core internal partial over
+        // the block's own keys (stream-K refresh kernel), then the K3 merge
+        const int64_t rows = groups * q_rows;
+        const size_t tmp = align_up((size_t)rows * (head_dim + 1) * sizeof(float), 256);
+        float* oi = o_int ? reinterpret_cast<float*>(o_int) : reinterpret_cast<float*>(workspace);
+        float* li = lse_int ? reinterpret_cast<float*>(lse_int)
+                            : reinterpret_cast<float*>(workspace) + (size_t)rows * head_dim;
+        int rc = launch_refresh_sm100(reinterpret_cast<const __nv_bfloat16*>(q),
+                                      reinterpret_cast<const __nv_bfloat16*>(k_in),
+                                      reinterpret_cast<const __nv_bfloat16*>(v_in), groups, q_rows,
+                                      head_dim, n_in, 0, n_in, scale, oi, li,
+                                      reinterpret_cast<char*>(workspace) + tmp, workspace_bytes - tmp, st);
+        if (rc) return rc;
+        const void* op[2] = {o_ext, oi};
+        const void* lp[2] = {lse_ext, li};
+        return combine_t<ModeBF16>(2, op, lp, rows, head_dim, out, out_dtype == FB_BF16, lse_merged,
+                                   empty_rows, st);
+      }
       return internal_merge_t<ModeBF16>(q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
                                         lse_ext, out, out_dtype == FB_BF16, lse_merged, o_int,
                                         lse_int, empty_rows, st);
@@ -457,7 +488,7 @@ int fb_full_attention(int dtype, const void* q, const void* k, const void* v, in
   if (rc) return rc;
   return fb_internal_merge(dtype, q, k_in, v_in, groups, q_rows, head_dim, n_in, scale,
                            o_ext_scratch, lse_ext_scratch, out, out_dtype, nullptr, nullptr, nullptr,
-                           empty_rows, stream);
+                           empty_rows, workspace, workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------- sparse

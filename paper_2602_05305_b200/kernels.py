@@ -167,9 +167,11 @@ def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
     l_int = torch.empty((groups, q_rows), dtype=lt, device=q3.device) if want_internal else None
     cnt = _empty_counter(q3.device) if check else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_internal_merge_workspace_bytes(code, groups, q_rows, d, k3.shape[1])
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
     _lib.call("fb_internal_merge", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
               scale, _p(o_ext), _p(lse_ext), _p(out), _OUT_CODE[out.dtype], _p(lse_m), _p(o_int),
-              _p(l_int), _p(cnt), _stream(q3))
+              _p(l_int), _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
     _raise_if_empty(cnt, "internal_merge")
     if not (want_lse or want_internal):
         return out
@@ -234,7 +236,9 @@ def full_attention(q, k, v, n_ext: int, k_in, v_in, scale: float | None = None,
         out = torch.empty((groups, q_rows, d), dtype=out_dtype, device=q3.device)
     cnt = _empty_counter(q3.device) if check else None
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
-    wsb = _lib.load().fb_partial_workspace_bytes(code, groups, q_rows, d, int(n_ext))
+    lib = _lib.load()
+    wsb = max(lib.fb_partial_workspace_bytes(code, groups, q_rows, d, int(n_ext)),
+              lib.fb_internal_merge_workspace_bytes(code, groups, q_rows, d, ki3.shape[1]))
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
     _lib.call("fb_full_attention", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
               int(n_ext), _p(ki3), _p(vi3), ki3.shape[1], scale, _p(o_ext), _p(lse_ext), _p(out),

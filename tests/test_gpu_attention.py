@@ -478,3 +478,26 @@ def test_bf16_sparse_partitioned_and_cached_vs_oracle(rng, n_ext, density):
         ref2, _, sel2 = orc.sparse_with_residual(q2g, sels[g], 16, n_ext, kk, vv, residual=ref_res)
         assert rel_err(out2[g].cpu().numpy(), ref2) <= 1e-2
         assert rel_err(only[g].cpu().numpy(), sel2.out) <= 1e-2
+
+
+@pytest.mark.parametrize("q_rows,n_in,n_ext", [(600, 600, 1000), (300, 200, 0), (4680 // 4, 4680 // 4, 700)])
+def test_bf16_large_block_cached_step_vs_oracle(rng, q_rows, n_in, n_ext):
+    """Video-shaped cached step (C5: one head per group, a block of hundreds to
+    thousands of queries attending its own keys): the tensor-core internal
+    partial + K3 merge path of fb_internal_merge, against the oracle."""
+    from paper_2602_05305_b200 import kernels as K
+
+    groups, d = 2, 128
+    q = bf16_exact(rng, (groups, q_rows, d))
+    k = bf16_exact(rng, (groups, n_ext + n_in, d))
+    v = bf16_exact(rng, (groups, n_ext + n_in, d))
+    qc, kc, vc = q.cuda(), k.cuda(), v.cuda()
+    o_ext, l_ext = K.attention_partial(qc, kc, vc, 0, n_ext)
+    kin, vin = kc[:, n_ext:].contiguous(), vc[:, n_ext:].contiguous()
+    out, lse_m = K.internal_merge(qc, kin, vin, o_ext, l_ext, out_dtype=torch.float32, want_lse=True)
+    full, _, _ = K.full_attention(qc, kc, vc, n_ext, kin, vin, out_dtype=torch.bfloat16)
+    for g in range(groups):
+        qq, kk, vv = q[g].double().numpy(), k[g].double().numpy(), v[g].double().numpy()
+        ref = orc.dense(qq, kk, vv)
+        assert rel_err(out[g].cpu().numpy(), ref) <= 1e-2
+        assert rel_err(full[g].float().cpu().numpy(), ref) <= 1.5e-2
