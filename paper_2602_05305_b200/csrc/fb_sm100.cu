@@ -286,6 +286,13 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int ke = min(kb + n * BN, key_end);
       float m_used = -INFINITY;  // running max, log2-scaled
       float l = 0.f;
+      int last_rows = 16;  // valid rows of the list's last block (gather mode)
+      if constexpr (GATHER) {
+        if (ga.n_list > 0) {
+          const int last = __ldg(ga.list + (long long)(item / sc.m_tiles) * ga.n_list + ga.n_list - 1);
+          last_rows = min(16, ga.n_ext - last * 16);
+        }
+      }
       for (int t = 0; t < n; ++t) {
         const int j = jg + t;
         const uint32_t s_col = (j & 1) ? C::COL_S1 : C::COL_S0;
@@ -308,19 +315,20 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         } else {
           const int lt = lt0 + t;
           if (lt < ga.sel_tiles) {
-            // per 16-key box: rows of the (possibly clipped tail / missing) block
-            int vr[8];
-            const int g_ = item / sc.m_tiles;
+            // 16 rows per listed block; entries past the list are empty; only the
+            // last entry of the ascending list can be the slab's clipped tail block
+            const int e0 = lt * 8;
+            if (e0 + 8 >= ga.n_list) {  // this tile holds the list's end
+              int vr[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int e = lt * 8 + i;
-              vr[i] = e < ga.n_list
-                          ? min(16, ga.n_ext - __ldg(ga.list + (long long)g_ * ga.n_list + e) * 16)
-                          : 0;
+              for (int i = 0; i < 8; ++i) {
+                const int e = e0 + i;
+                vr[i] = e < ga.n_list - 1 ? 16 : (e == ga.n_list - 1 ? last_rows : 0);
+              }
+#pragma unroll
+              for (int i = 0; i < BN; ++i)
+                if ((i & 15) >= vr[i >> 4]) s[i] = -INFINITY;
             }
-#pragma unroll
-            for (int i = 0; i < BN; ++i)
-              if ((i & 15) >= vr[i >> 4]) s[i] = -INFINITY;
           } else {
             const int valid = ga.n_in - (lt - ga.sel_tiles) * BN;
             if (valid < BN) {
@@ -485,8 +493,8 @@ struct ScoreCfg {
   static constexpr uint32_t OFF_Q = 0;
   static constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
   static constexpr uint32_t OFF_BAR = OFF_K + STAGES * TILE_BYTES;
-  static constexpr uint32_t OFF_RED = OFF_BAR + 512;  // [2][4][8] doubles
-  static constexpr uint32_t SMEM = OFF_RED + 2 * 4 * 8 * 8 + 1024;
+  static constexpr uint32_t OFF_RED = OFF_BAR + 512;  // [2][8][4] doubles + [2][128] floats
+  static constexpr uint32_t SMEM = OFF_RED + 2 * 8 * 4 * 8 + 2 * 128 * 4 + 1024;
 };
 
 struct ScoreBars {
@@ -496,8 +504,10 @@ struct ScoreBars {
   uint32_t tmem_base;
 };
 
+constexpr int SCORE_THREADS = 384;  // 4 control warps + 2 score warpgroups
+
 template <int D, bool MASS>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(SCORE_THREADS, 1)
 score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
              const __grid_constant__ CUtensorMap tm_ki, Sched sc, int q_rows, int n_ext, int n_in,
              int ext_tiles, float scale_log2, const float* __restrict__ lse2_in,
@@ -523,7 +533,7 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bar->s_full[b], 1);
-      ptx::mbar_init(&bar->s_free[b], 128);
+      ptx::mbar_init(&bar->s_free[b], 256);
     }
     ptx::fence_barrier_init();
   }
@@ -589,11 +599,16 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
       }
     }
   } else if (warp >= 4) {
+    // two score warpgroups: WG0 (warps 4-7) columns 0-63, WG1 (warps 8-11)
+    // columns 64-127 of every S tile; the same 128 rows (TMEM lanes).
+    constexpr int HALF = BN / 2;
     const int wq = warp & 3;
+    const int wg = (warp - 4) >> 2;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const int row = wq * 32 + lane;
+    float* xch = reinterpret_cast<float*>(red + 2 * 8 * 4);  // [2][128] (m, l) of WG1
     uint32_t r[32];
-    float s[BN];
+    float s[HALF];
     int j = 0, seg = 0;
     for (long long t0 = t_begin; t0 < t_end; ++seg) {
       const int item = (int)(t0 / sc.tpi);
@@ -610,8 +625,8 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          ptx::tmem_ld32(tmem + lane_off + (j & 1) * 128 + c * 32, r);
+        for (int c = 0; c < HALF / 32; ++c) {
+          ptx::tmem_ld32(tmem + lane_off + (j & 1) * 128 + wg * HALF + c * 32, r);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
@@ -619,60 +634,80 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bar->s_free[j & 1]);
         const bool ext = lt < ext_tiles;
-        const int valid = ext ? n_ext - lt * BN : n_in - (lt - ext_tiles) * BN;
+        const int valid = (ext ? n_ext - lt * BN : n_in - (lt - ext_tiles) * BN) - wg * HALF;
         if constexpr (!MASS) {
           float mx = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < BN; ++i) {
+          for (int i = 0; i < HALF; ++i) {
             if (i >= valid) s[i] = -INFINITY;
             mx = fmaxf(mx, s[i]);
           }
           const float m_new = fmaxf(m, mx * scale_log2);
-          float acc = 0.f;
+          if (m_new != -INFINITY) {  // a half tile may be fully masked
+            float acc = 0.f;
 #pragma unroll
-          for (int i = 0; i < BN; ++i) acc += ptx::ex2(fmaf(s[i], scale_log2, -m_new));
-          l = l * ptx::ex2(m - m_new) + acc;
-          m = m_new;
+            for (int i = 0; i < HALF; ++i) acc += ptx::ex2(fmaf(s[i], scale_log2, -m_new));
+            l = l * ptx::ex2(m - m_new) + acc;
+            m = m_new;
+          }
         } else {
-          double bsum[BN / 16];
+          // 4 blocks of 16 keys per thread; warp transpose-reduce: 6 shuffles
+          // leave block (2*bit4 + bit3) of lane's warp sum in every lane
+          float a[4];
 #pragma unroll
-          for (int bi = 0; bi < BN / 16; ++bi) {
-            float a = 0.f;
+          for (int bi = 0; bi < 4; ++bi) {
+            float acc = 0.f;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int c = bi * 16 + i;
-              a += (c < valid && live) ? ptx::ex2(fmaf(s[c], scale_log2, -lse2)) : 0.f;
+              acc += (c < valid && live) ? ptx::ex2(fmaf(s[c], scale_log2, -lse2)) : 0.f;
             }
-            double v = (double)a;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            bsum[bi] = v;
+            a[bi] = acc;
           }
-          double* rb = red + (j & 1) * 32;
-          if (lane == 0) {
-#pragma unroll
-            for (int bi = 0; bi < BN / 16; ++bi) rb[wq * 8 + bi] = bsum[bi];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (wq == 0 && lane < BN / 16) {
+          const bool b4 = lane & 16, b3 = lane & 8;
+          const float r0 = __shfl_xor_sync(0xffffffffu, b4 ? a[0] : a[2], 16);
+          const float r1 = __shfl_xor_sync(0xffffffffu, b4 ? a[1] : a[3], 16);
+          const float c0 = (b4 ? a[2] : a[0]) + r0;
+          const float c1 = (b4 ? a[3] : a[1]) + r1;
+          const float rr = __shfl_xor_sync(0xffffffffu, b3 ? c0 : c1, 8);
+          float v = (b3 ? c1 : c0) + rr;
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          double* rb = red + (j & 1) * 32;  // [8 blocks][4 warps]
+          if ((lane & 7) == 0) rb[(wg * 4 + (lane >> 3)) * 4 + wq] = (double)v;
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (wg == 0 && wq == 0 && lane < 8) {
             const int blk = lt * (BN / 16) + lane;
             if (blk < nb) {
-              const double tot = ((rb[lane] + rb[8 + lane]) + rb[16 + lane]) + rb[24 + lane];
-              mass[(long long)g * nb + blk] = tot;
+              const double* x = rb + lane * 4;
+              mass[(long long)g * nb + blk] = ((x[0] + x[1]) + x[2]) + x[3];
             }
           }
         }
       }
       t0 += n;
       if constexpr (!MASS) {
-        const int c_first = sc.cta_of((long long)item * sc.tpi);
-        const int nseg = sc.cta_of((long long)(item + 1) * sc.tpi - 1) - c_first + 1;
-        const float lse = m + log2f(l);
-        if (nseg == 1) {
-          if (live) lse2_out[orow] = lse;
-        } else {
-          ws_l[((long long)item * sc.maxseg + (blockIdx.x - c_first)) * BM + row] = lse;
+        // combine the two column halves of each row, then the split partials
+        if (wg == 1) {
+          xch[row] = m;
+          xch[BM + row] = l;
         }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (wg == 0) {
+          const float m1 = xch[row], l1 = xch[BM + row];
+          const float mm = fmaxf(m, m1);
+          const float lt = l * ptx::ex2(m - mm) + l1 * ptx::ex2(m1 - mm);
+          const int c_first = sc.cta_of((long long)item * sc.tpi);
+          const int nseg = sc.cta_of((long long)(item + 1) * sc.tpi - 1) - c_first + 1;
+          const float lse = mm + log2f(lt);
+          if (nseg == 1) {
+            if (live) lse2_out[orow] = lse;
+          } else {
+            ws_l[((long long)item * sc.maxseg + (blockIdx.x - c_first)) * BM + row] = lse;
+          }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
     }
   }
@@ -928,7 +963,7 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   RefreshPlan p = plan_refresh(groups, q_rows, 0, (int64_t)(ext_tiles + in_tiles) * 128);
   if (ws_bytes < lse_bytes + p.ws_bytes) return fail(FB_ERR_VALUE, "score workspace too small");
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
-  sm100::score_kernel<D, false><<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(
+  sm100::score_kernel<D, false><<<(unsigned)p.ctas, sm100::SCORE_THREADS, C::SMEM, st>>>(
       mq, mk, mki, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2, nullptr, lse2, ws_l,
       nullptr, (int)nb);
   count_launch();
@@ -942,7 +977,7 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   // MASS pass over the external keys
   RefreshPlan pm = plan_refresh(groups, q_rows, 0, (int64_t)ext_tiles * 128);
   sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.maxseg};
-  sm100::score_kernel<D, true><<<(unsigned)pm.ctas, sm100::THREADS, C::SMEM, st>>>(
+  sm100::score_kernel<D, true><<<(unsigned)pm.ctas, sm100::SCORE_THREADS, C::SMEM, st>>>(
       mq, mk, mki, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2, lse2, nullptr,
       nullptr, mass, (int)nb);
   count_launch();

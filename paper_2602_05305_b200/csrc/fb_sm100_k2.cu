@@ -26,22 +26,28 @@ constexpr int BM = 128;
 constexpr int THREADS = 160;  // warps 0-3 softmax/epilogue, warp 4 TMA + MMA
 constexpr int BOX = 64;  // bf16 columns per 128-byte swizzle span
 
+// The output columns of a query tile are split over SPLIT CTAs (each
+// recomputes the cheap S = Q K^T and softmax, then does P V, the merge and
+// the stores for its D/SPLIT columns): twice the CTAs, a third fewer bytes each.
 template <int D, int NT>
 struct Cfg {
+  static constexpr int SPLIT = D == 128 ? 2 : 1;
+  static constexpr int DC = D / SPLIT;                  // output columns per CTA
   static constexpr int NB = D / BOX;                    // 64-col boxes per bf16 row
+  static constexpr int NBV = DC / BOX;                  // V boxes per CTA
   static constexpr uint32_t QBOX = BM * 128;            // 16 KB
   static constexpr uint32_t KBOX = NT * 128;            // NT rows x 128 B
   static constexpr uint32_t OBOX = BM * 128;            // fp32: 32 cols x 128 rows
-  static constexpr int NOB = D / 32;                    // fp32 boxes of O_ext
+  static constexpr int NOB = DC / 32;                   // fp32 boxes of O_ext per CTA
   static constexpr uint32_t OFF_Q = 0;
   static constexpr uint32_t OFF_K = OFF_Q + NB * QBOX;
   static constexpr uint32_t OFF_V = OFF_K + NB * KBOX;
-  static constexpr uint32_t OFF_O = OFF_V + NB * KBOX;
+  static constexpr uint32_t OFF_O = OFF_V + NBV * KBOX;
   static constexpr uint32_t OFF_BAR = OFF_O + NOB * OBOX;
   static constexpr uint32_t SMEM = OFF_BAR + 128 + 1024;
   static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;  // P stores span >= 32 cols
-  static constexpr uint32_t TMEM_COLS = (COL_O + D) <= 128 ? 128 : (COL_O + D) <= 256 ? 256 : 512;
-  static constexpr uint32_t TX_QKV = NB * (QBOX + 2 * KBOX);
+  static constexpr uint32_t TMEM_COLS = (COL_O + DC) <= 128 ? 128 : (COL_O + DC) <= 256 ? 256 : 512;
+  static constexpr uint32_t TX_QKV = NB * (QBOX + KBOX) + NBV * KBOX;
 };
 
 struct Bars {
@@ -63,8 +69,10 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bar = reinterpret_cast<Bars*>(smem + C::OFF_BAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x / m_tiles;
-  const int mt = blockIdx.x % m_tiles;
+  const int h = blockIdx.x % C::SPLIT;  // output-column slice
+  const int g = (blockIdx.x / C::SPLIT) / m_tiles;
+  const int mt = (blockIdx.x / C::SPLIT) % m_tiles;
+  const int col0 = h * C::DC;
 
   if (threadIdx.x == 128) {
     ptx::tma_prefetch_desc(&tm_q);
@@ -91,14 +99,15 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       for (int b = 0; b < C::NB; ++b) {
         ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
         ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
-        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, b * BOX, 0, g, pol);
       }
+      for (int b = 0; b < C::NBV; ++b)
+        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, g, pol);
       ptx::mbar_expect_tx(&bar->load_o, C::NOB * C::OBOX);
       for (int b = 0; b < C::NOB; ++b)
-        ptx::tma_load_3d(smem + C::OFF_O + b * C::OBOX, &tm_o, &bar->load_o, b * 32, mt * BM, g, pol);
+        ptx::tma_load_3d(smem + C::OFF_O + b * C::OBOX, &tm_o, &bar->load_o, col0 + b * 32, mt * BM, g, pol);
 
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
-      constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
+      constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, C::DC, true);
       ptx::mbar_wait(&bar->load_qkv, 0);
       ptx::tc_fence_after();
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
@@ -192,7 +201,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     ptx::tc_fence_after();
     const unsigned char* o_sm = smem + C::OFF_O;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < C::DC / 32; ++c) {
       ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
       ptx::tmem_wait_ld();
       // cached external row chunk c (fp32, 128B-swizzled box c): 8 x 16-byte pieces
@@ -212,7 +221,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       }
       if (live_row) {
         if (out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * D + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * D + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             dst[j] = make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]),
@@ -220,13 +229,13 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                                 ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]),
                                 ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
         } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * D + c * 32);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * D + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             dst[j] = make_float4(val[4 * j], val[4 * j + 1], val[4 * j + 2], val[4 * j + 3]);
         }
         if (o_int) {
-          float4* di = reinterpret_cast<float4*>(o_int + rr * D + c * 32);
+          float4* di = reinterpret_cast<float4*>(o_int + rr * D + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             di[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
@@ -234,7 +243,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         }
       }
     }
-    if (live_row) {
+    if (live_row && h == 0) {
       if (lse_int) lse_int[rr] = li;
       if (lse_merged) lse_merged[rr] = live ? mm + logf(z) : -INFINITY;
       if (!live && empty_rows) atomicAdd(empty_rows, 1);
@@ -281,7 +290,7 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   }
   const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  kern<<<(unsigned)(groups * m_tiles), sm100k2::THREADS, C::SMEM, st>>>(
+  kern<<<(unsigned)(groups * m_tiles * C::SPLIT), sm100k2::THREADS, C::SMEM, st>>>(
       mq, mk, mv, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
       lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty));
   count_launch();
