@@ -121,6 +121,114 @@ __global__ void topk_bitonic_kernel(const double* __restrict__ mass, int64_t nb,
   }
 }
 
+// Radix select, one CTA (1024 threads) per group: the budget-th largest mass
+// T is found MSB-first over the 64-bit pattern of the (non-negative) double
+// masses, 8 bits per pass; then blocks with mass > T, plus the lowest-index
+// blocks with mass == T up to the budget, are emitted in ascending index
+// order -- exactly a stable sort on -mass truncated to the budget
+// (sparse.py:127-128).  Masses live in shared memory (nb <= 24K).
+constexpr int TOPK_THREADS = 1024;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_tot[lane];
+    int inc = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    warp_tot[lane] = inc - w;  // exclusive per warp
+    if (lane == 31) warp_tot[32] = inc;
+  }
+  __syncthreads();
+  const int res = warp_tot[warp] + x - v;
+  total = warp_tot[32];
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(TOPK_THREADS)
+topk_radix_kernel(const double* __restrict__ mass, int nb, int budget, int32_t* __restrict__ selected) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);
+  __shared__ int hist[256];
+  __shared__ int warp_tot[33];
+  __shared__ unsigned long long sh_prefix;
+  __shared__ int sh_k;
+  const int g = blockIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    key[i] = (unsigned long long)__double_as_longlong(mass[(long long)g * nb + i]);
+  if (threadIdx.x == 0) {
+    sh_prefix = 0ull;
+    sh_k = budget;
+  }
+  __syncthreads();
+  unsigned long long mask = 0ull;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = sh_prefix;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+      if ((key[i] & mask) == prefix) atomicAdd(&hist[(key[i] >> shift) & 255], 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // bins from the top: find digit d with (count above d) < k <= (count at or above d)
+      const int lane = threadIdx.x;
+      int k = sh_k;
+      int above = 0;
+      for (int base = 255; base >= 0; base -= 32) {
+        const int d = base - lane;
+        const int c = hist[d];
+        int inc = c;  // inclusive prefix from the top
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, above + inc >= k && above + inc - c < k);
+        if (hit) {
+          const int src = __ffs(hit) - 1;
+          const int cnt_before = __shfl_sync(0xffffffffu, above + inc - c, src);
+          if (lane == 0) {
+            sh_prefix = prefix | ((unsigned long long)(base - src) << shift);
+            sh_k = k - cnt_before;
+          }
+          break;
+        }
+        above += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    mask |= 0xffull << shift;
+    __syncthreads();
+  }
+  const unsigned long long T = sh_prefix;
+  const int take_eq = sh_k;  // blocks with mass == T to take, lowest indices first
+  int eq_base = 0, out_base = 0;
+  for (int c0 = 0; c0 < nb; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const unsigned long long kv = i < nb ? key[i] : 0ull;
+    const int eq = (i < nb && kv == T) ? 1 : 0;
+    int eq_tot;
+    const int eq_before = eq_base + block_exclusive_scan(eq, warp_tot, eq_tot);
+    const int sel = (i < nb) && (kv > T || (eq && eq_before < take_eq));
+    int sel_tot;
+    const int pos = out_base + block_exclusive_scan(sel, warp_tot, sel_tot);
+    if (sel) selected[(long long)g * budget + pos] = (int32_t)i;
+    eq_base += eq_tot;
+    out_base += sel_tot;
+  }
+}
+
 // Fallback for very large nb: rank by counting (O(nb^2), exact).
 __global__ void topk_rank_kernel(const double* __restrict__ mass, int64_t nb, int64_t budget,
                                  int32_t* __restrict__ selected, unsigned char* __restrict__ flag) {
@@ -202,6 +310,13 @@ template int launch_block_mass<ModeMaskBF16>(const __nv_bfloat16*, const __nv_bf
 int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, int32_t* selected,
                 void* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (groups == 0 || budget == 0) return FB_OK;
+  if (nb <= 24 * 1024) {
+    const size_t smem = (size_t)nb * sizeof(unsigned long long);
+    cudaFuncSetAttribute(topk_radix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    topk_radix_kernel<<<(unsigned)groups, TOPK_THREADS, smem, st>>>(mass, (int)nb, (int)budget, selected);
+    count_launch();
+    return check_launch("topk_radix_kernel");
+  }
   int pow2 = 1;
   while (pow2 < nb) pow2 <<= 1;
   const size_t smem = (size_t)pow2 * (sizeof(double) + sizeof(int)) + (size_t)(nb + 1) * sizeof(int);
