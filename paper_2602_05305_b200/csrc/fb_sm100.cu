@@ -299,12 +299,9 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, r);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-        }
+        for (int c = 0; c < BN / 32; ++c)  // all four loads in flight, one wait
+          ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, reinterpret_cast<uint32_t*>(s) + c * 32);
+        ptx::tmem_wait_ld();
         if constexpr (!GATHER) {
           const int valid = ke - (kb + t * BN);
           if (valid < BN) {
@@ -338,9 +335,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             }
           }
         }
-        float mx = s[0];
+        // row max and row sum as 8 independent chains (one softmax warp per
+        // SMSP: latency, not throughput, bounds this loop)
+        float mx8[8];
 #pragma unroll
-        for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
+        for (int k = 0; k < 8; ++k) mx8[k] = s[k];
+#pragma unroll
+        for (int i = 8; i < BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float m_new = fmaxf(m_used, mx * scale_log2);
         const bool need = m_new > m_used + RESCALE_THRESHOLD;
         if (__any_sync(0xffffffffu, need)) {
@@ -364,19 +367,19 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           m_used = m_new;
         }
         const float neg = -m_used;
-        float lsum = 0.f;
+        float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < BN / 64; ++c) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float p0 = ptx::ex2(fmaf(s[c * 64 + 2 * i], scale_log2, neg));
             const float p1 = ptx::ex2(fmaf(s[c * 64 + 2 * i + 1], scale_log2, neg));
-            lsum += p0 + p1;
+            ls8[i & 7] += p0 + p1;
             r[i] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
         }
-        l += lsum;
+        l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bar->p_ready[j & 1]);
@@ -625,28 +628,31 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < HALF / 32; ++c) {
-          ptx::tmem_ld32(tmem + lane_off + (j & 1) * 128 + wg * HALF + c * 32, r);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-        }
+        for (int c = 0; c < HALF / 32; ++c)
+          ptx::tmem_ld32(tmem + lane_off + (j & 1) * 128 + wg * HALF + c * 32,
+                         reinterpret_cast<uint32_t*>(s) + c * 32);
+        ptx::tmem_wait_ld();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bar->s_free[j & 1]);
         const bool ext = lt < ext_tiles;
         const int valid = (ext ? n_ext - lt * BN : n_in - (lt - ext_tiles) * BN) - wg * HALF;
         if constexpr (!MASS) {
-          float mx = -INFINITY;
+          float mx8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
 #pragma unroll
           for (int i = 0; i < HALF; ++i) {
             if (i >= valid) s[i] = -INFINITY;
-            mx = fmaxf(mx, s[i]);
+            mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
           }
+          const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
           const float m_new = fmaxf(m, mx * scale_log2);
           if (m_new != -INFINITY) {  // a half tile may be fully masked
-            float acc = 0.f;
+            float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int i = 0; i < HALF; ++i) acc += ptx::ex2(fmaf(s[i], scale_log2, -m_new));
+            for (int i = 0; i < HALF; ++i) a8[i & 7] += ptx::ex2(fmaf(s[i], scale_log2, -m_new));
+            const float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
             l = l * ptx::ex2(m - m_new) + acc;
             m = m_new;
           }
@@ -656,13 +662,13 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
           float a[4];
 #pragma unroll
           for (int bi = 0; bi < 4; ++bi) {
-            float acc = 0.f;
+            float p4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int c = bi * 16 + i;
-              acc += (c < valid && live) ? ptx::ex2(fmaf(s[c], scale_log2, -lse2)) : 0.f;
+              p4[i & 3] += (c < valid && live) ? ptx::ex2(fmaf(s[c], scale_log2, -lse2)) : 0.f;
             }
-            a[bi] = acc;
+            a[bi] = (p4[0] + p4[1]) + (p4[2] + p4[3]);
           }
           const bool b4 = lane & 16, b3 = lane & 8;
           const float r0 = __shfl_xor_sync(0xffffffffu, b4 ? a[0] : a[2], 16);
