@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <math.h>
 #include <string>
+#include <utility>
 
 #include "../../include/flashblock_b200.h"
 
@@ -70,6 +71,27 @@ inline int num_sms() {
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while the previous kernel on the stream finishes; kernels launched this way
+// call griddepcontrol.wait before reading global inputs.  FB_NO_PDL=1 in the
+// environment disables it (diagnostics).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Precision-mode type bundles (see flashblock_b200.h).
 struct ModeF64 { using Tin = double; using Ts = double; using Ta = double; using To = double; using Tl = double; };

@@ -145,6 +145,8 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
+  ptx::pdl_wait();               // inputs of this launch are final from here on
+  ptx::pdl_launch_dependents();  // let the next kernel's prologue start
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -442,6 +444,8 @@ __global__ void __launch_bounds__(256)
 refresh_merge_kernel(Sched sc, int ctas, int q_rows, int D, const float* __restrict__ ws_o,
                      const float* __restrict__ ws_l, float* __restrict__ o_out,
                      float* __restrict__ lse_out) {
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // item*BM + row
   const int lane = threadIdx.x & 31;
   const long long item = gw / BM;
@@ -545,6 +549,8 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -727,6 +733,8 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
 
 __global__ void score_lse_merge_kernel(Sched sc, int ctas, int q_rows, const float* __restrict__ ws_l,
                                        float* __restrict__ lse2_out) {
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
   const long long gr = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // item*BM + row
   const long long item = gr / BM;
   const int row = (int)(gr % BM);
@@ -878,15 +886,15 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   }
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  kern<<<(unsigned)p.ctas, sm100::THREADS, C::SMEM, st>>>(mq, mk, mv, mki, mvi, ga, sc, (int)q_rows, (int)key_begin,
-                                                         (int)key_end, scale_log2, o_out, lse_out,
-                                                         ws_o, ws_l, g_trace);
+  launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
+             sc, (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l,
+             g_trace);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
   if (p.T / p.ctas >= p.tpi && p.T % p.ctas == 0) return FB_OK;  // every item in one CTA
   const long long warps = items * sm100::BM;
-  sm100::refresh_merge_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
-      sc, p.ctas, (int)q_rows, D, ws_o, ws_l, o_out, lse_out);
+  launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
+             p.ctas, (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out);
   count_launch();
   return check_launch("refresh_merge_kernel(sm100)");
 }
@@ -969,23 +977,24 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   RefreshPlan p = plan_refresh(groups, q_rows, 0, (int64_t)(ext_tiles + in_tiles) * 128);
   if (ws_bytes < lse_bytes + p.ws_bytes) return fail(FB_ERR_VALUE, "score workspace too small");
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
-  sm100::score_kernel<D, false><<<(unsigned)p.ctas, sm100::SCORE_THREADS, C::SMEM, st>>>(
-      mq, mk, mki, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2, nullptr, lse2, ws_l,
-      nullptr, (int)nb);
+  launch_pdl(sm100::score_kernel<D, false>, dim3((unsigned)p.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
+             st, mq, mk, mki, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
+             (const float*)nullptr, lse2, ws_l, (double*)nullptr, (int)nb);
   count_launch();
   if ((rc = check_launch("score_kernel<lse>"))) return rc;
   if (!(p.T / p.ctas >= p.tpi && p.T % p.ctas == 0)) {
     const long long rows = groups * p.m_tiles * (long long)sm100::BM;
-    sm100::score_lse_merge_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(sc, p.ctas, (int)q_rows, ws_l, lse2);
+    launch_pdl(sm100::score_lse_merge_kernel, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, st, sc,
+               p.ctas, (int)q_rows, (const float*)ws_l, lse2);
     count_launch();
     if ((rc = check_launch("score_lse_merge_kernel"))) return rc;
   }
   // MASS pass over the external keys
   RefreshPlan pm = plan_refresh(groups, q_rows, 0, (int64_t)ext_tiles * 128);
   sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.maxseg};
-  sm100::score_kernel<D, true><<<(unsigned)pm.ctas, sm100::SCORE_THREADS, C::SMEM, st>>>(
-      mq, mk, mki, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2, lse2, nullptr,
-      nullptr, mass, (int)nb);
+  launch_pdl(sm100::score_kernel<D, true>, dim3((unsigned)pm.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
+             st, mq, mk, mki, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
+             (const float*)lse2, (float*)nullptr, (float*)nullptr, mass, (int)nb);
   count_launch();
   return check_launch("score_kernel<mass>");
 }

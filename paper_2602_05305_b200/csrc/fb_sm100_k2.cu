@@ -91,6 +91,8 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
+  ptx::pdl_wait();               // inputs of this launch are final from here on
+  ptx::pdl_launch_dependents();
 
   if (warp == 4) {
     if (lane == 0) {
@@ -290,9 +292,9 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   }
   const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  kern<<<(unsigned)(groups * m_tiles * C::SPLIT), sm100k2::THREADS, C::SMEM, st>>>(
-      mq, mk, mv, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
-      lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty));
+  launch_pdl(kern, dim3((unsigned)(groups * m_tiles * C::SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st,
+             mq, mk, mv, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
+             out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty));
   count_launch();
   return check_launch("internal_merge_kernel(sm100)");
 }
