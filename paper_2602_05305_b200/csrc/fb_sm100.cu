@@ -821,7 +821,11 @@ static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim
   return p;
 }
 
-void set_refresh_trace(void* p) { g_trace = reinterpret_cast<unsigned long long*>(p); }
+static int g_trace_launch = 0;  // successive launches stamp successive 148x8 slabs
+void set_refresh_trace(void* p) {
+  g_trace = reinterpret_cast<unsigned long long*>(p);
+  g_trace_launch = 0;
+}
 
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
   if (n_keys <= 0 || groups <= 0 || q_rows <= 0) return 0;
@@ -888,7 +892,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
              sc, (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l,
-             g_trace);
+             g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
   if (p.T / p.ctas >= p.tpi && p.T % p.ctas == 0) return FB_OK;  // every item in one CTA
