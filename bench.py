@@ -458,6 +458,74 @@ def run_e2e(args, eng, kc, vc, dev, sched, world):
                     "host wall clock"}
 
 
+def run_splitkv(args, rank: int, world: int, local_rank: int):
+    """C3: 128K context whose committed KV is split along the sequence over the
+    `world` ranks (strong scaling: the same b sequences on every rank count).
+    Per layer and block: refresh = K1 on the local shard -> ONE all_to_all of
+    the fp32 (O, LSE) partials -> K3 merge for this rank's kv-head shard -> K2;
+    31 cached steps = K2 on the head shard only (no KV, no exchange)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_05305_b200 import kernels as K
+    from paper_2602_05305_b200.splitkv import SplitKVRefresh, group_chunks, shard_bounds
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    b, N, L = args.batch, args.ctx, args.layers
+    groups, rows = b * HKV, (HQ // HKV) * BLK
+    lo, hi = shard_bounds(N, world, rank)
+    n_loc = hi - lo
+    g0, g1 = group_chunks(groups, world)[rank]
+    gen = torch.Generator(device=dev).manual_seed(99 + rank)
+    rnd = lambda *sh: torch.randn(sh, device=dev, generator=gen).to(torch.bfloat16)
+    kc = [rnd(groups, max(n_loc, 1), D) for _ in range(L)]
+    vc = [rnd(groups, max(n_loc, 1), D) for _ in range(L)]
+    q = [rnd(groups, rows, D) for _ in range(L)]
+    ki = [rnd(groups, BLK, D) for _ in range(L)]
+    vi = [rnd(groups, BLK, D) for _ in range(L)]
+    out = torch.empty((g1 - g0, rows, D), device=dev, dtype=torch.bfloat16)
+    ext = [None] * L
+    refresh = SplitKVRefresh(layout="all_to_all" if world > 1 else "all_gather")
+
+    def block():
+        for s in range(STEPS_PER_BLOCK):
+            for l in range(L):
+                if s == 0:
+                    ext[l] = refresh(q[l], kc[l], vc[l], n_loc)
+                o_e, l_e = ext[l]
+                K.internal_merge(q[l][g0:g1], ki[l][g0:g1], vi[l][g0:g1], o_e, l_e,
+                                 out_dtype=torch.bfloat16, out=out)
+
+    for _ in range(args.warmup):
+        block()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        block()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        value = b * BLK * args.steps / (ms / 1000.0)
+        print(json.dumps({
+            "metric": "block-diffusion tokens/s (FlashBlock attention, C3: 128K ctx split-KV)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "C3 split-KV refresh + head-sharded cached steps (eager launches)",
+                       "layers": L, "batch": b, "ctx": N, "shard_rows": n_loc,
+                       "exchange": "all_to_all of fp32 (O, LSE) partials, once per layer per block"}}),
+              flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -466,6 +534,10 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--mode", default="flashblock", choices=["flashblock", "splitkv"],
+                    help="flashblock: C2 headline (default); splitkv: C3 128K split-KV over ranks")
+    ap.add_argument("--ctx", type=int, default=131072, help="context for --mode splitkv")
+    ap.add_argument("--layers", type=int, default=8, help="layers for --mode splitkv")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -482,7 +554,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.mode == "splitkv":
+            run_splitkv(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
