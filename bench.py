@@ -208,7 +208,7 @@ def _config(args):
             "layers": LAYERS, "batch_per_gpu": args.batch, "q_heads": HQ, "kv_heads": HKV,
             "head_dim": D, "block": BLK, "ctx": CTX, "steps_per_block": STEPS_PER_BLOCK,
             "unmask_per_step": UNMASK_PER_STEP, "tau": TAU,
-            "l2": "inputs larger than L2 (distinct KV per layer, 1.07 GB/layer at b=8)"}
+            "l2": "inputs larger than L2 (distinct KV cache per layer: 2.15 GB/layer at b=16)"}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -531,7 +531,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--mode", default="flashblock", choices=["flashblock", "splitkv"],

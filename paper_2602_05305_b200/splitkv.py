@@ -81,8 +81,8 @@ class SplitKVRefresh:
         """q [groups, rows, d]; k/v_shard [groups, cap_local, d] with this rank's
         n_local committed rows.  Returns (o, lse): all groups for all_gather,
         this rank's group chunk for all_to_all."""
-        world = dist.get_world_size(self.group)
-        rank = dist.get_rank(self.group)
+        on = dist.is_available() and dist.is_initialized()
+        world = dist.get_world_size(self.group) if on else 1
         o, l = self.local_partial(q, k_shard, v_shard, n_local, scale)
         groups = o.shape[0]
         if world == 1:

@@ -101,3 +101,14 @@ def test_split_kv_world2_gloo_matches_single_process(layout, n):
         assert p.exitcode == 0
     errs = dict(q.get(timeout=10) for _ in range(2))
     assert max(errs.values()) < 1e-12, errs
+
+
+def test_split_kv_single_process_without_group():
+    # no process group: the refresh is the local partial (world size 1)
+    rng = np.random.Generator(np.random.Philox(5))
+    q = torch.from_numpy(rng.standard_normal((2, 3, 8)))
+    k = torch.from_numpy(rng.standard_normal((2, 10, 8)))
+    v = torch.from_numpy(rng.standard_normal((2, 10, 8)))
+    o, l = SplitKVRefresh(local_partial=_oracle_partial, combine=_oracle_combine)(q, k, v, 10)
+    full = orc.partial(q[1].numpy(), k[1].numpy(), v[1].numpy())
+    np.testing.assert_allclose(o[1].numpy(), full.out, atol=1e-13)
