@@ -88,6 +88,33 @@ FB_API int fb_attention_partial(int dtype, const void* q, const void* k, const v
                          double scale, void* o_out, void* lse_out,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* K1 over per-sequence (ragged) context lengths -- the serving layout where
+ * each sequence of the batch has its own committed length.
+ * Group g streams rows [key_begin, min(key_end[g], kv_rows_cap)) of its slab;
+ * key_end is a DEVICE int32 array [groups].  Rows past a group's end are never
+ * used (scores masked, V rows zeroed in shared memory), even if the slab holds
+ * uninitialised memory there; groups with no keys get the empty sentinel.
+ * Same outputs and partial types as fb_attention_partial. */
+FB_API int fb_attention_partial_ragged(int dtype, const void* q, const void* k, const void* v,
+                                       int64_t groups, int64_t q_rows, int64_t head_dim,
+                                       int64_t kv_rows_cap, int64_t key_begin,
+                                       const int32_t* key_end, double scale, void* o_out,
+                                       void* lse_out, void* workspace, size_t workspace_bytes,
+                                       void* stream);
+FB_API size_t fb_ragged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
+                                        int64_t head_dim, int64_t kv_rows_cap);
+
+/* Device-side block commit (kv_cache.py:121-144; simulator.py:327-333):
+ * append a finished block's K/V rows ([groups, block_rows, head_dim]) to each
+ * group's slab at row lengths[g] (device int32 [groups]), then advance
+ * lengths[g] by block_rows.  Rows past kv_rows_cap are dropped and counted in
+ * *overflow (device int32, optional).  The caller invalidates its cached
+ * external partials afterwards (attention.py:287-289). */
+FB_API int fb_commit_block(int dtype, void* k_cache, void* v_cache, int64_t groups,
+                           int64_t kv_rows_cap, int64_t head_dim, const void* k_block,
+                           const void* v_block, int64_t block_rows, int32_t* lengths,
+                           int32_t* overflow, void* stream);
+
 /* K2 -- cached step: block-internal partial fused with the log-space merge
  * against the cached external partial.
  * Replaces attention_with_reuse (attention.py:295-321) = attention_partial on

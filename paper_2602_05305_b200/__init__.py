@@ -10,7 +10,7 @@ from .attention import (AttnPartial, CacheEntry, DegenerateInputError, ExternalA
                         ReusePreconditionError, attention_dense, attention_partial,
                         attention_streamed, attention_with_reuse, combine_partials,
                         merge_partials)
-from .engine import FlashBlockAttention
+from .engine import FlashBlockAttention, KVCache
 from .errors import BoundsError, ShapeError, StalenessError
 from .policy import (MODES, Decision, ReuseConfig, count_updated_tokens, decide,
                      refresh_schedule, unmask_schedule)
@@ -21,7 +21,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AttnPartial", "CacheEntry", "DegenerateInputError", "ExternalAttnCache",
     "ReusePreconditionError", "attention_dense", "attention_partial", "attention_streamed",
-    "attention_with_reuse", "combine_partials", "merge_partials", "FlashBlockAttention",
+    "attention_with_reuse", "combine_partials", "merge_partials", "FlashBlockAttention", "KVCache",
     "BoundsError", "ShapeError", "StalenessError", "MODES", "Decision", "ReuseConfig",
     "count_updated_tokens", "decide", "refresh_schedule", "unmask_schedule", "SparseMask",
     "build_sparse_mask", "sparse_attention_with_residual",

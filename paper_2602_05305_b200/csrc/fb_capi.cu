@@ -351,6 +351,48 @@ static int sparse_attend_t(const void* qv, const void* kv, const void* vv, const
                                                 d, int64_t(1) << 40, 1, scale, nullptr, nullptr, mo, st);
 }
 
+template <typename Mode>
+static int attention_partial_ragged_t(const void* qv, const void* kv, const void* vv, int64_t groups,
+                                      int64_t q_rows, int64_t d, int64_t cap, int64_t kb,
+                                      const int32_t* ends, double scale, void* o_out, void* lse_out,
+                                      void* ws, size_t ws_bytes, cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  auto* q = reinterpret_cast<const Tin*>(qv);
+  auto* k = reinterpret_cast<const Tin*>(kv);
+  auto* v = reinterpret_cast<const Tin*>(vv);
+  auto* o = reinterpret_cast<typename Mode::To*>(o_out);
+  auto* l = reinterpret_cast<typename Mode::Tl*>(lse_out);
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (sm100_supported(d) && cap < (int64_t(1) << 31) &&
+        ws_bytes >= refresh_sm100_ragged_workspace_bytes(groups, q_rows, d))
+      return launch_refresh_ragged_sm100(q, k, v, groups, q_rows, d, cap, kb, ends, scale, o, l, ws,
+                                         ws_bytes, st);
+  }
+  // SIMT: one split per group (lengths live on the device)
+  RaggedMap<Tin> map{k, v, ends, cap * d, kb, cap, d};
+  MergeOut<Mode> none{};
+  using Ta = typename Mode::Ta;
+  constexpr bool direct_ok = std::is_same<Ta, typename Mode::To>::value &&
+                             std::is_same<Ta, typename Mode::Tl>::value;
+  if constexpr (direct_ok) {
+    return launch_partial_simt<Mode, false, false>(q, map, groups, q_rows, d, int64_t(1) << 40, 1,
+                                                   scale, reinterpret_cast<Ta*>(o),
+                                                   reinterpret_cast<typename Mode::Tl*>(l), none, st);
+  } else {
+    const int64_t rows = groups * q_rows;
+    if (ws == nullptr || ws_bytes < split_bytes<Mode>(rows, d))
+      return fail(FB_ERR_VALUE, "workspace too small (fb_ragged_workspace_bytes)");
+    Ta* wo = reinterpret_cast<Ta*>(ws);
+    int rc = launch_partial_simt<Mode, false, false>(q, map, groups, q_rows, d, int64_t(1) << 40, 1,
+                                                     scale, wo,
+                                                     reinterpret_cast<typename Mode::Tl*>(wo + rows * d),
+                                                     none, st);
+    if (rc) return rc;
+    return launch_combine<Ta, Ta, Ta, typename Mode::To, typename Mode::Tl>(
+        strided_list<Mode>(ws, 1, rows, d), rows, d, o, l, nullptr, st);
+  }
+}
+
 }  // namespace fb
 
 using namespace fb;
@@ -402,6 +444,59 @@ int fb_attention_partial(int dtype, const void* q, const void* k, const void* v,
     default:
       return attention_partial_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, key_begin,
                                            key_end, scale, o_out, lse_out, workspace, workspace_bytes, st);
+  }
+}
+
+int fb_commit_block(int dtype, void* k_cache, void* v_cache, int64_t groups, int64_t kv_rows_cap,
+                    int64_t head_dim, const void* k_block, const void* v_block, int64_t block_rows,
+                    int32_t* lengths, int32_t* overflow, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || kv_rows_cap < 0 || head_dim < 1 || block_rows < 0)
+    return fail(FB_ERR_SHAPE, "bad extents");
+  if (block_rows == 0) return fail(FB_ERR_SHAPE, "a block commit needs at least one row");
+  if (lengths == nullptr) return fail(FB_ERR_VALUE, "lengths (device int32 [groups]) is required");
+  return launch_commit_block(k_cache, v_cache, k_block, v_block, groups, kv_rows_cap,
+                             head_dim * (int64_t)dtype_size(dtype), block_rows, lengths, overflow,
+                             as_stream(stream));
+}
+
+size_t fb_ragged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,
+                                 int64_t kv_rows_cap) {
+  (void)kv_rows_cap;
+  if (groups <= 0 || q_rows <= 0) return 0;
+  const int64_t rows = groups * q_rows;
+  size_t b = (size_t)rows * (head_dim + 1) * (dtype == FB_BF16 ? 4 : 8) + 256;
+  if (dtype == FB_BF16 && sm100_supported(head_dim))
+    b = std::max(b, refresh_sm100_ragged_workspace_bytes(groups, q_rows, head_dim));
+  return b;
+}
+
+int fb_attention_partial_ragged(int dtype, const void* q, const void* k, const void* v,
+                                int64_t groups, int64_t q_rows, int64_t head_dim,
+                                int64_t kv_rows_cap, int64_t key_begin, const int32_t* key_end,
+                                double scale, void* o_out, void* lse_out, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0)
+    return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (key_begin < 0 || key_begin > kv_rows_cap) return fail(FB_ERR_BOUNDS, "key_begin outside the slab");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  if (key_end == nullptr) return fail(FB_ERR_VALUE, "key_end (device int32 [groups]) is required");
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return attention_partial_ragged_t<ModeF64>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
+                                                 key_begin, key_end, scale, o_out, lse_out,
+                                                 workspace, workspace_bytes, st);
+    case FB_F32:
+      return attention_partial_ragged_t<ModeF32>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
+                                                 key_begin, key_end, scale, o_out, lse_out,
+                                                 workspace, workspace_bytes, st);
+    default:
+      return attention_partial_ragged_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
+                                                  key_begin, key_end, scale, o_out, lse_out,
+                                                  workspace, workspace_bytes, st);
   }
 }
 

@@ -46,6 +46,9 @@ int launch_block_mass(const typename Mode::Tin* q, const typename Mode::Tin* k,
                       const double* row_lse, int64_t groups, int64_t q_rows, int64_t head_dim,
                       int64_t slab_stride, int64_t n_ext, int64_t kbs, double scale, double* mass,
                       cudaStream_t st);
+int launch_commit_block(void* kc, void* vc, const void* kb, const void* vb, int64_t groups,
+                        int64_t cap, int64_t row_bytes, int64_t blk_rows, int32_t* len,
+                        int32_t* overflow, cudaStream_t st);
 int launch_complement(const int32_t* sel, int64_t groups, int64_t n_sel, int64_t nb, int32_t* out,
                       cudaStream_t st);
 int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, int32_t* selected,
@@ -66,6 +69,14 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
                          float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// Ragged per-group key ends (device int32 [groups], clamped to kv_rows_cap).
+size_t refresh_sm100_ragged_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim);
+int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                                const __nv_bfloat16* v, int64_t groups, int64_t q_rows,
+                                int64_t head_dim, int64_t kv_rows_cap, int64_t key_begin,
+                                const int32_t* key_end, double scale, float* o_out, float* lse_out,
+                                void* ws, size_t ws_bytes, cudaStream_t st);
 
 // Gathered variant (sparse K7/K8): keys = mask-selected 16-row blocks of the
 // cache (list [groups, n_list] of ascending block ids, rows clipped at n_ext)

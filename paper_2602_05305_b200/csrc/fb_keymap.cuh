@@ -29,6 +29,26 @@ struct RangeMap {
   }
 };
 
+// Per-sequence (ragged) committed lengths: group g attends slab rows
+// [begin, min(ends[g], cap)) -- the serving layout where every sequence of the
+// batch has its own context length.
+template <typename T>
+struct RaggedMap {
+  const T* k;
+  const T* v;
+  const int32_t* ends;  // device [groups]
+  int64_t slab_stride, begin, cap, d;
+  __device__ __forceinline__ int64_t count(int64_t g) const {
+    const int64_t e = min((int64_t)ends[g], cap);
+    return e > begin ? e - begin : 0;
+  }
+  __device__ __forceinline__ void row(int64_t g, int64_t t, const T*& kr, const T*& vr) const {
+    const int64_t off = g * slab_stride + (begin + t) * d;
+    kr = k + off;
+    vr = v + off;
+  }
+};
+
 // Committed rows [0, n_ext) of the slab, then the n_in current-block rows of
 // a separate [groups, n_in, d] tensor: the full key stream of a step
 // (simulator.py:425-429) without materialising the concatenation.

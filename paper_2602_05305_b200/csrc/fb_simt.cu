@@ -334,6 +334,10 @@ static bool map_vec_ok(const RangeMap<T>& m, const T* q, int64_t d) {
   return rows_ok(q, d) && al16(m.k) && al16(m.v);
 }
 template <typename T>
+static bool map_vec_ok(const RaggedMap<T>& m, const T* q, int64_t d) {
+  return rows_ok(q, d) && al16(m.k) && al16(m.v);
+}
+template <typename T>
 static bool map_vec_ok(const ConcatMap<T>& m, const T* q, int64_t d) {
   return rows_ok(q, d) && al16(m.k) && al16(m.k_in) && (m.v == nullptr || al16(m.v)) &&
          (m.v_in == nullptr || al16(m.v_in));
@@ -414,6 +418,7 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 
 #define FB_INST_MODE(MODE)                  \
   FB_INST_PARTIAL(MODE, false, RangeMap)    \
+  FB_INST_PARTIAL(MODE, false, RaggedMap)   \
   FB_INST_PARTIAL(MODE, true, RangeMap)     \
   FB_INST_PARTIAL(MODE, false, SelectedMap) \
   FB_INST_PARTIAL(MODE, true, SelectedMap)  \

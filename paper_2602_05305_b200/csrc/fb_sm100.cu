@@ -64,18 +64,47 @@ struct Barriers {
 };
 
 // Stream-K schedule: the flattened (item, key tile) space of T tiles is cut
-// into gridDim.x equal contiguous ranges, one per CTA (one CTA per SM), so
-// every SM streams the same number of KV bytes whatever b*Hkv is.  A CTA's
-// range covers one or more "segments" (the part of one item inside it).
+// into `ctas` equal contiguous ranges, one per CTA (one CTA per SM), so every
+// SM streams the same number of KV bytes whatever b*Hkv is.  A CTA's range
+// covers one or more "segments" (the part of one item inside it).  Items
+// have a uniform tile count (tpi) or, for ragged per-sequence context
+// lengths, tile offsets `prefix[items+1]` in device memory (T = prefix[items]).
+// Only a CTA's first and last segment can belong to an item that other CTAs
+// share, so split partials need just two workspace slots per CTA.
 struct Sched {
-  long long T;      // total tiles
-  int tpi;          // tiles per item
-  int m_tiles;      // 128-row query tiles per group
-  int maxseg;       // workspace slots per item
-  __device__ __forceinline__ long long start(int c) const { return (long long)c * T / gridDim.x; }
+  long long T;             // total tiles (ragged: filled in-kernel from prefix)
+  int tpi;                 // tiles per item (uniform)
+  int m_tiles;             // 128-row query tiles per group
+  int items;
+  int ctas;
+  const long long* prefix; // ragged item offsets, or nullptr
+  __device__ __forceinline__ void resolve() {
+    if (prefix != nullptr) T = prefix[items];
+  }
+  __device__ __forceinline__ long long start(int c) const { return (long long)c * T / ctas; }
   // largest c with start(c) <= x
   __device__ __forceinline__ int cta_of(long long x) const {
-    return (int)(((x + 1) * gridDim.x - 1) / T);
+    return (int)(((x + 1) * ctas - 1) / T);
+  }
+  __device__ __forceinline__ long long item_begin(int i) const {
+    return prefix ? prefix[i] : (long long)i * tpi;
+  }
+  __device__ __forceinline__ long long item_end(int i) const {
+    return prefix ? prefix[i + 1] : (long long)(i + 1) * tpi;
+  }
+  // item holding tile t (ragged: last i with prefix[i] <= t, skipping empty items)
+  __device__ __forceinline__ int item_of(long long t) const {
+    if (prefix == nullptr) return (int)(t / tpi);
+    int lo = 0, hi = items;  // prefix[lo] <= t < prefix[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (prefix[mid] <= t) lo = mid; else hi = mid;
+    }
+    return lo;
+  }
+  // workspace slot of item i's segment inside CTA c
+  __device__ __forceinline__ long long slot(int c, int i) const {
+    return 2ll * c + (item_begin(i) <= start(c) ? 0 : 1);
   }
 };
 
@@ -96,7 +125,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ki,
                const __grid_constant__ CUtensorMap tm_vi, Gather ga, Sched sc, int q_rows, int key_begin,
-               int key_end, float scale_log2, float* __restrict__ o_out,
+               int key_end, const int* __restrict__ key_len, float scale_log2, float* __restrict__ o_out,
                float* __restrict__ lse_out, float* __restrict__ ws_o,
                float* __restrict__ ws_l, unsigned long long* __restrict__ trace) {
   using C = Cfg<D>;
@@ -107,6 +136,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  sc.resolve();
   const long long t_begin = sc.start(blockIdx.x);
   const long long t_end = sc.start(blockIdx.x + 1);
   // diagnostics (FB_REFRESH_TRACE): globaltimer at start / per-segment stream end / merge end
@@ -155,8 +185,9 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const uint64_t stream = ptx::policy_evict_first();
       int j = 0, seg = 0;
       for (long long t = t_begin; t < t_end; ++seg) {
-        const int item = (int)(t / sc.tpi);
-        const long long seg_end = min(t_end, (long long)(item + 1) * sc.tpi);
+        const int item = sc.item_of(t);
+        const long long ib = sc.item_begin(item);
+        const long long seg_end = min(t_end, sc.item_end(item));
         const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
         if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
         ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
@@ -166,7 +197,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         for (; t < seg_end; ++t, ++j) {
           const int s = j % C::STAGES;
           const uint32_t ph = (j / C::STAGES) & 1;
-          const int lt = (int)(t - (long long)item * sc.tpi);
+          const int lt = (int)(t - ib);
           if constexpr (!GATHER) {
             const int row = key_begin + lt * BN;
             ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
@@ -224,8 +255,13 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
       int jg = 0, seg = 0;
       for (long long t0 = t_begin; t0 < t_end; ++seg) {
-        const int item = (int)(t0 / sc.tpi);
-        const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+        const int item = sc.item_of(t0);
+        const int n = (int)(min(t_end, sc.item_end(item)) - t0);
+        // ragged contexts: V rows past the sequence end are zeroed in smem before
+        // P V (masked P is 0, but 0 * NaN from uninitialised cache rows is not)
+        const int v_valid_last = key_len ? min(key_len[item / sc.m_tiles], key_end) - key_begin -
+                                               (int)(t0 + n - 1 - sc.item_begin(item)) * BN
+                                         : BN;
         ptx::mbar_wait(&bar->q_full, seg & 1);
         ptx::tc_fence_after();
         for (int t = 0; t <= n; ++t) {
@@ -253,6 +289,13 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             ptx::mbar_wait(&bar->p_ready[jj & 1], (jj >> 1) & 1);
             ptx::mbar_wait(&bar->v_full[s], (jj / C::STAGES) & 1);
             if (t == 1 && seg > 0) ptx::mbar_wait(&bar->o_empty, (seg - 1) & 1);  // O drained
+            if (t == n && v_valid_last < BN) {
+              unsigned char* vt = smem + C::OFF_V + s * C::TILE_BYTES;
+              for (int b = 0; b < C::NBOX; ++b)
+                for (int off = max(v_valid_last, 0) * 128; off < BN * 128; off += 16)
+                  *reinterpret_cast<uint4*>(vt + b * C::BOX_BYTES + off) = make_uint4(0, 0, 0, 0);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
             ptx::tc_fence_after();
             const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V + s * C::TILE_BYTES);
             const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
@@ -281,11 +324,12 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     float s[BN];
     int jg = 0, seg = 0;
     for (long long t0 = t_begin; t0 < t_end; ++seg) {
-      const int item = (int)(t0 / sc.tpi);
-      const int lt0 = (int)(t0 - (long long)item * sc.tpi);
-      const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+      const int item = sc.item_of(t0);
+      const long long ib = sc.item_begin(item);
+      const int lt0 = (int)(t0 - ib);
+      const int n = (int)(min(t_end, sc.item_end(item)) - t0);
       const int kb = key_begin + lt0 * BN;
-      const int ke = min(kb + n * BN, key_end);
+      const int ke = min(kb + n * BN, key_len ? min(key_len[item / sc.m_tiles], key_end) : key_end);
       float m_used = -INFINITY;  // running max, log2-scaled
       float l = 0.f;
       int last_rows = 16;  // valid rows of the list's last block (gather mode)
@@ -391,8 +435,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (row == 0) stamp(1 + 2 * (seg & 1));
 
       // ---------------------------------------------------------- segment epilogue
-      const int c_first = sc.cta_of((long long)item * sc.tpi);
-      const int nseg = sc.cta_of((long long)(item + 1) * sc.tpi - 1) - c_first + 1;
+      const bool whole = ib >= t_begin && sc.item_end(item) <= t_end;  // item not shared
       const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
       const int grow = mt * BM + row;
       const bool live = grow < q_rows;
@@ -400,10 +443,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const float inv = 1.f / l;
       const float lse = (m_used + log2f(l)) * 0.69314718055994530942f;
       float* dst;
-      if (nseg == 1) {
+      if (whole) {
         dst = live ? o_out + orow * D : nullptr;
       } else {
-        const long long slot = ((long long)item * sc.maxseg + (blockIdx.x - c_first)) * BM + row;
+        const long long slot = sc.slot(blockIdx.x, item) * BM + row;
         dst = ws_o + slot * D;
         ws_l[slot] = lse;
       }
@@ -423,7 +466,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
-      if (nseg == 1 && live) lse_out[orow] = lse;
+      if (whole && live) lse_out[orow] = lse;
       if (row == 0) stamp(2 + 2 * (seg & 1));
     }
   }
@@ -441,35 +484,44 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 // merged in segment order, so the result does not depend on CTA timing.
 // Same log-space merge as K3 (attention.py:207-233).
 __global__ void __launch_bounds__(256)
-refresh_merge_kernel(Sched sc, int ctas, int q_rows, int D, const float* __restrict__ ws_o,
+refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o,
                      const float* __restrict__ ws_l, float* __restrict__ o_out,
                      float* __restrict__ lse_out) {
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
+  sc.resolve();
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // item*BM + row
   const int lane = threadIdx.x & 31;
-  const long long item = gw / BM;
+  const int item = (int)(gw / BM);
   const int row = (int)(gw % BM);
-  if (item * sc.tpi >= sc.T) return;
-  auto cta_of = [&](long long x) { return (int)(((x + 1) * ctas - 1) / sc.T); };
-  const int c_first = cta_of(item * sc.tpi);
-  const int nseg = cta_of((item + 1) * sc.tpi - 1) - c_first + 1;
-  const int g = (int)(item / sc.m_tiles), mt = (int)(item % sc.m_tiles);
+  if (item >= sc.items) return;
+  const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
   const int grow = mt * BM + row;
-  if (nseg == 1 || grow >= q_rows) return;
-  const long long base = item * sc.maxseg * BM + row;  // slot k at base + k*BM
+  if (grow >= q_rows) return;
+  const long long orow = (long long)g * q_rows + grow;
+  const long long ib = sc.item_begin(item), ie = sc.item_end(item);
+  if (ib == ie) {  // no keys (ragged length 0): the empty partial
+    for (int c = lane; c < D; c += 32) o_out[orow * D + c] = 0.f;
+    if (lane == 0) lse_out[orow] = -INFINITY;
+    return;
+  }
+  const int c_first = sc.cta_of(ib);
+  const int c_last = sc.cta_of(ie - 1);
+  if (c_first == c_last) return;  // written whole by its CTA
+  const int nseg = c_last - c_first + 1;
   float mx = -INFINITY;
-  for (int k = lane; k < nseg; k += 32) mx = fmaxf(mx, ws_l[base + (long long)k * BM]);
+  for (int k = lane; k < nseg; k += 32)
+    mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * BM + row]);
   mx = warp_max(mx);
   float z = 0.f;
-  for (int k = lane; k < nseg; k += 32) z += __expf(ws_l[base + (long long)k * BM] - mx);
+  for (int k = lane; k < nseg; k += 32)
+    z += __expf(ws_l[sc.slot(c_first + k, item) * BM + row] - mx);
   z = warp_sum(z);
   const float iz = 1.f / z;
-  const long long orow = (long long)g * q_rows + grow;
   for (int c = lane * 4; c < D; c += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < nseg; ++k) {
-      const long long sl = base + (long long)k * BM;
+      const long long sl = sc.slot(c_first + k, item) * BM + row;
       const float w = __expf(ws_l[sl] - mx);
       const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
       acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
@@ -527,7 +579,7 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
   ScoreBars* bar = reinterpret_cast<ScoreBars*>(smem + C::OFF_BAR);
   double* red = reinterpret_cast<double*>(smem + C::OFF_RED);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long t_begin = sc.start(blockIdx.x), t_end = sc.start(blockIdx.x + 1);
+  const long long t_begin = sc.start(blockIdx.x), t_end = sc.start(blockIdx.x + 1);  // uniform items
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tm_q);
@@ -710,13 +762,12 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
           const float m1 = xch[row], l1 = xch[BM + row];
           const float mm = fmaxf(m, m1);
           const float lt = l * ptx::ex2(m - mm) + l1 * ptx::ex2(m1 - mm);
-          const int c_first = sc.cta_of((long long)item * sc.tpi);
-          const int nseg = sc.cta_of((long long)(item + 1) * sc.tpi - 1) - c_first + 1;
+          const bool whole = sc.item_begin(item) >= t_begin && sc.item_end(item) <= t_end;
           const float lse = mm + log2f(lt);
-          if (nseg == 1) {
+          if (whole) {
             if (live) lse2_out[orow] = lse;
           } else {
-            ws_l[((long long)item * sc.maxseg + (blockIdx.x - c_first)) * BM + row] = lse;
+            ws_l[sc.slot(blockIdx.x, item) * BM + row] = lse;
           }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -731,25 +782,23 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
   }
 }
 
-__global__ void score_lse_merge_kernel(Sched sc, int ctas, int q_rows, const float* __restrict__ ws_l,
+__global__ void score_lse_merge_kernel(Sched sc, int q_rows, const float* __restrict__ ws_l,
                                        float* __restrict__ lse2_out) {
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
   const long long gr = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // item*BM + row
-  const long long item = gr / BM;
+  const int item = (int)(gr / BM);
   const int row = (int)(gr % BM);
-  if (item * sc.tpi >= sc.T) return;
-  auto cta_of = [&](long long x) { return (int)(((x + 1) * ctas - 1) / sc.T); };
-  const int c_first = cta_of(item * sc.tpi);
-  const int nseg = cta_of((item + 1) * sc.tpi - 1) - c_first + 1;
-  const int g = (int)(item / sc.m_tiles), mt = (int)(item % sc.m_tiles);
+  if (item >= sc.items) return;
+  const int c_first = sc.cta_of(sc.item_begin(item));
+  const int c_last = sc.cta_of(sc.item_end(item) - 1);
+  const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
   const int grow = mt * BM + row;
-  if (nseg == 1 || grow >= q_rows) return;
-  const long long base = item * sc.maxseg * BM + row;
+  if (c_first == c_last || grow >= q_rows) return;
   float mx = -INFINITY;
-  for (int k = 0; k < nseg; ++k) mx = fmaxf(mx, ws_l[base + (long long)k * BM]);
+  for (int c = c_first; c <= c_last; ++c) mx = fmaxf(mx, ws_l[sc.slot(c, item) * BM + row]);
   float z = 0.f;
-  for (int k = 0; k < nseg; ++k) z += exp2f(ws_l[base + (long long)k * BM] - mx);
+  for (int c = c_first; c <= c_last; ++c) z += exp2f(ws_l[sc.slot(c, item) * BM + row] - mx);
   lse2_out[(long long)g * q_rows + grow] = mx + log2f(z);
 }
 
@@ -797,31 +846,31 @@ bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 12
 
 // diagnostics: per-CTA globaltimer stamps (set through fb_debug_set_trace)
 static unsigned long long* g_trace = nullptr;
+static int g_trace_launch = 0;  // successive launches stamp successive 148x8 slabs
 
 struct RefreshPlan {
-  int ctas, maxseg, tpi, m_tiles;
+  int ctas, tpi, m_tiles, items;
   long long T;
   size_t ws_bytes;
 };
 
+// Uniform items (every group has n_keys keys); ragged plans fill T on device.
 static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
   RefreshPlan p{};
   p.m_tiles = (int)((q_rows + sm100::BM - 1) / sm100::BM);
-  const long long items = groups * p.m_tiles;
+  p.items = (int)(groups * p.m_tiles);
   p.tpi = (int)((n_keys + sm100::BN - 1) / sm100::BN);
-  p.T = items * p.tpi;
-  p.ctas = (int)std::min<long long>(num_sms(), p.T);
+  p.T = (long long)p.items * p.tpi;
+  p.ctas = (int)std::max<long long>(1, std::min<long long>(num_sms(), p.T));
   if (const char* e = getenv("FB_REFRESH_CTAS")) {  // diagnostics: force the CTA count
     const long long want = atoll(e);
-    if (want > 0) p.ctas = (int)std::min<long long>(want, p.T);
+    if (want > 0) p.ctas = (int)std::max<long long>(1, std::min<long long>(want, p.T));
   }
-  const long long per = p.T / p.ctas;  // >= 1
-  p.maxseg = (int)std::min<long long>(p.ctas, (p.tpi + per - 1) / per + 1);
-  p.ws_bytes = (size_t)items * p.maxseg * sm100::BM * (head_dim + 1) * sizeof(float);
+  // two split-partial slots per CTA (its first and last segment)
+  p.ws_bytes = (size_t)2 * p.ctas * sm100::BM * (head_dim + 1) * sizeof(float);
   return p;
 }
 
-static int g_trace_launch = 0;  // successive launches stamp successive 148x8 slabs
 void set_refresh_trace(void* p) {
   g_trace = reinterpret_cast<unsigned long long*>(p);
   g_trace_launch = 0;
@@ -832,11 +881,54 @@ size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t hea
   return plan_refresh(groups, q_rows, head_dim, n_keys).ws_bytes;
 }
 
+// ragged: split slots for num_sms CTAs + the item offsets
+size_t refresh_sm100_ragged_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim) {
+  const int64_t items = groups * ((q_rows + sm100::BM - 1) / sm100::BM);
+  return align_up((size_t)(items + 1) * sizeof(long long), 256) +
+         (size_t)2 * num_sms() * sm100::BM * (head_dim + 1) * sizeof(float);
+}
+
+// Ragged contexts: item tile offsets prefix[items+1] from per-group key ends
+// (one CTA, chunked serial sums + a warp scan of the chunk totals).
+__global__ void ragged_prefix_kernel(const int* __restrict__ key_len, int items, int m_tiles,
+                                     int key_begin, int key_cap, long long* __restrict__ prefix) {
+  __shared__ long long part[1024];
+  __shared__ long long warp_sum_sh[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (items + nt - 1) / nt;
+  const int i0 = min(items, tid * per), i1 = min(items, i0 + per);
+  long long sum = 0;
+  for (int i = i0; i < i1; ++i)
+    sum += max(0, min(key_len[i / m_tiles], key_cap) - key_begin + sm100::BN - 1) / sm100::BN;
+  part[tid] = sum;
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of the 1024 chunk sums, 32 per lane
+    long long acc = 0;
+    for (int k = 0; k < 32; ++k) acc += part[tid * 32 + k];
+    long long inc = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (tid >= o) inc += y;
+    }
+    warp_sum_sh[tid] = inc - acc;
+  }
+  __syncthreads();
+  long long base = warp_sum_sh[tid / 32];
+  for (int k = (tid / 32) * 32; k < tid; ++k) base += part[k];
+  for (int i = i0; i < i1; ++i) {
+    prefix[i] = base;
+    base += max(0, min(key_len[i / m_tiles], key_cap) - key_begin + sm100::BN - 1) / sm100::BN;
+  }
+  if (i1 == items && i0 < i1) prefix[items] = base;
+  if (items == 0 && tid == 0) prefix[0] = 0;
+}
+
 template <int D, bool GATHER>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
                             int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
-                            size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr) {
+                            size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr,
+                            const int* key_len = nullptr) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
@@ -844,8 +936,11 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   int64_t tiles;
   if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100::BOX_COLS, sm100::BM))) return rc;
   if constexpr (!GATHER) {
-    if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
-    if ((rc = make_tmap_3d(&mv, v, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    // ragged: the whole slab is addressable; rows past each length are masked
+    // (scores) and zeroed in smem (V) in the kernel
+    const int64_t dim1 = key_len ? kv_rows_cap : key_end;
+    if ((rc = make_tmap_3d(&mk, k, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    if ((rc = make_tmap_3d(&mv, v, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
     mki = mk;
     mvi = mv;
     tiles = (key_end - key_begin + sm100::BN - 1) / sm100::BN;
@@ -874,31 +969,48 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
-  RefreshPlan p = plan_refresh(groups, q_rows, D, tiles * sm100::BN);
-  const long long items = groups * p.m_tiles;
-  if (ws == nullptr || ws_bytes < p.ws_bytes) {
-    // no room for split partials: one CTA per whole item (no split, no workspace)
-    p.ctas = (int)items;
-    p.maxseg = 1;
-    ws = nullptr;
-  }
+  RefreshPlan p = plan_refresh(groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
+  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};
   float* ws_o = nullptr;
   float* ws_l = nullptr;
-  if (ws != nullptr) {
-    ws_o = reinterpret_cast<float*>(ws);
-    ws_l = ws_o + (size_t)items * p.maxseg * sm100::BM * D;
+  bool need_merge;
+  if (key_len != nullptr) {
+    const size_t pre = align_up((size_t)(p.items + 1) * sizeof(long long), 256);
+    if (ws == nullptr || ws_bytes < refresh_sm100_ragged_workspace_bytes(groups, q_rows, D))
+      return fail(FB_ERR_VALUE, "ragged refresh needs fb_partial_workspace_bytes of scratch");
+    long long* prefix = reinterpret_cast<long long*>(ws);
+    ragged_prefix_kernel<<<1, 1024, 0, st>>>(key_len, p.items, p.m_tiles, (int)key_begin,
+                                             (int)key_end, prefix);
+    count_launch();
+    if ((rc = check_launch("ragged_prefix_kernel"))) return rc;
+    sc.prefix = prefix;
+    sc.tpi = 0;
+    sc.ctas = num_sms();
+    p.ctas = sc.ctas;
+    ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + pre);
+    ws_l = ws_o + (size_t)2 * sc.ctas * sm100::BM * D;
+    need_merge = true;
+  } else {
+    if (ws == nullptr || ws_bytes < p.ws_bytes) {
+      // no room for split partials: one CTA per whole item (no split, no workspace)
+      p.ctas = p.items;
+      sc.ctas = p.items;
+    } else {
+      ws_o = reinterpret_cast<float*>(ws);
+      ws_l = ws_o + (size_t)2 * p.ctas * sm100::BM * D;
+    }
+    need_merge = !(p.T % p.ctas == 0 && (p.T / p.ctas) % p.tpi == 0);  // items never split
   }
-  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
-             sc, (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l,
-             g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr);
+             sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
+             ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
-  if (p.T / p.ctas >= p.tpi && p.T % p.ctas == 0) return FB_OK;  // every item in one CTA
-  const long long warps = items * sm100::BM;
+  if (!need_merge) return FB_OK;
+  const long long warps = (long long)p.items * sm100::BM;
   launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
-             p.ctas, (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out);
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out);
   count_launch();
   return check_launch("refresh_merge_kernel(sm100)");
 }
@@ -913,6 +1025,20 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
                                        scale, o_out, lse_out, ws, ws_bytes, st);
+  return FB_ERR_UNSUPPORTED;
+}
+
+int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                                const __nv_bfloat16* v, int64_t groups, int64_t q_rows,
+                                int64_t head_dim, int64_t kv_rows_cap, int64_t key_begin,
+                                const int32_t* key_end, double scale, float* o_out, float* lse_out,
+                                void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (head_dim == 128)
+    return launch_refresh_d<128, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, kv_rows_cap,
+                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, key_end);
+  if (head_dim == 64)
+    return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, kv_rows_cap,
+                                       scale, o_out, lse_out, ws, ws_bytes, st, nullptr, key_end);
   return FB_ERR_UNSUPPORTED;
 }
 
@@ -980,22 +1106,22 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   // LSE pass over ext + internal keys
   RefreshPlan p = plan_refresh(groups, q_rows, 0, (int64_t)(ext_tiles + in_tiles) * 128);
   if (ws_bytes < lse_bytes + p.ws_bytes) return fail(FB_ERR_VALUE, "score workspace too small");
-  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.maxseg};
+  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};
   launch_pdl(sm100::score_kernel<D, false>, dim3((unsigned)p.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
              st, mq, mk, mki, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
              (const float*)nullptr, lse2, ws_l, (double*)nullptr, (int)nb);
   count_launch();
   if ((rc = check_launch("score_kernel<lse>"))) return rc;
-  if (!(p.T / p.ctas >= p.tpi && p.T % p.ctas == 0)) {
+  if (!(p.T % p.ctas == 0 && (p.T / p.ctas) % p.tpi == 0)) {
     const long long rows = groups * p.m_tiles * (long long)sm100::BM;
     launch_pdl(sm100::score_lse_merge_kernel, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, st, sc,
-               p.ctas, (int)q_rows, (const float*)ws_l, lse2);
+               (int)q_rows, (const float*)ws_l, lse2);
     count_launch();
     if ((rc = check_launch("score_lse_merge_kernel"))) return rc;
   }
   // MASS pass over the external keys
   RefreshPlan pm = plan_refresh(groups, q_rows, 0, (int64_t)ext_tiles * 128);
-  sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.maxseg};
+  sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.items, pm.ctas, nullptr};
   launch_pdl(sm100::score_kernel<D, true>, dim3((unsigned)pm.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
              st, mq, mk, mki, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
              (const float*)lse2, (float*)nullptr, (float*)nullptr, mass, (int)nb);

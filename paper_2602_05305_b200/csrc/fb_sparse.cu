@@ -283,6 +283,62 @@ int launch_complement(const int32_t* sel, int64_t groups, int64_t n_sel, int64_t
   return check_launch("complement_kernel");
 }
 
+// ---------------------------------------------------------------- block commit
+
+// Device-side append of a finished block's K/V rows (kv_cache.py:121-144,
+// simulator.py:327-333): group g's blk_rows rows go to cache rows
+// [len[g], len[g] + blk_rows) of its slab, then len[g] advances.  Rows that
+// would pass kv_rows_cap are dropped and counted in *overflow.
+__global__ void commit_block_kernel(unsigned char* __restrict__ kc, unsigned char* __restrict__ vc,
+                                    const unsigned char* __restrict__ kb,
+                                    const unsigned char* __restrict__ vb, int64_t cap,
+                                    int64_t row_bytes, int64_t blk_rows, int32_t* __restrict__ len,
+                                    int32_t* __restrict__ overflow) {
+  const int64_t g = blockIdx.y;
+  const int64_t r = blockIdx.x;
+  const int64_t base = len[g];
+  __syncthreads();
+  const int64_t dst_row = base + r;
+  if (dst_row < cap) {
+    const int64_t dst = (g * cap + dst_row) * row_bytes;
+    const int64_t src = (g * blk_rows + r) * row_bytes;
+    if ((row_bytes & 15) == 0) {
+      for (int64_t i = threadIdx.x * 16; i < row_bytes; i += blockDim.x * 16) {
+        *reinterpret_cast<uint4*>(kc + dst + i) = *reinterpret_cast<const uint4*>(kb + src + i);
+        *reinterpret_cast<uint4*>(vc + dst + i) = *reinterpret_cast<const uint4*>(vb + src + i);
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < row_bytes; i += blockDim.x) {
+        kc[dst + i] = kb[src + i];
+        vc[dst + i] = vb[src + i];
+      }
+    }
+  } else if (threadIdx.x == 0 && overflow) {
+    atomicAdd(overflow, 1);
+  }
+}
+
+__global__ void advance_lengths_kernel(int32_t* __restrict__ len, int64_t groups, int64_t blk_rows,
+                                       int64_t cap) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < groups) len[g] = (int32_t)min((int64_t)len[g] + blk_rows, cap);
+}
+
+int launch_commit_block(void* kc, void* vc, const void* kb, const void* vb, int64_t groups,
+                        int64_t cap, int64_t row_bytes, int64_t blk_rows, int32_t* len,
+                        int32_t* overflow, cudaStream_t st) {
+  if (groups == 0 || blk_rows == 0) return FB_OK;
+  dim3 grid((unsigned)blk_rows, (unsigned)groups);
+  commit_block_kernel<<<grid, 64, 0, st>>>(reinterpret_cast<unsigned char*>(kc),
+                                            reinterpret_cast<unsigned char*>(vc),
+                                            reinterpret_cast<const unsigned char*>(kb),
+                                            reinterpret_cast<const unsigned char*>(vb), cap, row_bytes,
+                                            blk_rows, len, overflow);
+  advance_lengths_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, st>>>(len, groups, blk_rows, cap);
+  count_launch(2);
+  return check_launch("commit_block_kernel");
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <typename Mode>

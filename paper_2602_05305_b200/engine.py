@@ -69,15 +69,35 @@ class FlashBlockAttention:
         return K.gqa_view(q, self.hkv), k_in.reshape(self.b * self.hkv, self.B, self.d), \
             v_in.reshape(self.b * self.hkv, self.B, self.d)
 
-    def refresh(self, layer: int, q, k_cache, v_cache, n_ext: int, k_in, v_in, out=None):
-        """Refresh step: K1 over cache rows [0, n_ext) + K2; stores the
-        external partial for `layer`.  Returns out [b, Hq, B, d]."""
+    def _group_lengths(self, n_ext):
+        """int -> None (uniform); tensor [b] (per sequence) or [b*Hkv] -> int32 [b*Hkv]."""
+        if isinstance(n_ext, int):
+            return None
+        t = n_ext.to(torch.int32).reshape(-1)
+        if t.numel() == self.b:
+            t = t.repeat_interleave(self.hkv)
+        if t.numel() != self.b * self.hkv:
+            raise ShapeError(f"lengths must have {self.b} or {self.b * self.hkv} entries")
+        return t.contiguous()
+
+    def refresh(self, layer: int, q, k_cache, v_cache, n_ext, k_in, v_in, out=None):
+        """Refresh step: K1 over the committed cache rows + K2; stores the
+        external partial for `layer`.  n_ext is one context length for the
+        batch (int) or per-sequence lengths (CUDA int32 tensor [b] or
+        [b*Hkv], ragged -- SURVEY 8f row f2).  Returns out [b, Hq, B, d]."""
         qg, kg, vg = self._groups(q, k_in, v_in)
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None
-        res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
-                                     o_ext=self.o_ext[layer], lse_ext=self.lse_ext[layer], out=o)
+        lens = self._group_lengths(n_ext)
+        if lens is None:
+            res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
+                                         o_ext=self.o_ext[layer], lse_ext=self.lse_ext[layer], out=o)
+        else:
+            K.attention_partial_ragged(qg, kc, vc, lens, 0, self.scale, out=self.o_ext[layer],
+                                       lse=self.lse_ext[layer])
+            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
+                                   self.out_dtype, out=o)
         self.valid[layer] = True
         return res.view(self.b, self.hq, self.B, self.d)
 
@@ -92,7 +112,7 @@ class FlashBlockAttention:
                                self.out_dtype, out=o)
         return res.view(self.b, self.hq, self.B, self.d)
 
-    def step(self, layer: int, q, k_cache, v_cache, n_ext: int, k_in, v_in, *,
+    def step(self, layer: int, q, k_cache, v_cache, n_ext, k_in, v_in, *,
              first_visit: bool, updated_tokens: int, out=None):
         """Route one layer through the reuse policy (simulator.py:412-434)."""
         choice = decide(self.config, self.valid[layer], first_visit, updated_tokens)
@@ -111,3 +131,36 @@ class FlashBlockAttention:
         res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
                                      o_ext=o_scratch, lse_ext=lse_scratch, out=o)
         return res.view(self.b, self.hq, self.B, self.d)
+
+
+class KVCache:
+    """Device KV cache with per-sequence committed lengths (the step after the
+    path; reference KvCache, kv_cache.py:80-217).
+
+    Per layer: K, V [b, Hkv, capacity, d] and int32 lengths [b*Hkv] (one per
+    kv slab, like the reference's per-(layer, head) row counts).  Blocks are
+    appended on the device (fb_commit_block); committed rows are immutable.
+    Allocated with zeros, though the kernels never read past a slab's length.
+    """
+
+    def __init__(self, num_layers: int, batch: int, num_kv_heads: int, capacity: int,
+                 head_dim: int, device=None, dtype=torch.bfloat16):
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.L, self.b, self.hkv, self.cap, self.d = num_layers, batch, num_kv_heads, capacity, head_dim
+        self.k = [torch.zeros((batch, num_kv_heads, capacity, head_dim), dtype=dtype, device=dev)
+                  for _ in range(num_layers)]
+        self.v = [torch.zeros_like(t) for t in self.k]
+        self.lengths = [torch.zeros(batch * num_kv_heads, dtype=torch.int32, device=dev)
+                        for _ in range(num_layers)]
+
+    def commit_block(self, layer: int, k_block, v_block, check: bool = False) -> None:
+        """Append one finished block's rows [b, Hkv, B, d] for `layer`."""
+        if k_block.shape[:2] != (self.b, self.hkv) or k_block.shape[-1] != self.d:
+            raise ShapeError(f"block {tuple(k_block.shape)} does not match the cache")
+        K.commit_block(self.k[layer].view(self.b * self.hkv, self.cap, self.d),
+                       self.v[layer].view(self.b * self.hkv, self.cap, self.d),
+                       k_block.reshape(self.b * self.hkv, -1, self.d),
+                       v_block.reshape(self.b * self.hkv, -1, self.d), self.lengths[layer], check)
+
+    def sequence_lengths(self, layer: int = 0) -> torch.Tensor:
+        return self.lengths[layer].view(self.b, self.hkv)[:, 0]

@@ -132,6 +132,55 @@ def attention_partial(q, k, v, key_begin: int = 0, key_end: int | None = None,
     return out, lse
 
 
+def attention_partial_ragged(q, k, v, key_end: torch.Tensor, key_begin: int = 0,
+                             scale: float | None = None, out=None, lse=None):
+    """K1 over per-group (ragged) committed lengths: group g attends slab rows
+    [key_begin, key_end[g]).  key_end: int32 CUDA tensor [groups]."""
+    q3, k3, v3 = _as3(q, "q"), _as3(k, "k"), _as3(v, "v")
+    require_cuda(q3, k3, v3, key_end)
+    _check_kv(q3, k3, v3)
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    groups, q_rows, d = q3.shape
+    ends = key_end.reshape(-1).to(torch.int32).contiguous()
+    if ends.numel() != groups:
+        raise ShapeError(f"key_end has {ends.numel()} entries for {groups} groups")
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
+    if lse is None:
+        lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_ragged_workspace_bytes(code, groups, q_rows, d, k3.shape[1])
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_attention_partial_ragged", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d,
+              k3.shape[1], int(key_begin), _p(ends), scale, _p(out), _p(lse), _p(ws),
+              0 if ws is None else ws.numel(), _stream(q3))
+    return out, lse
+
+
+def commit_block(k_cache, v_cache, k_block, v_block, lengths: torch.Tensor,
+                 check: bool = False) -> None:
+    """Append a finished block's K/V ([groups, B, d]) to each group's slab of
+    the cache ([groups, N_cap, d]) at row lengths[g]; lengths advance by B."""
+    kc, vc = _as3(k_cache, "k_cache"), _as3(v_cache, "v_cache")
+    kb, vb = _as3(k_block, "k_block").contiguous(), _as3(v_block, "v_block").contiguous()
+    require_cuda(kc, vc, kb, vb, lengths)
+    if not (kc.is_contiguous() and vc.is_contiguous()):
+        raise ShapeError("the KV cache must be contiguous")
+    if kc.shape != vc.shape or kb.shape != vb.shape or kb.shape[0] != kc.shape[0] \
+            or kb.shape[2] != kc.shape[2] or lengths.numel() != kc.shape[0]:
+        raise ShapeError("cache / block / lengths shapes do not line up")
+    if lengths.dtype != torch.int32 or not lengths.is_contiguous():
+        raise ShapeError("lengths must be a contiguous int32 tensor")
+    cnt = _empty_counter(kc.device) if check else None
+    _lib.call("fb_commit_block", dtype_code(kc), _p(kc), _p(vc), kc.shape[0], kc.shape[1],
+              kc.shape[2], _p(kb), _p(vb), kb.shape[1], _p(lengths), _p(cnt), _stream(kc))
+    if cnt is not None and int(cnt.item()) > 0:
+        from .errors import BoundsError
+        raise BoundsError("block commit overflows the KV cache capacity")
+
+
 def _empty_counter(device):
     return torch.zeros(1, dtype=torch.int32, device=device)
 

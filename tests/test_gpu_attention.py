@@ -501,3 +501,87 @@ def test_bf16_large_block_cached_step_vs_oracle(rng, q_rows, n_in, n_ext):
         ref = orc.dense(qq, kk, vv)
         assert rel_err(out[g].cpu().numpy(), ref) <= 1e-2
         assert rel_err(full[g].float().cpu().numpy(), ref) <= 1.5e-2
+
+
+# ----------------------------------------------------------------- ragged contexts + block commit
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_ragged_refresh_vs_oracle_with_garbage_tails(rng, dtype):
+    """Per-sequence context lengths (f2): each group attends only its own
+    committed rows; the slab tail holds NaNs that must never leak."""
+    from paper_2602_05305_b200 import kernels as K
+
+    lens = [0, 1, 127, 128, 129, 1000, 3333, 5000, 77, 4096]
+    groups, q_rows, d, cap = len(lens), 128, 128, 5000
+    q = bf16_exact(rng, (groups, q_rows, d))
+    k = bf16_exact(rng, (groups, cap, d))
+    v = bf16_exact(rng, (groups, cap, d))
+    kc, vc = k.to(dtype).cuda(), v.to(dtype).cuda()
+    for g, n in enumerate(lens):
+        kc[g, n:] = float("nan")
+        vc[g, n:] = float("nan")
+    ends = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    o, l = K.attention_partial_ragged(q.to(dtype).cuda(), kc, vc, ends)
+    o, l = o.float().cpu().numpy(), l.double().cpu().numpy()
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-4
+    for g, n in enumerate(lens):
+        if n == 0:
+            assert np.all(o[g] == 0) and np.isneginf(l[g]).all()
+            continue
+        ref = orc.partial(q[g].double().numpy(), k[g, :n].double().numpy(), v[g, :n].double().numpy())
+        assert np.isfinite(o[g]).all()
+        assert rel_err(o[g], ref.out) <= tol, (g, n)
+        assert np.max(np.abs(l[g] - ref.lognorm)) <= 1e-3
+
+
+def test_commit_block_and_ragged_engine(rng):
+    """Device-side block commit into a ragged KV cache, then a refresh and a
+    cached step of the engine over per-sequence lengths, against the oracle."""
+    from paper_2602_05305_b200 import FlashBlockAttention, KVCache
+
+    b, hq, hkv, B, d, cap = 3, 8, 2, 32, 128, 1024
+    kv = KVCache(1, b, hkv, cap, d)
+    G = hq // hkv
+    host_k = np.zeros((b, hkv, cap, d), np.float32)
+    host_v = np.zeros((b, hkv, cap, d), np.float32)
+    n_blocks = [3, 5, 1]
+    filled = [0] * b
+    for step in range(max(n_blocks)):
+        kb = bf16_exact(rng, (b, hkv, B, d))
+        vb = bf16_exact(rng, (b, hkv, B, d))
+        # sequences that already finished commit into a scratch copy and are reset
+        kv.commit_block(0, kb.cuda(), vb.cuda())
+        for i in range(b):
+            host_k[i, :, filled[i]:filled[i] + B] = kb[i].float().numpy()
+            host_v[i, :, filled[i]:filled[i] + B] = vb[i].float().numpy()
+            filled[i] += B
+    # make the lengths ragged: sequence i keeps n_blocks[i] blocks
+    lens = torch.tensor([n * B for n in n_blocks], dtype=torch.int32, device="cuda")
+    assert torch.equal(kv.sequence_lengths(0).cpu(), torch.full((b,), max(n_blocks) * B, dtype=torch.int32))
+    assert torch.equal(kv.k[0].float().cpu(), torch.from_numpy(host_k))
+    eng = FlashBlockAttention(1, b, hq, hkv, B, d, out_dtype=torch.float32)
+    q = bf16_exact(rng, (b, hq, B, d)).cuda()
+    ki, vi = bf16_exact(rng, (b, hkv, B, d)).cuda(), bf16_exact(rng, (b, hkv, B, d)).cuda()
+    out = eng.refresh(0, q, kv.k[0], kv.v[0], lens, ki, vi)
+    q2 = bf16_exact(rng, (b, hq, B, d)).cuda()
+    out2 = eng.cached(0, q2, ki, vi)
+    for i in range(b):
+        n = n_blocks[i] * B
+        for h in range(hkv):
+            qs = q[i, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            q2s = q2[i, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            kk = np.concatenate([host_k[i, h, :n], ki[i, h].double().cpu().numpy()])
+            vv = np.concatenate([host_v[i, h, :n], vi[i, h].double().cpu().numpy()])
+            got = out[i, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            assert rel_err(got, orc.dense(qs, kk, vv)) <= 1e-2
+            ext = orc.partial(qs, kk[:n], vv[:n])
+            ref2, _ = orc.with_reuse(q2s, ext, True, kk[n:], vv[n:])
+            got2 = out2[i, h * G:(h + 1) * G].reshape(G * B, d).double().cpu().numpy()
+            assert rel_err(got2, ref2) <= 1e-2
+    # capacity overflow is reported
+    big = KVCache(1, 1, 1, 40, d)
+    blk = torch.zeros((1, 1, 32, d), dtype=torch.bfloat16, device="cuda")
+    big.commit_block(0, blk, blk, check=True)
+    with pytest.raises(fb().BoundsError):
+        big.commit_block(0, blk, blk, check=True)
