@@ -509,18 +509,21 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   const int c_last = sc.cta_of(ie - 1);
   if (c_first == c_last) return;  // written whole by its CTA
   const int nseg = c_last - c_first + 1;
+  // CTAs with empty ranges (more CTAs than tiles, ragged plans) hold no partial
+  auto has = [&](int c) { return sc.start(c + 1) > sc.start(c); };
   float mx = -INFINITY;
   for (int k = lane; k < nseg; k += 32)
-    mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * BM + row]);
+    if (has(c_first + k)) mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * BM + row]);
   mx = warp_max(mx);
   float z = 0.f;
   for (int k = lane; k < nseg; k += 32)
-    z += __expf(ws_l[sc.slot(c_first + k, item) * BM + row] - mx);
+    if (has(c_first + k)) z += __expf(ws_l[sc.slot(c_first + k, item) * BM + row] - mx);
   z = warp_sum(z);
   const float iz = 1.f / z;
   for (int c = lane * 4; c < D; c += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < nseg; ++k) {
+      if (!has(c_first + k)) continue;
       const long long sl = sc.slot(c_first + k, item) * BM + row;
       const float w = __expf(ws_l[sl] - mx);
       const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
