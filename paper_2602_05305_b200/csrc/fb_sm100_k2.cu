@@ -19,6 +19,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 namespace fb {
 namespace sm100k2 {
 
@@ -29,9 +31,9 @@ constexpr int BOX = 64;  // bf16 columns per 128-byte swizzle span
 // The output columns of a query tile are split over SPLIT CTAs (each
 // recomputes the cheap S = Q K^T and softmax, then does P V, the merge and
 // the stores for its D/SPLIT columns): twice the CTAs, a third fewer bytes each.
-template <int D, int NT>
+template <int D, int NT, int SPLIT_ = 1>
 struct Cfg {
-  static constexpr int SPLIT = D == 128 ? 2 : 1;
+  static constexpr int SPLIT = SPLIT_;
   static constexpr int DC = D / SPLIT;                  // output columns per CTA
   static constexpr int NB = D / BOX;                    // 64-col boxes per bf16 row
   static constexpr int NBV = DC / BOX;                  // V boxes per CTA
@@ -55,7 +57,7 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-template <int D, int NT>
+template <int D, int NT, int SPLIT>
 __global__ void __launch_bounds__(THREADS, 2)
 internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -63,7 +65,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                       float scale_log2, void* __restrict__ out, int out_bf16,
                       float* __restrict__ lse_merged, float* __restrict__ o_int,
                       float* __restrict__ lse_int, int* __restrict__ empty_rows) {
-  using C = Cfg<D, NT>;
+  using C = Cfg<D, NT, SPLIT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -271,12 +273,12 @@ bool sm100_k2_supported(int64_t head_dim, int64_t n_in) {
   return (head_dim == 128 || head_dim == 64) && n_in >= 1 && n_in <= 128;
 }
 
-template <int D, int NT>
+template <int D, int NT, int SPLIT>
 static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
                      int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
                      const float* lse_ext, void* out, bool out_bf16, float* lse_merged, float* o_int,
                      float* lse_int, int32_t* empty, cudaStream_t st) {
-  using C = sm100k2::Cfg<D, NT>;
+  using C = sm100k2::Cfg<D, NT, SPLIT>;
   CUtensorMap mq, mk, mv, mo;
   int rc;
   if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
@@ -284,7 +286,7 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&mo, o_ext, 4, D, q_rows, q_rows, groups, 32, sm100k2::BM))) return rc;
-  auto kern = sm100k2::internal_merge_kernel<D, NT>;
+  auto kern = sm100k2::internal_merge_kernel<D, NT, SPLIT>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -304,9 +306,15 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
                                 int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
                                 const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
                                 float* o_int, float* lse_int, int32_t* empty, cudaStream_t st) {
-#define FB_K2(DD, NN)                                                                          \
-  return launch_k2<DD, NN>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext, out,  \
-                           out_bf16, lse_merged, o_int, lse_int, empty, st)
+#define FB_K2(DD, NN)                                                                           \
+  return split ? launch_k2<DD, NN, (DD == 128 ? 2 : 1)>(q, k_in, v_in, groups, q_rows, n_in, scale, \
+                                                        o_ext, lse_ext, out, out_bf16, lse_merged,  \
+                                                        o_int, lse_int, empty, st)                  \
+               : launch_k2<DD, NN, 1>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext,   \
+                                      out, out_bf16, lse_merged, o_int, lse_int, empty, st)
+  // split the output columns over 2 CTAs only while that still adds SM coverage
+  bool split = groups * ((q_rows + sm100k2::BM - 1) / sm100k2::BM) * 2 <= 2 * num_sms();
+  if (const char* e = getenv("FB_K2_SPLIT")) split = e[0] == '1';  // diagnostics
   if (head_dim == 128) {
     if (n_in <= 16) FB_K2(128, 16);
     if (n_in <= 32) FB_K2(128, 32);
