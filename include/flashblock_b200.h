@@ -131,6 +131,18 @@ FB_API int fb_internal_merge(int dtype, const void* q, const void* k_in, const v
                       void* out, int out_dtype, void* lse_merged,
                       void* o_int, void* lse_int, int32_t* empty_rows,
                       void* workspace, size_t workspace_bytes, void* stream);
+/* fb_internal_merge with flags.  FB_EXT_STABLE: o_ext / lse_ext were not
+ * written by the kernel immediately preceding this call on the stream (true
+ * for every cached step: the external partial is produced at the last
+ * refresh), so the kernel may read them before its programmatic-dependent-
+ * launch wait and overlap those loads with the predecessor's tail. */
+#define FB_EXT_STABLE 1
+FB_API int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void* v_in,
+                                int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_in,
+                                double scale, const void* o_ext, const void* lse_ext, void* out,
+                                int out_dtype, void* lse_merged, void* o_int, void* lse_int,
+                                int32_t* empty_rows, void* workspace, size_t workspace_bytes,
+                                int flags, void* stream);
 /* Scratch fb_internal_merge needs at this shape: 0 for blocks of <= 128 keys
  * (one fused tcgen05 kernel); large blocks (video chunks) run the stream-K
  * tensor-core partial over the block's keys plus a K3 merge and need this

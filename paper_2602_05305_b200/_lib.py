@@ -14,10 +14,13 @@ from .errors import (BoundsError, DegenerateInputError, ReusePreconditionError, 
                      StalenessError)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfb200.so")
+# diagnostics only (A/B of two builds on one box): FB_LIB_PATH overrides the in-tree library
+LIB_PATH = os.environ.get("FB_LIB_PATH", LIB_PATH)
 
 FB_OK, FB_ERR_SHAPE, FB_ERR_BOUNDS, FB_ERR_DEGENERATE = 0, 1, 2, 3
 FB_ERR_REUSE, FB_ERR_STALE, FB_ERR_CUDA, FB_ERR_VALUE, FB_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
 FB_F64, FB_F32, FB_BF16 = 0, 1, 2
+FB_EXT_STABLE = 1  # fb_internal_merge_ex flag
 
 vp, i64, i32, dbl, sz = C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_size_t
 
@@ -35,6 +38,8 @@ SIGNATURES = {
     "fb_commit_block": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp, vp, vp]),
     "fb_internal_merge": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, i32, vp,
                                 vp, vp, vp, vp, sz, vp]),
+    "fb_internal_merge_ex": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, i32, vp,
+                                   vp, vp, vp, vp, sz, i32, vp]),
     "fb_internal_merge_workspace_bytes": (sz, [i32, i64, i64, i64, i64]),
     "fb_combine": (i32, [i32, i32, vp, vp, i64, i64, vp, i32, vp, vp, vp]),
     "fb_full_attention": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i64, dbl, vp,

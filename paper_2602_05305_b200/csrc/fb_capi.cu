@@ -138,7 +138,7 @@ static int internal_merge_t(const void* qv, const void* kv, const void* vv, int6
                             int64_t q_rows, int64_t d, int64_t n_in, double scale,
                             const void* o_ext, const void* lse_ext, void* out, bool out_bf16,
                             void* lse_merged, void* o_int, void* lse_int, int32_t* empty,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool ext_early = false) {
   using Tin = typename Mode::Tin;
   if constexpr (std::is_same<Mode, ModeBF16>::value) {
     auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
@@ -149,7 +149,7 @@ static int internal_merge_t(const void* qv, const void* kv, const void* vv, int6
           reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, n_in, scale,
           reinterpret_cast<const float*>(o_ext), reinterpret_cast<const float*>(lse_ext), out,
           out_bf16, reinterpret_cast<float*>(lse_merged), reinterpret_cast<float*>(o_int),
-          reinterpret_cast<float*>(lse_int), empty, st);
+          reinterpret_cast<float*>(lse_int), empty, ext_early, st);
   }
   MergeOut<Mode> mo{};
   mo.o_ext = reinterpret_cast<const typename Mode::To*>(o_ext);
@@ -403,6 +403,7 @@ const char* fb_last_error(void) { return g_last_error.c_str(); }
 const char* fb_version(void) { return "fb200 0.1.0 sm_100a"; }
 // Diagnostics (not in the public header): per-CTA timestamps of the refresh kernel.
 FB_API void fb_debug_set_trace(void* device_buffer) { set_refresh_trace(device_buffer); }
+FB_API void fb_debug_set_k1_diag(int diag) { set_k1_diag(diag); }
 int64_t fb_launch_count(void) { return g_launches.load(); }
 
 size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,
@@ -515,7 +516,19 @@ int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_
                       const void* o_ext, const void* lse_ext, void* out, int out_dtype,
                       void* lse_merged, void* o_int, void* lse_int, int32_t* empty_rows,
                       void* workspace, size_t workspace_bytes, void* stream) {
+  return fb_internal_merge_ex(dtype, q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
+                              lse_ext, out, out_dtype, lse_merged, o_int, lse_int, empty_rows,
+                              workspace, workspace_bytes, 0, stream);
+}
+
+int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void* v_in,
+                         int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_in,
+                         double scale, const void* o_ext, const void* lse_ext, void* out,
+                         int out_dtype, void* lse_merged, void* o_int, void* lse_int,
+                         int32_t* empty_rows, void* workspace, size_t workspace_bytes, int flags,
+                         void* stream) {
   if (int rc = check_dtype(dtype)) return rc;
+  if (flags & ~FB_EXT_STABLE) return fail(FB_ERR_VALUE, "unknown fb_internal_merge_ex flags");
   if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
   if (groups == 0 || q_rows == 0) return FB_OK;
@@ -556,7 +569,7 @@ int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_
       }
       return internal_merge_t<ModeBF16>(q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
                                         lse_ext, out, out_dtype == FB_BF16, lse_merged, o_int,
-                                        lse_int, empty_rows, st);
+                                        lse_int, empty_rows, st, (flags & FB_EXT_STABLE) != 0);
   }
 }
 

@@ -64,6 +64,7 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 // refresh_sm100_workspace_bytes; with less it runs one CTA per item).
 bool sm100_supported(int64_t head_dim);
 void set_refresh_trace(void* p);
+void set_k1_diag(int d);
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
@@ -107,6 +108,7 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
                                 const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
                                 int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
                                 const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
-                                float* o_int, float* lse_int, int32_t* empty, cudaStream_t st);
+                                float* o_int, float* lse_int, int32_t* empty, bool ext_early,
+                                cudaStream_t st);
 
 }  // namespace fb

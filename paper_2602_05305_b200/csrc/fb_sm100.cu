@@ -35,7 +35,7 @@ namespace sm100 {
 
 constexpr int BM = 128;       // query rows per tile (TMEM lanes)
 constexpr int BN = 128;       // keys per tile
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;  // 4 control warps + 2 softmax warpgroups
 constexpr int BOX_COLS = 64;  // 128-byte swizzle span in bf16
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P stays <= 256
@@ -51,15 +51,16 @@ struct Cfg {
   static constexpr uint32_t OFF_V = OFF_K + STAGES * TILE_BYTES;
   static constexpr uint32_t OFF_BAR = OFF_V + STAGES * TILE_BYTES;
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t SMEM = OFF_BAR + BAR_BYTES + 1024;  // + alignment slack
-  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O = 256;
+  static constexpr uint32_t OFF_XCH = OFF_BAR + BAR_BYTES;    // [2][128] fp32 epilogue exchange
+  static constexpr uint32_t SMEM = OFF_XCH + 2 * BM * 4 + 1024;  // + alignment slack
+  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
 };
 
 struct Barriers {
   uint64_t q_full, q_empty;
   uint64_t k_full[6], k_empty[6], v_full[6], v_empty[6];
   uint64_t s_full[2], p_ready[2];
-  uint64_t pv_done, o_full, o_empty;
+  uint64_t pv_done[2], o_full, o_empty;
   uint32_t tmem_base;
 };
 
@@ -120,7 +121,9 @@ struct Gather {
   int n_list, n_ext, n_in, sel_tiles;
 };
 
-template <int D, bool GATHER>
+// DIAG (diagnostics only, fb_debug_set_k1_diag): 1 = softmax warps load S but skip
+// the softmax math, 2 = they skip the TMEM load too (pure TMA + MMA pipeline).
+template <int D, bool GATHER, int DIAG = 0>
 __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ki,
@@ -133,6 +136,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Barriers* bar = reinterpret_cast<Barriers*>(smem + C::OFF_BAR);
+  float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);  // [2][128] epilogue exchange
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -164,10 +168,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bar->s_full[b], 1);
       ptx::mbar_init(&bar->p_ready[b], 128);
+      ptx::mbar_init(&bar->pv_done[b], 1);
     }
-    ptx::mbar_init(&bar->pv_done, 1);
     ptx::mbar_init(&bar->o_full, 1);
-    ptx::mbar_init(&bar->o_empty, 128);
+    ptx::mbar_init(&bar->o_empty, 256);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(&bar->tmem_base, TMEM_COLS);
@@ -177,7 +181,9 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const uint32_t tmem = bar->tmem_base;
   ptx::pdl_wait();               // inputs of this launch are final from here on
   ptx::pdl_launch_dependents();  // let the next kernel's prologue start
-
+  // registers: control warpgroup 56/thread, softmax warpgroups 224 (64,512 of 65,536)
+  if (warp < 4) {
+  ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -249,6 +255,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // Tile j goes to softmax warpgroup w = j & 1: S_j -> TMEM S[w], O[w] += P_j V_j.
     if (lane == 0) {
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, BN, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
@@ -299,15 +306,17 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             ptx::tc_fence_after();
             const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V + s * C::TILE_BYTES);
             const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
+            const uint32_t o_tmem = tmem + ((jj & 1) ? C::COL_O1 : C::COL_O0);
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
               // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
-              ptx::mma_ts(tmem + C::COL_O, p_tmem + kk * 8,
+              // (the first two tiles of a segment start their warpgroup's O afresh)
+              ptx::mma_ts(o_tmem, p_tmem + kk * 8,
                           ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
-                          (t > 1 || kk > 0) ? 1u : 0u);
+                          (t > 2 || kk > 0) ? 1u : 0u);
             }
             ptx::tc_commit(&bar->v_empty[s]);
-            ptx::tc_commit(&bar->pv_done);
+            ptx::tc_commit(&bar->pv_done[jj & 1]);
             if (t == n) ptx::tc_commit(&bar->o_full);
           }
         }
@@ -315,11 +324,18 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         t0 += n;
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    ptx::setmaxnreg_inc<224>();
     // ------------------------------------------------------------ softmax
+    // Two warpgroups take alternate key tiles, each with its own running
+    // (max, sum) and O accumulator, so one's softmax overlaps the other's.
+    const int wg = (warp - 4) >> 2;                // 0: warps 4-7, 1: warps 8-11
     const int wq = warp & 3;                       // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const int row = wq * 32 + lane;                // row inside the 128-row tile
+    const uint32_t s_col = wg ? C::COL_S1 : C::COL_S0;
+    const uint32_t o_col = wg ? C::COL_O1 : C::COL_O0;
     uint32_t r[32];
     float s[BN];
     int jg = 0, seg = 0;
@@ -339,11 +355,24 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           last_rows = min(16, ga.n_ext - last * 16);
         }
       }
-      for (int t = 0; t < n; ++t) {
+      for (int t = ((jg & 1) == wg) ? 0 : 1; t < n; t += 2) {
         const int j = jg + t;
-        const uint32_t s_col = (j & 1) ? C::COL_S1 : C::COL_S0;
-        ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
+        ptx::mbar_wait(&bar->s_full[wg], (j >> 1) & 1);
         ptx::tc_fence_after();
+        if constexpr (DIAG > 0) {
+          if constexpr (DIAG == 1) {
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c)
+              ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, reinterpret_cast<uint32_t*>(s) + c * 32);
+            ptx::tmem_wait_ld();
+            if (s[0] == 12345.f) l += 1.f;  // keep the load live
+          }
+          m_used = 0.f;
+          l += 1.f;
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&bar->p_ready[wg]);
+          continue;
+        }
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c)  // all four loads in flight, one wait
           ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, reinterpret_cast<uint32_t*>(s) + c * 32);
@@ -381,8 +410,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             }
           }
         }
-        // row max and row sum as 8 independent chains (one softmax warp per
-        // SMSP: latency, not throughput, bounds this loop)
+        // row max and row sum as 8 independent chains
         float mx8[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mx8[k] = s[k];
@@ -394,13 +422,13 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const bool need = m_new > m_used + RESCALE_THRESHOLD;
         if (__any_sync(0xffffffffu, need)) {
           const float alpha = ptx::ex2(m_used - m_new);
-          if (t > 0) {
-            // O holds this segment's P V so far: wait for the last PV before touching it
-            ptx::mbar_wait(&bar->pv_done, (j - 1) & 1);
+          if (t >= 2) {
+            // O[wg] holds this segment's P V so far: wait for its last PV (tile j-2)
+            ptx::mbar_wait(&bar->pv_done[wg], ((j - 2) >> 1) & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < D / 32; ++c) {
-              const uint32_t a = tmem + lane_off + C::COL_O + c * 32;
+              const uint32_t a = tmem + lane_off + o_col + c * 32;
               ptx::tmem_ld32(a, r);
               ptx::tmem_wait_ld();
 #pragma unroll
@@ -428,46 +456,80 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&bar->p_ready[j & 1]);
+        ptx::mbar_arrive(&bar->p_ready[wg]);
       }
       jg += n;
       t0 += n;
-      if (row == 0) stamp(1 + 2 * (seg & 1));
+      if (row == 0 && wg == 0) stamp(1 + 2 * (seg & 1));
 
       // ---------------------------------------------------------- segment epilogue
+      // Merge the two warpgroups' partials (exact log-space merge): WG0 posts
+      // (m0, l0), WG1 forms the weights and posts WG0's; each WG then writes
+      // half of the output columns from both O accumulators.
       const bool whole = ib >= t_begin && sc.item_end(item) <= t_end;  // item not shared
       const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
       const int grow = mt * BM + row;
       const bool live = grow < q_rows;
       const long long orow = (long long)g * q_rows + grow;
-      const float inv = 1.f / l;
-      const float lse = (m_used + log2f(l)) * 0.69314718055994530942f;
+      float c_own, c_oth, lse = 0.f;
+      if (wg == 0) {
+        xch[row] = m_used;
+        xch[BM + row] = l;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (wg == 1) {
+        const float m0 = xch[row], l0 = xch[BM + row];
+        const float m = fmaxf(m0, m_used);
+        const float a0 = l0 > 0.f ? ptx::ex2(m0 - m) : 0.f;
+        const float a1 = l > 0.f ? ptx::ex2(m_used - m) : 0.f;
+        const float z = a0 * l0 + a1 * l;
+        const float iz = 1.f / z;
+        c_own = a1 * iz;
+        c_oth = a0 * iz;
+        lse = (m + log2f(z)) * 0.69314718055994530942f;
+        xch[row] = c_oth;
+        xch[BM + row] = c_own;
+      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (wg == 0) {
+        c_own = xch[row];
+        c_oth = xch[BM + row];
+      }
+      // coefficient of O0 and O1 (a warpgroup without tiles in this segment has
+      // weight 0 and a stale accumulator, so it is selected out, not multiplied)
+      const float c0 = wg == 0 ? c_own : c_oth;
+      const float c1 = wg == 0 ? c_oth : c_own;
       float* dst;
       if (whole) {
         dst = live ? o_out + orow * D : nullptr;
       } else {
         const long long slot = sc.slot(blockIdx.x, item) * BM + row;
         dst = ws_o + slot * D;
-        ws_l[slot] = lse;
+        if (wg == 1) ws_l[slot] = lse;
       }
       ptx::mbar_wait(&bar->o_full, seg & 1);
       ptx::tc_fence_after();
+      uint32_t r1[32];
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
+      for (int c = wg * (D / 64); c < (wg + 1) * (D / 64); ++c) {
+        ptx::tmem_ld32(tmem + lane_off + C::COL_O0 + c * 32, r);
+        ptx::tmem_ld32(tmem + lane_off + C::COL_O1 + c * 32, r1);
         ptx::tmem_wait_ld();
         if (dst != nullptr) {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            v[i] = (c0 != 0.f ? c0 * __uint_as_float(r[i]) : 0.f) +
+                   (c1 != 0.f ? c1 * __uint_as_float(r1[i]) : 0.f);
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + i) =
-                make_float4(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv,
-                            __uint_as_float(r[i + 2]) * inv, __uint_as_float(r[i + 3]) * inv);
+            *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
-      if (whole && live) lse_out[orow] = lse;
-      if (row == 0) stamp(2 + 2 * (seg & 1));
+      if (whole && live && wg == 1) lse_out[orow] = lse;
+      if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
   }
 
@@ -849,6 +911,8 @@ bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 12
 
 // diagnostics: per-CTA globaltimer stamps (set through fb_debug_set_trace)
 static unsigned long long* g_trace = nullptr;
+static int g_k1_diag = 0;  // diagnostics: refresh_kernel<.., DIAG> variant
+void set_k1_diag(int d) { g_k1_diag = d; }
 static int g_trace_launch = 0;  // successive launches stamp successive 148x8 slabs
 
 struct RefreshPlan {
@@ -967,10 +1031,15 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   }
   auto kern = sm100::refresh_kernel<D, GATHER>;
-  static bool attr = false;
-  if (!attr) {
+  if constexpr (!GATHER && D == 128) {
+    if (g_k1_diag == 1) kern = sm100::refresh_kernel<D, false, 1>;
+    if (g_k1_diag == 2) kern = sm100::refresh_kernel<D, false, 2>;
+  }
+  static bool attr[3] = {false, false, false};
+  const int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 3 ? g_k1_diag : 0);
+  if (!attr[ai]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr = true;
+    attr[ai] = true;
   }
   RefreshPlan p = plan_refresh(groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};

@@ -5,14 +5,19 @@
 // over the current block's keys (:320) + merge_partials with the cached
 // external partial (:321, :207-245).  The KV cache is not an argument.
 //
-// One CTA per (group, 128-row query tile), 160 threads:
+// One CTA per (group, 128-row query tile, output-column slice), 160 threads:
 //   warps 0..3  softmax + merge epilogue, thread = query row = TMEM lane;
-//   warp 4      TMA (Q, K_in, V_in, and the fp32 O_ext tile, all 128B
-//               swizzled) and the tcgen05.mma issue (one thread).
+//               each thread loads its row of the cached O_ext slice and its
+//               LSE_ext straight into registers at kernel start;
+//   warp 4      TMA (Q, K_in, V_in, 128B swizzled) and the tcgen05.mma issue.
 // S = Q K_in^T (N = NT <= 128 keys) lands in TMEM; P (bf16) overwrites S;
 // O = P V_in (TS MMA) lands in TMEM; the epilogue normalises O, merges it
-// with O_ext / LSE_ext in fp32 and writes bf16 (or fp32) output.  Two CTAs
-// fit per SM (TMEM NT+D <= 256 columns, ~115 KB smem).
+// with O_ext / LSE_ext in fp32 and writes bf16 (or fp32) output.  ~45 KB of
+// shared memory, so the next launch's CTAs fit beside this one's (PDL).
+// ext_early: the caller guarantees the external partial was not written by
+// the kernel immediately preceding this launch in the stream (true for every
+// cached step), so its loads are issued before griddepcontrol.wait and
+// overlap the predecessor's tail.
 #include "fb_kernels.cuh"
 #include "fb_sm100_ptx.cuh"
 
@@ -35,17 +40,16 @@ template <int D, int NT, int SPLIT_ = 1>
 struct Cfg {
   static constexpr int SPLIT = SPLIT_;
   static constexpr int DC = D / SPLIT;                  // output columns per CTA
+  // O_ext columns prefetched into registers (fewer beside a 128-key score row)
+  static constexpr int PRE = NT >= 128 ? 32 : (DC > 64 ? 64 : DC);
   static constexpr int NB = D / BOX;                    // 64-col boxes per bf16 row
   static constexpr int NBV = DC / BOX;                  // V boxes per CTA
   static constexpr uint32_t QBOX = BM * 128;            // 16 KB
   static constexpr uint32_t KBOX = NT * 128;            // NT rows x 128 B
-  static constexpr uint32_t OBOX = BM * 128;            // fp32: 32 cols x 128 rows
-  static constexpr int NOB = DC / 32;                   // fp32 boxes of O_ext per CTA
   static constexpr uint32_t OFF_Q = 0;
   static constexpr uint32_t OFF_K = OFF_Q + NB * QBOX;
   static constexpr uint32_t OFF_V = OFF_K + NB * KBOX;
-  static constexpr uint32_t OFF_O = OFF_V + NBV * KBOX;
-  static constexpr uint32_t OFF_BAR = OFF_O + NOB * OBOX;
+  static constexpr uint32_t OFF_BAR = OFF_V + NBV * KBOX;
   static constexpr uint32_t SMEM = OFF_BAR + 128 + 1024;
   static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;  // P stores span >= 32 cols
   static constexpr uint32_t TMEM_COLS = (COL_O + DC) <= 128 ? 128 : (COL_O + DC) <= 256 ? 256 : 512;
@@ -53,18 +57,18 @@ struct Cfg {
 };
 
 struct Bars {
-  uint64_t load_qkv, load_o, s_full, p_ready, o_full;
+  uint64_t load_qkv, s_full, p_ready, o_full;
   uint32_t tmem_base;
 };
 
 template <int D, int NT, int SPLIT>
 __global__ void __launch_bounds__(THREADS, 2)
 internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                      const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ o_ext,
                       const float* __restrict__ lse_ext, int q_rows, int m_tiles, int n_in,
                       float scale_log2, void* __restrict__ out, int out_bf16,
                       float* __restrict__ lse_merged, float* __restrict__ o_int,
-                      float* __restrict__ lse_int, int* __restrict__ empty_rows) {
+                      float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early) {
   using C = Cfg<D, NT, SPLIT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -75,14 +79,35 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const int g = (blockIdx.x / C::SPLIT) / m_tiles;
   const int mt = (blockIdx.x / C::SPLIT) % m_tiles;
   const int col0 = h * C::DC;
+  const int row = (warp & 3) * 32 + lane;
+  const int grow = mt * BM + row;
+  const bool live_row = warp < 4 && grow < q_rows;
+  const long long rr = (long long)g * q_rows + grow;
+
+  // this thread's row of the cached external partial (its column slice)
+  float le = -INFINITY;
+  float oe[C::PRE];
+  auto load_ext = [&]() {
+    if (live_row) {
+      le = __ldg(lse_ext + rr);
+      const float4* src = reinterpret_cast<const float4*>(o_ext + rr * D + col0);
+#pragma unroll
+      for (int j = 0; j < C::PRE / 4; ++j) {
+        const float4 v4 = __ldg(src + j);
+        oe[4 * j] = v4.x; oe[4 * j + 1] = v4.y; oe[4 * j + 2] = v4.z; oe[4 * j + 3] = v4.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < C::PRE; ++i) oe[i] = 0.f;
+    }
+  };
+  if (ext_early) load_ext();
 
   if (threadIdx.x == 128) {
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
-    ptx::tma_prefetch_desc(&tm_o);
     ptx::mbar_init(&bar->load_qkv, 1);
-    ptx::mbar_init(&bar->load_o, 1);
     ptx::mbar_init(&bar->s_full, 1);
     ptx::mbar_init(&bar->p_ready, 128);
     ptx::mbar_init(&bar->o_full, 1);
@@ -106,9 +131,6 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       }
       for (int b = 0; b < C::NBV; ++b)
         ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, g, pol);
-      ptx::mbar_expect_tx(&bar->load_o, C::NOB * C::OBOX);
-      for (int b = 0; b < C::NOB; ++b)
-        ptx::tma_load_3d(smem + C::OFF_O + b * C::OBOX, &tm_o, &bar->load_o, col0 + b * 32, mt * BM, g, pol);
 
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, C::DC, true);
@@ -136,13 +158,8 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     }
   } else if (warp < 4) {
     // ------------------------------------------------ softmax + merge epilogue
+    if (!ext_early) load_ext();
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const int row = warp * 32 + lane;
-    const int grow = mt * BM + row;
-    const bool live_row = grow < q_rows;
-    const long long rr = (long long)g * q_rows + grow;
-    const float le = live_row ? lse_ext[rr] : -INFINITY;  // natural log
-
     uint32_t r[32];
     float s[NT];
     ptx::mbar_wait(&bar->s_full, 0);
@@ -200,27 +217,32 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     const float z = we + wi;
     const float iz = live ? 1.f / z : 0.f;
 
-    ptx::mbar_wait(&bar->load_o, 0);
     ptx::mbar_wait(&bar->o_full, 0);
     ptx::tc_fence_after();
-    const unsigned char* o_sm = smem + C::OFF_O;
-#pragma unroll 1
+#pragma unroll
     for (int c = 0; c < C::DC / 32; ++c) {
       ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
-      ptx::tmem_wait_ld();
-      // cached external row chunk c (fp32, 128B-swizzled box c): 8 x 16-byte pieces
-      float oe[32];
-      const unsigned char* brow = o_sm + c * C::OBOX + row * 128;
+      float oc[32];
+      if (c * 32 < C::PRE) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 v4 = *reinterpret_cast<const float4*>(brow + ((j ^ (row & 7)) * 16));
-        oe[4 * j] = v4.x; oe[4 * j + 1] = v4.y; oe[4 * j + 2] = v4.z; oe[4 * j + 3] = v4.w;
+        for (int i = 0; i < 32; ++i) oc[i] = oe[(c * 32 + i) % C::PRE];
+      } else if (live_row) {  // columns past the prefetched ones (unsplit D = 128)
+        const float4* src = reinterpret_cast<const float4*>(o_ext + rr * D + col0 + c * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v4 = __ldg(src + j);
+          oc[4 * j] = v4.x; oc[4 * j + 1] = v4.y; oc[4 * j + 2] = v4.z; oc[4 * j + 3] = v4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) oc[i] = 0.f;
       }
+      ptx::tmem_wait_ld();
       float val[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float oi = __uint_as_float(r[i]) * inv;
-        val[i] = live ? (__fmul_rn(we, oe[i]) + __fmul_rn(wi, oi)) * iz : 0.f;
+        val[i] = live ? (__fmul_rn(we, oc[i]) + __fmul_rn(wi, oi)) * iz : 0.f;
         r[i] = __float_as_uint(oi);
       }
       if (live_row) {
@@ -277,15 +299,14 @@ template <int D, int NT, int SPLIT>
 static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
                      int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
                      const float* lse_ext, void* out, bool out_bf16, float* lse_merged, float* o_int,
-                     float* lse_int, int32_t* empty, cudaStream_t st) {
+                     float* lse_int, int32_t* empty, bool ext_early, cudaStream_t st) {
   using C = sm100k2::Cfg<D, NT, SPLIT>;
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
   const int64_t nin_eff = n_in > 0 ? n_in : 1;  // zero-row maps are invalid; rows are masked
   if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
-  if ((rc = make_tmap_3d(&mo, o_ext, 4, D, q_rows, q_rows, groups, 32, sm100k2::BM))) return rc;
   auto kern = sm100k2::internal_merge_kernel<D, NT, SPLIT>;
   static bool attr = false;
   if (!attr) {
@@ -295,8 +316,9 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles * C::SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st,
-             mq, mk, mv, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
-             out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty));
+             mq, mk, mv, o_ext, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
+             out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
+             ext_early ? 1 : 0);
   count_launch();
   return check_launch("internal_merge_kernel(sm100)");
 }
@@ -305,13 +327,14 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
                                 const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
                                 int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
                                 const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
-                                float* o_int, float* lse_int, int32_t* empty, cudaStream_t st) {
+                                float* o_int, float* lse_int, int32_t* empty, bool ext_early,
+                                cudaStream_t st) {
 #define FB_K2(DD, NN)                                                                           \
   return split ? launch_k2<DD, NN, (DD == 128 ? 2 : 1)>(q, k_in, v_in, groups, q_rows, n_in, scale, \
                                                         o_ext, lse_ext, out, out_bf16, lse_merged,  \
-                                                        o_int, lse_int, empty, st)                  \
+                                                        o_int, lse_int, empty, ext_early, st)       \
                : launch_k2<DD, NN, 1>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext,   \
-                                      out, out_bf16, lse_merged, o_int, lse_int, empty, st)
+                                      out, out_bf16, lse_merged, o_int, lse_int, empty, ext_early, st)
   // split the output columns over 2 CTAs only while that still adds SM coverage
   bool split = groups * ((q_rows + sm100k2::BM - 1) / sm100k2::BM) * 2 <= 2 * num_sms();
   if (const char* e = getenv("FB_K2_SPLIT")) split = e[0] == '1';  // diagnostics

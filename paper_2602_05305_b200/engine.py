@@ -108,8 +108,11 @@ class FlashBlockAttention:
             raise ReusePreconditionError(f"no valid cached external partial for layer {layer}")
         qg, kg, vg = self._groups(q, k_in, v_in)
         o = out.view(qg.shape) if out is not None else None
+        # the external partial was written at the last refresh, never by the
+        # kernel right before this one (refresh ends with K2), so K2 may
+        # prefetch it before its PDL wait
         res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
-                               self.out_dtype, out=o)
+                               self.out_dtype, out=o, ext_stable=True)
         return res.view(self.b, self.hq, self.B, self.d)
 
     def step(self, layer: int, q, k_cache, v_cache, n_ext, k_in, v_in, *,

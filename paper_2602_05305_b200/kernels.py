@@ -192,9 +192,14 @@ def _raise_if_empty(counter, what):
 
 def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
                    out_dtype: torch.dtype | None = None, want_lse: bool = False,
-                   want_internal: bool = False, check: bool = False, out=None):
+                   want_internal: bool = False, check: bool = False, out=None,
+                   ext_stable: bool = False):
     """K2: block-internal partial fused with the merge against the cached
-    external partial.  Returns out, or a tuple (out, lse_merged?, (o_int, lse_int)?)."""
+    external partial.  Returns out, or a tuple (out, lse_merged?, (o_int, lse_int)?).
+
+    ext_stable: o_ext/lse_ext were not written by the kernel launched
+    immediately before this one on the stream (FB_EXT_STABLE; true for cached
+    steps), so the kernel may load them before its PDL wait."""
     q3, k3, v3 = _as3(q, "q"), _as3(k_in, "k_in"), _as3(v_in, "v_in")
     require_cuda(q3, k3, v3, o_ext, lse_ext)
     _check_kv(q3, k3, v3)
@@ -218,9 +223,10 @@ def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     wsb = _lib.load().fb_internal_merge_workspace_bytes(code, groups, q_rows, d, k3.shape[1])
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_internal_merge", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
+    _lib.call("fb_internal_merge_ex", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
               scale, _p(o_ext), _p(lse_ext), _p(out), _OUT_CODE[out.dtype], _p(lse_m), _p(o_int),
-              _p(l_int), _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
+              _p(l_int), _p(cnt), _p(ws), 0 if ws is None else ws.numel(),
+              _lib.FB_EXT_STABLE if ext_stable else 0, _stream(q3))
     _raise_if_empty(cnt, "internal_merge")
     if not (want_lse or want_internal):
         return out
