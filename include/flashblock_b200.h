@@ -104,6 +104,27 @@ FB_API int fb_attention_partial_ragged(int dtype, const void* q, const void* k, 
 FB_API size_t fb_ragged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
                                         int64_t head_dim, int64_t kv_rows_cap);
 
+/* Block-causal attention: the prefill / commit pass.
+ * Replaces the per-block attention_dense calls of the reference's commit pass
+ * (_context_hidden, simulator.py:297-325) over a whole prompt (prefill,
+ * simulator.py:343-354) in one launch.  q: [groups, q_rows, head_dim] with
+ * q_rows = heads_per_group * n_q (the group's query heads stacked, each n_q
+ * positions); k/v slabs hold the committed prefix in rows [0, n_prefix) and
+ * the new positions' keys in rows [n_prefix, n_prefix + n_q) (commit them
+ * with fb_commit_block first).  Query row r (position p = r % n_q) attends
+ * rows [0, n_prefix + min(n_q, (p / block_size + 1) * block_size)): every
+ * earlier block and its own block, bidirectionally.  Writes the attention
+ * output and its log-sum-exp in the mode's partial types (F64: f64/f64;
+ * F32: f32/f64, scores in float64 as attention_dense; BF16: f32/f32, the
+ * TMA + tcgen05 kernel for head_dim in {64,128}). */
+FB_API int fb_block_causal_attention(int dtype, const void* q, const void* k, const void* v,
+                                     int64_t groups, int64_t q_rows, int64_t n_q, int64_t head_dim,
+                                     int64_t kv_rows_cap, int64_t n_prefix, int64_t block_size,
+                                     double scale, void* o_out, void* lse_out, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+FB_API size_t fb_block_causal_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
+                                              int64_t head_dim);
+
 /* Device-side block commit (kv_cache.py:121-144; simulator.py:327-333):
  * append a finished block's K/V rows ([groups, block_rows, head_dim]) to each
  * group's slab at row lengths[g] (device int32 [groups]), then advance

@@ -79,6 +79,29 @@ def dense(q, keys, values, scale=None) -> np.ndarray:
     return np.matmul(w, values.astype(np.float64)) / np.sum(w, axis=1, keepdims=True)
 
 
+def block_causal(q, keys, values, n_prefix: int, n_q: int, block: int, scale=None) -> np.ndarray:
+    """Block-causal prefill / commit attention (simulator.py:297-354).
+
+    The reference commits a prompt block by block (prefill, simulator.py:343-354);
+    each block's commit pass runs attention_dense over the committed context
+    plus the block's own keys (simulator.py:316-320).  Restated for stacked
+    query heads: q holds heads * n_q rows (row r at position p = r % n_q);
+    rows of block j = p // block attend keys [0, n_prefix + min(n_q, (j+1)*block)).
+    Returns the float64 outputs [rows, d].
+    """
+    rows = q.shape[0]
+    if rows % n_q:
+        raise OracleShapeError("q rows must be heads * n_q")
+    out = np.empty((rows, values.shape[1]), dtype=np.float64)
+    for h in range(rows // n_q):
+        for j0 in range(0, n_q, block):
+            j1 = min(j0 + block, n_q)
+            lim = n_prefix + j1
+            out[h * n_q + j0:h * n_q + j1] = dense(q[h * n_q + j0:h * n_q + j1], keys[:lim],
+                                                   values[:lim], scale)
+    return out
+
+
 def partial(q, keys, values, scale=None, tile_size=DEFAULT_TILE) -> Partial:
     """Tile-streamed online-softmax partial (attention.py:136-182).
 

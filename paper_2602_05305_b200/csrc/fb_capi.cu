@@ -397,6 +397,54 @@ static int attention_partial_ragged_t(const void* qv, const void* kv, const void
 
 using namespace fb;
 
+// Scores in the dense oracle's precision: float64 for F64 / F32 inputs
+// (attention_dense, attention.py:113-133, used by the commit pass at
+// simulator.py:318-320), fp32 from bf16 products in BF16 mode.
+template <typename Mode> struct DenseMode { using type = Mode; };
+template <> struct DenseMode<ModeF32> { using type = ModeMaskF32; };
+
+template <typename Mode>
+static int block_causal_t(const void* qv, const void* kv, const void* vv, int64_t groups,
+                          int64_t q_rows, int64_t d, int64_t cap, int64_t n_q, int64_t n_prefix,
+                          int64_t blk, double scale, void* o_out, void* lse_out, void* ws,
+                          size_t ws_bytes, cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  using SM = typename DenseMode<Mode>::type;
+  using Ta = typename SM::Ta;
+  auto* q = reinterpret_cast<const Tin*>(qv);
+  auto* k = reinterpret_cast<const Tin*>(kv);
+  auto* v = reinterpret_cast<const Tin*>(vv);
+  auto* o = reinterpret_cast<typename Mode::To*>(o_out);
+  auto* l = reinterpret_cast<typename Mode::Tl*>(lse_out);
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (sm100_supported(d) && cap < (int64_t(1) << 31) && groups * q_rows < (int64_t(1) << 31) &&
+        ws_bytes >= refresh_sm100_ragged_workspace_bytes(groups, q_rows, d))
+      return launch_block_causal_sm100(q, k, v, groups, q_rows, d, cap, n_q, n_prefix, blk, scale,
+                                       o, l, ws, ws_bytes, st);
+  }
+  CausalMap<Tin> map{k, v, cap * d, d, n_q, blk, n_prefix};
+  MergeOut<SM> none{};
+  constexpr bool direct_ok = std::is_same<Ta, typename Mode::To>::value &&
+                             std::is_same<Ta, typename Mode::Tl>::value;
+  if constexpr (direct_ok) {
+    return launch_partial_simt<SM, false, false>(q, map, groups, q_rows, d, int64_t(1) << 40, 1,
+                                                 scale, reinterpret_cast<Ta*>(o),
+                                                 reinterpret_cast<typename SM::Tl*>(l), none, st);
+  } else {
+    const int64_t rows = groups * q_rows;
+    if (ws == nullptr || ws_bytes < split_bytes<SM>(rows, d))
+      return fail(FB_ERR_VALUE, "workspace too small (fb_block_causal_workspace_bytes)");
+    Ta* wo = reinterpret_cast<Ta*>(ws);
+    int rc = launch_partial_simt<SM, false, false>(q, map, groups, q_rows, d, int64_t(1) << 40, 1,
+                                                   scale, wo,
+                                                   reinterpret_cast<typename SM::Tl*>(wo + rows * d),
+                                                   none, st);
+    if (rc) return rc;
+    return launch_combine<Ta, Ta, Ta, typename Mode::To, typename Mode::Tl>(
+        strided_list<SM>(ws, 1, rows, d), rows, d, o, l, nullptr, st);
+  }
+}
+
 extern "C" {
 
 const char* fb_last_error(void) { return g_last_error.c_str(); }
@@ -498,6 +546,47 @@ int fb_attention_partial_ragged(int dtype, const void* q, const void* k, const v
       return attention_partial_ragged_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
                                                   key_begin, key_end, scale, o_out, lse_out,
                                                   workspace, workspace_bytes, st);
+  }
+}
+
+// ---------------------------------------------------------------- block-causal (prefill / commit)
+
+size_t fb_block_causal_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim) {
+  const int64_t rows = groups * q_rows;
+  switch (dtype) {
+    case FB_F64: return 0;
+    case FB_F32: return split_bytes<ModeMaskF32>(rows, head_dim);
+    default:
+      return sm100_supported(head_dim) ? refresh_sm100_ragged_workspace_bytes(groups, q_rows, head_dim) : 0;
+  }
+}
+
+int fb_block_causal_attention(int dtype, const void* q, const void* k, const void* v,
+                              int64_t groups, int64_t q_rows, int64_t n_q, int64_t head_dim,
+                              int64_t kv_rows_cap, int64_t n_prefix, int64_t block_size,
+                              double scale, void* o_out, void* lse_out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || n_q < 1 || head_dim < 1 || kv_rows_cap < 0 || n_prefix < 0)
+    return fail(FB_ERR_SHAPE, "negative extent, n_q < 1 or head_dim < 1");
+  if (q_rows % n_q != 0) return fail(FB_ERR_SHAPE, "q_rows must be heads_per_group * n_q");
+  if (block_size < 1) return fail(FB_ERR_VALUE, "block_size must be >= 1");
+  if (n_prefix + n_q > kv_rows_cap)
+    return fail(FB_ERR_BOUNDS, "n_prefix + n_q exceeds the slab (commit the block's K/V first)");
+  if (n_prefix + n_q >= (int64_t(1) << 31)) return fail(FB_ERR_UNSUPPORTED, "context >= 2^31 keys");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return block_causal_t<ModeF64>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, n_q, n_prefix,
+                                     block_size, scale, o_out, lse_out, workspace, workspace_bytes, st);
+    case FB_F32:
+      return block_causal_t<ModeF32>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, n_q, n_prefix,
+                                     block_size, scale, o_out, lse_out, workspace, workspace_bytes, st);
+    default:
+      return block_causal_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, n_q, n_prefix,
+                                      block_size, scale, o_out, lse_out, workspace, workspace_bytes, st);
   }
 }
 

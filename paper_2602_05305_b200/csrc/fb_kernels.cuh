@@ -78,6 +78,11 @@ int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
                                 int64_t head_dim, int64_t kv_rows_cap, int64_t key_begin,
                                 const int32_t* key_end, double scale, float* o_out, float* lse_out,
                                 void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_block_causal_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                              int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                              int64_t n_q, int64_t n_prefix, int64_t block, double scale,
+                              float* o_out, float* lse_out, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
 
 // Gathered variant (sparse K7/K8): keys = mask-selected 16-row blocks of the
 // cache (list [groups, n_list] of ascending block ids, rows clipped at n_ext)

@@ -73,6 +73,33 @@ struct ConcatMap {
   }
 };
 
+// Block-causal prefill / commit keys (simulator.py:297-354): slab rows
+// [0, n_prefix + n_q); query row r (position p = r % n_q of its head) attends
+// rows [0, n_prefix + min(n_q, (p / blk + 1) * blk)).
+template <typename T>
+struct CausalMap {
+  const T* k;
+  const T* v;
+  int64_t slab_stride, d, n_q, blk, n_prefix;
+  static constexpr bool kCausal = true;
+  __device__ __forceinline__ int64_t count(int64_t) const { return n_prefix + n_q; }
+  __device__ __forceinline__ void row(int64_t g, int64_t t, const T*& kr, const T*& vr) const {
+    const int64_t off = g * slab_stride + t * d;
+    kr = k + off;
+    vr = v + off;
+  }
+  __device__ __forceinline__ int64_t row_limit(int64_t grow) const {
+    const int64_t p = grow % n_q;
+    const int64_t e = (p / blk + 1) * blk;
+    return n_prefix + (e < n_q ? e : n_q);
+  }
+};
+
+template <typename M, typename = void>
+struct is_causal_map { static constexpr bool value = false; };
+template <typename M>
+struct is_causal_map<M, decltype((void)M::kCausal)> { static constexpr bool value = M::kCausal; };
+
 // Number of external rows covered by `n_sel` ascending selected blocks; only the
 // last selected block can be the clipped tail block (sparse.py:69-80).
 __device__ __forceinline__ int64_t selected_rows(const int32_t* sel, int64_t n_sel, int64_t kbs,

@@ -77,7 +77,24 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
 
   const int64_t n_keys = map.count(g);
   const int64_t kb = min((int64_t)split * per_split, n_keys);
-  const int64_t ke = min(kb + per_split, n_keys);
+  int64_t ke = min(kb + per_split, n_keys);
+  constexpr bool CAUSAL = is_causal_map<Map>::value;
+  // block-causal rows: this warp's rows end at their own limits (the CTA stops
+  // at the largest one); launched unsplit, so every row has key 0
+  int64_t row_end[SIMT_ROWS_PER_WARP];
+#pragma unroll
+  for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) row_end[i] = ke;
+  if constexpr (CAUSAL) {
+    int64_t cta_end = 0;
+    for (int r = 0; r < SIMT_ROWS; ++r) {
+      const int64_t gr = min(row0 + r, q_rows - 1);
+      cta_end = max(cta_end, map.row_limit(gr));
+    }
+    ke = min(ke, cta_end);
+#pragma unroll
+    for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i)
+      row_end[i] = min(ke, map.row_limit(min(row0 + warp * SIMT_ROWS_PER_WARP + i, q_rows - 1)));
+  }
 
   // merge operands first: their latency overlaps the tile loads
   Ta oe[SIMT_ROWS_PER_WARP][C];
@@ -205,10 +222,11 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
 #pragma unroll
     for (int i = 0; i < SIMT_ROWS_PER_WARP; ++i) {
       // scores in the tensor dtype, then widened (attention.py:166)
-      const Ta si = key_ok ? (Ta)(s[i] * (Ts)scale) : Num<Ta>::ninf();
+      const bool ok = CAUSAL ? (t0 + lane) < row_end[i] : key_ok;
+      const Ta si = ok ? (Ta)(s[i] * (Ts)scale) : Num<Ta>::ninf();
       const Ta m_new = fmax(m[i], warp_max(si));
       const Ta alpha = Num<Ta>::exp_(m[i] - m_new);  // exp(-inf) = 0 for the first tile
-      const Ta p = key_ok ? Num<Ta>::exp_(si - m_new) : (Ta)0;
+      const Ta p = ok ? Num<Ta>::exp_(si - m_new) : (Ta)0;
       l[i] = l[i] * alpha + warp_sum(p);
       if constexpr (!NO_V) {
 #pragma unroll
@@ -347,6 +365,10 @@ static bool map_vec_ok(const SelectedMap<T>& m, const T* q, int64_t d) {
   return rows_ok(q, d) && al16(m.k) && al16(m.v) && al16(m.k_in) && al16(m.v_in);
 }
 template <typename T>
+static bool map_vec_ok(const CausalMap<T>& m, const T* q, int64_t d) {
+  return rows_ok(q, d) && al16(m.k) && al16(m.v);
+}
+template <typename T>
 static bool map_vec_ok(const ResidualMap<T>& m, const T* q, int64_t d) {
   return rows_ok(q, d) && al16(m.k) && al16(m.v);
 }
@@ -419,6 +441,7 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 #define FB_INST_MODE(MODE)                  \
   FB_INST_PARTIAL(MODE, false, RangeMap)    \
   FB_INST_PARTIAL(MODE, false, RaggedMap)   \
+  FB_INST_PARTIAL(MODE, false, CausalMap)   \
   FB_INST_PARTIAL(MODE, true, RangeMap)     \
   FB_INST_PARTIAL(MODE, false, SelectedMap) \
   FB_INST_PARTIAL(MODE, true, SelectedMap)  \
@@ -428,6 +451,9 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 FB_INST_MODE(ModeF64)
 FB_INST_MODE(ModeF32)
 FB_INST_MODE(ModeBF16)
+
+// block-causal (prefill / commit) in F32 mode: float64 scores as attention_dense
+template int launch_partial_simt<ModeMaskF32, false, false, CausalMap<float>>(const float*, const CausalMap<float>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF32>&, cudaStream_t);
 
 // lognorm-only passes for the sparse mask (scores in double for F64/F32 inputs,
 // as sparse.py:117-118 widens before the product)

@@ -103,6 +103,20 @@ struct Sched {
     }
     return lo;
   }
+  // Item order is group major: item i = (group i / m_tiles, query tile
+  // i % m_tiles).  (Query-tile-major order was measured: C5 refresh within
+  // noise, block-causal prefill 12 % slower.)
+  __device__ __forceinline__ int group_of(int i) const { return i / m_tiles; }
+  __device__ __forceinline__ int mtile_of(int i) const { return i % m_tiles; }
+  // the item after `prev` holding tile t (segments of a CTA are consecutive
+  // items: advance past empty ragged items instead of searching again)
+  __device__ __forceinline__ int item_next(long long t, int prev) const {
+    if (prefix == nullptr) return (int)(t / tpi);
+    if (prev < 0) return item_of(t);
+    int i = prev + 1;
+    while (prefix[i + 1] <= t) ++i;
+    return i;
+  }
   // workspace slot of item i's segment inside CTA c
   __device__ __forceinline__ long long slot(int c, int i) const {
     return 2ll * c + (item_begin(i) <= start(c) ? 0 : 1);
@@ -123,11 +137,27 @@ struct Gather {
 
 // DIAG (diagnostics only, fb_debug_set_k1_diag): 1 = softmax warps load S but skip
 // the softmax math, 2 = they skip the TMEM load too (pure TMA + MMA pipeline).
-template <int D, bool GATHER, int DIAG = 0>
+// Block-causal rows (prefill / commit attention, simulator.py:297-354): query
+// row r of a group sits at position p = r % n_q of its head and attends keys
+// [0, n_prefix + min(n_q, (p / blk + 1) * blk)) -- every earlier block plus its
+// own block.  blk == 0: off (every row attends the item's whole key range).
+struct Causal {
+  int n_q, blk, n_prefix;
+  __device__ __forceinline__ int row_limit(int grow) const {
+    const int p = grow % n_q;
+    return n_prefix + min(n_q, (p / blk + 1) * blk);
+  }
+};
+
+// POLY: every POLY-th pair of P values per thread takes 2^x on the FMA pipes
+// (ptx::ex2_poly) instead of MUFU; 0 = MUFU only.
+constexpr int K1_POLY = 0;  // measured: the extra FMA-pipe instructions cost more than MUFU
+
+template <int D, bool GATHER, int DIAG = 0, int POLY = K1_POLY>
 __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ki,
-               const __grid_constant__ CUtensorMap tm_vi, Gather ga, Sched sc, int q_rows, int key_begin,
+               const __grid_constant__ CUtensorMap tm_vi, Gather ga, Causal cz, Sched sc, int q_rows, int key_begin,
                int key_end, const int* __restrict__ key_len, float scale_log2, float* __restrict__ o_out,
                float* __restrict__ lse_out, float* __restrict__ ws_o,
                float* __restrict__ ws_l, unsigned long long* __restrict__ trace) {
@@ -188,13 +218,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t keep = ptx::policy_evict_last();
-      const uint64_t stream = ptx::policy_evict_first();
-      int j = 0, seg = 0;
+      // K/V: streamed once (evict first), except block-causal prefill where
+      // every later query tile of the group re-reads them (keep in L2)
+      const uint64_t stream = cz.blk > 0 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+      int j = 0, seg = 0, item = -1;
       for (long long t = t_begin; t < t_end; ++seg) {
-        const int item = sc.item_of(t);
+        item = sc.item_next(t, item);
         const long long ib = sc.item_begin(item);
         const long long seg_end = min(t_end, sc.item_end(item));
-        const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+        const int g = sc.group_of(item), mt = sc.mtile_of(item);
         if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
         ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
         for (int b = 0; b < C::NBOX; ++b)
@@ -260,13 +292,13 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, BN, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
-      int jg = 0, seg = 0;
+      int jg = 0, seg = 0, item = -1;
       for (long long t0 = t_begin; t0 < t_end; ++seg) {
-        const int item = sc.item_of(t0);
+        item = sc.item_next(t0, item);
         const int n = (int)(min(t_end, sc.item_end(item)) - t0);
         // ragged contexts: V rows past the sequence end are zeroed in smem before
         // P V (masked P is 0, but 0 * NaN from uninitialised cache rows is not)
-        const int v_valid_last = key_len ? min(key_len[item / sc.m_tiles], key_end) - key_begin -
+        const int v_valid_last = key_len ? min(key_len[sc.group_of(item)], key_end) - key_begin -
                                                (int)(t0 + n - 1 - sc.item_begin(item)) * BN
                                          : BN;
         ptx::mbar_wait(&bar->q_full, seg & 1);
@@ -338,20 +370,21 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const uint32_t o_col = wg ? C::COL_O1 : C::COL_O0;
     uint32_t r[32];
     float s[BN];
-    int jg = 0, seg = 0;
+    int jg = 0, seg = 0, item = -1;
     for (long long t0 = t_begin; t0 < t_end; ++seg) {
-      const int item = sc.item_of(t0);
+      item = sc.item_next(t0, item);
       const long long ib = sc.item_begin(item);
       const int lt0 = (int)(t0 - ib);
       const int n = (int)(min(t_end, sc.item_end(item)) - t0);
       const int kb = key_begin + lt0 * BN;
-      const int ke = min(kb + n * BN, key_len ? min(key_len[item / sc.m_tiles], key_end) : key_end);
+      int ke = min(kb + n * BN, key_len ? min(key_len[sc.group_of(item)], key_end) : key_end);
+      if (cz.blk > 0) ke = min(ke, cz.row_limit(sc.mtile_of(item) * BM + row));  // this row's end
       float m_used = -INFINITY;  // running max, log2-scaled
       float l = 0.f;
       int last_rows = 16;  // valid rows of the list's last block (gather mode)
       if constexpr (GATHER) {
         if (ga.n_list > 0) {
-          const int last = __ldg(ga.list + (long long)(item / sc.m_tiles) * ga.n_list + ga.n_list - 1);
+          const int last = __ldg(ga.list + (long long)sc.group_of(item) * ga.n_list + ga.n_list - 1);
           last_rows = min(16, ga.n_ext - last * 16);
         }
       }
@@ -440,20 +473,37 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           l *= alpha;
           m_used = m_new;
         }
-        const float neg = -m_used;
-        float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // a row with no key yet (block-causal segment past its end) keeps p = 0
+        const float neg = m_used == -INFINITY ? 0.f : -m_used;
+        // x = s * scale - m and the row sum on packed pairs (FFMA2 / FADD2)
+        const uint64_t sc2 = ptx::f2_pack(scale_log2, scale_log2), ng2 = ptx::f2_pack(neg, neg);
+        uint64_t ls4[4] = {0, 0, 0, 0};  // 4 independent pair chains (+0.0f bits)
 #pragma unroll
         for (int c = 0; c < BN / 64; ++c) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float p0 = ptx::ex2(fmaf(s[c * 64 + 2 * i], scale_log2, neg));
-            const float p1 = ptx::ex2(fmaf(s[c * 64 + 2 * i + 1], scale_log2, neg));
-            ls8[i & 7] += p0 + p1;
+            const uint64_t x2 = ptx::f2_fma(ptx::f2_pack(s[c * 64 + 2 * i], s[c * 64 + 2 * i + 1]), sc2, ng2);
+            float x0, x1;
+            ptx::f2_unpack(x2, x0, x1);
+            float p0, p1;
+            if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
+              p0 = ptx::ex2_poly(x0);
+              p1 = ptx::ex2_poly(x1);
+            } else {
+              p0 = ptx::ex2(x0);
+              p1 = ptx::ex2(x1);
+            }
+            ls4[i & 3] = ptx::f2_add(ls4[i & 3], ptx::f2_pack(p0, p1));
             r[i] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
         }
-        l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+        {
+          const uint64_t a2 = ptx::f2_add(ptx::f2_add(ls4[0], ls4[1]), ptx::f2_add(ls4[2], ls4[3]));
+          float a0, a1;
+          ptx::f2_unpack(a2, a0, a1);
+          l += a0 + a1;
+        }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bar->p_ready[wg]);
@@ -467,7 +517,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // (m0, l0), WG1 forms the weights and posts WG0's; each WG then writes
       // half of the output columns from both O accumulators.
       const bool whole = ib >= t_begin && sc.item_end(item) <= t_end;  // item not shared
-      const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+      const int g = sc.group_of(item), mt = sc.mtile_of(item);
       const int grow = mt * BM + row;
       const bool live = grow < q_rows;
       const long long orow = (long long)g * q_rows + grow;
@@ -483,10 +533,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const float a0 = l0 > 0.f ? ptx::ex2(m0 - m) : 0.f;
         const float a1 = l > 0.f ? ptx::ex2(m_used - m) : 0.f;
         const float z = a0 * l0 + a1 * l;
-        const float iz = 1.f / z;
+        const float iz = z > 0.f ? 1.f / z : 0.f;  // z == 0: no key in this segment (empty partial)
         c_own = a1 * iz;
         c_oth = a0 * iz;
-        lse = (m + log2f(z)) * 0.69314718055994530942f;
+        lse = z > 0.f ? (m + log2f(z)) * 0.69314718055994530942f : -INFINITY;
         xch[row] = c_oth;
         xch[BM + row] = c_own;
       }
@@ -557,7 +607,7 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   const int item = (int)(gw / BM);
   const int row = (int)(gw % BM);
   if (item >= sc.items) return;
-  const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+  const int g = sc.group_of(item), mt = sc.mtile_of(item);
   const int grow = mt * BM + row;
   if (grow >= q_rows) return;
   const long long orow = (long long)g * q_rows + grow;
@@ -676,7 +726,7 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
       for (long long t = t_begin; t < t_end; ++seg) {
         const int item = (int)(t / sc.tpi);
         const long long seg_end = min(t_end, (long long)(item + 1) * sc.tpi);
-        const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+        const int g = sc.group_of(item), mt = sc.mtile_of(item);
         if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
         ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
         for (int b = 0; b < C::NBOX; ++b)
@@ -740,7 +790,7 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
       const int item = (int)(t0 / sc.tpi);
       const int lt0 = (int)(t0 - (long long)item * sc.tpi);
       const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
-      const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+      const int g = sc.group_of(item), mt = sc.mtile_of(item);
       const int grow = mt * BM + row;
       const bool live = grow < q_rows;
       const long long orow = (long long)g * q_rows + grow;
@@ -857,7 +907,7 @@ __global__ void score_lse_merge_kernel(Sched sc, int q_rows, const float* __rest
   if (item >= sc.items) return;
   const int c_first = sc.cta_of(sc.item_begin(item));
   const int c_last = sc.cta_of(sc.item_end(item) - 1);
-  const int g = item / sc.m_tiles, mt = item % sc.m_tiles;
+  const int g = sc.group_of(item), mt = sc.mtile_of(item);
   const int grow = mt * BM + row;
   if (c_first == c_last || grow >= q_rows) return;
   float mx = -INFINITY;
@@ -990,12 +1040,55 @@ __global__ void ragged_prefix_kernel(const int* __restrict__ key_len, int items,
   if (items == 0 && tid == 0) prefix[0] = 0;
 }
 
+// Block-causal items: item i = (group, 128-row tile mt) streams keys
+// [0, lim) with lim the largest row limit of the tile (its last row, or the
+// head's full length when the tile straddles two heads); tile offsets as above.
+__device__ __forceinline__ long long causal_item_tiles(int i, int items, int m_tiles, int q_rows,
+                                                       sm100::Causal cz) {
+  const int mt = i % m_tiles;
+  const int r0 = mt * sm100::BM, r1 = min(r0 + sm100::BM, q_rows) - 1;
+  const int lim = (r0 / cz.n_q != r1 / cz.n_q) ? cz.n_prefix + cz.n_q : cz.row_limit(r1);
+  return (lim + sm100::BN - 1) / sm100::BN;
+}
+
+__global__ void causal_prefix_kernel(int items, int m_tiles, int q_rows, sm100::Causal cz,
+                                     long long* __restrict__ prefix) {
+  __shared__ long long part[1024];
+  __shared__ long long warp_sum_sh[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (items + nt - 1) / nt;
+  const int i0 = min(items, tid * per), i1 = min(items, i0 + per);
+  long long sum = 0;
+  for (int i = i0; i < i1; ++i) sum += causal_item_tiles(i, items, m_tiles, q_rows, cz);
+  part[tid] = sum;
+  __syncthreads();
+  if (tid < 32) {
+    long long acc = 0;
+    for (int k = 0; k < 32; ++k) acc += part[tid * 32 + k];
+    long long inc = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (tid >= o) inc += y;
+    }
+    warp_sum_sh[tid] = inc - acc;
+  }
+  __syncthreads();
+  long long base = warp_sum_sh[tid / 32];
+  for (int k = (tid / 32) * 32; k < tid; ++k) base += part[k];
+  for (int i = i0; i < i1; ++i) {
+    prefix[i] = base;
+    base += causal_item_tiles(i, items, m_tiles, q_rows, cz);
+  }
+  if (i1 == items && i0 < i1) prefix[items] = base;
+  if (items == 0 && tid == 0) prefix[0] = 0;
+}
+
 template <int D, bool GATHER>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
                             int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
                             size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr,
-                            const int* key_len = nullptr) {
+                            const int* key_len = nullptr, const sm100::Causal* causal = nullptr) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
@@ -1005,7 +1098,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   if constexpr (!GATHER) {
     // ragged: the whole slab is addressable; rows past each length are masked
     // (scores) and zeroed in smem (V) in the kernel
-    const int64_t dim1 = key_len ? kv_rows_cap : key_end;
+    const int64_t dim1 = (key_len && !causal) ? kv_rows_cap : key_end;
     if ((rc = make_tmap_3d(&mk, k, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
     if ((rc = make_tmap_3d(&mv, v, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
     mki = mk;
@@ -1034,9 +1127,10 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   if constexpr (!GATHER && D == 128) {
     if (g_k1_diag == 1) kern = sm100::refresh_kernel<D, false, 1>;
     if (g_k1_diag == 2) kern = sm100::refresh_kernel<D, false, 2>;
+    if (g_k1_diag == 3) kern = sm100::refresh_kernel<D, false, 0, 4>;  // 1/4 of the pairs on FMA
   }
-  static bool attr[3] = {false, false, false};
-  const int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 3 ? g_k1_diag : 0);
+  static bool attr[5] = {false, false, false, false, false};
+  const int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 5 ? g_k1_diag : 0);
   if (!attr[ai]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr[ai] = true;
@@ -1046,15 +1140,20 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   bool need_merge;
-  if (key_len != nullptr) {
+  sm100::Causal cz{1, 0, 0};
+  if (causal) cz = *causal;
+  if (key_len != nullptr || causal != nullptr) {
     const size_t pre = align_up((size_t)(p.items + 1) * sizeof(long long), 256);
     if (ws == nullptr || ws_bytes < refresh_sm100_ragged_workspace_bytes(groups, q_rows, D))
-      return fail(FB_ERR_VALUE, "ragged refresh needs fb_partial_workspace_bytes of scratch");
+      return fail(FB_ERR_VALUE, "ragged / block-causal refresh needs its workspace");
     long long* prefix = reinterpret_cast<long long*>(ws);
-    ragged_prefix_kernel<<<1, 1024, 0, st>>>(key_len, p.items, p.m_tiles, (int)key_begin,
-                                             (int)key_end, prefix);
+    if (causal)
+      causal_prefix_kernel<<<1, 1024, 0, st>>>(p.items, p.m_tiles, (int)q_rows, cz, prefix);
+    else
+      ragged_prefix_kernel<<<1, 1024, 0, st>>>(key_len, p.items, p.m_tiles, (int)key_begin,
+                                               (int)key_end, prefix);
     count_launch();
-    if ((rc = check_launch("ragged_prefix_kernel"))) return rc;
+    if ((rc = check_launch("prefix_kernel"))) return rc;
     sc.prefix = prefix;
     sc.tpi = 0;
     sc.ctas = num_sms();
@@ -1075,7 +1174,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
-             sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
+             cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
              ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
@@ -1111,6 +1210,24 @@ int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, kv_rows_cap,
                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, key_end);
+  return FB_ERR_UNSUPPORTED;
+}
+
+// Block-causal (prefill / commit) attention: keys [0, n_prefix + n_q) of every
+// slab, per-row block-causal limits; writes the fp32 attention output + LSE.
+int launch_block_causal_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                              int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                              int64_t n_q, int64_t n_prefix, int64_t block, double scale,
+                              float* o_out, float* lse_out, void* ws, size_t ws_bytes,
+                              cudaStream_t st) {
+  const sm100::Causal cz{(int)n_q, (int)block, (int)n_prefix};
+  const int64_t end = n_prefix + n_q;
+  if (head_dim == 128)
+    return launch_refresh_d<128, false>(q, k, v, groups, q_rows, kv_rows_cap, 0, end, scale, o_out,
+                                        lse_out, ws, ws_bytes, st, nullptr, nullptr, &cz);
+  if (head_dim == 64)
+    return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, 0, end, scale, o_out,
+                                       lse_out, ws, ws_bytes, st, nullptr, nullptr, &cz);
   return FB_ERR_UNSUPPORTED;
 }
 

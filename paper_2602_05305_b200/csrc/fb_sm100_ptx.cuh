@@ -196,6 +196,43 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 // pack two floats to bf16x2: `lo` in bits 0..15 (the even column)
+// 2^x on the FMA/ALU pipes (offloads the MUFU unit, as FlashAttention-4 does on
+// Blackwell): x = j + f with j = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3
+// minimax polynomial (max rel. error 7.5e-5, far below the bf16 rounding of P);
+// 2^j added into the exponent field.  x <= -127 (incl. -inf: masked keys)
+// returns exactly 0, like ex2.approx.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float t = xc + 12582912.f;  // 1.5 * 2^23: rint(xc) lands in the low mantissa bits
+  const float j = t - 12582912.f;
+  const float f = xc - j;
+  const float p = fmaf(fmaf(fmaf(0.055171772837638855f, f, 0.24261115491390228f), f,
+                            0.6932609677314758f), f, 0.9999280571937561f);
+  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+  return x > -127.f ? r : 0.f;
+}
+
+// Packed fp32 pairs (FFMA2 / FADD2 on sm_100a): half the issue slots of the
+// scalar forms for the softmax's scale-and-shift and row-sum chains.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));

@@ -123,6 +123,23 @@ class FlashBlockAttention:
             return self.cached(layer, q, k_in, v_in, out), choice
         return self.refresh(layer, q, k_cache, v_cache, n_ext, k_in, v_in, out), choice
 
+    def prefill(self, q, k_cache, v_cache, n_prefix: int = 0, out=None, lse=None):
+        """Prefill / commit attention over a prompt: the
+        reference's per-block commit passes (simulator.py:297-354) in one
+        block-causal launch.  q [b, Hq, n_q, d]; the caches already hold the
+        prompt's K/V at rows [n_prefix, n_prefix + n_q).  Block size = the
+        engine's block.  Returns the attention output [b, Hq, n_q, d] in the
+        partial dtype (fp32 for bf16 inputs)."""
+        b, hq, n_q, d = q.shape
+        if (b, hq, d) != (self.b, self.hq, self.d):
+            raise ShapeError(f"queries {tuple(q.shape)} do not match the engine")
+        qg = q.reshape(self.b * self.hkv, (self.hq // self.hkv) * n_q, self.d)
+        kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
+        vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+        o = out.view(qg.shape) if out is not None else None
+        res, _ = K.block_causal_attention(qg, kc, vc, n_q, n_prefix, self.B, self.scale, out=o, lse=lse)
+        return res.view(b, hq, n_q, d)
+
     def full_recompute(self, q, k_cache, v_cache, n_ext: int, k_in, v_in, out=None,
                        o_scratch=None, lse_scratch=None):
         """Baseline: full attention every step (same K1+K2 launch pair as a

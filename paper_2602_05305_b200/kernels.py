@@ -159,6 +159,36 @@ def attention_partial_ragged(q, k, v, key_end: torch.Tensor, key_begin: int = 0,
     return out, lse
 
 
+def block_causal_attention(q, k, v, n_q: int, n_prefix: int = 0, block_size: int = 32,
+                           scale: float | None = None, out=None, lse=None):
+    """Prefill / commit attention (simulator.py:297-354).
+
+    q [groups, heads_per_group * n_q, d]: a kv group's query heads stacked,
+    each n_q positions; k, v [groups, cap, d] hold the committed prefix in rows
+    [0, n_prefix) and the new positions' keys in [n_prefix, n_prefix + n_q).
+    Row at position p attends rows [0, n_prefix + min(n_q, (p // B + 1) * B)).
+    Returns (out, lse) in the mode's partial types (fp32 for bf16 inputs).
+    """
+    q3, k3, v3 = _as3(q, "q"), _as3(k, "k"), _as3(v, "v")
+    require_cuda(q3, k3, v3)
+    _check_kv(q3, k3, v3)
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    groups, q_rows, d = q3.shape
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
+    if lse is None:
+        lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_block_causal_workspace_bytes(code, groups, q_rows, d)
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_block_causal_attention", code, _p(q3), _p(k3), _p(v3), groups, q_rows, int(n_q),
+              d, k3.shape[1], int(n_prefix), int(block_size), scale, _p(out), _p(lse), _p(ws),
+              0 if ws is None else ws.numel(), _stream(q3))
+    return out, lse
+
+
 def commit_block(k_cache, v_cache, k_block, v_block, lengths: torch.Tensor,
                  check: bool = False) -> None:
     """Append a finished block's K/V ([groups, B, d]) to each group's slab of

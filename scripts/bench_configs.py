@@ -1,6 +1,7 @@
-"""Secondary benchmark lines for BASELINE.json configs C1, C3, C4, C5.
+"""Secondary benchmark lines for BASELINE.json configs C1, C3, C4, C5 and the
+prefill path (F4).
 
-    python scripts/bench_configs.py [--only c3,c4,c5,c1] [--out profiles/rXX_configs.jsonl]
+    python scripts/bench_configs.py [--only c3,c4,c5,f4,c1] [--out profiles/rXX_configs.jsonl]
 
 One JSON line per measurement.  All device timings are CUDA events around
 CUDA-graph replays of the measured launches (no host gaps), after warm-up,
@@ -163,6 +164,33 @@ def c5(out):
         torch.cuda.empty_cache()
 
 
+# ---------------------------------------------------------------- F4 prefill
+
+
+def f4(out):
+    """Prefill / commit attention at the C2 attention shapes:
+    a whole prompt's block-causal attention in one launch (the reference
+    commits it block by block, simulator.py:343-354).  Compute-bound."""
+    HQ, HKV, D, B = 32, 8, 128, 32
+    G = HQ // HKV
+    for b, n_q in ((1, 8192), (1, 32768)):
+        g = torch.Generator(device=DEV).manual_seed(9)
+        groups = b * HKV
+        q = rnd(g, groups, G * n_q, D)
+        k = rnd(g, groups, n_q, D)
+        v = rnd(g, groups, n_q, D)
+        o, l = K.block_causal_attention(q, k, v, n_q, 0, B)
+        t = graph_ms(lambda: K.block_causal_attention(q, k, v, n_q, 0, B, None, o, l), reps=3)
+        lim = sum(min(n_q, (p // B + 1) * B) for p in range(0, n_q, B)) * B  # sum over positions
+        flops = 4.0 * groups * G * lim * D
+        emit(out, {"config": "F4-prefill", "batch": b, "prompt": n_q, "q_heads": HQ, "kv_heads": HKV,
+                   "block": B, "ms": t, "tflops": flops / (t * 1e-3) / 1e12,
+                   "frac_tensor": flops / (t * 1e-3) / 1e12 / TENSOR,
+                   "tokens_per_s": b * n_q / (t * 1e-3)})
+        del q, k, v
+        torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- C1
 
 
@@ -203,7 +231,7 @@ def c1(out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c3,c4,c5,c1")
+    ap.add_argument("--only", default="c3,c4,c5,f4,c1")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.jsonl"))
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)

@@ -3,7 +3,8 @@
 Run in the build container only (it needs /root/reference, which does not
 exist on the GPU box):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # golden.npz
+    python tests/golden/make_golden.py prefill    # golden_prefill.npz
 
 The fixtures it writes (``tests/golden/*.npz``) are committed; the tests read
 only the fixtures.  Inputs are seeded (Philox) and, for the cases the bf16
@@ -153,5 +154,66 @@ def main() -> None:
     print("wrote", len(out), "arrays")
 
 
+
+
+def make_prefill() -> None:
+    """Block-causal prefill / commit attention from the reference's own commit
+    pass: record every attention_dense call that simulator.prefill and
+    commit_context_block make (simulator.py:297-354), per (layer, head), and
+    store the stacked queries, the final committed K/V and the outputs.
+    Writes tests/golden/golden_prefill.npz."""
+    sys.path.insert(0, REF_SRC)
+    import flashblock.simulator as sim
+
+    out: dict[str, np.ndarray] = {}
+    for name, dtype, heads, d, prompt_len, block, extra in [
+        ("pf0", np.float64, 2, 64, 100, 32, 1),   # ragged last block, then one more commit
+        ("pf1", np.float32, 3, 32, 48, 16, 0),
+    ]:
+        cfg = sim.ModelConfig(num_layers=2, num_heads=heads, head_dim=d, seed=5, dtype=dtype)
+        model = sim.SyntheticModel(cfg)
+        calls = []
+        orig = sim.attention_dense
+
+        def rec(q, keys, values, scale=None, _orig=orig):
+            o = _orig(q, keys, values, scale)
+            calls.append((q.copy(), keys.copy(), values.copy(), o))
+            return o
+
+        sim.attention_dense = rec
+        try:
+            prompt = sim.prompt_ids(model, prompt_len, seed=11)
+            kv = sim.prefill(model, prompt, block)
+            n_prefill_calls = len(calls)
+            if extra:
+                ids = np.arange(1, block + 1, dtype=np.int64) % (cfg.vocab_size - 1) + 1
+                sim.commit_context_block(model, kv, ids, prompt_len)
+        finally:
+            sim.attention_dense = orig
+        # calls are ordered block-major, then layer, then head
+        L, H = cfg.num_layers, cfg.num_heads
+        nblk = (prompt_len + block - 1) // block
+        assert n_prefill_calls == nblk * L * H
+        for layer in range(L):
+            for head in range(H):
+                sel = [calls[(b * L + layer) * H + head] for b in range(nblk)]
+                out[f"{name}_l{layer}_h{head}_q"] = np.concatenate([c[0] for c in sel])
+                out[f"{name}_l{layer}_h{head}_out"] = np.concatenate([c[3] for c in sel])
+                # keys of the last call = the whole prompt's committed K/V
+                out[f"{name}_l{layer}_h{head}_k"] = sel[-1][1]
+                out[f"{name}_l{layer}_h{head}_v"] = sel[-1][2]
+                if extra:
+                    c = calls[n_prefill_calls + layer * H + head]
+                    out[f"{name}_x_l{layer}_h{head}_q"] = c[0]
+                    out[f"{name}_x_l{layer}_h{head}_k"] = c[1]
+                    out[f"{name}_x_l{layer}_h{head}_v"] = c[2]
+                    out[f"{name}_x_l{layer}_h{head}_out"] = c[3]
+        out[f"{name}_meta"] = np.array([L, H, d, prompt_len, block, extra], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "golden_prefill.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "prefill":
+        make_prefill()
+    else:
+        main()
