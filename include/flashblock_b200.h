@@ -125,6 +125,34 @@ FB_API int fb_block_causal_attention(int dtype, const void* q, const void* k, co
 FB_API size_t fb_block_causal_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
                                               int64_t head_dim);
 
+/* K1 over a subset of groups -- the head-gated refresh (policy.py:84-94 with
+ * per-head gates, simulator.py:401-405): only the groups listed in
+ * group_list (DEVICE int32 [n_list], distinct indices < groups) are refreshed;
+ * every other group's rows of o_out / lse_out are left untouched.  Same
+ * arguments and partial types as fb_attention_partial otherwise; scratch from
+ * fb_partial_workspace_bytes(dtype, n_list, ...).  F64 and BF16 modes (F32:
+ * FB_ERR_UNSUPPORTED). */
+FB_API int fb_attention_partial_groups(int dtype, const void* q, const void* k, const void* v,
+                                       int64_t groups, int64_t q_rows, int64_t head_dim,
+                                       int64_t kv_rows_cap, int64_t key_begin, int64_t key_end,
+                                       const int32_t* group_list, int64_t n_list, double scale,
+                                       void* o_out, void* lse_out, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+
+/* Cross-step similarity (head-gate calibration, policy.py:188-246; stability
+ * study, analysis.py:28-148).  a, b: [heads, rows, head_dim] partial outputs
+ * of the same rows at two steps, dtype FB_F64 / FB_F32 / FB_BF16 (the array
+ * type).  row_cos[heads*rows] (optional): cosine of row r of a and b, 0 when
+ * either norm < 1e-12 (linalg.py:68-80); head_mean[heads] (optional): its
+ * mean over the rows.  Float64 accumulation, fixed reduction order. */
+FB_API int fb_row_cosine(int dtype, const void* a, const void* b, int64_t heads, int64_t rows,
+                         int64_t head_dim, double* row_cos, double* head_mean, void* stream);
+/* All-pairs cosine between the rows of a later and an earlier step, per head:
+ * out[heads, rows, rows], entry (i, j) = cos(later_i, earlier_j); rows with
+ * norm < 1e-12 give 0 (pairwise_step_similarity, analysis.py:28-51). */
+FB_API int fb_pairwise_cosine(int dtype, const void* later, const void* earlier, int64_t heads,
+                              int64_t rows, int64_t head_dim, double* out, void* stream);
+
 /* Device-side block commit (kv_cache.py:121-144; simulator.py:327-333):
  * append a finished block's K/V rows ([groups, block_rows, head_dim]) to each
  * group's slab at row lengths[g] (device int32 [groups]), then advance

@@ -317,3 +317,51 @@ def refresh_schedule(block_size: int, steps: int, per_step: int, tau: int,
     sched = unmask_schedule(block_size, steps, per_step)
     return [decide(mode, tau, s > 0, s == 0, sched[s - 1] if s else 0)
             for s in range(steps)]
+
+
+# ---------------------------------------------------------------- similarity
+
+ZERO_NORM_EPS = 1e-12  # linalg.py:25
+
+
+def cosine_similarity(u, v) -> float:
+    """Cosine of two 1-D vectors, 0.0 if either norm < 1e-12 (linalg.py:68-80)."""
+    nu = float(np.linalg.norm(u))
+    nv = float(np.linalg.norm(v))
+    if nu < ZERO_NORM_EPS or nv < ZERO_NORM_EPS:
+        return 0.0
+    return float(np.dot(u, v) / (nu * nv))
+
+
+def pairwise_step_similarity(out_s, out_s1) -> np.ndarray:
+    """All-pairs cosine, entry (i, j) = cos(out_s1[i], out_s[j]) in float64;
+    rows with near-zero norm map to 0 (analysis.py:28-51)."""
+    a = np.asarray(out_s1, dtype=np.float64)
+    b = np.asarray(out_s, dtype=np.float64)
+    na = np.linalg.norm(a, axis=1)
+    nb = np.linalg.norm(b, axis=1)
+    den = np.outer(na, nb)
+    sim = np.zeros_like(den)
+    ok = den >= ZERO_NORM_EPS * ZERO_NORM_EPS
+    np.divide(a @ b.T, den, out=sim, where=ok)
+    sim[na < ZERO_NORM_EPS, :] = 0.0
+    sim[:, nb < ZERO_NORM_EPS] = 0.0
+    return sim
+
+
+def gate_stats(runs) -> dict:
+    """Head-gate statistics (policy.py:222-246): runs maps (layer, head) to a
+    list (one entry per rollout) of step-ordered external partial outputs
+    [steps, rows, d]; for every adjacent step pair the row-mean cosine is one
+    sample; returns {(layer, head): (mean, min)} over all samples."""
+    stats = {}
+    for key, rollouts in runs.items():
+        vals = []
+        for outs in rollouts:
+            for step in range(len(outs) - 1):
+                prev, curr = outs[step], outs[step + 1]
+                vals.append(float(np.mean([cosine_similarity(curr[r], prev[r])
+                                           for r in range(curr.shape[0])])))
+        stats[key] = (float(np.mean(vals)), float(np.min(vals)))
+    return stats
+

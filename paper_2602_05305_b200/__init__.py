@@ -10,10 +10,11 @@ from .attention import (AttnPartial, CacheEntry, DegenerateInputError, ExternalA
                         ReusePreconditionError, attention_dense, attention_partial,
                         attention_streamed, attention_with_reuse, combine_partials,
                         merge_partials)
+from .analysis import HeadGateCalibrator, pairwise_step_similarity
 from .engine import FlashBlockAttention, KVCache
 from .errors import BoundsError, ShapeError, StalenessError
-from .policy import (MODES, Decision, ReuseConfig, count_updated_tokens, decide,
-                     refresh_schedule, unmask_schedule)
+from .policy import (MODES, CalibrationError, Decision, HeadGate, HeadGateTable, ReuseConfig,
+                     count_updated_tokens, decide, refresh_schedule, unmask_schedule)
 from .sparse import SparseMask, build_sparse_mask, sparse_attention_with_residual
 
 __version__ = "0.1.0"
@@ -24,5 +25,6 @@ __all__ = [
     "attention_with_reuse", "combine_partials", "merge_partials", "FlashBlockAttention", "KVCache",
     "BoundsError", "ShapeError", "StalenessError", "MODES", "Decision", "ReuseConfig",
     "count_updated_tokens", "decide", "refresh_schedule", "unmask_schedule", "SparseMask",
-    "build_sparse_mask", "sparse_attention_with_residual",
+    "build_sparse_mask", "sparse_attention_with_residual", "CalibrationError", "HeadGate",
+    "HeadGateTable", "HeadGateCalibrator", "pairwise_step_similarity",
 ]

@@ -20,7 +20,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "fb200")
 LIB = os.path.join(PKG, "libfb200.so")
-SOURCES = ["fb_capi.cu", "fb_simt.cu", "fb_sm100.cu", "fb_sm100_k2.cu", "fb_sparse.cu"]
+SOURCES = ["fb_capi.cu", "fb_simt.cu", "fb_sm100.cu", "fb_sm100_k2.cu", "fb_sparse.cu",
+           "fb_similarity.cu"]
 GENCODE = "arch=compute_100a,code=sm_100a"
 
 

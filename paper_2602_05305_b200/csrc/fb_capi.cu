@@ -445,6 +445,41 @@ static int block_causal_t(const void* qv, const void* kv, const void* vv, int64_
   }
 }
 
+// K1 over a device list of groups (head-gated refresh).  F64 / BF16 write
+// directly (SIMT or tcgen05); F32 would need a scattered combine: unsupported.
+template <typename Mode>
+static int attention_partial_groups_t(const void* qv, const void* kv, const void* vv, int64_t groups,
+                                      int64_t q_rows, int64_t d, int64_t cap, int64_t kb, int64_t ke,
+                                      const int32_t* glist, int64_t n_list, double scale, void* o_out,
+                                      void* lse_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  using Tin = typename Mode::Tin;
+  using Ta = typename Mode::Ta;
+  auto* q = reinterpret_cast<const Tin*>(qv);
+  auto* k = reinterpret_cast<const Tin*>(kv);
+  auto* v = reinterpret_cast<const Tin*>(vv);
+  auto* o = reinterpret_cast<typename Mode::To*>(o_out);
+  auto* l = reinterpret_cast<typename Mode::Tl*>(lse_out);
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (ke > kb && sm100_supported(d) && ke < (int64_t(1) << 31) && q_rows < (int64_t(1) << 31) &&
+        (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
+        (reinterpret_cast<uintptr_t>(v) % 16 == 0) && groups < 65536)
+      return launch_refresh_groups_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, glist, n_list,
+                                         scale, o, l, ws, ws_bytes, st);
+  }
+  constexpr bool direct_ok = std::is_same<Ta, typename Mode::To>::value &&
+                             std::is_same<Ta, typename Mode::Tl>::value;
+  if constexpr (direct_ok) {
+    RangeMap<Tin> map{k, v, cap * d, kb, ke, d};
+    MergeOut<Mode> none{};
+    return launch_partial_simt<Mode, false, false>(q, map, n_list, q_rows, d, int64_t(1) << 40, 1,
+                                                   scale, reinterpret_cast<Ta*>(o),
+                                                   reinterpret_cast<typename Mode::Tl*>(l), none, st,
+                                                   glist);
+  } else {
+    return fail(FB_ERR_UNSUPPORTED, "group-subset refresh is not built for F32 mode");
+  }
+}
+
 extern "C" {
 
 const char* fb_last_error(void) { return g_last_error.c_str(); }
@@ -507,6 +542,65 @@ int fb_commit_block(int dtype, void* k_cache, void* v_cache, int64_t groups, int
   return launch_commit_block(k_cache, v_cache, k_block, v_block, groups, kv_rows_cap,
                              head_dim * (int64_t)dtype_size(dtype), block_rows, lengths, overflow,
                              as_stream(stream));
+}
+
+int fb_attention_partial_groups(int dtype, const void* q, const void* k, const void* v,
+                                int64_t groups, int64_t q_rows, int64_t head_dim,
+                                int64_t kv_rows_cap, int64_t key_begin, int64_t key_end,
+                                const int32_t* group_list, int64_t n_list, double scale,
+                                void* o_out, void* lse_out, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0 || n_list < 0)
+    return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (n_list > groups) return fail(FB_ERR_SHAPE, "group list longer than the batch of groups");
+  if (key_begin < 0 || key_end < key_begin || key_end > kv_rows_cap)
+    return fail(FB_ERR_BOUNDS, "key range outside the slab");
+  if (n_list == 0 || q_rows == 0) return FB_OK;
+  if (group_list == nullptr) return fail(FB_ERR_VALUE, "group_list (device int32 [n_list]) is required");
+  if (head_dim > 256) return fail(FB_ERR_UNSUPPORTED, "head_dim > 256");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64:
+      return attention_partial_groups_t<ModeF64>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
+                                                 key_begin, key_end, group_list, n_list, scale, o_out,
+                                                 lse_out, workspace, workspace_bytes, st);
+    case FB_F32:
+      return attention_partial_groups_t<ModeF32>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
+                                                 key_begin, key_end, group_list, n_list, scale, o_out,
+                                                 lse_out, workspace, workspace_bytes, st);
+    default:
+      return attention_partial_groups_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap,
+                                                  key_begin, key_end, group_list, n_list, scale,
+                                                  o_out, lse_out, workspace, workspace_bytes, st);
+  }
+}
+
+int fb_row_cosine(int dtype, const void* a, const void* b, int64_t heads, int64_t rows,
+                  int64_t head_dim, double* row_cos, double* head_mean, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (heads < 0 || rows < 0 || head_dim < 1) return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (heads == 0) return FB_OK;
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64: return launch_row_cosine<double>(a, b, heads, rows, head_dim, row_cos, head_mean, st);
+    case FB_F32: return launch_row_cosine<float>(a, b, heads, rows, head_dim, row_cos, head_mean, st);
+    default: return launch_row_cosine<__nv_bfloat16>(a, b, heads, rows, head_dim, row_cos, head_mean, st);
+  }
+}
+
+int fb_pairwise_cosine(int dtype, const void* later, const void* earlier, int64_t heads, int64_t rows,
+                       int64_t head_dim, double* out, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (heads < 0 || rows < 0 || head_dim < 1) return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (heads == 0 || rows == 0) return FB_OK;
+  if (rows > 65535 * 16) return fail(FB_ERR_UNSUPPORTED, "too many rows for the all-pairs matrix");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64: return launch_pairwise_cosine<double>(later, earlier, heads, rows, head_dim, out, st);
+    case FB_F32: return launch_pairwise_cosine<float>(later, earlier, heads, rows, head_dim, out, st);
+    default: return launch_pairwise_cosine<__nv_bfloat16>(later, earlier, heads, rows, head_dim, out, st);
+  }
 }
 
 size_t fb_ragged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,

@@ -35,7 +35,8 @@ template <typename Mode, bool MERGE, bool NO_V, typename Map>
 int launch_partial_simt(const typename Mode::Tin* q, const Map& map, int64_t groups,
                         int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
                         double scale, typename Mode::Ta* po, typename Mode::Tl* pl,
-                        const MergeOut<Mode>& mo, cudaStream_t st);
+                        const MergeOut<Mode>& mo, cudaStream_t st,
+                        const int32_t* glist = nullptr);  // grid groups -> slabs (subset)
 
 template <typename Tp, typename Tlp, typename Ta, typename To, typename Tlo>
 int launch_combine(const CombineList& list, int64_t rows, int64_t head_dim, To* o_out, Tlo* l_out,
@@ -78,6 +79,11 @@ int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
                                 int64_t head_dim, int64_t kv_rows_cap, int64_t key_begin,
                                 const int32_t* key_end, double scale, float* o_out, float* lse_out,
                                 void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_refresh_groups_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                                int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                                int64_t key_begin, int64_t key_end, const int32_t* glist,
+                                int64_t n_list, double scale, float* o_out, float* lse_out, void* ws,
+                                size_t ws_bytes, cudaStream_t st);
 int launch_block_causal_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                               int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                               int64_t n_q, int64_t n_prefix, int64_t block, double scale,
@@ -115,5 +121,13 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
                                 const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
                                 float* o_int, float* lse_int, int32_t* empty, bool ext_early,
                                 cudaStream_t st);
+
+// cross-step similarity (fb_similarity.cu)
+template <typename T>
+int launch_row_cosine(const void* a, const void* b, int64_t heads, int64_t rows, int64_t d,
+                      double* row_cos, double* head_mean, cudaStream_t st);
+template <typename T>
+int launch_pairwise_cosine(const void* later, const void* earlier, int64_t heads, int64_t n,
+                           int64_t d, double* out, cudaStream_t st);
 
 }  // namespace fb

@@ -53,7 +53,8 @@ template <typename Mode, int D, bool MERGE, bool NO_V, typename Map>
 __global__ void __launch_bounds__(32 * SIMT_WARPS)
 partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, int64_t head_dim,
              int64_t per_split, typename Mode::Ta scale, typename Mode::Ta* po,
-             typename Mode::Tl* pl, int64_t rows_total, MergeOut<Mode> mo, bool vec) {
+             typename Mode::Tl* pl, int64_t rows_total, MergeOut<Mode> mo, bool vec,
+             const int32_t* __restrict__ glist) {
   using Tin = typename Mode::Tin;
   using Ts = typename Mode::Ts;
   using Ta = typename Mode::Ta;
@@ -70,7 +71,7 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
   __shared__ const Tin* kptr[SIMT_KT];
   __shared__ const Tin* vptr[SIMT_KT];
 
-  const int64_t g = blockIdx.z;
+  const int64_t g = glist != nullptr ? (int64_t)glist[blockIdx.z] : (int64_t)blockIdx.z;  // group subset
   const int split = blockIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * SIMT_ROWS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -377,7 +378,7 @@ template <typename Mode, int D, bool MERGE, bool NO_V, typename Map>
 static int launch_partial_d(const typename Mode::Tin* q, const Map& map, int64_t groups,
                             int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
                             double scale, typename Mode::Ta* po, typename Mode::Tl* pl,
-                            const MergeOut<Mode>& mo, cudaStream_t st) {
+                            const MergeOut<Mode>& mo, cudaStream_t st, const int32_t* glist) {
   constexpr size_t smem = simt_smem_bytes<D, typename Mode::Ts, typename Mode::Ta>();
   auto kern = partial_simt<Mode, D, MERGE, NO_V, Map>;
   static bool attr_set = false;
@@ -389,7 +390,7 @@ static int launch_partial_d(const typename Mode::Tin* q, const Map& map, int64_t
   const bool vec = map_vec_ok(map, q, head_dim);
   kern<<<grid, 32 * SIMT_WARPS, smem, st>>>(q, map, q_rows, head_dim, per_split,
                                             (typename Mode::Ta)scale, po, pl, groups * q_rows, mo,
-                                            vec);
+                                            vec, glist);
   count_launch();
   return check_launch("partial_simt");
 }
@@ -398,15 +399,15 @@ template <typename Mode, bool MERGE, bool NO_V, typename Map>
 int launch_partial_simt(const typename Mode::Tin* q, const Map& map, int64_t groups,
                         int64_t q_rows, int64_t head_dim, int64_t per_split, int splits,
                         double scale, typename Mode::Ta* po, typename Mode::Tl* pl,
-                        const MergeOut<Mode>& mo, cudaStream_t st) {
+                        const MergeOut<Mode>& mo, cudaStream_t st, const int32_t* glist) {
   if (head_dim <= 32)
-    return launch_partial_d<Mode, 32, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+    return launch_partial_d<Mode, 32, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st, glist);
   if (head_dim <= 64)
-    return launch_partial_d<Mode, 64, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+    return launch_partial_d<Mode, 64, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st, glist);
   if (head_dim <= 128)
-    return launch_partial_d<Mode, 128, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+    return launch_partial_d<Mode, 128, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st, glist);
   if (head_dim <= 256)
-    return launch_partial_d<Mode, 256, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st);
+    return launch_partial_d<Mode, 256, MERGE, NO_V>(q, map, groups, q_rows, head_dim, per_split, splits, scale, po, pl, mo, st, glist);
   return fail(FB_ERR_UNSUPPORTED, "head_dim > 256 is not supported");
 }
 
@@ -436,7 +437,7 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 #define FB_INST_PARTIAL(MODE, MERGE, MAP)                                                      \
   template int launch_partial_simt<MODE, MERGE, false, MAP<MODE::Tin>>(                       \
       const MODE::Tin*, const MAP<MODE::Tin>&, int64_t, int64_t, int64_t, int64_t, int, double, \
-      MODE::Ta*, MODE::Tl*, const MergeOut<MODE>&, cudaStream_t);
+      MODE::Ta*, MODE::Tl*, const MergeOut<MODE>&, cudaStream_t, const int32_t*);
 
 #define FB_INST_MODE(MODE)                  \
   FB_INST_PARTIAL(MODE, false, RangeMap)    \
@@ -453,13 +454,13 @@ FB_INST_MODE(ModeF32)
 FB_INST_MODE(ModeBF16)
 
 // block-causal (prefill / commit) in F32 mode: float64 scores as attention_dense
-template int launch_partial_simt<ModeMaskF32, false, false, CausalMap<float>>(const float*, const CausalMap<float>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF32>&, cudaStream_t);
+template int launch_partial_simt<ModeMaskF32, false, false, CausalMap<float>>(const float*, const CausalMap<float>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF32>&, cudaStream_t, const int32_t*);
 
 // lognorm-only passes for the sparse mask (scores in double for F64/F32 inputs,
 // as sparse.py:117-118 widens before the product)
-template int launch_partial_simt<ModeMaskF64, false, true, ConcatMap<double>>(const double*, const ConcatMap<double>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF64>&, cudaStream_t);
-template int launch_partial_simt<ModeMaskF32, false, true, ConcatMap<float>>(const float*, const ConcatMap<float>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF32>&, cudaStream_t);
-template int launch_partial_simt<ModeMaskBF16, false, true, ConcatMap<__nv_bfloat16>>(const __nv_bfloat16*, const ConcatMap<__nv_bfloat16>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskBF16>&, cudaStream_t);
+template int launch_partial_simt<ModeMaskF64, false, true, ConcatMap<double>>(const double*, const ConcatMap<double>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF64>&, cudaStream_t, const int32_t*);
+template int launch_partial_simt<ModeMaskF32, false, true, ConcatMap<float>>(const float*, const ConcatMap<float>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskF32>&, cudaStream_t, const int32_t*);
+template int launch_partial_simt<ModeMaskBF16, false, true, ConcatMap<__nv_bfloat16>>(const __nv_bfloat16*, const ConcatMap<__nv_bfloat16>&, int64_t, int64_t, int64_t, int64_t, int, double, double*, double*, const MergeOut<ModeMaskBF16>&, cudaStream_t, const int32_t*);
 
 // combine: (part out, part lse, accumulate, out, lse out)
 template int launch_combine<double, double, double, double, double>(const CombineList&, int64_t, int64_t, double*, double*, int32_t*, cudaStream_t);

@@ -79,6 +79,7 @@ struct Sched {
   int items;
   int ctas;
   const long long* prefix; // ragged item offsets, or nullptr
+  const int* glist;        // group subset (head-gated refresh): item group -> slab, or nullptr
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -106,7 +107,10 @@ struct Sched {
   // Item order is group major: item i = (group i / m_tiles, query tile
   // i % m_tiles).  (Query-tile-major order was measured: C5 refresh within
   // noise, block-causal prefill 12 % slower.)
-  __device__ __forceinline__ int group_of(int i) const { return i / m_tiles; }
+  __device__ __forceinline__ int group_of(int i) const {
+    const int gi = i / m_tiles;
+    return glist != nullptr ? __ldg(glist + gi) : gi;
+  }
   __device__ __forceinline__ int mtile_of(int i) const { return i % m_tiles; }
   // the item after `prev` holding tile t (segments of a CTA are consecutive
   // items: advance past empty ragged items instead of searching again)
@@ -1088,7 +1092,8 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
                             int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
                             size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr,
-                            const int* key_len = nullptr, const sm100::Causal* causal = nullptr) {
+                            const int* key_len = nullptr, const sm100::Causal* causal = nullptr,
+                            const int32_t* glist = nullptr, int64_t n_list = 0) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
@@ -1135,8 +1140,9 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr[ai] = true;
   }
-  RefreshPlan p = plan_refresh(groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
-  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};
+  // group subset: items over the listed groups only (tensor maps span all groups)
+  RefreshPlan p = plan_refresh(glist ? n_list : groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
+  sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr, glist};
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   bool need_merge;
@@ -1210,6 +1216,24 @@ int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, kv_rows_cap,
                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, key_end);
+  return FB_ERR_UNSUPPORTED;
+}
+
+// Head-gated refresh: K1 over a device list of groups only;
+// the other groups' outputs are left untouched.
+int launch_refresh_groups_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                                int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
+                                int64_t key_begin, int64_t key_end, const int32_t* glist,
+                                int64_t n_list, double scale, float* o_out, float* lse_out, void* ws,
+                                size_t ws_bytes, cudaStream_t st) {
+  if (head_dim == 128)
+    return launch_refresh_d<128, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
+                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, nullptr,
+                                        nullptr, glist, n_list);
+  if (head_dim == 64)
+    return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
+                                       scale, o_out, lse_out, ws, ws_bytes, st, nullptr, nullptr,
+                                       nullptr, glist, n_list);
   return FB_ERR_UNSUPPORTED;
 }
 

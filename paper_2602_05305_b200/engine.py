@@ -29,7 +29,7 @@ class FlashBlockAttention:
     def __init__(self, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
                  block_len: int, head_dim: int, device=None, dtype=torch.bfloat16,
                  out_dtype: torch.dtype | None = None, scale: float | None = None,
-                 config: ReuseConfig | None = None):
+                 config: ReuseConfig | None = None, recorder=None):
         if num_q_heads % num_kv_heads:
             raise ShapeError("num_q_heads must be a multiple of num_kv_heads")
         self.L, self.b, self.hq, self.hkv = num_layers, batch, num_q_heads, num_kv_heads
@@ -47,6 +47,9 @@ class FlashBlockAttention:
         self.lse_ext = torch.full((num_layers, groups, rows), -math.inf, dtype=self.lt, device=self.device)
         self.valid = [False] * num_layers
         self.block_id = 0
+        # optional HeadGateCalibrator: sees every refreshed external partial
+        self.recorder = recorder
+        self._glists: dict = {}
 
     # -- cache lifecycle (ExternalAttnCache.invalidate_all, simulator.py:562-563)
     def begin_block(self, block_id: int) -> None:
@@ -99,6 +102,8 @@ class FlashBlockAttention:
             res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
                                    self.out_dtype, out=o)
         self.valid[layer] = True
+        if self.recorder is not None:
+            self.recorder.observe(layer, self.o_ext[layer], self.B)
         return res.view(self.b, self.hq, self.B, self.d)
 
     def cached(self, layer: int, q, k_in, v_in, out=None):
@@ -139,6 +144,40 @@ class FlashBlockAttention:
         o = out.view(qg.shape) if out is not None else None
         res, _ = K.block_causal_attention(qg, kc, vc, n_q, n_prefix, self.B, self.scale, out=o, lse=lse)
         return res.view(b, hq, n_q, d)
+
+    def step_gated(self, layer: int, q, k_cache, v_cache, n_ext: int, k_in, v_in, *,
+                   first_visit: bool, updated_tokens: int, gates, out=None):
+        """Head-gated mode: every query head decides on its
+        own (decide with its gate, policy.py:71-94; simulator.py:399-405); a kv
+        group is refreshed when any of its query heads recomputes, the others
+        keep their cached external partial.  With 1:1 heads (G = 1) this is
+        the reference's per-(layer, head) behaviour exactly.  K1 runs on the
+        refreshed groups only (fb_attention_partial_groups), then K2 merges
+        every group with its external partial.  Returns (out, per-head
+        decisions)."""
+        heads = [decide(self.config, self.valid[layer], first_visit, updated_tokens,
+                        gates.is_enabled(layer, h)) for h in range(self.hq)]
+        kv_refresh = [any(heads[kv * self.G + j] is Decision.RECOMPUTE for j in range(self.G))
+                      for kv in range(self.hkv)]
+        if all(kv_refresh):
+            return self.refresh(layer, q, k_cache, v_cache, n_ext, k_in, v_in, out), heads
+        if not any(kv_refresh):
+            return self.cached(layer, q, k_in, v_in, out), heads
+        key = tuple(kv_refresh)
+        gl = self._glists.get(key)
+        if gl is None:
+            ids = [bi * self.hkv + kv for bi in range(self.b) for kv in range(self.hkv) if kv_refresh[kv]]
+            gl = torch.tensor(ids, dtype=torch.int32, device=self.device)
+            self._glists[key] = gl
+        qg, kg, vg = self._groups(q, k_in, v_in)
+        kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
+        vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+        K.attention_partial_groups(qg, kc, vc, gl, 0, int(n_ext), self.scale,
+                                   out=self.o_ext[layer], lse=self.lse_ext[layer])
+        o = out.view(qg.shape) if out is not None else None
+        res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
+                               self.out_dtype, out=o)
+        return res.view(self.b, self.hq, self.B, self.d), heads
 
     def full_recompute(self, q, k_cache, v_cache, n_ext: int, k_in, v_in, out=None,
                        o_scratch=None, lse_scratch=None):

@@ -159,6 +159,71 @@ def attention_partial_ragged(q, k, v, key_end: torch.Tensor, key_begin: int = 0,
     return out, lse
 
 
+def attention_partial_groups(q, k, v, group_list: torch.Tensor, key_begin: int = 0,
+                             key_end: int | None = None, scale: float | None = None, out=None,
+                             lse=None):
+    """K1 over the groups in group_list only (head-gated refresh, SURVEY 8f
+    row f3): rows of the other groups in out / lse are left untouched.
+    group_list: CUDA int32 tensor of distinct group indices.  F64 / BF16."""
+    q3, k3, v3 = _as3(q, "q"), _as3(k, "k"), _as3(v, "v")
+    require_cuda(q3, k3, v3)
+    _check_kv(q3, k3, v3)
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    groups, q_rows, d = q3.shape
+    cap = k3.shape[1]
+    key_end = cap if key_end is None else int(key_end)
+    code = dtype_code(q3)
+    ot, lt = PARTIAL_TYPES[code]
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
+    if lse is None:
+        lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    gl = group_list.to(device=q3.device, dtype=torch.int32).contiguous()
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_partial_workspace_bytes(code, gl.numel(), q_rows, d,
+                                                 max(0, key_end - key_begin))
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_attention_partial_groups", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
+              int(key_begin), key_end, _p(gl), gl.numel(), scale, _p(out), _p(lse), _p(ws),
+              0 if ws is None else ws.numel(), _stream(q3))
+    return out, lse
+
+
+def _sim_code(t: torch.Tensor) -> int:
+    return {torch.float64: _lib.FB_F64, torch.float32: _lib.FB_F32,
+            torch.bfloat16: _lib.FB_BF16}[t.dtype]
+
+
+def row_cosine(a, b, want_rows: bool = False):
+    """Per-row cosine of a, b [heads, rows, d] (zero-norm rule of linalg.py:68-80)
+    and its per-head mean, float64.  Returns head_mean [heads] (and row_cos)."""
+    a3, b3 = _as3(a, "a").contiguous(), _as3(b, "b").contiguous()
+    require_cuda(a3, b3)
+    if a3.shape != b3.shape or a3.dtype != b3.dtype:
+        raise ShapeError(f"step outputs differ: {tuple(a3.shape)} vs {tuple(b3.shape)}")
+    heads, rows, d = a3.shape
+    mean = torch.empty(heads, dtype=torch.float64, device=a3.device)
+    rc = torch.empty((heads, rows), dtype=torch.float64, device=a3.device) if want_rows else None
+    _lib.call("fb_row_cosine", _sim_code(a3), _p(a3), _p(b3), heads, rows, d, _p(rc), _p(mean),
+              _stream(a3))
+    return (mean, rc) if want_rows else mean
+
+
+def pairwise_cosine(later, earlier):
+    """All-pairs cosine [heads, rows, rows] between a later and an earlier
+    step's rows (analysis.py:28-51), float64."""
+    a3, b3 = _as3(later, "later").contiguous(), _as3(earlier, "earlier").contiguous()
+    require_cuda(a3, b3)
+    if a3.shape != b3.shape or a3.dtype != b3.dtype:
+        raise ShapeError(f"step outputs must share a (block, head_dim) shape: "
+                         f"{tuple(a3.shape)} vs {tuple(b3.shape)}")
+    heads, rows, d = a3.shape
+    out = torch.empty((heads, rows, rows), dtype=torch.float64, device=a3.device)
+    _lib.call("fb_pairwise_cosine", _sim_code(a3), _p(a3), _p(b3), heads, rows, d, _p(out),
+              _stream(a3))
+    return out
+
+
 def block_causal_attention(q, k, v, n_q: int, n_prefix: int = 0, block_size: int = 32,
                            scale: float | None = None, out=None, lse=None):
     """Prefill / commit attention (simulator.py:297-354).

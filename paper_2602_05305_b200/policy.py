@@ -19,7 +19,7 @@ import numpy as np
 from .errors import ShapeError
 
 __all__ = ["Decision", "MODES", "ReuseConfig", "decide", "count_updated_tokens",
-           "unmask_schedule", "refresh_schedule"]
+           "unmask_schedule", "refresh_schedule", "CalibrationError", "HeadGate", "HeadGateTable"]
 
 MODES = ("token-threshold", "head-gated", "always-recompute", "always-reuse")  # policy.py:33
 
@@ -104,3 +104,63 @@ def refresh_schedule(config: ReuseConfig, block_size: int, steps: int,
     M = unmask_schedule[s-1])."""
     sched = unmask_schedule(block_size, steps, per_step)
     return [decide(config, s > 0, s == 0, sched[s - 1] if s > 0 else 0) for s in range(steps)]
+
+
+# ---------------------------------------------------------------- head gates (SURVEY 8f row f3)
+
+
+class CalibrationError(RuntimeError):
+    """No usable gating signal (policy.py:41-42)."""
+
+
+@dataclass(frozen=True)
+class HeadGate:
+    """Calibration record of one (layer, head) (policy.py:110-123): mean and
+    worst adjacent-step cosine similarity of its external partials."""
+
+    layer: int
+    head: int
+    similarity: float
+    similarity_min: float
+    enabled: bool
+
+
+class HeadGateTable:
+    """Per-head reuse gates (policy.py:126-181): enabled iff similarity > gamma.
+    Same constructors, queries and JSON form as the reference."""
+
+    def __init__(self, gamma: float, heads: list[HeadGate]):
+        for g in heads:
+            if g.enabled != (g.similarity > gamma):
+                raise ValueError(f"gate for ({g.layer}, {g.head}) inconsistent with gamma={gamma}")
+        self.gamma = gamma
+        self.heads = list(heads)
+        self._enabled = {(g.layer, g.head): g.enabled for g in heads}
+
+    @classmethod
+    def from_similarities(cls, gamma: float, stats: dict) -> "HeadGateTable":
+        heads = [HeadGate(layer, head, mean, worst, mean > gamma)
+                 for (layer, head), (mean, worst) in sorted(stats.items())]
+        return cls(gamma, heads)
+
+    def is_enabled(self, layer: int, head: int) -> bool:
+        return self._enabled.get((layer, head), False)
+
+    def to_json(self) -> str:
+        import json
+
+        return json.dumps({"gamma": self.gamma,
+                           "heads": [{"layer": g.layer, "head": g.head, "similarity": g.similarity,
+                                      "similarity_min": g.similarity_min, "enabled": g.enabled}
+                                     for g in self.heads]}, indent=2, sort_keys=True)
+
+    @classmethod
+    def from_json(cls, text: str) -> "HeadGateTable":
+        import json
+
+        doc = json.loads(text)
+        heads = [HeadGate(int(h["layer"]), int(h["head"]), float(h["similarity"]),
+                          float(h.get("similarity_min", h["similarity"])), bool(h["enabled"]))
+                 for h in doc["heads"]]
+        return cls(float(doc["gamma"]), heads)
+

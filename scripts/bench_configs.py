@@ -1,7 +1,7 @@
 """Secondary benchmark lines for BASELINE.json configs C1, C3, C4, C5 and the
-prefill path (F4).
+prefill path (F4) and the head-gated refresh (F3), SURVEY 8f.
 
-    python scripts/bench_configs.py [--only c3,c4,c5,f4,c1] [--out profiles/rXX_configs.jsonl]
+    python scripts/bench_configs.py [--only c3,c4,c5,f4,f3,c1] [--out profiles/rXX_configs.jsonl]
 
 One JSON line per measurement.  All device timings are CUDA events around
 CUDA-graph replays of the measured launches (no host gaps), after warm-up,
@@ -191,6 +191,37 @@ def f4(out):
         torch.cuda.empty_cache()
 
 
+# ---------------------------------------------------------------- F3 head-gated refresh
+
+
+def f3(out):
+    """Head-gated refresh at the C5 video shapes (12 heads,
+    1:1, chunk 4680, 18,720 external keys): K1 over the heads whose gate is
+    off + K2 for all, vs the full refresh; and the calibrator's per-step
+    cost (row cosine of the external partials)."""
+    from paper_2602_05305_b200.analysis import HeadGateCalibrator
+
+    H, D, B, n_ext = 12, 128, 4680, 18720
+    g = torch.Generator(device=DEV).manual_seed(6)
+    q, k, v = rnd(g, H, B, D), rnd(g, H, n_ext, D), rnd(g, H, n_ext, D)
+    ki, vi = rnd(g, H, B, D), rnd(g, H, B, D)
+    o_ext, l_ext = K.attention_partial(q, k, v, 0, n_ext)
+    t_full = graph_ms(lambda: (K.attention_partial(q, k, v, 0, n_ext, None, o_ext, l_ext),
+                               K.internal_merge(q, ki, vi, o_ext, l_ext, out_dtype=torch.bfloat16)), reps=3)
+    for n_on in (3, 6, 9):
+        gl = torch.arange(n_on, dtype=torch.int32, device=DEV)
+        t = graph_ms(lambda: (K.attention_partial_groups(q, k, v, gl, 0, n_ext, None, o_ext, l_ext),
+                              K.internal_merge(q, ki, vi, o_ext, l_ext, out_dtype=torch.bfloat16)), reps=3)
+        emit(out, {"config": "F3-head-gated", "heads": H, "block": B, "n_ext": n_ext,
+                   "heads_refreshed": n_on, "step_ms": t, "full_refresh_step_ms": t_full,
+                   "speedup_vs_full_refresh": t_full / t})
+    cal = HeadGateCalibrator(1, H)
+    cal.observe(0, o_ext, B)
+    t_cal = graph_ms(lambda: cal.observe(0, o_ext, B), reps=5)
+    emit(out, {"config": "F3-calibrator", "heads": H, "rows": B, "observe_ms": t_cal,
+               "bytes": 2 * H * B * D * 4, "gbs": 2 * H * B * D * 4 / (t_cal * 1e-3) / 1e9})
+
+
 # ---------------------------------------------------------------- C1
 
 
@@ -231,7 +262,7 @@ def c1(out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c3,c4,c5,f4,c1")
+    ap.add_argument("--only", default="c3,c4,c5,f4,f3,c1")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.jsonl"))
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)

@@ -5,6 +5,7 @@ exist on the GPU box):
 
     python tests/golden/make_golden.py            # golden.npz
     python tests/golden/make_golden.py prefill    # golden_prefill.npz
+    python tests/golden/make_golden.py analysis   # golden_analysis.npz
 
 The fixtures it writes (``tests/golden/*.npz``) are committed; the tests read
 only the fixtures.  Inputs are seeded (Philox) and, for the cases the bf16
@@ -212,8 +213,58 @@ def make_prefill() -> None:
     np.savez_compressed(os.path.join(HERE, "golden_prefill.npz"), **out)
 
 
+def make_analysis() -> None:
+    """Similarity statistics and head-gate calibration from the reference
+    (linalg.py:68-80, analysis.py:28-148, policy.py:110-246).  Writes
+    tests/golden/golden_analysis.npz."""
+    sys.path.insert(0, REF_SRC)
+    import flashblock as fb
+    from flashblock.analysis import PartialRecorder, pairwise_step_similarity
+    from flashblock.linalg import cosine_similarity
+    from flashblock.simulator import run_sequence
+
+    rng = np.random.Generator(np.random.Philox(777))
+    out: dict[str, np.ndarray] = {}
+    heads, rows, d = 3, 20, 16
+    a = rng.standard_normal((heads, rows, d))
+    b = a + 0.3 * rng.standard_normal((heads, rows, d))
+    a[0, 3] = 0.0           # zero-norm rows -> cosine 0
+    b[1, 7] = 1e-14
+    b[2] = -b[2]            # anti-correlated head
+    out["cos_a"], out["cos_b"] = a, b
+    out["cos_rows"] = np.array([[cosine_similarity(a[h, r], b[h, r]) for r in range(rows)]
+                                for h in range(heads)])
+    out["cos_mean"] = np.array([np.mean(out["cos_rows"][h]) for h in range(heads)])
+    out["pair"] = np.stack([pairwise_step_similarity(a[h], b[h]) for h in range(heads)])
+
+    # head-gate calibration on a tiny model: the recorded external partials of
+    # every (layer, head, step) and the reference's own table
+    cfg = fb.ModelConfig(num_layers=2, num_heads=3, head_dim=16, seed=4, query_noise=0.3,
+                         noisy_heads=frozenset({(1, 2)}))
+    model = fb.SyntheticModel(cfg)
+    samples, gamma = 2, 0.995
+    kw = dict(prompt_len=24, block_size=8, steps_per_block=6, unmask_per_step=1)
+    for i in range(samples):
+        rec = PartialRecorder()
+        run_sequence(model, kw["prompt_len"], 1, kw["block_size"], kw["steps_per_block"],
+                     fb.ReuseConfig(mode="always-recompute"), seed=i,
+                     unmask_per_step=kw["unmask_per_step"], recorder=rec)
+        for (layer, head, block), outs in rec.external_by_head().items():
+            out[f"cal_s{i}_l{layer}_h{head}"] = np.stack(outs)  # [steps, rows, d]
+    table = fb.calibrate_head_gates(model, samples, gamma, prompt_len=kw["prompt_len"],
+                                    block_size=kw["block_size"],
+                                    steps_per_block=kw["steps_per_block"],
+                                    unmask_per_step=kw["unmask_per_step"], base_seed=0)
+    out["cal_table_json"] = np.frombuffer(table.to_json().encode(), dtype=np.uint8)
+    out["cal_meta"] = np.array([cfg.num_layers, cfg.num_heads, samples], dtype=np.int64)
+    out["cal_gamma"] = np.array([gamma])
+    np.savez_compressed(os.path.join(HERE, "golden_analysis.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "prefill":
         make_prefill()
+    elif len(sys.argv) > 1 and sys.argv[1] == "analysis":
+        make_analysis()
     else:
         main()
