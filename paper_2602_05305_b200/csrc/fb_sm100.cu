@@ -51,8 +51,8 @@ struct Cfg {
   static constexpr uint32_t OFF_V = OFF_K + STAGES * TILE_BYTES;
   static constexpr uint32_t OFF_BAR = OFF_V + STAGES * TILE_BYTES;
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t OFF_XCH = OFF_BAR + BAR_BYTES;    // [2][128] fp32 epilogue exchange
-  static constexpr uint32_t SMEM = OFF_XCH + 2 * BM * 4 + 1024;  // + alignment slack
+  static constexpr uint32_t OFF_XCH = OFF_BAR + BAR_BYTES;    // [3][128] fp32 epilogue exchange
+  static constexpr uint32_t SMEM = OFF_XCH + 3 * BM * 4 + 1024;  // + alignment slack
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
 };
 
@@ -128,6 +128,34 @@ struct Sched {
 };
 
 static_assert(sizeof(Barriers) <= 512, "barrier block overflows its smem slot");
+static_assert(Cfg<128>::SMEM <= 232448, "K1 shared memory exceeds the 227 KB opt-in limit");
+
+// In-kernel split merge (stream-K fix-up): the CTA holding an item's first
+// tile finishes it last (it is that CTA's last segment), so it merges the
+// other CTAs' partials of the item -- each written in that CTA's FIRST
+// segment, long before -- instead of a separate merge kernel.  The "ready"
+// flag per CTA holds the grid's %gridid (unique per launch in the context),
+// so the flags need no initialisation or reset and a workspace reused by
+// other launches cannot produce a false match.
+__device__ __forceinline__ unsigned long long grid_id() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%gridid;" : "=l"(g));
+  return g;
+}
+__device__ __forceinline__ void flag_signal(unsigned long long* f, unsigned long long v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
+}
+__device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned long long v) {
+  uint32_t polls = 0;
+  while (true) {
+    unsigned long long x;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(f) : "memory");
+    if (x == v) break;
+    if (++polls == (1u << 26)) __trap();  // a schedule bug must not hang the GPU
+    __nanosleep(100);
+  }
+}
 
 // Gathered key source (sparse K7/K8, sparse.py:167-183): an item's first
 // sel_tiles tiles are 8 mask-selected 16-key blocks each (read straight from
@@ -164,7 +192,8 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                const __grid_constant__ CUtensorMap tm_vi, Gather ga, Causal cz, Sched sc, int q_rows, int key_begin,
                int key_end, const int* __restrict__ key_len, float scale_log2, float* __restrict__ o_out,
                float* __restrict__ lse_out, float* __restrict__ ws_o,
-               float* __restrict__ ws_l, unsigned long long* __restrict__ trace) {
+               float* __restrict__ ws_l, unsigned long long* __restrict__ trace,
+               unsigned long long* __restrict__ flags) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -543,23 +572,49 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         lse = z > 0.f ? (m + log2f(z)) * 0.69314718055994530942f : -INFINITY;
         xch[row] = c_oth;
         xch[BM + row] = c_own;
+        xch[2 * BM + row] = lse;
       }
       asm volatile("bar.sync 2, 256;" ::: "memory");
       if (wg == 0) {
         c_own = xch[row];
         c_oth = xch[BM + row];
+        lse = xch[2 * BM + row];
       }
       // coefficient of O0 and O1 (a warpgroup without tiles in this segment has
       // weight 0 and a stale accumulator, so it is selected out, not multiplied)
-      const float c0 = wg == 0 ? c_own : c_oth;
-      const float c1 = wg == 0 ? c_oth : c_own;
+      float c0 = wg == 0 ? c_own : c_oth;
+      float c1 = wg == 0 ? c_oth : c_own;
+      // in-kernel split merge: the item's first CTA (this segment is its last)
+      // merges the partials of CTAs cb+1..ce, written in their first segments
+      const bool owner = flags != nullptr && !whole && ib >= t_begin;
+      const int cb = blockIdx.x + 1, ce = owner ? sc.cta_of(sc.item_end(item) - 1) : 0;
       float* dst;
-      if (whole) {
+      if (whole || owner) {
         dst = live ? o_out + orow * D : nullptr;
       } else {
         const long long slot = sc.slot(blockIdx.x, item) * BM + row;
         dst = ws_o + slot * D;
         if (wg == 1) ws_l[slot] = lse;
+      }
+      float mmax = lse, inv_z = 1.f;
+      if (owner) {
+        if (wg == 0 && row == 0)
+          for (int cc = cb; cc <= ce; ++cc) flag_wait(flags + cc, grid_id());
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        // merge weights over this CTA's partial and the others' (same
+        // arithmetic in both warpgroups, so both get identical weights)
+        for (int cc = cb; cc <= ce; ++cc)
+          mmax = fmaxf(mmax, __ldcg(ws_l + sc.slot(cc, item) * BM + row));
+        float z = lse == -INFINITY ? 0.f : __expf(lse - mmax);
+        const float w_own = z;
+        for (int cc = cb; cc <= ce; ++cc) {
+          const float lk = __ldcg(ws_l + sc.slot(cc, item) * BM + row);
+          z += lk == -INFINITY ? 0.f : __expf(lk - mmax);
+        }
+        inv_z = 1.f / z;
+        c0 *= w_own * inv_z;
+        c1 *= w_own * inv_z;
+        lse = mmax + logf(z);
       }
       ptx::mbar_wait(&bar->o_full, seg & 1);
       ptx::tc_fence_after();
@@ -575,6 +630,19 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           for (int i = 0; i < 32; ++i)
             v[i] = (c0 != 0.f ? c0 * __uint_as_float(r[i]) : 0.f) +
                    (c1 != 0.f ? c1 * __uint_as_float(r1[i]) : 0.f);
+          if (owner) {
+            for (int cc = cb; cc <= ce; ++cc) {
+              const long long sl = sc.slot(cc, item) * BM + row;
+              const float lk = __ldcg(ws_l + sl);
+              const float w = lk == -INFINITY ? 0.f : __expf(lk - mmax) * inv_z;
+              const float4* src = reinterpret_cast<const float4*>(ws_o + sl * D + c * 32);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 x = __ldcg(src + i);
+                v[4 * i] += w * x.x; v[4 * i + 1] += w * x.y; v[4 * i + 2] += w * x.z; v[4 * i + 3] += w * x.w;
+              }
+            }
+          }
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
             *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -582,7 +650,12 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
-      if (whole && live && wg == 1) lse_out[orow] = lse;
+      if (flags != nullptr && !whole && !owner) {
+        // this CTA's share of an item begun by an earlier CTA: publish it
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, grid_id());
+      }
+      if ((whole || owner) && live && wg == 1) lse_out[orow] = lse;
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
   }
@@ -988,7 +1061,9 @@ static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim
     if (want > 0) p.ctas = (int)std::max<long long>(1, std::min<long long>(want, p.T));
   }
   // two split-partial slots per CTA (its first and last segment)
-  p.ws_bytes = (size_t)2 * p.ctas * sm100::BM * (head_dim + 1) * sizeof(float);
+  // + one ready flag (u64) per CTA for the in-kernel split merge
+  p.ws_bytes = (size_t)2 * p.ctas * sm100::BM * (head_dim + 1) * sizeof(float) +
+               (size_t)p.ctas * sizeof(unsigned long long);
   return p;
 }
 
@@ -1145,6 +1220,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr, glist};
   float* ws_o = nullptr;
   float* ws_l = nullptr;
+  unsigned long long* flags = nullptr;  // in-kernel split merge (uniform items only)
   bool need_merge;
   sm100::Causal cz{1, 0, 0};
   if (causal) cz = *causal;
@@ -1175,13 +1251,23 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     } else {
       ws_o = reinterpret_cast<float*>(ws);
       ws_l = ws_o + (size_t)2 * p.ctas * sm100::BM * D;
+      flags = reinterpret_cast<unsigned long long*>(ws_l + (size_t)2 * p.ctas * sm100::BM);
     }
     need_merge = !(p.T % p.ctas == 0 && (p.T / p.ctas) % p.tpi == 0);  // items never split
+    // split items are merged inside the kernel when every CTA is resident at
+    // once (one per SM: the waits always make progress) and an item spans at
+    // most 3 CTAs (the owner merges <= 2 partials; measured at b = 1, where an
+    // item spans ~19 CTAs, the parallel merge kernel is 2.6x faster)
+    const bool short_spans = 2 * (p.T / p.ctas) >= p.tpi;
+    if (need_merge && flags != nullptr && short_spans && p.ctas <= num_sms() && g_k1_diag != 5)
+      need_merge = false;
+    else
+      flags = nullptr;
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
              cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
-             ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr);
+             ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr, flags);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
   if (!need_merge) return FB_OK;
