@@ -142,7 +142,7 @@ FB_API int fb_attention_partial_groups(int dtype, const void* q, const void* k, 
 /* Cross-step similarity (head-gate calibration, policy.py:188-246; stability
  * study, analysis.py:28-148).  a, b: [heads, rows, head_dim] partial outputs
  * of the same rows at two steps, dtype FB_F64 / FB_F32 / FB_BF16 (the array
- * type).  row_cos[heads*rows] (optional): cosine of row r of a and b, 0 when
+ * type).  row_cos[heads*rows] (required): cosine of row r of a and b, 0 when
  * either norm < 1e-12 (linalg.py:68-80); head_mean[heads] (optional): its
  * mean over the rows.  Float64 accumulation, fixed reduction order. */
 FB_API int fb_row_cosine(int dtype, const void* a, const void* b, int64_t heads, int64_t rows,

@@ -581,6 +581,7 @@ int fb_row_cosine(int dtype, const void* a, const void* b, int64_t heads, int64_
   if (int rc = check_dtype(dtype)) return rc;
   if (heads < 0 || rows < 0 || head_dim < 1) return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
   if (heads == 0) return FB_OK;
+  if (row_cos == nullptr) return fail(FB_ERR_VALUE, "row_cos ([heads*rows] float64) is required");
   cudaStream_t st = as_stream(stream);
   switch (dtype) {
     case FB_F64: return launch_row_cosine<double>(a, b, heads, rows, head_dim, row_cos, head_mean, st);

@@ -21,40 +21,46 @@ __device__ __forceinline__ double ld64(const T* p) { return cvt<double>(*p); }
 template <>
 __device__ __forceinline__ double ld64<double>(const double* p) { return *p; }
 
-// grid: heads; block: 256 (8 warps, a warp per row, rows strided over warps)
+// grid: ceil(heads*rows / 8); block 256: one warp per row (all rows of all
+// heads in parallel) -> row_cos[h*rows + r]
 template <typename T>
 __global__ void __launch_bounds__(256)
-row_cosine_kernel(const T* __restrict__ a, const T* __restrict__ b, int64_t rows, int64_t d,
-                  double* __restrict__ row_cos, double* __restrict__ head_mean) {
-  __shared__ double part[8];
+row_cosine_kernel(const T* __restrict__ a, const T* __restrict__ b, int64_t n_rows, int64_t d,
+                  double* __restrict__ row_cos) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n_rows) return;
+  const T* u = a + r * d;
+  const T* v = b + r * d;
+  double uu = 0.0, vv = 0.0, uv = 0.0;
+  for (int64_t c = lane; c < d; c += 32) {
+    const double x = ld64(u + c), y = ld64(v + c);
+    uu += x * x;
+    vv += y * y;
+    uv += x * y;
+  }
+  uu = warp_sum(uu);
+  vv = warp_sum(vv);
+  uv = warp_sum(uv);
+  const double nu = sqrt(uu), nv = sqrt(vv);
+  if (lane == 0) row_cos[r] = (nu < ZERO_NORM_EPS || nv < ZERO_NORM_EPS) ? 0.0 : uv / (nu * nv);
+}
+
+// grid: heads; block 256: head_mean[h] = mean of row_cos[h, :], summed in a
+// fixed order (per-thread strided sums, then a fixed tree)
+__global__ void __launch_bounds__(256)
+head_mean_kernel(const double* __restrict__ row_cos, int64_t rows, double* __restrict__ head_mean) {
+  __shared__ double part[256];
   const int64_t h = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc = 0.0;
-  for (int64_t r = warp; r < rows; r += 8) {
-    const T* u = a + (h * rows + r) * d;
-    const T* v = b + (h * rows + r) * d;
-    double uu = 0.0, vv = 0.0, uv = 0.0;
-    for (int64_t c = lane; c < d; c += 32) {
-      const double x = ld64(u + c), y = ld64(v + c);
-      uu += x * x;
-      vv += y * y;
-      uv += x * y;
-    }
-    uu = warp_sum(uu);
-    vv = warp_sum(vv);
-    uv = warp_sum(uv);
-    const double nu = sqrt(uu), nv = sqrt(vv);
-    const double cs = (nu < ZERO_NORM_EPS || nv < ZERO_NORM_EPS) ? 0.0 : uv / (nu * nv);
-    if (lane == 0 && row_cos != nullptr) row_cos[h * rows + r] = cs;
-    acc += cs;
-  }
-  if (lane == 0) part[warp] = acc;
+  double s = 0.0;
+  for (int64_t r = threadIdx.x; r < rows; r += 256) s += row_cos[h * rows + r];
+  part[threadIdx.x] = s;
   __syncthreads();
-  if (threadIdx.x == 0 && head_mean != nullptr) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += part[w];
-    head_mean[h] = rows > 0 ? s / (double)rows : 0.0;
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) head_mean[h] = rows > 0 ? part[0] / (double)rows : 0.0;
 }
 
 // grid: (ceil(n/16), ceil(n/16), heads); block 16x16; out[h, i, j] =
@@ -105,11 +111,17 @@ pairwise_cosine_kernel(const T* __restrict__ later, const T* __restrict__ earlie
 template <typename T>
 int launch_row_cosine(const void* a, const void* b, int64_t heads, int64_t rows, int64_t d,
                       double* row_cos, double* head_mean, cudaStream_t st) {
-  row_cosine_kernel<T><<<(unsigned)heads, 256, 0, st>>>(reinterpret_cast<const T*>(a),
-                                                        reinterpret_cast<const T*>(b), rows, d,
-                                                        row_cos, head_mean);
+  const int64_t n = heads * rows;
+  if (n > 0) {
+    row_cosine_kernel<T><<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
+        reinterpret_cast<const T*>(a), reinterpret_cast<const T*>(b), n, d, row_cos);
+    count_launch();
+    if (int rc = check_launch("row_cosine_kernel")) return rc;
+  }
+  if (head_mean == nullptr) return FB_OK;
+  head_mean_kernel<<<(unsigned)heads, 256, 0, st>>>(row_cos, rows, head_mean);
   count_launch();
-  return check_launch("row_cosine_kernel");
+  return check_launch("head_mean_kernel");
 }
 
 template <typename T>

@@ -203,7 +203,7 @@ def row_cosine(a, b, want_rows: bool = False):
         raise ShapeError(f"step outputs differ: {tuple(a3.shape)} vs {tuple(b3.shape)}")
     heads, rows, d = a3.shape
     mean = torch.empty(heads, dtype=torch.float64, device=a3.device)
-    rc = torch.empty((heads, rows), dtype=torch.float64, device=a3.device) if want_rows else None
+    rc = torch.empty((heads, rows), dtype=torch.float64, device=a3.device)
     _lib.call("fb_row_cosine", _sim_code(a3), _p(a3), _p(b3), heads, rows, d, _p(rc), _p(mean),
               _stream(a3))
     return (mean, rc) if want_rows else mean
