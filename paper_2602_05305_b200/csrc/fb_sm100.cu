@@ -476,67 +476,82 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             }
           }
         }
-        // row max and row sum as 8 independent chains
-        float mx8[8];
+        // P = 2^(s*scale - m) into TMEM over S (bf16 pairs); returns the row sum.
+        // x = s * scale - m and the sum on packed pairs (FFMA2 / FADD2).
+        auto exp_tile = [&](float neg) -> float {
+          const uint64_t sc2 = ptx::f2_pack(scale_log2, scale_log2), ng2 = ptx::f2_pack(neg, neg);
+          uint64_t ls4[4] = {0, 0, 0, 0};  // 4 independent pair chains (+0.0f bits)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) mx8[k] = s[k];
+          for (int c = 0; c < BN / 64; ++c) {
 #pragma unroll
-        for (int i = 8; i < BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const float m_new = fmaxf(m_used, mx * scale_log2);
-        const bool need = m_new > m_used + RESCALE_THRESHOLD;
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = ptx::ex2(m_used - m_new);
-          if (t >= 2) {
-            // O[wg] holds this segment's P V so far: wait for its last PV (tile j-2)
-            ptx::mbar_wait(&bar->pv_done[wg], ((j - 2) >> 1) & 1);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-              const uint32_t a = tmem + lane_off + o_col + c * 32;
-              ptx::tmem_ld32(a, r);
-              ptx::tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              ptx::tmem_st32(a, r);
+            for (int i = 0; i < 32; ++i) {
+              const uint64_t x2 = ptx::f2_fma(ptx::f2_pack(s[c * 64 + 2 * i], s[c * 64 + 2 * i + 1]), sc2, ng2);
+              float x0, x1;
+              ptx::f2_unpack(x2, x0, x1);
+              float p0, p1;
+              if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
+                p0 = ptx::ex2_poly(x0);
+                p1 = ptx::ex2_poly(x1);
+              } else {
+                p0 = ptx::ex2(x0);
+                p1 = ptx::ex2(x1);
+              }
+              ls4[i & 3] = ptx::f2_add(ls4[i & 3], ptx::f2_pack(p0, p1));
+              r[i] = ptx::pack_bf16(p0, p1);
             }
-            ptx::tmem_wait_st();
+            ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
           }
-          l *= alpha;
-          m_used = m_new;
-        }
-        // a row with no key yet (block-causal segment past its end) keeps p = 0
-        const float neg = m_used == -INFINITY ? 0.f : -m_used;
-        // x = s * scale - m and the row sum on packed pairs (FFMA2 / FADD2)
-        const uint64_t sc2 = ptx::f2_pack(scale_log2, scale_log2), ng2 = ptx::f2_pack(neg, neg);
-        uint64_t ls4[4] = {0, 0, 0, 0};  // 4 independent pair chains (+0.0f bits)
-#pragma unroll
-        for (int c = 0; c < BN / 64; ++c) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const uint64_t x2 = ptx::f2_fma(ptx::f2_pack(s[c * 64 + 2 * i], s[c * 64 + 2 * i + 1]), sc2, ng2);
-            float x0, x1;
-            ptx::f2_unpack(x2, x0, x1);
-            float p0, p1;
-            if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
-              p0 = ptx::ex2_poly(x0);
-              p1 = ptx::ex2_poly(x1);
-            } else {
-              p0 = ptx::ex2(x0);
-              p1 = ptx::ex2(x1);
-            }
-            ls4[i & 3] = ptx::f2_add(ls4[i & 3], ptx::f2_pack(p0, p1));
-            r[i] = ptx::pack_bf16(p0, p1);
-          }
-          ptx::tmem_st32(tmem + lane_off + s_col + c * 32, r);
-        }
-        {
           const uint64_t a2 = ptx::f2_add(ptx::f2_add(ls4[0], ls4[1]), ptx::f2_add(ls4[2], ls4[3]));
           float a0, a1;
           ptx::f2_unpack(a2, a0, a1);
-          l += a0 + a1;
+          return a0 + a1;
+        };
+        // Fast path: exponentiate against the running max without a max pass.
+        // The max is exact in the result either way (l and O share it); it only
+        // has to keep P finite.  A row whose scores rose more than 2^32 / 128
+        // (log2: ~25) past it -- or inf / NaN -- shows in the tile sum, and
+        // the warp redoes the tile through the max pass below.
+        float lt = 0.f;
+        bool full = __any_sync(0xffffffffu, m_used == -INFINITY);
+        if (!full) {
+          lt = exp_tile(-m_used);
+          full = __any_sync(0xffffffffu, !(lt <= 4294967296.f));
         }
+        if (full) {
+          // row max as 8 independent chains
+          float mx8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mx8[k] = s[k];
+#pragma unroll
+          for (int i = 8; i < BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+          const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+          const float m_new = fmaxf(m_used, mx * scale_log2);
+          const bool need = m_new > m_used + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = ptx::ex2(m_used - m_new);
+            if (t >= 2) {
+              // O[wg] holds this segment's P V so far: wait for its last PV (tile j-2)
+              ptx::mbar_wait(&bar->pv_done[wg], ((j - 2) >> 1) & 1);
+              ptx::tc_fence_after();
+#pragma unroll 1
+              for (int c = 0; c < D / 32; ++c) {
+                const uint32_t a = tmem + lane_off + o_col + c * 32;
+                ptx::tmem_ld32(a, r);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                ptx::tmem_st32(a, r);
+              }
+              ptx::tmem_wait_st();
+            }
+            l *= alpha;
+            m_used = m_new;
+          }
+          // a row with no key yet (block-causal segment past its end) keeps p = 0
+          lt = exp_tile(m_used == -INFINITY ? 0.f : -m_used);
+        }
+        l += lt;
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bar->p_ready[wg]);
