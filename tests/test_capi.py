@@ -73,6 +73,35 @@ def test_validation_errors_need_no_device(lib):
         _lib.check(_lib.FB_ERR_VALUE, "x")
 
 
+def test_prefill_subset_and_similarity_validation_need_no_device(lib):
+    from paper_2602_05305_b200 import _lib
+
+    bc = lib.fb_block_causal_attention
+    # q_rows not a multiple of n_q -> ShapeError
+    assert bc(_lib.FB_BF16, None, None, None, 2, 100, 32, 128, 64, 0, 32, 1.0, None, None, None, 0,
+              None) == _lib.FB_ERR_SHAPE
+    # prompt does not fit the slab -> BoundsError
+    assert bc(_lib.FB_BF16, None, None, None, 2, 64, 32, 128, 40, 10, 32, 1.0, None, None, None, 0,
+              None) == _lib.FB_ERR_BOUNDS
+    # block size < 1 -> ValueError
+    assert bc(_lib.FB_BF16, None, None, None, 2, 64, 32, 128, 64, 0, 0, 1.0, None, None, None, 0,
+              None) == _lib.FB_ERR_VALUE
+    gp = lib.fb_attention_partial_groups
+    # list longer than the batch of groups -> ShapeError; no list -> ValueError
+    assert gp(_lib.FB_BF16, None, None, None, 2, 128, 128, 64, 0, 64, None, 3, 1.0, None, None,
+              None, 0, None) == _lib.FB_ERR_SHAPE
+    assert gp(_lib.FB_BF16, None, None, None, 2, 128, 128, 64, 0, 64, None, 1, 1.0, None, None,
+              None, 0, None) == _lib.FB_ERR_VALUE
+    assert gp(_lib.FB_BF16, None, None, None, 2, 128, 128, 64, 0, 65, None, 1, 1.0, None, None,
+              None, 0, None) == _lib.FB_ERR_BOUNDS
+    # row cosine needs its row buffer
+    assert lib.fb_row_cosine(_lib.FB_F32, None, None, 2, 3, 8, None, None, None) == _lib.FB_ERR_VALUE
+    # unknown cached-step flags
+    assert lib.fb_internal_merge_ex(_lib.FB_BF16, None, None, None, 1, 1, 128, 32, 1.0, None, None,
+                                    None, _lib.FB_BF16, None, None, None, None, None, 0, 8,
+                                    None) == _lib.FB_ERR_VALUE
+
+
 def test_status_maps_to_reference_exception_types():
     from paper_2602_05305_b200 import _lib
     from paper_2602_05305_b200.errors import (BoundsError, DegenerateInputError,
