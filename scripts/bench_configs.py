@@ -119,6 +119,14 @@ def c4(out):
                                  for l in range(L)]) / L
         t_k8 = graph_ms(lambda: [K.sparse_attend_merge(q[l], k[l], v[l], ki[l], vi[l], N, sel[l], res[l])
                                  for l in range(L)]) / L
+        # accuracy (sparse.py:303-325 measure_sparse_gap): a later step's drifted
+        # queries against the dense result; residual cached at the first step
+        q2 = (q[0].float() + 0.3 * torch.randn(q[0].shape, device=DEV, generator=g)).to(torch.bfloat16)
+        dense = K.full_attention(q2, k[0], v[0], N, ki[0], vi[0])[0].float()
+        so = K.sparse_attend_merge(q2, k[0], v[0], ki[0], vi[0], N, sel[0], None).float()
+        wr = K.sparse_attend_merge(q2, k[0], v[0], ki[0], vi[0], N, sel[0], res[0]).float()
+        l1_so = float((so - dense).abs().mean())
+        l1_wr = float((wr - dense).abs().mean())
         sel_keys = budget * 16
         k8_bytes = 2 * groups * sel_keys * D * 2 + groups * rows * (D + 1) * 4 * 2
         k7_bytes = 2 * groups * N * D * 2
@@ -131,7 +139,9 @@ def c4(out):
                    "k8_frac_hbm": k8_bytes / (t_k8 * 1e-3) / 1e9 / HBM,
                    "block_ms_per_layer_32_steps": step_block,
                    "dense_full_recompute_block_ms_per_layer": 32 * t_dense,
-                   "speedup_vs_dense_recompute": 32 * t_dense / step_block})
+                   "speedup_vs_dense_recompute": 32 * t_dense / step_block,
+                   "l1_sparse_only": l1_so, "l1_with_residual": l1_wr,
+                   "l1_note": "mean |out - dense| on a drifted query (q + 0.3 N(0,1)), random N(0,1) K/V"})
     del q, k, v
     torch.cuda.empty_cache()
 

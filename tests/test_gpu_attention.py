@@ -257,6 +257,32 @@ def test_bf16_refresh_c2_shape_split_invariance():
     assert (lc - l).abs().max().item() <= 1e-4
 
 
+@pytest.mark.parametrize("groups,n", [(128, 32768), (100, 8192), (40, 2048)])
+def test_bf16_refresh_stream_k_split_merges(groups, n):
+    """Stream-K splits at several spans: (128, 32768) is C2 b=16 (items span 2
+    CTAs: in-kernel merge), (100, 8192) spans <= 3 (in-kernel merge), (40,
+    2048) spans ~4 (separate merge kernel).  Checked against the oracle on
+    rows of groups whose items straddle CTA boundaries, and for determinism."""
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(groups + n)
+    q = torch.randn((groups, 128, 128), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((groups, n, 128), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((groups, n, 128), device="cuda", generator=g).to(torch.bfloat16)
+    o, l = K.attention_partial(q, k, v)
+    o2, l2 = K.attention_partial(q, k, v)
+    assert torch.equal(o, o2) and torch.equal(l, l2), "run-to-run bitwise determinism"
+    tiles = n // 128
+    per_cta = groups * tiles / 148
+    # groups holding a CTA boundary inside their item
+    cand = sorted({int(c * per_cta) // tiles for c in range(1, 148)})
+    for gi in [cand[0], cand[len(cand) // 2], cand[-1]]:
+        ref = orc.partial(q[gi].double().cpu().numpy(), k[gi].double().cpu().numpy(),
+                          v[gi].double().cpu().numpy())
+        assert rel_err(o[gi].cpu().numpy(), ref.out) <= 1e-2
+        assert np.max(np.abs(l[gi].cpu().numpy() - ref.lognorm)) <= 1e-3
+
+
 # ----------------------------------------------------------------- engine (GQA, batched)
 
 
