@@ -31,20 +31,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 0x989680;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
-// Wait until the phase with the given parity has completed.  A pipeline
-// bug must not wedge the GPU: after ~2^26 polls (seconds) trap, which
-// surfaces as a launch failure instead of a hang.
+// Wait until the phase with the given parity has completed (each try_wait may
+// suspend the thread in hardware up to the 10 ms hint instead of spinning).  A
+// pipeline bug must not wedge the GPU: a wait longer than 4 s (globaltimer)
+// traps, which surfaces as a launch failure instead of a hang.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t polls = 0;
+  if (mbar_try_wait(bar, parity)) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   while (!mbar_try_wait(bar, parity)) {
-    if (++polls == (1u << 26)) __trap();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) __trap();
   }
 }
 
