@@ -17,12 +17,31 @@ partial per layer is O_ext [b, Hq, B, d] fp32 + LSE_ext [b, Hq, B] fp32
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 
 import torch
 
 from . import kernels as K
 from .errors import ReusePreconditionError, ShapeError
 from .policy import Decision, ReuseConfig, decide
+
+
+@dataclass
+class AccessCounters:
+    """Counted cache traffic, the reference's AccessCounters (kv_cache.py:28-52):
+    key / value rows read from the committed cache (per kv slab, as the
+    reference counts per (layer, head) read_range), rows appended, and bytes
+    resident.  Cached steps read no cache rows (tests/test_acceptance.py:132-176
+    there); the kernels of a cached step never receive the cache pointer."""
+
+    key_rows_read: int = 0
+    value_rows_read: int = 0
+    rows_appended: int = 0
+    cache_bytes_resident: int = 0
+
+    def copy(self) -> "AccessCounters":
+        return AccessCounters(self.key_rows_read, self.value_rows_read, self.rows_appended,
+                              self.cache_bytes_resident)
 
 
 class FlashBlockAttention:
@@ -50,6 +69,22 @@ class FlashBlockAttention:
         # optional HeadGateCalibrator: sees every refreshed external partial
         self.recorder = recorder
         self._glists: dict = {}
+        # cache rows read (host count for uniform lengths, device count for ragged)
+        self._rows_read = 0
+        self._rows_read_dev = None
+
+    def _count_rows(self, rows) -> None:
+        if isinstance(rows, torch.Tensor):
+            if self._rows_read_dev is None:
+                self._rows_read_dev = torch.zeros((), dtype=torch.int64, device=self.device)
+            self._rows_read_dev += rows.to(torch.int64).sum()
+        else:
+            self._rows_read += int(rows)
+
+    def snapshot_counters(self) -> AccessCounters:
+        """Rows read so far (syncs once if ragged refreshes were counted on the device)."""
+        n = self._rows_read + (int(self._rows_read_dev) if self._rows_read_dev is not None else 0)
+        return AccessCounters(key_rows_read=n, value_rows_read=n)
 
     # -- cache lifecycle (ExternalAttnCache.invalidate_all, simulator.py:562-563)
     def begin_block(self, block_id: int) -> None:
@@ -94,9 +129,11 @@ class FlashBlockAttention:
         o = out.view(qg.shape) if out is not None else None
         lens = self._group_lengths(n_ext)
         if lens is None:
+            self._count_rows(self.b * self.hkv * int(n_ext))
             res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
                                          o_ext=self.o_ext[layer], lse_ext=self.lse_ext[layer], out=o)
         else:
+            self._count_rows(lens.clamp(max=kc.shape[1]))
             K.attention_partial_ragged(qg, kc, vc, lens, 0, self.scale, out=self.o_ext[layer],
                                        lse=self.lse_ext[layer])
             res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
@@ -142,6 +179,10 @@ class FlashBlockAttention:
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None
+        # the reference's commit passes read the committed prefix of every block
+        # (simulator.py:316-317): sum over blocks j of n_prefix + j * B rows
+        nblk = -(-n_q // self.B)
+        self._count_rows(self.b * self.hkv * (nblk * n_prefix + self.B * nblk * (nblk - 1) // 2))
         res, _ = K.block_causal_attention(qg, kc, vc, n_q, n_prefix, self.B, self.scale, out=o, lse=lse)
         return res.view(b, hq, n_q, d)
 
@@ -172,6 +213,7 @@ class FlashBlockAttention:
         qg, kg, vg = self._groups(q, k_in, v_in)
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+        self._count_rows(gl.numel() * int(n_ext))
         K.attention_partial_groups(qg, kc, vc, gl, 0, int(n_ext), self.scale,
                                    out=self.o_ext[layer], lse=self.lse_ext[layer])
         o = out.view(qg.shape) if out is not None else None
@@ -187,6 +229,7 @@ class FlashBlockAttention:
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None
+        self._count_rows(self.b * self.hkv * int(n_ext))
         res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
                                      o_ext=o_scratch, lse_ext=lse_scratch, out=o)
         return res.view(self.b, self.hq, self.B, self.d)
@@ -211,6 +254,7 @@ class KVCache:
         self.v = [torch.zeros_like(t) for t in self.k]
         self.lengths = [torch.zeros(batch * num_kv_heads, dtype=torch.int32, device=dev)
                         for _ in range(num_layers)]
+        self.rows_appended = 0
 
     def commit_block(self, layer: int, k_block, v_block, check: bool = False) -> None:
         """Append one finished block's rows [b, Hkv, B, d] for `layer`."""
@@ -220,6 +264,13 @@ class KVCache:
                        self.v[layer].view(self.b * self.hkv, self.cap, self.d),
                        k_block.reshape(self.b * self.hkv, -1, self.d),
                        v_block.reshape(self.b * self.hkv, -1, self.d), self.lengths[layer], check)
+        self.rows_appended += self.b * self.hkv * k_block.shape[-2]
+
+    def snapshot_counters(self) -> AccessCounters:
+        """Rows appended and bytes resident (committed rows of every slab; syncs)."""
+        rows = sum(int(t.clamp(max=self.cap).to(torch.int64).sum()) for t in self.lengths)
+        return AccessCounters(rows_appended=self.rows_appended,
+                              cache_bytes_resident=rows * 2 * self.d * self.k[0].element_size())
 
     def sequence_lengths(self, layer: int = 0) -> torch.Tensor:
         return self.lengths[layer].view(self.b, self.hkv)[:, 0]
