@@ -300,7 +300,7 @@ partial_simt(const typename Mode::Tin* __restrict__ q, Map map, int64_t q_rows, 
 // from a strided workspace (split-KV partials).
 template <typename Tp, typename Tlp, typename Ta, typename To, typename Tlo>
 __global__ void combine_parts(CombineList list, int64_t rows, int64_t head_dim, To* o_out,
-                              Tlo* l_out, int32_t* empty_rows) {
+                              Tlo* l_out, int32_t* empty_rows, bool vec) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -312,6 +312,70 @@ __global__ void combine_parts(CombineList list, int64_t rows, int64_t head_dim, 
     return list.strided ? reinterpret_cast<const Tlp*>(list.l[0]) + (int64_t)p * list.l_stride
                         : reinterpret_cast<const Tlp*>(list.l[p]);
   };
+  if (list.n <= FB_MAX_PARTS) {
+    // lane p holds part p's lognorm and merge weight, computed once per row and
+    // broadcast by shuffle; all parts' loads in flight before the sum; products
+    // rounded before summing, so a two-way merge stays bitwise symmetric like
+    // the reference's wa*A + wb*B
+    const Ta lp = lane < list.n ? (Ta)lptr(lane)[row] : Num<Ta>::ninf();
+    const Ta mx = warp_max(lp);
+    const bool live = mx != Num<Ta>::ninf();
+    const Ta w = (live && lane < list.n) ? Num<Ta>::exp_(lp - mx) : (Ta)0;
+    const Ta z = warp_sum(w);
+    Ta wv[FB_MAX_PARTS];
+#pragma unroll
+    for (int p = 0; p < FB_MAX_PARTS; ++p) wv[p] = __shfl_sync(0xffffffffu, w, p);
+    if (vec) {
+      // 16-byte loads: a lane owns VW consecutive columns, all parts in flight
+      constexpr int VW = 16 / sizeof(Tp);
+      for (int64_t c = (int64_t)lane * VW; c < head_dim; c += 32 * VW) {
+        Tp vals[FB_MAX_PARTS][VW];
+#pragma unroll
+        for (int p = 0; p < FB_MAX_PARTS; ++p) {
+          if (live && p < list.n) {
+            const uint4 u = *reinterpret_cast<const uint4*>(optr(p) + row * head_dim + c);
+            const Tp* e = reinterpret_cast<const Tp*>(&u);
+#pragma unroll
+            for (int i = 0; i < VW; ++i) vals[p][i] = e[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < VW; ++i) vals[p][i] = (Tp)0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < VW; ++i) {
+          Ta num = 0;
+          if (live) {
+#pragma unroll
+            for (int p = 0; p < FB_MAX_PARTS; ++p)
+              if (p < list.n) num += mul_rn(wv[p], (Ta)vals[p][i]);
+            num = num / z;
+          }
+          o_out[row * head_dim + c + i] = cvt<To>(num);
+        }
+      }
+    } else
+    for (int64_t c = lane; c < head_dim; c += 32) {
+      Ta vals[FB_MAX_PARTS];
+#pragma unroll
+      for (int p = 0; p < FB_MAX_PARTS; ++p)
+        vals[p] = (live && p < list.n) ? (Ta)optr(p)[row * head_dim + c] : (Ta)0;
+      Ta num = 0;
+      if (live) {
+#pragma unroll
+        for (int p = 0; p < FB_MAX_PARTS; ++p)
+          if (p < list.n) num += mul_rn(wv[p], vals[p]);
+        num = num / z;
+      }
+      o_out[row * head_dim + c] = cvt<To>(num);
+    }
+    if (lane == 0) {
+      if (l_out) l_out[row] = live ? (Tlo)(mx + Num<Ta>::log_(z)) : (Tlo)Num<Ta>::ninf();
+      if (!live && empty_rows) atomicAdd(empty_rows, 1);
+    }
+    return;
+  }
+  // many parts (in-GPU SIMT split-KV partials): sequential over parts
   Ta mx = Num<Ta>::ninf();
   for (int p = 0; p < list.n; ++p) mx = fmax(mx, (Ta)lptr(p)[row]);
   const bool live = mx != Num<Ta>::ninf();
@@ -417,8 +481,15 @@ int launch_combine(const CombineList& list, int64_t rows, int64_t head_dim, To* 
   if (rows == 0) return FB_OK;
   const int warps = 8;
   const unsigned blocks = (unsigned)((rows + warps - 1) / warps);
+  // 16-byte vector loads when every part's rows are 16-byte aligned
+  bool vec = (head_dim * (int64_t)sizeof(Tp)) % 16 == 0 && list.n <= FB_MAX_PARTS;
+  for (int p = 0; p < list.n && vec; ++p) {
+    const void* base = list.strided ? (const void*)(reinterpret_cast<const Tp*>(list.o[0]) + (int64_t)p * list.o_stride)
+                                    : list.o[p];
+    vec = (reinterpret_cast<uintptr_t>(base) & 15u) == 0;
+  }
   combine_parts<Tp, Tlp, Ta, To, Tlo><<<blocks, 32 * warps, 0, st>>>(list, rows, head_dim, o_out,
-                                                                      l_out, empty_rows);
+                                                                      l_out, empty_rows, vec);
   count_launch();
   return check_launch("combine_parts");
 }

@@ -79,7 +79,8 @@ def c3(out):
             n = N // P
             parts = [K.attention_partial(q[0], k[0], v[0], 0, n) for _ in range(P)]
             t_k1 = graph_ms(lambda: [K.attention_partial(q[l], k[l], v[l], 0, n) for l in range(L)]) / L
-            t_m = graph_ms(lambda: K.combine(parts)) if P > 1 else 0.0
+            # 8 merges per graph: a one-node graph would time the graph launch
+            t_m = graph_ms(lambda: [K.combine(parts) for _ in range(8)]) / 8 if P > 1 else 0.0
             res[P] = t_k1 + t_m
             kv_bytes = 2 * groups * n * D * 2
             payload = groups * rows * (D + 1) * 4

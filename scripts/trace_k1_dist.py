@@ -25,3 +25,7 @@ for b in [int(x) for x in sys.argv[1:]] or [16]:
     print(f"b={b} end   us pct0/10/50/90/100 {np.round(q(end),1)}  -> mean end {end.mean():.1f}, max {end.max():.1f}")
     byts = 2 * b * HKV * CTX * D * 2
     print(f"b={b} rate at median end {byts/np.median(end)/1e3:.0f} GB/s, at max end {byts/end.max()/1e3:.0f} GB/s")
+    # correlation of end time with CTA index (SM placement / segment layout)
+    smid_order = np.argsort(end)
+    print("earliest CTAs", smid_order[:12].tolist(), "latest CTAs", smid_order[-12:].tolist())
+    print("end by CTA-index decile (us):", [round(float(np.mean(end[i * 15:(i + 1) * 15])), 1) for i in range(10)])
