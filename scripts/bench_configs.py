@@ -79,8 +79,12 @@ def c3(out):
             n = N // P
             parts = [K.attention_partial(q[0], k[0], v[0], 0, n) for _ in range(P)]
             t_k1 = graph_ms(lambda: [K.attention_partial(q[l], k[l], v[l], 0, n) for l in range(L)]) / L
-            # 8 merges per graph: a one-node graph would time the graph launch
-            t_m = graph_ms(lambda: [K.combine(parts) for _ in range(8)]) / 8 if P > 1 else 0.0
+            # after the all_to_all each rank merges the P partials of its own
+            # kv-head shard only (splitkv.py): 1/P of the rows.  8 merges per
+            # graph: a one-node graph would time the graph launch
+            gs = max(1, groups // P)
+            mine = [(o[:gs], l_[:gs]) for o, l_ in parts]
+            t_m = graph_ms(lambda: [K.combine(mine) for _ in range(8)]) / 8 if P > 1 else 0.0
             res[P] = t_k1 + t_m
             kv_bytes = 2 * groups * n * D * 2
             payload = groups * rows * (D + 1) * 4
@@ -89,7 +93,8 @@ def c3(out):
                        "k1_gbs": kv_bytes / (t_k1 * 1e-3) / 1e9, "k1_frac_hbm": kv_bytes / (t_k1 * 1e-3) / 1e9 / HBM,
                        "exchange_bytes_per_gpu": payload * (P - 1) // max(P, 1),
                        "efficiency_T1_over_P_TP": res[1] / (P * res[P]),
-                       "note": "single-GPU emulation: shard K1 on the whole GPU + K3 merge; NCCL exchange not measured"})
+                       "note": "single-GPU emulation: shard K1 on the whole GPU + K3 merge of this "
+                               "rank's 1/P kv-head shard; NCCL exchange not measured"})
         del q, k, v
         torch.cuda.empty_cache()
 
