@@ -88,6 +88,22 @@ FB_API int fb_attention_partial(int dtype, const void* q, const void* k, const v
                          double scale, void* o_out, void* lse_out,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* K1 with the in-kernel split merge (stream-K fix-up without a second kernel).
+ * sync_flags: a DEVICE buffer of n_flags uint64 (>= fb_sync_flags_count()),
+ * all zero before the first use and not shared by launches that may run
+ * concurrently; every launch leaves it zero again.  Used when every split
+ * item spans <= 3 CTAs (C2 b >= 16); otherwise -- and with sync_flags NULL,
+ * which is fb_attention_partial -- split items are merged by a second kernel.
+ * Same arguments and results as fb_attention_partial otherwise. */
+FB_API int fb_attention_partial_sync(int dtype, const void* q, const void* k, const void* v,
+                                     int64_t groups, int64_t q_rows, int64_t head_dim,
+                                     int64_t kv_rows_cap, int64_t key_begin, int64_t key_end,
+                                     double scale, void* o_out, void* lse_out, void* workspace,
+                                     size_t workspace_bytes, uint64_t* sync_flags, int64_t n_flags,
+                                     void* stream);
+/* Length of the sync_flags buffer fb_attention_partial_sync expects. */
+FB_API int64_t fb_sync_flags_count(void);
+
 /* K1 over per-sequence (ragged) context lengths -- the serving layout where
  * each sequence of the batch has its own committed length.
  * Group g streams rows [key_begin, min(key_end[g], kv_rows_cap)) of its slab;

@@ -30,6 +30,9 @@ SIGNATURES = {
     "fb_version": (C.c_char_p, []),
     "fb_launch_count": (i64, []),
     "fb_partial_workspace_bytes": (sz, [i32, i64, i64, i64, i64]),
+    "fb_attention_partial_sync": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, i64, dbl, vp, vp,
+                                        vp, sz, vp, i64, vp]),
+    "fb_sync_flags_count": (i64, []),
     "fb_attention_partial": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, i64, dbl, vp, vp,
                                    vp, sz, vp]),
     "fb_attention_partial_ragged": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, vp, dbl, vp,

@@ -112,7 +112,8 @@ template <typename Mode>
 static int attention_partial_t(const void* qv, const void* kv, const void* vv, int64_t groups,
                                int64_t q_rows, int64_t d, int64_t cap, int64_t kb, int64_t ke,
                                double scale, void* o_out, void* lse_out, void* ws, size_t ws_bytes,
-                               cudaStream_t st) {
+                               cudaStream_t st, uint64_t* sync_flags = nullptr,
+                               int64_t n_flags = 0) {
   using Tin = typename Mode::Tin;
   auto* q = reinterpret_cast<const Tin*>(qv);
   auto* k = reinterpret_cast<const Tin*>(kv);
@@ -126,7 +127,8 @@ static int attention_partial_t(const void* qv, const void* kv, const void* vv, i
     if (sm100_supported(d) && ke < (int64_t(1) << 31) && q_rows < (int64_t(1) << 31) &&
         (reinterpret_cast<uintptr_t>(q) % 16 == 0) && (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
         (reinterpret_cast<uintptr_t>(v) % 16 == 0) && groups < 65536) {
-      return launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, scale, o, l, ws, ws_bytes, st);
+      return launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, scale, o, l, ws, ws_bytes, st,
+                                  reinterpret_cast<unsigned long long*>(sync_flags), n_flags);
     }
   }
   RangeMap<Tin> map{k, v, cap * d, kb, ke, d};
@@ -509,7 +511,21 @@ int fb_attention_partial(int dtype, const void* q, const void* k, const void* v,
                          int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap, int64_t key_begin,
                          int64_t key_end, double scale, void* o_out, void* lse_out, void* workspace,
                          size_t workspace_bytes, void* stream) {
+  return fb_attention_partial_sync(dtype, q, k, v, groups, q_rows, head_dim, kv_rows_cap, key_begin,
+                                   key_end, scale, o_out, lse_out, workspace, workspace_bytes,
+                                   nullptr, 0, stream);
+}
+
+int64_t fb_sync_flags_count(void) { return 1024; }
+
+int fb_attention_partial_sync(int dtype, const void* q, const void* k, const void* v,
+                              int64_t groups, int64_t q_rows, int64_t head_dim,
+                              int64_t kv_rows_cap, int64_t key_begin, int64_t key_end,
+                              double scale, void* o_out, void* lse_out, void* workspace,
+                              size_t workspace_bytes, uint64_t* sync_flags, int64_t n_flags,
+                              void* stream) {
   if (int rc = check_dtype(dtype)) return rc;
+  if (sync_flags != nullptr && n_flags < 1) return fail(FB_ERR_VALUE, "sync_flags needs n_flags >= 1");
   if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
   if (!(0 <= key_begin && key_begin <= key_end && key_end <= kv_rows_cap))
@@ -527,7 +543,8 @@ int fb_attention_partial(int dtype, const void* q, const void* k, const void* v,
                                           key_end, scale, o_out, lse_out, workspace, workspace_bytes, st);
     default:
       return attention_partial_t<ModeBF16>(q, k, v, groups, q_rows, head_dim, kv_rows_cap, key_begin,
-                                           key_end, scale, o_out, lse_out, workspace, workspace_bytes, st);
+                                           key_end, scale, o_out, lse_out, workspace, workspace_bytes, st,
+                                           sync_flags, n_flags);
   }
 }
 

@@ -70,7 +70,8 @@ size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t hea
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
-                         float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st);
+                         float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                         unsigned long long* sync_flags = nullptr, int64_t n_flags = 0);
 
 // Ragged per-group key ends (device int32 [groups], clamped to kv_rows_cap).
 size_t refresh_sm100_ragged_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim);

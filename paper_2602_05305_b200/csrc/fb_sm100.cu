@@ -133,15 +133,12 @@ static_assert(Cfg<128>::SMEM <= 232448, "K1 shared memory exceeds the 227 KB opt
 // In-kernel split merge (stream-K fix-up): the CTA holding an item's first
 // tile finishes it last (it is that CTA's last segment), so it merges the
 // other CTAs' partials of the item -- each written in that CTA's FIRST
-// segment, long before -- instead of a separate merge kernel.  The "ready"
-// flag per CTA holds the grid's %gridid (unique per launch in the context),
-// so the flags need no initialisation or reset and a workspace reused by
-// other launches cannot produce a false match.
-__device__ __forceinline__ unsigned long long grid_id() {
-  unsigned long long g;
-  asm volatile("mov.u64 %0, %%gridid;" : "=l"(g));
-  return g;
-}
+// segment, long before -- instead of a separate merge kernel.  Ready flags
+// live in a caller-owned buffer that is zero before the launch: a writer CTA
+// sets its flag to 1 (release), the merging CTA waits for 1 (acquire) and
+// sets it back to 0, so the buffer is zero again after every launch.  (The
+// grid's %gridid is NOT a usable per-launch token: CUDA-graph replays of one
+// node repeat it -- scripts/micro/gridid.cu.)
 __device__ __forceinline__ void flag_signal(unsigned long long* f, unsigned long long v) {
   __threadfence();
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
@@ -613,8 +610,12 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       float mmax = lse, inv_z = 1.f;
       if (owner) {
-        if (wg == 0 && row == 0)
-          for (int cc = cb; cc <= ce; ++cc) flag_wait(flags + cc, grid_id());
+        if (wg == 0 && row == 0) {
+          for (int cc = cb; cc <= ce; ++cc) {
+            flag_wait(flags + cc, 1ull);
+            flags[cc] = 0ull;  // consumed: zero again for the next launch
+          }
+        }
         asm volatile("bar.sync 3, 256;" ::: "memory");
         // merge weights over this CTA's partial and the others' (same
         // arithmetic in both warpgroups, so both get identical weights)
@@ -668,7 +669,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (flags != nullptr && !whole && !owner) {
         // this CTA's share of an item begun by an earlier CTA: publish it
         asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, grid_id());
+        if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, 1ull);
       }
       if ((whole || owner) && live && wg == 1) lse_out[orow] = lse;
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
@@ -1092,9 +1093,7 @@ static RefreshPlan plan_refresh(int64_t groups, int64_t q_rows, int64_t head_dim
     if (want > 0) p.ctas = (int)std::max<long long>(1, std::min<long long>(want, p.T));
   }
   // two split-partial slots per CTA (its first and last segment)
-  // + one ready flag (u64) per CTA for the in-kernel split merge
-  p.ws_bytes = (size_t)2 * p.ctas * sm100::BM * (head_dim + 1) * sizeof(float) +
-               (size_t)p.ctas * sizeof(unsigned long long);
+  p.ws_bytes = (size_t)2 * p.ctas * sm100::BM * (head_dim + 1) * sizeof(float);
   return p;
 }
 
@@ -1199,7 +1198,8 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
                             size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr,
                             const int* key_len = nullptr, const sm100::Causal* causal = nullptr,
-                            const int32_t* glist = nullptr, int64_t n_list = 0) {
+                            const int32_t* glist = nullptr, int64_t n_list = 0,
+                            unsigned long long* sync_flags = nullptr, int64_t n_flags = 0) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
@@ -1282,7 +1282,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     } else {
       ws_o = reinterpret_cast<float*>(ws);
       ws_l = ws_o + (size_t)2 * p.ctas * sm100::BM * D;
-      flags = reinterpret_cast<unsigned long long*>(ws_l + (size_t)2 * p.ctas * sm100::BM);
+      if (sync_flags != nullptr && n_flags >= p.ctas) flags = sync_flags;
     }
     need_merge = !(p.T % p.ctas == 0 && (p.T / p.ctas) % p.tpi == 0);  // items never split
     // split items are merged inside the kernel when every CTA is resident at
@@ -1312,13 +1312,16 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
-                         float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                         unsigned long long* sync_flags, int64_t n_flags) {
   if (head_dim == 128)
     return launch_refresh_d<128, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
-                                        scale, o_out, lse_out, ws, ws_bytes, st);
+                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, nullptr,
+                                        nullptr, nullptr, 0, sync_flags, n_flags);
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
-                                       scale, o_out, lse_out, ws, ws_bytes, st);
+                                       scale, o_out, lse_out, ws, ws_bytes, st, nullptr, nullptr,
+                                       nullptr, nullptr, 0, sync_flags, n_flags);
   return FB_ERR_UNSUPPORTED;
 }
 

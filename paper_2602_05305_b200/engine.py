@@ -130,8 +130,11 @@ class FlashBlockAttention:
         lens = self._group_lengths(n_ext)
         if lens is None:
             self._count_rows(self.b * self.hkv * int(n_ext))
-            res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
-                                         o_ext=self.o_ext[layer], lse_ext=self.lse_ext[layer], out=o)
+            # K1 (in-kernel split merge through the device's sync flags) then K2
+            K.attention_partial(qg, kc, vc, 0, int(n_ext), self.scale, out=self.o_ext[layer],
+                                lse=self.lse_ext[layer])
+            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
+                                   self.out_dtype, out=o)
         else:
             self._count_rows(lens.clamp(max=kc.shape[1]))
             K.attention_partial_ragged(qg, kc, vc, lens, 0, self.scale, out=self.o_ext[layer],
@@ -230,8 +233,9 @@ class FlashBlockAttention:
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None
         self._count_rows(self.b * self.hkv * int(n_ext))
-        res, _, _ = K.full_attention(qg, kc, vc, n_ext, kg, vg, self.scale, self.out_dtype,
-                                     o_ext=o_scratch, lse_ext=lse_scratch, out=o)
+        o_ext, l_ext = K.attention_partial(qg, kc, vc, 0, int(n_ext), self.scale, out=o_scratch,
+                                           lse=lse_scratch)
+        res = K.internal_merge(qg, kg, vg, o_ext, l_ext, self.scale, self.out_dtype, out=o)
         return res.view(self.b, self.hq, self.B, self.d)
 
 

@@ -76,6 +76,26 @@ class _Workspace:
 WORKSPACE = _Workspace()
 
 
+class _SyncFlags:
+    """Per-device ready-flag buffer for K1's in-kernel split merge: zeroed once,
+    left zeroed by every launch, never shared with other scratch."""
+
+    def __init__(self):
+        self._bufs: dict[int, torch.Tensor] = {}
+
+    def get(self, device: torch.device) -> torch.Tensor:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        buf = self._bufs.get(idx)
+        if buf is None:
+            n = int(_lib.load().fb_sync_flags_count())
+            buf = torch.zeros(n, dtype=torch.int64, device=device)
+            self._bufs[idx] = buf
+        return buf
+
+
+SYNC_FLAGS = _SyncFlags()
+
+
 def gqa_view(q: torch.Tensor, num_kv_heads: int) -> torch.Tensor:
     """[b, Hq, B, d] -> [b*Hkv, (Hq/Hkv)*B, d] (no copy)."""
     b, hq, blk, d = q.shape
@@ -126,9 +146,10 @@ def attention_partial(q, k, v, key_begin: int = 0, key_end: int | None = None,
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     wsb = _lib.load().fb_partial_workspace_bytes(code, groups, q_rows, d, max(0, key_end - key_begin))
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_attention_partial", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
+    flags = SYNC_FLAGS.get(q3.device)
+    _lib.call("fb_attention_partial_sync", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
               int(key_begin), key_end, scale, _p(out), _p(lse), _p(ws),
-              0 if ws is None else ws.numel(), _stream(q3))
+              0 if ws is None else ws.numel(), _p(flags), flags.numel(), _stream(q3))
     return out, lse
 
 
