@@ -489,6 +489,8 @@ const char* fb_version(void) { return "fb200 0.1.0 sm_100a"; }
 // Diagnostics (not in the public header): per-CTA timestamps of the refresh kernel.
 FB_API void fb_debug_set_trace(void* device_buffer) { set_refresh_trace(device_buffer); }
 FB_API void fb_debug_set_k1_diag(int diag) { set_k1_diag(diag); }
+FB_API void fb_debug_set_pair(int on) { set_pair_enabled(on); }
+FB_API int64_t fb_debug_pair_launches(void) { return (int64_t)pair_launches(); }
 int64_t fb_launch_count(void) { return g_launches.load(); }
 
 size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,

@@ -80,6 +80,7 @@ struct Sched {
   int ctas;
   const long long* prefix; // ragged item offsets, or nullptr
   const int* glist;        // group subset (head-gated refresh): item group -> slab, or nullptr
+  int kv_keep;             // K/V tiles re-read by other query tiles of the group: keep in L2
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -250,7 +251,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const uint64_t keep = ptx::policy_evict_last();
       // K/V: streamed once (evict first), except block-causal prefill where
       // every later query tile of the group re-reads them (keep in L2)
-      const uint64_t stream = cz.blk > 0 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+      const uint64_t stream = (cz.blk > 0 || sc.kv_keep) ? ptx::policy_evict_last() : ptx::policy_evict_first();
       int j = 0, seg = 0, item = -1;
       for (long long t = t_begin; t < t_end; ++seg) {
         item = sc.item_next(t, item);
@@ -487,8 +488,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               ptx::f2_unpack(x2, x0, x1);
               float p0, p1;
               if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
-                p0 = ptx::ex2_poly(x0);
-                p1 = ptx::ex2_poly(x1);
+                ptx::ex2_poly2(x2, p0, p1);
               } else {
                 p0 = ptx::ex2(x0);
                 p1 = ptx::ex2(x1);
@@ -691,17 +691,17 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 __global__ void __launch_bounds__(256)
 refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o,
                      const float* __restrict__ ws_l, float* __restrict__ o_out,
-                     float* __restrict__ lse_out) {
+                     float* __restrict__ lse_out, int bm) {
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
   sc.resolve();
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // item*BM + row
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // item*bm + row
   const int lane = threadIdx.x & 31;
-  const int item = (int)(gw / BM);
-  const int row = (int)(gw % BM);
+  const int item = (int)(gw / bm);
+  const int row = (int)(gw % bm);
   if (item >= sc.items) return;
   const int g = sc.group_of(item), mt = sc.mtile_of(item);
-  const int grow = mt * BM + row;
+  const int grow = mt * bm + row;
   if (grow >= q_rows) return;
   const long long orow = (long long)g * q_rows + grow;
   const long long ib = sc.item_begin(item), ie = sc.item_end(item);
@@ -718,18 +718,18 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   auto has = [&](int c) { return sc.start(c + 1) > sc.start(c); };
   float mx = -INFINITY;
   for (int k = lane; k < nseg; k += 32)
-    if (has(c_first + k)) mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * BM + row]);
+    if (has(c_first + k)) mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * bm + row]);
   mx = warp_max(mx);
   float z = 0.f;
   for (int k = lane; k < nseg; k += 32)
-    if (has(c_first + k)) z += __expf(ws_l[sc.slot(c_first + k, item) * BM + row] - mx);
+    if (has(c_first + k)) z += __expf(ws_l[sc.slot(c_first + k, item) * bm + row] - mx);
   z = warp_sum(z);
   const float iz = 1.f / z;
   for (int c = lane * 4; c < D; c += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < nseg; ++k) {
       if (!has(c_first + k)) continue;
-      const long long sl = sc.slot(c_first + k, item) * BM + row;
+      const long long sl = sc.slot(c_first + k, item) * bm + row;
       const float w = __expf(ws_l[sl] - mx);
       const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
       acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
@@ -739,6 +739,8 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   }
   if (lane == 0) lse_out[orow] = mx + logf(z);
 }
+
+#include "fb_sm100_pair.cuh"  // K1 on CTA pairs (tensor-bound shapes)
 
 // ---------------------------------------------------------------- K5 scoring
 //
@@ -1102,9 +1104,18 @@ void set_refresh_trace(void* p) {
   g_trace_launch = 0;
 }
 
+static int pair_clusters();
+
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
   if (n_keys <= 0 || groups <= 0 || q_rows <= 0) return 0;
-  return plan_refresh(groups, q_rows, head_dim, n_keys).ws_bytes;
+  size_t b = plan_refresh(groups, q_rows, head_dim, n_keys).ws_bytes;
+  if (head_dim == 128 && q_rows > sm100::BM) {  // CTA-pair plan: 256-row split slots
+    const long long T = groups * ((q_rows + sm100::pair::PM - 1) / sm100::pair::PM) *
+                        ((n_keys + sm100::BN - 1) / sm100::BN);
+    const long long pairs = std::min<long long>(pair_clusters(), T);
+    b = std::max<size_t>(b, (size_t)2 * pairs * sm100::pair::PM * (head_dim + 1) * sizeof(float));
+  }
+  return b;
 }
 
 // ragged: split slots for num_sms CTAs + the item offsets
@@ -1153,22 +1164,22 @@ __global__ void ragged_prefix_kernel(const int* __restrict__ key_len, int items,
 // [0, lim) with lim the largest row limit of the tile (its last row, or the
 // head's full length when the tile straddles two heads); tile offsets as above.
 __device__ __forceinline__ long long causal_item_tiles(int i, int items, int m_tiles, int q_rows,
-                                                       sm100::Causal cz) {
+                                                       sm100::Causal cz, int bm) {
   const int mt = i % m_tiles;
-  const int r0 = mt * sm100::BM, r1 = min(r0 + sm100::BM, q_rows) - 1;
+  const int r0 = mt * bm, r1 = min(r0 + bm, q_rows) - 1;
   const int lim = (r0 / cz.n_q != r1 / cz.n_q) ? cz.n_prefix + cz.n_q : cz.row_limit(r1);
   return (lim + sm100::BN - 1) / sm100::BN;
 }
 
 __global__ void causal_prefix_kernel(int items, int m_tiles, int q_rows, sm100::Causal cz,
-                                     long long* __restrict__ prefix) {
+                                     long long* __restrict__ prefix, int bm) {
   __shared__ long long part[1024];
   __shared__ long long warp_sum_sh[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (items + nt - 1) / nt;
   const int i0 = min(items, tid * per), i1 = min(items, i0 + per);
   long long sum = 0;
-  for (int i = i0; i < i1; ++i) sum += causal_item_tiles(i, items, m_tiles, q_rows, cz);
+  for (int i = i0; i < i1; ++i) sum += causal_item_tiles(i, items, m_tiles, q_rows, cz, bm);
   part[tid] = sum;
   __syncthreads();
   if (tid < 32) {
@@ -1186,10 +1197,138 @@ __global__ void causal_prefix_kernel(int items, int m_tiles, int q_rows, sm100::
   for (int k = (tid / 32) * 32; k < tid; ++k) base += part[k];
   for (int i = i0; i < i1; ++i) {
     prefix[i] = base;
-    base += causal_item_tiles(i, items, m_tiles, q_rows, cz);
+    base += causal_item_tiles(i, items, m_tiles, q_rows, cz, bm);
   }
   if (i1 == items && i0 < i1) prefix[items] = base;
   if (items == 0 && tid == 0) prefix[0] = 0;
+}
+
+// CTA-pair K1 (fb_sm100_pair.cuh) for many query rows per group.  Default:
+// block-causal prefill only, where it measured 1.09-1.17x faster than the
+// single-CTA kernel (32K / 8K prompts at the C2 shapes); for the non-causal
+// C5 refresh the single-CTA kernel stays faster (1.50 vs 1.65-1.70 ms at
+// 56,160 keys; profiles/r01f_pair_notes.md).  Returns -1 when it does not
+// apply (workspace too small), so the caller runs the single-CTA kernel.
+// FB_PAIR=0 / 1: never / for every shape with > 128 query rows (diagnostics).
+// K/V cache policy when several query tiles of a group stream the same keys
+// (C5 chunks, prefill): evict_last keeps them in L2 for the other tiles;
+// otherwise (C2: one tile per group) they stream evict_first.  FB_KV_KEEP=0
+// disables it (diagnostics).
+static bool kv_keep_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FB_KV_KEEP");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+static int pair_mode() {  // 0 never, 1 always, 2 block-causal only
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("FB_PAIR");
+    m = e == nullptr ? 2 : (e[0] == '0' ? 0 : 1);
+  }
+  return m;
+}
+static int g_pair_override = -1;
+void set_pair_enabled(int on) { g_pair_override = on; }
+static long long g_pair_launches = 0;
+long long pair_launches() { return g_pair_launches; }
+
+static int pair_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    auto kern = sm100::pair::pair_kernel<128>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm100::pair::PCfg<128>::SMEM);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * (num_sms() / 2)));
+    cfg.blockDim = dim3(sm100::THREADS);
+    cfg.dynamicSmemBytes = sm100::pair::PCfg<128>::SMEM;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
+      cudaGetLastError();
+      c = num_sms() / 2;
+    }
+    n = c;
+  }
+  return n;
+}
+
+static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const CUtensorMap& mv,
+                           int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
+                           int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
+                           size_t ws_bytes, cudaStream_t st, const sm100::Causal* causal,
+                           const int32_t* glist, int64_t n_list) {
+  constexpr int D = 128;
+  using P = sm100::pair::PCfg<D>;
+  constexpr int PM = sm100::pair::PM;
+  const int m_tiles = (int)((q_rows + PM - 1) / PM);
+  const int items = (int)((glist ? n_list : groups) * m_tiles);
+  const long long tpi = (key_end - key_begin + sm100::BN - 1) / sm100::BN;
+  if (items <= 0 || tpi <= 0) return -1;
+  CUtensorMap mk;
+  int rc;
+  if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::pair::HN)))
+    return rc;
+  sm100::Causal cz{1, 0, 0};
+  if (causal) cz = *causal;
+  const int maxp = pair_clusters();
+  sm100::Sched sc{(long long)items * tpi, (int)tpi, m_tiles, items, 0, nullptr, glist};
+  sc.kv_keep = m_tiles > 1 && kv_keep_enabled();
+  float* ws_o = nullptr;
+  float* ws_l = nullptr;
+  bool need_merge;
+  if (causal) {
+    const size_t pre = align_up((size_t)(items + 1) * sizeof(long long), 256);
+    const size_t need = pre + (size_t)2 * maxp * PM * (D + 1) * sizeof(float);
+    if (ws == nullptr || ws_bytes < need) return -1;
+    long long* prefix = reinterpret_cast<long long*>(ws);
+    causal_prefix_kernel<<<1, 1024, 0, st>>>(items, m_tiles, (int)q_rows, cz, prefix, PM);
+    count_launch();
+    if ((rc = check_launch("prefix_kernel"))) return rc;
+    sc.prefix = prefix;
+    sc.tpi = 0;
+    sc.ctas = maxp;
+    ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + pre);
+    ws_l = ws_o + (size_t)2 * maxp * PM * D;
+    need_merge = true;
+  } else {
+    sc.ctas = (int)std::min<long long>(maxp, sc.T);
+    need_merge = !(sc.T % sc.ctas == 0 && (sc.T / sc.ctas) % tpi == 0);
+    if (need_merge) {
+      const size_t need = (size_t)2 * sc.ctas * PM * (D + 1) * sizeof(float);
+      if (ws == nullptr || ws_bytes < need) return -1;
+      ws_o = reinterpret_cast<float*>(ws);
+      ws_l = ws_o + (size_t)2 * sc.ctas * PM * D;
+    }
+  }
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = getenv("FB_PAIR_POLY");  // diagnostics: MUFU offload share
+    poly = e ? atoi(e) : 0;
+  }
+  auto kern = poly == 4 ? sm100::pair::pair_kernel<D, 4>
+              : poly == 3 ? sm100::pair::pair_kernel<D, 3>
+              : poly == 2 ? sm100::pair::pair_kernel<D, 2> : sm100::pair::pair_kernel<D, 0>;
+  static bool attr[9] = {};
+  if (!attr[poly & 7]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    attr[poly & 7] = true;
+  }
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  launch_pdl(kern, dim3((unsigned)(2 * sc.ctas)), dim3(sm100::THREADS), P::SMEM, st, mq, mk, mv, cz, sc,
+             (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l);
+  count_launch();
+  ++g_pair_launches;
+  if ((rc = check_launch("pair_kernel(sm100)"))) return rc;
+  if (!need_merge) return FB_OK;
+  const long long warps = (long long)items * PM;
+  launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM);
+  count_launch();
+  return check_launch("refresh_merge_kernel(sm100, pair)");
 }
 
 template <int D, bool GATHER>
@@ -1234,14 +1373,35 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ga.sel_tiles = (int)((gs->n_list + 7) / 8);
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   }
+  if constexpr (!GATHER && D == 128) {
+    const int pm = g_pair_override >= 0 ? g_pair_override : pair_mode();
+    const bool pair_on = pm == 1 || (pm == 2 && causal != nullptr);
+    if (pair_on && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
+      const int prc = launch_pair_128(k, mq, mv, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
+                                      o_out, lse_out, ws, ws_bytes, st, causal, glist, n_list);
+      if (prc != -1) return prc;
+    }
+  }
   auto kern = sm100::refresh_kernel<D, GATHER>;
   if constexpr (!GATHER && D == 128) {
     if (g_k1_diag == 1) kern = sm100::refresh_kernel<D, false, 1>;
     if (g_k1_diag == 2) kern = sm100::refresh_kernel<D, false, 2>;
     if (g_k1_diag == 3) kern = sm100::refresh_kernel<D, false, 0, 4>;  // 1/4 of the pairs on FMA
   }
-  static bool attr[5] = {false, false, false, false, false};
-  const int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 5 ? g_k1_diag : 0);
+  int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 5 ? g_k1_diag : 0);
+  if constexpr (!GATHER && D == 128) {
+    static int poly = -1;
+    if (poly < 0) {
+      const char* e = getenv("FB_K1_POLY");  // diagnostics: MUFU offload share 1/POLY
+      poly = e ? atoi(e) : 0;
+    }
+    if (g_k1_diag == 0 && poly >= 2 && poly <= 4) {
+      kern = poly == 2 ? sm100::refresh_kernel<D, false, 0, 2>
+             : poly == 3 ? sm100::refresh_kernel<D, false, 0, 3> : sm100::refresh_kernel<D, false, 0, 4>;
+      ai = 5 + poly;
+    }
+  }
+  static bool attr[10] = {};
   if (!attr[ai]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr[ai] = true;
@@ -1249,6 +1409,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   // group subset: items over the listed groups only (tensor maps span all groups)
   RefreshPlan p = plan_refresh(glist ? n_list : groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr, glist};
+  sc.kv_keep = p.m_tiles > 1 && kv_keep_enabled();
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   unsigned long long* flags = nullptr;  // in-kernel split merge (uniform items only)
@@ -1261,7 +1422,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
       return fail(FB_ERR_VALUE, "ragged / block-causal refresh needs its workspace");
     long long* prefix = reinterpret_cast<long long*>(ws);
     if (causal)
-      causal_prefix_kernel<<<1, 1024, 0, st>>>(p.items, p.m_tiles, (int)q_rows, cz, prefix);
+      causal_prefix_kernel<<<1, 1024, 0, st>>>(p.items, p.m_tiles, (int)q_rows, cz, prefix, (int)sm100::BM);
     else
       ragged_prefix_kernel<<<1, 1024, 0, st>>>(key_len, p.items, p.m_tiles, (int)key_begin,
                                                (int)key_end, prefix);
@@ -1304,7 +1465,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   if (!need_merge) return FB_OK;
   const long long warps = (long long)p.items * sm100::BM;
   launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
-             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out);
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, (int)sm100::BM);
   count_launch();
   return check_launch("refresh_merge_kernel(sm100)");
 }

@@ -148,6 +148,82 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       : "memory");
 }
 
+// ---------------------------------------------------------------- CTA pairs
+// cta_group::2: two CTAs of a cluster (same TPC) run one M = 256 MMA; A and D
+// are split by rows over the two CTAs' smem / TMEM, B by N columns.  Only the
+// leader (rank 0) issues MMAs; every tcgen05 instruction of such a kernel uses
+// cta_group::2.
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// Arrive on a (possibly remote) cluster barrier.  Default .release.cta
+// semantics as CUTLASS's ClusterBarrier::arrive(cta_id): the data handed over
+// is TMEM (completed by tcgen05.wait::st + fence::before_thread_sync), not
+// global memory, so no GPU-scope membar is needed on this per-tile path.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the leader's mbarrier
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, uint32_t bar_cluster,
+                                                 int c0, int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* holder_smem, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(holder_smem)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+               : "memory");
+}
+// arrive once on the mbarrier at this offset in both CTAs of the pair when the
+// leader's prior tcgen05 ops complete
+__device__ __forceinline__ void tc_commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> f32, A K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool b_mn_major) {
   return (1u << 4)      // D format f32
@@ -199,23 +275,6 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// pack two floats to bf16x2: `lo` in bits 0..15 (the even column)
-// 2^x on the FMA/ALU pipes (offloads the MUFU unit, as FlashAttention-4 does on
-// Blackwell): x = j + f with j = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3
-// minimax polynomial (max rel. error 7.5e-5, far below the bf16 rounding of P);
-// 2^j added into the exponent field.  x <= -127 (incl. -inf: masked keys)
-// returns exactly 0, like ex2.approx.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -126.f);
-  const float t = xc + 12582912.f;  // 1.5 * 2^23: rint(xc) lands in the low mantissa bits
-  const float j = t - 12582912.f;
-  const float f = xc - j;
-  const float p = fmaf(fmaf(fmaf(0.055171772837638855f, f, 0.24261115491390228f), f,
-                            0.6932609677314758f), f, 0.9999280571937561f);
-  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-  return x > -127.f ? r : 0.f;
-}
-
 // Packed fp32 pairs (FFMA2 / FADD2 on sm_100a): half the issue slots of the
 // scalar forms for the softmax's scale-and-shift and row-sum chains.
 __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
@@ -235,6 +294,47 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
+}
+
+// pack two floats to bf16x2: `lo` in bits 0..15 (the even column)
+// 2^x on the FMA/ALU pipes (offloads the MUFU unit, as FlashAttention-4 does on
+// Blackwell): x = j + f with j = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3
+// minimax polynomial (max rel. error 7.5e-5, far below the bf16 rounding of P);
+// 2^j added into the exponent field.  x <= -127 (incl. -inf: masked keys)
+// returns exactly 0, like ex2.approx.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float t = xc + 12582912.f;  // 1.5 * 2^23: rint(xc) lands in the low mantissa bits
+  const float j = t - 12582912.f;
+  const float f = xc - j;
+  const float p = fmaf(fmaf(fmaf(0.055171772837638855f, f, 0.24261115491390228f), f,
+                            0.6932609677314758f), f, 0.9999280571937561f);
+  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+  return x > -127.f ? r : 0.f;
+}
+
+// 2^x for a packed pair on the FMA pipes (FFMA2 / FADD2: ~12 issue slots per
+// pair, no MUFU), the same range reduction and polynomial as ex2_poly.  Used
+// for a fixed share of each tile's P pairs where MUFU.EX2 is the binding pipe
+// (tensor-bound shapes: C5, prefill -- 4 SM-cycles per warp-wide MUFU.EX2).
+__device__ __forceinline__ void ex2_poly2(uint64_t x2, float& p0, float& p1) {
+  float x0, x1;
+  f2_unpack(x2, x0, x1);
+  const uint64_t xc = f2_pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t t = f2_add(xc, f2_pack(12582912.f, 12582912.f));   // rint in the low mantissa
+  const uint64_t j = f2_add(t, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = f2_fma(j, f2_pack(-1.f, -1.f), xc);             // f = x - rint(x)
+  uint64_t p = f2_fma(f2_pack(0.055171772837638855f, 0.055171772837638855f), f,
+                      f2_pack(0.24261115491390228f, 0.24261115491390228f));
+  p = f2_fma(p, f, f2_pack(0.6932609677314758f, 0.6932609677314758f));
+  p = f2_fma(p, f, f2_pack(0.9999280571937561f, 0.9999280571937561f));
+  float pa, pb, ta, tb;
+  f2_unpack(p, pa, pb);
+  f2_unpack(t, ta, tb);
+  const float r0 = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
+  const float r1 = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
+  p0 = x0 > -127.f ? r0 : 0.f;  // masked keys (-inf) give exactly 0, like ex2.approx
+  p1 = x1 > -127.f ? r1 : 0.f;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
