@@ -284,11 +284,262 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   }
 }
 
+
+// ---------------------------------------------------------------- K2 v2
+// d = 128: one CTA per (group, 128-row query tile) with the cached external
+// partial prefetched into shared memory by TMA (fp32, 128B-swizzled boxes of
+// 32 columns: the epilogue's row-per-thread reads are bank-conflict free)
+// instead of registers.  On cached steps (ext_early) that 64 KB load is issued
+// before griddepcontrol.wait, and at ~115 KB of shared memory two CTAs fit per
+// SM, so at C2 (128 CTAs) the next layer's whole grid is resident and
+// prefetching while this one computes.  288 threads: warps 0-3 and 4-7 run the
+// merge epilogue on output columns 0-63 / 64-127 of the same rows (TMEM lane
+// quarter = warp % 4); warps 0-3 also run the softmax; warp 8 allocates TMEM,
+// issues the TMA loads and the two MMAs.
+constexpr int V2_THREADS = 288;
+
+template <int NT>
+struct CfgV2 {
+  static constexpr int D = 128;
+  static constexpr uint32_t QBOX = BM * 128;   // 16 KB (128 rows x 64 bf16)
+  static constexpr uint32_t KBOX = NT * 128;   // NT rows x 64 bf16
+  static constexpr uint32_t EBOX = BM * 128;   // 16 KB (128 rows x 32 fp32)
+  // barriers sit below the 1024-aligned tile area (dynamic shared memory
+  // starts 1024-aligned after the 1 KB system reservation, so the tiles begin
+  // at base + 1024); two CTAs per SM need SMEM <= 115,712 B
+  static constexpr uint32_t OFF_Q = 0;  // offsets from the aligned tile base
+  static constexpr uint32_t OFF_K = OFF_Q + 2 * QBOX;
+  static constexpr uint32_t OFF_V = OFF_K + 2 * KBOX;
+  static constexpr uint32_t OFF_E = (OFF_V + 2 * KBOX + 1023) / 1024 * 1024;
+  static constexpr uint32_t OFF_X = OFF_K;  // [2][128] floats of WG0, over K (dead after S = Q K^T)
+  static constexpr uint32_t TILES = OFF_E + 4 * EBOX;
+  static constexpr uint32_t SMEM = 1024 + TILES;
+  static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;
+  static constexpr uint32_t TMEM_COLS = (COL_O + D) <= 256 ? 256 : 512;
+  static constexpr uint32_t TX_QKV = 2 * (QBOX + 2 * KBOX);
+  static constexpr uint32_t TX_E = 4 * EBOX;
+};
+
+struct BarsV2 {
+  uint64_t load_qkv, load_e, s_full, p_ready, o_full;
+  uint32_t tmem_base;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(V2_THREADS, 2)
+internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_e,
+                         const float* __restrict__ lse_ext, int q_rows, int m_tiles, int n_in,
+                         float scale_log2, void* __restrict__ out, int out_bf16,
+                         float* __restrict__ lse_merged, float* __restrict__ o_int,
+                         float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early) {
+  using C = CfgV2<NT>;
+  constexpr int D = C::D;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  BarsV2* bar = reinterpret_cast<BarsV2*>(smem_raw);
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + sizeof(BarsV2) + 1023) & ~uintptr_t(1023));
+  if (smem + C::TILES > smem_raw + C::SMEM) __trap();  // base not 1024-aligned: layout bug
+  float* xch = reinterpret_cast<float*>(smem + C::OFF_X);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x / m_tiles;
+  const int mt = blockIdx.x % m_tiles;
+  const int wq = warp & 3, wg = warp >> 2;  // epilogue: lane quarter, column half
+  const int row = wq * 32 + lane;
+  const int grow = mt * BM + row;
+  const bool live_row = warp < 8 && grow < q_rows;
+  const long long rr = (long long)g * q_rows + grow;
+
+  float le = -INFINITY;
+  if (ext_early && live_row) le = __ldg(lse_ext + rr);
+  if (threadIdx.x == 256) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+    ptx::tma_prefetch_desc(&tm_e);
+    ptx::mbar_init(&bar->load_qkv, 1);
+    ptx::mbar_init(&bar->load_e, 1);
+    ptx::mbar_init(&bar->s_full, 1);
+    ptx::mbar_init(&bar->p_ready, 128);
+    ptx::mbar_init(&bar->o_full, 1);
+    ptx::fence_barrier_init();
+    if (ext_early) {  // the cached partial is final before this launch: fetch it now
+      const uint64_t pol = ptx::policy_evict_first();
+      ptx::mbar_expect_tx(&bar->load_e, C::TX_E);
+      for (int b = 0; b < 4; ++b)
+        ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * 32, mt * BM, g, pol);
+    }
+  }
+  if (warp == 8) ptx::tmem_alloc(&bar->tmem_base, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bar->tmem_base;
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
+
+  if (warp == 8) {
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      if (!ext_early) {
+        ptx::mbar_expect_tx(&bar->load_e, C::TX_E);
+        for (int b = 0; b < 4; ++b)
+          ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * 32, mt * BM, g, pol);
+      }
+      ptx::mbar_expect_tx(&bar->load_qkv, C::TX_QKV);
+      for (int b = 0; b < 2; ++b) {
+        ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
+        ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
+        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, b * BOX, 0, g, pol);
+      }
+      constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
+      constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
+      ptx::mbar_wait(&bar->load_qkv, 0);
+      ptx::tc_fence_after();
+      const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
+      const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K);
+      const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        ptx::mma_ss(tmem + C::COL_S,
+                    ptx::sdesc_sw128(q_base + (kk / 4) * C::QBOX + (kk % 4) * 32, 16, 1024),
+                    ptx::sdesc_sw128(k_base + (kk / 4) * C::KBOX + (kk % 4) * 32, 16, 1024),
+                    IDESC_S, kk > 0);
+      ptx::tc_commit(&bar->s_full);
+      ptx::mbar_wait(&bar->p_ready, 0);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < NT / 16; ++kk)
+        ptx::mma_ts(tmem + C::COL_O, tmem + C::COL_S + kk * 8,
+                    ptx::sdesc_sw128(v_base + kk * 2048, C::KBOX, 1024), IDESC_O, kk > 0);
+      ptx::tc_commit(&bar->o_full);
+    }
+  } else {
+    if (!ext_early && live_row) le = __ldg(lse_ext + rr);
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    uint32_t r[32];
+    if (wg == 0) {
+      // ------------------------------------------------ softmax (WG0)
+      float s[NT];
+      ptx::mbar_wait(&bar->s_full, 0);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < NT / 32 + (NT % 32 ? 1 : 0); ++c) {
+        ptx::tmem_ld32(tmem + lane_off + C::COL_S + c * 32, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < NT) s[c * 32 + i] = __uint_as_float(r[i]);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        if (i >= n_in) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      const float m2 = mx * scale_log2;
+      const float neg = (n_in > 0) ? -m2 : 0.f;
+      float l = 0.f;
+#pragma unroll
+      for (int c = 0; c < (NT + 63) / 64; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int j = c * 64 + 2 * i;
+          float p0 = 0.f, p1 = 0.f;
+          if (j < NT) {
+            p0 = ptx::ex2(fmaf(s[j], scale_log2, neg));
+            p1 = ptx::ex2(fmaf(s[j + 1], scale_log2, neg));
+          }
+          l += p0 + p1;
+          r[i] = ptx::pack_bf16(p0, p1);
+        }
+        ptx::tmem_st32(tmem + lane_off + C::COL_S + c * 32, r);
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&bar->p_ready);
+      xch[row] = m2;
+      xch[BM + row] = l;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float m2 = xch[row], l = xch[BM + row];
+    const bool has_int = n_in > 0;
+    const float li = has_int ? (m2 + log2f(l)) * 0.69314718055994530942f : -INFINITY;
+    const float inv = has_int ? 1.f / l : 0.f;
+    const float mm = fmaxf(le, li);
+    const bool live = mm != -INFINITY;
+    const float we = live ? __expf(le - mm) : 0.f;
+    const float wi = live ? __expf(li - mm) : 0.f;
+    const float z = we + wi;
+    const float iz = live ? 1.f / z : 0.f;
+    ptx::mbar_wait(&bar->load_e, 0);
+    ptx::mbar_wait(&bar->o_full, 0);
+    ptx::tc_fence_after();
+    const unsigned char* erow = smem + C::OFF_E + row * 128;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int c = wg * 2 + cc;  // 32-column chunk = fp32 box c
+      ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
+      float oc[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v4 = *reinterpret_cast<const float4*>(erow + c * C::EBOX + ((j ^ (row & 7)) << 4));
+        oc[4 * j] = v4.x; oc[4 * j + 1] = v4.y; oc[4 * j + 2] = v4.z; oc[4 * j + 3] = v4.w;
+      }
+      ptx::tmem_wait_ld();
+      float val[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float oi = __uint_as_float(r[i]) * inv;
+        val[i] = live ? (__fmul_rn(we, oc[i]) + __fmul_rn(wi, oi)) * iz : 0.f;
+        r[i] = __float_as_uint(oi);
+      }
+      if (live_row) {
+        if (out_bf16) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * D + c * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]),
+                                ptx::pack_bf16(val[8 * j + 2], val[8 * j + 3]),
+                                ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]),
+                                ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
+        } else {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * D + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(val[4 * j], val[4 * j + 1], val[4 * j + 2], val[4 * j + 3]);
+        }
+        if (o_int) {
+          float4* di = reinterpret_cast<float4*>(o_int + rr * D + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            di[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+      }
+    }
+    if (live_row && wg == 0) {
+      if (lse_int) lse_int[rr] = li;
+      if (lse_merged) lse_merged[rr] = live ? mm + logf(z) : -INFINITY;
+      if (!live && empty_rows) atomicAdd(empty_rows, 1);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
 }  // namespace sm100k2
 
 // host: tensor maps shared with the refresh kernel's encoder
 int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t inner, int64_t dim1,
                  int64_t dim1_stride_elems, int64_t dim2, int box_inner, int box_rows);
+
+static int g_k2_v2_override = -1;
+void set_k2_v2(int v) { g_k2_v2_override = v; }
 
 bool sm100_k2_supported(int64_t head_dim, int64_t n_in) {
   // n_in == 0 (no current-block keys) takes the SIMT path: there is nothing to load
@@ -323,6 +574,35 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   return check_launch("internal_merge_kernel(sm100)");
 }
 
+template <int NT>
+static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
+                        int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
+                        const float* lse_ext, void* out, bool out_bf16, float* lse_merged, float* o_int,
+                        float* lse_int, int32_t* empty, bool ext_early, cudaStream_t st) {
+  using C = sm100k2::CfgV2<NT>;
+  constexpr int D = 128;
+  CUtensorMap mq, mk, mv, me;
+  int rc;
+  if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
+  const int64_t nin_eff = n_in > 0 ? n_in : 1;
+  if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
+  if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
+  if ((rc = make_tmap_3d(&me, o_ext, 4, D, q_rows, q_rows, groups, 32, sm100k2::BM))) return rc;
+  auto kern = sm100k2::internal_merge_v2_kernel<NT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  launch_pdl(kern, dim3((unsigned)(groups * m_tiles)), dim3(sm100k2::V2_THREADS), C::SMEM, st, mq, mk,
+             mv, me, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
+             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), ext_early ? 1 : 0);
+  count_launch();
+  return check_launch("internal_merge_v2_kernel(sm100)");
+}
+
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,
                                 const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
                                 int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
@@ -339,6 +619,28 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
   // (C2 b=16: 5.7 vs 8.2 us; b=24: 9.9 vs 10.8; b=32: 11.3 vs 14.5, 1.7 waves)
   bool split = true;
   if (const char* e = getenv("FB_K2_SPLIT")) split = e[0] == '1';  // diagnostics
+  // v2 (O_ext prefetched into smem by TMA, whole rows per CTA, two CTAs per
+  // SM) once the query tiles outnumber the SMs: measured at C2 (36 layers x 31
+  // cached steps in one graph) b=32 9.2 vs 11.3 us per launch, while at b=16 /
+  // b=4 (128 / 32 tiles) v1's column split over 2 CTAs stays faster (5.7 vs
+  // 6.0 us, 4.2 vs 5.1 us).  FB_K2_V2=0 / 1 forces v1 / v2 (diagnostics).
+  static int v2_env = -2;
+  if (v2_env == -2) {
+    const char* e = getenv("FB_K2_V2");
+    v2_env = e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
+  }
+  const int v2 = g_k2_v2_override >= 0 ? g_k2_v2_override : v2_env;
+  const int64_t k2_tiles = groups * ((q_rows + sm100k2::BM - 1) / sm100k2::BM);
+  const bool use_v2 = v2 == 1 || (v2 == -1 && k2_tiles > num_sms());
+  if (head_dim == 128 && use_v2 && n_in <= 64 && (reinterpret_cast<uintptr_t>(o_ext) & 15) == 0) {
+#define FB_K2V2(NN) return launch_k2_v2<NN>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext, out, \
+                                            out_bf16, lse_merged, o_int, lse_int, empty, ext_early, st)
+    if (n_in <= 16) FB_K2V2(16);
+    if (n_in <= 32) FB_K2V2(32);
+    if (n_in <= 64) FB_K2V2(64);
+#undef FB_K2V2
+    // (n_in > 64: the 128-key score row does not fit beside 96 registers; v1)
+  }
   if (head_dim == 128) {
     if (n_in <= 16) FB_K2(128, 16);
     if (n_in <= 32) FB_K2(128, 32);

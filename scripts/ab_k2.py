@@ -1,8 +1,14 @@
 """Interleaved A/B of the cached step (K2, engine.cached -> fb_internal_merge_ex)
-between two library builds: graph of 36 layers x 31 cached steps at C2 b=16."""
+between two library builds: graph of 36 layers x 31 cached steps at C2 b=16.
+
+    python scripts/ab_k2.py libA.so libB.so [batch] [ENV=VAL for A] [ENV=VAL for B]
+
+The optional environment settings are applied just before each library's
+first call (the library reads its FB_* switches once)."""
 import ctypes as C, math, os, sys, torch
 A, B = sys.argv[1], sys.argv[2]
 b = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+ENV = {"A": sys.argv[4] if len(sys.argv) > 4 else "", "B": sys.argv[5] if len(sys.argv) > 5 else ""}
 HQ, HKV, D, BLK, L = 32, 8, 128, 32, 36
 groups, rows = b * HKV, 4 * BLK
 libs = {}
@@ -33,6 +39,9 @@ for n, lib in libs.items():
                                               out[i].data_ptr(), 2, None, None, None, None, None, 0, 1,
                                               s.cuda_stream)
                 assert rc == 0, rc
+    if ENV[n]:
+        k, v = ENV[n].split("=", 1)
+        os.environ[k] = v
     with torch.cuda.stream(s):
         fn(); torch.cuda.synchronize()
         gr = torch.cuda.CUDAGraph()

@@ -6,6 +6,8 @@ Parity: against the float64 oracle on bf16-exact inputs (max|diff| <=
 and against the single-CTA kernel on the same inputs (both run the same
 per-row online softmax; outputs within 5e-3 relative, lognorms 1e-4).  Each
 case asserts that the pair kernel actually ran (fb_debug_pair_launches).
+The cached-step (K2) variants v1 / v2 are checked against each other and the
+oracle at the end (fb_debug_set_k2_variant).
 """
 
 import ctypes
@@ -146,3 +148,35 @@ def test_pair_large_block_cached_step(lib):
     for h in (0, H - 1):
         ref = orc.dense(q[h].double().cpu().numpy(), kk[h], vv[h])
         assert _rel(outp[h].cpu().numpy(), ref) <= 1e-2
+
+
+@pytest.mark.parametrize("b,n_in", [(2, 32), (20, 32), (3, 16), (2, 64), (1, 1)])
+def test_cached_step_v1_v2_agree_and_match_oracle(lib, b, n_in):
+    """K2 variants (v1: O_ext in registers, columns split over 2 CTAs; v2:
+    O_ext prefetched into swizzled smem by TMA, whole rows per CTA) on the
+    same C2-shaped inputs: both within the bf16 bound of the oracle and of
+    each other.  The size rule picks v2 only when query tiles > SMs."""
+    from paper_2602_05305_b200 import kernels as K
+
+    lib.fb_debug_set_k2_variant.argtypes = [ctypes.c_int]
+    g = torch.Generator(device="cuda").manual_seed(b * 10 + n_in)
+    groups, rows, d = b * 8, 128, 128
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    q, ki, vi = r(groups, rows, d), r(groups, n_in, d), r(groups, n_in, d)
+    k, v = r(groups, 300, d), r(groups, 300, d)
+    o_ext, l_ext = K.attention_partial(q, k, v)
+    outs = []
+    for var in (0, 1):
+        lib.fb_debug_set_k2_variant(var)
+        o, lse = K.internal_merge(q, ki, vi, o_ext, l_ext, out_dtype=torch.float32, want_lse=True)
+        torch.cuda.synchronize()
+        outs.append((o, lse))
+    lib.fb_debug_set_k2_variant(-1)
+    (o1, l1), (o2, l2) = outs
+    assert ((o1 - o2).abs().amax() / o1.abs().amax()).item() <= 1e-5
+    assert (l1 - l2).abs().max().item() <= 1e-5
+    kk = torch.cat([k, ki], 1).double().cpu().numpy()
+    vv = torch.cat([v, vi], 1).double().cpu().numpy()
+    for gi in (0, groups - 1):
+        ref = orc.dense(q[gi].double().cpu().numpy(), kk[gi], vv[gi])
+        assert _rel(o2[gi].cpu().numpy(), ref) <= 1e-2
