@@ -1450,7 +1450,9 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     // once (one per SM: the waits always make progress) and an item spans at
     // most 3 CTAs (the owner merges <= 2 partials; measured at b = 1, where an
     // item spans ~19 CTAs, the parallel merge kernel is 2.6x faster)
-    const bool short_spans = 2 * (p.T / p.ctas) >= p.tpi;
+    int max_span = 3;
+    if (const char* e = getenv("FB_K1_MAXSPAN")) max_span = std::max(2, atoi(e));  // diagnostics
+    const bool short_spans = (long long)(max_span - 1) * (p.T / p.ctas) >= p.tpi;
     if (need_merge && flags != nullptr && short_spans && p.ctas <= num_sms() && g_k1_diag != 5)
       need_merge = false;
     else
