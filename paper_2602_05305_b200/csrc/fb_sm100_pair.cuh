@@ -99,9 +99,10 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     ptx::mbar_init(&bar->o_empty, 16);       // 8 softmax warps x 2 CTAs
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc2(&bar->tmem_base, TMEM_COLS);
-  ptx::tc_fence_before();
   ptx::cluster_sync();  // both CTAs' barriers initialised before any remote arrive / TMA
+  if (warp == 2) ptx::tmem_alloc2(&bar->tmem_base, TMEM_COLS);  // after the cluster barrier
+  ptx::tc_fence_before();
+  __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
   ptx::pdl_wait();

@@ -180,3 +180,33 @@ def test_cached_step_v1_v2_agree_and_match_oracle(lib, b, n_in):
     for gi in (0, groups - 1):
         ref = orc.dense(q[gi].double().cpu().numpy(), kk[gi], vv[gi])
         assert _rel(o2[gi].cpu().numpy(), ref) <= 1e-2
+
+
+def test_pair_full_size_properties(lib):
+    """BASELINE sizes, size-independent properties (the oracle cannot run
+    these in seconds): C5 (12 heads x 4680 rows x 56,160 keys) pair kernel ==
+    single-CTA kernel, and K1 over [0, N) == combine(K1 [0, a), K1 [a, N)) on
+    the pair kernel; prefill at the C2 shapes with an 8K prompt: pair ==
+    single-CTA."""
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(4680)
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    q, k, v = r(12, 4680, 128), r(12, 56160, 128), r(12, 56160, 128)
+    (op, lp), (o1, l1) = _run_both(lib, lambda: K.attention_partial(q, k, v))
+    assert ((op - o1).abs().amax() / o1.abs().amax()).item() <= 5e-3
+    assert (lp - l1).abs().max().item() <= 1e-4
+    lib.fb_debug_set_pair(1)
+    a = 20000
+    pa = K.attention_partial(q, k, v, 0, a)
+    pb = K.attention_partial(q, k, v, a, 56160)
+    lib.fb_debug_set_pair(-1)
+    oc, lc = K.combine([pa, pb])
+    assert ((oc - op).abs().amax() / op.abs().amax()).item() <= 5e-3
+    assert (lc - lp).abs().max().item() <= 1e-4
+    del q, k, v
+    n_q = 8192
+    qp, kp, vp = r(8, 4 * n_q, 128), r(8, n_q, 128), r(8, n_q, 128)
+    (op, lp), (o1, l1) = _run_both(lib, lambda: K.block_causal_attention(qp, kp, vp, n_q, 0, 32))
+    assert ((op - o1).abs().amax() / o1.abs().amax()).item() <= 5e-3
+    assert (lp - l1).abs().max().item() <= 1e-4
