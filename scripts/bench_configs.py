@@ -59,6 +59,71 @@ def emit(out, rec):
     out.write(line + "\n")
 
 
+# ---------------------------------------------------------------- C2 layer
+
+
+def c2layer(out):
+    """the C2 attention LAYER -- QKV projection (4096 -> 6144),
+    FlashBlock attention, O projection (4096 -> 4096) -- with random-init bf16
+    weights, b=16, 32K context, tau=2 schedule (1 refresh + 31 cached steps per
+    32-step block) vs full recompute every step.  Projections are plain cuBLAS
+    GEMMs (torch.matmul), head-major outputs straight from a batched GEMM; no
+    RoPE / norms (not part of the reference's attention path).  L distinct
+    layers (weights + KV) per graph so nothing stays in L2; per-layer times."""
+    from paper_2602_05305_b200 import FlashBlockAttention
+    HQ, HKV, D, B, N, DM, b, L = 32, 8, 128, 32, 32768, 4096, 16, 6
+    g = torch.Generator(device=DEV).manual_seed(2)
+    NQKV = (HQ + 2 * HKV) * D  # 6144
+    x = [rnd(g, b * B, DM) for _ in range(L)]
+    wqkv = [(rnd(g, DM, NQKV).float() * DM ** -0.5).to(torch.bfloat16) for _ in range(L)]
+    wo = [(rnd(g, DM, DM).float() * DM ** -0.5).to(torch.bfloat16) for _ in range(L)]
+    qkv = [torch.empty(b * B, NQKV, device=DEV, dtype=torch.bfloat16) for _ in range(L)]
+    kc = [rnd(g, b, HKV, N, D) for _ in range(L)]
+    vc = [rnd(g, b, HKV, N, D) for _ in range(L)]
+    att = [torch.empty(b, HQ, B, D, device=DEV, dtype=torch.bfloat16) for _ in range(L)]
+    y = [torch.empty(b * B, DM, device=DEV, dtype=torch.bfloat16) for _ in range(L)]
+    eng = FlashBlockAttention(L, b, HQ, HKV, B, D, device=DEV)
+    groups, rows = b * HKV, (HQ // HKV) * B
+    o_scr = torch.empty(groups, rows, D, device=DEV, dtype=torch.float32)
+    l_scr = torch.empty(groups, rows, device=DEV, dtype=torch.float32)
+
+    def proj_in(l):
+        torch.matmul(x[l], wqkv[l], out=qkv[l])            # one fused QKV GEMM
+        t = qkv[l].view(b, B, HQ + 2 * HKV, D).permute(0, 2, 1, 3)  # head-major views
+        return (t[:, :HQ].contiguous(), t[:, HQ:HQ + HKV].contiguous(), t[:, HQ + HKV:].contiguous())
+
+    def layer(l, mode):
+        q, ki, vi = proj_in(l)
+        if mode == "refresh":
+            eng.refresh(l, q, kc[l], vc[l], N, ki, vi, out=att[l])
+        elif mode == "cached":
+            eng.cached(l, q, ki, vi, out=att[l])
+        else:
+            eng.full_recompute(q, kc[l], vc[l], N, ki, vi, out=att[l], o_scratch=o_scr, lse_scratch=l_scr)
+        torch.matmul(att[l].permute(0, 2, 1, 3).reshape(b * B, DM), wo[l].t(), out=y[l])
+
+    eng.begin_block(0)
+    for l in range(L):
+        layer(l, "refresh")
+    t_ref = graph_ms(lambda: [layer(l, "refresh") for l in range(L)], reps=3) / L
+    t_cac = graph_ms(lambda: [layer(l, "cached") for l in range(L)], reps=3) / L
+    t_full = graph_ms(lambda: [layer(l, "full") for l in range(L)], reps=3) / L
+    t_gemm = graph_ms(lambda: [(proj_in(l), torch.matmul(att[l].permute(0, 2, 1, 3).reshape(b * B, DM),
+                                                         wo[l].t(), out=y[l])) for l in range(L)], reps=3) / L
+    fb_block = t_ref + 31 * t_cac
+    full_block = 32 * t_full
+    emit(out, {"config": "C2-layer", "batch": b, "ctx": N, "d_model": DM, "q_heads": HQ, "kv_heads": HKV,
+               "layer_refresh_ms": t_ref, "layer_cached_ms": t_cac, "layer_full_recompute_ms": t_full,
+               "projections_only_ms": t_gemm,
+               "tokens_per_s_36_layers": b * B / (36 * fb_block * 1e-3),
+               "full_recompute_tokens_per_s_36_layers": b * B / (36 * full_block * 1e-3),
+               "speedup_vs_full_recompute": full_block / fb_block,
+               "note": "per layer: QKV GEMM + attention + O GEMM (cuBLAS projections, random-init "
+                       "weights); block = 1 refresh + 31 cached steps (tau=2 schedule)"})
+    del kc, vc
+    torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- C3
 
 
@@ -278,7 +343,7 @@ def c1(out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c3,c4,c5,f4,f3,c1")
+    ap.add_argument("--only", default="c2layer,c3,c4,c5,f4,f3,c1")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.jsonl"))
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
