@@ -81,6 +81,7 @@ struct Sched {
   const long long* prefix; // ragged item offsets, or nullptr
   const int* glist;        // group subset (head-gated refresh): item group -> slab, or nullptr
   int kv_keep;             // K/V tiles re-read by other query tiles of the group: keep in L2
+  int rr;                  // pair kernel: round-robin whole items (block-causal), no stream-K
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -526,7 +527,9 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           const float m_new = fmaxf(m_used, mx * scale_log2);
           const bool need = m_new > m_used + RESCALE_THRESHOLD;
           if (__any_sync(0xffffffffu, need)) {
-            const float alpha = ptx::ex2(m_used - m_new);
+            // a row with no key yet on both sides (m_used = m_new = -inf) keeps l = 0:
+            // ex2(-inf - -inf) would be NaN
+            const float alpha = m_new == -INFINITY ? 1.f : ptx::ex2(m_used - m_new);
             if (t >= 2) {
               // O[wg] holds this segment's P V so far: wait for its last PV (tile j-2)
               ptx::mbar_wait(&bar->pv_done[wg], ((j - 2) >> 1) & 1);
@@ -1281,19 +1284,12 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   float* ws_l = nullptr;
   bool need_merge;
   if (causal) {
-    const size_t pre = align_up((size_t)(items + 1) * sizeof(long long), 256);
-    const size_t need = pre + (size_t)2 * maxp * PM * (D + 1) * sizeof(float);
-    if (ws == nullptr || ws_bytes < need) return -1;
-    long long* prefix = reinterpret_cast<long long*>(ws);
-    causal_prefix_kernel<<<1, 1024, 0, st>>>(items, m_tiles, (int)q_rows, cz, prefix, PM);
-    count_launch();
-    if ((rc = check_launch("prefix_kernel"))) return rc;
-    sc.prefix = prefix;
+    // whole items round-robin over the pairs (SegIter): no prefix scan, no
+    // split partials, no merge kernel; all pairs on one group's K/V at a time
+    sc.rr = 1;
     sc.tpi = 0;
-    sc.ctas = maxp;
-    ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + pre);
-    ws_l = ws_o + (size_t)2 * maxp * PM * D;
-    need_merge = true;
+    sc.ctas = std::min(maxp, items);
+    need_merge = false;
   } else {
     sc.ctas = (int)std::min<long long>(maxp, sc.T);
     need_merge = !(sc.T % sc.ctas == 0 && (sc.T / sc.ctas) % tpi == 0);

@@ -57,6 +57,56 @@ struct PBars {
 static_assert(sizeof(PBars) <= 512, "pair barrier block overflows its smem slot");
 static_assert(PCfg<128>::SMEM <= 232448, "pair kernel shared memory exceeds 227 KB");
 
+// A pair's work as a sequence of segments (part of one item each).
+//  * stream-K (sc.rr == 0): the pair's contiguous tile range [t_begin, t_end);
+//  * round-robin whole items (sc.rr == 1, block-causal prefill): pair p runs
+//    items p, p + P, p + 2P, ... of one group after another, each in one
+//    segment (no split partials, no merge kernel), so at any time all pairs
+//    stream the same group's keys and its K/V (16.8 MB at a 32K prompt) stays
+//    in L2.  Within a group the items go longest first (query positions
+//    descending, heads interleaved) when 256-row tiles do not straddle heads.
+struct Seg {
+  int item;
+  long long ib, t0;  // item's first tile, segment's first tile (same space)
+  int n;             // tiles in the segment
+  bool whole;
+};
+struct SegIter {
+  long long t, t_begin, t_end;
+  int item, k, pr, npairs;
+  __device__ __forceinline__ bool next(const Sched& sc, const Causal& cz, int q_rows, Seg& s) {
+    if (sc.rr) {
+      const int idx = k * npairs + pr;
+      if (idx >= sc.items) return false;
+      ++k;
+      const int gi = idx / sc.m_tiles, r = idx % sc.m_tiles;
+      int mt = r;
+      if (cz.n_q % PM == 0 && sc.m_tiles % (cz.n_q / PM) == 0) {
+        const int tph = cz.n_q / PM, heads = sc.m_tiles / tph;
+        mt = (r % heads) * tph + (tph - 1 - r / heads);
+      }
+      s.item = gi * sc.m_tiles + mt;
+      const int r0 = mt * PM, r1 = min(r0 + PM, q_rows) - 1;
+      const int lim = (r0 / cz.n_q != r1 / cz.n_q) ? cz.n_prefix + cz.n_q : cz.row_limit(r1);
+      s.ib = 0;
+      s.t0 = 0;
+      s.n = (lim + BN - 1) / BN;
+      s.whole = true;
+      return true;
+    }
+    if (t >= t_end) return false;
+    item = sc.item_next(t, item);
+    s.item = item;
+    s.ib = sc.item_begin(item);
+    s.t0 = t;
+    const long long ie = sc.item_end(item);
+    s.n = (int)(min(t_end, ie) - t);
+    s.whole = s.ib >= t_begin && ie <= t_end;
+    t += s.n;
+    return true;
+  }
+};
+
 template <int D, int POLY = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -74,9 +124,10 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
   const int pr = blockIdx.x >> 1;  // pair index = stream-K "CTA"
-  sc.resolve();
-  const long long t_begin = sc.start(pr);
-  const long long t_end = sc.start(pr + 1);
+  const int npairs = gridDim.x >> 1;
+  if (!sc.rr) sc.resolve();
+  const long long t_begin = sc.rr ? 0 : sc.start(pr);
+  const long long t_end = sc.rr ? 0 : sc.start(pr + 1);
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tm_q);
@@ -115,12 +166,14 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       if (lane == 0) {
         const uint64_t keep = ptx::policy_evict_last();
         const uint64_t stream = (cz.blk > 0 || sc.kv_keep) ? ptx::policy_evict_last() : ptx::policy_evict_first();
-        int j = 0, seg = 0, item = -1;
-        for (long long t = t_begin; t < t_end; ++seg) {
-          item = sc.item_next(t, item);
-          const long long ib = sc.item_begin(item);
-          const long long seg_end = min(t_end, sc.item_end(item));
-          const int g = sc.group_of(item), mt = sc.mtile_of(item);
+        int j = 0, seg = 0;
+        SegIter it{t_begin, t_begin, t_end, -1, 0, pr, npairs};
+        Seg sg;
+        for (; it.next(sc, cz, q_rows, sg); ++seg) {
+          const long long ib = sg.ib;
+          long long t = sg.t0;
+          const long long seg_end = sg.t0 + sg.n;
+          const int g = sc.group_of(sg.item), mt = sc.mtile_of(sg.item);
           if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
           if (leader) ptx::mbar_expect_tx(&bar->q_full, 2 * C::Q_BYTES);
           const uint32_t qf = ptx::mapa(&bar->q_full, 0);
@@ -150,10 +203,11 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(PM, BN, false);
         constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(PM, D, true);
         const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
-        int jg = 0, seg = 0, item = -1;
-        for (long long t0 = t_begin; t0 < t_end; ++seg) {
-          item = sc.item_next(t0, item);
-          const int n = (int)(min(t_end, sc.item_end(item)) - t0);
+        int jg = 0, seg = 0;
+        SegIter it{t_begin, t_begin, t_end, -1, 0, pr, npairs};
+        Seg sg;
+        for (; it.next(sc, cz, q_rows, sg); ++seg) {
+          const int n = sg.n;
           ptx::mbar_wait(&bar->q_full, seg & 1);
           ptx::tc_fence_after();
           for (int t = 0; t <= n; ++t) {
@@ -194,7 +248,6 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
             }
           }
           jg += n;
-          t0 += n;
         }
       }
     }
@@ -211,12 +264,14 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const uint32_t o_empty_l = ptx::mapa(&bar->o_empty, 0);
     uint32_t r[32];
     float s[BN];
-    int jg = 0, seg = 0, item = -1;
-    for (long long t0 = t_begin; t0 < t_end; ++seg) {
-      item = sc.item_next(t0, item);
-      const long long ib = sc.item_begin(item);
-      const int lt0 = (int)(t0 - ib);
-      const int n = (int)(min(t_end, sc.item_end(item)) - t0);
+    int jg = 0, seg = 0;
+    SegIter it{t_begin, t_begin, t_end, -1, 0, pr, npairs};
+    Seg sg;
+    for (; it.next(sc, cz, q_rows, sg); ++seg) {
+      const int item = sg.item;
+      const long long ib = sg.ib;
+      const int lt0 = (int)(sg.t0 - ib);
+      const int n = sg.n;
       const int kb = key_begin + lt0 * BN;
       const int mt = sc.mtile_of(item);
       const int grow = mt * PM + (int)rank * BM + row;
@@ -284,7 +339,9 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           const float m_new = fmaxf(m_used, mx * scale_log2);
           const bool need = m_new > m_used + RESCALE_THRESHOLD;
           if (__any_sync(0xffffffffu, need)) {
-            const float alpha = ptx::ex2(m_used - m_new);
+            // a row with no key yet on both sides (m_used = m_new = -inf) keeps l = 0:
+            // ex2(-inf - -inf) would be NaN
+            const float alpha = m_new == -INFINITY ? 1.f : ptx::ex2(m_used - m_new);
             if (t >= 2) {
               ptx::mbar_wait(&bar->pv_done[wg], ((j - 2) >> 1) & 1);
               ptx::tc_fence_after();
@@ -311,10 +368,9 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         if (lane == 0) ptx::mbar_arrive_cluster(p_ready_l);
       }
       jg += n;
-      t0 += n;
 
       // ---------------------------------------------------------- segment epilogue
-      const bool whole = ib >= t_begin && sc.item_end(item) <= t_end;
+      const bool whole = sg.whole;
       const int g = sc.group_of(item);
       const bool live = grow < q_rows;
       const long long orow = (long long)g * q_rows + grow;

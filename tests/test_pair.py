@@ -107,6 +107,8 @@ def test_pair_refresh_deterministic_and_large_scores(lib):
     (4, 384, 32, 1000),   # committed prefix + prompt
     (1, 300, 16, 0),      # ragged last pair tile
     (3, 200, 64, 17),     # pair tiles straddle heads
+    (3, 600, 64, 17),     # straddling tiles + multi-tile segments in both kernels: a warp whose
+                          # first tile has rows with and without keys (the -inf - -inf rescale)
 ])
 def test_pair_block_causal_vs_oracle(lib, G, n_q, blk, n_prefix):
     from paper_2602_05305_b200 import kernels as K
@@ -121,6 +123,7 @@ def test_pair_block_causal_vs_oracle(lib, G, n_q, blk, n_prefix):
     qc, kc, vc = q.cuda(), k.cuda(), v.cuda()
     (op, lp), (o1, l1) = _run_both(lib, lambda: K.block_causal_attention(qc, kc, vc, n_q, n_prefix, blk))
     assert torch.isfinite(op).all() and torch.isfinite(lp).all()
+    assert torch.isfinite(o1).all() and torch.isfinite(l1).all()
     assert ((op - o1).abs().amax() / o1.abs().amax()).item() <= 5e-3
     assert (lp - l1).abs().max().item() <= 1e-4
     op = op.cpu().numpy()
