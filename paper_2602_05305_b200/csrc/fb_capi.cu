@@ -267,13 +267,19 @@ static int sparse_partitioned_t(const void* qv, const void* kv, const void* vv, 
                                  reinterpret_cast<float*>(l_sel), gws, ws_bytes - list_bytes, st);
         if (rc) return rc;
         GatherSpec gres{res_list, n_res, n_ext, 0, nullptr, nullptr};
+        // the residual pass's merge kernel also merges the selected partial and
+        // writes the step's output (K3 fused), unless no output is wanted
+        const MergeFinal fin{reinterpret_cast<const float*>(o_sel), reinterpret_cast<const float*>(l_sel),
+                             out, out_bf16 ? 1 : 0, empty};
+        const bool fuse = out != nullptr && n_res > 0;
         rc = launch_gather_sm100(reinterpret_cast<const __nv_bfloat16*>(qv),
                                  reinterpret_cast<const __nv_bfloat16*>(kv),
                                  reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, cap,
                                  gres, scale, reinterpret_cast<float*>(o_res),
-                                 reinterpret_cast<float*>(l_res), gws, ws_bytes - list_bytes, st);
+                                 reinterpret_cast<float*>(l_res), gws, ws_bytes - list_bytes, st,
+                                 fuse ? &fin : nullptr);
         if (rc) return rc;
-        if (out == nullptr) return FB_OK;
+        if (out == nullptr || fuse) return FB_OK;
         const void* op[2] = {o_sel, o_res};
         const void* lp[2] = {l_sel, l_res};
         return combine_t<Mode>(2, op, lp, groups * q_rows, d, out, out_bf16, nullptr, empty, st);
@@ -329,12 +335,18 @@ static int sparse_attend_t(const void* qv, const void* kv, const void* vv, const
       float* l_tmp = o_tmp + (size_t)rows * d;
       GatherSpec gsel{sel, n_sel, n_ext, n_in, reinterpret_cast<const __nv_bfloat16*>(kin),
                       reinterpret_cast<const __nv_bfloat16*>(vin)};
+      // selected-blocks partial, merged with the cached residual and written as
+      // the output inside K1's merge kernel (no separate K3 launch)
+      const MergeFinal fin{reinterpret_cast<const float*>(o_res), reinterpret_cast<const float*>(l_res),
+                           out, out_bf16 ? 1 : 0, empty};
       int rc = launch_gather_sm100(reinterpret_cast<const __nv_bfloat16*>(qv),
                                    reinterpret_cast<const __nv_bfloat16*>(kv),
                                    reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d,
                                    cap, gsel, scale, o_tmp, l_tmp,
-                                   reinterpret_cast<char*>(ws) + tmp_bytes, ws_bytes - tmp_bytes, st);
+                                   reinterpret_cast<char*>(ws) + tmp_bytes, ws_bytes - tmp_bytes, st,
+                                   n_sel + n_in > 0 ? &fin : nullptr);
       if (rc) return rc;
+      if (n_sel + n_in > 0) return FB_OK;
       const void* op[2] = {o_tmp, o_res};
       const void* lp[2] = {l_tmp, l_res};
       return combine_t<Mode>(o_res ? 2 : 1, op, lp, rows, d, out, out_bf16, nullptr, empty, st);

@@ -105,10 +105,21 @@ struct GatherSpec {
 };
 size_t gather_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim,
                                     int64_t n_list, int64_t n_in);
+// Optional final step fused into K1's split-merge kernel: merge every row's
+// partial with a second fp32 partial (o2, l2; e.g. the cached residual) and
+// write the attention output (bf16 or fp32) instead of a partial, counting
+// rows empty on both sides -- K3 folded into the same launch.
+struct MergeFinal {
+  const float* o2;
+  const float* l2;
+  void* out;
+  int out_bf16;
+  int32_t* empty_rows;
+};
 int launch_gather_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                         int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                         const GatherSpec& gs, double scale, float* o_out, float* lse_out, void* ws,
-                        size_t ws_bytes, cudaStream_t st);
+                        size_t ws_bytes, cudaStream_t st, const MergeFinal* fin = nullptr);
 
 // K5 on the tensor cores (bf16, q_rows <= 128, kbs == 16): float64 block masses.
 bool score_sm100_supported(int64_t head_dim, int64_t q_rows, int64_t kbs);

@@ -687,6 +687,82 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 }
 
+// Fused final merge (MergeFinal): the row's K1 partial -- merged from the
+// split workspace and stored to (o_k1, l_k1) like the plain merge, or the
+// whole-item partial K1 already wrote there -- is merged with (o2, l2) and
+// written as the attention output in the same pass.  Two-way log-space merge
+// as K3 (attention.py:207-233), products rounded before the sum; a row empty
+// on both sides gives 0 and is counted (merge_partials' DegenerateInputError).
+__device__ __forceinline__ void final_merge_row(const Sched& sc, int item, int row, long long orow,
+                                                int D, int bm, const float* __restrict__ ws_o,
+                                                const float* __restrict__ ws_l, float* __restrict__ o_k1,
+                                                float* __restrict__ l_k1, const MergeFinal& fin, int lane) {
+  const long long ib = sc.item_begin(item), ie = sc.item_end(item);
+  const int c_first = ib < ie ? sc.cta_of(ib) : 0;
+  const int c_last = ib < ie ? sc.cta_of(ie - 1) : 0;
+  const bool split = ib < ie && c_last > c_first;
+  const int c = lane * 4;  // this lane's 4 columns (D <= 128)
+  const bool col = c < D;
+  float lp;
+  float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ib == ie) {  // no keys: the empty partial
+    lp = -INFINITY;
+    if (col) *reinterpret_cast<float4*>(o_k1 + orow * D + c) = pv;
+    if (lane == 0) l_k1[orow] = lp;
+  } else if (!split) {
+    lp = l_k1[orow];
+    if (col) pv = *reinterpret_cast<const float4*>(o_k1 + orow * D + c);
+  } else {
+    const int nseg = c_last - c_first + 1;
+    auto has = [&](int cc) { return sc.start(cc + 1) > sc.start(cc); };
+    float mx = -INFINITY;
+    for (int k = lane; k < nseg; k += 32)
+      if (has(c_first + k)) mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * bm + row]);
+    mx = warp_max(mx);
+    float z = 0.f;
+    for (int k = lane; k < nseg; k += 32)
+      if (has(c_first + k)) z += __expf(ws_l[sc.slot(c_first + k, item) * bm + row] - mx);
+    z = warp_sum(z);
+    const float iz = 1.f / z;
+    if (col) {
+      for (int k = 0; k < nseg; ++k) {
+        if (!has(c_first + k)) continue;
+        const long long sl = sc.slot(c_first + k, item) * bm + row;
+        const float w = __expf(ws_l[sl] - mx);
+        const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
+        pv.x += w * v.x; pv.y += w * v.y; pv.z += w * v.z; pv.w += w * v.w;
+      }
+      pv = make_float4(pv.x * iz, pv.y * iz, pv.z * iz, pv.w * iz);
+      *reinterpret_cast<float4*>(o_k1 + orow * D + c) = pv;
+    }
+    lp = mx + logf(z);
+    if (lane == 0) l_k1[orow] = lp;
+  }
+  const float l2 = fin.l2 ? fin.l2[orow] : -INFINITY;
+  const float m = fmaxf(lp, l2);
+  const bool live = m != -INFINITY;
+  const float wp = (live && lp != -INFINITY) ? __expf(lp - m) : 0.f;
+  const float w2 = (live && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
+  const float iz = live ? 1.f / (wp + w2) : 0.f;
+  if (col) {
+    float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (w2 != 0.f) o2 = *reinterpret_cast<const float4*>(fin.o2 + orow * D + c);
+    const float4 o = make_float4((__fmul_rn(wp, pv.x) + __fmul_rn(w2, o2.x)) * iz,
+                                 (__fmul_rn(wp, pv.y) + __fmul_rn(w2, o2.y)) * iz,
+                                 (__fmul_rn(wp, pv.z) + __fmul_rn(w2, o2.z)) * iz,
+                                 (__fmul_rn(wp, pv.w) + __fmul_rn(w2, o2.w)) * iz);
+    if (fin.out_bf16) {
+      uint2 u;
+      u.x = ptx::pack_bf16(o.x, o.y);
+      u.y = ptx::pack_bf16(o.z, o.w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + c) = u;
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(fin.out) + orow * D + c) = o;
+    }
+  }
+  if (!live && lane == 0 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
+}
+
 // Split merge for items covered by several CTAs: one warp per query row,
 // lanes over columns (coalesced 512 B per partial row); the partials are
 // merged in segment order, so the result does not depend on CTA timing.
@@ -694,7 +770,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 __global__ void __launch_bounds__(256)
 refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o,
                      const float* __restrict__ ws_l, float* __restrict__ o_out,
-                     float* __restrict__ lse_out, int bm) {
+                     float* __restrict__ lse_out, int bm, MergeFinal fin) {
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
   sc.resolve();
@@ -708,6 +784,10 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   if (grow >= q_rows) return;
   const long long orow = (long long)g * q_rows + grow;
   const long long ib = sc.item_begin(item), ie = sc.item_end(item);
+  if (fin.out != nullptr) {  // fused final merge: this row's partial(s) + (o2, l2) -> out
+    final_merge_row(sc, item, row, orow, D, bm, ws_o, ws_l, o_out, lse_out, fin, lane);
+    return;
+  }
   if (ib == ie) {  // no keys (ragged length 0): the empty partial
     for (int c = lane; c < D; c += 32) o_out[orow * D + c] = 0.f;
     if (lane == 0) lse_out[orow] = -INFINITY;
@@ -1322,7 +1402,7 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   if (!need_merge) return FB_OK;
   const long long warps = (long long)items * PM;
   launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
-             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM);
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM, MergeFinal{});
   count_launch();
   return check_launch("refresh_merge_kernel(sm100, pair)");
 }
@@ -1334,7 +1414,8 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             size_t ws_bytes, cudaStream_t st, const GatherSpec* gs = nullptr,
                             const int* key_len = nullptr, const sm100::Causal* causal = nullptr,
                             const int32_t* glist = nullptr, int64_t n_list = 0,
-                            unsigned long long* sync_flags = nullptr, int64_t n_flags = 0) {
+                            unsigned long long* sync_flags = nullptr, int64_t n_flags = 0,
+                            const MergeFinal* fin = nullptr) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
@@ -1453,6 +1534,10 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
       need_merge = false;
     else
       flags = nullptr;
+    if (fin != nullptr) {  // the merge kernel finishes every row (fused K3)
+      need_merge = true;
+      flags = nullptr;
+    }
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
@@ -1463,7 +1548,8 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   if (!need_merge) return FB_OK;
   const long long warps = (long long)p.items * sm100::BM;
   launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
-             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, (int)sm100::BM);
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, (int)sm100::BM,
+             fin ? *fin : MergeFinal{});
   count_launch();
   return check_launch("refresh_merge_kernel(sm100)");
 }
@@ -1544,15 +1630,19 @@ size_t gather_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head
 int launch_gather_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                         int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                         const GatherSpec& gs, double scale, float* o_out, float* lse_out, void* ws,
-                        size_t ws_bytes, cudaStream_t st) {
+                        size_t ws_bytes, cudaStream_t st, const MergeFinal* fin) {
   const int64_t tiles = (gs.n_list + 7) / 8 + (gs.n_in + sm100::BN - 1) / sm100::BN;
-  if (tiles == 0) return launch_fill_sentinel<float, float>(o_out, lse_out, groups * q_rows, head_dim, st);
+  if (tiles == 0 && fin == nullptr)
+    return launch_fill_sentinel<float, float>(o_out, lse_out, groups * q_rows, head_dim, st);
+  if (tiles == 0) return FB_ERR_UNSUPPORTED;  // caller combines the sentinel itself
   if (head_dim == 128)
     return launch_refresh_d<128, true>(q, k, v, groups, q_rows, kv_rows_cap, 0, 0, scale, o_out,
-                                       lse_out, ws, ws_bytes, st, &gs);
+                                       lse_out, ws, ws_bytes, st, &gs, nullptr, nullptr, nullptr, 0,
+                                       nullptr, 0, fin);
   if (head_dim == 64)
     return launch_refresh_d<64, true>(q, k, v, groups, q_rows, kv_rows_cap, 0, 0, scale, o_out,
-                                      lse_out, ws, ws_bytes, st, &gs);
+                                      lse_out, ws, ws_bytes, st, &gs, nullptr, nullptr, nullptr, 0,
+                                      nullptr, 0, fin);
   return FB_ERR_UNSUPPORTED;
 }
 
