@@ -82,6 +82,7 @@ struct Sched {
   const int* glist;        // group subset (head-gated refresh): item group -> slab, or nullptr
   int kv_keep;             // K/V tiles re-read by other query tiles of the group: keep in L2
   int rr;                  // pair kernel: round-robin whole items (block-causal), no stream-K
+  int vprod;               // refresh kernel: warp 3 issues the V tiles (warp 0 Q and K)
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -246,9 +247,13 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   // registers: control warpgroup 56/thread, softmax warpgroups 224 (64,512 of 65,536)
   if (warp < 4) {
   ptx::setmaxnreg_dec<56>();
-  if (warp == 0) {
+  if (warp == 0 || (warp == 3 && sc.vprod)) {
     // ------------------------------------------------------------ TMA producer
+    // warp 0 issues Q and K; V comes from warp 3 when sc.vprod (two issuing
+    // threads: a V slot wait never delays the next K tile's issue, and the
+    // gathered path's 16 small boxes per K / V tile go out in parallel)
     if (lane == 0) {
+      const bool do_k = warp == 0, do_v = warp == 3 || !sc.vprod;
       const uint64_t keep = ptx::policy_evict_last();
       // K/V: streamed once (evict first), except block-causal prefill where
       // every later query tile of the group re-reads them (keep in L2)
@@ -259,27 +264,33 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const long long ib = sc.item_begin(item);
         const long long seg_end = min(t_end, sc.item_end(item));
         const int g = sc.group_of(item), mt = sc.mtile_of(item);
-        if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
-        ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
-        for (int b = 0; b < C::NBOX; ++b)
-          ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
-                           mt * BM, g, keep);
+        if (do_k) {
+          if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
+          ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
+          for (int b = 0; b < C::NBOX; ++b)
+            ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
+                             mt * BM, g, keep);
+        }
         for (; t < seg_end; ++t, ++j) {
           const int s = j % C::STAGES;
           const uint32_t ph = (j / C::STAGES) & 1;
           const int lt = (int)(t - ib);
           if constexpr (!GATHER) {
             const int row = key_begin + lt * BN;
-            ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
-            ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-            for (int b = 0; b < C::NBOX; ++b)
-              ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
-                               &bar->k_full[s], b * BOX_COLS, row, g, stream);
-            ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
-            ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-            for (int b = 0; b < C::NBOX; ++b)
-              ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
-                               &bar->v_full[s], b * BOX_COLS, row, g, stream);
+            if (do_k) {
+              ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+              ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+              for (int b = 0; b < C::NBOX; ++b)
+                ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
+                                 &bar->k_full[s], b * BOX_COLS, row, g, stream);
+            }
+            if (do_v) {
+              ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+              ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+              for (int b = 0; b < C::NBOX; ++b)
+                ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
+                                 &bar->v_full[s], b * BOX_COLS, row, g, stream);
+            }
           } else if (lt < ga.sel_tiles) {
             int rows[8];
 #pragma unroll
@@ -287,32 +298,40 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               const int e = lt * 8 + i;
               rows[i] = e < ga.n_list ? __ldg(ga.list + (long long)g * ga.n_list + e) * 16 : ga.n_ext;
             }
-            ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
-            ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-            for (int b = 0; b < C::NBOX; ++b)
+            if (do_k) {
+              ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+              ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+              for (int b = 0; b < C::NBOX; ++b)
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
-                                 &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], g, stream);
-            ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
-            ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-            for (int b = 0; b < C::NBOX; ++b)
+                for (int i = 0; i < 8; ++i)
+                  ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
+                                   &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], g, stream);
+            }
+            if (do_v) {
+              ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+              ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+              for (int b = 0; b < C::NBOX; ++b)
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
-                                 &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], g, stream);
+                for (int i = 0; i < 8; ++i)
+                  ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
+                                   &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], g, stream);
+            }
           } else {
             const int row = (lt - ga.sel_tiles) * BN;
-            ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
-            ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-            for (int b = 0; b < C::NBOX; ++b)
-              ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_ki,
-                               &bar->k_full[s], b * BOX_COLS, row, g, stream);
-            ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
-            ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-            for (int b = 0; b < C::NBOX; ++b)
-              ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_vi,
-                               &bar->v_full[s], b * BOX_COLS, row, g, stream);
+            if (do_k) {
+              ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
+              ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+              for (int b = 0; b < C::NBOX; ++b)
+                ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_ki,
+                                 &bar->k_full[s], b * BOX_COLS, row, g, stream);
+            }
+            if (do_v) {
+              ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
+              ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
+              for (int b = 0; b < C::NBOX; ++b)
+                ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_vi,
+                                 &bar->v_full[s], b * BOX_COLS, row, g, stream);
+            }
           }
         }
       }
@@ -1487,6 +1506,18 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   RefreshPlan p = plan_refresh(glist ? n_list : groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr, glist};
   sc.kv_keep = p.m_tiles > 1 && kv_keep_enabled();
+  {
+    // V from a second producer thread: measured on the gathered path (C4
+    // cached sparse step, 16 small boxes per K / V tile) 11 % faster at 50 %
+    // density, 4 % at 10 %; ~1 % slower on the dense streams (C2 / C3 / C5),
+    // so dense keeps one producer.  FB_K1_VPROD=0 / 1 forces it (diagnostics).
+    static int vp = -2;
+    if (vp == -2) {
+      const char* e = getenv("FB_K1_VPROD");
+      vp = e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
+    }
+    sc.vprod = vp >= 0 ? vp : (GATHER ? 1 : 0);
+  }
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   unsigned long long* flags = nullptr;  // in-kernel split merge (uniform items only)
