@@ -1404,6 +1404,21 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
     const char* e = getenv("FB_PAIR_POLY");  // diagnostics: MUFU offload share
     poly = e ? atoi(e) : 0;
   }
+  if (poly < 0) {  // diagnostics: the pipeline without softmax math
+    auto kd = sm100::pair::pair_kernel<D, -1>;
+    cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    const float sl = (float)(scale * 1.4426950408889634);
+    launch_pdl(kd, dim3((unsigned)(2 * sc.ctas)), dim3(sm100::THREADS), P::SMEM, st, mq, mk, mv, cz, sc,
+               (int)q_rows, (int)key_begin, (int)key_end, sl, o_out, lse_out, ws_o, ws_l);
+    count_launch();
+    if ((rc = check_launch("pair_kernel(diag)"))) return rc;
+    if (!need_merge) return FB_OK;
+    const long long warps = (long long)items * PM;
+    launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
+               (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM, MergeFinal{});
+    count_launch();
+    return check_launch("refresh_merge_kernel(sm100, pair diag)");
+  }
   auto kern = poly == 4 ? sm100::pair::pair_kernel<D, 4>
               : poly == 3 ? sm100::pair::pair_kernel<D, 3>
               : poly == 2 ? sm100::pair::pair_kernel<D, 2> : sm100::pair::pair_kernel<D, 0>;

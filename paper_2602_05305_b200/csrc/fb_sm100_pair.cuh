@@ -283,6 +283,14 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         const int j = jg + t;
         ptx::mbar_wait(&bar->s_full[wg], (j >> 1) & 1);
         ptx::tc_fence_after();
+        if constexpr (POLY == -1) {  // diagnostics (FB_PAIR_POLY=-1): no softmax, P = stale S
+          m_used = 0.f;
+          l += 1.f;
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(p_ready_l);
+          continue;
+        }
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c)
           ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, reinterpret_cast<uint32_t*>(s) + c * 32);
