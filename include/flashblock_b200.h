@@ -180,6 +180,31 @@ FB_API int fb_commit_block(int dtype, void* k_cache, void* v_cache, int64_t grou
                            const void* v_block, int64_t block_rows, int32_t* lengths,
                            int32_t* overflow, void* stream);
 
+/* Paged KV cache (the serving layout): K and V of every
+ * group live in a shared page pool [num_pages, page_rows, head_dim]; group
+ * g's logical row r is row r % page_rows of page page_table[g * max_pages +
+ * r / page_rows] (device int32).  K1 over rows [0, key_len[g]) of each group
+ * (device int32 [groups]) -- same outputs as fb_attention_partial_ragged on
+ * the equivalent contiguous slabs.  Page-table entries covering rows below
+ * key_len[g] must be valid pages.  BF16 with head_dim 64 / 128 and page_rows a
+ * multiple of 128 (one TMA box per 128-key tile); FB_ERR_UNSUPPORTED
+ * otherwise. */
+FB_API int fb_attention_partial_paged(int dtype, const void* q, const void* k_pages,
+                                      const void* v_pages, int64_t num_pages, int64_t page_rows,
+                                      const int32_t* page_table, int64_t max_pages, int64_t groups,
+                                      int64_t q_rows, int64_t head_dim, const int32_t* key_len,
+                                      double scale, void* o_out, void* lse_out, void* workspace,
+                                      size_t workspace_bytes, void* stream);
+FB_API size_t fb_paged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim);
+/* Paged block commit: rows lengths[g] .. lengths[g] + block_rows - 1 of group
+ * g go to their pages (rows past the table or onto a negative page id are
+ * dropped and counted in *overflow); lengths advance by block_rows. */
+FB_API int fb_commit_block_paged(int dtype, void* k_pages, void* v_pages, int64_t page_rows,
+                                 const int32_t* page_table, int64_t max_pages, int64_t groups,
+                                 int64_t head_dim, const void* k_block, const void* v_block,
+                                 int64_t block_rows, int32_t* lengths, int32_t* overflow,
+                                 void* stream);
+
 /* K2 -- cached step: block-internal partial fused with the log-space merge
  * against the cached external partial.
  * Replaces attention_with_reuse (attention.py:295-321) = attention_partial on

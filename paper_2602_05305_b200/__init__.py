@@ -11,7 +11,7 @@ from .attention import (AttnPartial, CacheEntry, DegenerateInputError, ExternalA
                         attention_streamed, attention_with_reuse, combine_partials,
                         merge_partials)
 from .analysis import HeadGateCalibrator, pairwise_step_similarity
-from .engine import FlashBlockAttention, KVCache
+from .engine import FlashBlockAttention, KVCache, PagedKVCache
 from .errors import BoundsError, ShapeError, StalenessError
 from .policy import (MODES, CalibrationError, Decision, HeadGate, HeadGateTable, ReuseConfig,
                      count_updated_tokens, decide, refresh_schedule, unmask_schedule)
@@ -22,7 +22,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AttnPartial", "CacheEntry", "DegenerateInputError", "ExternalAttnCache",
     "ReusePreconditionError", "attention_dense", "attention_partial", "attention_streamed",
-    "attention_with_reuse", "combine_partials", "merge_partials", "FlashBlockAttention", "KVCache",
+    "attention_with_reuse", "combine_partials", "merge_partials", "FlashBlockAttention", "KVCache", "PagedKVCache",
     "BoundsError", "ShapeError", "StalenessError", "MODES", "Decision", "ReuseConfig",
     "count_updated_tokens", "decide", "refresh_schedule", "unmask_schedule", "SparseMask",
     "build_sparse_mask", "sparse_attention_with_residual", "CalibrationError", "HeadGate",

@@ -576,6 +576,51 @@ int fb_commit_block(int dtype, void* k_cache, void* v_cache, int64_t groups, int
                              as_stream(stream));
 }
 
+size_t fb_paged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim) {
+  if (dtype != FB_BF16 || !sm100_supported(head_dim) || groups <= 0 || q_rows <= 0) return 0;
+  return refresh_sm100_ragged_workspace_bytes(groups, q_rows, head_dim);
+}
+
+int fb_attention_partial_paged(int dtype, const void* q, const void* k_pages, const void* v_pages,
+                               int64_t num_pages, int64_t page_rows, const int32_t* page_table,
+                               int64_t max_pages, int64_t groups, int64_t q_rows, int64_t head_dim,
+                               const int32_t* key_len, double scale, void* o_out, void* lse_out,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || num_pages < 0 || max_pages < 0)
+    return fail(FB_ERR_SHAPE, "bad extents");
+  if (page_table == nullptr || key_len == nullptr)
+    return fail(FB_ERR_VALUE, "page_table and key_len (device int32) are required");
+  if (dtype != FB_BF16 || !sm100_supported(head_dim))
+    return fail(FB_ERR_UNSUPPORTED, "paged KV: bf16 with head_dim 64 or 128");
+  if (page_rows <= 0 || page_rows % 128 != 0)
+    return fail(FB_ERR_UNSUPPORTED, "page_rows must be a positive multiple of 128");
+  if (max_pages * page_rows >= (int64_t(1) << 31)) return fail(FB_ERR_SHAPE, "logical capacity >= 2^31 rows");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  if (workspace == nullptr || workspace_bytes < fb_paged_workspace_bytes(dtype, groups, q_rows, head_dim))
+    return fail(FB_ERR_VALUE, "workspace too small (fb_paged_workspace_bytes)");
+  return launch_refresh_paged_sm100(
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k_pages),
+      reinterpret_cast<const __nv_bfloat16*>(v_pages), num_pages, page_rows, page_table, max_pages,
+      groups, q_rows, head_dim, key_len, scale, reinterpret_cast<float*>(o_out),
+      reinterpret_cast<float*>(lse_out), workspace, workspace_bytes, as_stream(stream));
+}
+
+int fb_commit_block_paged(int dtype, void* k_pages, void* v_pages, int64_t page_rows,
+                          const int32_t* page_table, int64_t max_pages, int64_t groups,
+                          int64_t head_dim, const void* k_block, const void* v_block,
+                          int64_t block_rows, int32_t* lengths, int32_t* overflow, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || head_dim < 1 || block_rows < 0 || page_rows < 1 || max_pages < 0)
+    return fail(FB_ERR_SHAPE, "bad extents");
+  if (block_rows == 0) return fail(FB_ERR_SHAPE, "a block commit needs at least one row");
+  if (lengths == nullptr || page_table == nullptr)
+    return fail(FB_ERR_VALUE, "lengths and page_table (device int32) are required");
+  return launch_commit_block_paged(k_pages, v_pages, page_rows, page_table, max_pages, k_block, v_block,
+                                   groups, head_dim * (int64_t)dtype_size(dtype), block_rows, lengths,
+                                   overflow, as_stream(stream));
+}
+
 int fb_attention_partial_groups(int dtype, const void* q, const void* k, const void* v,
                                 int64_t groups, int64_t q_rows, int64_t head_dim,
                                 int64_t kv_rows_cap, int64_t key_begin, int64_t key_end,

@@ -167,6 +167,15 @@ struct Gather {
   int n_list, n_ext, n_in, sel_tiles;
 };
 
+// Paged KV cache (serving layout): a group's logical key row
+// r lives in page table[g * max_pages + r / page_rows] at row r % page_rows of
+// a shared page pool [num_pages, page_rows, d]; page_rows is a multiple of 128,
+// so every 128-key tile sits inside one page (one TMA box per 64 columns).
+struct Paged {
+  const int32_t* table;  // [groups, max_pages] page ids, or nullptr (contiguous slabs)
+  int max_pages, page_rows;
+};
+
 // DIAG (diagnostics only, fb_debug_set_k1_diag): 1 = softmax warps load S but skip
 // the softmax math, 2 = they skip the TMEM load too (pure TMA + MMA pipeline).
 // Block-causal rows (prefill / commit attention, simulator.py:297-354): query
@@ -189,7 +198,7 @@ template <int D, bool GATHER, int DIAG = 0, int POLY = K1_POLY>
 __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ki,
-               const __grid_constant__ CUtensorMap tm_vi, Gather ga, Causal cz, Sched sc, int q_rows, int key_begin,
+               const __grid_constant__ CUtensorMap tm_vi, Gather ga, Paged pg, Causal cz, Sched sc, int q_rows, int key_begin,
                int key_end, const int* __restrict__ key_len, float scale_log2, float* __restrict__ o_out,
                float* __restrict__ lse_out, float* __restrict__ ws_o,
                float* __restrict__ ws_l, unsigned long long* __restrict__ trace,
@@ -276,20 +285,25 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           const uint32_t ph = (j / C::STAGES) & 1;
           const int lt = (int)(t - ib);
           if constexpr (!GATHER) {
-            const int row = key_begin + lt * BN;
+            int row = key_begin + lt * BN;
+            int slab = g;
+            if (pg.table != nullptr) {  // paged: the tile's page, row inside it
+              slab = __ldg(pg.table + (long long)g * pg.max_pages + row / pg.page_rows);
+              row %= pg.page_rows;
+            }
             if (do_k) {
               ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
               for (int b = 0; b < C::NBOX; ++b)
                 ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_k,
-                                 &bar->k_full[s], b * BOX_COLS, row, g, stream);
+                                 &bar->k_full[s], b * BOX_COLS, row, slab, stream);
             }
             if (do_v) {
               ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
               for (int b = 0; b < C::NBOX; ++b)
                 ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_v,
-                                 &bar->v_full[s], b * BOX_COLS, row, g, stream);
+                                 &bar->v_full[s], b * BOX_COLS, row, slab, stream);
             }
           } else if (lt < ga.sel_tiles) {
             int rows[8];
@@ -1449,7 +1463,8 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             const int* key_len = nullptr, const sm100::Causal* causal = nullptr,
                             const int32_t* glist = nullptr, int64_t n_list = 0,
                             unsigned long long* sync_flags = nullptr, int64_t n_flags = 0,
-                            const MergeFinal* fin = nullptr) {
+                            const MergeFinal* fin = nullptr, const sm100::Paged* paged = nullptr,
+                            int64_t num_pages = 0) {
   using C = sm100::Cfg<D>;
   CUtensorMap mq, mk, mv, mki, mvi;
   int rc;
@@ -1460,8 +1475,14 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     // ragged: the whole slab is addressable; rows past each length are masked
     // (scores) and zeroed in smem (V) in the kernel
     const int64_t dim1 = (key_len && !causal) ? kv_rows_cap : key_end;
-    if ((rc = make_tmap_3d(&mk, k, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
-    if ((rc = make_tmap_3d(&mv, v, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    if (paged != nullptr) {  // page pool [num_pages, page_rows, D]
+      const int64_t pr = paged->page_rows;
+      if ((rc = make_tmap_3d(&mk, k, 2, D, pr, pr, num_pages, sm100::BOX_COLS, sm100::BN))) return rc;
+      if ((rc = make_tmap_3d(&mv, v, 2, D, pr, pr, num_pages, sm100::BOX_COLS, sm100::BN))) return rc;
+    } else {
+      if ((rc = make_tmap_3d(&mk, k, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+      if ((rc = make_tmap_3d(&mv, v, 2, D, dim1, kv_rows_cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+    }
     mki = mk;
     mvi = mv;
     tiles = (key_end - key_begin + sm100::BN - 1) / sm100::BN;
@@ -1586,8 +1607,9 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     }
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
+  const sm100::Paged pgv = paged ? *paged : sm100::Paged{nullptr, 0, 1};
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
-             cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
+             pgv, cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
              ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr, flags);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
@@ -1627,6 +1649,28 @@ int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, kv_rows_cap,
                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, key_end);
+  return FB_ERR_UNSUPPORTED;
+}
+
+// Paged KV cache: K1 over per-sequence lengths whose keys
+// live in a shared page pool addressed through per-group page tables.
+int launch_refresh_paged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_pages,
+                               const __nv_bfloat16* v_pages, int64_t num_pages, int64_t page_rows,
+                               const int32_t* page_table, int64_t max_pages, int64_t groups,
+                               int64_t q_rows, int64_t head_dim, const int32_t* key_len, double scale,
+                               float* o_out, float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (page_rows <= 0 || page_rows % sm100::BN != 0)
+    return fail(FB_ERR_UNSUPPORTED, "page_rows must be a positive multiple of 128");
+  const sm100::Paged pg{page_table, (int)max_pages, (int)page_rows};
+  const int64_t cap = max_pages * page_rows;
+  if (head_dim == 128)
+    return launch_refresh_d<128, false>(q, k_pages, v_pages, groups, q_rows, cap, 0, cap, scale, o_out,
+                                        lse_out, ws, ws_bytes, st, nullptr, key_len, nullptr, nullptr, 0,
+                                        nullptr, 0, nullptr, &pg, num_pages);
+  if (head_dim == 64)
+    return launch_refresh_d<64, false>(q, k_pages, v_pages, groups, q_rows, cap, 0, cap, scale, o_out,
+                                       lse_out, ws, ws_bytes, st, nullptr, key_len, nullptr, nullptr, 0,
+                                       nullptr, 0, nullptr, &pg, num_pages);
   return FB_ERR_UNSUPPORTED;
 }
 

@@ -339,6 +339,55 @@ int launch_commit_block(void* kc, void* vc, const void* kb, const void* vb, int6
   return check_launch("commit_block_kernel");
 }
 
+// Paged variant: logical row len[g] + r of group g goes to page
+// table[g * max_pages + row / page_rows], row % page_rows of the page pool.
+// Rows past the table (or into a negative page id) are dropped and counted.
+__global__ void commit_block_paged_kernel(unsigned char* __restrict__ kp, unsigned char* __restrict__ vp,
+                                          int64_t page_rows, const int32_t* __restrict__ table,
+                                          int64_t max_pages, const unsigned char* __restrict__ kb,
+                                          const unsigned char* __restrict__ vb, int64_t row_bytes,
+                                          int64_t blk_rows, int32_t* __restrict__ len,
+                                          int32_t* __restrict__ overflow) {
+  const int64_t g = blockIdx.y;
+  const int64_t r = blockIdx.x;
+  const int64_t dst_row = (int64_t)len[g] + r;
+  const int64_t pi = dst_row / page_rows;
+  const int32_t page = pi < max_pages ? table[g * max_pages + pi] : -1;
+  if (page >= 0) {
+    const int64_t dst = ((int64_t)page * page_rows + dst_row % page_rows) * row_bytes;
+    const int64_t src = (g * blk_rows + r) * row_bytes;
+    if ((row_bytes & 15) == 0) {
+      for (int64_t i = threadIdx.x * 16; i < row_bytes; i += blockDim.x * 16) {
+        *reinterpret_cast<uint4*>(kp + dst + i) = *reinterpret_cast<const uint4*>(kb + src + i);
+        *reinterpret_cast<uint4*>(vp + dst + i) = *reinterpret_cast<const uint4*>(vb + src + i);
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < row_bytes; i += blockDim.x) {
+        kp[dst + i] = kb[src + i];
+        vp[dst + i] = vb[src + i];
+      }
+    }
+  } else if (threadIdx.x == 0 && overflow) {
+    atomicAdd(overflow, 1);
+  }
+}
+
+int launch_commit_block_paged(void* kp, void* vp, int64_t page_rows, const int32_t* table,
+                              int64_t max_pages, const void* kb, const void* vb, int64_t groups,
+                              int64_t row_bytes, int64_t blk_rows, int32_t* len, int32_t* overflow,
+                              cudaStream_t st) {
+  if (groups == 0 || blk_rows == 0) return FB_OK;
+  dim3 grid((unsigned)blk_rows, (unsigned)groups);
+  commit_block_paged_kernel<<<grid, 64, 0, st>>>(
+      reinterpret_cast<unsigned char*>(kp), reinterpret_cast<unsigned char*>(vp), page_rows, table,
+      max_pages, reinterpret_cast<const unsigned char*>(kb), reinterpret_cast<const unsigned char*>(vb),
+      row_bytes, blk_rows, len, overflow);
+  advance_lengths_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, st>>>(len, groups, blk_rows,
+                                                                          max_pages * page_rows);
+  count_launch(2);
+  return check_launch("commit_block_paged_kernel");
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <typename Mode>

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import torch
 
 from . import kernels as K
-from .errors import ReusePreconditionError, ShapeError
+from .errors import BoundsError, ReusePreconditionError, ShapeError
 from .policy import Decision, ReuseConfig, decide
 
 
@@ -278,3 +278,82 @@ class KVCache:
 
     def sequence_lengths(self, layer: int = 0) -> torch.Tensor:
         return self.lengths[layer].view(self.b, self.hkv)[:, 0]
+
+
+class PagedKVCache:
+    """Paged device KV cache (the serving layout): per layer
+    one page pool K, V [num_pages, page_rows, d] shared by every (sequence,
+    kv-head) slab, an int32 page table [b*Hkv, max_pages] and int32 committed
+    lengths [b*Hkv] on the device.  Pages are handed out from a host free list
+    when a block is committed and returned when a sequence is released, so
+    sequences of very different lengths share one pool.  Attention reads the
+    pages through the table inside K1 (fb_attention_partial_paged); the results
+    equal the contiguous-slab ragged path on the same rows."""
+
+    def __init__(self, num_layers: int, batch: int, num_kv_heads: int, num_pages: int,
+                 page_rows: int, head_dim: int, max_pages_per_slab: int, device=None,
+                 dtype=torch.bfloat16):
+        if page_rows % 128:
+            raise ShapeError("page_rows must be a multiple of 128")
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.L, self.b, self.hkv, self.P, self.d = num_layers, batch, num_kv_heads, page_rows, head_dim
+        self.groups = batch * num_kv_heads
+        self.max_pages = max_pages_per_slab
+        self.k = [torch.zeros((num_pages, page_rows, head_dim), dtype=dtype, device=dev)
+                  for _ in range(num_layers)]
+        self.v = [torch.zeros_like(t) for t in self.k]
+        self.table = [torch.full((self.groups, max_pages_per_slab), -1, dtype=torch.int32, device=dev)
+                      for _ in range(num_layers)]
+        self.lengths = [torch.zeros(self.groups, dtype=torch.int32, device=dev) for _ in range(num_layers)]
+        self._len = [[0] * self.groups for _ in range(num_layers)]
+        self._pages = [[[] for _ in range(self.groups)] for _ in range(num_layers)]
+        self._free = [list(range(num_pages - 1, -1, -1)) for _ in range(num_layers)]
+
+    def _reserve(self, layer: int, rows: int) -> None:
+        changed = False
+        for g in range(self.groups):
+            need = -(-(self._len[layer][g] + rows) // self.P)
+            while len(self._pages[layer][g]) < need:
+                if len(self._pages[layer][g]) >= self.max_pages:
+                    raise BoundsError("slab would exceed max_pages_per_slab")
+                if not self._free[layer]:
+                    raise BoundsError("page pool exhausted")
+                self._pages[layer][g].append(self._free[layer].pop())
+                changed = True
+        if changed:
+            host = torch.full((self.groups, self.max_pages), -1, dtype=torch.int32)
+            for g, pages in enumerate(self._pages[layer]):
+                host[g, :len(pages)] = torch.tensor(pages, dtype=torch.int32)
+            self.table[layer].copy_(host, non_blocking=False)
+
+    def commit_block(self, layer: int, k_block, v_block) -> None:
+        """Append one finished block's rows [b, Hkv, B, d] for `layer`."""
+        if k_block.shape[:2] != (self.b, self.hkv) or k_block.shape[-1] != self.d:
+            raise ShapeError(f"block {tuple(k_block.shape)} does not match the cache")
+        rows = k_block.shape[-2]
+        self._reserve(layer, rows)
+        K.commit_block_paged(self.k[layer], self.v[layer], self.table[layer],
+                             k_block.reshape(self.groups, rows, self.d),
+                             v_block.reshape(self.groups, rows, self.d), self.lengths[layer])
+        for g in range(self.groups):
+            self._len[layer][g] += rows
+
+    def release(self, seq: int) -> None:
+        """Return sequence `seq`'s pages (all layers) to the pools; its slabs restart empty."""
+        for layer in range(self.L):
+            for g in range(seq * self.hkv, (seq + 1) * self.hkv):
+                self._free[layer].extend(reversed(self._pages[layer][g]))
+                self._pages[layer][g] = []
+                self._len[layer][g] = 0
+            self.table[layer][seq * self.hkv:(seq + 1) * self.hkv] = -1
+            self.lengths[layer][seq * self.hkv:(seq + 1) * self.hkv] = 0
+
+    def attention_partial(self, layer: int, q):
+        """K1 (refresh) for `layer`: q [b, Hq, B, d] -> (O_ext, LSE_ext) over
+        every slab's committed rows, read through the page table."""
+        q3 = K.gqa_view(q, self.hkv)
+        return K.attention_partial_paged(q3, self.k[layer], self.v[layer], self.table[layer],
+                                         self.lengths[layer])
+
+    def free_pages(self, layer: int = 0) -> int:
+        return len(self._free[layer])

@@ -180,6 +180,60 @@ def attention_partial_ragged(q, k, v, key_end: torch.Tensor, key_begin: int = 0,
     return out, lse
 
 
+def attention_partial_paged(q, k_pages, v_pages, page_table: torch.Tensor, key_len: torch.Tensor,
+                            scale: float | None = None, out=None, lse=None):
+    """K1 over a paged KV cache: group g attends its logical
+    rows [0, key_len[g]), row r stored at row r % P of page page_table[g, r // P]
+    of the pools k_pages / v_pages [num_pages, P, d] (P a multiple of 128).
+    bf16 only; same outputs as attention_partial_ragged on contiguous slabs."""
+    q3 = _as3(q, "q").contiguous()
+    require_cuda(q3, k_pages, v_pages, page_table, key_len)
+    if k_pages.dim() != 3 or k_pages.shape != v_pages.shape or k_pages.shape[2] != q3.shape[2]:
+        raise ShapeError("page pools must be [num_pages, page_rows, head_dim] and match q")
+    if q3.dtype != torch.bfloat16 or k_pages.dtype != torch.bfloat16 or v_pages.dtype != torch.bfloat16:
+        raise ShapeError("the paged path is bf16")
+    kp, vp = k_pages.contiguous(), v_pages.contiguous()
+    groups, q_rows, d = q3.shape
+    table = page_table.reshape(groups, -1).to(torch.int32).contiguous()
+    lens = key_len.reshape(-1).to(torch.int32).contiguous()
+    if lens.numel() != groups:
+        raise ShapeError(f"key_len has {lens.numel()} entries for {groups} groups")
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=torch.float32, device=q3.device)
+    if lse is None:
+        lse = torch.empty((groups, q_rows), dtype=torch.float32, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_paged_workspace_bytes(_CODE[torch.bfloat16], groups, q_rows, d)
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_attention_partial_paged", _CODE[torch.bfloat16], _p(q3), _p(kp), _p(vp), kp.shape[0],
+              kp.shape[1], _p(table), table.shape[1], groups, q_rows, d, _p(lens), scale, _p(out),
+              _p(lse), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
+    return out, lse
+
+
+def commit_block_paged(k_pages, v_pages, page_table: torch.Tensor, k_block, v_block,
+                       lengths: torch.Tensor, check: bool = False) -> None:
+    """Append a finished block's K/V ([groups, B, d]) to each group's pages at
+    logical row lengths[g]; lengths advance by B (kv_cache.py:121-144)."""
+    kb, vb = _as3(k_block, "k_block").contiguous(), _as3(v_block, "v_block").contiguous()
+    require_cuda(k_pages, v_pages, page_table, kb, vb, lengths)
+    if not (k_pages.is_contiguous() and v_pages.is_contiguous()) or k_pages.shape != v_pages.shape:
+        raise ShapeError("page pools must be contiguous and alike")
+    groups = kb.shape[0]
+    table = page_table.reshape(groups, -1)
+    if table.dtype != torch.int32 or not table.is_contiguous():
+        raise ShapeError("page_table must be a contiguous int32 tensor [groups, max_pages]")
+    if lengths.dtype != torch.int32 or lengths.numel() != groups:
+        raise ShapeError("lengths must be an int32 tensor [groups]")
+    cnt = _empty_counter(kb.device) if check else None
+    _lib.call("fb_commit_block_paged", dtype_code(kb), _p(k_pages), _p(v_pages), k_pages.shape[1],
+              _p(table), table.shape[1], groups, kb.shape[2], _p(kb), _p(vb), kb.shape[1],
+              _p(lengths), _p(cnt), _stream(kb))
+    if cnt is not None and int(cnt.item()) > 0:
+        from .errors import BoundsError
+        raise BoundsError("block commit runs past the allocated pages")
+
+
 def attention_partial_groups(q, k, v, group_list: torch.Tensor, key_begin: int = 0,
                              key_end: int | None = None, scale: float | None = None, out=None,
                              lse=None):

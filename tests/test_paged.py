@@ -1,0 +1,85 @@
+"""Paged KV cache (serving layout): K1 reading keys through
+per-slab page tables (fb_attention_partial_paged) and the paged block commit
+(fb_commit_block_paged).
+
+Parity: the same rows laid out in contiguous slabs and run through the ragged
+K1 path give the SAME outputs bit for bit (identical tiles in identical order);
+the ragged path itself is checked against the oracle in test_gpu_attention.
+The PagedKVCache built by block commits agrees with the contiguous KVCache."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import flashblock_oracle as orc  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+@pytest.mark.parametrize("page_rows,d", [(128, 128), (256, 128), (512, 64)])
+def test_paged_equals_ragged_contiguous_bitwise(page_rows, d):
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(page_rows + d)
+    groups, q_rows, cap = 6, 128, 2600
+    lens = torch.tensor([2600, 0, 1, 127, 1000, 2049], dtype=torch.int32, device="cuda")
+    q = torch.randn((groups, q_rows, d), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((groups, cap, d), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((groups, cap, d), device="cuda", generator=g).to(torch.bfloat16)
+    max_pages = -(-cap // page_rows)
+    num_pages = groups * max_pages + 3
+    perm = torch.randperm(num_pages, generator=torch.Generator().manual_seed(1)).tolist()
+    kp = torch.full((num_pages, page_rows, d), float("nan"), device="cuda").to(torch.bfloat16)
+    vp = torch.full((num_pages, page_rows, d), float("nan"), device="cuda").to(torch.bfloat16)
+    table = torch.full((groups, max_pages), -1, dtype=torch.int32)
+    for gi in range(groups):
+        for pi in range(-(-int(lens[gi]) // page_rows)):
+            page = perm.pop()
+            table[gi, pi] = page
+            r0, r1 = pi * page_rows, min((pi + 1) * page_rows, int(lens[gi]))
+            kp[page, :r1 - r0] = k[gi, r0:r1]
+            vp[page, :r1 - r0] = v[gi, r0:r1]
+    o_p, l_p = K.attention_partial_paged(q, kp, vp, table.cuda(), lens)
+    o_r, l_r = K.attention_partial_ragged(q, k, v, lens)
+    assert torch.equal(o_p, o_r) and torch.equal(l_p, l_r)
+    assert torch.isneginf(l_p[1]).all() and (o_p[1] == 0).all()  # empty slab: the sentinel
+    ref = orc.partial(q[4].double().cpu().numpy(), k[4, :1000].double().cpu().numpy(),
+                      v[4, :1000].double().cpu().numpy())
+    err = float(np.max(np.abs(o_p[4].double().cpu().numpy() - ref.out))) / float(np.max(np.abs(ref.out)))
+    assert err <= 1e-2
+
+
+def test_paged_cache_commits_match_contiguous_cache():
+    from paper_2602_05305_b200 import KVCache, PagedKVCache
+    from paper_2602_05305_b200.errors import BoundsError
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    b, hq, hkv, blk, d = 2, 8, 2, 32, 128
+    paged = PagedKVCache(1, b, hkv, num_pages=40, page_rows=128, head_dim=d, max_pages_per_slab=16)
+    flat = KVCache(1, b, hkv, capacity=16 * 128, head_dim=d)
+    for step in range(21):  # 672 rows: 6 pages per slab, the last partly filled
+        kb = torch.randn((b, hkv, blk, d), device="cuda", generator=g).to(torch.bfloat16)
+        vb = torch.randn((b, hkv, blk, d), device="cuda", generator=g).to(torch.bfloat16)
+        paged.commit_block(0, kb, vb)
+        flat.commit_block(0, kb, vb)
+    assert torch.equal(paged.lengths[0], flat.lengths[0])
+    assert paged.free_pages() == 40 - b * hkv * 6
+    q = torch.randn((b, hq, blk, d), device="cuda", generator=g).to(torch.bfloat16)
+    from paper_2602_05305_b200 import kernels as K
+    o_p, l_p = paged.attention_partial(0, q)
+    o_f, l_f = K.attention_partial_ragged(K.gqa_view(q, hkv), flat.k[0].view(b * hkv, -1, d),
+                                          flat.v[0].view(b * hkv, -1, d), flat.lengths[0])
+    assert torch.equal(o_p, o_f) and torch.equal(l_p, l_f)
+    paged.release(0)
+    assert paged.free_pages() == 40 - hkv * 6
+    assert int(paged.lengths[0][:hkv].sum()) == 0
+    tiny = PagedKVCache(1, 1, 1, num_pages=1, page_rows=128, head_dim=d, max_pages_per_slab=4)
+    kb = torch.zeros((1, 1, 129, d), device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(BoundsError):
+        tiny.commit_block(0, kb, kb)  # needs 2 pages, the pool has 1
