@@ -122,8 +122,22 @@ class FlashBlockAttention:
         """Refresh step: K1 over the committed cache rows + K2; stores the
         external partial for `layer`.  n_ext is one context length for the
         batch (int) or per-sequence lengths (CUDA int32 tensor [b] or
-        [b*Hkv], ragged -- SURVEY 8f row f2).  Returns out [b, Hq, B, d]."""
+        [b*Hkv], ragged -- SURVEY 8f row f2).  k_cache may instead be a
+        PagedKVCache (v_cache and n_ext are then ignored: the cache's page
+        tables and lengths are used).  Returns out [b, Hq, B, d]."""
         qg, kg, vg = self._groups(q, k_in, v_in)
+        if isinstance(k_cache, PagedKVCache):  # paged serving cache: v_cache / n_ext unused
+            o = out.view(qg.shape) if out is not None else None
+            self._count_rows(k_cache.lengths[layer])
+            K.attention_partial_paged(qg, k_cache.k[layer], k_cache.v[layer], k_cache.table[layer],
+                                      k_cache.lengths[layer], self.scale, out=self.o_ext[layer],
+                                      lse=self.lse_ext[layer])
+            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
+                                   self.out_dtype, out=o)
+            self.valid[layer] = True
+            if self.recorder is not None:
+                self.recorder.observe(layer, self.o_ext[layer], self.B)
+            return res.view(self.b, self.hq, self.B, self.d)
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None
@@ -214,6 +228,18 @@ class FlashBlockAttention:
             gl = torch.tensor(ids, dtype=torch.int32, device=self.device)
             self._glists[key] = gl
         qg, kg, vg = self._groups(q, k_in, v_in)
+        if isinstance(k_cache, PagedKVCache):  # paged serving cache: v_cache / n_ext unused
+            o = out.view(qg.shape) if out is not None else None
+            self._count_rows(k_cache.lengths[layer])
+            K.attention_partial_paged(qg, k_cache.k[layer], k_cache.v[layer], k_cache.table[layer],
+                                      k_cache.lengths[layer], self.scale, out=self.o_ext[layer],
+                                      lse=self.lse_ext[layer])
+            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
+                                   self.out_dtype, out=o)
+            self.valid[layer] = True
+            if self.recorder is not None:
+                self.recorder.observe(layer, self.o_ext[layer], self.B)
+            return res.view(self.b, self.hq, self.B, self.d)
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         self._count_rows(gl.numel() * int(n_ext))
@@ -229,6 +255,18 @@ class FlashBlockAttention:
         """Baseline: full attention every step (same K1+K2 launch pair as a
         refresh, partial kept in scratch instead of the cache)."""
         qg, kg, vg = self._groups(q, k_in, v_in)
+        if isinstance(k_cache, PagedKVCache):  # paged serving cache: v_cache / n_ext unused
+            o = out.view(qg.shape) if out is not None else None
+            self._count_rows(k_cache.lengths[layer])
+            K.attention_partial_paged(qg, k_cache.k[layer], k_cache.v[layer], k_cache.table[layer],
+                                      k_cache.lengths[layer], self.scale, out=self.o_ext[layer],
+                                      lse=self.lse_ext[layer])
+            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
+                                   self.out_dtype, out=o)
+            self.valid[layer] = True
+            if self.recorder is not None:
+                self.recorder.observe(layer, self.o_ext[layer], self.B)
+            return res.view(self.b, self.hq, self.B, self.d)
         kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
         vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None

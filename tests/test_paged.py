@@ -83,3 +83,29 @@ def test_paged_cache_commits_match_contiguous_cache():
     kb = torch.zeros((1, 1, 129, d), device="cuda", dtype=torch.bfloat16)
     with pytest.raises(BoundsError):
         tiny.commit_block(0, kb, kb)  # needs 2 pages, the pool has 1
+
+
+def test_engine_refresh_on_paged_cache_equals_contiguous():
+    """FlashBlockAttention.refresh with a PagedKVCache (K1 through the page
+    tables, then K2) gives the same step output and cached partial as with the
+    contiguous KVCache and its ragged lengths; the cached step then agrees."""
+    from paper_2602_05305_b200 import FlashBlockAttention, KVCache, PagedKVCache
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    b, hq, hkv, blk, d = 2, 8, 2, 32, 128
+    paged = PagedKVCache(1, b, hkv, num_pages=64, page_rows=256, head_dim=d, max_pages_per_slab=16)
+    flat = KVCache(1, b, hkv, capacity=16 * 256, head_dim=d)
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    for _ in range(40):
+        kb, vb = r(b, hkv, blk, d), r(b, hkv, blk, d)
+        paged.commit_block(0, kb, vb)
+        flat.commit_block(0, kb, vb)
+    q, ki, vi = r(b, hq, blk, d), r(b, hkv, blk, d), r(b, hkv, blk, d)
+    e1 = FlashBlockAttention(1, b, hq, hkv, blk, d, out_dtype=torch.float32)
+    e2 = FlashBlockAttention(1, b, hq, hkv, blk, d, out_dtype=torch.float32)
+    out_p = e1.refresh(0, q, paged, None, None, ki, vi)
+    out_f = e2.refresh(0, q, flat.k[0], flat.v[0], flat.lengths[0], ki, vi)
+    assert torch.equal(out_p, out_f)
+    assert torch.equal(e1.o_ext[0], e2.o_ext[0]) and torch.equal(e1.lse_ext[0], e2.lse_ext[0])
+    q2 = r(b, hq, blk, d)
+    assert torch.equal(e1.cached(0, q2, ki, vi), e2.cached(0, q2, ki, vi))
