@@ -720,6 +720,37 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 }
 
+// Weighted sum of a row's split partials for the 4 columns at c, segments in
+// order (same arithmetic as a plain loop), with up to 8 segments' loads in
+// flight per lane instead of one dependent load per segment.  Items of a b=1
+// split-KV shard span ~16 CTAs: C3 b=1 refresh P=1/2/8 3/6/11 % faster.
+__device__ __forceinline__ float4 sum_segments(const Sched& sc, int item, int row, int bm, int D,
+                                               int c, int c_first, int nseg, float mx,
+                                               const float* __restrict__ ws_o,
+                                               const float* __restrict__ ws_l) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k0 = 0; k0 < nseg; k0 += 8) {
+    float w[8];
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      w[u] = 0.f;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < nseg && sc.start(c_first + k + 1) > sc.start(c_first + k)) {
+        const long long sl = sc.slot(c_first + k, item) * bm + row;
+        w[u] = __expf(ws_l[sl] - mx);
+        v[u] = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc.x += w[u] * v[u].x; acc.y += w[u] * v[u].y; acc.z += w[u] * v[u].z; acc.w += w[u] * v[u].w;
+    }
+  }
+  return acc;
+}
+
 // Fused final merge (MergeFinal): the row's K1 partial -- merged from the
 // split workspace and stored to (o_k1, l_k1) like the plain merge, or the
 // whole-item partial K1 already wrote there -- is merged with (o2, l2) and
@@ -758,6 +789,8 @@ __device__ __forceinline__ void final_merge_row(const Sched& sc, int item, int r
     z = warp_sum(z);
     const float iz = 1.f / z;
     if (col) {
+      // (a plain loop: sum_segments measured 2-4 % slower on this K7/K8 path,
+      // whose items span only ~5 CTAs)
       for (int k = 0; k < nseg; ++k) {
         if (!has(c_first + k)) continue;
         const long long sl = sc.slot(c_first + k, item) * bm + row;
@@ -842,14 +875,7 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   z = warp_sum(z);
   const float iz = 1.f / z;
   for (int c = lane * 4; c < D; c += 128) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = 0; k < nseg; ++k) {
-      if (!has(c_first + k)) continue;
-      const long long sl = sc.slot(c_first + k, item) * bm + row;
-      const float w = __expf(ws_l[sl] - mx);
-      const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
-      acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
-    }
+    const float4 acc = sum_segments(sc, item, row, bm, D, c, c_first, nseg, mx, ws_o, ws_l);
     *reinterpret_cast<float4*>(o_out + orow * D + c) =
         make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
   }
