@@ -504,6 +504,7 @@ FB_API void fb_debug_set_k1_diag(int diag) { set_k1_diag(diag); }
 FB_API void fb_debug_set_pair(int on) { set_pair_enabled(on); }
 FB_API int64_t fb_debug_pair_launches(void) { return (int64_t)pair_launches(); }
 FB_API void fb_debug_set_k2_variant(int v) { set_k2_v2(v); }
+FB_API void fb_debug_set_k2_trace(void* p, int launches) { set_k2_trace(p, launches); }
 int64_t fb_launch_count(void) { return g_launches.load(); }
 
 size_t fb_partial_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim,

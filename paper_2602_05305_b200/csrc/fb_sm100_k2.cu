@@ -41,7 +41,10 @@ struct Cfg {
   static constexpr int SPLIT = SPLIT_;
   static constexpr int DC = D / SPLIT;                  // output columns per CTA
   // O_ext columns prefetched into registers (fewer beside a 128-key score row)
-  static constexpr int PRE = NT >= 128 ? 32 : (DC > 64 ? 64 : DC);
+#ifndef FB_K2_PRE_MAX
+#define FB_K2_PRE_MAX 64  // diagnostics build knob (O_ext columns prefetched into registers)
+#endif
+  static constexpr int PRE = NT >= 128 ? 32 : (DC > FB_K2_PRE_MAX ? FB_K2_PRE_MAX : DC);
   static constexpr int NB = D / BOX;                    // 64-col boxes per bf16 row
   static constexpr int NBV = DC / BOX;                  // V boxes per CTA
   static constexpr uint32_t QBOX = BM * 128;            // 16 KB
@@ -61,15 +64,28 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-template <int D, int NT, int SPLIT>
-__global__ void __launch_bounds__(THREADS, 2)  // (3 CTAs/SM measured 8 % slower at C2 b=16)
+template <int D, int NT, int SPLIT, bool TRACE = false>
+#ifndef FB_K2_MIN_BLOCKS
+#define FB_K2_MIN_BLOCKS 2  // diagnostics build knob
+#endif
+__global__ void __launch_bounds__(THREADS, FB_K2_MIN_BLOCKS)  // (3 CTAs/SM at 136 regs: 8 % slower, C2 b=16)
 internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ o_ext,
                       const float* __restrict__ lse_ext, int q_rows, int m_tiles, int n_in,
                       float scale_log2, void* __restrict__ out, int out_bf16,
                       float* __restrict__ lse_merged, float* __restrict__ o_int,
-                      float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early) {
+                      float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early,
+                      unsigned long long* __restrict__ trace) {
   using C = Cfg<D, NT, SPLIT>;
+  // diagnostics (TRACE): per-CTA globaltimer stamps, 8 per CTA
+  auto stamp = [&](int i) {
+    if constexpr (TRACE) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[blockIdx.x * 8 + i] = t;
+    }
+  };
+  if (threadIdx.x == 128) stamp(0);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -118,8 +134,10 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
+  if (threadIdx.x == 128) stamp(1);
   ptx::pdl_wait();               // inputs of this launch are final from here on
   ptx::pdl_launch_dependents();
+  if (threadIdx.x == 128) stamp(2);
 
   if (warp == 4) {
     if (lane == 0) {
@@ -135,6 +153,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, C::DC, true);
       ptx::mbar_wait(&bar->load_qkv, 0);
+      stamp(3);
       ptx::tc_fence_after();
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
       const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K);
@@ -163,6 +182,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint32_t r[32];
     float s[NT];
     ptx::mbar_wait(&bar->s_full, 0);
+    if (threadIdx.x == 0) stamp(4);
     ptx::tc_fence_after();
 #pragma unroll
     for (int c = 0; c < NT / 32 + (NT % 32 ? 1 : 0); ++c) {
@@ -205,6 +225,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     ptx::tmem_wait_st();
     ptx::tc_fence_before();
     ptx::mbar_arrive(&bar->p_ready);
+    if (threadIdx.x == 0) stamp(5);
 
     // internal partial statistics (natural log), rounded as stored (fp32)
     const bool has_int = n_in > 0;
@@ -218,6 +239,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     const float iz = live ? 1.f / z : 0.f;
 
     ptx::mbar_wait(&bar->o_full, 0);
+    if (threadIdx.x == 0) stamp(6);
     ptx::tc_fence_after();
 #pragma unroll
     for (int c = 0; c < C::DC / 32; ++c) {
@@ -269,6 +291,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         }
       }
     }
+    if (threadIdx.x == 0) stamp(7);
     if (live_row && h == 0) {
       if (lse_int) lse_int[rr] = li;
       if (lse_merged) lse_merged[rr] = live ? mm + logf(z) : -INFINITY;
@@ -546,6 +569,14 @@ bool sm100_k2_supported(int64_t head_dim, int64_t n_in) {
   return (head_dim == 128 || head_dim == 64) && n_in >= 1 && n_in <= 128;
 }
 
+static unsigned long long* g_k2_trace = nullptr;  // diagnostics: fb_debug_set_k2_trace
+static int g_k2_trace_n = 0, g_k2_trace_i = 0;
+void set_k2_trace(void* p, int launches) {
+  g_k2_trace = reinterpret_cast<unsigned long long*>(p);
+  g_k2_trace_n = launches;
+  g_k2_trace_i = 0;
+}
+
 template <int D, int NT, int SPLIT>
 static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
                      int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
@@ -558,18 +589,22 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   const int64_t nin_eff = n_in > 0 ? n_in : 1;  // zero-row maps are invalid; rows are masked
   if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
-  auto kern = sm100k2::internal_merge_kernel<D, NT, SPLIT>;
-  static bool attr = false;
-  if (!attr) {
+  unsigned long long* trace = nullptr;
+  if (g_k2_trace != nullptr && g_k2_trace_i < g_k2_trace_n)
+    trace = g_k2_trace + (size_t)(g_k2_trace_i++) * 1024 * 8;  // slab per traced launch
+  auto kern = trace ? sm100k2::internal_merge_kernel<D, NT, SPLIT, true>
+                    : sm100k2::internal_merge_kernel<D, NT, SPLIT, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[trace ? 1 : 0]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr = true;
+    attr[trace ? 1 : 0] = true;
   }
   const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles * C::SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st,
              mq, mk, mv, o_ext, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
              out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
-             ext_early ? 1 : 0);
+             ext_early ? 1 : 0, trace);
   count_launch();
   return check_launch("internal_merge_kernel(sm100)");
 }
