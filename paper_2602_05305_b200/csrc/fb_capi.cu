@@ -818,12 +818,20 @@ int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void*
         float* oi = o_int ? reinterpret_cast<float*>(o_int) : reinterpret_cast<float*>(workspace);
         float* li = lse_int ? reinterpret_cast<float*>(lse_int)
                             : reinterpret_cast<float*>(workspace) + (size_t)rows * head_dim;
+        // without an lse_merged output the K3 merge with the cached external
+        // partial runs inside K1's split-merge kernel (MergeFinal): one launch
+        // and one pass over the internal partial fewer
+        const MergeFinal fin{reinterpret_cast<const float*>(o_ext), reinterpret_cast<const float*>(lse_ext),
+                             out, out_dtype == FB_BF16 ? 1 : 0, empty_rows};
+        const bool fuse = lse_merged == nullptr;
         int rc = launch_refresh_sm100(reinterpret_cast<const __nv_bfloat16*>(q),
                                       reinterpret_cast<const __nv_bfloat16*>(k_in),
                                       reinterpret_cast<const __nv_bfloat16*>(v_in), groups, q_rows,
                                       head_dim, n_in, 0, n_in, scale, oi, li,
-                                      reinterpret_cast<char*>(workspace) + tmp, workspace_bytes - tmp, st);
+                                      reinterpret_cast<char*>(workspace) + tmp, workspace_bytes - tmp, st,
+                                      nullptr, 0, fuse ? &fin : nullptr);
         if (rc) return rc;
+        if (fuse) return FB_OK;
         const void* op[2] = {o_ext, oi};
         const void* lp[2] = {lse_ext, li};
         return combine_t<ModeBF16>(2, op, lp, rows, head_dim, out, out_dtype == FB_BF16, lse_merged,

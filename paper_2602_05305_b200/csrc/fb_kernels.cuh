@@ -58,6 +58,18 @@ int launch_topk(const double* mass, int64_t groups, int64_t nb, int64_t budget, 
 template <typename To, typename Tl>
 int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStream_t st);
 
+// Optional final step fused into K1's split-merge kernel: merge every row's
+// partial with a second fp32 partial (o2, l2; e.g. the cached residual) and
+// write the attention output (bf16 or fp32) instead of a partial, counting
+// rows empty on both sides -- K3 folded into the same launch.
+struct MergeFinal {
+  const float* o2;
+  const float* l2;
+  void* out;
+  int out_bf16;
+  int32_t* empty_rows;
+};
+
 // tcgen05 / TMA refresh kernel (bf16, head_dim 64 or 128): normalised fp32
 // partial + fp32 natural-log lse over keys [key_begin, key_end) of every
 // group, written to (o_out, lse_out).  Stream-K over all SMs; split partials
@@ -75,7 +87,8 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
                          float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st,
-                         unsigned long long* sync_flags = nullptr, int64_t n_flags = 0);
+                         unsigned long long* sync_flags = nullptr, int64_t n_flags = 0,
+                         const MergeFinal* fin = nullptr);
 
 // Ragged per-group key ends (device int32 [groups], clamped to kv_rows_cap).
 size_t refresh_sm100_ragged_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim);
@@ -115,17 +128,6 @@ struct GatherSpec {
 };
 size_t gather_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim,
                                     int64_t n_list, int64_t n_in);
-// Optional final step fused into K1's split-merge kernel: merge every row's
-// partial with a second fp32 partial (o2, l2; e.g. the cached residual) and
-// write the attention output (bf16 or fp32) instead of a partial, counting
-// rows empty on both sides -- K3 folded into the same launch.
-struct MergeFinal {
-  const float* o2;
-  const float* l2;
-  void* out;
-  int out_bf16;
-  int32_t* empty_rows;
-};
 int launch_gather_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                         int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                         const GatherSpec& gs, double scale, float* o_out, float* lse_out, void* ws,

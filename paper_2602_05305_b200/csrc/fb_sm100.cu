@@ -1402,7 +1402,7 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
                            int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
                            int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
                            size_t ws_bytes, cudaStream_t st, const sm100::Causal* causal,
-                           const int32_t* glist, int64_t n_list) {
+                           const int32_t* glist, int64_t n_list, const MergeFinal* fin = nullptr) {
   constexpr int D = 128;
   using P = sm100::pair::PCfg<D>;
   constexpr int PM = sm100::pair::PM;
@@ -1422,6 +1422,7 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   bool need_merge;
+  if (causal && fin != nullptr) return -1;
   if (causal) {
     // whole items round-robin over the pairs (SegIter): no prefix scan, no
     // split partials, no merge kernel; all pairs on one group's K/V at a time
@@ -1432,7 +1433,9 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   } else {
     sc.ctas = (int)std::min<long long>(maxp, sc.T);
     need_merge = !(sc.T % sc.ctas == 0 && (sc.T / sc.ctas) % tpi == 0);
-    if (need_merge) {
+    const bool split = need_merge;
+    if (fin != nullptr) need_merge = true;  // the merge kernel writes the final output
+    if (split) {
       const size_t need = (size_t)2 * sc.ctas * PM * (D + 1) * sizeof(float);
       if (ws == nullptr || ws_bytes < need) return -1;
       ws_o = reinterpret_cast<float*>(ws);
@@ -1476,7 +1479,8 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   if (!need_merge) return FB_OK;
   const long long warps = (long long)items * PM;
   launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
-             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM, MergeFinal{});
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM,
+             fin ? *fin : MergeFinal{});
   count_launch();
   return check_launch("refresh_merge_kernel(sm100, pair)");
 }
@@ -1536,7 +1540,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     const bool pair_on = pm == 1 || (pm == 2 && causal != nullptr);
     if (pair_on && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
       const int prc = launch_pair_128(k, mq, mv, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
-                                      o_out, lse_out, ws, ws_bytes, st, causal, glist, n_list);
+                                      o_out, lse_out, ws, ws_bytes, st, causal, glist, n_list, fin);
       if (prc != -1) return prc;
     }
   }
@@ -1652,15 +1656,15 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t kv_rows_cap,
                          int64_t key_begin, int64_t key_end, double scale, float* o_out,
                          float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st,
-                         unsigned long long* sync_flags, int64_t n_flags) {
+                         unsigned long long* sync_flags, int64_t n_flags, const MergeFinal* fin) {
   if (head_dim == 128)
     return launch_refresh_d<128, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
                                         scale, o_out, lse_out, ws, ws_bytes, st, nullptr, nullptr,
-                                        nullptr, nullptr, 0, sync_flags, n_flags);
+                                        nullptr, nullptr, 0, sync_flags, n_flags, fin);
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, key_end,
                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, nullptr,
-                                       nullptr, nullptr, 0, sync_flags, n_flags);
+                                       nullptr, nullptr, 0, sync_flags, n_flags, fin);
   return FB_ERR_UNSUPPORTED;
 }
 
