@@ -196,6 +196,18 @@ FB_API int fb_attention_partial_paged(int dtype, const void* q, const void* k_pa
                                       double scale, void* o_out, void* lse_out, void* workspace,
                                       size_t workspace_bytes, void* stream);
 FB_API size_t fb_paged_workspace_bytes(int dtype, int64_t groups, int64_t q_rows, int64_t head_dim);
+/* Block-causal (prefill / commit) attention over a paged cache: the same
+ * rows and limits as fb_block_causal_attention, keys [0, n_prefix + n_q) of
+ * group g read through its page table (the prompt committed into the pages
+ * first).  BF16, head_dim 64 / 128, page_rows a multiple of 128; workspace
+ * fb_paged_workspace_bytes. */
+FB_API int fb_block_causal_attention_paged(int dtype, const void* q, const void* k_pages,
+                                           const void* v_pages, int64_t num_pages, int64_t page_rows,
+                                           const int32_t* page_table, int64_t max_pages,
+                                           int64_t groups, int64_t q_rows, int64_t n_q,
+                                           int64_t head_dim, int64_t n_prefix, int64_t block_size,
+                                           double scale, void* o_out, void* lse_out,
+                                           void* workspace, size_t workspace_bytes, void* stream);
 /* Paged block commit: rows lengths[g] .. lengths[g] + block_rows - 1 of group
  * g go to their pages (rows past the table or onto a negative page id are
  * dropped and counted in *overflow); lengths advance by block_rows. */

@@ -607,6 +607,33 @@ int fb_attention_partial_paged(int dtype, const void* q, const void* k_pages, co
       reinterpret_cast<float*>(lse_out), workspace, workspace_bytes, as_stream(stream));
 }
 
+int fb_block_causal_attention_paged(int dtype, const void* q, const void* k_pages, const void* v_pages,
+                                    int64_t num_pages, int64_t page_rows, const int32_t* page_table,
+                                    int64_t max_pages, int64_t groups, int64_t q_rows, int64_t n_q,
+                                    int64_t head_dim, int64_t n_prefix, int64_t block_size, double scale,
+                                    void* o_out, void* lse_out, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (groups < 0 || q_rows < 0 || n_q < 1 || head_dim < 1 || n_prefix < 0 || block_size < 1 ||
+      num_pages < 0 || max_pages < 0)
+    return fail(FB_ERR_SHAPE, "bad extents");
+  if (q_rows % n_q != 0) return fail(FB_ERR_SHAPE, "q_rows must be heads_per_group * n_q");
+  if (page_table == nullptr) return fail(FB_ERR_VALUE, "page_table (device int32) is required");
+  if (dtype != FB_BF16 || !sm100_supported(head_dim))
+    return fail(FB_ERR_UNSUPPORTED, "paged KV: bf16 with head_dim 64 or 128");
+  if (page_rows <= 0 || page_rows % 128 != 0)
+    return fail(FB_ERR_UNSUPPORTED, "page_rows must be a positive multiple of 128");
+  if (n_prefix + n_q > max_pages * page_rows) return fail(FB_ERR_BOUNDS, "prompt exceeds the pages");
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  if (workspace == nullptr || workspace_bytes < fb_paged_workspace_bytes(dtype, groups, q_rows, head_dim))
+    return fail(FB_ERR_VALUE, "workspace too small (fb_paged_workspace_bytes)");
+  return launch_block_causal_paged_sm100(
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k_pages),
+      reinterpret_cast<const __nv_bfloat16*>(v_pages), num_pages, page_rows, page_table, max_pages,
+      groups, q_rows, head_dim, n_q, n_prefix, block_size, scale, reinterpret_cast<float*>(o_out),
+      reinterpret_cast<float*>(lse_out), workspace, workspace_bytes, as_stream(stream));
+}
+
 int fb_commit_block_paged(int dtype, void* k_pages, void* v_pages, int64_t page_rows,
                           const int32_t* page_table, int64_t max_pages, int64_t groups,
                           int64_t head_dim, const void* k_block, const void* v_block,

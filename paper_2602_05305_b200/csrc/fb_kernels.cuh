@@ -97,6 +97,12 @@ int launch_refresh_paged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_pa
                                const int32_t* page_table, int64_t max_pages, int64_t groups,
                                int64_t q_rows, int64_t head_dim, const int32_t* key_len, double scale,
                                float* o_out, float* lse_out, void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_block_causal_paged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_pages,
+                                    const __nv_bfloat16* v_pages, int64_t num_pages, int64_t page_rows,
+                                    const int32_t* page_table, int64_t max_pages, int64_t groups,
+                                    int64_t q_rows, int64_t head_dim, int64_t n_q, int64_t n_prefix,
+                                    int64_t block, double scale, float* o_out, float* lse_out, void* ws,
+                                    size_t ws_bytes, cudaStream_t st);
 int launch_commit_block_paged(void* kp, void* vp, int64_t page_rows, const int32_t* table,
                               int64_t max_pages, const void* kb, const void* vb, int64_t groups,
                               int64_t row_bytes, int64_t blk_rows, int32_t* len, int32_t* overflow,

@@ -1402,7 +1402,8 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
                            int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
                            int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
                            size_t ws_bytes, cudaStream_t st, const sm100::Causal* causal,
-                           const int32_t* glist, int64_t n_list, const MergeFinal* fin = nullptr) {
+                           const int32_t* glist, int64_t n_list, const MergeFinal* fin = nullptr,
+                           const sm100::Paged* paged = nullptr, int64_t num_pages = 0) {
   constexpr int D = 128;
   using P = sm100::pair::PCfg<D>;
   constexpr int PM = sm100::pair::PM;
@@ -1412,8 +1413,15 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   if (items <= 0 || tpi <= 0) return -1;
   CUtensorMap mk;
   int rc;
-  if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS, sm100::pair::HN)))
+  if (paged != nullptr) {  // K halves over the page pool [num_pages, page_rows, D]
+    if ((rc = make_tmap_3d(&mk, k, 2, D, paged->page_rows, paged->page_rows, num_pages, sm100::BOX_COLS,
+                           sm100::pair::HN)))
+      return rc;
+  } else if ((rc = make_tmap_3d(&mk, k, 2, D, key_end, kv_rows_cap, groups, sm100::BOX_COLS,
+                                sm100::pair::HN))) {
     return rc;
+  }
+  const sm100::Paged pgv = paged ? *paged : sm100::Paged{nullptr, 0, 1};
   sm100::Causal cz{1, 0, 0};
   if (causal) cz = *causal;
   const int maxp = pair_clusters();
@@ -1451,7 +1459,7 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
     auto kd = sm100::pair::pair_kernel<D, -1>;
     cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
     const float sl = (float)(scale * 1.4426950408889634);
-    launch_pdl(kd, dim3((unsigned)(2 * sc.ctas)), dim3(sm100::THREADS), P::SMEM, st, mq, mk, mv, cz, sc,
+    launch_pdl(kd, dim3((unsigned)(2 * sc.ctas)), dim3(sm100::THREADS), P::SMEM, st, mq, mk, mv, pgv, cz, sc,
                (int)q_rows, (int)key_begin, (int)key_end, sl, o_out, lse_out, ws_o, ws_l);
     count_launch();
     if ((rc = check_launch("pair_kernel(diag)"))) return rc;
@@ -1471,7 +1479,7 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
     attr[poly & 7] = true;
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  launch_pdl(kern, dim3((unsigned)(2 * sc.ctas)), dim3(sm100::THREADS), P::SMEM, st, mq, mk, mv, cz, sc,
+  launch_pdl(kern, dim3((unsigned)(2 * sc.ctas)), dim3(sm100::THREADS), P::SMEM, st, mq, mk, mv, pgv, cz, sc,
              (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l);
   count_launch();
   ++g_pair_launches;
@@ -1540,7 +1548,8 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     const bool pair_on = pm == 1 || (pm == 2 && causal != nullptr);
     if (pair_on && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
       const int prc = launch_pair_128(k, mq, mv, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
-                                      o_out, lse_out, ws, ws_bytes, st, causal, glist, n_list, fin);
+                                      o_out, lse_out, ws, ws_bytes, st, causal, glist, n_list, fin,
+                                      paged, num_pages);
       if (prc != -1) return prc;
     }
   }
@@ -1679,6 +1688,30 @@ int launch_refresh_ragged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k,
   if (head_dim == 64)
     return launch_refresh_d<64, false>(q, k, v, groups, q_rows, kv_rows_cap, key_begin, kv_rows_cap,
                                        scale, o_out, lse_out, ws, ws_bytes, st, nullptr, key_end);
+  return FB_ERR_UNSUPPORTED;
+}
+
+// Block-causal (prefill / commit) attention reading the prompt's keys through
+// a paged cache: same rows and limits as launch_block_causal_sm100.
+int launch_block_causal_paged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_pages,
+                                    const __nv_bfloat16* v_pages, int64_t num_pages, int64_t page_rows,
+                                    const int32_t* page_table, int64_t max_pages, int64_t groups,
+                                    int64_t q_rows, int64_t head_dim, int64_t n_q, int64_t n_prefix,
+                                    int64_t block, double scale, float* o_out, float* lse_out, void* ws,
+                                    size_t ws_bytes, cudaStream_t st) {
+  if (page_rows <= 0 || page_rows % sm100::BN != 0)
+    return fail(FB_ERR_UNSUPPORTED, "page_rows must be a positive multiple of 128");
+  const sm100::Paged pg{page_table, (int)max_pages, (int)page_rows};
+  const sm100::Causal cz{(int)n_q, (int)block, (int)n_prefix};
+  const int64_t cap = max_pages * page_rows, end = n_prefix + n_q;
+  if (head_dim == 128)
+    return launch_refresh_d<128, false>(q, k_pages, v_pages, groups, q_rows, cap, 0, end, scale, o_out,
+                                        lse_out, ws, ws_bytes, st, nullptr, nullptr, &cz, nullptr, 0,
+                                        nullptr, 0, nullptr, &pg, num_pages);
+  if (head_dim == 64)
+    return launch_refresh_d<64, false>(q, k_pages, v_pages, groups, q_rows, cap, 0, end, scale, o_out,
+                                       lse_out, ws, ws_bytes, st, nullptr, nullptr, &cz, nullptr, 0,
+                                       nullptr, 0, nullptr, &pg, num_pages);
   return FB_ERR_UNSUPPORTED;
 }
 

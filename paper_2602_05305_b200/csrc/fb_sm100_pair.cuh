@@ -110,7 +110,7 @@ struct SegIter {
 template <int D, int POLY = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-            const __grid_constant__ CUtensorMap tm_v, Causal cz, Sched sc, int q_rows, int key_begin,
+            const __grid_constant__ CUtensorMap tm_v, Paged pg, Causal cz, Sched sc, int q_rows, int key_begin,
             int key_end, float scale_log2, float* __restrict__ o_out, float* __restrict__ lse_out,
             float* __restrict__ ws_o, float* __restrict__ ws_l) {
   using C = PCfg<D>;
@@ -183,17 +183,22 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           for (; t < seg_end; ++t, ++j) {
             const int s = j % C::STAGES;
             const uint32_t ph = (j / C::STAGES) & 1;
-            const int row = key_begin + (int)(t - ib) * BN;
+            int row = key_begin + (int)(t - ib) * BN;
+            int slab = g;
+            if (pg.table != nullptr) {  // paged cache: the tile's page, row inside it
+              slab = __ldg(pg.table + (long long)g * pg.max_pages + row / pg.page_rows);
+              row %= pg.page_rows;
+            }
             ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
             if (leader) ptx::mbar_expect_tx(&bar->k_full[s], 2 * C::K_BYTES);
             const uint32_t kf = ptx::mapa(&bar->k_full[s], 0);
             for (int b = 0; b < D / BOX_COLS; ++b)
               ptx::tma_load_3d_pair(smem + C::OFF_K + s * C::K_BYTES + b * C::KBOX, &tm_k, kf,
-                                    b * BOX_COLS, row + (int)rank * HN, g, stream);
+                                    b * BOX_COLS, row + (int)rank * HN, slab, stream);
             ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
             if (leader) ptx::mbar_expect_tx(&bar->v_full[s], 2 * C::V_BYTES);
             ptx::tma_load_3d_pair(smem + C::OFF_V + s * C::V_BYTES, &tm_v, ptx::mapa(&bar->v_full[s], 0),
-                                  (int)rank * HN, row, g, stream);
+                                  (int)rank * HN, row, slab, stream);
           }
         }
       }

@@ -203,6 +203,21 @@ class FlashBlockAttention:
         res, _ = K.block_causal_attention(qg, kc, vc, n_q, n_prefix, self.B, self.scale, out=o, lse=lse)
         return res.view(b, hq, n_q, d)
 
+    def prefill_paged(self, q, cache: "PagedKVCache", layer: int, n_prefix: int = 0, out=None, lse=None):
+        """prefill() with the prompt's K/V read through a PagedKVCache's page
+        tables for `layer` (commit the prompt into the cache first; every slab
+        must hold n_prefix + n_q rows)."""
+        b, hq, n_q, d = q.shape
+        if (b, hq, d) != (self.b, self.hq, self.d):
+            raise ShapeError(f"queries {tuple(q.shape)} do not match the engine")
+        qg = q.reshape(self.b * self.hkv, (self.hq // self.hkv) * n_q, self.d)
+        o = out.view(qg.shape) if out is not None else None
+        nblk = -(-n_q // self.B)
+        self._count_rows(self.b * self.hkv * (nblk * n_prefix + self.B * nblk * (nblk - 1) // 2))
+        res, _ = K.block_causal_attention_paged(qg, cache.k[layer], cache.v[layer], cache.table[layer], n_q,
+                                                n_prefix, self.B, self.scale, out=o, lse=lse)
+        return res.view(b, hq, n_q, d)
+
     def step_gated(self, layer: int, q, k_cache, v_cache, n_ext: int, k_in, v_in, *,
                    first_visit: bool, updated_tokens: int, gates, out=None):
         """Head-gated mode: every query head decides on its

@@ -211,6 +211,35 @@ def attention_partial_paged(q, k_pages, v_pages, page_table: torch.Tensor, key_l
     return out, lse
 
 
+def block_causal_attention_paged(q, k_pages, v_pages, page_table: torch.Tensor, n_q: int,
+                                 n_prefix: int = 0, block_size: int = 32, scale: float | None = None,
+                                 out=None, lse=None):
+    """Prefill / commit attention (block_causal_attention) with the keys read
+    through a paged cache's page tables (the prompt committed into the pages
+    first).  bf16; q [groups, heads_per_group * n_q, d]."""
+    q3 = _as3(q, "q").contiguous()
+    require_cuda(q3, k_pages, v_pages, page_table)
+    if k_pages.dim() != 3 or k_pages.shape != v_pages.shape or k_pages.shape[2] != q3.shape[2]:
+        raise ShapeError("page pools must be [num_pages, page_rows, head_dim] and match q")
+    if q3.dtype != torch.bfloat16 or k_pages.dtype != torch.bfloat16:
+        raise ShapeError("the paged path is bf16")
+    kp, vp = k_pages.contiguous(), v_pages.contiguous()
+    groups, q_rows, d = q3.shape
+    table = page_table.reshape(groups, -1).to(torch.int32).contiguous()
+    if out is None:
+        out = torch.empty((groups, q_rows, d), dtype=torch.float32, device=q3.device)
+    if lse is None:
+        lse = torch.empty((groups, q_rows), dtype=torch.float32, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    wsb = _lib.load().fb_paged_workspace_bytes(_CODE[torch.bfloat16], groups, q_rows, d)
+    ws = WORKSPACE.get(q3.device, wsb) if wsb else None
+    _lib.call("fb_block_causal_attention_paged", _CODE[torch.bfloat16], _p(q3), _p(kp), _p(vp),
+              kp.shape[0], kp.shape[1], _p(table), table.shape[1], groups, q_rows, int(n_q), d,
+              int(n_prefix), int(block_size), scale, _p(out), _p(lse), _p(ws),
+              0 if ws is None else ws.numel(), _stream(q3))
+    return out, lse
+
+
 def commit_block_paged(k_pages, v_pages, page_table: torch.Tensor, k_block, v_block,
                        lengths: torch.Tensor, check: bool = False) -> None:
     """Append a finished block's K/V ([groups, B, d]) to each group's pages at

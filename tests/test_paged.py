@@ -109,3 +109,36 @@ def test_engine_refresh_on_paged_cache_equals_contiguous():
     assert torch.equal(e1.o_ext[0], e2.o_ext[0]) and torch.equal(e1.lse_ext[0], e2.lse_ext[0])
     q2 = r(b, hq, blk, d)
     assert torch.equal(e1.cached(0, q2, ki, vi), e2.cached(0, q2, ki, vi))
+
+
+@pytest.mark.parametrize("pair", [1, 0])
+def test_paged_prefill_equals_contiguous_bitwise(pair):
+    """Block-causal prefill reading the prompt through page tables (CTA-pair
+    kernel by default, single-CTA forced) equals the contiguous-slab prefill
+    bit for bit; engine.prefill_paged after committing the prompt into a
+    PagedKVCache equals engine.prefill on the contiguous cache."""
+    import ctypes
+
+    from paper_2602_05305_b200 import FlashBlockAttention, KVCache, PagedKVCache, _lib
+
+    lib = _lib.load()
+    lib.fb_debug_set_pair.argtypes = [ctypes.c_int]
+    g = torch.Generator(device="cuda").manual_seed(21 + pair)
+    b, hq, hkv, blk, d, n_q = 2, 8, 2, 32, 128, 640
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    paged = PagedKVCache(1, b, hkv, num_pages=32, page_rows=128, head_dim=d, max_pages_per_slab=8)
+    flat = KVCache(1, b, hkv, capacity=8 * 128, head_dim=d)
+    kp, vp = r(b, hkv, n_q, d), r(b, hkv, n_q, d)
+    for c0 in range(0, n_q, 128):  # commit the prompt block by block (pages from the free list)
+        paged.commit_block(0, kp[:, :, c0:c0 + 128], vp[:, :, c0:c0 + 128])
+        flat.commit_block(0, kp[:, :, c0:c0 + 128], vp[:, :, c0:c0 + 128])
+    q = r(b, hq, n_q, d)
+    eng = FlashBlockAttention(1, b, hq, hkv, blk, d)
+    lib.fb_debug_set_pair(pair)
+    try:
+        o_p = eng.prefill_paged(q, paged, 0)
+        o_f = eng.prefill(q, flat.k[0], flat.v[0])
+    finally:
+        lib.fb_debug_set_pair(-1)
+    assert torch.isfinite(o_p).all()
+    assert torch.equal(o_p, o_f)
