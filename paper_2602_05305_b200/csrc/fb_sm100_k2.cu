@@ -64,10 +64,10 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-template <int D, int NT, int SPLIT, bool TRACE = false>
 #ifndef FB_K2_MIN_BLOCKS
 #define FB_K2_MIN_BLOCKS 2  // diagnostics build knob
 #endif
+template <int D, int NT, int SPLIT, bool TRACE = false>
 __global__ void __launch_bounds__(THREADS, FB_K2_MIN_BLOCKS)  // (3 CTAs/SM at 136 regs: 8 % slower, C2 b=16)
 internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ o_ext,
