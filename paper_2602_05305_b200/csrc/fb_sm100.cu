@@ -404,13 +404,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V + s * C::TILE_BYTES);
             const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
             const uint32_t o_tmem = tmem + ((jj & 1) ? C::COL_O1 : C::COL_O0);
+            if constexpr (DIAG != 3) {  // DIAG 3 (diagnostics): no P V MMA, S = Q K^T only
 #pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk) {
-              // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
-              // (the first two tiles of a segment start their warpgroup's O afresh)
-              ptx::mma_ts(o_tmem, p_tmem + kk * 8,
-                          ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
-                          (t > 2 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BN / 16; ++kk) {
+                // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
+                // (the first two tiles of a segment start their warpgroup's O afresh)
+                ptx::mma_ts(o_tmem, p_tmem + kk * 8,
+                            ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
+                            (t > 2 || kk > 0) ? 1u : 0u);
+              }
             }
             ptx::tc_commit(&bar->v_empty[s]);
             ptx::tc_commit(&bar->pv_done[jj & 1]);
@@ -1558,8 +1560,9 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     if (g_k1_diag == 1) kern = sm100::refresh_kernel<D, false, 1>;
     if (g_k1_diag == 2) kern = sm100::refresh_kernel<D, false, 2>;
     if (g_k1_diag == 3) kern = sm100::refresh_kernel<D, false, 0, 4>;  // 1/4 of the pairs on FMA
+    if (g_k1_diag == 6) kern = sm100::refresh_kernel<D, false, 3>;     // no softmax, no P V
   }
-  int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 5 ? g_k1_diag : 0);
+  int ai = GATHER ? 0 : (g_k1_diag > 0 && g_k1_diag < 5 ? g_k1_diag : (g_k1_diag == 6 ? 5 : 0));
   if constexpr (!GATHER && D == 128) {
     static int poly = -1;
     if (poly < 0) {

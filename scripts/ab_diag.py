@@ -34,7 +34,7 @@ op, lp = K.block_causal_attention(qp, kp, vp, n_q, 0, 32)
 fl_c5 = 4.0 * 12 * 4680 * 56160 * 128
 fl_pf = 4.0 * 8 * 4 * sum(min(n_q, (p // 32 + 1) * 32) for p in range(0, n_q, 32)) * 32 * 128
 res = {"pair_poly_env": os.environ.get("FB_PAIR_POLY", "0")}
-for name, pair, diag in (("pair", 1, 0), ("single", 0, 0), ("single_nosoftmax", 0, 2)):
+for name, pair, diag in (("pair", 1, 0), ("single", 0, 0), ("single_nosoftmax", 0, 2), ("single_nosoftmax_nopv", 0, 6)):
     lib.fb_debug_set_pair(pair); lib.fb_debug_set_k1_diag(diag)
     t5 = gms(lambda: K.attention_partial(qv, kv, vv, 0, None, None, ov, lv))
     tp = gms(lambda: K.block_causal_attention(qp, kp, vp, n_q, 0, 32, None, op, lp))
