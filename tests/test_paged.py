@@ -142,3 +142,30 @@ def test_paged_prefill_equals_contiguous_bitwise(pair):
         lib.fb_debug_set_pair(-1)
     assert torch.isfinite(o_p).all()
     assert torch.equal(o_p, o_f)
+
+
+def test_paged_api_errors():
+    """The paged entry points refuse what they do not support, with the
+    reference's exception types: non-bf16 inputs (ShapeError from the
+    wrapper), page_rows not a multiple of 128 (UnsupportedError), and a commit
+    past the pages (BoundsError with check=True)."""
+    from paper_2602_05305_b200 import kernels as K
+    from paper_2602_05305_b200.errors import BoundsError, ShapeError
+
+    d = 128
+    q = torch.zeros((2, 128, d), device="cuda", dtype=torch.bfloat16)
+    pool = torch.zeros((4, 128, d), device="cuda", dtype=torch.bfloat16)
+    table = torch.tensor([[0, 1], [2, 3]], dtype=torch.int32, device="cuda")
+    lens = torch.tensor([200, 0], dtype=torch.int32, device="cuda")
+    with pytest.raises(ShapeError):
+        K.attention_partial_paged(q.float(), pool, pool, table, lens)
+    bad = torch.zeros((4, 96, d), device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(Exception) as ei:
+        K.attention_partial_paged(q, bad, bad, table, lens)
+    assert "128" in str(ei.value)
+    o, l = K.attention_partial_paged(q, pool, pool, table, lens)
+    assert torch.isneginf(l[1]).all() and (o[1] == 0).all()  # empty slab: the sentinel
+    lengths = torch.tensor([250, 0], dtype=torch.int32, device="cuda")
+    blk = torch.ones((2, 32, d), device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(BoundsError):
+        K.commit_block_paged(pool, pool, table, blk, blk, lengths, check=True)  # 250 + 32 > 2 pages
