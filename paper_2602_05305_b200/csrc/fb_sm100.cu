@@ -1,25 +1,31 @@
 // K1 -- block-external ("refresh") partial attention on sm_100a.
 //
 // Computes, per group g (a kv head of one sequence, its G query heads stacked
-// into 128-row query tiles) and per key split, the normalised online-softmax
-// partial over keys [kb, ke) of the slab -- the reference's attention_partial
-// over the committed context (attention.py:136-182, called at :202).  This is
-// the HBM-bound kernel: the KV cache is streamed exactly once.
+// into 128-row query tiles), the normalised online-softmax partial over keys
+// [kb, ke) of the slab -- the reference's attention_partial over the committed
+// context (attention.py:136-182, called at :202).  At C2 this is the HBM-bound
+// kernel: the KV cache is streamed exactly once.
 //
-// Structure (one CTA per (split, group, 128-row query tile); 256 threads):
-//   warp 0      TMA producer: Q tile once, then K/V 128-key tiles into a
-//               STAGES-deep ring (128B-swizzled boxes of 64 columns).
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T  (SS, tcgen05.mma into
+// Structure (persistent: one CTA per SM, stream-K over (item, key tile); 384
+// threads):
+//   warp 0      TMA producer: Q tile once per segment, then K/V 128-key tiles
+//               into a STAGES-deep ring (128B-swizzled boxes of 64 columns);
+//               on the gathered path warp 3 issues the V tiles.
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T (SS, tcgen05.mma into
 //               TMEM, double-buffered S), then O += P_{j-1} V_{j-1} with P
 //               read straight from TMEM (TS form) -- QK^T of tile j overlaps
 //               the softmax of tile j-1.
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O).
-//   warps 4..7  softmax: thread t owns query row t (TMEM lane t); reads S,
-//               keeps (max, sum) in registers, writes P (bf16) back over S,
-//               rescales O in TMEM only when the running max grows by more
-//               than 2^8 (exact: the same max is used for l and O), and
-//               finally normalises O and writes the fp32 partial and the
-//               natural-log lognorm.
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1).
+//   warps 4-11  two softmax warpgroups on alternate key tiles: thread t owns
+//               query row t (TMEM lane t); reads S, keeps (max, sum) in
+//               registers, writes P (bf16) back over S, rescales its O in
+//               TMEM only when the running max grows by more than 2^8 (exact:
+//               the same max is used for l and O); the segment epilogue merges
+//               the two warpgroups' partials and writes the fp32 partial and
+//               the natural-log lognorm (or a split partial for the merge).
+// Key sources: contiguous slabs, ragged lengths, page tables (Paged), block-
+// causal row limits (Causal) and mask-selected 16-key blocks (Gather, K7/K8).
+// The CTA-pair (cta_group::2) variant lives in fb_sm100_pair.cuh.
 #include "fb_kernels.cuh"
 #include "fb_sm100_ptx.cuh"
 
