@@ -208,6 +208,39 @@ FB_API int fb_block_causal_attention_paged(int dtype, const void* q, const void*
                                            int64_t head_dim, int64_t n_prefix, int64_t block_size,
                                            double scale, void* o_out, void* lse_out,
                                            void* workspace, size_t workspace_bytes, void* stream);
+/* Sparse path (K5 block mass, K7 first step, K8 cached step) over a paged
+ * cache: the same semantics as fb_block_mass / fb_sparse_partitioned /
+ * fb_sparse_attend_merge, with group g's cache row r read from row
+ * r % page_rows of page page_table[g * max_pages + r / page_rows] of the
+ * pools [num_pages, page_rows, head_dim].  BF16, head_dim 64 / 128,
+ * key_block_size 16, page_rows a multiple of 128 (fb_block_mass_paged: q_rows
+ * <= 128); rows of the last page past n_ext must hold finite values.
+ * Workspace: fb_block_mass_workspace_bytes_ex / fb_sparse_workspace_bytes. */
+FB_API int fb_block_mass_paged(int dtype, const void* q, const void* k_pages, const void* k_in,
+                               int64_t num_pages, int64_t page_rows, const int32_t* page_table,
+                               int64_t max_pages, int64_t groups, int64_t q_rows, int64_t head_dim,
+                               int64_t n_ext, int64_t n_in, int64_t key_block_size, double scale,
+                               double* mass, void* workspace, size_t workspace_bytes, void* stream);
+FB_API int fb_sparse_partitioned_paged(int dtype, const void* q, const void* k_pages,
+                                       const void* v_pages, const void* k_in, const void* v_in,
+                                       int64_t num_pages, int64_t page_rows,
+                                       const int32_t* page_table, int64_t max_pages, int64_t groups,
+                                       int64_t q_rows, int64_t head_dim, int64_t n_ext, int64_t n_in,
+                                       const int32_t* selected, int64_t n_sel,
+                                       int64_t key_block_size, double scale, void* o_sel,
+                                       void* lse_sel, void* o_res, void* lse_res, void* out,
+                                       int out_dtype, int32_t* empty_rows, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+FB_API int fb_sparse_attend_merge_paged(int dtype, const void* q, const void* k_pages,
+                                        const void* v_pages, const void* k_in, const void* v_in,
+                                        int64_t num_pages, int64_t page_rows,
+                                        const int32_t* page_table, int64_t max_pages, int64_t groups,
+                                        int64_t q_rows, int64_t head_dim, int64_t n_ext, int64_t n_in,
+                                        const int32_t* selected, int64_t n_sel,
+                                        int64_t key_block_size, double scale, const void* o_res,
+                                        const void* lse_res, void* out, int out_dtype,
+                                        int32_t* empty_rows, void* workspace,
+                                        size_t workspace_bytes, void* stream);
 /* Paged block commit: rows lengths[g] .. lengths[g] + block_rows - 1 of group
  * g go to their pages (rows past the table or onto a negative page id are
  * dropped and counted in *overflow); lengths advance by block_rows. */

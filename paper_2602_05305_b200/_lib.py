@@ -51,6 +51,14 @@ SIGNATURES = {
     "fb_paged_workspace_bytes": (sz, [i32, i64, i64, i64]),
     "fb_block_causal_attention_paged": (i32, [i32, vp, vp, vp, i64, i64, vp, i64, i64, i64, i64, i64,
                                               i64, i64, dbl, vp, vp, vp, sz, vp]),
+    "fb_block_mass_paged": (i32, [i32, vp, vp, vp, i64, i64, vp, i64, i64, i64, i64, i64, i64, i64,
+                                  dbl, vp, vp, sz, vp]),
+    "fb_sparse_partitioned_paged": (i32, [i32, vp, vp, vp, vp, vp, i64, i64, vp, i64, i64, i64, i64,
+                                          i64, i64, vp, i64, i64, dbl, vp, vp, vp, vp, vp, i32, vp, vp,
+                                          sz, vp]),
+    "fb_sparse_attend_merge_paged": (i32, [i32, vp, vp, vp, vp, vp, i64, i64, vp, i64, i64, i64, i64,
+                                           i64, i64, vp, i64, i64, dbl, vp, vp, vp, i32, vp, vp, sz,
+                                           vp]),
     "fb_commit_block_paged": (i32, [i32, vp, vp, i64, vp, i64, i64, i64, vp, vp, i64, vp, vp, vp]),
     "fb_internal_merge": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, i32, vp,
                                 vp, vp, vp, vp, sz, vp]),

@@ -634,6 +634,79 @@ int fb_block_causal_attention_paged(int dtype, const void* q, const void* k_page
       reinterpret_cast<float*>(lse_out), workspace, workspace_bytes, as_stream(stream));
 }
 
+// ---- sparse path over a paged cache: the bf16 tcgen05 kernels with the page
+// translation (PagingCtx) active for the duration of the call
+static int paged_sparse_check(int dtype, int64_t head_dim, int64_t kbs, int64_t page_rows,
+                              const int32_t* table, int64_t max_pages, int64_t n_ext) {
+  if (dtype != FB_BF16 || !sm100_supported(head_dim) || kbs != 16)
+    return fail(FB_ERR_UNSUPPORTED, "paged sparse path: bf16, head_dim 64 / 128, key_block_size 16");
+  if (page_rows <= 0 || page_rows % 128 != 0)
+    return fail(FB_ERR_UNSUPPORTED, "page_rows must be a positive multiple of 128");
+  if (table == nullptr) return fail(FB_ERR_VALUE, "page_table (device int32) is required");
+  if (n_ext < 0 || n_ext > max_pages * page_rows) return fail(FB_ERR_SHAPE, "n_ext outside the pages");
+  return FB_OK;
+}
+
+int fb_block_mass_paged(int dtype, const void* q, const void* k_pages, const void* k_in,
+                        int64_t num_pages, int64_t page_rows, const int32_t* page_table,
+                        int64_t max_pages, int64_t groups, int64_t q_rows, int64_t head_dim,
+                        int64_t n_ext, int64_t n_in, int64_t key_block_size, double scale,
+                        double* mass, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = paged_sparse_check(dtype, head_dim, key_block_size, page_rows, page_table, max_pages, n_ext))
+    return rc;
+  if (!score_sm100_supported(head_dim, q_rows, key_block_size))
+    return fail(FB_ERR_UNSUPPORTED, "paged block mass: q_rows <= 128");
+  if (workspace_bytes < score_sm100_workspace_bytes(groups, q_rows, n_ext, n_in))
+    return fail(FB_ERR_VALUE, "workspace too small (fb_block_mass_workspace_bytes_ex)");
+  const PagingCtx pc{page_table, max_pages, page_rows, num_pages};
+  ScopedPaging guard(&pc);
+  return fb_block_mass(dtype, q, k_pages, k_in, groups, q_rows, head_dim, max_pages * page_rows, n_ext,
+                       n_in, key_block_size, scale, mass, workspace, workspace_bytes, stream);
+}
+
+int fb_sparse_partitioned_paged(int dtype, const void* q, const void* k_pages, const void* v_pages,
+                                const void* k_in, const void* v_in, int64_t num_pages,
+                                int64_t page_rows, const int32_t* page_table, int64_t max_pages,
+                                int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_ext,
+                                int64_t n_in, const int32_t* selected, int64_t n_sel,
+                                int64_t key_block_size, double scale, void* o_sel, void* lse_sel,
+                                void* o_res, void* lse_res, void* out, int out_dtype,
+                                int32_t* empty_rows, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  if (int rc = paged_sparse_check(dtype, head_dim, key_block_size, page_rows, page_table, max_pages, n_ext))
+    return rc;
+  if (workspace_bytes < fb_sparse_workspace_bytes(dtype, groups, q_rows, head_dim, n_ext, n_sel, n_in,
+                                                  key_block_size))
+    return fail(FB_ERR_VALUE, "workspace too small (fb_sparse_workspace_bytes)");
+  const PagingCtx pc{page_table, max_pages, page_rows, num_pages};
+  ScopedPaging guard(&pc);
+  return fb_sparse_partitioned(dtype, q, k_pages, v_pages, k_in, v_in, groups, q_rows, head_dim,
+                               max_pages * page_rows, n_ext, n_in, selected, n_sel, key_block_size,
+                               scale, o_sel, lse_sel, o_res, lse_res, out, out_dtype, empty_rows,
+                               workspace, workspace_bytes, stream);
+}
+
+int fb_sparse_attend_merge_paged(int dtype, const void* q, const void* k_pages, const void* v_pages,
+                                 const void* k_in, const void* v_in, int64_t num_pages,
+                                 int64_t page_rows, const int32_t* page_table, int64_t max_pages,
+                                 int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_ext,
+                                 int64_t n_in, const int32_t* selected, int64_t n_sel,
+                                 int64_t key_block_size, double scale, const void* o_res,
+                                 const void* lse_res, void* out, int out_dtype, int32_t* empty_rows,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = paged_sparse_check(dtype, head_dim, key_block_size, page_rows, page_table, max_pages, n_ext))
+    return rc;
+  if (workspace_bytes < fb_sparse_workspace_bytes(dtype, groups, q_rows, head_dim, n_ext, n_sel, n_in,
+                                                  key_block_size))
+    return fail(FB_ERR_VALUE, "workspace too small (fb_sparse_workspace_bytes)");
+  const PagingCtx pc{page_table, max_pages, page_rows, num_pages};
+  ScopedPaging guard(&pc);
+  return fb_sparse_attend_merge(dtype, q, k_pages, v_pages, k_in, v_in, groups, q_rows, head_dim,
+                                max_pages * page_rows, n_ext, n_in, selected, n_sel, key_block_size,
+                                scale, o_res, lse_res, out, out_dtype, empty_rows, workspace,
+                                workspace_bytes, stream);
+}
+
 int fb_commit_block_paged(int dtype, void* k_pages, void* v_pages, int64_t page_rows,
                           const int32_t* page_table, int64_t max_pages, int64_t groups,
                           int64_t head_dim, const void* k_block, const void* v_block,

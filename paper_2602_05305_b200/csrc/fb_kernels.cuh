@@ -92,6 +92,19 @@ int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const _
 
 // Ragged per-group key ends (device int32 [groups], clamped to kv_rows_cap).
 size_t refresh_sm100_ragged_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim);
+// Paging context for the sparse path (K5 / K7 / K8) over a paged cache: set
+// for the duration of one fb_*_paged call on the calling thread (re-entrant
+// across threads), read by launch_score_sm100 / launch_gather_sm100 to build
+// tensor maps over the page pool and translate block rows through the table.
+struct PagingCtx {
+  const int32_t* table;
+  int64_t max_pages, page_rows, num_pages;
+};
+const PagingCtx* current_paging();
+struct ScopedPaging {
+  explicit ScopedPaging(const PagingCtx* p);
+  ~ScopedPaging();
+};
 int launch_refresh_paged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_pages,
                                const __nv_bfloat16* v_pages, int64_t num_pages, int64_t page_rows,
                                const int32_t* page_table, int64_t max_pages, int64_t groups,

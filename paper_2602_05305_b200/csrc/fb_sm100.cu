@@ -312,11 +312,21 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                                  &bar->v_full[s], b * BOX_COLS, row, slab, stream);
             }
           } else if (lt < ga.sel_tiles) {
-            int rows[8];
+            int rows[8], slabs[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int e = lt * 8 + i;
               rows[i] = e < ga.n_list ? __ldg(ga.list + (long long)g * ga.n_list + e) * 16 : ga.n_ext;
+              slabs[i] = g;
+              if (pg.table != nullptr) {  // paged cache: block -> (page, row); none -> past a page
+                if (e < ga.n_list) {
+                  slabs[i] = __ldg(pg.table + (long long)g * pg.max_pages + rows[i] / pg.page_rows);
+                  rows[i] %= pg.page_rows;
+                } else {
+                  slabs[i] = 0;
+                  rows[i] = pg.page_rows;
+                }
+              }
             }
             if (do_k) {
               ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
@@ -325,7 +335,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                   ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
-                                   &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], g, stream);
+                                   &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], slabs[i], stream);
             }
             if (do_v) {
               ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
@@ -334,7 +344,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                   ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
-                                   &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], g, stream);
+                                   &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], slabs[i], stream);
             }
           } else {
             const int row = (lt - ga.sel_tiles) * BN;
@@ -928,7 +938,7 @@ constexpr int SCORE_THREADS = 384;  // 4 control warps + 2 score warpgroups
 template <int D, bool MASS>
 __global__ void __launch_bounds__(SCORE_THREADS, 1)
 score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-             const __grid_constant__ CUtensorMap tm_ki, Sched sc, int q_rows, int n_ext, int n_in,
+             const __grid_constant__ CUtensorMap tm_ki, Paged pg, Sched sc, int q_rows, int n_ext, int n_in,
              int ext_tiles, float scale_log2, const float* __restrict__ lse2_in,
              float* __restrict__ lse2_out, float* __restrict__ ws_l, double* __restrict__ mass,
              int nb) {
@@ -981,12 +991,17 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
           const int s = j % C::STAGES;
           const int lt = (int)(t - (long long)item * sc.tpi);
           const bool ext = lt < ext_tiles;
-          const int row = ext ? lt * BN : (lt - ext_tiles) * BN;
+          int row = ext ? lt * BN : (lt - ext_tiles) * BN;
+          int slab = g;
+          if (ext && pg.table != nullptr) {  // paged cache: the tile's page, row inside it
+            slab = __ldg(pg.table + (long long)g * pg.max_pages + row / pg.page_rows);
+            row %= pg.page_rows;
+          }
           ptx::mbar_wait(&bar->k_empty[s], ((j / C::STAGES) & 1) ^ 1);
           ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
           for (int b = 0; b < C::NBOX; ++b)
             ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES,
-                             ext ? &tm_k : &tm_ki, &bar->k_full[s], b * BOX_COLS, row, g, stream);
+                             ext ? &tm_k : &tm_ki, &bar->k_full[s], b * BOX_COLS, row, slab, stream);
         }
       }
     }
@@ -1381,6 +1396,11 @@ static int pair_mode() {  // 0 never, 1 always, 2 block-causal only
   }
   return m;
 }
+static thread_local const PagingCtx* t_paging = nullptr;
+const PagingCtx* current_paging() { return t_paging; }
+ScopedPaging::ScopedPaging(const PagingCtx* p) { t_paging = p; }
+ScopedPaging::~ScopedPaging() { t_paging = nullptr; }
+
 static int g_pair_override = -1;
 void set_pair_enabled(int on) { g_pair_override = on; }
 static long long g_pair_launches = 0;
@@ -1535,8 +1555,15 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   } else {
     // cache rows [0, n_ext) in 16-row boxes; current block [0, n_in) in 128-row boxes
     const int64_t n_ext_eff = gs->n_ext > 0 ? gs->n_ext : 1;
-    if ((rc = make_tmap_3d(&mk, k, 2, D, n_ext_eff, kv_rows_cap, groups, sm100::BOX_COLS, 16))) return rc;
-    if ((rc = make_tmap_3d(&mv, v, 2, D, n_ext_eff, kv_rows_cap, groups, sm100::BOX_COLS, 16))) return rc;
+    if (const PagingCtx* pc = current_paging()) {  // page pool [num_pages, page_rows, D]
+      if ((rc = make_tmap_3d(&mk, k, 2, D, pc->page_rows, pc->page_rows, pc->num_pages, sm100::BOX_COLS, 16)))
+        return rc;
+      if ((rc = make_tmap_3d(&mv, v, 2, D, pc->page_rows, pc->page_rows, pc->num_pages, sm100::BOX_COLS, 16)))
+        return rc;
+    } else {
+      if ((rc = make_tmap_3d(&mk, k, 2, D, n_ext_eff, kv_rows_cap, groups, sm100::BOX_COLS, 16))) return rc;
+      if ((rc = make_tmap_3d(&mv, v, 2, D, n_ext_eff, kv_rows_cap, groups, sm100::BOX_COLS, 16))) return rc;
+    }
     if (gs->n_in > 0) {
       if ((rc = make_tmap_3d(&mki, gs->k_in, 2, D, gs->n_in, gs->n_in, groups, sm100::BOX_COLS, sm100::BN))) return rc;
       if ((rc = make_tmap_3d(&mvi, gs->v_in, 2, D, gs->n_in, gs->n_in, groups, sm100::BOX_COLS, sm100::BN))) return rc;
@@ -1655,7 +1682,11 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     }
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
-  const sm100::Paged pgv = paged ? *paged : sm100::Paged{nullptr, 0, 1};
+  sm100::Paged pgv = paged ? *paged : sm100::Paged{nullptr, 0, 1};
+  if (GATHER && current_paging() != nullptr) {
+    const PagingCtx* pc = current_paging();
+    pgv = sm100::Paged{pc->table, (int)pc->max_pages, (int)pc->page_rows};
+  }
   launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
              pgv, cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
              ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr, flags);
@@ -1828,7 +1859,16 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   CUtensorMap mq, mk, mki;
   int rc;
   if ((rc = make_tmap_3d(&mq, q, 2, D, q_rows, q_rows, groups, sm100::BOX_COLS, sm100::BM))) return rc;
-  if ((rc = make_tmap_3d(&mk, k, 2, D, n_ext, cap, groups, sm100::BOX_COLS, sm100::BN))) return rc;
+  const PagingCtx* pc = current_paging();
+  if (pc != nullptr) {  // page pool [num_pages, page_rows, D]
+    if ((rc = make_tmap_3d(&mk, k, 2, D, pc->page_rows, pc->page_rows, pc->num_pages, sm100::BOX_COLS,
+                           sm100::BN)))
+      return rc;
+  } else if ((rc = make_tmap_3d(&mk, k, 2, D, n_ext, cap, groups, sm100::BOX_COLS, sm100::BN))) {
+    return rc;
+  }
+  const sm100::Paged pgv = pc ? sm100::Paged{pc->table, (int)pc->max_pages, (int)pc->page_rows}
+                              : sm100::Paged{nullptr, 0, 1};
   if (n_in > 0) {
     if ((rc = make_tmap_3d(&mki, k_in, 2, D, n_in, n_in, groups, sm100::BOX_COLS, sm100::BN))) return rc;
   } else {
@@ -1852,7 +1892,7 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   if (ws_bytes < lse_bytes + p.ws_bytes) return fail(FB_ERR_VALUE, "score workspace too small");
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};
   launch_pdl(sm100::score_kernel<D, false>, dim3((unsigned)p.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
-             st, mq, mk, mki, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
+             st, mq, mk, mki, pgv, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
              (const float*)nullptr, lse2, ws_l, (double*)nullptr, (int)nb);
   count_launch();
   if ((rc = check_launch("score_kernel<lse>"))) return rc;
@@ -1867,7 +1907,7 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   RefreshPlan pm = plan_refresh(groups, q_rows, 0, (int64_t)ext_tiles * 128);
   sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.items, pm.ctas, nullptr};
   launch_pdl(sm100::score_kernel<D, true>, dim3((unsigned)pm.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
-             st, mq, mk, mki, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
+             st, mq, mk, mki, pgv, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
              (const float*)lse2, (float*)nullptr, (float*)nullptr, mass, (int)nb);
   count_launch();
   return check_launch("score_kernel<mass>");

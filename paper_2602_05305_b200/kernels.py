@@ -509,12 +509,23 @@ def mask_budget(n_ext: int, density: float, key_block_size: int) -> int:
     return int(_lib.load().fb_mask_budget(int(n_ext), float(density), int(key_block_size)))
 
 
-def block_mass(q, k, k_in, n_ext: int, key_block_size: int = 16, scale: float | None = None):
-    """K5: float64 softmax mass per external key block, summed over each group's rows."""
+def _paged_table(page_table, groups):
+    t = page_table.reshape(groups, -1)
+    if t.dtype != torch.int32:
+        t = t.to(torch.int32)
+    return t.contiguous()
+
+
+def block_mass(q, k, k_in, n_ext: int, key_block_size: int = 16, scale: float | None = None, *,
+               page_table=None):
+    """K5: float64 softmax mass per external key block, summed over each group's rows.
+    With page_table ([groups, max_pages] int32), k is a page pool
+    [num_pages, page_rows, d] read through the table (paged serving cache)."""
     q3, k3, ki3 = _as3(q, "q").contiguous(), _as3(k, "k").contiguous(), _as3(k_in, "k_in").contiguous()
     require_cuda(q3, k3, ki3)
     groups, q_rows, d = q3.shape
-    if k3.shape[0] != groups or k3.shape[2] != d or ki3.shape[0] != groups or ki3.shape[2] != d:
+    if (page_table is None and k3.shape[0] != groups) or k3.shape[2] != d or ki3.shape[0] != groups \
+            or ki3.shape[2] != d:
         raise ShapeError("q and keys must be 2-D with matching feature dim")
     code = dtype_code(q3)
     nb = -(-int(n_ext) // int(key_block_size))
@@ -523,6 +534,13 @@ def block_mass(q, k, k_in, n_ext: int, key_block_size: int = 16, scale: float | 
                                                        ki3.shape[1], int(key_block_size))
     ws = WORKSPACE.get(q3.device, wsb)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if page_table is not None:
+        require_cuda(page_table)
+        t = _paged_table(page_table, groups)
+        _lib.call("fb_block_mass_paged", code, _p(q3), _p(k3), _p(ki3), k3.shape[0], k3.shape[1], _p(t),
+                  t.shape[1], groups, q_rows, d, int(n_ext), ki3.shape[1], int(key_block_size), scale,
+                  _p(mass), _p(ws), ws.numel(), _stream(q3))
+        return mass
     _lib.call("fb_block_mass", code, _p(q3), _p(k3), _p(ki3), groups, q_rows, d, k3.shape[1],
               int(n_ext), ki3.shape[1], int(key_block_size), scale, _p(mass), _p(ws), ws.numel(),
               _stream(q3))
@@ -540,15 +558,17 @@ def topk_blocks(mass: torch.Tensor, budget: int) -> torch.Tensor:
 
 def sparse_partitioned(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
                        key_block_size: int = 16, scale: float | None = None,
-                       out_dtype: torch.dtype | None = None, check: bool = False):
-    """K7: first sparse step -- (out, selected partial, residual partial)."""
+                       out_dtype: torch.dtype | None = None, check: bool = False, *, page_table=None):
+    """K7: first sparse step -- (out, selected partial, residual partial).
+    With page_table, k / v are page pools read through it (see block_mass)."""
     q3, k3, v3 = _as3(q, "q").contiguous(), _as3(k, "k").contiguous(), _as3(v, "v").contiguous()
     ki3, vi3 = _as3(k_in, "k_in").contiguous(), _as3(v_in, "v_in").contiguous()
     require_cuda(q3, k3, v3, ki3, vi3, selected)
-    _check_kv(q3, k3, v3)
+    if page_table is None:
+        _check_kv(q3, k3, v3)
     _check_kv(q3, ki3, vi3)
     groups, q_rows, d = q3.shape
-    if k3.shape[1] < n_ext:
+    if page_table is None and k3.shape[1] < n_ext:
         raise ShapeError(f"key set has {k3.shape[1]} rows but mask covers {n_ext} external keys")
     sel = selected.reshape(groups, -1).to(torch.int32).contiguous()
     code = dtype_code(q3)
@@ -564,26 +584,35 @@ def sparse_partitioned(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
     wsb = _lib.load().fb_sparse_workspace_bytes(code, groups, q_rows, d, int(n_ext), sel.shape[1],
                                                 ki3.shape[1], int(key_block_size))
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_sparse_partitioned", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
-              q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
-              int(key_block_size), scale, _p(o_sel), _p(l_sel), _p(o_res), _p(l_res), _p(out),
-              _OUT_CODE[out_dtype], _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
+    if page_table is not None:
+        t = _paged_table(page_table, groups)
+        _lib.call("fb_sparse_partitioned_paged", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3),
+                  k3.shape[0], k3.shape[1], _p(t), t.shape[1], groups, q_rows, d, int(n_ext),
+                  ki3.shape[1], _p(sel), sel.shape[1], int(key_block_size), scale, _p(o_sel), _p(l_sel),
+                  _p(o_res), _p(l_res), _p(out), _OUT_CODE[out_dtype], _p(cnt), _p(ws),
+                  0 if ws is None else ws.numel(), _stream(q3))
+    else:
+        _lib.call("fb_sparse_partitioned", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
+                  q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
+                  int(key_block_size), scale, _p(o_sel), _p(l_sel), _p(o_res), _p(l_res), _p(out),
+                  _OUT_CODE[out_dtype], _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
     _raise_if_empty(cnt, "sparse_partitioned")
     return out, (o_sel, l_sel), (o_res, l_res)
 
 
 def sparse_attend_merge(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
                         residual=None, key_block_size: int = 16, scale: float | None = None,
-                        out_dtype: torch.dtype | None = None, check: bool = False):
+                        out_dtype: torch.dtype | None = None, check: bool = False, *, page_table=None):
     """K8: later sparse steps -- selected blocks + current block, merged with
     the cached residual (or renormalised sparse-only when residual is None)."""
     q3, k3, v3 = _as3(q, "q").contiguous(), _as3(k, "k").contiguous(), _as3(v, "v").contiguous()
     ki3, vi3 = _as3(k_in, "k_in").contiguous(), _as3(v_in, "v_in").contiguous()
     require_cuda(q3, k3, v3, ki3, vi3, selected)
-    _check_kv(q3, k3, v3)
+    if page_table is None:
+        _check_kv(q3, k3, v3)
     _check_kv(q3, ki3, vi3)
     groups, q_rows, d = q3.shape
-    if k3.shape[1] < n_ext:
+    if page_table is None and k3.shape[1] < n_ext:
         raise ShapeError(f"key set has {k3.shape[1]} rows but mask covers {n_ext} external keys")
     sel = selected.reshape(groups, -1).to(torch.int32).contiguous()
     code = dtype_code(q3)
@@ -600,9 +629,17 @@ def sparse_attend_merge(q, k, v, k_in, v_in, n_ext: int, selected: torch.Tensor,
     wsb = _lib.load().fb_sparse_workspace_bytes(code, groups, q_rows, d, int(n_ext), sel.shape[1],
                                                 ki3.shape[1], int(key_block_size))
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_sparse_attend_merge", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
-              q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
-              int(key_block_size), scale, _p(o_res), _p(l_res), _p(out), _OUT_CODE[out_dtype],
-              _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
+    if page_table is not None:
+        t = _paged_table(page_table, groups)
+        _lib.call("fb_sparse_attend_merge_paged", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3),
+                  k3.shape[0], k3.shape[1], _p(t), t.shape[1], groups, q_rows, d, int(n_ext),
+                  ki3.shape[1], _p(sel), sel.shape[1], int(key_block_size), scale, _p(o_res), _p(l_res),
+                  _p(out), _OUT_CODE[out_dtype], _p(cnt), _p(ws), 0 if ws is None else ws.numel(),
+                  _stream(q3))
+    else:
+        _lib.call("fb_sparse_attend_merge", code, _p(q3), _p(k3), _p(v3), _p(ki3), _p(vi3), groups,
+                  q_rows, d, k3.shape[1], int(n_ext), ki3.shape[1], _p(sel), sel.shape[1],
+                  int(key_block_size), scale, _p(o_res), _p(l_res), _p(out), _OUT_CODE[out_dtype],
+                  _p(cnt), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
     _raise_if_empty(cnt, "sparse_attend_merge")
     return out

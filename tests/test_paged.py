@@ -169,3 +169,39 @@ def test_paged_api_errors():
     blk = torch.ones((2, 32, d), device="cuda", dtype=torch.bfloat16)
     with pytest.raises(BoundsError):
         K.commit_block_paged(pool, pool, table, blk, blk, lengths, check=True)  # 250 + 32 > 2 pages
+
+
+@pytest.mark.parametrize("n_ext,page_rows", [(4101, 256), (2048, 128)])
+def test_paged_sparse_path_equals_contiguous_bitwise(n_ext, page_rows):
+    """The sparse path over a paged cache -- K5 block masses, K6 selection, K7
+    first step (selected + residual) and K8 cached step -- equals the same
+    calls on contiguous slabs bit for bit (pages shuffled over the pool)."""
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(n_ext)
+    groups, rows, d, n_in = 4, 128, 128, 32
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    q, ki, vi = r(groups, rows, d), r(groups, n_in, d), r(groups, n_in, d)
+    cap = -(-n_ext // page_rows) * page_rows
+    k, v = r(groups, cap, d), r(groups, cap, d)
+    mp = cap // page_rows
+    perm = torch.randperm(groups * mp, generator=torch.Generator().manual_seed(3)).cuda()
+    table = perm.view(groups, mp).to(torch.int32).contiguous()
+    kp = torch.empty((groups * mp, page_rows, d), device="cuda", dtype=torch.bfloat16)
+    vp = torch.empty_like(kp)
+    kp[perm] = k.view(groups * mp, page_rows, d)
+    vp[perm] = v.view(groups * mp, page_rows, d)
+    m_c = K.block_mass(q, k, ki, n_ext, 16)
+    m_p = K.block_mass(q, kp, ki, n_ext, 16, page_table=table)
+    assert torch.equal(m_c, m_p)
+    sel = K.topk_blocks(m_c, K.mask_budget(n_ext, 0.2, 16))
+    out_c, sel_c, res_c = K.sparse_partitioned(q, k, v, ki, vi, n_ext, sel, out_dtype=torch.float32)
+    out_p, sel_p, res_p = K.sparse_partitioned(q, kp, vp, ki, vi, n_ext, sel, out_dtype=torch.float32,
+                                               page_table=table)
+    assert torch.equal(out_c, out_p)
+    assert torch.equal(res_c[0], res_p[0]) and torch.equal(res_c[1], res_p[1])
+    q2 = r(groups, rows, d)
+    a = K.sparse_attend_merge(q2, k, v, ki, vi, n_ext, sel, res_c, out_dtype=torch.float32)
+    b = K.sparse_attend_merge(q2, kp, vp, ki, vi, n_ext, sel, res_p, out_dtype=torch.float32,
+                              page_table=table)
+    assert torch.equal(a, b)
