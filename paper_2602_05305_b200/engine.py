@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import torch
 
 from . import kernels as K
-from .errors import BoundsError, ReusePreconditionError, ShapeError
+from .errors import BoundsError, ReusePreconditionError, ShapeError, StalenessError
 from .policy import Decision, ReuseConfig, decide
 
 
@@ -217,6 +217,59 @@ class FlashBlockAttention:
         res, _ = K.block_causal_attention_paged(qg, cache.k[layer], cache.v[layer], cache.table[layer], n_q,
                                                 n_prefix, self.B, self.scale, out=o, lse=lse)
         return res.view(b, hq, n_q, d)
+
+    # -- sparse + residual reuse (sparse.py:83-183), batched over the engine's groups
+    def sparse_first_step(self, layer: int, q, k_cache, v_cache, n_ext: int, k_in, v_in,
+                          density: float, key_block_size: int = 16, out=None):
+        """First step of a block with the sparse variant: K5 + K6 select the
+        top-k external key blocks per kv group (pooled over the group's rows,
+        build_sparse_mask, sparse.py:83-136), K7 computes the exact partition
+        (selected + current block, and the residual over the unselected
+        blocks, sparse.py:166-175) and the output; the selection and the
+        residual partial are kept for `layer`'s later steps.  k_cache may be a
+        PagedKVCache (v_cache ignored; uniform n_ext).  Returns out
+        [b, Hq, B, d]."""
+        qg, kg, vg = self._groups(q, k_in, v_in)
+        kc, vc, pt = self._sparse_kv(layer, k_cache, v_cache)
+        budget = K.mask_budget(int(n_ext), density, key_block_size)
+        mass = K.block_mass(qg, kc, kg, int(n_ext), key_block_size, self.scale, page_table=pt)
+        sel = K.topk_blocks(mass, budget)
+        res, _, resid = K.sparse_partitioned(qg, kc, vc, kg, vg, int(n_ext), sel, key_block_size,
+                                             self.scale, self.out_dtype, page_table=pt)
+        if not hasattr(self, "_sparse"):
+            self._sparse = {}
+        self._sparse[layer] = (sel, resid, int(n_ext), key_block_size, self.block_id)
+        self._count_rows(self.b * self.hkv * int(n_ext))
+        if out is not None:
+            out.view(res.shape).copy_(res)
+            return out
+        return res.view(self.b, self.hq, self.B, self.d)
+
+    def sparse_cached_step(self, layer: int, q, k_cache, v_cache, k_in, v_in, out=None):
+        """Later steps: K8 attends the stored selected blocks + the current
+        block with the current queries and merges the cached residual
+        (sparse.py:177-183).  StalenessError when `layer` has no residual for
+        this block (sparse.py:177-181)."""
+        st = getattr(self, "_sparse", {}).get(layer)
+        if st is None or st[4] != self.block_id:
+            raise StalenessError(f"no residual for layer {layer} in block {self.block_id}")
+        sel, resid, n_ext, kbs, _ = st
+        qg, kg, vg = self._groups(q, k_in, v_in)
+        kc, vc, pt = self._sparse_kv(layer, k_cache, v_cache)
+        res = K.sparse_attend_merge(qg, kc, vc, kg, vg, n_ext, sel, resid, kbs, self.scale,
+                                    self.out_dtype, page_table=pt)
+        self._count_rows(self.b * self.hkv * sel.shape[-1] * kbs)
+        if out is not None:
+            out.view(res.shape).copy_(res)
+            return out
+        return res.view(self.b, self.hq, self.B, self.d)
+
+    def _sparse_kv(self, layer: int, k_cache, v_cache):
+        if isinstance(k_cache, PagedKVCache):
+            return k_cache.k[layer], k_cache.v[layer], k_cache.table[layer]
+        kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
+        vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+        return kc, vc, None
 
     def step_gated(self, layer: int, q, k_cache, v_cache, n_ext: int, k_in, v_in, *,
                    first_visit: bool, updated_tokens: int, gates, out=None):

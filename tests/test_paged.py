@@ -205,3 +205,39 @@ def test_paged_sparse_path_equals_contiguous_bitwise(n_ext, page_rows):
     b = K.sparse_attend_merge(q2, kp, vp, ki, vi, n_ext, sel, res_p, out_dtype=torch.float32,
                               page_table=table)
     assert torch.equal(a, b)
+
+
+def test_engine_sparse_steps_contiguous_and_paged():
+    """FlashBlockAttention.sparse_first_step / sparse_cached_step (K5+K6+K7,
+    then K8 with the stored residual) give the same bits on a contiguous
+    KVCache and on a PagedKVCache holding the same rows; at full density the
+    first step equals the dense refresh (exact partition); a new block without
+    a first step raises StalenessError (sparse.py:177-181)."""
+    from paper_2602_05305_b200 import FlashBlockAttention, KVCache, PagedKVCache
+    from paper_2602_05305_b200.errors import StalenessError
+
+    g = torch.Generator(device="cuda").manual_seed(31)
+    b, hq, hkv, blk, d, n_ext = 2, 8, 2, 32, 128, 1536
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    paged = PagedKVCache(1, b, hkv, num_pages=32, page_rows=256, head_dim=d, max_pages_per_slab=8)
+    flat = KVCache(1, b, hkv, capacity=8 * 256, head_dim=d)
+    for _ in range(n_ext // 256):
+        kb, vb = r(b, hkv, 256, d), r(b, hkv, 256, d)
+        paged.commit_block(0, kb, vb)
+        flat.commit_block(0, kb, vb)
+    q, ki, vi = r(b, hq, blk, d), r(b, hkv, blk, d), r(b, hkv, blk, d)
+    e1 = FlashBlockAttention(1, b, hq, hkv, blk, d, out_dtype=torch.float32)
+    e2 = FlashBlockAttention(1, b, hq, hkv, blk, d, out_dtype=torch.float32)
+    o1 = e1.sparse_first_step(0, q, flat.k[0], flat.v[0], n_ext, ki, vi, density=0.25)
+    o2 = e2.sparse_first_step(0, q, paged, None, n_ext, ki, vi, density=0.25)
+    assert torch.equal(o1, o2)
+    q2 = r(b, hq, blk, d)
+    c1 = e1.sparse_cached_step(0, q2, flat.k[0], flat.v[0], ki, vi)
+    c2 = e2.sparse_cached_step(0, q2, paged, None, ki, vi)
+    assert torch.equal(c1, c2)
+    dense = e1.refresh(0, q, flat.k[0], flat.v[0], n_ext, ki, vi)
+    full = e2.sparse_first_step(0, q, paged, None, n_ext, ki, vi, density=1.0)
+    assert ((full - dense).abs().max() / dense.abs().max()).item() <= 5e-3
+    e1.begin_block(1)
+    with pytest.raises(StalenessError):
+        e1.sparse_cached_step(0, q2, flat.k[0], flat.v[0], ki, vi)
