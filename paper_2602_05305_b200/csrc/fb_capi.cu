@@ -503,6 +503,8 @@ FB_API void fb_debug_set_trace(void* device_buffer) { set_refresh_trace(device_b
 FB_API void fb_debug_set_k1_diag(int diag) { set_k1_diag(diag); }
 FB_API void fb_debug_set_pair(int on) { set_pair_enabled(on); }
 FB_API int64_t fb_debug_pair_launches(void) { return (int64_t)pair_launches(); }
+FB_API void fb_debug_set_quad(int m) { set_quad_mode(m); }
+FB_API int64_t fb_debug_quad_launches(void) { return (int64_t)quad_launches(); }
 FB_API void fb_debug_set_k2_variant(int v) { set_k2_v2(v); }
 FB_API void fb_debug_set_k2_trace(void* p, int launches) { set_k2_trace(p, launches); }
 int64_t fb_launch_count(void) { return g_launches.load(); }

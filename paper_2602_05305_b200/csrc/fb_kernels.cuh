@@ -80,6 +80,8 @@ void set_refresh_trace(void* p);
 void set_k1_diag(int d);
 void set_pair_enabled(int on);  // -1 default (env FB_PAIR; block-causal only), 0 off, 1 all shapes
 long long pair_launches();       // CTA-pair K1 launches so far (diagnostics)
+void set_quad_mode(int m);        // two-query-tile K1: -1 default (causal), 0 off, 1 all shapes
+long long quad_launches();
 void set_k2_trace(void* p, int launches);  // diagnostics: K2 v1 per-CTA stamps
 void set_k2_v2(int v);           // K2 variant: -1 by size (default), 0 v1, 1 v2 (diagnostics)
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);

@@ -901,6 +901,7 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
 }
 
 #include "fb_sm100_pair.cuh"  // K1 on CTA pairs (tensor-bound shapes)
+#include "fb_sm100_quad.cuh"  // K1 with two query tiles per CTA (experimental)
 
 // ---------------------------------------------------------------- K5 scoring
 //
@@ -1270,6 +1271,7 @@ void set_refresh_trace(void* p) {
 }
 
 static int pair_clusters();
+static bool quad_enabled();
 
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys) {
   if (n_keys <= 0 || groups <= 0 || q_rows <= 0) return 0;
@@ -1279,6 +1281,10 @@ size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t hea
                         ((n_keys + sm100::BN - 1) / sm100::BN);
     const long long pairs = std::min<long long>(pair_clusters(), T);
     b = std::max<size_t>(b, (size_t)2 * pairs * sm100::pair::PM * (head_dim + 1) * sizeof(float));
+    if (quad_enabled()) {
+      const long long qc = std::min<long long>(num_sms(), T);
+      b = std::max<size_t>(b, (size_t)2 * qc * sm100::pair::PM * (head_dim + 1) * sizeof(float));
+    }
   }
   return b;
 }
@@ -1521,6 +1527,88 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   return check_launch("refresh_merge_kernel(sm100, pair)");
 }
 
+// Two-query-tile K1 (fb_sm100_quad.cuh).  Default: block-causal prefill
+// (32K prompt 7.72 ms vs 8.67 on CTA pairs and 9.5 single-CTA); the
+// non-causal C5 refresh keeps the single-CTA kernel (1.65 vs 1.53 ms -- the
+// 256-row stream-K ranges drift off the lock-step L2 reuse, as the pair's do).
+// FB_K1_QUAD=0 / 1: never / every shape with > 128 query rows (diagnostics);
+// fb_debug_set_quad overrides (tests).
+static int g_quad_override = -1;
+void set_quad_mode(int m) { g_quad_override = m; }
+static long long g_quad_launches = 0;
+long long quad_launches() { return g_quad_launches; }
+static int quad_mode() {  // 0 never, 1 always, 2 block-causal only
+  if (g_quad_override >= 0) return g_quad_override;
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("FB_K1_QUAD");
+    m = e == nullptr ? 2 : (e[0] == '0' ? 0 : 1);
+  }
+  return m;
+}
+static bool quad_enabled() { return quad_mode() != 0; }
+
+static int launch_quad_128(const __nv_bfloat16* k, const CUtensorMap& mq, const CUtensorMap& mk,
+                           const CUtensorMap& mv, int64_t groups, int64_t q_rows, int64_t key_begin,
+                           int64_t key_end, double scale, float* o_out, float* lse_out, void* ws,
+                           size_t ws_bytes, cudaStream_t st, const sm100::Causal* causal,
+                           const int32_t* glist, int64_t n_list, const MergeFinal* fin,
+                           const sm100::Paged* paged) {
+  constexpr int D = 128;
+  using Q = sm100::quad::QCfg<D>;
+  const sm100::Paged pgv = paged ? *paged : sm100::Paged{nullptr, 0, 1};
+  constexpr int PM = sm100::pair::PM;
+  const int m_tiles = (int)((q_rows + PM - 1) / PM);
+  const int items = (int)((glist ? n_list : groups) * m_tiles);
+  const long long tpi = (key_end - key_begin + sm100::BN - 1) / sm100::BN;
+  if (items <= 0 || tpi <= 0) return -1;
+  if (causal && fin != nullptr) return -1;
+  sm100::Causal cz{1, 0, 0};
+  if (causal) cz = *causal;
+  sm100::Sched sc{(long long)items * tpi, (int)tpi, m_tiles, items, 0, nullptr, glist};
+  sc.kv_keep = m_tiles > 1 && kv_keep_enabled();
+  float* ws_o = nullptr;
+  float* ws_l = nullptr;
+  bool need_merge;
+  if (causal) {
+    sc.rr = 1;
+    sc.tpi = 0;
+    sc.ctas = std::min(num_sms(), items);
+    need_merge = false;
+  } else {
+    sc.ctas = (int)std::min<long long>(num_sms(), sc.T);
+    need_merge = !(sc.T % sc.ctas == 0 && (sc.T / sc.ctas) % tpi == 0);
+    const bool split = need_merge;
+    if (fin != nullptr) need_merge = true;
+    if (split) {
+      const size_t need = (size_t)2 * sc.ctas * PM * (D + 1) * sizeof(float);
+      if (ws == nullptr || ws_bytes < need) return -1;
+      ws_o = reinterpret_cast<float*>(ws);
+      ws_l = ws_o + (size_t)2 * sc.ctas * PM * D;
+    }
+  }
+  auto kern = sm100::quad::quad_kernel<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
+    attr = true;
+  }
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  int rc;
+  launch_pdl(kern, dim3((unsigned)sc.ctas), dim3(sm100::THREADS), Q::SMEM, st, mq, mk, mv, pgv, cz, sc,
+             (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l);
+  count_launch();
+  ++g_quad_launches;
+  if ((rc = check_launch("quad_kernel(sm100)"))) return rc;
+  if (!need_merge) return FB_OK;
+  const long long warps = (long long)items * PM;
+  launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
+             (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, PM,
+             fin ? *fin : MergeFinal{});
+  count_launch();
+  return check_launch("refresh_merge_kernel(sm100, quad)");
+}
+
 template <int D, bool GATHER>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
@@ -1577,6 +1665,16 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ga.n_in = (int)gs->n_in;
     ga.sel_tiles = (int)((gs->n_list + 7) / 8);
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
+  }
+  if constexpr (!GATHER && D == 128) {
+    const int qm = quad_mode();
+    const bool pair_forced = (g_pair_override >= 0 ? g_pair_override : pair_mode()) == 1;
+    const bool quad_on = !pair_forced && (qm == 1 || (qm == 2 && causal != nullptr));
+    if (quad_on && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
+      const int qrc = launch_quad_128(k, mq, mk, mv, groups, q_rows, key_begin, key_end, scale, o_out, lse_out,
+                                      ws, ws_bytes, st, causal, glist, n_list, fin, paged);
+      if (qrc != -1) return qrc;
+    }
   }
   if constexpr (!GATHER && D == 128) {
     const int pm = g_pair_override >= 0 ? g_pair_override : pair_mode();
