@@ -241,6 +241,20 @@ FB_API int fb_sparse_attend_merge_paged(int dtype, const void* q, const void* k_
                                         const void* lse_res, void* out, int out_dtype,
                                         int32_t* empty_rows, void* workspace,
                                         size_t workspace_bytes, void* stream);
+/* Cached step (K2) on token-major tensors: q [batch, block, num_q_heads,
+ * head_dim], k_in / v_in [batch, block, num_kv_heads, head_dim] given by their
+ * token strides in elements (e.g. views into one fused QKV projection output
+ * [batch * block, (Hq + 2 Hkv) * d]), output written token-major with
+ * out_token_stride (the O projection's input [batch * block, Hq * d]); the
+ * cached external partial keeps the stacked [batch * Hkv, G * block, d]
+ * layout.  Same arithmetic as fb_internal_merge_ex; bf16, head_dim 128,
+ * G * block <= 128, block <= 64. */
+FB_API int fb_internal_merge_tok(int dtype, const void* q, int64_t q_token_stride, const void* k_in,
+                                 int64_t k_token_stride, const void* v_in, int64_t v_token_stride,
+                                 int64_t batch, int64_t block, int64_t num_q_heads,
+                                 int64_t num_kv_heads, int64_t head_dim, double scale,
+                                 const void* o_ext, const void* lse_ext, void* out, int out_dtype,
+                                 int64_t out_token_stride, int flags, void* stream);
 /* Paged block commit: rows lengths[g] .. lengths[g] + block_rows - 1 of group
  * g go to their pages (rows past the table or onto a negative page id are
  * dropped and counted in *overflow); lengths advance by block_rows. */

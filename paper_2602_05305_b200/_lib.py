@@ -59,6 +59,8 @@ SIGNATURES = {
     "fb_sparse_attend_merge_paged": (i32, [i32, vp, vp, vp, vp, vp, i64, i64, vp, i64, i64, i64, i64,
                                            i64, i64, vp, i64, i64, dbl, vp, vp, vp, i32, vp, vp, sz,
                                            vp]),
+    "fb_internal_merge_tok": (i32, [i32, vp, i64, vp, i64, vp, i64, i64, i64, i64, i64, i64, dbl, vp, vp,
+                                    vp, i32, i64, i32, vp]),
     "fb_commit_block_paged": (i32, [i32, vp, vp, i64, vp, i64, i64, i64, vp, vp, i64, vp, vp, vp]),
     "fb_internal_merge": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, i32, vp,
                                 vp, vp, vp, vp, sz, vp]),

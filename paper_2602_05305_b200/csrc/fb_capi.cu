@@ -709,6 +709,26 @@ int fb_sparse_attend_merge_paged(int dtype, const void* q, const void* k_pages, 
                                 workspace_bytes, stream);
 }
 
+int fb_internal_merge_tok(int dtype, const void* q, int64_t q_token_stride, const void* k_in,
+                          int64_t k_token_stride, const void* v_in, int64_t v_token_stride,
+                          int64_t batch, int64_t block, int64_t num_q_heads, int64_t num_kv_heads,
+                          int64_t head_dim, double scale, const void* o_ext, const void* lse_ext,
+                          void* out, int out_dtype, int64_t out_token_stride, int flags, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (dtype != FB_BF16) return fail(FB_ERR_UNSUPPORTED, "token-major cached step: bf16");
+  if (out_dtype != FB_BF16 && out_dtype != FB_F32) return fail(FB_ERR_VALUE, "BF16 mode writes F32 or BF16 output");
+  if (flags & ~FB_EXT_STABLE) return fail(FB_ERR_VALUE, "unknown flags");
+  if (batch < 0 || block < 1 || num_q_heads < 1 || num_kv_heads < 1) return fail(FB_ERR_SHAPE, "bad extents");
+  if (num_q_heads % num_kv_heads) return fail(FB_ERR_SHAPE, "num_q_heads must be a multiple of num_kv_heads");
+  if (batch == 0) return FB_OK;
+  return launch_internal_merge_tok_sm100(
+      reinterpret_cast<const __nv_bfloat16*>(q), q_token_stride, reinterpret_cast<const __nv_bfloat16*>(k_in),
+      k_token_stride, reinterpret_cast<const __nv_bfloat16*>(v_in), v_token_stride, batch, block, num_q_heads,
+      num_kv_heads, head_dim, scale, reinterpret_cast<const float*>(o_ext),
+      reinterpret_cast<const float*>(lse_ext), out, out_token_stride, out_dtype == FB_BF16,
+      (flags & FB_EXT_STABLE) != 0, as_stream(stream));
+}
+
 int fb_commit_block_paged(int dtype, void* k_pages, void* v_pages, int64_t page_rows,
                           const int32_t* page_table, int64_t max_pages, int64_t groups,
                           int64_t head_dim, const void* k_block, const void* v_block,

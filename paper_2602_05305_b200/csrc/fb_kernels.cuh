@@ -163,6 +163,11 @@ int launch_score_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __n
                        cudaStream_t st);
 
 bool sm100_k2_supported(int64_t head_dim, int64_t n_in);
+int launch_internal_merge_tok_sm100(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat16* k,
+                                    int64_t k_ts, const __nv_bfloat16* v, int64_t v_ts, int64_t batch,
+                                    int64_t B, int64_t Hq, int64_t Hkv, int64_t d, double scale,
+                                    const float* o_ext, const float* lse_ext, void* out, int64_t out_ts,
+                                    bool out_bf16, bool ext_early, cudaStream_t st);
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,
                                 const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
                                 int64_t head_dim, int64_t n_in, double scale, const float* o_ext,

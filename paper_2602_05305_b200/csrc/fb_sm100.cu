@@ -1218,6 +1218,28 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t in
   return FB_OK;
 }
 
+// N-D bf16 view (rank 2..5): dims[0] = contiguous elements, byte strides for
+// dims 1..rank-1, 128B-swizzled box.  Out-of-bounds boxes read as zero.
+int make_tmap_nd(CUtensorMap* map, const void* base, int rank, const int64_t* dims,
+                 const int64_t* stride_bytes, const int* box) {
+  auto enc = sm100::get_encode();
+  if (!enc) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    bx[i] = (cuuint32_t)box[i];
+    es[i] = 1;
+    if (i > 0) st[i - 1] = (cuuint64_t)stride_bytes[i];
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled (nd) failed: " + std::to_string((int)r));
+  return FB_OK;
+}
+
 bool sm100_supported(int64_t head_dim) { return head_dim == 64 || head_dim == 128; }
 
 // diagnostics: per-CTA globaltimer stamps (set through fb_debug_set_trace)

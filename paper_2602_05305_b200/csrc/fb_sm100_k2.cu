@@ -64,10 +64,19 @@ struct Bars {
   uint32_t tmem_base;
 };
 
+// Token-major layout (TOK): Q / K_in / V_in are strided views of a QKV
+// projection output [b * B, ...] and the output is written token-major
+// ([b * B, out_ts], head h of kv group kvh at columns (kvh * G + h) * D), so
+// the attention layer needs no head-major copies around its GEMMs.
+struct TokLayout {
+  int B, G, Hkv;
+  long long out_ts;  // output token stride (elements)
+};
+
 #ifndef FB_K2_MIN_BLOCKS
 #define FB_K2_MIN_BLOCKS 2  // diagnostics build knob
 #endif
-template <int D, int NT, int SPLIT, bool TRACE = false>
+template <int D, int NT, int SPLIT, bool TRACE = false, bool TOK = false>
 __global__ void __launch_bounds__(THREADS, FB_K2_MIN_BLOCKS)  // (3 CTAs/SM at 136 regs: 8 % slower, C2 b=16)
 internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ o_ext,
@@ -75,7 +84,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                       float scale_log2, void* __restrict__ out, int out_bf16,
                       float* __restrict__ lse_merged, float* __restrict__ o_int,
                       float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early,
-                      unsigned long long* __restrict__ trace) {
+                      unsigned long long* __restrict__ trace, TokLayout tl) {
   using C = Cfg<D, NT, SPLIT>;
   // diagnostics (TRACE): per-CTA globaltimer stamps, 8 per CTA
   auto stamp = [&](int i) {
@@ -99,6 +108,12 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const int grow = mt * BM + row;
   const bool live_row = warp < 4 && grow < q_rows;
   const long long rr = (long long)g * q_rows + grow;
+  // output row offset (elements): stacked [groups, q_rows, D] or token-major
+  long long orr = rr * D;
+  if constexpr (TOK) {
+    const int bi = g / tl.Hkv, kvh = g % tl.Hkv, hh = grow / tl.B, tt = grow % tl.B;
+    orr = (long long)(bi * tl.B + tt) * tl.out_ts + (long long)(kvh * tl.G + hh) * D;
+  }
 
   // this thread's row of the cached external partial (its column slice)
   float le = -INFINITY;
@@ -142,13 +157,25 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   if (warp == 4) {
     if (lane == 0) {
       const uint64_t pol = ptx::policy_evict_first();
-      ptx::mbar_expect_tx(&bar->load_qkv, C::TX_QKV);
-      for (int b = 0; b < C::NB; ++b) {
-        ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
-        ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
+      // (TOK: the Q box holds G * B rows, not BM, so fewer bytes land)
+      ptx::mbar_expect_tx(&bar->load_qkv, TOK ? C::TX_QKV - C::NB * (uint32_t)(BM - tl.B * tl.G) * 128u
+                                              : C::TX_QKV);
+      if constexpr (TOK) {  // 5-D Q {d, B, G, Hkv, b}, 4-D K / V {d, B, Hkv, b}
+        const int bi = g / tl.Hkv, kvh = g % tl.Hkv;
+        for (int b = 0; b < C::NB; ++b) {
+          ptx::tma_load_5d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, 0, 0, kvh, bi, pol);
+          ptx::tma_load_4d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, kvh, bi, pol);
+        }
+        for (int b = 0; b < C::NBV; ++b)
+          ptx::tma_load_4d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, kvh, bi, pol);
+      } else {
+        for (int b = 0; b < C::NB; ++b) {
+          ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
+          ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
+        }
+        for (int b = 0; b < C::NBV; ++b)
+          ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, g, pol);
       }
-      for (int b = 0; b < C::NBV; ++b)
-        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, g, pol);
 
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, C::DC, true);
@@ -269,7 +296,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       }
       if (live_row) {
         if (out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * D + col0 + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + orr + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             dst[j] = make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]),
@@ -277,7 +304,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                                 ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]),
                                 ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
         } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * D + col0 + c * 32);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + orr + col0 + c * 32);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             dst[j] = make_float4(val[4 * j], val[4 * j + 1], val[4 * j + 2], val[4 * j + 3]);
@@ -604,7 +631,7 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles * C::SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st,
              mq, mk, mv, o_ext, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
              out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
-             ext_early ? 1 : 0, trace);
+             ext_early ? 1 : 0, trace, sm100k2::TokLayout{1, 1, 1, 0});
   count_launch();
   return check_launch("internal_merge_kernel(sm100)");
 }
@@ -636,6 +663,70 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
              lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), ext_early ? 1 : 0);
   count_launch();
   return check_launch("internal_merge_v2_kernel(sm100)");
+}
+
+int make_tmap_nd(CUtensorMap* map, const void* base, int rank, const int64_t* dims,
+                 const int64_t* stride_bytes, const int* box);
+
+// Token-major cached step (TokLayout): q / k_in / v_in are [batch, B, H, d]
+// views with token strides q_ts / k_ts / v_ts (elements; e.g. the row pitch of
+// a fused QKV projection output) and the output is [batch, B, Hq, d] with
+// token stride out_ts.  d = 128, G * B <= 128, B <= 64.
+template <int NT>
+static int launch_k2_tok(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat16* k, int64_t k_ts,
+                         const __nv_bfloat16* v, int64_t v_ts, int64_t batch, int64_t B, int64_t Hq,
+                         int64_t Hkv, double scale, const float* o_ext, const float* lse_ext, void* out,
+                         int64_t out_ts, bool out_bf16, bool ext_early, cudaStream_t st) {
+  constexpr int D = 128, SPLIT = 2;
+  using C = sm100k2::Cfg<D, NT, SPLIT>;
+  const int64_t G = Hq / Hkv;
+  CUtensorMap mq, mk, mv;
+  int rc;
+  {
+    const int64_t dims[5] = {D, B, G, Hkv, batch};
+    const int64_t str[5] = {2, q_ts * 2, D * 2, G * D * 2, B * q_ts * 2};
+    const int box[5] = {sm100k2::BOX, (int)B, (int)G, 1, 1};
+    if ((rc = make_tmap_nd(&mq, q, 5, dims, str, box))) return rc;
+  }
+  {
+    const int64_t dims[4] = {D, B, Hkv, batch};
+    const int64_t sk[4] = {2, k_ts * 2, D * 2, B * k_ts * 2};
+    const int64_t sv[4] = {2, v_ts * 2, D * 2, B * v_ts * 2};
+    const int box[4] = {sm100k2::BOX, NT, 1, 1};
+    if ((rc = make_tmap_nd(&mk, k, 4, dims, sk, box))) return rc;
+    if ((rc = make_tmap_nd(&mv, v, 4, dims, sv, box))) return rc;
+  }
+  auto kern = sm100k2::internal_merge_kernel<D, NT, SPLIT, false, true>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const int64_t groups = batch * Hkv, q_rows = G * B;
+  const float scale_log2 = (float)(scale * 1.4426950408889634);
+  launch_pdl(kern, dim3((unsigned)(groups * SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st, mq, mk, mv, o_ext,
+             lse_ext, (int)q_rows, 1, (int)B, scale_log2, out, out_bf16 ? 1 : 0, (float*)nullptr,
+             (float*)nullptr, (float*)nullptr, (int*)nullptr, ext_early ? 1 : 0,
+             (unsigned long long*)nullptr, sm100k2::TokLayout{(int)B, (int)G, (int)Hkv, (long long)out_ts});
+  count_launch();
+  return check_launch("internal_merge_kernel(sm100, token-major)");
+}
+
+int launch_internal_merge_tok_sm100(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat16* k,
+                                    int64_t k_ts, const __nv_bfloat16* v, int64_t v_ts, int64_t batch,
+                                    int64_t B, int64_t Hq, int64_t Hkv, int64_t d, double scale,
+                                    const float* o_ext, const float* lse_ext, void* out, int64_t out_ts,
+                                    bool out_bf16, bool ext_early, cudaStream_t st) {
+  if (d != 128 || Hkv <= 0 || Hq % Hkv != 0 || (Hq / Hkv) * B > 128 || B < 1 || B > 64)
+    return fail(FB_ERR_UNSUPPORTED, "token-major cached step: d 128, (Hq/Hkv)*B <= 128, 1 <= B <= 64");
+  if (B <= 16)
+    return launch_k2_tok<16>(q, q_ts, k, k_ts, v, v_ts, batch, B, Hq, Hkv, scale, o_ext, lse_ext, out, out_ts,
+                             out_bf16, ext_early, st);
+  if (B <= 32)
+    return launch_k2_tok<32>(q, q_ts, k, k_ts, v, v_ts, batch, B, Hq, Hkv, scale, o_ext, lse_ext, out, out_ts,
+                             out_bf16, ext_early, st);
+  return launch_k2_tok<64>(q, q_ts, k, k_ts, v, v_ts, batch, B, Hq, Hkv, scale, o_ext, lse_ext, out, out_ts,
+                           out_bf16, ext_early, st);
 }
 
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,

@@ -174,6 +174,30 @@ class FlashBlockAttention:
                                self.out_dtype, out=o, ext_stable=True)
         return res.view(self.b, self.hq, self.B, self.d)
 
+    # -- token-major variants: q / k_in / v_in as [b, B, H, d] views of a fused
+    # QKV projection output and the output token-major for the O projection,
+    # so the attention layer needs no head-major copies on cached steps
+    def cached_tokmajor(self, layer: int, q_tok, k_tok, v_tok, out_tok):
+        """cached() on token-major tensors (fb_internal_merge_tok)."""
+        if not self.valid[layer]:
+            raise ReusePreconditionError(f"no valid cached external partial for layer {layer}")
+        K.internal_merge_tok(q_tok, k_tok, v_tok, self.o_ext[layer], self.lse_ext[layer], out_tok, self.scale,
+                             ext_stable=True)
+        return out_tok
+
+    def refresh_tokmajor(self, layer: int, q_tok, k_cache, v_cache, n_ext: int, k_tok, v_tok, out_tok):
+        """refresh() on token-major tensors: K1 on a head-major copy of the
+        queries (one copy per refresh step), K2 token-major."""
+        q = q_tok.permute(0, 2, 1, 3).contiguous()
+        qg = K.gqa_view(q, self.hkv)
+        kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
+        vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+        self._count_rows(self.b * self.hkv * int(n_ext))
+        K.attention_partial(qg, kc, vc, 0, int(n_ext), self.scale, out=self.o_ext[layer], lse=self.lse_ext[layer])
+        K.internal_merge_tok(q_tok, k_tok, v_tok, self.o_ext[layer], self.lse_ext[layer], out_tok, self.scale)
+        self.valid[layer] = True
+        return out_tok
+
     def step(self, layer: int, q, k_cache, v_cache, n_ext, k_in, v_in, *,
              first_visit: bool, updated_tokens: int, out=None):
         """Route one layer through the reuse policy (simulator.py:412-434)."""

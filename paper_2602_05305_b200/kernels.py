@@ -437,6 +437,36 @@ def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
     return tuple(res)
 
 
+def _tok_stride(t: torch.Tensor, name: str) -> int:
+    """Token stride of a token-major [b, B, H, d] view (heads x d contiguous)."""
+    if t.dim() != 4 or t.stride(-1) != 1 or t.stride(-2) != t.shape[-1] \
+            or t.stride(0) != t.shape[1] * t.stride(1):
+        raise ShapeError(f"{name} must be a token-major [b, B, H, d] view with contiguous heads x d")
+    return t.stride(1)
+
+
+def internal_merge_tok(q_tok, k_tok, v_tok, o_ext, lse_ext, out_tok, scale: float | None = None,
+                       ext_stable: bool = False):
+    """K2 on token-major tensors (fb_internal_merge_tok): q_tok [b, B, Hq, d],
+    k_tok / v_tok [b, B, Hkv, d] (views into a fused QKV projection output),
+    out_tok [b, B, Hq, d] (the O projection's input); o_ext / lse_ext keep the
+    stacked [b*Hkv, G*B, d] layout.  Same arithmetic as internal_merge."""
+    require_cuda(q_tok, k_tok, v_tok, o_ext, lse_ext, out_tok)
+    b, B, hq, d = q_tok.shape
+    hkv = k_tok.shape[2]
+    if k_tok.shape != (b, B, hkv, d) or v_tok.shape != k_tok.shape or out_tok.shape != q_tok.shape:
+        raise ShapeError("token-major q / k / v / out shapes do not line up")
+    qs, ks, vs, os_ = (_tok_stride(q_tok, "q"), _tok_stride(k_tok, "k_in"), _tok_stride(v_tok, "v_in"),
+                       _tok_stride(out_tok, "out"))
+    if o_ext.dtype != torch.float32 or o_ext.numel() != b * hq * B * d or lse_ext.numel() != b * hq * B:
+        raise ShapeError("cached partial does not match the queries")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    _lib.call("fb_internal_merge_tok", _CODE[q_tok.dtype], _p(q_tok), qs, _p(k_tok), ks, _p(v_tok), vs, b, B,
+              hq, hkv, d, scale, _p(o_ext), _p(lse_ext), _p(out_tok), _OUT_CODE[out_tok.dtype], os_,
+              _lib.FB_EXT_STABLE if ext_stable else 0, _stream(q_tok))
+    return out_tok
+
+
 def combine(parts, out_dtype: torch.dtype | None = None, want_lse: bool = True,
             check: bool = False):
     """K3: log-space merge of partials [(o, lse), ...] over disjoint key groups."""

@@ -102,6 +102,20 @@ def c2layer(out):
             eng.full_recompute(q, kc[l], vc[l], N, ki, vi, out=att[l], o_scratch=o_scr, lse_scratch=l_scr)
         torch.matmul(att[l].permute(0, 2, 1, 3).reshape(b * B, DM), wo[l].t(), out=y[l])
 
+    att_tok = [torch.empty(b * B, DM, device=DEV, dtype=torch.bfloat16) for _ in range(L)]
+
+    def layer_tok(l, mode):
+        # token-major: attention reads q / k / v straight out of the QKV GEMM's
+        # output and writes the O GEMM's input; no head-major copies
+        torch.matmul(x[l], wqkv[l], out=qkv[l])
+        t = qkv[l].view(b, B, HQ + 2 * HKV, D)
+        q, ki, vi, o = t[:, :, :HQ], t[:, :, HQ:HQ + HKV], t[:, :, HQ + HKV:], att_tok[l].view(b, B, HQ, D)
+        if mode == "refresh":
+            eng.refresh_tokmajor(l, q, kc[l], vc[l], N, ki, vi, o)
+        else:
+            eng.cached_tokmajor(l, q, ki, vi, o)
+        torch.matmul(att_tok[l], wo[l].t(), out=y[l])
+
     eng.begin_block(0)
     for l in range(L):
         layer(l, "refresh")
@@ -110,7 +124,10 @@ def c2layer(out):
     t_full = graph_ms(lambda: [layer(l, "full") for l in range(L)], reps=3) / L
     t_gemm = graph_ms(lambda: [(proj_in(l), torch.matmul(att[l].permute(0, 2, 1, 3).reshape(b * B, DM),
                                                          wo[l].t(), out=y[l])) for l in range(L)], reps=3) / L
+    t_ref_tok = graph_ms(lambda: [layer_tok(l, "refresh") for l in range(L)], reps=3) / L
+    t_cac_tok = graph_ms(lambda: [layer_tok(l, "cached") for l in range(L)], reps=3) / L
     fb_block = t_ref + 31 * t_cac
+    tok_block = t_ref_tok + 31 * t_cac_tok
     full_block = 32 * t_full
     emit(out, {"config": "C2-layer", "batch": b, "ctx": N, "d_model": DM, "q_heads": HQ, "kv_heads": HKV,
                "layer_refresh_ms": t_ref, "layer_cached_ms": t_cac, "layer_full_recompute_ms": t_full,
@@ -118,6 +135,9 @@ def c2layer(out):
                "tokens_per_s_36_layers": b * B / (36 * fb_block * 1e-3),
                "full_recompute_tokens_per_s_36_layers": b * B / (36 * full_block * 1e-3),
                "speedup_vs_full_recompute": full_block / fb_block,
+               "token_major": {"layer_refresh_ms": t_ref_tok, "layer_cached_ms": t_cac_tok,
+                               "tokens_per_s_36_layers": b * B / (36 * tok_block * 1e-3),
+                               "speedup_vs_full_recompute": full_block / tok_block},
                "note": "per layer: QKV GEMM + attention + O GEMM (cuBLAS projections, random-init "
                        "weights); block = 1 refresh + 31 cached steps (tau=2 schedule)"})
     del kc, vc
