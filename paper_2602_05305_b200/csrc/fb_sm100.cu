@@ -738,34 +738,61 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 }
 
-// Weighted sum of a row's split partials for the 4 columns at c, segments in
-// order (same arithmetic as a plain loop), with up to 8 segments' loads in
-// flight per lane instead of one dependent load per segment.  Items of a b=1
-// split-KV shard span ~16 CTAs: C3 b=1 refresh P=1/2/8 3/6/11 % faster.
-__device__ __forceinline__ float4 sum_segments(const Sched& sc, int item, int row, int bm, int D,
-                                               int c, int c_first, int nseg, float mx,
-                                               const float* __restrict__ ws_o,
-                                               const float* __restrict__ ws_l) {
+// A row's split partials, merged in segment order: max and sum of the
+// weights exp(L_k - max) and the weighted sum of the 4 columns at lane*4.
+// Lane u resolves segment k0 + u's workspace row (two 64-bit divisions) once
+// per 32-segment chunk and broadcasts it by shuffle; every lane then keeps 8
+// segments' loads in flight.  (Resolving every segment in every lane cost
+// ~100 dependent 64-bit divisions per lane: the C3 b=1 merge took 16 us.)
+// Same arithmetic and order as a plain per-segment loop.
+__device__ __forceinline__ long long seg_row(const Sched& sc, int item, int row, int bm, int c) {
+  const long long s0 = sc.start(c), s1 = sc.start(c + 1);
+  if (s1 <= s0) return -1;  // CTAs with empty ranges hold no partial
+  return (2ll * c + (sc.item_begin(item) <= s0 ? 0 : 1)) * bm + row;
+}
+
+__device__ __forceinline__ float4 merge_segments(const Sched& sc, int item, int row, int bm, int D,
+                                                 int c_first, int nseg, const float* __restrict__ ws_o,
+                                                 const float* __restrict__ ws_l, int lane, float& mx_out,
+                                                 float& z_out) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int c = lane * 4;
+  const bool col = c < D;
+  float mx = -INFINITY;
+  for (int k0 = 0; k0 < nseg; k0 += 32) {
+    const long long sl = k0 + lane < nseg ? seg_row(sc, item, row, bm, c_first + k0 + lane) : -1;
+    if (sl >= 0) mx = fmaxf(mx, ws_l[sl]);
+  }
+  mx = warp_max(mx);
+  float z = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k0 = 0; k0 < nseg; k0 += 8) {
-    float w[8];
-    float4 v[8];
+  for (int k0 = 0; k0 < nseg; k0 += 32) {
+    const long long sl = k0 + lane < nseg ? seg_row(sc, item, row, bm, c_first + k0 + lane) : -1;
+    const float w = sl >= 0 ? __expf(ws_l[sl] - mx) : 0.f;
+    z += w;
+    const int n = min(32, nseg - k0);
+    for (int u0 = 0; u0 < n; u0 += 8) {
+      float wu[8];
+      float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = k0 + u;
-      w[u] = 0.f;
-      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k < nseg && sc.start(c_first + k + 1) > sc.start(c_first + k)) {
-        const long long sl = sc.slot(c_first + k, item) * bm + row;
-        w[u] = __expf(ws_l[sl] - mx);
-        v[u] = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
+      for (int u = 0; u < 8; ++u) {
+        const long long su = __shfl_sync(FULL, sl, u0 + u);
+        wu[u] = __shfl_sync(FULL, w, u0 + u);
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u0 + u < n && su >= 0) {
+          if (col) v[u] = *reinterpret_cast<const float4*>(ws_o + su * D + c);
+        } else {
+          wu[u] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x += wu[u] * v[u].x; acc.y += wu[u] * v[u].y; acc.z += wu[u] * v[u].z; acc.w += wu[u] * v[u].w;
       }
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      acc.x += w[u] * v[u].x; acc.y += w[u] * v[u].y; acc.z += w[u] * v[u].z; acc.w += w[u] * v[u].w;
-    }
   }
+  mx_out = mx;
+  z_out = warp_sum(z);
   return acc;
 }
 
@@ -796,26 +823,10 @@ __device__ __forceinline__ void final_merge_row(const Sched& sc, int item, int r
     if (col) pv = *reinterpret_cast<const float4*>(o_k1 + orow * D + c);
   } else {
     const int nseg = c_last - c_first + 1;
-    auto has = [&](int cc) { return sc.start(cc + 1) > sc.start(cc); };
-    float mx = -INFINITY;
-    for (int k = lane; k < nseg; k += 32)
-      if (has(c_first + k)) mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * bm + row]);
-    mx = warp_max(mx);
-    float z = 0.f;
-    for (int k = lane; k < nseg; k += 32)
-      if (has(c_first + k)) z += __expf(ws_l[sc.slot(c_first + k, item) * bm + row] - mx);
-    z = warp_sum(z);
+    float mx, z;
+    pv = merge_segments(sc, item, row, bm, D, c_first, nseg, ws_o, ws_l, lane, mx, z);
     const float iz = 1.f / z;
     if (col) {
-      // (a plain loop: sum_segments measured 2-4 % slower on this K7/K8 path,
-      // whose items span only ~5 CTAs)
-      for (int k = 0; k < nseg; ++k) {
-        if (!has(c_first + k)) continue;
-        const long long sl = sc.slot(c_first + k, item) * bm + row;
-        const float w = __expf(ws_l[sl] - mx);
-        const float4 v = *reinterpret_cast<const float4*>(ws_o + sl * D + c);
-        pv.x += w * v.x; pv.y += w * v.y; pv.z += w * v.z; pv.w += w * v.w;
-      }
       pv = make_float4(pv.x * iz, pv.y * iz, pv.z * iz, pv.w * iz);
       *reinterpret_cast<float4*>(o_k1 + orow * D + c) = pv;
     }
@@ -881,22 +892,12 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   const int c_last = sc.cta_of(ie - 1);
   if (c_first == c_last) return;  // written whole by its CTA
   const int nseg = c_last - c_first + 1;
-  // CTAs with empty ranges (more CTAs than tiles, ragged plans) hold no partial
-  auto has = [&](int c) { return sc.start(c + 1) > sc.start(c); };
-  float mx = -INFINITY;
-  for (int k = lane; k < nseg; k += 32)
-    if (has(c_first + k)) mx = fmaxf(mx, ws_l[sc.slot(c_first + k, item) * bm + row]);
-  mx = warp_max(mx);
-  float z = 0.f;
-  for (int k = lane; k < nseg; k += 32)
-    if (has(c_first + k)) z += __expf(ws_l[sc.slot(c_first + k, item) * bm + row] - mx);
-  z = warp_sum(z);
+  float mx, z;
+  const float4 acc = merge_segments(sc, item, row, bm, D, c_first, nseg, ws_o, ws_l, lane, mx, z);
   const float iz = 1.f / z;
-  for (int c = lane * 4; c < D; c += 128) {
-    const float4 acc = sum_segments(sc, item, row, bm, D, c, c_first, nseg, mx, ws_o, ws_l);
-    *reinterpret_cast<float4*>(o_out + orow * D + c) =
+  if (lane * 4 < D)
+    *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) =
         make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
-  }
   if (lane == 0) lse_out[orow] = mx + logf(z);
 }
 

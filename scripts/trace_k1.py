@@ -2,7 +2,7 @@ import sys, os, ctypes, torch, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_05305_b200 import kernels as K, _lib
 lib = _lib.load(); lib.fb_debug_set_trace.argtypes = [ctypes.c_void_p]
-HKV, D, CTX = 8, 128, 32768
+HKV, D, CTX = 8, 128, int(os.environ.get("CTX", 32768))
 for b in [int(x) for x in sys.argv[1:]] or [1, 8]:
     g = torch.Generator(device="cuda").manual_seed(1)
     q = torch.randn((b * HKV, 128, D), device="cuda", generator=g).to(torch.bfloat16)
