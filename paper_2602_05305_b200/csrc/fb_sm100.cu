@@ -741,7 +741,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 // A row's split partials, merged in segment order: max and sum of the
 // weights exp(L_k - max) and the weighted sum of the 4 columns at lane*4.
 // Lane u resolves segment k0 + u's workspace row (two 64-bit divisions) once
-// per 32-segment chunk and broadcasts it by shuffle; every lane then keeps 8
+// per 32-segment chunk and broadcasts it by shuffle; every lane then keeps 16
 // segments' loads in flight.  (Resolving every segment in every lane cost
 // ~100 dependent 64-bit divisions per lane: the C3 b=1 merge took 16 us.)
 // Same arithmetic and order as a plain per-segment loop.
@@ -759,7 +759,10 @@ __device__ __forceinline__ float4 merge_segments(const Sched& sc, int item, int 
   const int c = lane * 4;
   const bool col = c < D;
   float mx = -INFINITY;
-  for (int k0 = 0; k0 < nseg; k0 += 32) {
+  const long long sl0 = lane < nseg ? seg_row(sc, item, row, bm, c_first + lane) : -1;
+  const float lk0 = sl0 >= 0 ? ws_l[sl0] : -INFINITY;  // first chunk's LSEs, kept for the sum
+  if (sl0 >= 0) mx = lk0;
+  for (int k0 = 32; k0 < nseg; k0 += 32) {
     const long long sl = k0 + lane < nseg ? seg_row(sc, item, row, bm, c_first + k0 + lane) : -1;
     if (sl >= 0) mx = fmaxf(mx, ws_l[sl]);
   }
@@ -767,17 +770,17 @@ __device__ __forceinline__ float4 merge_segments(const Sched& sc, int item, int 
   float z = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k0 = 0; k0 < nseg; k0 += 32) {
-    const long long sl = k0 + lane < nseg ? seg_row(sc, item, row, bm, c_first + k0 + lane) : -1;
-    const float w = sl >= 0 ? __expf(ws_l[sl] - mx) : 0.f;
+    const long long sl = k0 == 0 ? sl0 : k0 + lane < nseg ? seg_row(sc, item, row, bm, c_first + k0 + lane) : -1;
+    const float w = sl >= 0 ? __expf((k0 == 0 ? lk0 : ws_l[sl]) - mx) : 0.f;
     z += w;
     const int n = min(32, nseg - k0);
-    for (int u0 = 0; u0 < n; u0 += 8) {
-      float wu[8];
-      float4 v[8];
+    for (int u0 = 0; u0 < n; u0 += 16) {  // 16 segments' loads in flight
+      float wu[16];
+      float4 v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const long long su = __shfl_sync(FULL, sl, u0 + u);
-        wu[u] = __shfl_sync(FULL, w, u0 + u);
+      for (int u = 0; u < 16; ++u) {
+        const long long su = __shfl_sync(FULL, sl, (u0 + u) & 31);
+        wu[u] = __shfl_sync(FULL, w, (u0 + u) & 31);
         v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (u0 + u < n && su >= 0) {
           if (col) v[u] = *reinterpret_cast<const float4*>(ws_o + su * D + c);
@@ -786,7 +789,7 @@ __device__ __forceinline__ float4 merge_segments(const Sched& sc, int item, int 
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         acc.x += wu[u] * v[u].x; acc.y += wu[u] * v[u].y; acc.z += wu[u] * v[u].z; acc.w += wu[u] * v[u].w;
       }
     }

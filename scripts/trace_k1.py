@@ -16,6 +16,7 @@ for b in [int(x) for x in sys.argv[1:]] or [1, 8]:
         e0.record(); K.attention_partial(q, k, v); e1.record(); torch.cuda.synchronize()
     lib.fb_debug_set_trace(None)
     t = tr.view(148, 8).cpu().numpy().astype(np.int64)
+    t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     rel = lambda x: (x - t0) / 1000.0
     st = t[:, 0]; s1 = np.where(t[:, 1] > 0, t[:, 1], 0); m1 = np.where(t[:, 2] > 0, t[:, 2], 0)
