@@ -713,9 +713,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               }
             }
           }
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          ptx::st_row32(dst + c * 32, v);
         }
       }
       ptx::tc_fence_before();

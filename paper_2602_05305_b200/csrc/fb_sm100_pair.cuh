@@ -437,9 +437,7 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           for (int i = 0; i < 32; ++i)
             v[i] = (c0 != 0.f ? c0 * __uint_as_float(r[i]) : 0.f) +
                    (c1 != 0.f ? c1 * __uint_as_float(r1[i]) : 0.f);
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          ptx::st_row32(dst + c * 32, v);
         }
       }
       ptx::tc_fence_before();

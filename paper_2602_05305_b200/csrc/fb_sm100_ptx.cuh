@@ -357,6 +357,26 @@ __device__ __forceinline__ void ex2_poly2(uint64_t x2, float& p0, float& p1) {
   p1 = x1 > -127.f ? r1 : 0.f;
 }
 
+// 256-bit global store (STG.E.ENL2.256): a full 32-byte sector per request,
+// half the requests of float4 stores.  p must be 32-byte aligned.
+__device__ __forceinline__ void st_v8(float* p, float a0, float a1, float a2, float a3, float a4, float a5,
+                                      float a6, float a7) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(a0), "f"(a1),
+               "f"(a2), "f"(a3), "f"(a4), "f"(a5), "f"(a6), "f"(a7)
+               : "memory");
+}
+
+// 32 consecutive floats of a row: 256-bit stores when aligned, else float4
+__device__ __forceinline__ void st_row32(float* p, const float* v) {
+  if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) st_v8(p + i, v[i], v[i + 1], v[i + 2], v[i + 3], v[i + 4], v[i + 5], v[i + 6], v[i + 7]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  }
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));

@@ -305,11 +305,10 @@ quad_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         ptx::tmem_ld32(tmem + lane_off + o_col + c * 32, r);
         ptx::tmem_wait_ld();
         if (dst != nullptr) {
+          float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + i) =
-                make_float4(__uint_as_float(r[i]) * iz, __uint_as_float(r[i + 1]) * iz,
-                            __uint_as_float(r[i + 2]) * iz, __uint_as_float(r[i + 3]) * iz);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * iz;
+          ptx::st_row32(dst + c * 32, v);
         }
       }
       ptx::tc_fence_before();
