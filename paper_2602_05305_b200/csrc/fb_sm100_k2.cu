@@ -121,11 +121,17 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   auto load_ext = [&]() {
     if (live_row) {
       le = __ldg(lse_ext + rr);
-      const float4* src = reinterpret_cast<const float4*>(o_ext + rr * D + col0);
+      const float* srow = o_ext + rr * D + col0;
+      if ((reinterpret_cast<uintptr_t>(srow) & 31) == 0 && C::PRE % 8 == 0) {  // 256-bit loads
 #pragma unroll
-      for (int j = 0; j < C::PRE / 4; ++j) {
-        const float4 v4 = __ldg(src + j);
-        oe[4 * j] = v4.x; oe[4 * j + 1] = v4.y; oe[4 * j + 2] = v4.z; oe[4 * j + 3] = v4.w;
+        for (int j = 0; j < C::PRE / 8; ++j) ptx::ld_v8_nc(srow + 8 * j, oe + 8 * j);
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(srow);
+#pragma unroll
+        for (int j = 0; j < C::PRE / 4; ++j) {
+          const float4 v4 = __ldg(src + j);
+          oe[4 * j] = v4.x; oe[4 * j + 1] = v4.y; oe[4 * j + 2] = v4.z; oe[4 * j + 3] = v4.w;
+        }
       }
     } else {
 #pragma unroll
@@ -296,18 +302,20 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       }
       if (live_row) {
         if (out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + orr + col0 + c * 32);
+          __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(out) + orr + col0 + c * 32;
+          uint32_t pk[16];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]),
-                                ptx::pack_bf16(val[8 * j + 2], val[8 * j + 3]),
-                                ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]),
-                                ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
+          for (int j = 0; j < 16; ++j) pk[j] = ptx::pack_bf16(val[2 * j], val[2 * j + 1]);
+          if ((reinterpret_cast<uintptr_t>(drow) & 31) == 0) {  // 256-bit stores
+            ptx::st_v8_b32(drow, pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], pk[6], pk[7]);
+            ptx::st_v8_b32(drow + 16, pk[8], pk[9], pk[10], pk[11], pk[12], pk[13], pk[14], pk[15]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(drow);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
         } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + orr + col0 + c * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(val[4 * j], val[4 * j + 1], val[4 * j + 2], val[4 * j + 3]);
+          ptx::st_row32(reinterpret_cast<float*>(out) + orr + col0 + c * 32, val);
         }
         if (o_int) {
           float4* di = reinterpret_cast<float4*>(o_int + rr * D + col0 + c * 32);
@@ -546,18 +554,20 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
       }
       if (live_row) {
         if (out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * D + c * 32);
+          __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(out) + rr * D + c * 32;
+          uint32_t pk[16];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]),
-                                ptx::pack_bf16(val[8 * j + 2], val[8 * j + 3]),
-                                ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]),
-                                ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
+          for (int j = 0; j < 16; ++j) pk[j] = ptx::pack_bf16(val[2 * j], val[2 * j + 1]);
+          if ((reinterpret_cast<uintptr_t>(drow) & 31) == 0) {  // 256-bit stores
+            ptx::st_v8_b32(drow, pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], pk[6], pk[7]);
+            ptx::st_v8_b32(drow + 16, pk[8], pk[9], pk[10], pk[11], pk[12], pk[13], pk[14], pk[15]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(drow);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
         } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * D + c * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(val[4 * j], val[4 * j + 1], val[4 * j + 2], val[4 * j + 3]);
+          ptx::st_row32(reinterpret_cast<float*>(out) + rr * D + c * 32, val);
         }
         if (o_int) {
           float4* di = reinterpret_cast<float4*>(o_int + rr * D + c * 32);

@@ -366,6 +366,20 @@ __device__ __forceinline__ void st_v8(float* p, float a0, float a1, float a2, fl
                : "memory");
 }
 
+__device__ __forceinline__ void st_v8_b32(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a0), "r"(a1),
+               "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+               : "memory");
+}
+
+// 256-bit read-only global load (LDG.E.ENL2.256.CONSTANT); p 32-byte aligned
+__device__ __forceinline__ void ld_v8_nc(const float* p, float* v) {
+  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
 // 32 consecutive floats of a row: 256-bit stores when aligned, else float4
 __device__ __forceinline__ void st_row32(float* p, const float* v) {
   if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
