@@ -688,6 +688,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       ptx::mbar_wait(&bar->o_full, seg & 1);
       ptx::tc_fence_after();
+      if (row == 0 && wg == 0 && seg == 0) stamp(5);
       uint32_t r1[32];
 #pragma unroll 1
       for (int c = wg * (D / 64); c < (wg + 1) * (D / 64); ++c) {
@@ -716,6 +717,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::st_row32(dst + c * 32, v);
         }
       }
+      if (row == 0 && wg == 0 && seg == 0) stamp(6);
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
       if (flags != nullptr && !whole && !owner) {
@@ -730,6 +732,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) stamp(7);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, TMEM_COLS);

@@ -26,3 +26,8 @@ for b in [int(x) for x in sys.argv[1:]] or [1, 8]:
           f"stream-end(seg0) min/med/max {rel(s1[s1>0].min()):.1f}/{rel(np.median(s1[s1>0])):.1f}/{rel(s1.max()):.1f}us; "
           f"merge-end(seg0) max {rel(m1.max()) if m1.max() else 0:.1f}; seg1 stream-end max {rel(s2.max()) if s2.max() else 0:.1f} "
           f"merge-end max {rel(m2.max()) if m2.max() else 0:.1f}; cta end max {rel(end.max()):.1f}us")
+    # epilogue detail (segment 0): 5 = O accumulators final, 6 = rows stored, 7 = CTA done
+    if t.shape[0] and (t[:, 5] > 0).any():
+        for k, nm in ((1, "softmax done"), (5, "o_full"), (6, "stored"), (7, "cta done")):
+            x = t[:, k][t[:, k] > 0]
+            print(f"  {nm:13s} min/med/max {rel(x.min()):.1f}/{rel(np.median(x)):.1f}/{rel(x.max()):.1f} us")
