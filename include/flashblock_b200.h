@@ -163,6 +163,14 @@ FB_API int fb_attention_partial_groups(int dtype, const void* q, const void* k, 
  * mean over the rows.  Float64 accumulation, fixed reduction order. */
 FB_API int fb_row_cosine(int dtype, const void* a, const void* b, int64_t heads, int64_t rows,
                          int64_t head_dim, double* row_cos, double* head_mean, void* stream);
+/* fb_row_cosine for the calibrator's step (policy.py:232-240 per adjacent step
+ * pair): the same statistics of a against b, then b <- a (b is the previous
+ * step's copy, in place), and *nonzero (optional int32) set to 1 if any row of
+ * a is nonzero (the all-zero-partials CalibrationError check).  One pass:
+ * 2 reads + 1 write per element. */
+FB_API int fb_row_cosine_update(int dtype, const void* a, void* b, int64_t heads, int64_t rows,
+                                int64_t head_dim, double* row_cos, double* head_mean, int32_t* nonzero,
+                                void* stream);
 /* All-pairs cosine between the rows of a later and an earlier step, per head:
  * out[heads, rows, rows], entry (i, j) = cos(later_i, earlier_j); rows with
  * norm < 1e-12 give 0 (pairwise_step_similarity, analysis.py:28-51). */

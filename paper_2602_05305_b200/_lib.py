@@ -44,6 +44,7 @@ SIGNATURES = {
     "fb_attention_partial_groups": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp, i64,
                                           dbl, vp, vp, vp, sz, vp]),
     "fb_row_cosine": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, vp]),
+    "fb_row_cosine_update": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
     "fb_pairwise_cosine": (i32, [i32, vp, vp, i64, i64, i64, vp, vp]),
     "fb_commit_block": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp, vp, vp]),
     "fb_attention_partial_paged": (i32, [i32, vp, vp, vp, i64, i64, vp, i64, i64, i64, i64, vp, dbl,

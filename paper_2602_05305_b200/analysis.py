@@ -69,6 +69,7 @@ class HeadGateCalibrator:
         self.min = torch.full((num_layers, num_q_heads), float("inf"), dtype=torch.float64, device=dev)
         self.count = [0] * num_layers
         self.signal = torch.zeros((), dtype=torch.bool, device=dev)
+        self.nonzero = torch.zeros((), dtype=torch.int32, device=dev)  # set by row_cosine_update
         self.prev: list = [None] * num_layers
 
     def begin_rollout(self) -> None:
@@ -80,14 +81,14 @@ class HeadGateCalibrator:
         x = o_ext.reshape(-1, rows_per_head, o_ext.shape[-1])
         if x.shape[0] % self.hq:
             raise ShapeError(f"{x.shape[0]} heads of rows is not a multiple of {self.hq} query heads")
-        self.signal |= (x != 0).any()
         if self.prev[layer] is not None:
-            m = K.row_cosine(x, self.prev[layer]).view(-1, self.hq)  # [b, Hq]
+            # one pass: row cosines against the previous step, prev <- x, nonzero flag
+            m = K.row_cosine_update(x, self.prev[layer], self.nonzero).view(-1, self.hq)  # [b, Hq]
             self.sum[layer] += m.sum(dim=0)
             self.min[layer] = torch.minimum(self.min[layer], m.min(dim=0).values)
             self.count[layer] += m.shape[0]
-            self.prev[layer].copy_(x)
         else:
+            self.signal |= (x != 0).any()
             self.prev[layer] = x.clone()
 
     def stats(self) -> dict:
@@ -96,6 +97,6 @@ class HeadGateCalibrator:
                 for l in range(self.L) if self.count[l] for h in range(self.hq)}
 
     def table(self, gamma: float) -> HeadGateTable:
-        if not bool(self.signal):
+        if not (bool(self.signal) or bool(self.nonzero)):
             raise CalibrationError("all recorded external partials are zero")
         return HeadGateTable.from_similarities(gamma, self.stats())

@@ -790,6 +790,21 @@ int fb_row_cosine(int dtype, const void* a, const void* b, int64_t heads, int64_
   }
 }
 
+int fb_row_cosine_update(int dtype, const void* a, void* b, int64_t heads, int64_t rows, int64_t head_dim,
+                         double* row_cos, double* head_mean, int32_t* nonzero, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (heads < 0 || rows < 0 || head_dim < 1) return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (heads == 0) return FB_OK;
+  if (row_cos == nullptr) return fail(FB_ERR_VALUE, "row_cos ([heads*rows] float64) is required");
+  cudaStream_t st = as_stream(stream);
+  switch (dtype) {
+    case FB_F64: return launch_row_cosine<double>(a, b, heads, rows, head_dim, row_cos, head_mean, st, true, nonzero);
+    case FB_F32: return launch_row_cosine<float>(a, b, heads, rows, head_dim, row_cos, head_mean, st, true, nonzero);
+    default:
+      return launch_row_cosine<__nv_bfloat16>(a, b, heads, rows, head_dim, row_cos, head_mean, st, true, nonzero);
+  }
+}
+
 int fb_pairwise_cosine(int dtype, const void* later, const void* earlier, int64_t heads, int64_t rows,
                        int64_t head_dim, double* out, void* stream) {
   if (int rc = check_dtype(dtype)) return rc;

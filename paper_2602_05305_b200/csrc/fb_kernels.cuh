@@ -178,7 +178,8 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
 // cross-step similarity (fb_similarity.cu)
 template <typename T>
 int launch_row_cosine(const void* a, const void* b, int64_t heads, int64_t rows, int64_t d,
-                      double* row_cos, double* head_mean, cudaStream_t st);
+                      double* row_cos, double* head_mean, cudaStream_t st, bool update = false,
+                      int* nonzero = nullptr);
 template <typename T>
 int launch_pairwise_cosine(const void* later, const void* earlier, int64_t heads, int64_t n,
                            int64_t d, double* out, cudaStream_t st);

@@ -25,25 +25,54 @@ __device__ __forceinline__ double ld64<double>(const double* p) { return *p; }
 // heads in parallel) -> row_cos[h*rows + r]
 template <typename T>
 __global__ void __launch_bounds__(256)
-row_cosine_kernel(const T* __restrict__ a, const T* __restrict__ b, int64_t n_rows, int64_t d,
-                  double* __restrict__ row_cos) {
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+row_cosine_kernel(const T* __restrict__ a, T* b, int64_t n_rows, int64_t d,
+                  double* __restrict__ row_cos, int update, int* __restrict__ nonzero) {
   const int lane = threadIdx.x & 31;
-  if (r >= n_rows) return;
-  const T* u = a + r * d;
-  const T* v = b + r * d;
-  double uu = 0.0, vv = 0.0, uv = 0.0;
-  for (int64_t c = lane; c < d; c += 32) {
-    const double x = ld64(u + c), y = ld64(v + c);
-    uu += x * x;
-    vv += y * y;
-    uv += x * y;
+  bool any = false;
+  // grid-stride over rows (the grid is capped at 8 blocks per SM, so the
+  // nonzero flag is written at most once per block, not once per row: one
+  // address written by every warp serialises in its L2 slice)
+  for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < n_rows; r += (int64_t)gridDim.x * 8) {
+    const T* u = a + r * d;
+    T* v = b + r * d;
+    double uu = 0.0, vv = 0.0, uv = 0.0;
+    // 128 columns per pass with all 8 loads of a lane issued before the math
+    // (same per-lane order c = lane, lane + 32, ... as a plain loop)
+    for (int64_t c0 = 0; c0 < d; c0 += 128) {
+      T xr[4], yr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t c = c0 + lane + 32 * i;
+        if (c < d) {
+          xr[i] = u[c];
+          yr[i] = v[c];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (c0 + lane + 32 * i < d) {
+          const double x = ld64(&xr[i]), y = ld64(&yr[i]);
+          uu += x * x;
+          vv += y * y;
+          uv += x * y;
+        }
+      }
+      // calibrator step (update): b becomes a for the next step's comparison,
+      // read above before written by the same thread
+      if (update) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (c0 + lane + 32 * i < d) v[c0 + lane + 32 * i] = xr[i];
+      }
+    }
+    uu = warp_sum(uu);
+    vv = warp_sum(vv);
+    uv = warp_sum(uv);
+    any |= uu != 0.0;
+    const double nu = sqrt(uu), nv = sqrt(vv);
+    if (lane == 0) row_cos[r] = (nu < ZERO_NORM_EPS || nv < ZERO_NORM_EPS) ? 0.0 : uv / (nu * nv);
   }
-  uu = warp_sum(uu);
-  vv = warp_sum(vv);
-  uv = warp_sum(uv);
-  const double nu = sqrt(uu), nv = sqrt(vv);
-  if (lane == 0) row_cos[r] = (nu < ZERO_NORM_EPS || nv < ZERO_NORM_EPS) ? 0.0 : uv / (nu * nv);
+  if (nonzero != nullptr && __syncthreads_or(any) && threadIdx.x == 0) *nonzero = 1;
 }
 
 // grid: heads; block 256: head_mean[h] = mean of row_cos[h, :], summed in a
@@ -53,7 +82,8 @@ head_mean_kernel(const double* __restrict__ row_cos, int64_t rows, double* __res
   __shared__ double part[256];
   const int64_t h = blockIdx.x;
   double s = 0.0;
-  for (int64_t r = threadIdx.x; r < rows; r += 256) s += row_cos[h * rows + r];
+#pragma unroll 8
+  for (int64_t r = threadIdx.x; r < rows; r += 256) s += row_cos[h * rows + r];  // loads batched, adds in order
   part[threadIdx.x] = s;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
@@ -110,11 +140,12 @@ pairwise_cosine_kernel(const T* __restrict__ later, const T* __restrict__ earlie
 
 template <typename T>
 int launch_row_cosine(const void* a, const void* b, int64_t heads, int64_t rows, int64_t d,
-                      double* row_cos, double* head_mean, cudaStream_t st) {
+                      double* row_cos, double* head_mean, cudaStream_t st, bool update, int* nonzero) {
   const int64_t n = heads * rows;
   if (n > 0) {
-    row_cosine_kernel<T><<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
-        reinterpret_cast<const T*>(a), reinterpret_cast<const T*>(b), n, d, row_cos);
+    row_cosine_kernel<T><<<(unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * 8), 256, 0, st>>>(
+        reinterpret_cast<const T*>(a), const_cast<T*>(reinterpret_cast<const T*>(b)), n, d, row_cos,
+        update ? 1 : 0, nonzero);
     count_launch();
     if (int rc = check_launch("row_cosine_kernel")) return rc;
   }
@@ -134,9 +165,12 @@ int launch_pairwise_cosine(const void* later, const void* earlier, int64_t heads
   return check_launch("pairwise_cosine_kernel");
 }
 
-template int launch_row_cosine<double>(const void*, const void*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t);
-template int launch_row_cosine<float>(const void*, const void*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t);
-template int launch_row_cosine<__nv_bfloat16>(const void*, const void*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t);
+template int launch_row_cosine<double>(const void*, const void*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t,
+                                       bool, int*);
+template int launch_row_cosine<float>(const void*, const void*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t,
+                                       bool, int*);
+template int launch_row_cosine<__nv_bfloat16>(const void*, const void*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t,
+                                       bool, int*);
 template int launch_pairwise_cosine<double>(const void*, const void*, int64_t, int64_t, int64_t, double*, cudaStream_t);
 template int launch_pairwise_cosine<float>(const void*, const void*, int64_t, int64_t, int64_t, double*, cudaStream_t);
 template int launch_pairwise_cosine<__nv_bfloat16>(const void*, const void*, int64_t, int64_t, int64_t, double*, cudaStream_t);

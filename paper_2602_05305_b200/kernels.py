@@ -313,6 +313,22 @@ def row_cosine(a, b, want_rows: bool = False):
     return (mean, rc) if want_rows else mean
 
 
+def row_cosine_update(a, prev, nonzero=None):
+    """row_cosine(a, prev)'s per-head mean [heads] (float64), then prev <- a in
+    the same pass (fb_row_cosine_update); nonzero (int32 scalar tensor, optional)
+    is set to 1 if a has a nonzero row.  prev must be contiguous, a's shape."""
+    a3 = _as3(a, "a").contiguous()
+    require_cuda(a3, prev)
+    if not prev.is_contiguous() or prev.shape != a3.shape or prev.dtype != a3.dtype:
+        raise ShapeError(f"previous step copy must be a contiguous {tuple(a3.shape)} {a3.dtype} tensor")
+    heads, rows, d = a3.shape
+    mean = torch.empty(heads, dtype=torch.float64, device=a3.device)
+    rc = torch.empty((heads, rows), dtype=torch.float64, device=a3.device)
+    _lib.call("fb_row_cosine_update", _sim_code(a3), _p(a3), _p(prev), heads, rows, d, _p(rc), _p(mean),
+              None if nonzero is None else _p(nonzero), _stream(a3))
+    return mean
+
+
 def pairwise_cosine(later, earlier):
     """All-pairs cosine [heads, rows, rows] between a later and an earlier
     step's rows (analysis.py:28-51), float64."""

@@ -320,7 +320,9 @@ def f3(out):
     cal.observe(0, o_ext, B)
     t_cal = graph_ms(lambda: cal.observe(0, o_ext, B), reps=5)
     emit(out, {"config": "F3-calibrator", "heads": H, "rows": B, "observe_ms": t_cal,
-               "bytes": 2 * H * B * D * 4, "gbs": 2 * H * B * D * 4 / (t_cal * 1e-3) / 1e9})
+               "bytes": 3 * H * B * D * 4, "gbs": 3 * H * B * D * 4 / (t_cal * 1e-3) / 1e9,
+               "note": "fb_row_cosine_update: reads this and the previous step's partial, writes the copy; "
+                       "+ per-head means and the [b, Hq] sum / min"})
 
 
 # ---------------------------------------------------------------- C1

@@ -181,3 +181,27 @@ def test_gpu_engine_head_gated_step_matches_per_head_reference():
                 ref, _ = orc.with_reuse(qq2, ext, True, kk[n:], vv[n:])
             err = float(np.max(np.abs(out2[bi, hh] - ref))) / float(np.max(np.abs(ref)))
             assert err <= 1e-2, (bi, hh, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", ["f64", "f32", "bf16"])
+def test_gpu_row_cosine_update_is_cosine_then_copy(dt):
+    """fb_row_cosine_update: the same per-head means as fb_row_cosine, prev
+    replaced by a in the same pass, nonzero flag raised only by nonzero rows."""
+    torch = _torch()
+    from paper_2602_05305_b200 import kernels as K
+
+    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dt]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn((6, 77, 128), device="cuda", generator=g).to(tdt)
+    prev = torch.randn((6, 77, 128), device="cuda", generator=g).to(tdt)
+    want = K.row_cosine(a, prev)
+    flag = torch.zeros((), dtype=torch.int32, device="cuda")
+    got = K.row_cosine_update(a, prev, flag)
+    assert torch.equal(got, want)
+    assert torch.equal(prev, a)
+    assert int(flag) == 1
+    z = torch.zeros_like(a)
+    flag.zero_()
+    K.row_cosine_update(z, prev, flag)
+    assert int(flag) == 0 and bool((prev == 0).all())
