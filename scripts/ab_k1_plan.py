@@ -33,6 +33,10 @@ cases = [("C3 b=8 P=8", 64, 16384), ("C3 b=8 P=4", 64, 32768), ("C3 b=1 P=2", 8,
 variants = [("default", {}), ("ctas148", {"FB_REFRESH_CTAS": "148"}),
             ("span4", {"FB_K1_MAXSPAN": "4"}), ("ctas148+span4", {"FB_REFRESH_CTAS": "148", "FB_K1_MAXSPAN": "4"}),
             ("ctas148+span5", {"FB_REFRESH_CTAS": "148", "FB_K1_MAXSPAN": "5"})]
+if os.environ.get("AB_SMALL"):  # latency-bound shapes: CTA count only
+    cases = [("C3 b=1 P=8", 8, 16384), ("C3 b=1 P=4", 8, 32768), ("C3 b=1 P=2", 8, 65536),
+             ("C2 b=1", 8, 32768), ("C2 b=2", 16, 32768), ("C2 b=4", 32, 32768)]
+    variants = [("default", {}), ("ctas148", {"FB_REFRESH_CTAS": "148"}), ("ctas144", {"FB_REFRESH_CTAS": "144"})]
 res = {}
 for name, groups, n in cases:
     q = r(groups, 128, 128)
