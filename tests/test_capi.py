@@ -96,6 +96,16 @@ def test_prefill_subset_and_similarity_validation_need_no_device(lib):
               None, 0, None) == _lib.FB_ERR_BOUNDS
     # row cosine needs its row buffer
     assert lib.fb_row_cosine(_lib.FB_F32, None, None, 2, 3, 8, None, None, None) == _lib.FB_ERR_VALUE
+    assert lib.fb_row_cosine_update(_lib.FB_F32, None, None, 2, 3, 8, None, None, None, None) == _lib.FB_ERR_VALUE
+    # token-major cached step: bf16 only, GQA divisibility, d 128 and G * B <= 128 (checked before any launch)
+    tok = lambda dt, b, blk, hq, hkv, d, od=_lib.FB_BF16, fl=0: lib.fb_internal_merge_tok(
+        dt, None, 6144, None, 6144, None, 6144, b, blk, hq, hkv, d, 1.0, None, None, None, od, 4096, fl, None)
+    assert tok(_lib.FB_F32, 2, 32, 32, 8, 128) == _lib.FB_ERR_UNSUPPORTED
+    assert tok(_lib.FB_BF16, 2, 32, 32, 6, 128) == _lib.FB_ERR_SHAPE
+    assert tok(_lib.FB_BF16, 2, 32, 32, 8, 64) == _lib.FB_ERR_UNSUPPORTED
+    assert tok(_lib.FB_BF16, 2, 64, 32, 8, 128) == _lib.FB_ERR_UNSUPPORTED  # G * B = 256 rows
+    assert tok(_lib.FB_BF16, 2, 32, 32, 8, 128, fl=8) == _lib.FB_ERR_VALUE
+    assert tok(_lib.FB_BF16, 0, 32, 32, 8, 128) == _lib.FB_OK  # empty batch: nothing to do
     # unknown cached-step flags
     assert lib.fb_internal_merge_ex(_lib.FB_BF16, None, None, None, 1, 1, 128, 32, 1.0, None, None,
                                     None, _lib.FB_BF16, None, None, None, None, None, 0, 8,
