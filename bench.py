@@ -1,19 +1,29 @@
-"""Benchmark: FlashBlock attention on B200 (BASELINE.json metric, config C2).
+"""Benchmark: FlashBlock attention on B200 (BASELINE.json metric).
 
-One bench *step* = one block of block-diffusion decoding on the C2 shapes:
-L=36 layers of 8B-class GQA attention (32 q / 8 kv heads, head_dim 128),
-batch b, block B=32, committed context N=32768, S=32 diffusion steps with
-1 unmask per step and tau=2 -> the refresh schedule is [Recompute, Reuse x31]
-(policy.refresh_schedule; the reference simulator's decisions).  Refresh
-steps run K1 (tcgen05 refresh over the KV cache) + K2 (internal + merge);
-cached steps run K2 only.  The full-recompute baseline runs K1+K2 on every
-step.  Synthetic bf16 inputs, N(0,1), seeded; every layer has its own KV
-cache (inputs > L2).
+N = 1 (default): config C2 (BASELINE.json configs[1]).  One bench *step* =
+one block of block-diffusion decoding: L=36 layers of 8B-class GQA attention
+(32 q / 8 kv heads, head_dim 128), batch b, block B=32, committed context
+N=32768, S=32 diffusion steps with 1 unmask per step and tau=2 -> the refresh
+schedule is [Recompute, Reuse x31] (policy.refresh_schedule; the reference
+simulator's decisions).  Refresh steps run K1 (tcgen05 refresh over the KV
+cache) + K2 (internal + merge); cached steps run K2 only.  The
+full-recompute baseline runs K1+K2 on every step.  Synthetic bf16 inputs,
+N(0,1), seeded; every layer has its own KV cache (inputs > L2).  The line also
+carries the schedule sweep (unmask per step x tau) against full recompute.
+
+N > 1 (or --workload c3): config C3 (configs[2]) -- 128K context, the KV
+cache of each sequence split along the sequence over the N ranks (strong
+scaling: the same b sequences whatever N).  Refresh step per layer: K1 on
+the local shard -> ONE packed exchange of the (O, LSE) partials (grouped
+NCCL send/recv by kv-group chunk) -> K3 merge of this rank's kv-head shard
+-> K2 on the shard; the 31 cached steps run K2 on the head shard only (no
+KV, no exchange).  Time = max over ranks of CUDA events on each rank.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+                    [--workload c2|c3]
 
-Under torchrun (N>1) each rank runs its own b sequences (weak scaling, no
-data-path collective); time is the max over ranks.
+--gpus N without torchrun re-launches itself under torch.distributed.run
+with N local ranks (127.0.0.1 rendezvous).
 """
 
 from __future__ import annotations
@@ -54,8 +64,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, gpu):
+        # a UUID ("GPU-...") names the physical device whatever CUDA_VISIBLE_DEVICES says
+        self.gpu = gpu
         self.proc = None
         self.lines: list[str] = []
         self.t = None
@@ -98,7 +109,32 @@ class ClockSampler:
                 if val.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "gpu": str(self.gpu)}
+
+
+def gpu_smi_id(device) -> str:
+    """nvidia-smi --id for a torch device: its UUID (GPU-xxxxxxxx-...), so the
+    sampler watches the device this process really runs on."""
+    import torch
+
+    try:
+        u = str(torch.cuda.get_device_properties(device).uuid)
+        if u:
+            return u if u.startswith(("GPU-", "MIG-")) else f"GPU-{u}"
+    except Exception:
+        pass
+    return str(device.index if device.index is not None else 0)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------- CPU reference
@@ -106,14 +142,17 @@ class ClockSampler:
 
 def _reference_module():
     """The unmodified reference package (baseline/_ref) if installed, else the
-    oracle port.  Used only for the cpu_baseline / --impl reference legs."""
+    oracle port.  Used only for the cpu_baseline / --impl reference legs.
+    Returns (kind, attention_streamed, merge_partials, attention_with_reuse,
+    CacheEntry)."""
     ref_dir = os.path.join(ROOT, "baseline", "_ref")
     if os.path.isdir(os.path.join(ref_dir, "flashblock")):
         sys.path.insert(0, ref_dir)
         try:
-            import flashblock.attention as A  # noqa: F401
+            import flashblock.attention as A
 
-            return "reference", A.attention_partial, A.attention_with_reuse, A.CacheEntry
+            return ("reference", A.attention_streamed, A.merge_partials, A.attention_with_reuse,
+                    A.CacheEntry)
         except Exception:
             sys.path.remove(ref_dir)
     from oracle import flashblock_oracle as O
@@ -125,79 +164,99 @@ def _reference_module():
         def __init__(self, partial, step_created, block_id=-1):
             self.partial = partial
 
-    return "port", O.partial, reuse, Entry
+    return "port", O.streamed, O.merge, reuse, Entry
 
 
-def cpu_reference_sample(ctx: int = CTX, reps: int = 3):
-    """Time the reference CPU path for ONE kv-head group (G*B = 128 stacked
-    fp32 query rows, d=128) of one layer: a refresh (attention_partial over
-    the ctx committed keys + internal partial + merge) and a cached step
-    (attention_with_reuse).  Tile 512 as the reference simulator
-    (simulator.py:87).  Returns per-kv-head seconds (best of reps)."""
+def cpu_layer_block(ctx: int, sched, reps: int = 1):
+    """Time the reference CPU path over ONE layer x all Hkv kv-heads x one
+    whole block schedule at b=1, routed exactly as the reference step driver
+    (simulator.py:412-434): a Recompute step concatenates the committed rows
+    with the block's K/V and runs attention_streamed + merge_partials, caching
+    the external partial; a Reuse step runs attention_with_reuse against it.
+    Per kv-head the G=4 query heads are stacked (128 fp32 rows, d=128; rows
+    are independent); tile 512 as simulator.py:87.  Returns the
+    best-of-`reps` seconds and the reference kind."""
     import numpy as np
 
-    kind, partial, reuse, Entry = _reference_module()
+    kind, streamed, merge, reuse, Entry = _reference_module()
     rng = np.random.Generator(np.random.Philox(1234))
     rows = (HQ // HKV) * BLK
-    q = rng.standard_normal((rows, D)).astype(np.float32)
-    k = rng.standard_normal((ctx, D)).astype(np.float32)
-    v = rng.standard_normal((ctx, D)).astype(np.float32)
-    ki = rng.standard_normal((BLK, D)).astype(np.float32)
-    vi = rng.standard_normal((BLK, D)).astype(np.float32)
-    t_ref = t_c = float("inf")
-    ext = None
+    heads = []
+    for _ in range(HKV):
+        heads.append(tuple(rng.standard_normal(s).astype(np.float32) for s in
+                           ((rows, D), (ctx, D), (ctx, D), (BLK, D), (BLK, D))))
+    best = float("inf")
     for _ in range(reps):
         t0 = time.perf_counter()
-        ext = partial(q, k, v, None, 512)
-        reuse(q, Entry(ext, 0, 0), ki, vi, None, 512)  # internal + merge of the refresh step
-        t_ref = min(t_ref, time.perf_counter() - t0)
-        t0 = time.perf_counter()
-        for _ in range(10):
-            reuse(q, Entry(ext, 0, 0), ki, vi, None, 512)
-        t_c = min(t_c, (time.perf_counter() - t0) / 10)
-    return kind, t_ref, t_c
+        entries = [None] * HKV
+        for dec in sched:
+            for h, (q, k, v, ki, vi) in enumerate(heads):
+                if dec == "Recompute":
+                    keys = np.concatenate([k, ki])
+                    values = np.concatenate([v, vi])
+                    ext, inn = streamed(q, keys, values, ctx, None, 512)
+                    merge(ext, inn)
+                    entries[h] = Entry(ext, 0, 0)
+                else:
+                    reuse(q, entries[h], ki, vi, None, 512)
+        best = min(best, time.perf_counter() - t0)
+    return kind, best
 
 
-def cpu_tokens_per_s(t_refresh: float, t_cached: float, n_refresh: int) -> float:
-    """Extrapolate per-kv-head times to the whole block: L layers x Hkv heads
-    x (n_refresh refreshes + the rest cached); b sequences cancel (tokens
-    and work both scale with b)."""
-    per_block = LAYERS * HKV * (n_refresh * t_refresh + (STEPS_PER_BLOCK - n_refresh) * t_cached)
-    return BLK / per_block
+def cpu_tokens_per_s(t_layer_block: float) -> float:
+    """tokens/s of the whole C2 job from one layer's block at b=1: the block
+    yields BLK tokens per sequence after LAYERS such layers; batch cancels
+    (tokens and work both scale with b).  Extrapolation factor: x LAYERS."""
+    return BLK / (LAYERS * t_layer_block)
+
+
+def _sched_names(per_step: int = UNMASK_PER_STEP, tau: int = TAU):
+    from paper_2602_05305_b200.policy import ReuseConfig, refresh_schedule
+
+    return [d.value for d in refresh_schedule(ReuseConfig(tau=tau), BLK, STEPS_PER_BLOCK, per_step)]
+
+
+def _cpu_sample_text(kind, t, sched, reps):
+    n_ref = sum(1 for d in sched if d == "Recompute")
+    return (f"1 layer x {HKV} kv-heads (G={HQ // HKV} stacked -> {(HQ // HKV) * BLK} fp32 rows, d={D}) "
+            f"x one {STEPS_PER_BLOCK}-step block ({n_ref} refresh over {CTX} keys via attention_streamed + "
+            f"merge_partials, {STEPS_PER_BLOCK - n_ref} attention_with_reuse), b=1, tile 512, best of {reps}: "
+            f"{t:.3f} s; extrapolated x{LAYERS} layers (batch cancels); {kind} on {os.cpu_count()} host "
+            f"threads ({cpu_model()})")
 
 
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-    from paper_2602_05305_b200.policy import ReuseConfig, refresh_schedule
-
-    sched = refresh_schedule(ReuseConfig(tau=TAU), BLK, STEPS_PER_BLOCK, UNMASK_PER_STEP)
-    n_ref = sum(1 for d in sched if d.value == "Recompute")
+    threads = str(os.cpu_count())
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(var, threads)
+    sched = _sched_names()
     for _ in range(args.warmup):
-        cpu_reference_sample(reps=1)
-    vals = []
+        cpu_layer_block(CTX, sched, reps=1)
+    vals, times = [], []
     kind = None
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        kind, tr, tc = cpu_reference_sample(reps=1)
-        vals.append(cpu_tokens_per_s(tr, tc, n_ref))
+        kind, t = cpu_layer_block(CTX, sched, reps=1)
+        times.append(t)
+        vals.append(cpu_tokens_per_s(t))
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
-    cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
+        # one bench step = one C2 block for the whole batch: b x the per-sequence block time
         "ms_per_step": 1000.0 * args.batch * BLK / value if value else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
         "data": "synthetic N(0,1), seeded",
         "config": _config(args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"per step: 1 layer x 1 kv-head (128 stacked fp32 rows, d=128) "
-                                   f"refresh over {CTX} keys + 1 cached step, tile 512, "
-                                   f"extrapolated x{LAYERS} layers x{HKV} heads x schedule "
-                                   f"({n_ref} refresh / {STEPS_PER_BLOCK})"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                         "cpu_model": cpu_model(),
+                         "sample": _cpu_sample_text(kind, statistics.median(times), sched, 1),
+                         "extrapolation": f"x{LAYERS} layers (measured: a whole layer-block at b=1)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "measured_s_per_step": statistics.median(times),
         "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
@@ -297,7 +356,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             dist.barrier()
         return ms
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(gpu_smi_id(dev))
     sampler.start()
     ms_fb = timed(g_fb, args.steps, args.warmup)
     clocks = sampler.stop()
@@ -371,16 +430,44 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- e2e: public API, host buffers, copies in the timed region
     e2e = run_e2e(args, eng, kc, vc, dev, sched, world)
 
+    # ---- schedule sweep: unmask per step x tau, each against the
+    # full recompute of the same block; every point is one graph of a whole block
+    sweep = []
+    if not args.no_sweep:
+        ms_full_block = ms_full / steps_full
+        for per_step in (1, 2, 3):
+            for tau in (2, 3):
+                sch = refresh_schedule(ReuseConfig(tau=tau), BLK, STEPS_PER_BLOCK, per_step)
+                nr = sum(1 for d in sch if d is Decision.RECOMPUTE)
+
+                def blk(sch=sch):
+                    eng.begin_block(0)
+                    for dec in sch:
+                        for l in range(LAYERS):
+                            if dec is Decision.RECOMPUTE:
+                                eng.refresh(l, qs[l], kc[l], vc[l], CTX, kis[l], vis[l], out=outs[l])
+                            else:
+                                eng.cached(l, qs[l], kis[l], vis[l], out=outs[l])
+
+                g_s, _ = capture(blk)
+                reps = 3 if nr < STEPS_PER_BLOCK else 2
+                ms_s = timed(g_s, reps, 1) / reps
+                del g_s
+                sweep.append({"unmask_per_step": per_step, "tau": tau,
+                              "refresh_steps": f"{nr}/{STEPS_PER_BLOCK}",
+                              "tokens_per_s": world * b * BLK / (ms_s / 1000.0), "ms_per_block": ms_s,
+                              "speedup_vs_full_recompute": ms_full_block / ms_s,
+                              "clears_1p4x": ms_full_block / ms_s >= 1.4})
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-        kind, tr, tcached = cpu_reference_sample(reps=2)
-        cpu = {"value": cpu_tokens_per_s(tr, tcached, n_ref), "unit": UNIT, "cores": os.cpu_count(),
-               "kind": kind,
-               "sample": f"1 layer x 1 kv-head refresh ({CTX} keys, {tr*1e3:.1f} ms) + cached "
-                         f"step ({tcached*1e3:.2f} ms), fp32, tile 512, best of 2, extrapolated "
-                         f"x{LAYERS} layers x{HKV} kv-heads x schedule ({n_ref} refresh/"
-                         f"{STEPS_PER_BLOCK} steps)"}
+        for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ.setdefault(var, str(os.cpu_count()))
+        names = _sched_names()
+        kind, t_lb = cpu_layer_block(CTX, names, reps=2)
+        cpu = {"value": cpu_tokens_per_s(t_lb), "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+               "cpu_model": cpu_model(), "sample": _cpu_sample_text(kind, t_lb, names, 2),
+               "extrapolation": f"x{LAYERS} layers (measured: a whole layer-block at b=1)"}
 
     if rank == 0:
         line = {
@@ -403,6 +490,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "tensor_tflops": k1_flops / (k1_ms * 1e-3) / 1e12},
             "k2_cached_step": {"avg_launch_ms": k2_ms, "algorithmic_bytes": k2_bytes,
                                "achieved_gbs": k2_bytes / (k2_ms * 1e-3) / 1e9},
+            "schedule_sweep": sweep,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_fb * args.steps,
@@ -412,12 +500,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
 
 def run_e2e(args, eng, kc, vc, dev, sched, world):
-    """Same metric through the public engine API (eager, no graph): every
-    diffusion step copies its Q / K_in / V_in for all layers from pinned host
-    memory and reads back a per-step checksum of the attention outputs.
-    Copies run on their own stream into double-buffered device slots, one
-    copy per tensor per step, so the next step's PCIe transfer overlaps this
-    step's attention."""
+    """Same metric through the public engine API (eager launches, no graph):
+    every diffusion step copies its Q / K_in / V_in for all layers from pinned
+    host memory and copies the step's attention outputs (all layers, bf16)
+    back to pinned host memory.  H2D copies run on one copy stream, D2H on
+    another (PCIe is full duplex), into / out of double-buffered device slots,
+    so step s+1's inputs and step s-1's outputs move while step s computes.
+    Timed on the host wall clock around whole blocks, after a synchronize on
+    both sides."""
     import torch
 
     from paper_2602_05305_b200.policy import Decision
@@ -427,40 +517,43 @@ def run_e2e(args, eng, kc, vc, dev, sched, world):
     host_q = torch.randn((LAYERS,) + hq_shape, dtype=torch.float32).to(torch.bfloat16).pin_memory()
     host_k = torch.randn((LAYERS,) + kv_shape, dtype=torch.float32).to(torch.bfloat16).pin_memory()
     host_v = torch.randn((LAYERS,) + kv_shape, dtype=torch.float32).to(torch.bfloat16).pin_memory()
+    host_o = [torch.empty((LAYERS,) + hq_shape, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
     dq = [torch.empty_like(host_q, device=dev) for _ in range(2)]
     dk = [torch.empty_like(host_k, device=dev) for _ in range(2)]
     dv = [torch.empty_like(host_v, device=dev) for _ in range(2)]
-    outs = torch.empty((LAYERS,) + hq_shape, dtype=torch.bfloat16, device=dev)
-    csum = torch.empty(STEPS_PER_BLOCK, dtype=torch.float32, device=dev)
-    host_c = torch.empty(STEPS_PER_BLOCK, dtype=torch.float32).pin_memory()
+    outs = [torch.empty((LAYERS,) + hq_shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(device=dev)
-    # one copy per tensor per step (whole-step copies reach ~55 GB/s over PCIe,
-    # per-layer ones ~50): step s+1's inputs stream in while step s computes
-    ready = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
+    h2d = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    ready = [torch.cuda.Event() for _ in range(2)]     # inputs of slot landed
+    consumed = [torch.cuda.Event() for _ in range(2)]  # attention done with slot inputs / outputs written
+    drained = [torch.cuda.Event() for _ in range(2)]   # outputs of slot copied to the host
     for sl in range(2):
-        done[sl].record(comp)
+        consumed[sl].record(comp)
+        drained[sl].record(comp)
 
     def block():
         eng.begin_block(0)
         for s, dec in enumerate(sched):
             sl = s & 1
-            with torch.cuda.stream(copy):
-                copy.wait_event(done[sl])  # slot free: step s-2 has consumed it
+            with torch.cuda.stream(h2d):
+                h2d.wait_event(consumed[sl])  # slot free: step s-2 has consumed it
                 dq[sl].copy_(host_q, non_blocking=True)
                 dk[sl].copy_(host_k, non_blocking=True)
                 dv[sl].copy_(host_v, non_blocking=True)
-                ready[sl].record(copy)
+                ready[sl].record(h2d)
             comp.wait_event(ready[sl])
+            comp.wait_event(drained[sl])  # step s-2's outputs have left this slot
             for l in range(LAYERS):
                 if dec is Decision.RECOMPUTE:
-                    eng.refresh(l, dq[sl][l], kc[l], vc[l], CTX, dk[sl][l], dv[sl][l], out=outs[l])
+                    eng.refresh(l, dq[sl][l], kc[l], vc[l], CTX, dk[sl][l], dv[sl][l], out=outs[sl][l])
                 else:
-                    eng.cached(l, dq[sl][l], dk[sl][l], dv[sl][l], out=outs[l])
-            done[sl].record(comp)
-            csum[s] = outs.sum(dtype=torch.float32)
-        host_c.copy_(csum, non_blocking=True)
+                    eng.cached(l, dq[sl][l], dk[sl][l], dv[sl][l], out=outs[sl][l])
+            consumed[sl].record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(consumed[sl])
+                host_o[sl].copy_(outs[sl], non_blocking=True)
+                drained[sl].record(d2h)
 
     steps = max(1, args.steps // 2)
     block()
@@ -470,81 +563,182 @@ def run_e2e(args, eng, kc, vc, dev, sched, world):
         block()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    h2d = STEPS_PER_BLOCK * (host_q.numel() + host_k.numel() + host_v.numel()) * 2
-    return {"value": world * b * BLK * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": STEPS_PER_BLOCK * 4,
-            "h2d_gbs": h2d * steps / dt / 1e9,
-            "note": "public engine API, eager launches, per-diffusion-step H2D of Q/K_in/V_in "
-                    "(all layers) from pinned memory on a copy stream overlapping the attention, "
-                    "+ D2H of per-step output checksums; host wall clock; PCIe-bound"}
+    h2d_b = STEPS_PER_BLOCK * (host_q.numel() + host_k.numel() + host_v.numel()) * 2
+    d2h_b = STEPS_PER_BLOCK * host_o[0].numel() * 2
+    return {"value": world * b * BLK * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
+            "d2h_bytes_per_step": d2h_b,
+            "h2d_gbs": h2d_b * steps / dt / 1e9, "d2h_gbs": d2h_b * steps / dt / 1e9,
+            "note": "public engine API, eager launches; per diffusion step: H2D of Q/K_in/V_in (all "
+                    "layers) and D2H of the attention outputs (all layers, bf16) from/to pinned host "
+                    "memory on two copy streams overlapping the attention; host wall clock; PCIe-bound"}
+
+
+C3_CTX = 131072
 
 
 def run_splitkv(args, rank: int, world: int, local_rank: int):
-    """C3: 128K context whose committed KV is split along the sequence over the
-    `world` ranks (strong scaling: the same b sequences on every rank count).
-    Per layer and block: refresh = K1 on the local shard -> ONE all_to_all of
-    the fp32 (O, LSE) partials -> K3 merge for this rank's kv-head shard -> K2;
-    31 cached steps = K2 on the head shard only (no KV, no exchange)."""
+    """C3 (BASELINE.json configs[2]): 128K context whose committed KV is split
+    along the sequence over the `world` ranks (strong scaling: the same b
+    sequences whatever the rank count).  Per layer and block:
+      refresh step = K1 on the local shard -> ONE packed exchange of the fp32
+                     (O, LSE) partials (grouped NCCL send/recv by kv-group
+                     chunk; splitkv.py) -> K3 merge for this rank's kv-head
+                     shard -> K2 on the shard;
+      31 cached steps = K2 on the head shard only (no KV, no exchange).
+    The refresh step runs eagerly (the exchange stays outside CUDA graphs);
+    the cached steps of a block replay as one CUDA graph.  All 36 layers have
+    their own KV shard (b=4: 77 GB at N=1, 9.7 GB per rank at N=8)."""
     import torch
     import torch.distributed as dist
 
+    from paper_2602_05305_b200 import _lib
     from paper_2602_05305_b200 import kernels as K
     from paper_2602_05305_b200.splitkv import SplitKVRefresh, group_chunks, shard_bounds
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    b, N, L = args.batch, args.ctx, args.layers
+    lib = _lib.load()
+    b, N, L = args.c3_batch, args.ctx, args.layers
     groups, rows = b * HKV, (HQ // HKV) * BLK
     lo, hi = shard_bounds(N, world, rank)
     n_loc = hi - lo
     g0, g1 = group_chunks(groups, world)[rank]
+    per = g1 - g0
     gen = torch.Generator(device=dev).manual_seed(99 + rank)
-    rnd = lambda *sh: torch.randn(sh, device=dev, generator=gen).to(torch.bfloat16)
+
+    def rnd(*sh):
+        return torch.randn(sh, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+
     kc = [rnd(groups, max(n_loc, 1), D) for _ in range(L)]
     vc = [rnd(groups, max(n_loc, 1), D) for _ in range(L)]
-    q = [rnd(groups, rows, D) for _ in range(L)]
-    ki = [rnd(groups, BLK, D) for _ in range(L)]
-    vi = [rnd(groups, BLK, D) for _ in range(L)]
-    out = torch.empty((g1 - g0, rows, D), device=dev, dtype=torch.bfloat16)
-    ext = [None] * L
-    refresh = SplitKVRefresh(layout="all_to_all" if world > 1 else "all_gather")
+    # queries and the current block are the same on every rank (seeded alike)
+    gq = torch.Generator(device=dev).manual_seed(7)
+    q = [torch.randn((groups, rows, D), device=dev, generator=gq).to(torch.bfloat16) for _ in range(L)]
+    ki = [torch.randn((groups, BLK, D), device=dev, generator=gq).to(torch.bfloat16) for _ in range(L)]
+    vi = [torch.randn((groups, BLK, D), device=dev, generator=gq).to(torch.bfloat16) for _ in range(L)]
+    o_ext = [torch.empty((per, rows, D), device=dev, dtype=torch.float32) for _ in range(L)]
+    l_ext = [torch.empty((per, rows), device=dev, dtype=torch.float32) for _ in range(L)]
+    out = [torch.empty((per, rows, D), device=dev, dtype=torch.bfloat16) for _ in range(L)]
+    refresh = SplitKVRefresh(layout="all_to_all")
+
+    def refresh_step():
+        for l in range(L):
+            refresh(q[l], kc[l], vc[l], n_loc, None, out=o_ext[l], lse=l_ext[l])
+            K.internal_merge(q[l][g0:g1], ki[l][g0:g1], vi[l][g0:g1], o_ext[l], l_ext[l],
+                             out_dtype=torch.bfloat16, out=out[l])
+
+    def cached_steps():
+        for _ in range(STEPS_PER_BLOCK - 1):
+            for l in range(L):
+                K.internal_merge(q[l][g0:g1], ki[l][g0:g1], vi[l][g0:g1], o_ext[l], l_ext[l],
+                                 out_dtype=torch.bfloat16, out=out[l], ext_stable=True)
+
+    stream = torch.cuda.current_stream(dev)
+    refresh_step()
+    cached_steps()
+    torch.cuda.synchronize()
+    g_cached = torch.cuda.CUDAGraph()
+    c0 = lib.fb_launch_count()
+    with torch.cuda.graph(g_cached):
+        cached_steps()
+    cached_launches = lib.fb_launch_count() - c0
+    torch.cuda.synchronize()
 
     def block():
-        for s in range(STEPS_PER_BLOCK):
-            for l in range(L):
-                if s == 0:
-                    ext[l] = refresh(q[l], kc[l], vc[l], n_loc)
-                o_e, l_e = ext[l]
-                K.internal_merge(q[l][g0:g1], ki[l][g0:g1], vi[l][g0:g1], o_e, l_e,
-                                 out_dtype=torch.bfloat16, out=out)
+        refresh_step()
+        g_cached.replay()
 
-    for _ in range(args.warmup):
-        block()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        block()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
+    def max_over_ranks(ms: float) -> float:
+        if world == 1:
+            return ms
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        if world > 1:
+            dist.barrier()
+        return ms
+
+    sampler = ClockSampler(gpu_smi_id(dev))
+    sampler.start()
+    l0 = lib.fb_launch_count()
+    ms = timed(block, args.steps, args.warmup)
+    eager_launches = lib.fb_launch_count() - l0  # the graph replays are not counted by the host
+    clocks = sampler.stop()
+    # the two parts of the block alone: T_refresh(P) (K1 + exchange + K3 + K2 over 36
+    # layers) and the cached steps
+    ms_ref = timed(refresh_step, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
+    ms_cached = timed(g_cached.replay, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
+
+    # K1 on the local shard alone (roofline of the dominant kernel at this P)
+    o_s = torch.empty((groups, rows, D), device=dev, dtype=torch.float32)
+    l_s = torch.empty((groups, rows), device=dev, dtype=torch.float32)
+
+    def k1_only():
+        for l in range(L):
+            K.attention_partial(q[l], kc[l], vc[l], 0, n_loc, None, out=o_s, lse=l_s)
+
+    ms_k1 = timed(k1_only, 2, 1) / 2 / L
+    k1_bytes = 2 * groups * n_loc * D * 2 + groups * rows * D * 2 + groups * rows * (D + 1) * 4
+    peak, peak_kind = _peaks()
     if rank == 0:
         value = b * BLK * args.steps / (ms / 1000.0)
+        exch = groups * rows * (D + 1) * 4 * (world - 1) // world if world > 1 else 0
         print(json.dumps({
             "metric": "block-diffusion tokens/s (FlashBlock attention, C3: 128K ctx split-KV)",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C3 split-KV refresh + head-sharded cached steps (eager launches)",
-                       "layers": L, "batch": b, "ctx": N, "shard_rows": n_loc,
-                       "exchange": "all_to_all of fp32 (O, LSE) partials, once per layer per block"}}),
-              flush=True)
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) bf16, seeded; distinct KV shard per layer",
+            "config": {"workload": "C3: 8B-class GQA, 128K ctx, KV split along the sequence over "
+                                   f"{world} GPU(s), FlashBlock tau=2 (1 refresh / 32 steps)",
+                       "layers": L, "batch": b, "ctx": N, "shard_rows": n_loc, "q_heads": HQ,
+                       "kv_heads": HKV, "head_dim": D, "block": BLK, "steps_per_block": STEPS_PER_BLOCK,
+                       "kv_groups_per_rank": per,
+                       "exchange": "packed fp32 (O, LSE) partials, one grouped send/recv per layer "
+                                   "per block (all_to_all by kv-group chunk); cached steps exchange nothing",
+                       "parallelism": f"split-KV x{world} (refresh) + kv-head shards (cached steps)",
+                       "l2": "inputs larger than L2 (distinct KV shard per layer)"},
+            "refresh_step_ms": ms_ref, "refresh_ms_per_layer": ms_ref / L,
+            "cached_steps_ms": ms_cached,
+            "exchange_bytes_sent_per_layer_per_rank": exch,
+            "roofline": {"bound": "hbm", "kernel": "K1 on the local KV shard",
+                         "achieved": k1_bytes / (ms_k1 * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": k1_bytes / (ms_k1 * 1e-3) / 1e9 / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": ms_k1,
+                         "peak_kind": peak_kind},
+            "e2e": None,
+            "gpu_launches": eager_launches + cached_launches * args.steps,
+            "clocks": clocks,
+            "nccl_debug": os.environ.get("NCCL_DEBUG"),
+        }), flush=True)
+
+
+def _relaunch(args) -> int:
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run
+    with N local ranks and a 127.0.0.1 rendezvous; returns its exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -552,30 +746,38 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=16, help="C2 sequences per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--mode", default="flashblock", choices=["flashblock", "splitkv"],
-                    help="flashblock: C2 headline (default); splitkv: C3 128K split-KV over ranks")
-    ap.add_argument("--ctx", type=int, default=131072, help="context for --mode splitkv")
-    ap.add_argument("--layers", type=int, default=8, help="layers for --mode splitkv")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the schedule sweep")
+    ap.add_argument("--workload", default=None, choices=["c2", "c3"],
+                    help="c2: 32K headline (default at 1 GPU); c3: 128K split-KV (default at >1 GPU)")
+    ap.add_argument("--ctx", type=int, default=C3_CTX, help="context for C3")
+    ap.add_argument("--layers", type=int, default=LAYERS, help="layers for C3")
+    ap.add_argument("--c3-batch", type=int, default=4, help="sequences for C3 (whole job)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(_relaunch(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    workload = args.workload or ("c3" if world > 1 else "c2")
     if world > 1:
         import torch
         import torch.distributed as dist
 
+        # communicator ranks / NVLS visible in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if args.mode == "splitkv":
+        if workload == "c3":
             run_splitkv(args, rank, world, local_rank)
         else:
             run_ours(args, rank, world, local_rank)

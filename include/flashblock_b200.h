@@ -94,6 +94,11 @@ FB_API int fb_attention_partial(int dtype, const void* q, const void* k, const v
  * concurrently; every launch leaves it zero again.  Used when every split
  * item spans <= 3 CTAs (C2 b >= 16); otherwise -- and with sync_flags NULL,
  * which is fb_attention_partial -- split items are merged by a second kernel.
+ * The merging CTA spin-waits (bounded, 4 s watchdog) on partials written by
+ * other CTAs of the same launch: the grid is one CTA per SM, so the wait
+ * makes progress when the launch owns the GPU; a kernel running concurrently
+ * on another stream only delays it.  Keep one buffer per stream (the Python
+ * layer keys it by stream).
  * Same arguments and results as fb_attention_partial otherwise. */
 FB_API int fb_attention_partial_sync(int dtype, const void* q, const void* k, const void* v,
                                      int64_t groups, int64_t q_rows, int64_t head_dim,

@@ -721,6 +721,16 @@ int fb_internal_merge_tok(int dtype, const void* q, int64_t q_token_stride, cons
   if (batch < 0 || block < 1 || num_q_heads < 1 || num_kv_heads < 1) return fail(FB_ERR_SHAPE, "bad extents");
   if (num_q_heads % num_kv_heads) return fail(FB_ERR_SHAPE, "num_q_heads must be a multiple of num_kv_heads");
   if (batch == 0) return FB_OK;
+  if (!q || !k_in || !v_in || !o_ext || !lse_ext || !out)
+    return fail(FB_ERR_VALUE, "q, k_in, v_in, o_ext, lse_ext and out are required (device pointers)");
+  // rows are read / written with >= 16-byte vector accesses (32-byte when aligned) and
+  // mapped by TMA (16-byte strides)
+  const int64_t osz = out_dtype == FB_BF16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(o_ext) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      ((out_token_stride * osz) & 15) || (reinterpret_cast<uintptr_t>(q) & 15) ||
+      (reinterpret_cast<uintptr_t>(k_in) & 15) || (reinterpret_cast<uintptr_t>(v_in) & 15) ||
+      ((q_token_stride * 2) & 15) || ((k_token_stride * 2) & 15) || ((v_token_stride * 2) & 15))
+    return fail(FB_ERR_VALUE, "o_ext, out, q, k_in and v_in need 16-byte aligned rows");
   return launch_internal_merge_tok_sm100(
       reinterpret_cast<const __nv_bfloat16*>(q), q_token_stride, reinterpret_cast<const __nv_bfloat16*>(k_in),
       k_token_stride, reinterpret_cast<const __nv_bfloat16*>(v_in), v_token_stride, batch, block, num_q_heads,

@@ -282,7 +282,9 @@ class FlashBlockAttention:
         kc, vc, pt = self._sparse_kv(layer, k_cache, v_cache)
         res = K.sparse_attend_merge(qg, kc, vc, kg, vg, n_ext, sel, resid, kbs, self.scale,
                                     self.out_dtype, page_table=pt)
-        self._count_rows(self.b * self.hkv * sel.shape[-1] * kbs)
+        # exactly the selected committed rows, the tail block clipped at n_ext
+        # (read_selected_rows, sparse.py:186-212)
+        self._count_rows((n_ext - sel.to(torch.int64) * kbs).clamp(min=0, max=kbs))
         if out is not None:
             out.view(res.shape).copy_(res)
             return out
@@ -321,50 +323,51 @@ class FlashBlockAttention:
             self._glists[key] = gl
         qg, kg, vg = self._groups(q, k_in, v_in)
         if isinstance(k_cache, PagedKVCache):  # paged serving cache: v_cache / n_ext unused
-            o = out.view(qg.shape) if out is not None else None
-            self._count_rows(k_cache.lengths[layer])
-            K.attention_partial_paged(qg, k_cache.k[layer], k_cache.v[layer], k_cache.table[layer],
-                                      k_cache.lengths[layer], self.scale, out=self.o_ext[layer],
-                                      lse=self.lse_ext[layer])
-            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
-                                   self.out_dtype, out=o)
-            self.valid[layer] = True
-            if self.recorder is not None:
-                self.recorder.observe(layer, self.o_ext[layer], self.B)
-            return res.view(self.b, self.hq, self.B, self.d)
-        kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
-        vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
-        self._count_rows(gl.numel() * int(n_ext))
-        K.attention_partial_groups(qg, kc, vc, gl, 0, int(n_ext), self.scale,
-                                   out=self.o_ext[layer], lse=self.lse_ext[layer])
+            # K1 over the refreshed groups only: their queries, page-table rows and
+            # lengths gathered into a sub-batch, the partials scattered back into
+            # the layer's external partial (other groups keep their cached rows)
+            gl64 = gl.to(torch.int64)
+            lens = k_cache.lengths[layer].index_select(0, gl64)
+            self._count_rows(lens)
+            o_sub, l_sub = K.attention_partial_paged(qg.index_select(0, gl64), k_cache.k[layer],
+                                                     k_cache.v[layer],
+                                                     k_cache.table[layer].index_select(0, gl64), lens,
+                                                     self.scale)
+            self.o_ext[layer].index_copy_(0, gl64, o_sub)
+            self.lse_ext[layer].index_copy_(0, gl64, l_sub)
+        else:
+            kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
+            vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+            self._count_rows(gl.numel() * int(n_ext))
+            K.attention_partial_groups(qg, kc, vc, gl, 0, int(n_ext), self.scale,
+                                       out=self.o_ext[layer], lse=self.lse_ext[layer])
         o = out.view(qg.shape) if out is not None else None
         res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
                                self.out_dtype, out=o)
         return res.view(self.b, self.hq, self.B, self.d), heads
 
     def full_recompute(self, q, k_cache, v_cache, n_ext: int, k_in, v_in, out=None,
-                       o_scratch=None, lse_scratch=None):
+                       o_scratch=None, lse_scratch=None, layer: int | None = None):
         """Baseline: full attention every step (same K1+K2 launch pair as a
-        refresh, partial kept in scratch instead of the cache)."""
+        refresh, partial kept in scratch instead of the cache -- the layer's
+        cached external partial and its valid flag are left alone).  k_cache
+        may be a PagedKVCache; then `layer` selects its page tables (v_cache
+        and n_ext are unused)."""
         qg, kg, vg = self._groups(q, k_in, v_in)
-        if isinstance(k_cache, PagedKVCache):  # paged serving cache: v_cache / n_ext unused
-            o = out.view(qg.shape) if out is not None else None
-            self._count_rows(k_cache.lengths[layer])
-            K.attention_partial_paged(qg, k_cache.k[layer], k_cache.v[layer], k_cache.table[layer],
-                                      k_cache.lengths[layer], self.scale, out=self.o_ext[layer],
-                                      lse=self.lse_ext[layer])
-            res = K.internal_merge(qg, kg, vg, self.o_ext[layer], self.lse_ext[layer], self.scale,
-                                   self.out_dtype, out=o)
-            self.valid[layer] = True
-            if self.recorder is not None:
-                self.recorder.observe(layer, self.o_ext[layer], self.B)
-            return res.view(self.b, self.hq, self.B, self.d)
-        kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
-        vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
         o = out.view(qg.shape) if out is not None else None
-        self._count_rows(self.b * self.hkv * int(n_ext))
-        o_ext, l_ext = K.attention_partial(qg, kc, vc, 0, int(n_ext), self.scale, out=o_scratch,
-                                           lse=lse_scratch)
+        if isinstance(k_cache, PagedKVCache):  # paged serving cache: v_cache / n_ext unused
+            if layer is None:
+                raise ValueError("full_recompute on a PagedKVCache needs layer=")
+            self._count_rows(k_cache.lengths[layer])
+            o_ext, l_ext = K.attention_partial_paged(qg, k_cache.k[layer], k_cache.v[layer],
+                                                     k_cache.table[layer], k_cache.lengths[layer],
+                                                     self.scale, out=o_scratch, lse=lse_scratch)
+        else:
+            kc = k_cache.reshape(self.b * self.hkv, k_cache.shape[-2], self.d)
+            vc = v_cache.reshape(self.b * self.hkv, v_cache.shape[-2], self.d)
+            self._count_rows(self.b * self.hkv * int(n_ext))
+            o_ext, l_ext = K.attention_partial(qg, kc, vc, 0, int(n_ext), self.scale, out=o_scratch,
+                                               lse=lse_scratch)
         res = K.internal_merge(qg, kg, vg, o_ext, l_ext, self.scale, self.out_dtype, out=o)
         return res.view(self.b, self.hq, self.B, self.d)
 
@@ -388,17 +391,28 @@ class KVCache:
         self.v = [torch.zeros_like(t) for t in self.k]
         self.lengths = [torch.zeros(batch * num_kv_heads, dtype=torch.int32, device=dev)
                         for _ in range(num_layers)]
+        # host mirror of the (uniform) committed length per layer: every commit
+        # advances every slab by the block's rows, so overflow is caught before
+        # the launch without a device sync
+        self._len = [0] * num_layers
         self.rows_appended = 0
 
     def commit_block(self, layer: int, k_block, v_block, check: bool = False) -> None:
-        """Append one finished block's rows [b, Hkv, B, d] for `layer`."""
+        """Append one finished block's rows [b, Hkv, B, d] for `layer`.  Raises
+        BoundsError (before launching) when the block would run past the
+        capacity -- committed rows are never dropped (kv_cache.py:121-144).
+        check=True additionally reads the device overflow counter back."""
         if k_block.shape[:2] != (self.b, self.hkv) or k_block.shape[-1] != self.d:
             raise ShapeError(f"block {tuple(k_block.shape)} does not match the cache")
+        rows = k_block.shape[-2]
+        if self._len[layer] + rows > self.cap:
+            raise BoundsError(f"commit of {rows} rows at length {self._len[layer]} exceeds capacity {self.cap}")
         K.commit_block(self.k[layer].view(self.b * self.hkv, self.cap, self.d),
                        self.v[layer].view(self.b * self.hkv, self.cap, self.d),
                        k_block.reshape(self.b * self.hkv, -1, self.d),
                        v_block.reshape(self.b * self.hkv, -1, self.d), self.lengths[layer], check)
-        self.rows_appended += self.b * self.hkv * k_block.shape[-2]
+        self._len[layer] += rows
+        self.rows_appended += self.b * self.hkv * rows
 
     def snapshot_counters(self) -> AccessCounters:
         """Rows appended and bytes resident (committed rows of every slab; syncs)."""

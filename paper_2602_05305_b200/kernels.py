@@ -59,17 +59,26 @@ def _stream(t: torch.Tensor) -> int:
 
 
 class _Workspace:
-    """Per-device scratch buffer for split-KV partials, grown on demand."""
+    """Scratch buffer for split-KV partials per (device, stream), grown on demand.
+
+    Keyed by the launching stream, so kernels on different streams never share
+    scratch.  A buffer that was outgrown is kept alive (not freed): a CUDA graph
+    captured earlier may still hold its pointer and replay into it.  Graphs that
+    are replayed concurrently must therefore be captured on distinct streams."""
 
     def __init__(self):
-        self._bufs: dict[int, torch.Tensor] = {}
+        self._bufs: dict[tuple[int, int], torch.Tensor] = {}
+        self._retired: list[torch.Tensor] = []
 
     def get(self, device: torch.device, nbytes: int) -> torch.Tensor:
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        buf = self._bufs.get(idx)
+        key = (idx, torch.cuda.current_stream(idx).cuda_stream)
+        buf = self._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                self._retired.append(buf)
             buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-            self._bufs[idx] = buf
+            self._bufs[key] = buf
         return buf
 
 
@@ -77,19 +86,22 @@ WORKSPACE = _Workspace()
 
 
 class _SyncFlags:
-    """Per-device ready-flag buffer for K1's in-kernel split merge: zeroed once,
-    left zeroed by every launch, never shared with other scratch."""
+    """Ready-flag buffer for K1's in-kernel split merge per (device, stream):
+    zeroed once, left zeroed by every launch, never shared with other scratch
+    or with launches on another stream (the flag protocol assumes one K1 in
+    flight per buffer; launches on one stream are ordered)."""
 
     def __init__(self):
-        self._bufs: dict[int, torch.Tensor] = {}
+        self._bufs: dict[tuple[int, int], torch.Tensor] = {}
 
     def get(self, device: torch.device) -> torch.Tensor:
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        buf = self._bufs.get(idx)
+        key = (idx, torch.cuda.current_stream(idx).cuda_stream)
+        buf = self._bufs.get(key)
         if buf is None:
             n = int(_lib.load().fb_sync_flags_count())
             buf = torch.zeros(n, dtype=torch.int64, device=device)
-            self._bufs[idx] = buf
+            self._bufs[key] = buf
         return buf
 
 
@@ -476,6 +488,8 @@ def internal_merge_tok(q_tok, k_tok, v_tok, o_ext, lse_ext, out_tok, scale: floa
                        _tok_stride(out_tok, "out"))
     if o_ext.dtype != torch.float32 or o_ext.numel() != b * hq * B * d or lse_ext.numel() != b * hq * B:
         raise ShapeError("cached partial does not match the queries")
+    if lse_ext.dtype != torch.float32 or not (o_ext.is_contiguous() and lse_ext.is_contiguous()):
+        raise ShapeError("the cached partial must be contiguous float32 (o_ext, lse_ext)")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     _lib.call("fb_internal_merge_tok", _CODE[q_tok.dtype], _p(q_tok), qs, _p(k_tok), ks, _p(v_tok), vs, b, B,
               hq, hkv, d, scale, _p(o_ext), _p(lse_ext), _p(out_tok), _OUT_CODE[out_tok.dtype], os_,
@@ -484,8 +498,9 @@ def internal_merge_tok(q_tok, k_tok, v_tok, o_ext, lse_ext, out_tok, scale: floa
 
 
 def combine(parts, out_dtype: torch.dtype | None = None, want_lse: bool = True,
-            check: bool = False):
-    """K3: log-space merge of partials [(o, lse), ...] over disjoint key groups."""
+            check: bool = False, out=None, lse=None):
+    """K3: log-space merge of partials [(o, lse), ...] over disjoint key groups.
+    out / lse: optional contiguous destinations (out's dtype is the output dtype)."""
     if not 1 <= len(parts) <= 16:
         raise ValueError("combine takes 1..16 partials")
     o0, l0 = parts[0]
@@ -502,9 +517,18 @@ def combine(parts, out_dtype: torch.dtype | None = None, want_lse: bool = True,
     d = o0.shape[-1]
     rows = l0.numel()
     ot, lt = PARTIAL_TYPES[code]
+    if out is not None:
+        out_dtype = out.dtype
+        if out.shape != o0.shape or not out.is_contiguous():
+            raise ShapeError("combine: out must be a contiguous tensor of the partials' shape")
     out_dtype = ot if out_dtype is None else out_dtype
-    out = torch.empty(o0.shape, dtype=out_dtype, device=o0.device)
-    lse = torch.empty(l0.shape, dtype=lt, device=o0.device) if want_lse else None
+    if out is None:
+        out = torch.empty(o0.shape, dtype=out_dtype, device=o0.device)
+    if lse is not None:
+        if lse.shape != l0.shape or lse.dtype != lt or not lse.is_contiguous():
+            raise ShapeError("combine: lse must be a contiguous tensor of the lognorms' shape and dtype")
+    elif want_lse:
+        lse = torch.empty(l0.shape, dtype=lt, device=o0.device)
     cnt = _empty_counter(o0.device) if check else None
     _lib.call("fb_combine", code, len(parts), _lib.ptr_array([_p(o) for o in os_]),
               _lib.ptr_array([_p(l) for l in ls_]), rows, d, _p(out), _OUT_CODE[out_dtype], _p(lse),

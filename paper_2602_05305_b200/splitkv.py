@@ -1,27 +1,36 @@
 """Split-KV context parallelism for the refresh pass.
 
 The committed context of one sequence is split along N across the P ranks
-of one node.  Each rank runs K1 over its shard, giving an fp32 partial
-(O_p, LSE_p) over disjoint key groups; ONE collective exchanges the
-partials and K3 merges them -- exact by the associativity of the log-space
-merge (attention.py:207-233; reference check verification.py:99-117).
-Cached steps read no KV and exchange nothing.
+of one node.  Each rank runs K1 over its shard, giving a partial
+(O_p, LSE_p) over disjoint key groups; ONE exchange moves the partials and K3
+merges them -- exact by the associativity of the log-space merge
+(attention.py:207-233; reference check verification.py:99-117).  Cached steps
+read no KV and exchange nothing.
 
-Two exchange layouts:
-  * ``all_gather``  -- every rank receives all P partials and merges all
-    groups (replicated O_ext; the next cached step can run on any rank).
+K1 writes O and LSE into one packed byte buffer ``[O (groups, rows, d) |
+LSE (groups, rows)]`` so the exchange is a single operation:
+
+  * ``all_gather``  -- one ``all_gather_into_tensor`` of the packed buffer;
+    every rank receives all P partials and merges all groups (replicated
+    O_ext; the next cached step can run on any rank).
   * ``all_to_all``  -- group-sharded: rank r receives the P partials of its
-    groups only (groups split into P contiguous chunks) and merges those
-    (each rank then owns O_ext for its kv-head shard -- the TP layout).
+    group chunk only (groups split into P contiguous chunks) and merges those
+    (each rank then owns O_ext for its kv-head shard -- the TP layout).  The
+    O and LSE slices for every peer go out as one grouped point-to-point
+    exchange (``batch_isend_irecv``: with NCCL one ncclGroupStart/End, one
+    kernel launch); the local chunk never leaves the device.
 
 The local partial and the merge default to the CUDA kernels (K1, K3); the
 hooks exist so the collective choreography can be tested with world-size-2
 ``gloo`` process groups on CPU, where tests pass oracle-backed callables.
+With a gloo group and CUDA tensors the packed buffer is staged through host
+memory (``host_staged``), which lets several processes share one GPU in
+tests; NCCL groups exchange device memory directly.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Callable
 
 import torch
@@ -49,19 +58,46 @@ def group_chunks(groups: int, world: int) -> list[tuple[int, int]]:
 
 
 PartialFn = Callable[..., tuple[torch.Tensor, torch.Tensor]]
-CombineFn = Callable[[list], tuple[torch.Tensor, torch.Tensor]]
+CombineFn = Callable[..., tuple[torch.Tensor, torch.Tensor]]
+
+# (O dtype, LSE dtype) of a partial for each input dtype (kernels.PARTIAL_TYPES)
+_PARTIAL_DTYPES = {torch.bfloat16: (torch.float32, torch.float32),
+                   torch.float32: (torch.float32, torch.float64),
+                   torch.float64: (torch.float64, torch.float64)}
 
 
-def _default_partial(q, k, v, n_local, scale):
+def _default_partial(q, k, v, n_local, scale, out, lse):
     from . import kernels as K
 
-    return K.attention_partial(q, k, v, 0, n_local, scale)
+    return K.attention_partial(q, k, v, 0, n_local, scale, out=out, lse=lse)
 
 
-def _default_combine(parts):
+def _default_combine(parts, out=None, lse=None):
     from . import kernels as K
 
-    return K.combine(parts)
+    return K.combine(parts, out=out, lse=lse)
+
+
+class PackedPartial:
+    """One byte buffer holding a partial's O [groups, rows, d] then its LSE
+    [groups, rows] (LSE offset rounded up to 16 bytes, the whole record to 256
+    so stacked records keep the kernels' vector alignment)."""
+
+    def __init__(self, groups: int, rows: int, d: int, in_dtype: torch.dtype, device, lead: int = 0):
+        self.ot, self.lt = _PARTIAL_DTYPES[in_dtype]
+        self.shape = (groups, rows, d)
+        self.o_bytes = groups * rows * d * torch.empty((), dtype=self.ot).element_size()
+        self.l_off = -(-self.o_bytes // 16) * 16
+        self.l_end = self.l_off + groups * rows * torch.empty((), dtype=self.lt).element_size()
+        self.nbytes = -(-self.l_end // 256) * 256
+        lead_shape = (lead,) if lead else ()
+        self.buf = torch.empty(lead_shape + (self.nbytes,), dtype=torch.uint8, device=device)
+
+    def views(self, buf: torch.Tensor):
+        g, r, d = self.shape
+        o = buf[..., :self.o_bytes].view(self.ot).view(buf.shape[:-1] + (g, r, d))
+        l = buf[..., self.l_off:self.l_end].view(self.lt).view(buf.shape[:-1] + (g, r))
+        return o, l
 
 
 @dataclass
@@ -72,51 +108,83 @@ class SplitKVRefresh:
     layout: str = "all_gather"
     local_partial: PartialFn = _default_partial
     combine: CombineFn = _default_combine
+    # filled per call: whether the last exchange went through host memory
+    host_staged: bool = field(default=False, init=False)
 
     def __post_init__(self):
         if self.layout not in ("all_gather", "all_to_all"):
             raise ValueError(f"unknown layout {self.layout!r}")
 
-    def __call__(self, q, k_shard, v_shard, n_local: int, scale: float | None = None):
+    def _stage(self, t: torch.Tensor) -> bool:
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
+    def __call__(self, q, k_shard, v_shard, n_local: int, scale: float | None = None, out=None, lse=None):
         """q [groups, rows, d]; k/v_shard [groups, cap_local, d] with this rank's
         n_local committed rows.  Returns (o, lse): all groups for all_gather,
-        this rank's group chunk for all_to_all."""
+        this rank's group chunk for all_to_all (written into out / lse when
+        given)."""
         on = dist.is_available() and dist.is_initialized()
         world = dist.get_world_size(self.group) if on else 1
-        o, l = self.local_partial(q, k_shard, v_shard, n_local, scale)
-        groups = o.shape[0]
-        if world == 1:
-            return o, l
+        rank = dist.get_rank(self.group) if on else 0
+        groups, rows, d = q.shape
+        if world == 1:  # nothing to exchange: K1 straight into the destination
+            return self.local_partial(q, k_shard, v_shard, n_local, scale, out, lse)
+        pk = PackedPartial(groups, rows, d, q.dtype, q.device)
+        o, l = pk.views(pk.buf)
+        self.local_partial(q, k_shard, v_shard, n_local, scale, o, l)
         if self.layout == "all_gather":
-            # concatenated along dim 0 (the form every backend accepts), viewed as [P, ...]
-            o_all = torch.empty((world * o.shape[0],) + tuple(o.shape[1:]), dtype=o.dtype,
-                                device=o.device)
-            l_all = torch.empty((world * l.shape[0],) + tuple(l.shape[1:]), dtype=l.dtype,
-                                device=l.device)
-            dist.all_gather_into_tensor(o_all, o.contiguous(), group=self.group)
-            dist.all_gather_into_tensor(l_all, l.contiguous(), group=self.group)
-            return self._merge(o_all.view(world, *o.shape), l_all.view(world, *l.shape))
-        # all_to_all: rank r gets every rank's partial for its group chunk
+            return self._merge(self._all_gather(pk, world), out, lse)
         chunks = group_chunks(groups, world)
         if any(hi - lo != chunks[0][1] - chunks[0][0] for lo, hi in chunks):
             raise ShapeError(f"all_to_all needs groups ({groups}) divisible by world ({world})")
-        per = chunks[0][1] - chunks[0][0]
-        o_in = o.contiguous().view(world, per, *o.shape[1:])
-        l_in = l.contiguous().view(world, per, *l.shape[1:])
-        o_out = torch.empty_like(o_in)
-        l_out = torch.empty_like(l_in)
-        dist.all_to_all_single(o_out, o_in, group=self.group)
-        dist.all_to_all_single(l_out, l_in, group=self.group)
-        return self._merge(o_out, l_out)
+        lo, hi = chunks[rank]
+        parts = self._all_to_all(o, l, chunks, rank, world)
+        parts[rank] = (o[lo:hi], l[lo:hi])
+        return self._merge(parts, out, lse)
 
-    def _merge(self, o_all, l_all):
-        parts = [(o_all[p], l_all[p]) for p in range(o_all.shape[0])]
-        out = None
+    def _all_gather(self, pk: PackedPartial, world: int):
+        stage = self._stage(pk.buf)
+        self.host_staged = stage
+        src = pk.buf.cpu() if stage else pk.buf
+        dst = torch.empty((world, pk.nbytes), dtype=torch.uint8, device=src.device)
+        dist.all_gather_into_tensor(dst.view(-1), src, group=self.group)
+        if stage:
+            dst = dst.to(pk.buf.device)
+        o_all, l_all = pk.views(dst)
+        return [(o_all[p], l_all[p]) for p in range(world)]
+
+    def _all_to_all(self, o, l, chunks, rank: int, world: int):
+        stage = self._stage(o)
+        self.host_staged = stage
+        per = chunks[0][1] - chunks[0][0]
+        dev = torch.device("cpu") if stage else o.device
+        src_o = o.cpu() if stage else o
+        src_l = l.cpu() if stage else l
+        recv_o = torch.empty((world, per) + tuple(o.shape[1:]), dtype=o.dtype, device=dev)
+        recv_l = torch.empty((world, per) + tuple(l.shape[1:]), dtype=l.dtype, device=dev)
+        ops = []
+        for p in range(world):
+            if p == rank:
+                continue
+            plo, phi = chunks[p]
+            peer = p if self.group is None else dist.get_global_rank(self.group, p)
+            ops.append(dist.P2POp(dist.isend, src_o[plo:phi], peer, self.group, tag=0))
+            ops.append(dist.P2POp(dist.isend, src_l[plo:phi], peer, self.group, tag=1))
+            ops.append(dist.P2POp(dist.irecv, recv_o[p], peer, self.group, tag=0))
+            ops.append(dist.P2POp(dist.irecv, recv_l[p], peer, self.group, tag=1))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if stage:
+            recv_o, recv_l = recv_o.to(o.device), recv_l.to(l.device)
+        return [(recv_o[p], recv_l[p]) for p in range(world)]
+
+    def _merge(self, parts, out=None, lse=None):
         # K3 takes up to 16 partials per launch; fold larger worlds in chunks
-        while len(parts) > 1 or out is None:
+        res = None
+        while True:
             chunk, parts = parts[:16], parts[16:]
-            out = self.combine(chunk)
-            if not parts:
-                break
-            parts = [out] + parts
-        return out
+            last = not parts
+            res = self.combine(chunk, out=out if last else None, lse=lse if last else None)
+            if last:
+                return res
+            parts = [res] + parts

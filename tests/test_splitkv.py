@@ -35,20 +35,26 @@ def test_least_filled_and_group_chunks():
     assert group_chunks(8, 2) == [(0, 4), (4, 8)]
 
 
-def _oracle_partial(q, k, v, n_local, scale):
-    outs, lses = [], []
+def _oracle_partial(q, k, v, n_local, scale, out, lse):
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float64)
+        lse = torch.empty(q.shape[:2], dtype=torch.float64)
     for g in range(q.shape[0]):
         p = orc.partial(q[g].numpy(), k[g, :n_local].numpy(), v[g, :n_local].numpy(), scale)
-        outs.append(p.out)
-        lses.append(p.lognorm)
-    return torch.from_numpy(np.stack(outs)), torch.from_numpy(np.stack(lses))
+        out[g] = torch.from_numpy(p.out)
+        lse[g] = torch.from_numpy(p.lognorm)
+    return out, lse
 
 
-def _oracle_combine(parts):
+def _oracle_combine(parts, out=None, lse=None):
     o, l = parts[0]
     acc = orc.Partial(o.numpy(), l.numpy())
     for o2, l2 in parts[1:]:
         acc = orc.combine(acc, orc.Partial(o2.numpy(), l2.numpy()))
+    if out is not None:
+        out.copy_(torch.from_numpy(acc.out))
+        lse.copy_(torch.from_numpy(acc.lognorm))
+        return out, lse
     return torch.from_numpy(acc.out), torch.from_numpy(acc.lognorm)
 
 
@@ -88,18 +94,18 @@ def _free_port():
 
 
 @pytest.mark.parametrize("layout", ["all_gather", "all_to_all"])
-@pytest.mark.parametrize("n", [50, 1])
-def test_split_kv_world2_gloo_matches_single_process(layout, n):
+@pytest.mark.parametrize("n,world", [(50, 2), (1, 2), (37, 4)])
+def test_split_kv_gloo_matches_single_process(layout, n, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, layout, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, n, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    errs = dict(q.get(timeout=10) for _ in range(2))
+    errs = dict(q.get(timeout=10) for _ in range(world))
     assert max(errs.values()) < 1e-12, errs
 
 
