@@ -58,20 +58,42 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region.
+
+    NVML (pynvml) polled from a thread every 5 ms on the device selected by
+    UUID, so even a sub-second timed region gets tens of samples; falls back
+    to `nvidia-smi -lms 50` when NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu):
         # a UUID ("GPU-...") names the physical device whatever CUDA_VISIBLE_DEVICES says
         self.gpu = gpu
         self.proc = None
         self.lines: list[str] = []
+        self.samples: list[tuple[float, int, float]] = []
         self.t = None
+        self._stop = threading.Event()
+        self._nvml = None
+        self._smax = None
 
     def start(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = (nv.nvmlDeviceGetHandleByUUID(self.gpu) if str(self.gpu).startswith(("GPU-", "MIG-"))
+                 else nv.nvmlDeviceGetHandleByIndex(int(self.gpu)))
+            self._smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nvml = (nv, h)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self._nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
@@ -82,11 +104,36 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.samples.append((sm, rs, pw))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
     def _pump(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self) -> dict:
+        if self._nvml is not None:
+            nv, _ = self._nvml
+            self._stop.set()
+            self.t.join(timeout=2)
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted({nm for _, rs, _ in self.samples for nm, bit in bits.items() if rs & bit})
+            sm = [x[0] for x in self.samples]
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self._smax,
+                    "reasons": reasons, "samples": len(sm), "sampler": "nvml 5 ms",
+                    "power_w_max": max((x[2] for x in self.samples), default=None), "gpu": str(self.gpu)}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -95,7 +142,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
@@ -105,11 +151,12 @@ class ClockSampler:
                 smax = float(parts[2])
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
+            for nm, val in zip(self.NAMES, parts[5:9]):
                 if val.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm), "gpu": str(self.gpu)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": "nvidia-smi 50 ms",
+                "gpu": str(self.gpu)}
 
 
 def gpu_smi_id(device) -> str:
@@ -772,7 +819,7 @@ def main():
         import torch.distributed as dist
 
         # communicator ranks / NVLS visible in the log
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))

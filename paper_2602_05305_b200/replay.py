@@ -43,3 +43,28 @@ def patch_reference_simulator(sim_module, sparse_module=None):
             setattr(sim_module, name, fn)
         for name, fn in saved_sparse.items():
             setattr(sparse_module, name, fn)
+
+
+VERIFICATION_PATCHED = ("attention_dense", "attention_partial", "attention_streamed",
+                        "combine_partials", "merge_partials")
+
+
+@contextlib.contextmanager
+def patch_reference(pkg):
+    """Route every attention evaluation of the reference package ``pkg``
+    (the imported ``flashblock``) through libfb200.so: the step driver
+    (simulator.py:28-34), the sparse module (sparse.py:19-25) and the
+    invariant suite (verification.py:14) import the functions by name, so
+    their module-level names are swapped for the device implementations.
+    The reference's own policy, KV cache, counters, model and checks run
+    unchanged -- its verification suite and acceptance criteria then test the
+    device path."""
+    saved = {name: getattr(pkg.verification, name) for name in VERIFICATION_PATCHED}
+    try:
+        for name in VERIFICATION_PATCHED:
+            setattr(pkg.verification, name, getattr(A, name))
+        with patch_reference_simulator(pkg.simulator, pkg.sparse):
+            yield
+    finally:
+        for name, fn in saved.items():
+            setattr(pkg.verification, name, fn)
