@@ -86,9 +86,23 @@ def _check_qkv(q, keys, values) -> None:
         raise ShapeError(f"key dim {keys.shape[1]} != query dim {q.shape[1]}")
     if values.shape[0] != keys.shape[0]:
         raise ShapeError(f"{values.shape[0]} value rows for {keys.shape[0]} keys")
-    if values.shape[1] != q.shape[1]:
-        raise ShapeError(f"value dim {values.shape[1]} != query dim {q.shape[1]} "
-                         "(the device kernels need d_v == d)")
+
+
+def _widen(qt, kt, vt):
+    """The kernels take one head_dim for q, k and v; the reference allows a
+    value width d_v != d (its shift-stability check attends [n, 17] keys with
+    [n, 16] values, verification.py:137-147).  Zero columns are exact padding:
+    appended to q and k they add 0 * 0 to every score, appended to v they give
+    zero output columns that are sliced off.  Returns (q, k, v, d_v)."""
+    d, dv = qt.shape[-1], vt.shape[-1]
+    if dv == d:
+        return qt, kt, vt, dv
+    if dv < d:
+        vt = torch.cat([vt, vt.new_zeros(vt.shape[:-1] + (d - dv,))], dim=-1)
+    else:
+        qt = torch.cat([qt, qt.new_zeros(qt.shape[:-1] + (dv - d,))], dim=-1)
+        kt = torch.cat([kt, kt.new_zeros(kt.shape[:-1] + (dv - d,))], dim=-1)
+    return qt, kt, vt, dv
 
 
 @dataclass
@@ -136,8 +150,9 @@ class AttnPartial:
 def _partial_dev(q, keys, values, scale, begin=0, end=None):
     """Device partial of keys[begin:end] for the 2-D reference signature."""
     dt = _common_dtype(q, keys, values)
-    qt, kt, vt = _to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt)
-    return K.attention_partial(qt, kt, vt, begin, end, scale)
+    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
+    o, l = K.attention_partial(qt, kt, vt, begin, end, scale)
+    return o[..., :dv], l
 
 
 def _wrap(o3, l3, as_numpy: bool, out_np_dtype=None) -> AttnPartial:
@@ -166,7 +181,9 @@ def attention_dense(q, keys, values, scale: float | None = None):
     dt = _common_dtype(q, keys, values)
     if dt != torch.bfloat16:
         dt = torch.float64
-    o, _ = K.attention_partial(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt), 0, None, scale)
+    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
+    o, _ = K.attention_partial(qt, kt, vt, 0, None, scale)
+    o = o[..., :dv]
     if _is_np(q):
         return o[0].cpu().numpy().astype(np.float64, copy=False)
     return o[0]
@@ -197,10 +214,11 @@ def attention_streamed(q, keys, values, boundary: int, scale: float | None = Non
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[1])
     dt = _common_dtype(q, keys, values)
-    qt, kt, vt = _to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt)
+    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
     n = kt.shape[0]
     eo, el = K.attention_partial(qt, kt, vt, 0, boundary, scale)
     io, il = K.attention_partial(qt, kt, vt, boundary, n, scale)
+    eo, io = eo[..., :dv], io[..., :dv]
     np_out = q.dtype if _is_np(q) else None
     return _wrap(eo, el, _is_np(q), np_out), _wrap(io, il, _is_np(q), np_out)
 
@@ -299,13 +317,17 @@ def attention_with_reuse(q, entry: CacheEntry | None, internal_keys, internal_va
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[1])
     dt = _common_dtype(q, internal_keys, internal_values)
-    qt = _to_dev(q, dt)
-    kt, vt = _to_dev(internal_keys, dt), _to_dev(internal_values, dt)
+    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(internal_keys, dt), _to_dev(internal_values, dt))
     eo, el = _partial_to_dev(entry.partial)
+    if eo.shape[-1] != dv:
+        raise ShapeError(f"cached partial has {eo.shape[-1]} value columns, internal values {dv}")
     ot, lt = K.PARTIAL_TYPES[K.dtype_code(qt)]
     eo, el = eo.to(ot), el.to(lt)
+    if eo.shape[-1] < qt.shape[-1]:
+        eo = torch.cat([eo, eo.new_zeros(eo.shape[:-1] + (qt.shape[-1] - dv,))], dim=-1)
     out, lse_m, (io, il) = K.internal_merge(qt, kt, vt, eo, el, scale, want_lse=True,
                                             want_internal=True)
+    out, io = out[..., :dv], io[..., :dv]
     if bool(torch.isneginf(lse_m).any()):
         raise DegenerateInputError("some query rows have no keys on either side")
     if _is_np(q):

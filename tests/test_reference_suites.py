@@ -206,3 +206,24 @@ def test_acceptance_8_external_partials_stable_under_internal_noise(fb, on_gpu):
         worst_out = min(worst_out, min(r.mean_diag_out for r in result.records))
         worst_in = max(worst_in, max(r.mean_diag_in for r in result.records))
     assert worst_out >= 0.999 and worst_in < 0.9, (worst_out, worst_in)
+
+
+def test_value_width_differs_from_key_width(fb, on_gpu):
+    """d_v != d (the shift check's [n, 17] keys with [n, 16] values) in both
+    directions, against the reference functions themselves."""
+    from paper_2602_05305_b200 import attention as A
+
+    ref = sys.modules["flashblock.attention"]
+    rng = np.random.Generator(np.random.Philox(3))
+    for d, dv in ((17, 16), (8, 24)):
+        q = rng.standard_normal((5, d))
+        k = rng.standard_normal((40, d))
+        v = rng.standard_normal((40, dv))
+        np.testing.assert_allclose(A.attention_dense(q, k, v), ref.attention_dense(q, k, v), atol=1e-12)
+        e, i = A.attention_streamed(q, k, v, 25)
+        re, ri = ref.attention_streamed(q, k, v, 25)
+        assert e.out.shape == (5, dv)
+        np.testing.assert_allclose(A.merge_partials(e, i), ref.merge_partials(re, ri), atol=1e-12)
+        out, _ = A.attention_with_reuse(q, A.CacheEntry(e, 0, 0), k[25:], v[25:])
+        rout, _ = ref.attention_with_reuse(q, ref.CacheEntry(re, 0, 0), k[25:], v[25:])
+        np.testing.assert_allclose(out, rout, atol=1e-12)
