@@ -720,6 +720,8 @@ int fb_internal_merge_tok(int dtype, const void* q, int64_t q_token_stride, cons
   if (flags & ~FB_EXT_STABLE) return fail(FB_ERR_VALUE, "unknown flags");
   if (batch < 0 || block < 1 || num_q_heads < 1 || num_kv_heads < 1) return fail(FB_ERR_SHAPE, "bad extents");
   if (num_q_heads % num_kv_heads) return fail(FB_ERR_SHAPE, "num_q_heads must be a multiple of num_kv_heads");
+  if (head_dim != 128 || (num_q_heads / num_kv_heads) * block > 128 || block > 64)
+    return fail(FB_ERR_UNSUPPORTED, "token-major cached step: d 128, (Hq/Hkv)*B <= 128, 1 <= B <= 64");
   if (batch == 0) return FB_OK;
   if (!q || !k_in || !v_in || !o_ext || !lse_ext || !out)
     return fail(FB_ERR_VALUE, "q, k_in, v_in, o_ext, lse_ext and out are required (device pointers)");

@@ -103,6 +103,8 @@ def test_prefill_subset_and_similarity_validation_need_no_device(lib):
     assert tok(_lib.FB_F32, 2, 32, 32, 8, 128) == _lib.FB_ERR_UNSUPPORTED
     assert tok(_lib.FB_BF16, 2, 32, 32, 6, 128) == _lib.FB_ERR_SHAPE
     assert tok(_lib.FB_BF16, 2, 32, 32, 8, 64) == _lib.FB_ERR_UNSUPPORTED
+    # supported shape but null device pointers -> ValueError before any tensor map is built
+    assert tok(_lib.FB_BF16, 2, 32, 32, 8, 128) == _lib.FB_ERR_VALUE
     assert tok(_lib.FB_BF16, 2, 64, 32, 8, 128) == _lib.FB_ERR_UNSUPPORTED  # G * B = 256 rows
     assert tok(_lib.FB_BF16, 2, 32, 32, 8, 128, fl=8) == _lib.FB_ERR_VALUE
     assert tok(_lib.FB_BF16, 0, 32, 32, 8, 128) == _lib.FB_OK  # empty batch: nothing to do
