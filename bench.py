@@ -346,7 +346,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     outs = [torch.empty(b, HQ, BLK, D, device=dev, dtype=torch.bfloat16) for _ in range(LAYERS)]
     eng = FlashBlockAttention(LAYERS, b, HQ, HKV, BLK, D, device=dev, config=ReuseConfig(tau=TAU))
     groups, rows = b * HKV, (HQ // HKV) * BLK
-    o_scr = torch.empty(groups, rows, D, device=dev, dtype=torch.float32)
+    # the full-recompute baseline and the K1 roofline leg write the partial in
+    # the engine's cached-partial layout (bf16 O, fp32 LSE)
+    o_scr = torch.empty(groups, rows, D, device=dev, dtype=eng.ext_dtype)
+    EXT_B = eng.o_ext.element_size()
     l_scr = torch.empty(groups, rows, device=dev, dtype=torch.float32)
     sched = refresh_schedule(ReuseConfig(tau=TAU), BLK, STEPS_PER_BLOCK, UNMASK_PER_STEP)
     n_ref = sum(1 for d in sched if d is Decision.RECOMPUTE)
@@ -413,7 +416,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ---- K1 roofline: refresh kernel pair (tcgen05 + split combine) timed alone
     kv_bytes = 2 * b * HKV * CTX * D * 2
-    k1_bytes = kv_bytes + b * HQ * BLK * D * 2 + b * HQ * BLK * D * 4 + b * HQ * BLK * 4
+    k1_bytes = kv_bytes + b * HQ * BLK * D * 2 + b * HQ * BLK * D * EXT_B + b * HQ * BLK * 4
     k1_flops = 4 * b * HQ * BLK * CTX * D
     qg = [K.gqa_view(qs[l], HKV) for l in range(LAYERS)]
     kg = [kc[l].view(groups, cap, D) for l in range(LAYERS)]
@@ -458,7 +461,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ms_full = timed(g_full, max(1, args.steps // 2), max(3, args.warmup // 2))
     steps_full = max(1, args.steps // 2)
     full_value = world * b * BLK * steps_full / (ms_full / 1000.0)
-    k2_bytes = (b * HQ * BLK * D * 2 + 2 * b * HKV * BLK * D * 2 + b * HQ * BLK * D * 4
+    k2_bytes = (b * HQ * BLK * D * 2 + 2 * b * HKV * BLK * D * 2 + b * HQ * BLK * D * EXT_B
                 + b * HQ * BLK * 4 + b * HQ * BLK * D * 2)
 
     peak, peak_kind = _peaks()
@@ -663,7 +666,9 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     q = [torch.randn((groups, rows, D), device=dev, generator=gq).to(torch.bfloat16) for _ in range(L)]
     ki = [torch.randn((groups, BLK, D), device=dev, generator=gq).to(torch.bfloat16) for _ in range(L)]
     vi = [torch.randn((groups, BLK, D), device=dev, generator=gq).to(torch.bfloat16) for _ in range(L)]
-    o_ext = [torch.empty((per, rows, D), device=dev, dtype=torch.float32) for _ in range(L)]
+    # cached external partial: bf16 O (the engine's layout), fp32 LSE; the
+    # exchanged shard partials stay fp32 (splitkv.PackedPartial)
+    o_ext = [torch.empty((per, rows, D), device=dev, dtype=torch.bfloat16) for _ in range(L)]
     l_ext = [torch.empty((per, rows), device=dev, dtype=torch.float32) for _ in range(L)]
     out = [torch.empty((per, rows, D), device=dev, dtype=torch.bfloat16) for _ in range(L)]
     refresh = SplitKVRefresh(layout="all_to_all")
@@ -732,7 +737,8 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     ms_cached = timed(g_cached.replay, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
 
     # K1 on the local shard alone (roofline of the dominant kernel at this P)
-    o_s = torch.empty((groups, rows, D), device=dev, dtype=torch.float32)
+    o_dt = torch.bfloat16 if world == 1 else torch.float32  # N=1 writes the cached partial directly
+    o_s = torch.empty((groups, rows, D), device=dev, dtype=o_dt)
     l_s = torch.empty((groups, rows), device=dev, dtype=torch.float32)
 
     def k1_only():
@@ -740,7 +746,7 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
             K.attention_partial(q[l], kc[l], vc[l], 0, n_loc, None, out=o_s, lse=l_s)
 
     ms_k1 = timed(k1_only, 2, 1) / 2 / L
-    k1_bytes = 2 * groups * n_loc * D * 2 + groups * rows * D * 2 + groups * rows * (D + 1) * 4
+    k1_bytes = 2 * groups * n_loc * D * 2 + groups * rows * D * 2 + groups * rows * (D * o_s.element_size() + 4)
     peak, peak_kind = _peaks()
     if rank == 0:
         value = b * BLK * args.steps / (ms / 1000.0)

@@ -64,6 +64,15 @@ typedef enum fb_status {
 } fb_status;
 
 typedef enum fb_dtype { FB_F64 = 0, FB_F32 = 1, FB_BF16 = 2 } fb_dtype;
+/* OR'ed into dtype FB_BF16 where an entry point says so: the partial out of
+ * the mode is stored as bf16 (the lognorm stays fp32).  The reference keeps a
+ * partial's out in the tensor dtype (attention.py:70-71); for the cached
+ * external partial this halves the bytes every cached step re-reads.
+ * Accepted by fb_attention_partial(_sync/_ragged/_paged/_groups) (o_out
+ * written bf16), fb_internal_merge(_ex) and fb_internal_merge_tok (o_ext read
+ * as bf16; o_int not supported) and fb_combine (every o_parts[p] bf16).
+ * Other entry points reject it (FB_ERR_VALUE). */
+#define FB_PARTIAL_BF16 0x100
 
 /* Message for the last non-OK status returned on this host thread. */
 FB_API const char* fb_last_error(void);

@@ -21,6 +21,7 @@ FB_OK, FB_ERR_SHAPE, FB_ERR_BOUNDS, FB_ERR_DEGENERATE = 0, 1, 2, 3
 FB_ERR_REUSE, FB_ERR_STALE, FB_ERR_CUDA, FB_ERR_VALUE, FB_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
 FB_F64, FB_F32, FB_BF16 = 0, 1, 2
 FB_EXT_STABLE = 1  # fb_internal_merge_ex flag
+FB_PARTIAL_BF16 = 0x100  # OR'ed into FB_BF16: the partial's O is stored as bf16
 
 vp, i64, i32, dbl, sz = C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_size_t
 

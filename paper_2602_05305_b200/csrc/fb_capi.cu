@@ -108,6 +108,18 @@ static int check_dtype(int dt) {
   return FB_OK;
 }
 
+static const char* const PB16_MSG =
+    "FB_PARTIAL_BF16 needs the tcgen05 refresh path (head_dim 64 / 128, 16-byte aligned, non-empty range)";
+
+// dtype with an optional FB_PARTIAL_BF16 bit (BF16 mode only): strips the bit
+static int split_partial_bf16(int& dt, bool& pb) {
+  pb = (dt & FB_PARTIAL_BF16) != 0;
+  dt &= ~FB_PARTIAL_BF16;
+  if (int rc = check_dtype(dt)) return rc;
+  if (pb && dt != FB_BF16) return fail(FB_ERR_VALUE, "FB_PARTIAL_BF16 applies to FB_BF16 mode only");
+  return FB_OK;
+}
+
 template <typename Mode>
 static int attention_partial_t(const void* qv, const void* kv, const void* vv, int64_t groups,
                                int64_t q_rows, int64_t d, int64_t cap, int64_t kb, int64_t ke,
@@ -122,6 +134,10 @@ static int attention_partial_t(const void* qv, const void* kv, const void* vv, i
   auto* l = reinterpret_cast<typename Mode::Tl*>(lse_out);
   const int64_t rows = groups * q_rows;
   const int64_t n = ke - kb;
+  if constexpr (std::is_same<Mode, ModeBF16>::value) {
+    if (n == 0 && partial_out_bf16())
+      return launch_fill_sentinel<__nv_bfloat16, float>(reinterpret_cast<__nv_bfloat16*>(o_out), l, rows, d, st);
+  }
   if (n == 0) return launch_fill_sentinel<typename Mode::To, typename Mode::Tl>(o, l, rows, d, st);
   if constexpr (std::is_same<Mode, ModeBF16>::value) {
     if (sm100_supported(d) && ke < (int64_t(1) << 31) && q_rows < (int64_t(1) << 31) &&
@@ -130,6 +146,7 @@ static int attention_partial_t(const void* qv, const void* kv, const void* vv, i
       return launch_refresh_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, scale, o, l, ws, ws_bytes, st,
                                   reinterpret_cast<unsigned long long*>(sync_flags), n_flags);
     }
+    if (partial_out_bf16()) return fail(FB_ERR_UNSUPPORTED, PB16_MSG);
   }
   RangeMap<Tin> map{k, v, cap * d, kb, ke, d};
   return partial_any<Mode>(q, map, groups, q_rows, d, n, scale, o, l, ws, ws_bytes, st);
@@ -140,7 +157,7 @@ static int internal_merge_t(const void* qv, const void* kv, const void* vv, int6
                             int64_t q_rows, int64_t d, int64_t n_in, double scale,
                             const void* o_ext, const void* lse_ext, void* out, bool out_bf16,
                             void* lse_merged, void* o_int, void* lse_int, int32_t* empty,
-                            cudaStream_t st, bool ext_early = false) {
+                            cudaStream_t st, bool ext_early = false, bool extb = false) {
   using Tin = typename Mode::Tin;
   if constexpr (std::is_same<Mode, ModeBF16>::value) {
     auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
@@ -148,11 +165,13 @@ static int internal_merge_t(const void* qv, const void* kv, const void* vv, int6
         a16(kv) && a16(vv) && a16(o_ext) && a16(out) && a16(o_int) && groups * ((q_rows + 127) / 128) < (1LL << 31))
       return launch_internal_merge_sm100(
           reinterpret_cast<const __nv_bfloat16*>(qv), reinterpret_cast<const __nv_bfloat16*>(kv),
-          reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, n_in, scale,
-          reinterpret_cast<const float*>(o_ext), reinterpret_cast<const float*>(lse_ext), out,
-          out_bf16, reinterpret_cast<float*>(lse_merged), reinterpret_cast<float*>(o_int),
-          reinterpret_cast<float*>(lse_int), empty, ext_early, st);
+          reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d, n_in, scale, o_ext,
+          reinterpret_cast<const float*>(lse_ext), out, out_bf16, reinterpret_cast<float*>(lse_merged),
+          reinterpret_cast<float*>(o_int), reinterpret_cast<float*>(lse_int), empty, ext_early, extb, st);
   }
+  if (extb)  // the SIMT kernel reads the mode's fp32 partial
+    return fail(FB_ERR_UNSUPPORTED, "FB_PARTIAL_BF16 cached step needs the tcgen05 kernel "
+                                    "(head_dim 64 / 128, 1 <= n_in <= 128, 16-byte aligned rows)");
   MergeOut<Mode> mo{};
   mo.o_ext = reinterpret_cast<const typename Mode::To*>(o_ext);
   mo.lse_ext = reinterpret_cast<const typename Mode::Tl*>(lse_ext);
@@ -381,6 +400,7 @@ static int attention_partial_ragged_t(const void* qv, const void* kv, const void
         ws_bytes >= refresh_sm100_ragged_workspace_bytes(groups, q_rows, d))
       return launch_refresh_ragged_sm100(q, k, v, groups, q_rows, d, cap, kb, ends, scale, o, l, ws,
                                          ws_bytes, st);
+    if (partial_out_bf16()) return fail(FB_ERR_UNSUPPORTED, PB16_MSG);
   }
   // SIMT: one split per group (lengths live on the device)
   RaggedMap<Tin> map{k, v, ends, cap * d, kb, cap, d};
@@ -479,6 +499,7 @@ static int attention_partial_groups_t(const void* qv, const void* kv, const void
         (reinterpret_cast<uintptr_t>(v) % 16 == 0) && groups < 65536)
       return launch_refresh_groups_sm100(q, k, v, groups, q_rows, d, cap, kb, ke, glist, n_list,
                                          scale, o, l, ws, ws_bytes, st);
+    if (partial_out_bf16()) return fail(FB_ERR_UNSUPPORTED, PB16_MSG);
   }
   constexpr bool direct_ok = std::is_same<Ta, typename Mode::To>::value &&
                              std::is_same<Ta, typename Mode::Tl>::value;
@@ -542,7 +563,9 @@ int fb_attention_partial_sync(int dtype, const void* q, const void* k, const voi
                               double scale, void* o_out, void* lse_out, void* workspace,
                               size_t workspace_bytes, uint64_t* sync_flags, int64_t n_flags,
                               void* stream) {
-  if (int rc = check_dtype(dtype)) return rc;
+  bool pb = false;
+  if (int rc = split_partial_bf16(dtype, pb)) return rc;
+  ScopedPartialBf16 pb_scope(pb);
   if (sync_flags != nullptr && n_flags < 1) return fail(FB_ERR_VALUE, "sync_flags needs n_flags >= 1");
   if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
@@ -589,7 +612,9 @@ int fb_attention_partial_paged(int dtype, const void* q, const void* k_pages, co
                                int64_t max_pages, int64_t groups, int64_t q_rows, int64_t head_dim,
                                const int32_t* key_len, double scale, void* o_out, void* lse_out,
                                void* workspace, size_t workspace_bytes, void* stream) {
-  if (int rc = check_dtype(dtype)) return rc;
+  bool pb = false;
+  if (int rc = split_partial_bf16(dtype, pb)) return rc;
+  ScopedPartialBf16 pb_scope(pb);
   if (groups < 0 || q_rows < 0 || head_dim < 1 || num_pages < 0 || max_pages < 0)
     return fail(FB_ERR_SHAPE, "bad extents");
   if (page_table == nullptr || key_len == nullptr)
@@ -714,7 +739,8 @@ int fb_internal_merge_tok(int dtype, const void* q, int64_t q_token_stride, cons
                           int64_t batch, int64_t block, int64_t num_q_heads, int64_t num_kv_heads,
                           int64_t head_dim, double scale, const void* o_ext, const void* lse_ext,
                           void* out, int out_dtype, int64_t out_token_stride, int flags, void* stream) {
-  if (int rc = check_dtype(dtype)) return rc;
+  bool extb = false;
+  if (int rc = split_partial_bf16(dtype, extb)) return rc;
   if (dtype != FB_BF16) return fail(FB_ERR_UNSUPPORTED, "token-major cached step: bf16");
   if (out_dtype != FB_BF16 && out_dtype != FB_F32) return fail(FB_ERR_VALUE, "BF16 mode writes F32 or BF16 output");
   if (flags & ~FB_EXT_STABLE) return fail(FB_ERR_VALUE, "unknown flags");
@@ -736,9 +762,8 @@ int fb_internal_merge_tok(int dtype, const void* q, int64_t q_token_stride, cons
   return launch_internal_merge_tok_sm100(
       reinterpret_cast<const __nv_bfloat16*>(q), q_token_stride, reinterpret_cast<const __nv_bfloat16*>(k_in),
       k_token_stride, reinterpret_cast<const __nv_bfloat16*>(v_in), v_token_stride, batch, block, num_q_heads,
-      num_kv_heads, head_dim, scale, reinterpret_cast<const float*>(o_ext),
-      reinterpret_cast<const float*>(lse_ext), out, out_token_stride, out_dtype == FB_BF16,
-      (flags & FB_EXT_STABLE) != 0, as_stream(stream));
+      num_kv_heads, head_dim, scale, o_ext, reinterpret_cast<const float*>(lse_ext), out, out_token_stride,
+      out_dtype == FB_BF16, (flags & FB_EXT_STABLE) != 0, extb, as_stream(stream));
 }
 
 int fb_commit_block_paged(int dtype, void* k_pages, void* v_pages, int64_t page_rows,
@@ -762,7 +787,9 @@ int fb_attention_partial_groups(int dtype, const void* q, const void* k, const v
                                 const int32_t* group_list, int64_t n_list, double scale,
                                 void* o_out, void* lse_out, void* workspace,
                                 size_t workspace_bytes, void* stream) {
-  if (int rc = check_dtype(dtype)) return rc;
+  bool pb = false;
+  if (int rc = split_partial_bf16(dtype, pb)) return rc;
+  ScopedPartialBf16 pb_scope(pb);
   if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0 || n_list < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
   if (n_list > groups) return fail(FB_ERR_SHAPE, "group list longer than the batch of groups");
@@ -847,7 +874,9 @@ int fb_attention_partial_ragged(int dtype, const void* q, const void* k, const v
                                 int64_t kv_rows_cap, int64_t key_begin, const int32_t* key_end,
                                 double scale, void* o_out, void* lse_out, void* workspace,
                                 size_t workspace_bytes, void* stream) {
-  if (int rc = check_dtype(dtype)) return rc;
+  bool pb = false;
+  if (int rc = split_partial_bf16(dtype, pb)) return rc;
+  ScopedPartialBf16 pb_scope(pb);
   if (groups < 0 || q_rows < 0 || head_dim < 1 || kv_rows_cap < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
   if (key_begin < 0 || key_begin > kv_rows_cap) return fail(FB_ERR_BOUNDS, "key_begin outside the slab");
@@ -938,7 +967,8 @@ int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void*
                          int out_dtype, void* lse_merged, void* o_int, void* lse_int,
                          int32_t* empty_rows, void* workspace, size_t workspace_bytes, int flags,
                          void* stream) {
-  if (int rc = check_dtype(dtype)) return rc;
+  bool extb = false;
+  if (int rc = split_partial_bf16(dtype, extb)) return rc;
   if (flags & ~FB_EXT_STABLE) return fail(FB_ERR_VALUE, "unknown fb_internal_merge_ex flags");
   if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0)
     return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
@@ -957,6 +987,8 @@ int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void*
     default:
       if (out_dtype != FB_F32 && out_dtype != FB_BF16)
         return fail(FB_ERR_VALUE, "BF16 mode writes F32 or BF16 output");
+      if (extb && (o_int != nullptr || lse_int != nullptr))
+        return fail(FB_ERR_UNSUPPORTED, "FB_PARTIAL_BF16 cached step: o_int / lse_int not supported");
       if (sm100_supported(head_dim) && !sm100_k2_supported(head_dim, n_in) && n_in > 0 &&
           n_in < (int64_t(1) << 31) && workspace != nullptr &&
           workspace_bytes >= fb_internal_merge_workspace_bytes(dtype, groups, q_rows, head_dim, n_in)) {
@@ -970,9 +1002,11 @@ int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void*
         // without an lse_merged output the K3 merge with the cached external
         // partial runs inside K1's split-merge kernel (MergeFinal): one launch
         // and one pass over the internal partial fewer
-        const MergeFinal fin{reinterpret_cast<const float*>(o_ext), reinterpret_cast<const float*>(lse_ext),
-                             out, out_dtype == FB_BF16 ? 1 : 0, empty_rows};
+        const MergeFinal fin{o_ext, reinterpret_cast<const float*>(lse_ext), out, out_dtype == FB_BF16 ? 1 : 0,
+                             empty_rows, extb ? 1 : 0};
         const bool fuse = lse_merged == nullptr;
+        if (extb && !fuse)
+          return fail(FB_ERR_UNSUPPORTED, "FB_PARTIAL_BF16 large-block cached step: lse_merged not supported");
         int rc = launch_refresh_sm100(reinterpret_cast<const __nv_bfloat16*>(q),
                                       reinterpret_cast<const __nv_bfloat16*>(k_in),
                                       reinterpret_cast<const __nv_bfloat16*>(v_in), groups, q_rows,
@@ -988,7 +1022,7 @@ int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void*
       }
       return internal_merge_t<ModeBF16>(q, k_in, v_in, groups, q_rows, head_dim, n_in, scale, o_ext,
                                         lse_ext, out, out_dtype == FB_BF16, lse_merged, o_int,
-                                        lse_int, empty_rows, st, (flags & FB_EXT_STABLE) != 0);
+                                        lse_int, empty_rows, st, (flags & FB_EXT_STABLE) != 0, extb);
   }
 }
 

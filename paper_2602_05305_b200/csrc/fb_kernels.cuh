@@ -63,11 +63,12 @@ int launch_fill_sentinel(To* o, Tl* l, int64_t rows, int64_t head_dim, cudaStrea
 // write the attention output (bf16 or fp32) instead of a partial, counting
 // rows empty on both sides -- K3 folded into the same launch.
 struct MergeFinal {
-  const float* o2;
+  const void* o2;  // fp32, or bf16 when o2_bf16
   const float* l2;
   void* out;
   int out_bf16;
   int32_t* empty_rows;
+  int o2_bf16;
 };
 
 // tcgen05 / TMA refresh kernel (bf16, head_dim 64 or 128): normalised fp32
@@ -107,6 +108,14 @@ struct ScopedPaging {
   explicit ScopedPaging(const PagingCtx* p);
   ~ScopedPaging();
 };
+// Partial-out context (FB_PARTIAL_BF16): set for the duration of one
+// fb_attention_partial* call on the calling thread; the refresh launcher then
+// writes the final partial O as bf16 (split workspace partials stay fp32).
+struct ScopedPartialBf16 {
+  explicit ScopedPartialBf16(bool on);
+  ~ScopedPartialBf16();
+};
+bool partial_out_bf16();
 int launch_refresh_paged_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_pages,
                                const __nv_bfloat16* v_pages, int64_t num_pages, int64_t page_rows,
                                const int32_t* page_table, int64_t max_pages, int64_t groups,
@@ -166,14 +175,14 @@ bool sm100_k2_supported(int64_t head_dim, int64_t n_in);
 int launch_internal_merge_tok_sm100(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat16* k,
                                     int64_t k_ts, const __nv_bfloat16* v, int64_t v_ts, int64_t batch,
                                     int64_t B, int64_t Hq, int64_t Hkv, int64_t d, double scale,
-                                    const float* o_ext, const float* lse_ext, void* out, int64_t out_ts,
-                                    bool out_bf16, bool ext_early, cudaStream_t st);
+                                    const void* o_ext, const float* lse_ext, void* out, int64_t out_ts,
+                                    bool out_bf16, bool ext_early, bool extb, cudaStream_t st);
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,
                                 const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
-                                int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
+                                int64_t head_dim, int64_t n_in, double scale, const void* o_ext,
                                 const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
                                 float* o_int, float* lse_int, int32_t* empty, bool ext_early,
-                                cudaStream_t st);
+                                bool extb, cudaStream_t st);
 
 // cross-step similarity (fb_similarity.cu)
 template <typename T>

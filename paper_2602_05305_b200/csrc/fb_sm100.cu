@@ -89,6 +89,7 @@ struct Sched {
   int kv_keep;             // K/V tiles re-read by other query tiles of the group: keep in L2
   int rr;                  // pair kernel: round-robin whole items (block-causal), no stream-K
   int vprod;               // refresh kernel: warp 3 issues the V tiles (warp 0 Q and K)
+  int o_bf16;              // final partial O rows stored as bf16 (FB_PARTIAL_BF16)
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -714,7 +715,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               }
             }
           }
-          ptx::st_row32(dst + c * 32, v);
+          if (sc.o_bf16 && (whole || owner))  // final row into a bf16 partial
+            ptx::st_row32_bf16(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + c * 32, v);
+          else
+            ptx::st_row32(dst + c * 32, v);
         }
       }
       if (row == 0 && wg == 0 && seg == 0) stamp(6);
@@ -845,7 +849,14 @@ __device__ __forceinline__ void final_merge_row(const Sched& sc, int item, int r
   const float iz = live ? 1.f / (wp + w2) : 0.f;
   if (col) {
     float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (w2 != 0.f) o2 = *reinterpret_cast<const float4*>(fin.o2 + orow * D + c);
+    if (w2 != 0.f) {
+      if (fin.o2_bf16) {
+        const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(fin.o2) + orow * D + c);
+        o2 = make_float4(ptx::bf16_lo(u.x), ptx::bf16_hi(u.x), ptx::bf16_lo(u.y), ptx::bf16_hi(u.y));
+      } else {
+        o2 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(fin.o2) + orow * D + c);
+      }
+    }
     const float4 o = make_float4((__fmul_rn(wp, pv.x) + __fmul_rn(w2, o2.x)) * iz,
                                  (__fmul_rn(wp, pv.y) + __fmul_rn(w2, o2.y)) * iz,
                                  (__fmul_rn(wp, pv.z) + __fmul_rn(w2, o2.z)) * iz,
@@ -888,7 +899,10 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
     return;
   }
   if (ib == ie) {  // no keys (ragged length 0): the empty partial
-    for (int c = lane; c < D; c += 32) o_out[orow * D + c] = 0.f;
+    if (sc.o_bf16)
+      for (int c = lane; c < D; c += 32) reinterpret_cast<__nv_bfloat16*>(o_out)[orow * D + c] = __float2bfloat16(0.f);
+    else
+      for (int c = lane; c < D; c += 32) o_out[orow * D + c] = 0.f;
     if (lane == 0) lse_out[orow] = -INFINITY;
     return;
   }
@@ -899,9 +913,17 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
   float mx, z;
   const float4 acc = merge_segments(sc, item, row, bm, D, c_first, nseg, ws_o, ws_l, lane, mx, z);
   const float iz = 1.f / z;
-  if (lane * 4 < D)
-    *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) =
-        make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
+  if (lane * 4 < D) {
+    if (sc.o_bf16) {
+      uint2 u;
+      u.x = ptx::pack_bf16(acc.x * iz, acc.y * iz);
+      u.y = ptx::pack_bf16(acc.z * iz, acc.w * iz);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + lane * 4) = u;
+    } else {
+      *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) =
+          make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
+    }
+  }
   if (lane == 0) lse_out[orow] = mx + logf(z);
 }
 
@@ -1429,6 +1451,10 @@ static int pair_mode() {  // 0 never, 1 always, 2 block-causal only
   }
   return m;
 }
+static thread_local bool t_partial_bf16 = false;
+bool partial_out_bf16() { return t_partial_bf16; }
+ScopedPartialBf16::ScopedPartialBf16(bool on) { t_partial_bf16 = on; }
+ScopedPartialBf16::~ScopedPartialBf16() { t_partial_bf16 = false; }
 static thread_local const PagingCtx* t_paging = nullptr;
 const PagingCtx* current_paging() { return t_paging; }
 ScopedPaging::ScopedPaging(const PagingCtx* p) { t_paging = p; }
@@ -1693,11 +1719,13 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ga.sel_tiles = (int)((gs->n_list + 7) / 8);
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   }
+  const bool o_bf16 = !GATHER && partial_out_bf16();
+  if (o_bf16 && fin != nullptr) return fail(FB_ERR_UNSUPPORTED, "bf16 partial with a fused final merge");
   if constexpr (!GATHER && D == 128) {
     const int qm = quad_mode();
     const bool pair_forced = (g_pair_override >= 0 ? g_pair_override : pair_mode()) == 1;
     const bool quad_on = !pair_forced && (qm == 1 || (qm == 2 && causal != nullptr));
-    if (quad_on && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
+    if (quad_on && !o_bf16 && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
       const int qrc = launch_quad_128(k, mq, mk, mv, groups, q_rows, key_begin, key_end, scale, o_out, lse_out,
                                       ws, ws_bytes, st, causal, glist, n_list, fin, paged);
       if (qrc != -1) return qrc;
@@ -1706,7 +1734,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   if constexpr (!GATHER && D == 128) {
     const int pm = g_pair_override >= 0 ? g_pair_override : pair_mode();
     const bool pair_on = pm == 1 || (pm == 2 && causal != nullptr);
-    if (pair_on && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
+    if (pair_on && !o_bf16 && key_len == nullptr && q_rows > sm100::BM && g_k1_diag == 0) {
       const int prc = launch_pair_128(k, mq, mv, groups, q_rows, kv_rows_cap, key_begin, key_end, scale,
                                       o_out, lse_out, ws, ws_bytes, st, causal, glist, n_list, fin,
                                       paged, num_pages);
@@ -1742,6 +1770,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   RefreshPlan p = plan_refresh(glist ? n_list : groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr, glist};
   sc.kv_keep = p.m_tiles > 1 && kv_keep_enabled();
+  sc.o_bf16 = o_bf16 ? 1 : 0;
   {
     // V from a second producer thread: measured on the gathered path (C4
     // cached sparse step, 16 small boxes per K / V tile) 11 % faster at 50 %

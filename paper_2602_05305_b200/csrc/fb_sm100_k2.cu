@@ -76,10 +76,12 @@ struct TokLayout {
 #ifndef FB_K2_MIN_BLOCKS
 #define FB_K2_MIN_BLOCKS 2  // diagnostics build knob
 #endif
-template <int D, int NT, int SPLIT, bool TRACE = false, bool TOK = false>
+// EXTB: the cached external partial's O is bf16 (fp32 LSE), half the bytes of
+// the fp32 layout; the merge arithmetic stays fp32.
+template <int D, int NT, int SPLIT, bool TRACE = false, bool TOK = false, bool EXTB = false>
 __global__ void __launch_bounds__(THREADS, FB_K2_MIN_BLOCKS)  // (3 CTAs/SM at 136 regs: 8 % slower, C2 b=16)
 internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ o_ext,
+                      const __grid_constant__ CUtensorMap tm_v, const void* __restrict__ o_ext_,
                       const float* __restrict__ lse_ext, int q_rows, int m_tiles, int n_in,
                       float scale_log2, void* __restrict__ out, int out_bf16,
                       float* __restrict__ lse_merged, float* __restrict__ o_int,
@@ -117,8 +119,32 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 
   // this thread's row of the cached external partial (its column slice)
   float le = -INFINITY;
-  float oe[C::PRE];
+  const float* o_ext = reinterpret_cast<const float*>(o_ext_);
+  const __nv_bfloat16* o_extb = reinterpret_cast<const __nv_bfloat16*>(o_ext_);
+  float oe[EXTB ? 1 : C::PRE];
+  uint32_t ob[EXTB ? C::PRE / 2 : 1];  // bf16x2 words
   auto load_ext = [&]() {
+    if constexpr (EXTB) {
+      if (live_row) {
+        le = __ldg(lse_ext + rr);
+        const __nv_bfloat16* srow = o_extb + rr * D + col0;
+        if ((reinterpret_cast<uintptr_t>(srow) & 31) == 0 && C::PRE % 16 == 0) {  // 256-bit loads
+#pragma unroll
+          for (int j = 0; j < C::PRE / 16; ++j) ptx::ld_v8_nc_b32(srow + 16 * j, ob + 8 * j);
+        } else {
+          const uint4* src = reinterpret_cast<const uint4*>(srow);
+#pragma unroll
+          for (int j = 0; j < C::PRE / 8; ++j) {
+            const uint4 v4 = __ldg(src + j);
+            ob[4 * j] = v4.x; ob[4 * j + 1] = v4.y; ob[4 * j + 2] = v4.z; ob[4 * j + 3] = v4.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < C::PRE / 2; ++i) ob[i] = 0u;
+      }
+      return;
+    }
     if (live_row) {
       le = __ldg(lse_ext + rr);
       const float* srow = o_ext + rr * D + col0;
@@ -278,7 +304,31 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     for (int c = 0; c < C::DC / 32; ++c) {
       ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
       float oc[32];
-      if (c * 32 < C::PRE) {
+      if constexpr (EXTB) {
+        if (c * 32 < C::PRE) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t u = ob[((c * 32) % C::PRE) / 2 + i];
+            oc[2 * i] = ptx::bf16_lo(u);
+            oc[2 * i + 1] = ptx::bf16_hi(u);
+          }
+        } else if (live_row) {  // columns past the prefetched ones
+          const uint4* src = reinterpret_cast<const uint4*>(o_extb + rr * D + col0 + c * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 v4 = __ldg(src + j);
+            const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              oc[8 * j + 2 * k] = ptx::bf16_lo(w[k]);
+              oc[8 * j + 2 * k + 1] = ptx::bf16_hi(w[k]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) oc[i] = 0.f;
+        }
+      } else if (c * 32 < C::PRE) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) oc[i] = oe[(c * 32 + i) % C::PRE];
       } else if (live_row) {  // columns past the prefetched ones (unsplit D = 128)
@@ -356,12 +406,14 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 // issues the TMA loads and the two MMAs.
 constexpr int V2_THREADS = 288;
 
-template <int NT>
+template <int NT, bool EXTB = false>
 struct CfgV2 {
   static constexpr int D = 128;
   static constexpr uint32_t QBOX = BM * 128;   // 16 KB (128 rows x 64 bf16)
   static constexpr uint32_t KBOX = NT * 128;   // NT rows x 64 bf16
-  static constexpr uint32_t EBOX = BM * 128;   // 16 KB (128 rows x 32 fp32)
+  static constexpr uint32_t EBOX = BM * 128;   // 16 KB (128 rows x 32 fp32, or x 64 bf16)
+  static constexpr int NE = EXTB ? 2 : 4;      // O_ext boxes per 128-column row
+  static constexpr int ECOLS = EXTB ? 64 : 32; // O_ext columns per box
   // barriers sit below the 1024-aligned tile area (dynamic shared memory
   // starts 1024-aligned after the 1 KB system reservation, so the tiles begin
   // at base + 1024); two CTAs per SM need SMEM <= 115,712 B
@@ -370,12 +422,12 @@ struct CfgV2 {
   static constexpr uint32_t OFF_V = OFF_K + 2 * KBOX;
   static constexpr uint32_t OFF_E = (OFF_V + 2 * KBOX + 1023) / 1024 * 1024;
   static constexpr uint32_t OFF_X = OFF_K;  // [2][128] floats of WG0, over K (dead after S = Q K^T)
-  static constexpr uint32_t TILES = OFF_E + 4 * EBOX;
+  static constexpr uint32_t TILES = OFF_E + NE * EBOX;
   static constexpr uint32_t SMEM = 1024 + TILES;
   static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;
   static constexpr uint32_t TMEM_COLS = (COL_O + D) <= 256 ? 256 : 512;
   static constexpr uint32_t TX_QKV = 2 * (QBOX + 2 * KBOX);
-  static constexpr uint32_t TX_E = 4 * EBOX;
+  static constexpr uint32_t TX_E = NE * EBOX;
 };
 
 struct BarsV2 {
@@ -383,7 +435,7 @@ struct BarsV2 {
   uint32_t tmem_base;
 };
 
-template <int NT>
+template <int NT, bool EXTB = false>
 __global__ void __launch_bounds__(V2_THREADS, 2)
 internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_e,
@@ -391,7 +443,7 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                          float scale_log2, void* __restrict__ out, int out_bf16,
                          float* __restrict__ lse_merged, float* __restrict__ o_int,
                          float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early) {
-  using C = CfgV2<NT>;
+  using C = CfgV2<NT, EXTB>;
   constexpr int D = C::D;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   BarsV2* bar = reinterpret_cast<BarsV2*>(smem_raw);
@@ -424,8 +476,8 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     if (ext_early) {  // the cached partial is final before this launch: fetch it now
       const uint64_t pol = ptx::policy_evict_first();
       ptx::mbar_expect_tx(&bar->load_e, C::TX_E);
-      for (int b = 0; b < 4; ++b)
-        ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * 32, mt * BM, g, pol);
+      for (int b = 0; b < C::NE; ++b)
+        ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * C::ECOLS, mt * BM, g, pol);
     }
   }
   if (warp == 8) ptx::tmem_alloc(&bar->tmem_base, C::TMEM_COLS);
@@ -441,8 +493,8 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
       const uint64_t pol = ptx::policy_evict_first();
       if (!ext_early) {
         ptx::mbar_expect_tx(&bar->load_e, C::TX_E);
-        for (int b = 0; b < 4; ++b)
-          ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * 32, mt * BM, g, pol);
+        for (int b = 0; b < C::NE; ++b)
+          ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * C::ECOLS, mt * BM, g, pol);
       }
       ptx::mbar_expect_tx(&bar->load_qkv, C::TX_QKV);
       for (int b = 0; b < 2; ++b) {
@@ -539,10 +591,24 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
       const int c = wg * 2 + cc;  // 32-column chunk = fp32 box c
       ptx::tmem_ld32(tmem + lane_off + C::COL_O + c * 32, r);
       float oc[32];
+      if constexpr (EXTB) {  // box c / 2, 16-byte chunks (c % 2) * 4 + j (8 bf16 each)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 v4 = *reinterpret_cast<const float4*>(erow + c * C::EBOX + ((j ^ (row & 7)) << 4));
-        oc[4 * j] = v4.x; oc[4 * j + 1] = v4.y; oc[4 * j + 2] = v4.z; oc[4 * j + 3] = v4.w;
+        for (int j = 0; j < 4; ++j) {
+          const uint4 v4 = *reinterpret_cast<const uint4*>(erow + (c >> 1) * C::EBOX +
+                                                           ((((c & 1) * 4 + j) ^ (row & 7)) << 4));
+          const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            oc[8 * j + 2 * k] = ptx::bf16_lo(w[k]);
+            oc[8 * j + 2 * k + 1] = ptx::bf16_hi(w[k]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v4 = *reinterpret_cast<const float4*>(erow + c * C::EBOX + ((j ^ (row & 7)) << 4));
+          oc[4 * j] = v4.x; oc[4 * j + 1] = v4.y; oc[4 * j + 2] = v4.z; oc[4 * j + 3] = v4.w;
+        }
       }
       ptx::tmem_wait_ld();
       float val[32];
@@ -616,9 +682,9 @@ void set_k2_trace(void* p, int launches) {
 
 template <int D, int NT, int SPLIT>
 static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
-                     int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
+                     int64_t groups, int64_t q_rows, int64_t n_in, double scale, const void* o_ext,
                      const float* lse_ext, void* out, bool out_bf16, float* lse_merged, float* o_int,
-                     float* lse_int, int32_t* empty, bool ext_early, cudaStream_t st) {
+                     float* lse_int, int32_t* empty, bool ext_early, bool extb, cudaStream_t st) {
   using C = sm100k2::Cfg<D, NT, SPLIT>;
   CUtensorMap mq, mk, mv;
   int rc;
@@ -629,12 +695,15 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   unsigned long long* trace = nullptr;
   if (g_k2_trace != nullptr && g_k2_trace_i < g_k2_trace_n)
     trace = g_k2_trace + (size_t)(g_k2_trace_i++) * 1024 * 8;  // slab per traced launch
-  auto kern = trace ? sm100k2::internal_merge_kernel<D, NT, SPLIT, true>
-                    : sm100k2::internal_merge_kernel<D, NT, SPLIT, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[trace ? 1 : 0]) {
+  auto kern = trace ? (extb ? sm100k2::internal_merge_kernel<D, NT, SPLIT, true, false, true>
+                            : sm100k2::internal_merge_kernel<D, NT, SPLIT, true>)
+                    : (extb ? sm100k2::internal_merge_kernel<D, NT, SPLIT, false, false, true>
+                            : sm100k2::internal_merge_kernel<D, NT, SPLIT, false>);
+  static bool attr[4] = {false, false, false, false};
+  const int ai = (trace ? 1 : 0) + (extb ? 2 : 0);
+  if (!attr[ai]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr[trace ? 1 : 0] = true;
+    attr[ai] = true;
   }
   const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
   const float scale_log2 = (float)(scale * 1.4426950408889634);
@@ -646,12 +715,12 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   return check_launch("internal_merge_kernel(sm100)");
 }
 
-template <int NT>
+template <int NT, bool EXTB>
 static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __nv_bfloat16* v_in,
-                        int64_t groups, int64_t q_rows, int64_t n_in, double scale, const float* o_ext,
+                        int64_t groups, int64_t q_rows, int64_t n_in, double scale, const void* o_ext,
                         const float* lse_ext, void* out, bool out_bf16, float* lse_merged, float* o_int,
                         float* lse_int, int32_t* empty, bool ext_early, cudaStream_t st) {
-  using C = sm100k2::CfgV2<NT>;
+  using C = sm100k2::CfgV2<NT, EXTB>;
   constexpr int D = 128;
   CUtensorMap mq, mk, mv, me;
   int rc;
@@ -659,8 +728,8 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   const int64_t nin_eff = n_in > 0 ? n_in : 1;
   if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
-  if ((rc = make_tmap_3d(&me, o_ext, 4, D, q_rows, q_rows, groups, 32, sm100k2::BM))) return rc;
-  auto kern = sm100k2::internal_merge_v2_kernel<NT>;
+  if ((rc = make_tmap_3d(&me, o_ext, EXTB ? 2 : 4, D, q_rows, q_rows, groups, C::ECOLS, sm100k2::BM))) return rc;
+  auto kern = sm100k2::internal_merge_v2_kernel<NT, EXTB>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -685,8 +754,8 @@ int make_tmap_nd(CUtensorMap* map, const void* base, int rank, const int64_t* di
 template <int NT>
 static int launch_k2_tok(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat16* k, int64_t k_ts,
                          const __nv_bfloat16* v, int64_t v_ts, int64_t batch, int64_t B, int64_t Hq,
-                         int64_t Hkv, double scale, const float* o_ext, const float* lse_ext, void* out,
-                         int64_t out_ts, bool out_bf16, bool ext_early, cudaStream_t st) {
+                         int64_t Hkv, double scale, const void* o_ext, const float* lse_ext, void* out,
+                         int64_t out_ts, bool out_bf16, bool ext_early, bool extb, cudaStream_t st) {
   constexpr int D = 128, SPLIT = 2;
   using C = sm100k2::Cfg<D, NT, SPLIT>;
   const int64_t G = Hq / Hkv;
@@ -706,11 +775,12 @@ static int launch_k2_tok(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat
     if ((rc = make_tmap_nd(&mk, k, 4, dims, sk, box))) return rc;
     if ((rc = make_tmap_nd(&mv, v, 4, dims, sv, box))) return rc;
   }
-  auto kern = sm100k2::internal_merge_kernel<D, NT, SPLIT, false, true>;
-  static bool attr = false;
-  if (!attr) {
+  auto kern = extb ? sm100k2::internal_merge_kernel<D, NT, SPLIT, false, true, true>
+                   : sm100k2::internal_merge_kernel<D, NT, SPLIT, false, true>;
+  static bool attr[2] = {false, false};
+  if (!attr[extb ? 1 : 0]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr = true;
+    attr[extb ? 1 : 0] = true;
   }
   const int64_t groups = batch * Hkv, q_rows = G * B;
   const float scale_log2 = (float)(scale * 1.4426950408889634);
@@ -725,32 +795,33 @@ static int launch_k2_tok(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat
 int launch_internal_merge_tok_sm100(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat16* k,
                                     int64_t k_ts, const __nv_bfloat16* v, int64_t v_ts, int64_t batch,
                                     int64_t B, int64_t Hq, int64_t Hkv, int64_t d, double scale,
-                                    const float* o_ext, const float* lse_ext, void* out, int64_t out_ts,
-                                    bool out_bf16, bool ext_early, cudaStream_t st) {
+                                    const void* o_ext, const float* lse_ext, void* out, int64_t out_ts,
+                                    bool out_bf16, bool ext_early, bool extb, cudaStream_t st) {
   if (d != 128 || Hkv <= 0 || Hq % Hkv != 0 || (Hq / Hkv) * B > 128 || B < 1 || B > 64)
     return fail(FB_ERR_UNSUPPORTED, "token-major cached step: d 128, (Hq/Hkv)*B <= 128, 1 <= B <= 64");
   if (B <= 16)
     return launch_k2_tok<16>(q, q_ts, k, k_ts, v, v_ts, batch, B, Hq, Hkv, scale, o_ext, lse_ext, out, out_ts,
-                             out_bf16, ext_early, st);
+                             out_bf16, ext_early, extb, st);
   if (B <= 32)
     return launch_k2_tok<32>(q, q_ts, k, k_ts, v, v_ts, batch, B, Hq, Hkv, scale, o_ext, lse_ext, out, out_ts,
-                             out_bf16, ext_early, st);
+                             out_bf16, ext_early, extb, st);
   return launch_k2_tok<64>(q, q_ts, k, k_ts, v, v_ts, batch, B, Hq, Hkv, scale, o_ext, lse_ext, out, out_ts,
-                           out_bf16, ext_early, st);
+                           out_bf16, ext_early, extb, st);
 }
 
 int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_in,
                                 const __nv_bfloat16* v_in, int64_t groups, int64_t q_rows,
-                                int64_t head_dim, int64_t n_in, double scale, const float* o_ext,
+                                int64_t head_dim, int64_t n_in, double scale, const void* o_ext,
                                 const float* lse_ext, void* out, bool out_bf16, float* lse_merged,
                                 float* o_int, float* lse_int, int32_t* empty, bool ext_early,
-                                cudaStream_t st) {
+                                bool extb, cudaStream_t st) {
 #define FB_K2(DD, NN)                                                                           \
   return split ? launch_k2<DD, NN, (DD == 128 ? 2 : 1)>(q, k_in, v_in, groups, q_rows, n_in, scale, \
                                                         o_ext, lse_ext, out, out_bf16, lse_merged,  \
-                                                        o_int, lse_int, empty, ext_early, st)       \
+                                                        o_int, lse_int, empty, ext_early, extb, st) \
                : launch_k2<DD, NN, 1>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext,   \
-                                      out, out_bf16, lse_merged, o_int, lse_int, empty, ext_early, st)
+                                      out, out_bf16, lse_merged, o_int, lse_int, empty, ext_early,  \
+                                      extb, st)
   // split the output columns over 2 CTAs: measured faster at every batch
   // (C2 b=16: 5.7 vs 8.2 us; b=24: 9.9 vs 10.8; b=32: 11.3 vs 14.5, 1.7 waves)
   bool split = true;
@@ -767,10 +838,16 @@ int launch_internal_merge_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k_i
   }
   const int v2 = g_k2_v2_override >= 0 ? g_k2_v2_override : v2_env;
   const int64_t k2_tiles = groups * ((q_rows + sm100k2::BM - 1) / sm100k2::BM);
-  const bool use_v2 = v2 == 1 || (v2 == -1 && k2_tiles > num_sms());
+  // with a bf16 cached partial (FB_PARTIAL_BF16) v2's O_ext tile is 32 KB and
+  // it wins as soon as v1's column-split grid (2 CTAs per tile) exceeds the
+  // SMs: C2 b=16 5.42 vs 6.12 us (v1), b=32 8.09 vs 10.57; b=4 v1 3.70 vs 4.66
+  const bool use_v2 = v2 == 1 || (v2 == -1 && (extb ? 2 * k2_tiles > num_sms() : k2_tiles > num_sms()));
   if (head_dim == 128 && use_v2 && n_in <= 64 && (reinterpret_cast<uintptr_t>(o_ext) & 15) == 0) {
-#define FB_K2V2(NN) return launch_k2_v2<NN>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext, out, \
-                                            out_bf16, lse_merged, o_int, lse_int, empty, ext_early, st)
+#define FB_K2V2(NN)                                                                                     \
+  return extb ? launch_k2_v2<NN, true>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext, out,  \
+                                       out_bf16, lse_merged, o_int, lse_int, empty, ext_early, st)       \
+              : launch_k2_v2<NN, false>(q, k_in, v_in, groups, q_rows, n_in, scale, o_ext, lse_ext, out, \
+                                        out_bf16, lse_merged, o_int, lse_int, empty, ext_early, st)
     if (n_in <= 16) FB_K2V2(16);
     if (n_in <= 32) FB_K2V2(32);
     if (n_in <= 64) FB_K2V2(64);

@@ -380,6 +380,16 @@ __device__ __forceinline__ void ld_v8_nc(const float* p, float* v) {
                : "l"(p));
 }
 
+__device__ __forceinline__ void ld_v8_nc_b32(const void* p, uint32_t* v) {
+  asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+
+// bf16x2 word -> its low / high element as fp32 (exact)
+__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
 // 32 consecutive floats of a row: 256-bit stores when aligned, else float4
 __device__ __forceinline__ void st_row32(float* p, const float* v) {
   if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
@@ -395,6 +405,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
+}
+
+// 32 consecutive floats of a row stored as bf16 (64 B): 256-bit stores when aligned
+__device__ __forceinline__ void st_row32_bf16(void* p, const float* v) {
+  uint32_t pk[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+  if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+    st_v8_b32(p, pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], pk[6], pk[7]);
+    st_v8_b32(reinterpret_cast<char*>(p) + 32, pk[8], pk[9], pk[10], pk[11], pk[12], pk[13], pk[14], pk[15]);
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+  }
 }
 
 }  // namespace ptx

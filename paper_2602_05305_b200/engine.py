@@ -10,8 +10,10 @@ batched launch pair.
 
 Layouts: Q [b, Hq, B, d], KV cache [b, Hkv, N_cap, d], current-block K/V
 [b, Hkv, B, d] -- all bf16 (or f32/f64 for parity runs); the external
-partial per layer is O_ext [b, Hq, B, d] fp32 + LSE_ext [b, Hq, B] fp32
-(the reference's cache entry, attention.py:248-292, batched).
+partial per layer is O_ext [b, Hq, B, d] + LSE_ext [b, Hq, B] fp32 (the
+reference's cache entry, attention.py:248-292, batched).  In bf16 mode O_ext
+is stored in bf16 by default (ext_dtype): the reference keeps a partial's out
+in the tensor dtype (attention.py:70-71), and every cached step re-reads it.
 """
 
 from __future__ import annotations
@@ -48,7 +50,8 @@ class FlashBlockAttention:
     def __init__(self, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
                  block_len: int, head_dim: int, device=None, dtype=torch.bfloat16,
                  out_dtype: torch.dtype | None = None, scale: float | None = None,
-                 config: ReuseConfig | None = None, recorder=None):
+                 config: ReuseConfig | None = None, recorder=None,
+                 ext_dtype: torch.dtype | None = None):
         if num_q_heads % num_kv_heads:
             raise ShapeError("num_q_heads must be a multiple of num_kv_heads")
         self.L, self.b, self.hq, self.hkv = num_layers, batch, num_q_heads, num_kv_heads
@@ -62,7 +65,14 @@ class FlashBlockAttention:
         self.scale = 1.0 / math.sqrt(head_dim) if scale is None else float(scale)
         self.config = config or ReuseConfig()
         groups, rows = batch * num_kv_heads, self.G * block_len
-        self.o_ext = torch.zeros((num_layers, groups, rows, head_dim), dtype=self.ot, device=self.device)
+        # cached external partial's O: bf16 in bf16 mode where the tcgen05
+        # kernels run (head_dim 64 / 128), else the mode's partial type
+        if ext_dtype is None:
+            ext_dtype = torch.bfloat16 if (dtype == torch.bfloat16 and head_dim in (64, 128)) else self.ot
+        if ext_dtype not in (self.ot, torch.bfloat16) or (ext_dtype == torch.bfloat16 and dtype != torch.bfloat16):
+            raise ShapeError(f"ext_dtype {ext_dtype} is not a partial type of {dtype} mode")
+        self.ext_dtype = ext_dtype
+        self.o_ext = torch.zeros((num_layers, groups, rows, head_dim), dtype=ext_dtype, device=self.device)
         self.lse_ext = torch.full((num_layers, groups, rows), -math.inf, dtype=self.lt, device=self.device)
         self.valid = [False] * num_layers
         self.block_id = 0
@@ -329,10 +339,12 @@ class FlashBlockAttention:
             gl64 = gl.to(torch.int64)
             lens = k_cache.lengths[layer].index_select(0, gl64)
             self._count_rows(lens)
+            o_sub = torch.empty((gl64.numel(),) + tuple(self.o_ext.shape[2:]), dtype=self.o_ext.dtype,
+                                device=self.device)
             o_sub, l_sub = K.attention_partial_paged(qg.index_select(0, gl64), k_cache.k[layer],
                                                      k_cache.v[layer],
                                                      k_cache.table[layer].index_select(0, gl64), lens,
-                                                     self.scale)
+                                                     self.scale, out=o_sub)
             self.o_ext[layer].index_copy_(0, gl64, o_sub)
             self.lse_ext[layer].index_copy_(0, gl64, l_sub)
         else:

@@ -44,6 +44,23 @@ def mode_of_partial(out: torch.Tensor, lse: torch.Tensor) -> int:
     raise ShapeError(f"partial dtypes {key} match no precision mode")
 
 
+def _partial_code(code: int, o: torch.Tensor) -> int:
+    """The mode code, with FB_PARTIAL_BF16 when a BF16-mode partial's O is bf16
+    (the reference keeps a partial's out in the tensor dtype, attention.py:70-71)."""
+    if code == _lib.FB_BF16 and o.dtype == torch.bfloat16:
+        return code | _lib.FB_PARTIAL_BF16
+    return code
+
+
+def _check_partial_out(code: int, out: torch.Tensor, lse: torch.Tensor) -> None:
+    ot, lt = PARTIAL_TYPES[code]
+    ok_o = out.dtype == ot or (code == _lib.FB_BF16 and out.dtype == torch.bfloat16)
+    if not ok_o or lse.dtype != lt:
+        raise ShapeError(f"partial out {out.dtype} / lognorm {lse.dtype} do not match the mode")
+    if not (out.is_contiguous() and lse.is_contiguous()):
+        raise ShapeError("partial out / lognorm must be contiguous")
+
+
 def require_cuda(*ts: torch.Tensor) -> None:
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -155,11 +172,12 @@ def attention_partial(q, k, v, key_begin: int = 0, key_end: int | None = None,
         out = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
     if lse is None:
         lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    _check_partial_out(code, out, lse)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     wsb = _lib.load().fb_partial_workspace_bytes(code, groups, q_rows, d, max(0, key_end - key_begin))
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
     flags = SYNC_FLAGS.get(q3.device)
-    _lib.call("fb_attention_partial_sync", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
+    _lib.call("fb_attention_partial_sync", _partial_code(code, out), _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
               int(key_begin), key_end, scale, _p(out), _p(lse), _p(ws),
               0 if ws is None else ws.numel(), _p(flags), flags.numel(), _stream(q3))
     return out, lse
@@ -183,10 +201,11 @@ def attention_partial_ragged(q, k, v, key_end: torch.Tensor, key_begin: int = 0,
         out = torch.empty((groups, q_rows, d), dtype=ot, device=q3.device)
     if lse is None:
         lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
+    _check_partial_out(code, out, lse)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     wsb = _lib.load().fb_ragged_workspace_bytes(code, groups, q_rows, d, k3.shape[1])
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_attention_partial_ragged", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d,
+    _lib.call("fb_attention_partial_ragged", _partial_code(code, out), _p(q3), _p(k3), _p(v3), groups, q_rows, d,
               k3.shape[1], int(key_begin), _p(ends), scale, _p(out), _p(lse), _p(ws),
               0 if ws is None else ws.numel(), _stream(q3))
     return out, lse
@@ -214,10 +233,11 @@ def attention_partial_paged(q, k_pages, v_pages, page_table: torch.Tensor, key_l
         out = torch.empty((groups, q_rows, d), dtype=torch.float32, device=q3.device)
     if lse is None:
         lse = torch.empty((groups, q_rows), dtype=torch.float32, device=q3.device)
+    _check_partial_out(_lib.FB_BF16, out, lse)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     wsb = _lib.load().fb_paged_workspace_bytes(_CODE[torch.bfloat16], groups, q_rows, d)
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_attention_partial_paged", _CODE[torch.bfloat16], _p(q3), _p(kp), _p(vp), kp.shape[0],
+    _lib.call("fb_attention_partial_paged", _partial_code(_lib.FB_BF16, out), _p(q3), _p(kp), _p(vp), kp.shape[0],
               kp.shape[1], _p(table), table.shape[1], groups, q_rows, d, _p(lens), scale, _p(out),
               _p(lse), _p(ws), 0 if ws is None else ws.numel(), _stream(q3))
     return out, lse
@@ -296,10 +316,11 @@ def attention_partial_groups(q, k, v, group_list: torch.Tensor, key_begin: int =
         lse = torch.empty((groups, q_rows), dtype=lt, device=q3.device)
     gl = group_list.to(device=q3.device, dtype=torch.int32).contiguous()
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    _check_partial_out(code, out, lse)
     wsb = _lib.load().fb_partial_workspace_bytes(code, gl.numel(), q_rows, d,
                                                  max(0, key_end - key_begin))
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_attention_partial_groups", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
+    _lib.call("fb_attention_partial_groups", _partial_code(code, out), _p(q3), _p(k3), _p(v3), groups, q_rows, d, cap,
               int(key_begin), key_end, _p(gl), gl.numel(), scale, _p(out), _p(lse), _p(ws),
               0 if ws is None else ws.numel(), _stream(q3))
     return out, lse
@@ -436,9 +457,12 @@ def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
     ot, lt = PARTIAL_TYPES[code]
     o_ext = o_ext.contiguous()
     lse_ext = lse_ext.contiguous()
-    if o_ext.dtype != ot or lse_ext.dtype != lt or o_ext.numel() != groups * q_rows * d \
+    o_ok = o_ext.dtype == ot or (code == _lib.FB_BF16 and o_ext.dtype == torch.bfloat16)
+    if not o_ok or lse_ext.dtype != lt or o_ext.numel() != groups * q_rows * d \
             or lse_ext.numel() != groups * q_rows:
         raise ShapeError("cached partial does not match the queries (shape or precision)")
+    if want_internal and o_ext.dtype != ot:
+        raise ShapeError("want_internal needs the mode's fp32 cached partial")
     if out_dtype is None:
         out_dtype = ot
     if out is None:
@@ -450,7 +474,7 @@ def internal_merge(q, k_in, v_in, o_ext, lse_ext, scale: float | None = None,
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     wsb = _lib.load().fb_internal_merge_workspace_bytes(code, groups, q_rows, d, k3.shape[1])
     ws = WORKSPACE.get(q3.device, wsb) if wsb else None
-    _lib.call("fb_internal_merge_ex", code, _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
+    _lib.call("fb_internal_merge_ex", _partial_code(code, o_ext), _p(q3), _p(k3), _p(v3), groups, q_rows, d, k3.shape[1],
               scale, _p(o_ext), _p(lse_ext), _p(out), _OUT_CODE[out.dtype], _p(lse_m), _p(o_int),
               _p(l_int), _p(cnt), _p(ws), 0 if ws is None else ws.numel(),
               _lib.FB_EXT_STABLE if ext_stable else 0, _stream(q3))
@@ -486,12 +510,13 @@ def internal_merge_tok(q_tok, k_tok, v_tok, o_ext, lse_ext, out_tok, scale: floa
         raise ShapeError("token-major q / k / v / out shapes do not line up")
     qs, ks, vs, os_ = (_tok_stride(q_tok, "q"), _tok_stride(k_tok, "k_in"), _tok_stride(v_tok, "v_in"),
                        _tok_stride(out_tok, "out"))
-    if o_ext.dtype != torch.float32 or o_ext.numel() != b * hq * B * d or lse_ext.numel() != b * hq * B:
+    if o_ext.dtype not in (torch.float32, torch.bfloat16) or o_ext.numel() != b * hq * B * d \
+            or lse_ext.numel() != b * hq * B:
         raise ShapeError("cached partial does not match the queries")
     if lse_ext.dtype != torch.float32 or not (o_ext.is_contiguous() and lse_ext.is_contiguous()):
-        raise ShapeError("the cached partial must be contiguous float32 (o_ext, lse_ext)")
+        raise ShapeError("the cached partial must be contiguous (o_ext float32 or bfloat16, lse_ext float32)")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
-    _lib.call("fb_internal_merge_tok", _CODE[q_tok.dtype], _p(q_tok), qs, _p(k_tok), ks, _p(v_tok), vs, b, B,
+    _lib.call("fb_internal_merge_tok", _partial_code(_CODE[q_tok.dtype], o_ext), _p(q_tok), qs, _p(k_tok), ks, _p(v_tok), vs, b, B,
               hq, hkv, d, scale, _p(o_ext), _p(lse_ext), _p(out_tok), _OUT_CODE[out_tok.dtype], os_,
               _lib.FB_EXT_STABLE if ext_stable else 0, _stream(q_tok))
     return out_tok
