@@ -164,6 +164,8 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       for (int i = 0; i < C::PRE; ++i) oe[i] = 0.f;
     }
   };
+  const bool pdl_late = (ext_early & 2) != 0;  // see internal_merge_v2_kernel
+  ext_early &= 1;
   if (ext_early) load_ext();
 
   if (threadIdx.x == 128) {
@@ -183,7 +185,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const uint32_t tmem = bar->tmem_base;
   if (threadIdx.x == 128) stamp(1);
   ptx::pdl_wait();               // inputs of this launch are final from here on
-  ptx::pdl_launch_dependents();
+  if (!pdl_late) ptx::pdl_launch_dependents();
   if (threadIdx.x == 128) stamp(2);
 
   if (warp == 4) {
@@ -212,6 +214,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, C::DC, true);
       ptx::mbar_wait(&bar->load_qkv, 0);
+      if (pdl_late) ptx::pdl_launch_dependents();
       stamp(3);
       ptx::tc_fence_after();
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
@@ -460,6 +463,11 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
   const bool live_row = warp < 8 && grow < q_rows;
   const long long rr = (long long)g * q_rows + grow;
 
+  // ext_early bit 1 (pdl_late): signal the dependent launch only once this
+  // CTA's Q / K / V have landed, so the next launch's O_ext prefetch does not
+  // compete with this launch's post-wait loads
+  const bool pdl_late = (ext_early & 2) != 0;
+  ext_early &= 1;
   float le = -INFINITY;
   if (ext_early && live_row) le = __ldg(lse_ext + rr);
   if (threadIdx.x == 256) {
@@ -486,7 +494,7 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
   ptx::tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
   ptx::pdl_wait();
-  ptx::pdl_launch_dependents();
+  if (!pdl_late) ptx::pdl_launch_dependents();
 
   if (warp == 8) {
     if (lane == 0) {
@@ -505,6 +513,7 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
       ptx::mbar_wait(&bar->load_qkv, 0);
+      if (pdl_late) ptx::pdl_launch_dependents();
       ptx::tc_fence_after();
       const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
       const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K);
@@ -666,6 +675,15 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t in
 
 static int g_k2_v2_override = -1;
 void set_k2_v2(int v) { g_k2_v2_override = v; }
+// diagnostics: FB_K2_PDL_LATE=1 signals the dependent launch after the Q/K/V loads landed
+static int k2_pdl_late() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_K2_PDL_LATE");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
 
 bool sm100_k2_supported(int64_t head_dim, int64_t n_in) {
   // n_in == 0 (no current-block keys) takes the SIMT path: there is nothing to load
@@ -710,7 +728,7 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles * C::SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st,
              mq, mk, mv, o_ext, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
              out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
-             ext_early ? 1 : 0, trace, sm100k2::TokLayout{1, 1, 1, 0});
+             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0), trace, sm100k2::TokLayout{1, 1, 1, 0});
   count_launch();
   return check_launch("internal_merge_kernel(sm100)");
 }
@@ -739,7 +757,7 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles)), dim3(sm100k2::V2_THREADS), C::SMEM, st, mq, mk,
              mv, me, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
-             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), ext_early ? 1 : 0);
+             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0));
   count_launch();
   return check_launch("internal_merge_v2_kernel(sm100)");
 }
@@ -786,7 +804,7 @@ static int launch_k2_tok(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st, mq, mk, mv, o_ext,
              lse_ext, (int)q_rows, 1, (int)B, scale_log2, out, out_bf16 ? 1 : 0, (float*)nullptr,
-             (float*)nullptr, (float*)nullptr, (int*)nullptr, ext_early ? 1 : 0,
+             (float*)nullptr, (float*)nullptr, (int*)nullptr, (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0),
              (unsigned long long*)nullptr, sm100k2::TokLayout{(int)B, (int)G, (int)Hkv, (long long)out_ts});
   count_launch();
   return check_launch("internal_merge_kernel(sm100, token-major)");

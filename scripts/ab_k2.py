@@ -4,7 +4,8 @@ between two library builds: graph of 36 layers x 31 cached steps at C2 b=16.
     python scripts/ab_k2.py libA.so libB.so [batch] [ENV=VAL for A] [ENV=VAL for B]
 
 The optional environment settings are applied just before each library's
-first call (the library reads its FB_* switches once)."""
+first call (the library reads its FB_* switches once).  AB_EXTB=1: the
+cached external partial's O in bf16 (FB_PARTIAL_BF16), the engine default."""
 import ctypes as C, math, os, sys, torch
 A, B = sys.argv[1], sys.argv[2]
 b = int(sys.argv[3]) if len(sys.argv) > 3 else 16
@@ -25,7 +26,11 @@ r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
 qs = [r(groups, rows, D) for _ in range(L)]
 ks = [r(groups, BLK, D) for _ in range(L)]
 vs = [r(groups, BLK, D) for _ in range(L)]
+EXTB = os.environ.get("AB_EXTB") == "1"
 oe = [torch.randn((groups, rows, D), device="cuda", generator=g) for _ in range(L)]
+if EXTB:
+    oe = [o.to(torch.bfloat16) for o in oe]
+DT = 2 | (0x100 if EXTB else 0)
 le = [torch.randn((groups, rows), device="cuda", generator=g) for _ in range(L)]
 out = [torch.empty((groups, rows, D), device="cuda", dtype=torch.bfloat16) for _ in range(L)]
 s = torch.cuda.Stream()
@@ -34,7 +39,7 @@ for n, lib in libs.items():
     def fn(lib=lib):
         for _ in range(31):
             for i in range(L):
-                rc = lib.fb_internal_merge_ex(2, qs[i].data_ptr(), ks[i].data_ptr(), vs[i].data_ptr(), groups, rows,
+                rc = lib.fb_internal_merge_ex(DT, qs[i].data_ptr(), ks[i].data_ptr(), vs[i].data_ptr(), groups, rows,
                                               D, BLK, 1 / math.sqrt(D), oe[i].data_ptr(), le[i].data_ptr(),
                                               out[i].data_ptr(), 2, None, None, None, None, None, 0, 1,
                                               s.cuda_stream)
@@ -53,7 +58,7 @@ for rnd in range(6):
     for n in (("A", "B") if rnd % 2 == 0 else ("B", "A")):
         graphs[n].replay(); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(); graphs[n].replay(); e1.record(); torch.cuda.synchronize()
+        e0.record(); graphs[n].replay(); e1.record(); torch.cuda.synchronize()  # replay on the current stream
         res.setdefault(n, []).append(e0.elapsed_time(e1) / (31 * L) * 1000)
 for n in res:
     v = sorted(res[n])
