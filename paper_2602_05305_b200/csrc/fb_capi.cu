@@ -356,8 +356,8 @@ static int sparse_attend_t(const void* qv, const void* kv, const void* vv, const
                       reinterpret_cast<const __nv_bfloat16*>(vin)};
       // selected-blocks partial, merged with the cached residual and written as
       // the output inside K1's merge kernel (no separate K3 launch)
-      const MergeFinal fin{reinterpret_cast<const float*>(o_res), reinterpret_cast<const float*>(l_res),
-                           out, out_bf16 ? 1 : 0, empty};
+      // (the selected partial itself is scratch here: skip_partial)
+      const MergeFinal fin{o_res, reinterpret_cast<const float*>(l_res), out, out_bf16 ? 1 : 0, empty, 0, 1};
       int rc = launch_gather_sm100(reinterpret_cast<const __nv_bfloat16*>(qv),
                                    reinterpret_cast<const __nv_bfloat16*>(kv),
                                    reinterpret_cast<const __nv_bfloat16*>(vv), groups, q_rows, d,
@@ -526,6 +526,8 @@ FB_API void fb_debug_set_pair(int on) { set_pair_enabled(on); }
 FB_API int64_t fb_debug_pair_launches(void) { return (int64_t)pair_launches(); }
 FB_API void fb_debug_set_quad(int m) { set_quad_mode(m); }
 FB_API int64_t fb_debug_quad_launches(void) { return (int64_t)quad_launches(); }
+FB_API void fb_debug_set_k1_cluster(int m) { set_k1_cluster_mode(m); }
+FB_API int64_t fb_debug_k1_cluster_launches(void) { return (int64_t)k1_cluster_launches(); }
 FB_API void fb_debug_set_k2_variant(int v) { set_k2_v2(v); }
 FB_API void fb_debug_set_k2_trace(void* p, int launches) { set_k2_trace(p, launches); }
 int64_t fb_launch_count(void) { return g_launches.load(); }

@@ -69,6 +69,7 @@ struct MergeFinal {
   int out_bf16;
   int32_t* empty_rows;
   int o2_bf16;
+  int skip_partial;  // the K1 partial itself is scratch: the cluster reduction does not store it (K8)
 };
 
 // tcgen05 / TMA refresh kernel (bf16, head_dim 64 or 128): normalised fp32
@@ -83,6 +84,8 @@ void set_pair_enabled(int on);  // -1 default (env FB_PAIR; block-causal only), 
 long long pair_launches();       // CTA-pair K1 launches so far (diagnostics)
 void set_quad_mode(int m);        // two-query-tile K1: -1 default (causal), 0 off, 1 all shapes
 long long quad_launches();
+void set_k1_cluster_mode(int m);  // cluster split-K K1: -1 default (auto), 0 off, 1 whenever feasible
+long long k1_cluster_launches();
 void set_k2_trace(void* p, int launches);  // diagnostics: K2 v1 per-CTA stamps
 void set_k2_v2(int v);           // K2 variant: -1 by size (default), 0 v1, 1 v2 (diagnostics)
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);

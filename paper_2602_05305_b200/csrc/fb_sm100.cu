@@ -60,6 +60,12 @@ struct Cfg {
   static constexpr uint32_t OFF_XCH = OFF_BAR + BAR_BYTES;    // [3][128] fp32 epilogue exchange
   static constexpr uint32_t SMEM = OFF_XCH + 3 * BM * 4 + 1024;  // + alignment slack
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
+  // cluster split-K: the CTA's normalised partial staged over the idle K/V ring
+  // (row stride SROW floats: row-per-thread v4 stores take the minimum 4
+  // wavefronts, row reads by a warp are conflict free), then its LSE
+  static constexpr int SROW = D + 4;
+  static constexpr uint32_t OFF_STG = OFF_K;
+  static_assert(BM * SROW * 4 + BM * 4 <= 2 * STAGES * TILE_BYTES, "staging exceeds the ring");
 };
 
 struct Barriers {
@@ -90,10 +96,17 @@ struct Sched {
   int rr;                  // pair kernel: round-robin whole items (block-causal), no stream-K
   int vprod;               // refresh kernel: warp 3 issues the V tiles (warp 0 Q and K)
   int o_bf16;              // final partial O rows stored as bf16 (FB_PARTIAL_BF16)
+  int clus;                // cluster split-K: CTAs per item (one cluster each), 0 = stream-K
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
-  __device__ __forceinline__ long long start(int c) const { return (long long)c * T / ctas; }
+  __device__ __forceinline__ long long start(int c) const {
+    if (clus > 0) {  // item-aligned: CTA c takes part c % clus of item c / clus
+      const int it = c / clus, r = c % clus;
+      return (long long)it * tpi + (long long)r * tpi / clus;
+    }
+    return (long long)c * T / ctas;
+  }
   // largest c with start(c) <= x
   __device__ __forceinline__ int cta_of(long long x) const {
     return (int)(((x + 1) * ctas - 1) / T);
@@ -172,6 +185,7 @@ __device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned 
 struct Gather {
   const int32_t* list;  // [groups, n_list] ascending block ids
   int n_list, n_ext, n_in, sel_tiles;
+  int diag_contig;      // diagnostics (FB_K8_DIAG=1): read contiguous rows instead of the list
 };
 
 // Paged KV cache (serving layout): a group's logical key row
@@ -209,7 +223,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                int key_end, const int* __restrict__ key_len, float scale_log2, float* __restrict__ o_out,
                float* __restrict__ lse_out, float* __restrict__ ws_o,
                float* __restrict__ ws_l, unsigned long long* __restrict__ trace,
-               unsigned long long* __restrict__ flags) {
+               unsigned long long* __restrict__ flags, MergeFinal fin) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -318,6 +332,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             for (int i = 0; i < 8; ++i) {
               const int e = lt * 8 + i;
               rows[i] = e < ga.n_list ? __ldg(ga.list + (long long)g * ga.n_list + e) * 16 : ga.n_ext;
+              if (ga.diag_contig) rows[i] = (lt * 128 + i * 16) % ga.n_ext;  // diagnostics: same bytes, contiguous
               slabs[i] = g;
               if (pg.table != nullptr) {  // paged cache: block -> (page, row); none -> past a page
                 if (e < ga.n_list) {
@@ -656,7 +671,11 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const bool owner = flags != nullptr && !whole && ib >= t_begin;
       const int cb = blockIdx.x + 1, ce = owner ? sc.cta_of(sc.item_end(item) - 1) : 0;
       float* dst;
-      if (whole || owner) {
+      float* stg = reinterpret_cast<float*>(smem + C::OFF_STG);  // cluster split-K staging
+      if (sc.clus > 0) {
+        dst = stg + row * C::SROW;
+        if (wg == 1) stg[BM * C::SROW + row] = lse;
+      } else if (whole || owner) {
         dst = live ? o_out + orow * D : nullptr;
       } else {
         const long long slot = sc.slot(blockIdx.x, item) * BM + row;
@@ -715,10 +734,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               }
             }
           }
-          if (sc.o_bf16 && (whole || owner))  // final row into a bf16 partial
+          if (sc.clus > 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else if (sc.o_bf16 && (whole || owner)) {  // final row into a bf16 partial
             ptx::st_row32_bf16(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + c * 32, v);
-          else
+          } else {
             ptx::st_row32(dst + c * 32, v);
+          }
         }
       }
       if (row == 0 && wg == 0 && seg == 0) stamp(6);
@@ -729,13 +753,101 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, 1ull);
       }
-      if ((whole || owner) && live && wg == 1) lse_out[orow] = lse;
+      if (sc.clus == 0 && (whole || owner) && live && wg == 1) lse_out[orow] = lse;
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
   }
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (sc.clus > 0) {
+    // Cluster split-K reduction: the item's CTAs (one cluster) staged their
+    // normalised partials; CTA `rank` merges rows [rank*BM/clus, ...) over all
+    // of them through distributed shared memory, in rank order (the same
+    // log-space merge as combine_partials, attention.py:207-233), and writes
+    // the finished rows -- no split workspace, no merge kernel.
+    ptx::cluster_sync();
+    const int cl = sc.clus;
+    const int rank = (int)ptx::cluster_ctarank();
+    const int item = blockIdx.x / cl;
+    const int g = sc.group_of(item), mt = sc.mtile_of(item);
+    const int rows_per = BM / cl;
+    const float* stg = reinterpret_cast<const float*>(smem + C::OFF_STG);
+    const bool col = lane * 4 < D;
+    for (int rr = warp; rr < rows_per; rr += THREADS / 32) {
+      const int row = rank * rows_per + rr;
+      const int grow = mt * BM + row;
+      if (grow >= q_rows) continue;
+      const long long orow = (long long)g * q_rows + grow;
+      const float li = lane < cl ? ptx::ld_cluster_f32(ptx::mapa(stg + BM * C::SROW + row, lane)) : -INFINITY;
+      const float mx = warp_max(li);
+      const float w = (lane < cl && li != -INFINITY) ? __expf(li - mx) : 0.f;
+      const float z = warp_sum(w);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)  // all loads in flight
+        x[i] = (i < cl && col) ? ptx::ld_cluster_v4(ptx::mapa(stg + row * C::SROW + lane * 4, i))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float wi = __shfl_sync(0xffffffffu, w, i & 31);
+        if (i < cl && wi != 0.f) {
+          acc.x += wi * x[i].x; acc.y += wi * x[i].y; acc.z += wi * x[i].z; acc.w += wi * x[i].w;
+        }
+      }
+      const float iz = z > 0.f ? 1.f / z : 0.f;
+      const float4 o = make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
+      const float L = z > 0.f ? mx + logf(z) : -INFINITY;
+      if (fin.out == nullptr || !fin.skip_partial) {
+        if (col) {
+          if (sc.o_bf16) {
+            uint2 u;
+            u.x = ptx::pack_bf16(o.x, o.y);
+            u.y = ptx::pack_bf16(o.z, o.w);
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + lane * 4) = u;
+          } else {
+            *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) = o;
+          }
+        }
+        if (lane == 0) lse_out[orow] = L;
+      }
+      if (fin.out != nullptr) {  // fused final merge with (o2, l2), as final_merge_row
+        const float l2 = fin.l2 ? fin.l2[orow] : -INFINITY;
+        const float m = fmaxf(L, l2);
+        const bool flive = m != -INFINITY;
+        const float wp = (flive && L != -INFINITY) ? __expf(L - m) : 0.f;
+        const float w2 = (flive && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
+        const float fiz = flive ? 1.f / (wp + w2) : 0.f;
+        if (col) {
+          float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (w2 != 0.f) {
+            if (fin.o2_bf16) {
+              const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(fin.o2) +
+                                                              orow * D + lane * 4);
+              o2 = make_float4(ptx::bf16_lo(u.x), ptx::bf16_hi(u.x), ptx::bf16_lo(u.y), ptx::bf16_hi(u.y));
+            } else {
+              o2 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(fin.o2) + orow * D + lane * 4);
+            }
+          }
+          const float4 f = make_float4((__fmul_rn(wp, o.x) + __fmul_rn(w2, o2.x)) * fiz,
+                                       (__fmul_rn(wp, o.y) + __fmul_rn(w2, o2.y)) * fiz,
+                                       (__fmul_rn(wp, o.z) + __fmul_rn(w2, o2.z)) * fiz,
+                                       (__fmul_rn(wp, o.w) + __fmul_rn(w2, o2.w)) * fiz);
+          if (fin.out_bf16) {
+            uint2 u;
+            u.x = ptx::pack_bf16(f.x, f.y);
+            u.y = ptx::pack_bf16(f.z, f.w);
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + lane * 4) = u;
+          } else {
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(fin.out) + orow * D + lane * 4) = f;
+          }
+        }
+        if (!flive && lane == 0 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
+      }
+    }
+    ptx::cluster_sync();  // the other CTAs' reads of this CTA's staging are done
+  }
   if (threadIdx.x == 0) stamp(7);
   if (warp == 2) {
     ptx::tc_fence_after();
@@ -1662,6 +1774,67 @@ static int launch_quad_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   return check_launch("refresh_merge_kernel(sm100, quad)");
 }
 
+// Cluster split-K (few items, e.g. C3 b=1 shards, C2 b <= 4, C4 K8): every
+// item runs on one cluster of CTAs that merge their partials through DSMEM at
+// the end of the kernel (no split workspace, no merge kernel; a MergeFinal is
+// applied in the same pass).  FB_K1_CLUSTER=0 never, 1 whenever feasible,
+// default: when the stream-K plan would need the split-merge kernel.
+static int g_cluster_override = -1;
+void set_k1_cluster_mode(int m) { g_cluster_override = m; }
+static int k1_cluster_mode() {
+  if (g_cluster_override >= 0) return g_cluster_override;
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("FB_K1_CLUSTER");
+    m = e == nullptr ? 2 : atoi(e);
+  }
+  return m;
+}
+static long long g_cluster_launches = 0;
+long long k1_cluster_launches() { return g_cluster_launches; }
+
+// co-resident clusters of `cl` refresh-kernel CTAs (one CTA per SM)
+template <int D, bool GATHER>
+static int k1_max_clusters(int cl) {
+  static int cache[17] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[cl] == 0) {
+    auto kern = sm100::refresh_kernel<D, GATHER>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm100::Cfg<D>::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cl);
+    cfg.blockDim = dim3(sm100::THREADS);
+    cfg.dynamicSmemBytes = sm100::Cfg<D>::SMEM;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = cl;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cache[cl] = n > 0 ? n : -1;
+  }
+  return cache[cl] > 0 ? cache[cl] : 0;
+}
+
+// diagnostics: FB_K8_DIAG=1 gathers contiguous rows (same bytes, 16-row boxes),
+// 2 skips the split-merge kernel after a gather launch
+static int k8_diag() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_K8_DIAG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int D, bool GATHER>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
@@ -1717,6 +1890,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ga.n_ext = (int)gs->n_ext;
     ga.n_in = (int)gs->n_in;
     ga.sel_tiles = (int)((gs->n_list + 7) / 8);
+    ga.diag_contig = k8_diag() == 1;
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   }
   const bool o_bf16 = !GATHER && partial_out_bf16();
@@ -1786,6 +1960,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   unsigned long long* flags = nullptr;  // in-kernel split merge (uniform items only)
+  MergeFinal kfin{};                    // final merge applied by the cluster reduction
   bool need_merge;
   sm100::Causal cz{1, 0, 0};
   if (causal) cz = *causal;
@@ -1830,9 +2005,34 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
       need_merge = false;
     else
       flags = nullptr;
-    if (fin != nullptr) {  // the merge kernel finishes every row (fused K3)
+    // the merge kernel finishes every row (fused K3).  (Measured: the owner CTAs
+    // doing this final merge themselves, C4 K8 at 10 % density with items over
+    // ~5 CTAs, 64.5 vs 44.9 us -- the owners wait for CTAs that finish last.)
+    if (fin != nullptr) {
       need_merge = true;
       flags = nullptr;
+    }
+    // cluster split-K instead of the merge kernel: the largest cluster that
+    // gives every item its own cluster in one wave, >= 2 tiles per CTA.  Auto
+    // mode: clusters of <= 4 CTAs, and only while the CTAs' tile count stays
+    // within 3 of the stream-K plan's (measured, scripts/ab_cluster.py: C2 b=4
+    // 90 vs 97 us, C4 K8 at 10 % density 39 vs 45 us; clusters of 8 / 16 --
+    // C2 b=2 / b=1, C3 b=1 shards -- 1.3-1.6x slower, their launch waits for
+    // whole free GPC slices)
+    const int cm = k1_cluster_mode();
+    if (cm != 0 && g_k1_diag == 0 && (cm == 1 || need_merge)) {
+      const long long per_streamk = (p.T + p.ctas - 1) / p.ctas;
+      for (int cl = cm == 1 ? 16 : 4; cl >= 2; cl >>= 1) {
+        if ((long long)p.items * cl > num_sms() || p.tpi < 2 * cl) continue;
+        if (cm != 1 && (p.tpi + cl - 1) / cl > per_streamk + 3) continue;
+        if (k1_max_clusters<D, GATHER>(cl) < p.items) continue;
+        sc.clus = cl;
+        p.ctas = sc.ctas = p.items * cl;
+        need_merge = false;
+        flags = nullptr;
+        if (fin != nullptr) kfin = *fin;
+        break;
+      }
     }
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
@@ -1841,12 +2041,22 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     const PagingCtx* pc = current_paging();
     pgv = sm100::Paged{pc->table, (int)pc->max_pages, (int)pc->page_rows};
   }
-  launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, mq, mk, mv, mki, mvi, ga,
-             pgv, cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out, lse_out,
-             ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr, flags);
+  if (sc.clus > 0) {
+    static bool npc[16] = {};
+    if (!npc[ai]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      npc[ai] = true;
+    }
+    ++g_cluster_launches;
+  }
+  launch_pdl_cluster(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, sc.clus, mq, mk, mv, mki,
+                     mvi, ga, pgv, cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out,
+                     lse_out, ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr,
+                     flags, kfin);
   count_launch();
   if ((rc = check_launch("refresh_kernel(sm100)"))) return rc;
   if (!need_merge) return FB_OK;
+  if (GATHER && k8_diag() == 2) return FB_OK;  // diagnostics: gather kernel alone
   const long long warps = (long long)p.items * sm100::BM;
   launch_pdl(sm100::refresh_merge_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, sc,
              (int)q_rows, D, (const float*)ws_o, (const float*)ws_l, o_out, lse_out, (int)sm100::BM,
