@@ -474,8 +474,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         try:
             with open(tpath) as fh:
                 tj = json.load(fh)
-            if tj.get("batch") == b:
-                traffic = tj.get("dram_bytes_per_launch")
+            ent = tj.get("by_batch", {}).get(str(b))
+            if ent is not None:
+                traffic = ent.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
