@@ -86,6 +86,7 @@ void set_quad_mode(int m);        // two-query-tile K1: -1 default (causal), 0 o
 long long quad_launches();
 void set_k1_cluster_mode(int m);  // cluster split-K K1: -1 default (auto), 0 off, 1 whenever feasible
 long long k1_cluster_launches();
+void set_gather_atoms(int m);     // K7 / K8 atom layout: -1 default (on), 0 off, 1 on
 void set_k2_trace(void* p, int launches);  // diagnostics: K2 v1 per-CTA stamps
 void set_k2_v2(int v);           // K2 variant: -1 by size (default), 0 v1, 1 v2 (diagnostics)
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);

@@ -186,6 +186,13 @@ struct Gather {
   const int32_t* list;  // [groups, n_list] ascending block ids
   int n_list, n_ext, n_in, sel_tiles;
   int diag_contig;      // diagnostics (FB_K8_DIAG=1): read contiguous rows instead of the list
+  // Atom layout (d = 128): a K / V tile is 16 atoms of 8 keys x [2 d-halves x
+  // 128 B] (2 KB each), so a whole 16-key block -- both d-halves, two atoms --
+  // is ONE 4 KB TMA box of a 5-D view {64 cols, 8 rows, 2 halves, atoms,
+  // slabs} instead of two 64-column boxes (scripts/micro/tma_gather.cu: 5.07
+  // vs 4.22 TB/s of pure gather streaming).  MMA descriptors: K-major K with
+  // the d-half 1 KB apart and SBO 2 KB; MN-major V with LBO 1 KB, SBO 2 KB.
+  int atoms;
 };
 
 // Paged KV cache (serving layout): a group's logical key row
@@ -347,36 +354,58 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             if (do_k) {
               ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-              for (int b = 0; b < C::NBOX; ++b)
+              if (ga.atoms) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                  ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
-                                   &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], slabs[i], stream);
+                  ptx::tma_load_5d(smem + C::OFF_K + s * C::TILE_BYTES + i * 4096, &tm_k, &bar->k_full[s], 0, 0,
+                                   0, rows[i] / 8, slabs[i], stream);
+              } else {
+                for (int b = 0; b < C::NBOX; ++b)
+#pragma unroll
+                  for (int i = 0; i < 8; ++i)
+                    ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
+                                     &tm_k, &bar->k_full[s], b * BOX_COLS, rows[i], slabs[i], stream);
+              }
             }
             if (do_v) {
               ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-              for (int b = 0; b < C::NBOX; ++b)
+              if (ga.atoms) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                  ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
-                                   &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], slabs[i], stream);
+                  ptx::tma_load_5d(smem + C::OFF_V + s * C::TILE_BYTES + i * 4096, &tm_v, &bar->v_full[s], 0, 0,
+                                   0, rows[i] / 8, slabs[i], stream);
+              } else {
+                for (int b = 0; b < C::NBOX; ++b)
+#pragma unroll
+                  for (int i = 0; i < 8; ++i)
+                    ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES + i * 2048,
+                                     &tm_v, &bar->v_full[s], b * BOX_COLS, rows[i], slabs[i], stream);
+              }
             }
           } else {
             const int row = (lt - ga.sel_tiles) * BN;
             if (do_k) {
               ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-              for (int b = 0; b < C::NBOX; ++b)
-                ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_ki,
-                                 &bar->k_full[s], b * BOX_COLS, row, g, stream);
+              if (ga.atoms)
+                ptx::tma_load_5d(smem + C::OFF_K + s * C::TILE_BYTES, &tm_ki, &bar->k_full[s], 0, 0, 0, row / 8, g,
+                                 stream);
+              else
+                for (int b = 0; b < C::NBOX; ++b)
+                  ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_ki,
+                                   &bar->k_full[s], b * BOX_COLS, row, g, stream);
             }
             if (do_v) {
               ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-              for (int b = 0; b < C::NBOX; ++b)
-                ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_vi,
-                                 &bar->v_full[s], b * BOX_COLS, row, g, stream);
+              if (ga.atoms)
+                ptx::tma_load_5d(smem + C::OFF_V + s * C::TILE_BYTES, &tm_vi, &bar->v_full[s], 0, 0, 0, row / 8, g,
+                                 stream);
+              else
+                for (int b = 0; b < C::NBOX; ++b)
+                  ptx::tma_load_3d(smem + C::OFF_V + s * C::TILE_BYTES + b * C::BOX_BYTES, &tm_vi,
+                                   &bar->v_full[s], b * BOX_COLS, row, g, stream);
             }
           }
         }
@@ -408,12 +437,15 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             ptx::tc_fence_after();
             const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
             const uint32_t d_s = tmem + ((j & 1) ? C::COL_S1 : C::COL_S0);
+            const bool at = GATHER && ga.atoms;
+            const uint32_t k_half = at ? 1024u : C::BOX_BYTES, k_sbo = at ? 2048u : 1024u;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               // K-major SW128: a 16-element K step is +32 B inside a 64-column box
               const uint32_t off = (kk / 4) * C::BOX_BYTES + (kk % 4) * 32;
+              const uint32_t koff = (kk / 4) * k_half + (kk % 4) * 32;
               ptx::mma_ss(d_s, ptx::sdesc_sw128(q_base + off, 16, 1024),
-                          ptx::sdesc_sw128(k_base + off, 16, 1024), IDESC_S, kk > 0);
+                          ptx::sdesc_sw128(k_base + koff, 16, k_sbo), IDESC_S, kk > 0);
             }
             ptx::tc_commit(&bar->k_empty[s]);
             ptx::tc_commit(&bar->s_full[j & 1]);
@@ -437,13 +469,16 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
             const uint32_t o_tmem = tmem + ((jj & 1) ? C::COL_O1 : C::COL_O0);
             if constexpr (DIAG != 3) {  // DIAG 3 (diagnostics): no P V MMA, S = Q K^T only
+              const bool at = GATHER && ga.atoms;
 #pragma unroll
               for (int kk = 0; kk < BN / 16; ++kk) {
                 // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
-                // (the first two tiles of a segment start their warpgroup's O afresh)
+                // (the first two tiles of a segment start their warpgroup's O afresh);
+                // atom layout: 16 keys = two 2 KB atoms, d halves 1 KB apart
                 ptx::mma_ts(o_tmem, p_tmem + kk * 8,
-                            ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024), IDESC_O,
-                            (t > 2 || kk > 0) ? 1u : 0u);
+                            at ? ptx::sdesc_sw128(v_base + kk * 4096, 1024, 2048)
+                               : ptx::sdesc_sw128(v_base + kk * 2048, C::BOX_BYTES, 1024),
+                            IDESC_O, (t > 2 || kk > 0) ? 1u : 0u);
               }
             }
             ptx::tc_commit(&bar->v_empty[s]);
@@ -1835,6 +1870,19 @@ static int k8_diag() {
   return v;
 }
 
+// Gather::atoms on / off (FB_GATHER_ATOMS=0: the two-box-per-block layout)
+static int g_atoms_override = -1;
+void set_gather_atoms(int m) { g_atoms_override = m; }
+static bool gather_atoms_enabled() {
+  if (g_atoms_override >= 0) return g_atoms_override != 0;
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_GATHER_ATOMS");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
 template <int D, bool GATHER>
 static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             int64_t groups, int64_t q_rows, int64_t kv_rows_cap, int64_t key_begin,
@@ -1866,6 +1914,36 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     mki = mk;
     mvi = mv;
     tiles = (key_end - key_begin + sm100::BN - 1) / sm100::BN;
+  } else if (D == 128 && gather_atoms_enabled() && gs->n_ext > 0 && gs->n_ext % 8 == 0 && gs->n_in > 0 &&
+             gs->n_in % 8 == 0) {
+    // atom layout (Gather::atoms): 5-D views {64 cols, 8 rows, 2 halves, atoms, slabs};
+    // a 16-key block is one {64, 8, 2, 2, 1} box, a current-block tile one {64, 8, 2, 16, 1}
+    const int box_blk[5] = {64, 8, 2, 2, 1}, box_tile[5] = {64, 8, 2, 16, 1};
+    if (const PagingCtx* pc = current_paging()) {  // page pool [num_pages, page_rows, D]
+      const int64_t dims[5] = {64, 8, 2, pc->page_rows / 8, pc->num_pages};
+      const int64_t str[5] = {2, 256, 128, 2048, pc->page_rows * 256};
+      if ((rc = make_tmap_nd(&mk, k, 5, dims, str, box_blk))) return rc;
+      if ((rc = make_tmap_nd(&mv, v, 5, dims, str, box_blk))) return rc;
+    } else {
+      const int64_t dims[5] = {64, 8, 2, gs->n_ext / 8, groups};
+      const int64_t str[5] = {2, 256, 128, 2048, kv_rows_cap * 256};
+      if ((rc = make_tmap_nd(&mk, k, 5, dims, str, box_blk))) return rc;
+      if ((rc = make_tmap_nd(&mv, v, 5, dims, str, box_blk))) return rc;
+    }
+    {
+      const int64_t dims[5] = {64, 8, 2, gs->n_in / 8, groups};
+      const int64_t str[5] = {2, 256, 128, 2048, gs->n_in * 256};
+      if ((rc = make_tmap_nd(&mki, gs->k_in, 5, dims, str, box_tile))) return rc;
+      if ((rc = make_tmap_nd(&mvi, gs->v_in, 5, dims, str, box_tile))) return rc;
+    }
+    ga.atoms = 1;
+    ga.list = gs->list;
+    ga.n_list = (int)gs->n_list;
+    ga.n_ext = (int)gs->n_ext;
+    ga.n_in = (int)gs->n_in;
+    ga.sel_tiles = (int)((gs->n_list + 7) / 8);
+    ga.diag_contig = k8_diag() == 1;
+    tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   } else {
     // cache rows [0, n_ext) in 16-row boxes; current block [0, n_in) in 128-row boxes
     const int64_t n_ext_eff = gs->n_ext > 0 ? gs->n_ext : 1;
