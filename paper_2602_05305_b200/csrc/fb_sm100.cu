@@ -97,6 +97,7 @@ struct Sched {
   int vprod;               // refresh kernel: warp 3 issues the V tiles (warp 0 Q and K)
   int o_bf16;              // final partial O rows stored as bf16 (FB_PARTIAL_BF16)
   int clus;                // cluster split-K: CTAs per item (one cluster each), 0 = stream-K
+  int clus_dsm;            // cluster reduction reads the partials through DSMEM (else via L2)
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -491,6 +492,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
     }
   }
+  if (sc.clus > 0) {  // the cluster reduction's barrier(s) (softmax warps do the work)
+    ptx::cluster_sync();
+    if (sc.clus_dsm) ptx::cluster_sync();
+  }
   } else {
     ptx::setmaxnreg_inc<224>();
     // ------------------------------------------------------------ softmax
@@ -791,98 +796,169 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (sc.clus == 0 && (whole || owner) && live && wg == 1) lse_out[orow] = lse;
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
+    if (sc.clus > 0) {
+      // Cluster split-K reduction: the item's CTAs (one cluster) publish their
+      // normalised partials, meet at the cluster barrier, and CTA `rank` merges
+      // rows [rank*BM/clus, ...) over all of them in rank order (the same
+      // log-space merge as combine_partials, attention.py:207-233) and writes
+      // the finished rows -- no merge-kernel launch.
+      const int cl = sc.clus;
+      const int rank = (int)ptx::cluster_ctarank();
+      const int item = blockIdx.x / cl;
+      const int g = sc.group_of(item), mt = sc.mtile_of(item);
+      const int rows_per = BM / cl;
+      const int w8 = warp - 4;                                  // the 8 softmax warps do the reduction
+      const int nrw = (rows_per + 7) / 8;                       // rows per warp; nrw * cl <= 16
+      const float* stg = reinterpret_cast<const float*>(smem + C::OFF_STG);
+      const bool col = lane * 4 < D;
+      constexpr int MAXR = 8;  // rows per warp (rows_per / 8 <= 8 for clus >= 2)
+      // the fused merge's (o2, l2) rows are final before this launch: their
+      // loads go out first and overlap the publishing below
+      float l2v[MAXR];
+      float4 o2v[MAXR];
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        const int rr = w8 + r * 8, row = rank * rows_per + rr;
+        const bool ok = r < nrw && rr < rows_per && mt * BM + row < q_rows;
+        const long long orow = (long long)g * q_rows + mt * BM + row;
+        l2v[r] = -INFINITY;
+        o2v[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok && fin.out != nullptr && fin.l2 != nullptr) {
+          l2v[r] = __ldg(fin.l2 + orow);
+          if (col) {
+            if (fin.o2_bf16) {
+              const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(fin.o2) +
+                                                                   orow * D + lane * 4));
+              o2v[r] = make_float4(ptx::bf16_lo(u.x), ptx::bf16_hi(u.x), ptx::bf16_lo(u.y), ptx::bf16_hi(u.y));
+            } else {
+              o2v[r] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(fin.o2) + orow * D +
+                                                             lane * 4));
+            }
+          }
+        }
+      }
+      // publish the staged partial to this CTA's global slot (coalesced 512 B
+      // rows; the cluster's CTAs read it back from L2 -- DSMEM reads of the
+      // same 64 KB per CTA took ~8 us, its bandwidth is ~17 B/clk per SM)
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (!sc.clus_dsm) {
+        float* my_o = ws_o + (long long)blockIdx.x * BM * D;
+        float* my_l = ws_l + (long long)blockIdx.x * BM;
+        for (int r = w8; r < BM; r += 8) {
+          if (col)
+            __stcg(reinterpret_cast<float4*>(my_o + r * D + lane * 4),
+                   *reinterpret_cast<const float4*>(stg + r * C::SROW + lane * 4));
+          if (lane == 0) __stcg(my_l + r, stg[BM * C::SROW + r]);
+        }
+        __threadfence();
+      }
+      if (row == 0 && wg == 0) stamp(3);  // (cluster mode uses segment 0's slots only)
+      ptx::cluster_sync();
+      if (row == 0 && wg == 0) stamp(4);
+      const float* part_o = ws_o + (long long)item * cl * BM * D;  // the cluster's partial slots
+      const float* part_l = ws_l + (long long)item * cl * BM;
+      // one row: lane i < cl holds partial i's LSE; up to 4 partials' O slices
+      auto load_row = [&](int row, float& li, float4* x) {
+        if (sc.clus_dsm) {  // partial i staged in cluster CTA i's shared memory
+          li = lane < cl ? ptx::ld_cluster_f32(ptx::mapa(stg + BM * C::SROW + row, lane)) : -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            x[k] = (col && k < cl) ? ptx::ld_cluster_v4(ptx::mapa(stg + row * C::SROW + lane * 4, k))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          return;
+        }
+        li = lane < cl ? __ldcg(part_l + (long long)lane * BM + row) : -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          x[k] = (col && k < cl)
+                     ? __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)k * BM + row) * D + lane * 4))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      auto finish_row = [&](int row, float li, const float4* x, float l2, float4 o2) {
+        const long long orow = (long long)g * q_rows + mt * BM + row;
+        const float mx = warp_max(li);
+        const float w = (lane < cl && li != -INFINITY) ? __expf(li - mx) : 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i0 = 0; i0 < cl; i0 += 4) {  // clus <= 4 (auto mode): one pass over x
+          float4 y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            y[k] = i0 == 0 ? x[k]
+                   : !(col && i0 + k < cl) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                   : sc.clus_dsm ? ptx::ld_cluster_v4(ptx::mapa(stg + row * C::SROW + lane * 4, i0 + k))
+                                 : __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(i0 + k) * BM + row) * D +
+                                                                          lane * 4));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float wi = __shfl_sync(0xffffffffu, w, (i0 + k) & 31);
+            if (wi != 0.f) {
+              acc.x += wi * y[k].x; acc.y += wi * y[k].y; acc.z += wi * y[k].z; acc.w += wi * y[k].w;
+            }
+          }
+        }
+        const float z = warp_sum(w);
+        const float iz = z > 0.f ? 1.f / z : 0.f;
+        const float4 o = make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
+        const float L = z > 0.f ? mx + logf(z) : -INFINITY;
+        if (fin.out == nullptr || !fin.skip_partial) {
+          if (col) {
+            if (sc.o_bf16) {
+              uint2 u;
+              u.x = ptx::pack_bf16(o.x, o.y);
+              u.y = ptx::pack_bf16(o.z, o.w);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + lane * 4) = u;
+            } else {
+              *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) = o;
+            }
+          }
+          if (lane == 0) lse_out[orow] = L;
+        }
+        if (fin.out != nullptr) {  // fused final merge with (o2, l2), as final_merge_row
+          const float m = fmaxf(L, l2);
+          const bool flive = m != -INFINITY;
+          const float wp = (flive && L != -INFINITY) ? __expf(L - m) : 0.f;
+          const float w2 = (flive && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
+          const float fiz = flive ? 1.f / (wp + w2) : 0.f;
+          if (col) {
+            const float4 f = make_float4((__fmul_rn(wp, o.x) + __fmul_rn(w2, o2.x)) * fiz,
+                                         (__fmul_rn(wp, o.y) + __fmul_rn(w2, o2.y)) * fiz,
+                                         (__fmul_rn(wp, o.z) + __fmul_rn(w2, o2.z)) * fiz,
+                                         (__fmul_rn(wp, o.w) + __fmul_rn(w2, o2.w)) * fiz);
+            if (fin.out_bf16) {
+              uint2 u;
+              u.x = ptx::pack_bf16(f.x, f.y);
+              u.y = ptx::pack_bf16(f.z, f.w);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + lane * 4) = u;
+            } else {
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(fin.out) + orow * D + lane * 4) = f;
+            }
+          }
+          if (!flive && lane == 0 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
+        }
+      };
+      auto row_ok = [&](int r) {
+        const int rr = w8 + r * 8;
+        return r < nrw && rr < rows_per && mt * BM + rank * rows_per + rr < q_rows;
+      };
+#pragma unroll
+      for (int r = 0; r < MAXR; r += 2) {  // two rows' loads in flight at a time
+        const bool ok0 = row_ok(r), ok1 = row_ok(r + 1);  // warp-uniform
+        if (!ok0) continue;
+        const int row0 = rank * rows_per + w8 + r * 8, row1 = row0 + 8;
+        float li0, li1 = -INFINITY;
+        float4 x0[4], x1[4];
+        load_row(row0, li0, x0);
+        if (ok1) load_row(row1, li1, x1);
+        finish_row(row0, li0, x0, l2v[r], o2v[r]);
+        if (ok1) finish_row(row1, li1, x1, l2v[r + 1], o2v[r + 1]);
+      }
+      if (row == 0 && wg == 0) stamp(1);  // reduction done (stream end was read at the epilogue)
+      if (sc.clus_dsm) ptx::cluster_sync();  // the other CTAs' reads of this CTA's staging are done
+    }
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (sc.clus > 0) {
-    // Cluster split-K reduction: the item's CTAs (one cluster) staged their
-    // normalised partials; CTA `rank` merges rows [rank*BM/clus, ...) over all
-    // of them through distributed shared memory, in rank order (the same
-    // log-space merge as combine_partials, attention.py:207-233), and writes
-    // the finished rows -- no split workspace, no merge kernel.
-    ptx::cluster_sync();
-    const int cl = sc.clus;
-    const int rank = (int)ptx::cluster_ctarank();
-    const int item = blockIdx.x / cl;
-    const int g = sc.group_of(item), mt = sc.mtile_of(item);
-    const int rows_per = BM / cl;
-    const float* stg = reinterpret_cast<const float*>(smem + C::OFF_STG);
-    const bool col = lane * 4 < D;
-    for (int rr = warp; rr < rows_per; rr += THREADS / 32) {
-      const int row = rank * rows_per + rr;
-      const int grow = mt * BM + row;
-      if (grow >= q_rows) continue;
-      const long long orow = (long long)g * q_rows + grow;
-      const float li = lane < cl ? ptx::ld_cluster_f32(ptx::mapa(stg + BM * C::SROW + row, lane)) : -INFINITY;
-      const float mx = warp_max(li);
-      const float w = (lane < cl && li != -INFINITY) ? __expf(li - mx) : 0.f;
-      const float z = warp_sum(w);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 x[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)  // all loads in flight
-        x[i] = (i < cl && col) ? ptx::ld_cluster_v4(ptx::mapa(stg + row * C::SROW + lane * 4, i))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float wi = __shfl_sync(0xffffffffu, w, i & 31);
-        if (i < cl && wi != 0.f) {
-          acc.x += wi * x[i].x; acc.y += wi * x[i].y; acc.z += wi * x[i].z; acc.w += wi * x[i].w;
-        }
-      }
-      const float iz = z > 0.f ? 1.f / z : 0.f;
-      const float4 o = make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
-      const float L = z > 0.f ? mx + logf(z) : -INFINITY;
-      if (fin.out == nullptr || !fin.skip_partial) {
-        if (col) {
-          if (sc.o_bf16) {
-            uint2 u;
-            u.x = ptx::pack_bf16(o.x, o.y);
-            u.y = ptx::pack_bf16(o.z, o.w);
-            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + lane * 4) = u;
-          } else {
-            *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) = o;
-          }
-        }
-        if (lane == 0) lse_out[orow] = L;
-      }
-      if (fin.out != nullptr) {  // fused final merge with (o2, l2), as final_merge_row
-        const float l2 = fin.l2 ? fin.l2[orow] : -INFINITY;
-        const float m = fmaxf(L, l2);
-        const bool flive = m != -INFINITY;
-        const float wp = (flive && L != -INFINITY) ? __expf(L - m) : 0.f;
-        const float w2 = (flive && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
-        const float fiz = flive ? 1.f / (wp + w2) : 0.f;
-        if (col) {
-          float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (w2 != 0.f) {
-            if (fin.o2_bf16) {
-              const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(fin.o2) +
-                                                              orow * D + lane * 4);
-              o2 = make_float4(ptx::bf16_lo(u.x), ptx::bf16_hi(u.x), ptx::bf16_lo(u.y), ptx::bf16_hi(u.y));
-            } else {
-              o2 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(fin.o2) + orow * D + lane * 4);
-            }
-          }
-          const float4 f = make_float4((__fmul_rn(wp, o.x) + __fmul_rn(w2, o2.x)) * fiz,
-                                       (__fmul_rn(wp, o.y) + __fmul_rn(w2, o2.y)) * fiz,
-                                       (__fmul_rn(wp, o.z) + __fmul_rn(w2, o2.z)) * fiz,
-                                       (__fmul_rn(wp, o.w) + __fmul_rn(w2, o2.w)) * fiz);
-          if (fin.out_bf16) {
-            uint2 u;
-            u.x = ptx::pack_bf16(f.x, f.y);
-            u.y = ptx::pack_bf16(f.z, f.w);
-            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + lane * 4) = u;
-          } else {
-            *reinterpret_cast<float4*>(reinterpret_cast<float*>(fin.out) + orow * D + lane * 4) = f;
-          }
-        }
-        if (!flive && lane == 0 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
-      }
-    }
-    ptx::cluster_sync();  // the other CTAs' reads of this CTA's staging are done
-  }
   if (threadIdx.x == 0) stamp(7);
   if (warp == 2) {
     ptx::tc_fence_after();
@@ -1825,6 +1901,15 @@ static int k1_cluster_mode() {
   }
   return m;
 }
+// FB_K1_CLUSTER_DSMEM=1: the cluster reduction reads partials through DSMEM
+static bool k1_cluster_dsmem() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_K1_CLUSTER_DSMEM");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v != 0;
+}
 static long long g_cluster_launches = 0;
 long long k1_cluster_launches() { return g_cluster_launches; }
 
@@ -2102,10 +2187,14 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
       const long long per_streamk = (p.T + p.ctas - 1) / p.ctas;
       for (int cl = cm == 1 ? 16 : 4; cl >= 2; cl >>= 1) {
         if ((long long)p.items * cl > num_sms() || p.tpi < 2 * cl) continue;
+        if (ws == nullptr || ws_bytes < (size_t)p.items * cl * sm100::BM * (D + 1) * sizeof(float)) continue;
         if (cm != 1 && (p.tpi + cl - 1) / cl > per_streamk + 3) continue;
         if (k1_max_clusters<D, GATHER>(cl) < p.items) continue;
         sc.clus = cl;
+        sc.clus_dsm = k1_cluster_dsmem() ? 1 : 0;
         p.ctas = sc.ctas = p.items * cl;
+        ws_o = reinterpret_cast<float*>(ws);  // one partial slot per CTA
+        ws_l = ws_o + (size_t)p.ctas * sm100::BM * D;
         need_merge = false;
         flags = nullptr;
         if (fin != nullptr) kfin = *fin;

@@ -20,6 +20,8 @@ for dens in [float(x) for x in sys.argv[1:]] or [0.1]:
         torch.cuda.synchronize()
     lib.fb_debug_set_trace(None)
     t = tr.view(148, 8).cpu().numpy().astype(np.int64)
+    t = t[t[:, 0] > 0]  # CTAs of this launch (cluster plans use fewer than 148)
+    print(f"  CTAs traced: {t.shape[0]}")
     t0 = t[:, 0].min()
     rel = lambda x: (x - t0) / 1e3
     pc = lambda x: np.round(np.percentile(x, [0, 10, 50, 90, 100]), 1)
@@ -30,4 +32,8 @@ for dens in [float(x) for x in sys.argv[1:]] or [0.1]:
     print("  seg0 stored      ", pc(rel(t[:, 6])))
     last = np.max(np.where(t[:, 1:5] > 0, t[:, 1:5], 0), axis=1)
     print("  last epi end     ", pc(rel(last)))
+    if os.environ.get("CLUSTER_STAMPS"):  # cluster plan: 3 = before the 1st cluster barrier, 4 = after, 1 = reduced
+        print("  cl: prefetched   ", pc(rel(t[:, 3])))
+        print("  cl: barrier 1    ", pc(rel(t[:, 4])))
+        print("  cl: reduced      ", pc(rel(t[:, 1])))
     print("  CTA done         ", pc(rel(t[:, 7])))
