@@ -98,6 +98,7 @@ struct Sched {
   int o_bf16;              // final partial O rows stored as bf16 (FB_PARTIAL_BF16)
   int clus;                // cluster split-K: CTAs per item (one cluster each), 0 = stream-K
   int clus_dsm;            // cluster reduction reads the partials through DSMEM (else via L2)
+  int rot;                 // two-query-tile kernel: rotate each segment's key tiles (Seg::shift)
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -1843,6 +1844,14 @@ static int launch_quad_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   if (causal) cz = *causal;
   sm100::Sched sc{(long long)items * tpi, (int)tpi, m_tiles, items, 0, nullptr, glist};
   sc.kv_keep = m_tiles > 1 && kv_keep_enabled();
+  {
+    static int rot = -1;  // FB_QUAD_ROT=0: no key-tile rotation (diagnostics)
+    if (rot < 0) {
+      const char* e = getenv("FB_QUAD_ROT");
+      rot = (e != nullptr && e[0] == '0') ? 0 : 1;
+    }
+    sc.rot = causal == nullptr ? rot : 0;
+  }
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   bool need_merge;

@@ -70,11 +70,13 @@ struct Seg {
   long long ib, t0;  // item's first tile, segment's first tile (same space)
   int n;             // tiles in the segment
   bool whole;
+  int shift;         // key-tile rotation (Sched::rot): local tile lt reads key tile (lt + shift) % tpi
 };
 struct SegIter {
   long long t, t_begin, t_end;
   int item, k, pr, npairs;
   __device__ __forceinline__ bool next(const Sched& sc, const Causal& cz, int q_rows, Seg& s) {
+    s.shift = 0;
     if (sc.rr) {
       const int idx = k * npairs + pr;
       if (idx >= sc.items) return false;
@@ -102,6 +104,17 @@ struct SegIter {
     const long long ie = sc.item_end(item);
     s.n = (int)(min(t_end, ie) - t);
     s.whole = s.ib >= t_begin && ie <= t_end;
+    // Key-tile rotation (attention over an item's keys is order-free): every
+    // CTA starts streaming at key tile 0 of its first segment and whole items
+    // start at the CTA's clock, so the CTAs sharing a head read the same K/V
+    // tiles at about the same time (L2 reuse without lock-step items).  A
+    // split item's part [x, y) reads key tiles [tpi - y, tpi - x): the parts
+    // stay disjoint and cover the item.
+    if (sc.rot && sc.prefix == nullptr) {
+      const int tpi = sc.tpi;
+      const int x = (int)(t - s.ib), y = x + s.n;
+      s.shift = s.whole ? (int)((t - t_begin) % tpi) : (int)(((long long)2 * tpi - x - y) % tpi);
+    }
     t += s.n;
     return true;
   }

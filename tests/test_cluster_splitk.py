@@ -134,3 +134,30 @@ def test_cluster_large_block_cached_step_with_bf16_ext(lib):
     b, nb = _run(lib, 0, lambda: K.internal_merge(q, ki, vi, ob, le, out_dtype=torch.float32))
     assert na == 1 and nb == 0
     assert float((a - b).abs().max()) <= 5e-3 * float(b.abs().max())
+
+
+@pytest.mark.parametrize("n_ext,n_in", [(16384, 32), (4104, 32), (4096, 24)])
+def test_gather_atom_layout_is_bitwise_equal(lib, n_ext, n_in):
+    """K7 / K8 with the atom smem layout (one 4 KB TMA box per 16-key block)
+    compute exactly what the two-box layout does: same tiles, same MMAs."""
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(n_ext + n_in)
+    groups, rows = 8, 4 * n_in
+    q, k, v = _r(g, groups, rows, 128), _r(g, groups, n_ext, 128), _r(g, groups, n_ext, 128)
+    ki, vi = _r(g, groups, n_in, 128), _r(g, groups, n_in, 128)
+    budget = K.mask_budget(n_ext, 0.2, 16)
+    sel = K.topk_blocks(K.block_mass(q, k, ki, n_ext, 16), budget)
+    outs = []
+    try:
+        for atoms in (1, 0):
+            lib.fb_debug_set_gather_atoms(atoms)
+            o7, _, res = K.sparse_partitioned(q, k, v, ki, vi, n_ext, sel)
+            o8 = K.sparse_attend_merge(_r(torch.Generator(device="cuda").manual_seed(1), groups, rows, 128),
+                                       k, v, ki, vi, n_ext, sel, res, out_dtype=torch.float32)
+            torch.cuda.synchronize()
+            outs.append((o7, res[0], res[1], o8))
+    finally:
+        lib.fb_debug_set_gather_atoms(-1)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
