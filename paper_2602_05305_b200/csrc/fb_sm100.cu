@@ -187,7 +187,6 @@ __device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned 
 struct Gather {
   const int32_t* list;  // [groups, n_list] ascending block ids
   int n_list, n_ext, n_in, sel_tiles;
-  int diag_contig;      // diagnostics (FB_K8_DIAG=1): read contiguous rows instead of the list
   // Atom layout (d = 128): a K / V tile is 16 atoms of 8 keys x [2 d-halves x
   // 128 B] (2 KB each), so a whole 16-key block -- both d-halves, two atoms --
   // is ONE 4 KB TMA box of a 5-D view {64 cols, 8 rows, 2 halves, atoms,
@@ -224,7 +223,11 @@ struct Causal {
 // (ptx::ex2_poly) instead of MUFU; 0 = MUFU only.
 constexpr int K1_POLY = 0;  // measured: the extra FMA-pipe instructions cost more than MUFU
 
-template <int D, bool GATHER, int DIAG = 0, int POLY = K1_POLY>
+// CL: cluster split-K variant (Sched::clus > 0); AT: atom-layout gather
+// (Gather::atoms).  Compile-time, so the common kernels stay lean: the extra
+// code in one kernel cost the gathered K7 residual pass 50 % through
+// instruction-cache misses (ncu: no-instruction stalls 0.43 -> 2.26 per issue).
+template <int D, bool GATHER, int DIAG = 0, int POLY = K1_POLY, bool CL = false, bool AT = false>
 __global__ void __launch_bounds__(THREADS, 1)
 refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ki,
@@ -283,9 +286,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const uint32_t tmem = bar->tmem_base;
   ptx::pdl_wait();               // inputs of this launch are final from here on
   ptx::pdl_launch_dependents();  // let the next kernel's prologue start
-  // registers: control warpgroup 56/thread, softmax warpgroups 224 (64,512 of 65,536)
+  // registers: control warpgroup 72/thread, softmax warpgroups 216 (64,512 of 65,536; at 56 / 224
+  // the gathered producer spilled and K7 streamed ~25 % slower)
   if (warp < 4) {
-  ptx::setmaxnreg_dec<56>();
+  ptx::setmaxnreg_dec<72>();
   if (warp == 0 || (warp == 3 && sc.vprod)) {
     // ------------------------------------------------------------ TMA producer
     // warp 0 issues Q and K; V comes from warp 3 when sc.vprod (two issuing
@@ -341,7 +345,6 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             for (int i = 0; i < 8; ++i) {
               const int e = lt * 8 + i;
               rows[i] = e < ga.n_list ? __ldg(ga.list + (long long)g * ga.n_list + e) * 16 : ga.n_ext;
-              if (ga.diag_contig) rows[i] = (lt * 128 + i * 16) % ga.n_ext;  // diagnostics: same bytes, contiguous
               slabs[i] = g;
               if (pg.table != nullptr) {  // paged cache: block -> (page, row); none -> past a page
                 if (e < ga.n_list) {
@@ -356,7 +359,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             if (do_k) {
               ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-              if (ga.atoms) {
+              if constexpr (AT) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                   ptx::tma_load_5d(smem + C::OFF_K + s * C::TILE_BYTES + i * 4096, &tm_k, &bar->k_full[s], 0, 0,
@@ -372,7 +375,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             if (do_v) {
               ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-              if (ga.atoms) {
+              if constexpr (AT) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                   ptx::tma_load_5d(smem + C::OFF_V + s * C::TILE_BYTES + i * 4096, &tm_v, &bar->v_full[s], 0, 0,
@@ -390,7 +393,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             if (do_k) {
               ptx::mbar_wait(&bar->k_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
-              if (ga.atoms)
+              if constexpr (AT)
                 ptx::tma_load_5d(smem + C::OFF_K + s * C::TILE_BYTES, &tm_ki, &bar->k_full[s], 0, 0, 0, row / 8, g,
                                  stream);
               else
@@ -401,7 +404,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             if (do_v) {
               ptx::mbar_wait(&bar->v_empty[s], ph ^ 1);
               ptx::mbar_expect_tx(&bar->v_full[s], C::TILE_BYTES);
-              if (ga.atoms)
+              if constexpr (AT)
                 ptx::tma_load_5d(smem + C::OFF_V + s * C::TILE_BYTES, &tm_vi, &bar->v_full[s], 0, 0, 0, row / 8, g,
                                  stream);
               else
@@ -439,7 +442,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             ptx::tc_fence_after();
             const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
             const uint32_t d_s = tmem + ((j & 1) ? C::COL_S1 : C::COL_S0);
-            const bool at = GATHER && ga.atoms;
+            constexpr bool at = GATHER && AT;
             const uint32_t k_half = at ? 1024u : C::BOX_BYTES, k_sbo = at ? 2048u : 1024u;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
@@ -471,7 +474,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             const uint32_t p_tmem = tmem + ((jj & 1) ? C::COL_S1 : C::COL_S0);
             const uint32_t o_tmem = tmem + ((jj & 1) ? C::COL_O1 : C::COL_O0);
             if constexpr (DIAG != 3) {  // DIAG 3 (diagnostics): no P V MMA, S = Q K^T only
-              const bool at = GATHER && ga.atoms;
+              constexpr bool at = GATHER && AT;
 #pragma unroll
               for (int kk = 0; kk < BN / 16; ++kk) {
                 // MN-major SW128 V: 16 keys = 16 rows of 128 B; d halves LBO apart
@@ -493,12 +496,12 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
     }
   }
-  if (sc.clus > 0) {  // the cluster reduction's barrier(s) (softmax warps do the work)
+  if constexpr (CL) {  // the cluster reduction's barrier(s) (softmax warps do the work)
     ptx::cluster_sync();
     if (sc.clus_dsm) ptx::cluster_sync();
   }
   } else {
-    ptx::setmaxnreg_inc<224>();
+    ptx::setmaxnreg_inc<216>();
     // ------------------------------------------------------------ softmax
     // Two warpgroups take alternate key tiles, each with its own running
     // (max, sum) and O accumulator, so one's softmax overlaps the other's.
@@ -713,7 +716,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int cb = blockIdx.x + 1, ce = owner ? sc.cta_of(sc.item_end(item) - 1) : 0;
       float* dst;
       float* stg = reinterpret_cast<float*>(smem + C::OFF_STG);  // cluster split-K staging
-      if (sc.clus > 0) {
+      if constexpr (CL) {
         dst = stg + row * C::SROW;
         if (wg == 1) stg[BM * C::SROW + row] = lse;
       } else if (whole || owner) {
@@ -775,7 +778,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               }
             }
           }
-          if (sc.clus > 0) {
+          if constexpr (CL) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
               *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -794,10 +797,10 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, 1ull);
       }
-      if (sc.clus == 0 && (whole || owner) && live && wg == 1) lse_out[orow] = lse;
+      if (!CL && (whole || owner) && live && wg == 1) lse_out[orow] = lse;
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
-    if (sc.clus > 0) {
+    if constexpr (CL) {
       // Cluster split-K reduction: the item's CTAs (one cluster) publish their
       // normalised partials, meet at the cluster barrier, and CTA `rank` merges
       // rows [rank*BM/clus, ...) over all of them in rank order (the same
@@ -1929,7 +1932,7 @@ static int k1_max_clusters(int cl) {
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   if (cache[cl] == 0) {
-    auto kern = sm100::refresh_kernel<D, GATHER>;
+    auto kern = sm100::refresh_kernel<D, GATHER, 0, sm100::K1_POLY, true, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm100::Cfg<D>::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
@@ -1953,8 +1956,8 @@ static int k1_max_clusters(int cl) {
   return cache[cl] > 0 ? cache[cl] : 0;
 }
 
-// diagnostics: FB_K8_DIAG=1 gathers contiguous rows (same bytes, 16-row boxes),
-// 2 skips the split-merge kernel after a gather launch
+// diagnostics: FB_K8_DIAG=2 skips the split-merge kernel after a gather launch
+// (round 2 also measured gathering contiguous rows, FB_K8_DIAG=1: slower)
 static int k8_diag() {
   static int v = -1;
   if (v < 0) {
@@ -2036,7 +2039,6 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ga.n_ext = (int)gs->n_ext;
     ga.n_in = (int)gs->n_in;
     ga.sel_tiles = (int)((gs->n_list + 7) / 8);
-    ga.diag_contig = k8_diag() == 1;
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   } else {
     // cache rows [0, n_ext) in 16-row boxes; current block [0, n_in) in 128-row boxes
@@ -2062,7 +2064,6 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ga.n_ext = (int)gs->n_ext;
     ga.n_in = (int)gs->n_in;
     ga.sel_tiles = (int)((gs->n_list + 7) / 8);
-    ga.diag_contig = k8_diag() == 1;
     tiles = ga.sel_tiles + (gs->n_in + sm100::BN - 1) / sm100::BN;
   }
   const bool o_bf16 = !GATHER && partial_out_bf16();
@@ -2106,11 +2107,6 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
              : poly == 3 ? sm100::refresh_kernel<D, false, 0, 3> : sm100::refresh_kernel<D, false, 0, 4>;
       ai = 5 + poly;
     }
-  }
-  static bool attr[10] = {};
-  if (!attr[ai]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr[ai] = true;
   }
   // group subset: items over the listed groups only (tensor maps span all groups)
   RefreshPlan p = plan_refresh(glist ? n_list : groups, q_rows, D, std::max<int64_t>(tiles, 1) * sm100::BN);
@@ -2217,14 +2213,27 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     const PagingCtx* pc = current_paging();
     pgv = sm100::Paged{pc->table, (int)pc->max_pages, (int)pc->page_rows};
   }
-  if (sc.clus > 0) {
-    static bool npc[16] = {};
-    if (!npc[ai]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      npc[ai] = true;
+  // lean variants: cluster split-K and / or the atom-layout gather (diagnostic
+  // variants above are plain stream-K kernels)
+  if (ai == 0 && (sc.clus > 0 || ga.atoms)) {
+    constexpr int PL = sm100::K1_POLY;
+    const bool cl = sc.clus > 0, at = GATHER && ga.atoms;
+    if constexpr (GATHER) {
+      kern = cl ? (at ? sm100::refresh_kernel<D, true, 0, PL, true, true>
+                      : sm100::refresh_kernel<D, true, 0, PL, true, false>)
+                : sm100::refresh_kernel<D, true, 0, PL, false, true>;
+    } else {
+      kern = sm100::refresh_kernel<D, false, 0, PL, true, false>;
     }
-    ++g_cluster_launches;
+    ai = 10 + (cl ? 1 : 0) + (at ? 2 : 0);
   }
+  static bool attr[14] = {};
+  if (!attr[ai]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (ai >= 10) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr[ai] = true;
+  }
+  if (sc.clus > 0) ++g_cluster_launches;
   launch_pdl_cluster(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, sc.clus, mq, mk, mv, mki,
                      mvi, ga, pgv, cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out,
                      lse_out, ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr,
