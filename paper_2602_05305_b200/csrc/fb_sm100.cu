@@ -97,7 +97,6 @@ struct Sched {
   int vprod;               // refresh kernel: warp 3 issues the V tiles (warp 0 Q and K)
   int o_bf16;              // final partial O rows stored as bf16 (FB_PARTIAL_BF16)
   int clus;                // cluster split-K: CTAs per item (one cluster each), 0 = stream-K
-  int clus_dsm;            // cluster reduction reads the partials through DSMEM (else via L2)
   int rot;                 // two-query-tile kernel: rotate each segment's key tiles (Seg::shift)
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
@@ -222,6 +221,153 @@ struct Causal {
 // POLY: every POLY-th pair of P values per thread takes 2^x on the FMA pipes
 // (ptx::ex2_poly) instead of MUFU; 0 = MUFU only.
 constexpr int K1_POLY = 0;  // measured: the extra FMA-pipe instructions cost more than MUFU
+
+// Cluster split-K reduction.  The CLS CTAs of an item's cluster publish their
+// staged normalised partials to global slots (coalesced 512 B rows), meet at
+// the cluster barrier, and CTA `rank` merges rows [rank*128/CLS, ...) over all
+// of them in rank order -- the log-space merge of combine_partials
+// (attention.py:207-233) -- then applies the MergeFinal merge if any and
+// writes the finished rows.  The 8 softmax warps each take 16/CLS rows, all
+// at once: a row is spread over 2*CLS lanes of D/(2*CLS) columns each; every
+// lane loads the row's CLS LSEs and its column slice of the CLS partials (all
+// in flight), so the merge costs one L2 round trip per warp.  (DSMEM instead
+// of L2 measured equal; one row per warp at a time was 2-4x slower.)
+template <int CLS, int D, int SROW>
+__device__ __forceinline__ void cluster_reduce(int rank, const Sched& sc, int item, int w8, int lane, int q_rows,
+                                               const float* stg, float* __restrict__ ws_o,
+                                               float* __restrict__ ws_l, float* __restrict__ o_out,
+                                               float* __restrict__ lse_out, const MergeFinal& fin,
+                                               unsigned long long* trace) {
+  // diagnostics (trace != nullptr): globaltimer after publishing (slot 3) and after the barrier (slot 4)
+  auto stamp = [&](int slot) {
+    if (trace != nullptr && w8 == 0 && lane == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[blockIdx.x * 8 + slot] = t;
+    }
+  };
+  constexpr int NRW = 16 / CLS;      // rows per warp (rows_per = BM / CLS over 8 warps)
+  constexpr int LPR = 32 / NRW;      // lanes per row
+  constexpr int NV = (D / 4 + LPR - 1) / LPR;  // float4 chunks per lane: chunk v = columns 4 * (v * LPR + lsub)
+  constexpr int ROWS_PER = BM / CLS;
+  static_assert(NV >= 1 && NRW * LPR == 32 && (D / 4) % LPR == 0 || NV == 1, "cluster_reduce mapping");
+  const int g = sc.group_of(item), mt = sc.mtile_of(item);
+  const int rsub = lane / LPR, lsub = lane % LPR;
+  const int row = rank * ROWS_PER + w8 + rsub * 8;  // this lane's row (tile-local)
+  const bool ok = mt * BM + row < q_rows;
+  const long long orow = (long long)g * q_rows + mt * BM + row;
+  auto colv = [&](int v) { return 4 * (v * LPR + lsub); };  // coalesced: a row's lanes read adjacent 16 B
+  const bool cok = colv(0) < D;  // (d = 64 on 16-CTA clusters: half the lanes idle)
+  // the MergeFinal (o2, l2) rows are final before this launch: load them first
+  float l2 = -INFINITY;
+  float4 o2[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) o2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok && fin.out != nullptr && fin.l2 != nullptr) {
+    l2 = __ldg(fin.l2 + orow);
+    if (l2 != -INFINITY && cok) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (fin.o2_bf16) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(fin.o2) +
+                                                               orow * D + colv(v)));
+          o2[v] = make_float4(ptx::bf16_lo(u.x), ptx::bf16_hi(u.x), ptx::bf16_lo(u.y), ptx::bf16_hi(u.y));
+        } else {
+          o2[v] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(fin.o2) + orow * D + colv(v)));
+        }
+      }
+    }
+  }
+  // publish this CTA's partial: staged rows (stride SROW) -> its global slot
+  asm volatile("bar.sync 5, 256;" ::: "memory");
+  {
+    float* my_o = ws_o + (long long)blockIdx.x * BM * D;
+    float* my_l = ws_l + (long long)blockIdx.x * BM;
+    const bool colp = lane * 4 < D;
+    for (int r = w8; r < BM; r += 8) {
+      if (colp)
+        *reinterpret_cast<float4*>(my_o + r * D + lane * 4) = *reinterpret_cast<const float4*>(stg + r * SROW + lane * 4);
+      if (lane == 0) my_l[r] = stg[BM * SROW + r];
+    }
+  }
+  stamp(3);
+  ptx::cluster_sync();  // release / acquire (cluster scope; invalidates L1): every CTA of the cluster published
+  stamp(4);
+  const float* part_o = ws_o + (long long)item * CLS * BM * D;
+  const float* part_l = ws_l + (long long)item * CLS * BM;
+  float li[CLS];
+  float4 x[CLS][NV];
+#pragma unroll
+  for (int i = 0; i < CLS; ++i) {
+    li[i] = ok ? part_l[(long long)i * BM + row] : -INFINITY;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      x[i][v] = (ok && cok) ? *reinterpret_cast<const float4*>(part_o + ((long long)i * BM + row) * D + colv(v))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (!ok) return;
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < CLS; ++i) mx = fmaxf(mx, li[i]);
+  float w[CLS], z = 0.f;
+#pragma unroll
+  for (int i = 0; i < CLS; ++i) {
+    w[i] = li[i] != -INFINITY ? __expf(li[i] - mx) : 0.f;
+    z += w[i];
+  }
+  const float iz = z > 0.f ? 1.f / z : 0.f;
+  float4 acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < CLS; ++i) {  // rank order
+      acc[v].x += w[i] * x[i][v].x; acc[v].y += w[i] * x[i][v].y;
+      acc[v].z += w[i] * x[i][v].z; acc[v].w += w[i] * x[i][v].w;
+    }
+    acc[v] = make_float4(acc[v].x * iz, acc[v].y * iz, acc[v].z * iz, acc[v].w * iz);
+  }
+  const float L = z > 0.f ? mx + logf(z) : -INFINITY;
+  if (fin.out == nullptr || !fin.skip_partial) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!cok) break;
+      if (sc.o_bf16) {
+        uint2 u;
+        u.x = ptx::pack_bf16(acc[v].x, acc[v].y);
+        u.y = ptx::pack_bf16(acc[v].z, acc[v].w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + colv(v)) = u;
+      } else {
+        *reinterpret_cast<float4*>(o_out + orow * D + colv(v)) = acc[v];
+      }
+    }
+    if (lsub == 0) lse_out[orow] = L;
+  }
+  if (fin.out != nullptr) {  // fused final merge with (o2, l2), as final_merge_row
+    const float m = fmaxf(L, l2);
+    const bool flive = m != -INFINITY;
+    const float wp = (flive && L != -INFINITY) ? __expf(L - m) : 0.f;
+    const float w2 = (flive && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
+    const float fiz = flive ? 1.f / (wp + w2) : 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!cok) break;
+      const float4 f = make_float4((__fmul_rn(wp, acc[v].x) + __fmul_rn(w2, o2[v].x)) * fiz,
+                                   (__fmul_rn(wp, acc[v].y) + __fmul_rn(w2, o2[v].y)) * fiz,
+                                   (__fmul_rn(wp, acc[v].z) + __fmul_rn(w2, o2[v].z)) * fiz,
+                                   (__fmul_rn(wp, acc[v].w) + __fmul_rn(w2, o2[v].w)) * fiz);
+      if (fin.out_bf16) {
+        uint2 u;
+        u.x = ptx::pack_bf16(f.x, f.y);
+        u.y = ptx::pack_bf16(f.z, f.w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + colv(v)) = u;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(fin.out) + orow * D + colv(v)) = f;
+      }
+    }
+    if (!flive && lsub == 0 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
+  }
+}
 
 // CL: cluster split-K variant (Sched::clus > 0); AT: atom-layout gather
 // (Gather::atoms).  Compile-time, so the common kernels stay lean: the extra
@@ -496,10 +642,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
     }
   }
-  if constexpr (CL) {  // the cluster reduction's barrier(s) (softmax warps do the work)
-    ptx::cluster_sync();
-    if (sc.clus_dsm) ptx::cluster_sync();
-  }
+  if constexpr (CL) ptx::cluster_sync();  // the cluster reduction's barrier (softmax warps do the work)
   } else {
     ptx::setmaxnreg_inc<216>();
     // ------------------------------------------------------------ softmax
@@ -801,163 +944,18 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
     if constexpr (CL) {
-      // Cluster split-K reduction: the item's CTAs (one cluster) publish their
-      // normalised partials, meet at the cluster barrier, and CTA `rank` merges
-      // rows [rank*BM/clus, ...) over all of them in rank order (the same
-      // log-space merge as combine_partials, attention.py:207-233) and writes
-      // the finished rows -- no merge-kernel launch.
-      const int cl = sc.clus;
-      const int rank = (int)ptx::cluster_ctarank();
-      const int item = blockIdx.x / cl;
-      const int g = sc.group_of(item), mt = sc.mtile_of(item);
-      const int rows_per = BM / cl;
-      const int w8 = warp - 4;                                  // the 8 softmax warps do the reduction
-      const int nrw = (rows_per + 7) / 8;                       // rows per warp; nrw * cl <= 16
+      // Cluster split-K reduction (see cluster_reduce); the CTA's rows are
+      // staged in shared memory by the epilogue above
+      const int item = blockIdx.x / sc.clus;
+      const int rk = (int)ptx::cluster_ctarank();
       const float* stg = reinterpret_cast<const float*>(smem + C::OFF_STG);
-      const bool col = lane * 4 < D;
-      constexpr int MAXR = 8;  // rows per warp (rows_per / 8 <= 8 for clus >= 2)
-      // the fused merge's (o2, l2) rows are final before this launch: their
-      // loads go out first and overlap the publishing below
-      float l2v[MAXR];
-      float4 o2v[MAXR];
-#pragma unroll
-      for (int r = 0; r < MAXR; ++r) {
-        const int rr = w8 + r * 8, row = rank * rows_per + rr;
-        const bool ok = r < nrw && rr < rows_per && mt * BM + row < q_rows;
-        const long long orow = (long long)g * q_rows + mt * BM + row;
-        l2v[r] = -INFINITY;
-        o2v[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ok && fin.out != nullptr && fin.l2 != nullptr) {
-          l2v[r] = __ldg(fin.l2 + orow);
-          if (col) {
-            if (fin.o2_bf16) {
-              const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(fin.o2) +
-                                                                   orow * D + lane * 4));
-              o2v[r] = make_float4(ptx::bf16_lo(u.x), ptx::bf16_hi(u.x), ptx::bf16_lo(u.y), ptx::bf16_hi(u.y));
-            } else {
-              o2v[r] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(fin.o2) + orow * D +
-                                                             lane * 4));
-            }
-          }
-        }
+      switch (sc.clus) {
+        case 2: cluster_reduce<2, D, C::SROW>(rk, sc, item, warp - 4, lane, q_rows, stg, ws_o, ws_l, o_out, lse_out, fin, trace); break;
+        case 4: cluster_reduce<4, D, C::SROW>(rk, sc, item, warp - 4, lane, q_rows, stg, ws_o, ws_l, o_out, lse_out, fin, trace); break;
+        case 8: cluster_reduce<8, D, C::SROW>(rk, sc, item, warp - 4, lane, q_rows, stg, ws_o, ws_l, o_out, lse_out, fin, trace); break;
+        default: cluster_reduce<16, D, C::SROW>(rk, sc, item, warp - 4, lane, q_rows, stg, ws_o, ws_l, o_out, lse_out, fin, trace); break;
       }
-      // publish the staged partial to this CTA's global slot (coalesced 512 B
-      // rows; the cluster's CTAs read it back from L2 -- DSMEM reads of the
-      // same 64 KB per CTA took ~8 us, its bandwidth is ~17 B/clk per SM)
-      asm volatile("bar.sync 5, 256;" ::: "memory");
-      if (!sc.clus_dsm) {
-        float* my_o = ws_o + (long long)blockIdx.x * BM * D;
-        float* my_l = ws_l + (long long)blockIdx.x * BM;
-        for (int r = w8; r < BM; r += 8) {
-          if (col)
-            __stcg(reinterpret_cast<float4*>(my_o + r * D + lane * 4),
-                   *reinterpret_cast<const float4*>(stg + r * C::SROW + lane * 4));
-          if (lane == 0) __stcg(my_l + r, stg[BM * C::SROW + r]);
-        }
-        __threadfence();
-      }
-      if (row == 0 && wg == 0) stamp(3);  // (cluster mode uses segment 0's slots only)
-      ptx::cluster_sync();
-      if (row == 0 && wg == 0) stamp(4);
-      const float* part_o = ws_o + (long long)item * cl * BM * D;  // the cluster's partial slots
-      const float* part_l = ws_l + (long long)item * cl * BM;
-      // one row: lane i < cl holds partial i's LSE; up to 4 partials' O slices
-      auto load_row = [&](int row, float& li, float4* x) {
-        if (sc.clus_dsm) {  // partial i staged in cluster CTA i's shared memory
-          li = lane < cl ? ptx::ld_cluster_f32(ptx::mapa(stg + BM * C::SROW + row, lane)) : -INFINITY;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            x[k] = (col && k < cl) ? ptx::ld_cluster_v4(ptx::mapa(stg + row * C::SROW + lane * 4, k))
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-          return;
-        }
-        li = lane < cl ? __ldcg(part_l + (long long)lane * BM + row) : -INFINITY;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          x[k] = (col && k < cl)
-                     ? __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)k * BM + row) * D + lane * 4))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-      };
-      auto finish_row = [&](int row, float li, const float4* x, float l2, float4 o2) {
-        const long long orow = (long long)g * q_rows + mt * BM + row;
-        const float mx = warp_max(li);
-        const float w = (lane < cl && li != -INFINITY) ? __expf(li - mx) : 0.f;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int i0 = 0; i0 < cl; i0 += 4) {  // clus <= 4 (auto mode): one pass over x
-          float4 y[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            y[k] = i0 == 0 ? x[k]
-                   : !(col && i0 + k < cl) ? make_float4(0.f, 0.f, 0.f, 0.f)
-                   : sc.clus_dsm ? ptx::ld_cluster_v4(ptx::mapa(stg + row * C::SROW + lane * 4, i0 + k))
-                                 : __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(i0 + k) * BM + row) * D +
-                                                                          lane * 4));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float wi = __shfl_sync(0xffffffffu, w, (i0 + k) & 31);
-            if (wi != 0.f) {
-              acc.x += wi * y[k].x; acc.y += wi * y[k].y; acc.z += wi * y[k].z; acc.w += wi * y[k].w;
-            }
-          }
-        }
-        const float z = warp_sum(w);
-        const float iz = z > 0.f ? 1.f / z : 0.f;
-        const float4 o = make_float4(acc.x * iz, acc.y * iz, acc.z * iz, acc.w * iz);
-        const float L = z > 0.f ? mx + logf(z) : -INFINITY;
-        if (fin.out == nullptr || !fin.skip_partial) {
-          if (col) {
-            if (sc.o_bf16) {
-              uint2 u;
-              u.x = ptx::pack_bf16(o.x, o.y);
-              u.y = ptx::pack_bf16(o.z, o.w);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + lane * 4) = u;
-            } else {
-              *reinterpret_cast<float4*>(o_out + orow * D + lane * 4) = o;
-            }
-          }
-          if (lane == 0) lse_out[orow] = L;
-        }
-        if (fin.out != nullptr) {  // fused final merge with (o2, l2), as final_merge_row
-          const float m = fmaxf(L, l2);
-          const bool flive = m != -INFINITY;
-          const float wp = (flive && L != -INFINITY) ? __expf(L - m) : 0.f;
-          const float w2 = (flive && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
-          const float fiz = flive ? 1.f / (wp + w2) : 0.f;
-          if (col) {
-            const float4 f = make_float4((__fmul_rn(wp, o.x) + __fmul_rn(w2, o2.x)) * fiz,
-                                         (__fmul_rn(wp, o.y) + __fmul_rn(w2, o2.y)) * fiz,
-                                         (__fmul_rn(wp, o.z) + __fmul_rn(w2, o2.z)) * fiz,
-                                         (__fmul_rn(wp, o.w) + __fmul_rn(w2, o2.w)) * fiz);
-            if (fin.out_bf16) {
-              uint2 u;
-              u.x = ptx::pack_bf16(f.x, f.y);
-              u.y = ptx::pack_bf16(f.z, f.w);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + lane * 4) = u;
-            } else {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(fin.out) + orow * D + lane * 4) = f;
-            }
-          }
-          if (!flive && lane == 0 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
-        }
-      };
-      auto row_ok = [&](int r) {
-        const int rr = w8 + r * 8;
-        return r < nrw && rr < rows_per && mt * BM + rank * rows_per + rr < q_rows;
-      };
-#pragma unroll
-      for (int r = 0; r < MAXR; r += 2) {  // two rows' loads in flight at a time
-        const bool ok0 = row_ok(r), ok1 = row_ok(r + 1);  // warp-uniform
-        if (!ok0) continue;
-        const int row0 = rank * rows_per + w8 + r * 8, row1 = row0 + 8;
-        float li0, li1 = -INFINITY;
-        float4 x0[4], x1[4];
-        load_row(row0, li0, x0);
-        if (ok1) load_row(row1, li1, x1);
-        finish_row(row0, li0, x0, l2v[r], o2v[r]);
-        if (ok1) finish_row(row1, li1, x1, l2v[r + 1], o2v[r + 1]);
-      }
-      if (row == 0 && wg == 0) stamp(1);  // reduction done (stream end was read at the epilogue)
-      if (sc.clus_dsm) ptx::cluster_sync();  // the other CTAs' reads of this CTA's staging are done
+      if (row == 0 && wg == 0) stamp(1);  // reduction done
     }
   }
 
@@ -1913,15 +1911,6 @@ static int k1_cluster_mode() {
   }
   return m;
 }
-// FB_K1_CLUSTER_DSMEM=1: the cluster reduction reads partials through DSMEM
-static bool k1_cluster_dsmem() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FB_K1_CLUSTER_DSMEM");
-    v = (e != nullptr && e[0] == '1') ? 1 : 0;
-  }
-  return v != 0;
-}
 static long long g_cluster_launches = 0;
 long long k1_cluster_launches() { return g_cluster_launches; }
 
@@ -2196,7 +2185,6 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
         if (cm != 1 && (p.tpi + cl - 1) / cl > per_streamk + 3) continue;
         if (k1_max_clusters<D, GATHER>(cl) < p.items) continue;
         sc.clus = cl;
-        sc.clus_dsm = k1_cluster_dsmem() ? 1 : 0;
         p.ctas = sc.ctas = p.items * cl;
         ws_o = reinterpret_cast<float*>(ws);  // one partial slot per CTA
         ws_l = ws_o + (size_t)p.ctas * sm100::BM * D;

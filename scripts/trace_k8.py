@@ -32,8 +32,8 @@ for dens in [float(x) for x in sys.argv[1:]] or [0.1]:
     print("  seg0 stored      ", pc(rel(t[:, 6])))
     last = np.max(np.where(t[:, 1:5] > 0, t[:, 1:5], 0), axis=1)
     print("  last epi end     ", pc(rel(last)))
-    if os.environ.get("CLUSTER_STAMPS"):  # cluster plan: 3 = before the 1st cluster barrier, 4 = after, 1 = reduced
-        print("  cl: prefetched   ", pc(rel(t[:, 3])))
-        print("  cl: barrier 1    ", pc(rel(t[:, 4])))
+    if os.environ.get("CLUSTER_STAMPS"):  # cluster plan: 3 = published, 4 = past the barrier, 1 = reduced
+        print("  cl: published    ", pc(rel(t[:, 3])))
+        print("  cl: barrier      ", pc(rel(t[:, 4])))
         print("  cl: reduced      ", pc(rel(t[:, 1])))
     print("  CTA done         ", pc(rel(t[:, 7])))
