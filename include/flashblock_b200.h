@@ -69,9 +69,11 @@ typedef enum fb_dtype { FB_F64 = 0, FB_F32 = 1, FB_BF16 = 2 } fb_dtype;
  * partial's out in the tensor dtype (attention.py:70-71); for the cached
  * external partial this halves the bytes every cached step re-reads.
  * Accepted by fb_attention_partial(_sync/_ragged/_paged/_groups) (o_out
- * written bf16), fb_internal_merge(_ex) and fb_internal_merge_tok (o_ext read
- * as bf16; o_int not supported) and fb_combine (every o_parts[p] bf16).
- * Other entry points reject it (FB_ERR_VALUE). */
+ * written bf16; the tcgen05 path only, else FB_ERR_UNSUPPORTED) and by
+ * fb_internal_merge(_ex) / fb_internal_merge_tok (o_ext read as bf16; o_int /
+ * lse_int not supported).  fb_combine already writes a bf16 o_out through
+ * out_dtype FB_BF16 (its inputs stay fp32).  Other entry points reject the
+ * bit (FB_ERR_VALUE: unknown dtype). */
 #define FB_PARTIAL_BF16 0x100
 
 /* Message for the last non-OK status returned on this host thread. */
