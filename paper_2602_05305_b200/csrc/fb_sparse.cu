@@ -199,6 +199,7 @@ topk_radix_kernel(const double* __restrict__ mass, int nb, int budget, int32_t* 
         if (hit) {
           const int src = __ffs(hit) - 1;
           const int cnt_before = __shfl_sync(0xffffffffu, above + inc - c, src);
+          __syncwarp();  // every lane's read of sh_k (above) precedes lane 0's write
           if (lane == 0) {
             sh_prefix = prefix | ((unsigned long long)(base - src) << shift);
             sh_k = k - cnt_before;
