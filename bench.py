@@ -11,9 +11,14 @@ full-recompute baseline runs K1+K2 on every step.  Synthetic bf16 inputs,
 N(0,1), seeded; every layer has its own KV cache (inputs > L2).  The line also
 carries the schedule sweep (unmask per step x tau) against full recompute.
 
-N > 1 (or --workload c3): config C3 (configs[2]) -- 128K context, the KV
-cache of each sequence split along the sequence over the N ranks (strong
-scaling: the same b sequences whatever N).  Refresh step per layer: K1 on
+N > 1: the same C2 line with N ranks each running its own batch (sequences
+are independent: no data-path collective, weak scaling, value = all ranks'
+tokens / max-over-ranks time), so the curve over N is one workload; the run
+then measures config C3 and attaches it as "c3_split_kv".
+
+--workload c3 (main line) / "c3_split_kv": config C3 (configs[2]) -- 128K
+context, the KV cache of each sequence split along the sequence over the N
+ranks (strong scaling: the same b sequences whatever N).  Refresh step per layer: K1 on
 the local shard -> ONE packed exchange of the (O, LSE) partials (grouped
 NCCL send/recv by kv-group chunk) -> K3 merge of this rank's kv-head shard
 -> K2 on the shard; the 31 cached steps run K2 on the head shard only (no
@@ -309,8 +314,10 @@ def run_reference_arm(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
-def _config(args):
+def _config(args, world: int = 1):
     return {"workload": "C2: 8B-class GQA block-diffusion attention, 32K ctx, FlashBlock tau=2",
+            "parallelism": f"dp{world} (independent sequences per rank, no data-path collective)",
+            "global_batch": args.batch * world,
             "layers": LAYERS, "batch_per_gpu": args.batch, "q_heads": HQ, "kv_heads": HKV,
             "head_dim": D, "block": BLK, "ctx": CTX, "steps_per_block": STEPS_PER_BLOCK,
             "unmask_per_step": UNMASK_PER_STEP, "tau": TAU,
@@ -528,7 +535,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "warmup": args.warmup, "ms_per_step": ms_fb / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0,1) bf16, seeded; random KV cache per layer",
-            "config": _config(args),
+            "config": _config(args, world),
             "attention_ms_per_diffusion_step": ms_fb / args.steps / STEPS_PER_BLOCK,
             "full_recompute": {"value": full_value, "unit": UNIT,
                                "ms_per_step": ms_full / steps_full,
@@ -549,7 +556,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "gpu_launches": launches_fb * args.steps,
             "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
 def run_e2e(args, eng, kc, vc, dev, sched, world):
@@ -754,7 +762,7 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     if rank == 0:
         value = b * BLK * args.steps / (ms / 1000.0)
         exch = groups * rows * (D + 1) * 4 * (world - 1) // world if world > 1 else 0
-        print(json.dumps({
+        return {
             "metric": "block-diffusion tokens/s (FlashBlock attention, C3: 128K ctx split-KV)",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -781,7 +789,8 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
             "gpu_launches": eager_launches + cached_launches * args.steps,
             "clocks": clocks,
             "nccl_debug": os.environ.get("NCCL_DEBUG"),
-        }), flush=True)
+        }
+    return None
 
 
 def _relaunch(args) -> int:
@@ -807,7 +816,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-sweep", action="store_true", help="skip the schedule sweep")
     ap.add_argument("--workload", default=None, choices=["c2", "c3"],
-                    help="c2: 32K headline (default at 1 GPU); c3: 128K split-KV (default at >1 GPU)")
+                    help="c2: 32K headline (default; at N > 1 also measures C3 into c3_split_kv); "
+                         "c3: the 128K split-KV line as the main line")
     ap.add_argument("--ctx", type=int, default=C3_CTX, help="context for C3")
     ap.add_argument("--layers", type=int, default=LAYERS, help="layers for C3")
     ap.add_argument("--c3-batch", type=int, default=4, help="sequences for C3 (whole job)")
@@ -822,7 +832,13 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
-    workload = args.workload or ("c3" if world > 1 else "c2")
+    # C2 (the headline, configs[1]) at every N: sequences are independent, so
+    # N ranks run N x the batch with no data-path collective (weak scaling) and
+    # the curve over N stays one workload.  At N > 1 the same run then measures
+    # C3 (configs[2]: 128K context split along the sequence over the N GPUs,
+    # one packed NCCL exchange per refresh) and attaches it as "c3_split_kv".
+    # --workload c3 makes C3 the main line.
+    workload = args.workload or "c2"
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -834,9 +850,24 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         if workload == "c3":
-            run_splitkv(args, rank, world, local_rank)
+            line = run_splitkv(args, rank, world, local_rank)
         else:
-            run_ours(args, rank, world, local_rank)
+            line = run_ours(args, rank, world, local_rank)
+            if world > 1 and args.workload is None:
+                import gc
+
+                import torch
+
+                gc.collect()
+                torch.cuda.empty_cache()  # the C2 caches (155 GB at b=32) go before C3's shards
+                c3 = run_splitkv(args, rank, world, local_rank)
+                if line is not None and c3 is not None:
+                    line["c3_split_kv"] = {k: c3[k] for k in (
+                        "metric", "value", "unit", "ms_per_step", "scaling", "config", "refresh_step_ms",
+                        "refresh_ms_per_layer", "cached_steps_ms", "exchange_bytes_sent_per_layer_per_rank",
+                        "roofline", "gpu_launches")}
+        if line is not None:
+            print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             import torch.distributed as dist
