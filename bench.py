@@ -829,6 +829,10 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("FB_BENCH_BACKEND", "nccl") != "nccl":  # diagnostics: ranks may share GPUs
+        import torch
+
+        local_rank %= max(1, torch.cuda.device_count())
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
@@ -847,7 +851,11 @@ def main():
         os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("FB_BENCH_BACKEND", "nccl")  # gloo: diagnostics (ranks sharing one GPU)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         if workload == "c3":
             line = run_splitkv(args, rank, world, local_rank)
