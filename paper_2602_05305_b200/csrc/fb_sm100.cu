@@ -1745,6 +1745,14 @@ static int launch_pair_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
   const int maxp = pair_clusters();
   sm100::Sched sc{(long long)items * tpi, (int)tpi, m_tiles, items, 0, nullptr, glist};
   sc.kv_keep = m_tiles > 1 && kv_keep_enabled();
+  {
+    static int rot = -1;  // key-tile rotation for non-causal pair plans (FB_QUAD_ROT=0: off)
+    if (rot < 0) {
+      const char* e = getenv("FB_QUAD_ROT");
+      rot = (e != nullptr && e[0] == '0') ? 0 : 1;
+    }
+    sc.rot = causal == nullptr ? rot : 0;
+  }
   float* ws_o = nullptr;
   float* ws_l = nullptr;
   bool need_merge;

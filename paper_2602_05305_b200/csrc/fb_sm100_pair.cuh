@@ -196,7 +196,9 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           for (; t < seg_end; ++t, ++j) {
             const int s = j % C::STAGES;
             const uint32_t ph = (j / C::STAGES) & 1;
-            int row = key_begin + (int)(t - ib) * BN;
+            int lt = (int)(t - ib);
+            if (sg.shift) lt = (lt + sg.shift) % sc.tpi;  // key-tile rotation (Seg::shift)
+            int row = key_begin + lt * BN;
             int slab = g;
             if (pg.table != nullptr) {  // paged cache: the tile's page, row inside it
               slab = __ldg(pg.table + (long long)g * pg.max_pages + row / pg.page_rows);
@@ -314,7 +316,8 @@ pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, reinterpret_cast<uint32_t*>(s) + c * 32);
         ptx::tmem_wait_ld();
         {
-          const int valid = ke - (kb + t * BN);
+          const int valid = sg.shift ? key_end - (key_begin + ((lt0 + t + sg.shift) % sc.tpi) * BN)
+                                     : ke - (kb + t * BN);
           if (valid < BN) {
 #pragma unroll
             for (int i = 0; i < BN; ++i)

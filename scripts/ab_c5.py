@@ -29,8 +29,9 @@ for n_ext in (56160, 18720, 0):
         fl = 4.0 * H * B * B * D
         name = "cached step (4680-key block)"
     graphs = {}
-    for mode in (2, 1):
-        lib.fb_debug_set_quad(mode)
+    for mode in (2, 1, 3):  # 3: CTA pairs (quad off, pair forced)
+        lib.fb_debug_set_quad(0 if mode == 3 else mode)
+        lib.fb_debug_set_pair(1 if mode == 3 else -1)
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):
             fn(); torch.cuda.synchronize()
@@ -40,15 +41,16 @@ for n_ext in (56160, 18720, 0):
                     fn()
         graphs[mode] = gr
     lib.fb_debug_set_quad(-1)
-    res = {2: [], 1: []}
+    lib.fb_debug_set_pair(-1)
+    res = {2: [], 1: [], 3: []}
     for rnd in range(8):
-        for mode in ((2, 1) if rnd % 2 == 0 else (1, 2)):
+        for mode in ((2, 1, 3) if rnd % 2 == 0 else (3, 1, 2)):
             graphs[mode].replay(); torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); graphs[mode].replay(); e1.record(); torch.cuda.synchronize()
             res[mode].append(e0.elapsed_time(e1) / 3)
     rec = {"shape": name}
-    for mode, nm in ((2, "single"), (1, "quad_rot")):
+    for mode, nm in ((2, "single"), (1, "quad_rot"), (3, "pair_rot")):
         ms = sorted(res[mode])[len(res[mode]) // 2]
         rec[nm + "_ms"] = round(ms, 4)
         rec[nm + "_frac"] = round(fl / (ms * 1e-3) / 1e12 / PEAK, 3)
