@@ -161,3 +161,19 @@ def test_gather_atom_layout_is_bitwise_equal(lib, n_ext, n_in):
         lib.fb_debug_set_gather_atoms(-1)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("groups,q_rows,n", [(4, 128, 4096), (3, 64, 2500)])
+def test_cluster_k1_head_dim_64(lib, groups, q_rows, n):
+    from oracle import flashblock_oracle as orc
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(64 + n)
+    q, k, v = _r(g, groups, q_rows, 64), _r(g, groups, n, 64), _r(g, groups, n, 64)
+    (o_c, l_c), nc = _run(lib, 1, lambda: K.attention_partial(q, k, v, 0, n))
+    (o_s, l_s), _ = _run(lib, 0, lambda: K.attention_partial(q, k, v, 0, n))
+    assert nc == 1
+    assert float((o_c - o_s).abs().max()) <= 5e-3 * float(o_s.abs().max())
+    for gi in range(groups):
+        ref = orc.partial(q[gi].double().cpu().numpy(), k[gi].double().cpu().numpy(), v[gi].double().cpu().numpy())
+        assert np.max(np.abs(o_c[gi].double().cpu().numpy() - ref.out)) <= 1e-2 * np.max(np.abs(ref.out))
