@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full sizes through size-independent properties
-(the float64 oracle cannot run these in seconds):
+(the direct float64-oracle comparisons at these sizes -- C4 64K index sets,
+C3 128K split-KV, a full C5 block -- are in tests/test_config_parity.py):
 
 * C3 (128K context, 8 kv heads x 128 stacked rows, d 128): the split-KV
   refresh -- K1 on each of P = 2 / 8 key shards, then the K3 merge of the
