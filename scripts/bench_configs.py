@@ -1,7 +1,7 @@
 """Secondary benchmark lines for BASELINE.json configs C1, C3, C4, C5 and the
 prefill path (F4) and the head-gated refresh (F3), SURVEY 8f.
 
-    python scripts/bench_configs.py [--only c3,c4,c5,f4,f3,c1] [--out profiles/rXX_configs.jsonl]
+    python scripts/bench_configs.py [--only c3,c4,c5,f4,f3,c1,cpu] [--out profiles/rXX_configs.jsonl]
 
 One JSON line per measurement.  All device timings are CUDA events around
 CUDA-graph replays of the measured launches (no host gaps), after warm-up,
@@ -363,9 +363,61 @@ def c1(out):
                            "round trip per (layer, head) call, as the reference API is synchronous numpy"})
 
 
+# ---------------------------------------------------------------- CPU reference at C3 / C4
+
+
+def cpu(out):
+    """The reference CPU path at the C3 (128K) and C4 (64K sparse, 10 / 50 %)
+    shapes: one layer x 8 kv-heads x one 32-step block at b=1
+    (G = 4 query heads stacked per kv head), on all host cores, with the GPU
+    time of the same layer-block for the ratio."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import bench as BN
+
+    threads = str(os.cpu_count())
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(var, threads)
+    sched = BN._sched_names()
+    # C3: dense FlashBlock layer-block over 131,072 committed keys
+    kind, t = BN.cpu_layer_block(131072, sched, reps=1)
+    emit(out, {"config": "C3-cpu", "ctx": 131072, "kind": kind, "cores": os.cpu_count(),
+               "cpu_model": BN.cpu_model(), "layer_block_s_b1": t,
+               "tokens_per_s_36_layers": BN.cpu_tokens_per_s(t),
+               "sample": "1 layer x 8 kv-heads x one 32-step block (1 refresh + 31 reuse), b=1, tile 512"})
+    # C4: sparse + residual reuse at 64K: build_sparse_mask + the exact first
+    # step, then 31 later steps against the cached residual (sparse.py:83-183)
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "flashblock")):
+        return
+    sys.path.insert(0, ref_dir)
+    import flashblock.sparse as S
+    import flashblock.attention as A
+
+    N, B, G, D = 65536, 32, 4, 128
+    rng = np.random.Generator(np.random.Philox(77))
+    heads = [tuple(rng.standard_normal(sh).astype(np.float32) for sh in ((G * B, D), (N + B, D), (N + B, D)))
+             for _ in range(8)]
+    for dens in (0.1, 0.5):
+        t0 = time.perf_counter()
+        for q, k, v in heads:
+            mask = S.build_sparse_mask(q, k, N, dens, 16)
+            _, resid = S.sparse_attention_with_residual(q, mask, k, v, None, tile_size=512)
+            entry = A.CacheEntry(resid, 0, 0)
+            for _ in range(31):
+                S.sparse_attention_with_residual(q, mask, k, v, entry, tile_size=512)
+        t = time.perf_counter() - t0
+        emit(out, {"config": "C4-cpu", "ctx": N, "density": dens, "kind": "reference", "cores": os.cpu_count(),
+                   "cpu_model": BN.cpu_model(), "layer_block_s_b1": t,
+                   "tokens_per_s_36_layers": B / (36 * t),
+                   "sample": "1 layer x 8 kv-heads: build_sparse_mask + the exact first step + 31 cached-residual "
+                             "steps, b=1, tile 512"})
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c2layer,c3,c4,c5,f4,f3,c1")
+    ap.add_argument("--only", default="c2layer,c3,c4,c5,f4,f3,c1,cpu")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.jsonl"))
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
