@@ -97,6 +97,8 @@ struct Sched {
   int vprod;               // refresh kernel: warp 3 issues the V tiles (warp 0 Q and K)
   int o_bf16;              // final partial O rows stored as bf16 (FB_PARTIAL_BF16)
   int clus;                // cluster split-K: CTAs per item (one cluster each), 0 = stream-K
+  int gbar;                // ... with the item's CTAs meeting at a counter in global memory
+                           // instead of a cluster barrier (any co-resident CTAs, no GPC placement)
   int rot;                 // two-query-tile kernel: rotate each segment's key tiles (Seg::shift)
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
@@ -178,6 +180,17 @@ __device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned 
   }
 }
 
+__device__ __forceinline__ void flag_wait_ge(const unsigned long long* f, unsigned long long v) {
+  uint32_t polls = 0;
+  while (true) {
+    unsigned long long x;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(f) : "memory");
+    if (x >= v) break;
+    if (++polls == (1u << 26)) __trap();  // a schedule bug must not hang the GPU
+    __nanosleep(64);
+  }
+}
+
 // Gathered key source (sparse K7/K8, sparse.py:167-183): an item's first
 // sel_tiles tiles are 8 mask-selected 16-key blocks each (read straight from
 // the cache by block index: one 16-row TMA box per block; missing entries
@@ -238,7 +251,7 @@ __device__ __forceinline__ void cluster_reduce(int rank, const Sched& sc, int it
                                                float* __restrict__ ws_o,
                                                float* __restrict__ ws_l, float* __restrict__ o_out,
                                                float* __restrict__ lse_out, const MergeFinal& fin,
-                                               unsigned long long* trace) {
+                                               unsigned long long* trace, unsigned long long* counters) {
   // diagnostics (trace != nullptr): globaltimer after publishing (slot 3) and after the barrier (slot 4)
   auto stamp = [&](int slot) {
     if (trace != nullptr && w8 == 0 && lane == 0) {
@@ -294,7 +307,21 @@ __device__ __forceinline__ void cluster_reduce(int rank, const Sched& sc, int it
     ptx::fence_proxy_async_global();
   }
   stamp(3);
-  ptx::cluster_sync();  // release / acquire (cluster scope; invalidates L1): every CTA of the cluster published
+  if (sc.gbar) {
+    // grid barrier of the item's CLS CTAs (all co-resident: one CTA per SM,
+    // ctas <= SMs): arrive (release) and wait for CLS arrivals (acquire); the
+    // last CTA to leave resets both counters, so every launch finds them zero
+    unsigned long long* arrive = counters + 2 * item;
+    if (w8 == 0 && lane == 0) {
+      __threadfence();
+      atomicAdd(arrive, 1ull);
+      flag_wait_ge(arrive, (unsigned long long)CLS);
+    }
+    asm volatile("bar.sync 6, 256;" ::: "memory");
+    __threadfence();
+  } else {
+    ptx::cluster_sync();  // release / acquire (cluster scope; invalidates L1): every CTA of the cluster published
+  }
   stamp(4);
   const float* part_o = ws_o + (long long)item * CLS * BM * D;
   const float* part_l = ws_l + (long long)item * CLS * BM;
@@ -302,11 +329,21 @@ __device__ __forceinline__ void cluster_reduce(int rank, const Sched& sc, int it
   float4 x[CLS][NV];
 #pragma unroll
   for (int i = 0; i < CLS; ++i) {
-    li[i] = ok ? part_l[(long long)i * BM + row] : -INFINITY;
+    li[i] = ok ? __ldcg(part_l + (long long)i * BM + row) : -INFINITY;
 #pragma unroll
     for (int v = 0; v < NV; ++v)
-      x[i][v] = (ok && cok) ? *reinterpret_cast<const float4*>(part_o + ((long long)i * BM + row) * D + colv(v))
+      x[i][v] = (ok && cok) ? __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)i * BM + row) * D + colv(v)))
                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (sc.gbar) {  // every read of the item's slots is issued and complete (values in registers)
+    asm volatile("bar.sync 6, 256;" ::: "memory");
+    if (w8 == 0 && lane == 0) {
+      unsigned long long* arrive = counters + 2 * item;
+      if (atomicAdd(arrive + 1, 1ull) == (unsigned long long)CLS - 1) {  // the last CTA to leave
+        atomicExch(arrive, 0ull);
+        atomicExch(arrive + 1, 0ull);
+      }
+    }
   }
   if (!ok) return;
   float mx = -INFINITY;
@@ -646,7 +683,9 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
     }
   }
-  if constexpr (CL) ptx::cluster_sync();  // the cluster reduction's barrier (softmax warps do the work)
+  if constexpr (CL) {  // the cluster reduction's barrier (softmax warps do the work)
+    if (!sc.gbar) ptx::cluster_sync();
+  }
   } else {
     ptx::setmaxnreg_inc<216>();
     // ------------------------------------------------------------ softmax
@@ -859,7 +898,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       float c1 = wg == 0 ? c_oth : c_own;
       // in-kernel split merge: the item's first CTA (this segment is its last)
       // merges the partials of CTAs cb+1..ce, written in their first segments
-      const bool owner = flags != nullptr && !whole && ib >= t_begin;
+      const bool owner = !CL && flags != nullptr && !whole && ib >= t_begin;
       const int cb = blockIdx.x + 1, ce = owner ? sc.cta_of(sc.item_end(item) - 1) : 0;
       float* dst;
       float* stg = reinterpret_cast<float*>(smem + C::OFF_STG);  // cluster split-K staging
@@ -941,7 +980,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (row == 0 && wg == 0 && seg == 0) stamp(6);
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bar->o_empty);  // MMA may overwrite O for the next segment
-      if (flags != nullptr && !whole && !owner) {
+      if (!CL && flags != nullptr && !whole && !owner) {
         // this CTA's share of an item begun by an earlier CTA: publish it
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, 1ull);
@@ -953,13 +992,14 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // Cluster split-K reduction (see cluster_reduce); the CTA's rows are
       // staged in shared memory by the epilogue above
       const int item = blockIdx.x / sc.clus;
-      const int rk = (int)ptx::cluster_ctarank();
+      const int rk = sc.gbar ? (int)(blockIdx.x % sc.clus) : (int)ptx::cluster_ctarank();
+      unsigned long long* counters = flags + 512;  // grid-barrier counters (two per item)
       const unsigned char* stgb = smem + C::OFF_STG;
       switch (sc.clus) {
-        case 2: cluster_reduce<2, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace); break;
-        case 4: cluster_reduce<4, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace); break;
-        case 8: cluster_reduce<8, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace); break;
-        default: cluster_reduce<16, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace); break;
+        case 2: cluster_reduce<2, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace, counters); break;
+        case 4: cluster_reduce<4, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace, counters); break;
+        case 8: cluster_reduce<8, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace, counters); break;
+        default: cluster_reduce<16, D>(rk, sc, item, warp - 4, lane, q_rows, stgb, &tm_ws, ws_o, ws_l, o_out, lse_out, fin, trace, counters); break;
       }
       if (row == 0 && wg == 0) stamp(1);  // reduction done
     }
@@ -1925,6 +1965,15 @@ static int k1_cluster_mode() {
   }
   return m;
 }
+// FB_K1_GBAR=0: no grid-barrier split-K (diagnostics)
+static bool k1_gbar_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_K1_GBAR");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
 static long long g_cluster_launches = 0;
 long long k1_cluster_launches() { return g_cluster_launches; }
 
@@ -2208,6 +2257,27 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
         break;
       }
     }
+    // grid-barrier split-K: the same per-item reduction for larger CTA groups
+    // (C2 b=1 / 2, C3 b=1 shards: 8-16 CTAs per item), the item's CTAs meeting
+    // at a counter in the caller's sync-flag buffer instead of a cluster
+    // barrier -- co-resident by construction (one CTA per SM, ctas <= SMs) --
+    // so no merge-kernel launch and no GPC-placement wait
+    if (cm == 2 && need_merge && sc.clus == 0 && g_k1_diag == 0 && k1_gbar_enabled() && sync_flags != nullptr &&
+        n_flags >= 512 + 2 * (int64_t)p.items) {
+      for (int k = 16; k >= 2; k >>= 1) {
+        if ((long long)p.items * k > num_sms() || p.tpi < 2 * k) continue;
+        if (ws == nullptr || ws_bytes < (size_t)p.items * k * sm100::BM * (D + 1) * sizeof(float)) break;
+        sc.clus = k;
+        sc.gbar = 1;
+        p.ctas = sc.ctas = p.items * k;
+        ws_o = reinterpret_cast<float*>(ws);
+        ws_l = ws_o + (size_t)p.ctas * sm100::BM * D;
+        need_merge = false;
+        flags = sync_flags;  // counters at flags + 512
+        if (fin != nullptr) kfin = *fin;
+        break;
+      }
+    }
   }
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   sm100::Paged pgv = paged ? *paged : sm100::Paged{nullptr, 0, 1};
@@ -2240,7 +2310,7 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     ++g_cluster_launches;
     if ((rc = make_tmap_3d(&mws, ws_o, 4, D, sm100::BM, sm100::BM, p.ctas, 32, sm100::BM))) return rc;
   }
-  launch_pdl_cluster(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, sc.clus, mq, mk, mv, mki,
+  launch_pdl_cluster(kern, dim3((unsigned)p.ctas), dim3(sm100::THREADS), C::SMEM, st, sc.gbar ? 0 : sc.clus, mq, mk, mv, mki,
                      mvi, ga, pgv, cz, sc, (int)q_rows, (int)key_begin, (int)key_end, key_len, scale_log2, o_out,
                      lse_out, ws_o, ws_l, g_trace ? g_trace + (size_t)(g_trace_launch++) * 148 * 8 : nullptr,
                      flags, kfin, mws);

@@ -177,3 +177,29 @@ def test_cluster_k1_head_dim_64(lib, groups, q_rows, n):
     for gi in range(groups):
         ref = orc.partial(q[gi].double().cpu().numpy(), k[gi].double().cpu().numpy(), v[gi].double().cpu().numpy())
         assert np.max(np.abs(o_c[gi].double().cpu().numpy() - ref.out)) <= 1e-2 * np.max(np.abs(ref.out))
+
+
+@pytest.mark.parametrize("groups,n", [(8, 16384), (16, 8192), (8, 32768), (3, 6000)])
+def test_grid_barrier_split_k(lib, groups, n):
+    """Auto mode on few items with 8-16 CTAs each (C3 b=1 shards, C2 b=1/2):
+    the item's CTAs meet at a counter in the sync-flag buffer instead of a
+    cluster barrier; the counters are left zero for the next launch."""
+    from oracle import flashblock_oracle as orc
+    from paper_2602_05305_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(groups * 31 + n)
+    q, k, v = _r(g, groups, 128, 128), _r(g, groups, n, 128), _r(g, groups, n, 128)
+    outs = []
+    for rep in range(2):  # twice: the counters must come back zero
+        (o_a, l_a), na = _run(lib, -1, lambda: K.attention_partial(q, k, v, 0, n))
+        assert na == 1, "the grid-barrier plan was not taken"
+        outs.append((o_a, l_a))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    (o_s, l_s), ns = _run(lib, 0, lambda: K.attention_partial(q, k, v, 0, n))
+    assert ns == 0
+    o_a, l_a = outs[0]
+    assert float((o_a - o_s).abs().max()) <= 5e-3 * float(o_s.abs().max())
+    assert float((l_a - l_s).abs().max()) <= 1e-4
+    for gi in (0, groups - 1):
+        ref = orc.partial(q[gi].double().cpu().numpy(), k[gi].double().cpu().numpy(), v[gi].double().cpu().numpy())
+        assert np.max(np.abs(o_a[gi].double().cpu().numpy() - ref.out)) <= 1e-2 * np.max(np.abs(ref.out))
