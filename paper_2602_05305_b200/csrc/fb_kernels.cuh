@@ -87,6 +87,7 @@ long long quad_launches();
 void set_k1_cluster_mode(int m);  // cluster split-K K1: -1 default (auto), 0 off, 1 whenever feasible
 long long k1_cluster_launches();
 void set_gather_atoms(int m);     // K7 / K8 atom layout: -1 default (on), 0 off, 1 on
+void set_k1_gbar_mode(int m);     // grid-barrier split-K: -1 default, 0 off, 1 vs merge kernel, 2 also vs owner merge
 void set_k2_trace(void* p, int launches);  // diagnostics: K2 v1 per-CTA stamps
 void set_k2_v2(int v);           // K2 variant: -1 by size (default), 0 v1, 1 v2 (diagnostics)
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);

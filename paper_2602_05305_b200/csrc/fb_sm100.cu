@@ -1965,14 +1965,18 @@ static int k1_cluster_mode() {
   }
   return m;
 }
-// FB_K1_GBAR=0: no grid-barrier split-K (diagnostics)
-static bool k1_gbar_enabled() {
+// grid-barrier split-K: 0 off, 1 instead of the split-merge kernel (default),
+// 2 also instead of the in-kernel owner merge (FB_K1_GBAR / fb_debug_set_k1_gbar)
+static int g_gbar_override = -1;
+void set_k1_gbar_mode(int m) { g_gbar_override = m; }
+static int k1_gbar_mode() {
+  if (g_gbar_override >= 0) return g_gbar_override;
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("FB_K1_GBAR");
-    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+    v = e == nullptr ? 1 : atoi(e);
   }
-  return v != 0;
+  return v;
 }
 static long long g_cluster_launches = 0;
 long long k1_cluster_launches() { return g_cluster_launches; }
@@ -2262,10 +2266,14 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     // at a counter in the caller's sync-flag buffer instead of a cluster
     // barrier -- co-resident by construction (one CTA per SM, ctas <= SMs) --
     // so no merge-kernel launch and no GPC-placement wait
-    if (cm == 2 && need_merge && sc.clus == 0 && g_k1_diag == 0 && k1_gbar_enabled() && sync_flags != nullptr &&
-        n_flags >= 512 + 2 * (int64_t)p.items) {
+    const int gm = k1_gbar_mode();
+    const bool owner_path = flags != nullptr && !need_merge && !(p.T % p.ctas == 0 && (p.T / p.ctas) % p.tpi == 0);
+    if (cm == 2 && (need_merge || (gm == 2 && owner_path)) && sc.clus == 0 && g_k1_diag == 0 && gm >= 1 &&
+        sync_flags != nullptr && n_flags >= 512 + 2 * (int64_t)p.items) {
+      const long long per_streamk = (p.T + p.ctas - 1) / p.ctas;
       for (int k = 16; k >= 2; k >>= 1) {
         if ((long long)p.items * k > num_sms() || p.tpi < 2 * k) continue;
+        if (!need_merge && (p.tpi + k - 1) / k > per_streamk + per_streamk / 5) break;  // owner path: <= +20 % tiles
         if (ws == nullptr || ws_bytes < (size_t)p.items * k * sm100::BM * (D + 1) * sizeof(float)) break;
         sc.clus = k;
         sc.gbar = 1;
