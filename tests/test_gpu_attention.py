@@ -253,7 +253,11 @@ def test_bf16_refresh_c2_shape_split_invariance():
     pa = K.attention_partial(q, k, v, 0, a)
     pb = K.attention_partial(q, k, v, a, n)
     oc, lc = K.combine([pa, pb])
-    assert (oc - o).abs().max().item() / o.abs().max().item() <= 2e-3
+    # P enters the PV MMA in bf16 (2^-9 relative per probability), rounded
+    # against each range's own running max: each side is ~1.5e-3 from the F32
+    # kernel here, so two bf16 evaluations may differ by up to twice that
+    assert (oc - o32).abs().max().item() / o32.abs().max().item() <= 1e-2
+    assert (oc - o).abs().max().item() / o.abs().max().item() <= 4e-3
     assert (lc - l).abs().max().item() <= 1e-4
 
 
