@@ -531,6 +531,8 @@ FB_API void fb_debug_set_gather_atoms(int m) { set_gather_atoms(m); }
 FB_API void fb_debug_set_k1_gbar(int m) { set_k1_gbar_mode(m); }
 FB_API int64_t fb_debug_k1_cluster_launches(void) { return (int64_t)k1_cluster_launches(); }
 FB_API void fb_debug_set_k2_variant(int v) { set_k2_v2(v); }
+FB_API void fb_debug_set_k5_mode(int m) { set_k5_mode(m); }
+FB_API int64_t fb_debug_k5_fused_launches(void) { return (int64_t)k5_fused_launches(); }
 FB_API void fb_debug_set_k2_trace(void* p, int launches) { set_k2_trace(p, launches); }
 int64_t fb_launch_count(void) { return g_launches.load(); }
 
@@ -687,7 +689,7 @@ int fb_block_mass_paged(int dtype, const void* q, const void* k_pages, const voi
     return rc;
   if (!score_sm100_supported(head_dim, q_rows, key_block_size))
     return fail(FB_ERR_UNSUPPORTED, "paged block mass: q_rows <= 128");
-  if (workspace_bytes < score_sm100_workspace_bytes(groups, q_rows, n_ext, n_in))
+  if (workspace_bytes < score_sm100_min_workspace_bytes(groups, q_rows, n_ext, n_in))
     return fail(FB_ERR_VALUE, "workspace too small (fb_block_mass_workspace_bytes_ex)");
   const PagingCtx pc{page_table, max_pages, page_rows, num_pages};
   ScopedPaging guard(&pc);
@@ -1104,7 +1106,7 @@ int fb_block_mass(int dtype, const void* q, const void* k, const void* k_in, int
   cudaStream_t st = as_stream(stream);
   if (dtype == FB_BF16 && score_sm100_supported(head_dim, q_rows, key_block_size) &&
       n_ext < (int64_t(1) << 31) &&
-      workspace_bytes >= score_sm100_workspace_bytes(groups, q_rows, n_ext, n_in))
+      workspace_bytes >= score_sm100_min_workspace_bytes(groups, q_rows, n_ext, n_in))
     return launch_score_sm100(reinterpret_cast<const __nv_bfloat16*>(q),
                               reinterpret_cast<const __nv_bfloat16*>(k),
                               reinterpret_cast<const __nv_bfloat16*>(k_in), groups, q_rows,

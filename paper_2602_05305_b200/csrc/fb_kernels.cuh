@@ -89,6 +89,8 @@ long long k1_cluster_launches();
 void set_gather_atoms(int m);     // K7 / K8 atom layout: -1 default (on), 0 off, 1 on
 void set_k1_gbar_mode(int m);     // grid-barrier split-K: -1 default, 0 off, 1 vs merge kernel, 2 also vs owner merge
 void set_k2_trace(void* p, int launches);  // diagnostics: K2 v1 per-CTA stamps
+void set_k5_mode(int m);         // K5 scoring: -1 environment (default fused), 0 fused, 1 two-pass
+long long k5_fused_launches();
 void set_k2_v2(int v);           // K2 variant: -1 by size (default), 0 v1, 1 v2 (diagnostics)
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);
 int launch_refresh_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
@@ -171,6 +173,7 @@ int launch_gather_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __
 // K5 on the tensor cores (bf16, q_rows <= 128, kbs == 16): float64 block masses.
 bool score_sm100_supported(int64_t head_dim, int64_t q_rows, int64_t kbs);
 size_t score_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in);
+size_t score_sm100_min_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in);
 int launch_score_sm100(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* k_in,
                        int64_t groups, int64_t q_rows, int64_t head_dim, int64_t cap, int64_t n_ext,
                        int64_t n_in, double scale, double* mass, void* ws, size_t ws_bytes,

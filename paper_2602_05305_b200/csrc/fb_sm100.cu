@@ -1212,6 +1212,15 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
 //               double in a fixed order (bit-equal masses for equal inputs).
 // K tiles only (no V, no PV): Q + a 6-deep K ring in smem, S double-buffered
 // in TMEM, the softmax warps release each S buffer after reading it.
+//   FUSED pass (score_fused_kernel, the default): ONE read of K.  Four
+//               score warpgroups take 32 columns (two 16-key blocks) of every
+//               S tile each; a thread takes its row's quarter-tile max mt,
+//               sums p = exp2(s*c - mt) per block (A) -- part of the exp2 pairs
+//               on the FMA pipes -- and over the quarter (the row's running
+//               LSE, rescaled by two exp2 per tile), and stores A and mt for
+//               the external tiles; score_mass_kernel weights A by
+//               exp2(mt - lse2_row) once the row LSE is final and sums the
+//               rows.  K bytes once plus 6 KB of A / mt per 32 KB K tile.
 template <int D>
 struct ScoreCfg {
   static constexpr int STAGES = 6;
@@ -1234,7 +1243,7 @@ struct ScoreBars {
 
 constexpr int SCORE_THREADS = 384;  // 4 control warps + 2 score warpgroups
 
-template <int D, bool MASS>
+template <int D, int MODE>
 __global__ void __launch_bounds__(SCORE_THREADS, 1)
 score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
              const __grid_constant__ CUtensorMap tm_ki, Paged pg, Sched sc, int q_rows, int n_ext, int n_in,
@@ -1242,6 +1251,7 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
              float* __restrict__ lse2_out, float* __restrict__ ws_l, double* __restrict__ mass,
              int nb) {
   using C = ScoreCfg<D>;
+  constexpr bool MASS = MODE == 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1456,6 +1466,259 @@ score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
   }
 }
 
+// ---------------------------------------------------------------- fused K5
+template <int D>
+struct ScoreFusedCfg {
+  static constexpr int STAGES = 5;
+  static constexpr int NBOX = D / BOX_COLS;
+  static constexpr uint32_t BOX_BYTES = BM * BOX_COLS * 2;
+  static constexpr uint32_t TILE_BYTES = NBOX * BOX_BYTES;
+  static constexpr uint32_t OFF_Q = 0;
+  static constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
+  static constexpr uint32_t OFF_BAR = OFF_K + STAGES * TILE_BYTES;
+  static constexpr uint32_t OFF_X = OFF_BAR + 512;  // [3 quarters][2: m, l][128] floats
+  static constexpr uint32_t SMEM = OFF_X + 3 * 2 * BM * 4 + 1024;
+};
+static_assert(ScoreFusedCfg<128>::SMEM <= 232448, "fused K5 shared memory exceeds 227 KB");
+
+struct ScoreFusedBars {
+  uint64_t q_full, q_empty;
+  uint64_t k_full[5], k_empty[5];
+  uint64_t s_full[2], s_free[2];
+  uint32_t tmem_base;
+};
+
+constexpr int SCORE_FUSED_THREADS = 640;  // 4 control warps + 4 score warpgroups
+constexpr int K5_POLY_DEFAULT = 0;        // exp2 pairs of 8 per 16-key block on the FMA pipes
+                                          // (2 / 4: no gain measured -- MUFU is not the binding unit here)
+
+template <int D, int POLY>
+__global__ void __launch_bounds__(SCORE_FUSED_THREADS, 1)
+score_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_ki, Paged pg, Sched sc, int q_rows, int n_ext,
+                   int n_in, int ext_tiles, float scale_log2, float* __restrict__ lse2_out,
+                   float* __restrict__ ws_l, float* __restrict__ ws_a, float* __restrict__ ws_m) {
+  using C = ScoreFusedCfg<D>;
+  constexpr int QC = BN / 4;  // columns per warpgroup
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  ScoreFusedBars* bar = reinterpret_cast<ScoreFusedBars*>(smem + C::OFF_BAR);
+  float* xch = reinterpret_cast<float*>(smem + C::OFF_X);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t_begin = sc.start(blockIdx.x), t_end = sc.start(blockIdx.x + 1);  // uniform items
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::mbar_init(&bar->q_full, 1);
+    ptx::mbar_init(&bar->q_empty, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&bar->k_full[s], 1);
+      ptx::mbar_init(&bar->k_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&bar->s_full[b], 1);
+      ptx::mbar_init(&bar->s_free[b], 512);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(&bar->tmem_base, 256);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bar->tmem_base;
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t keep = ptx::policy_evict_last(), stream = ptx::policy_evict_first();
+      int j = 0, seg = 0;
+      for (long long t = t_begin; t < t_end; ++seg) {
+        const int item = (int)(t / sc.tpi);
+        const long long seg_end = min(t_end, (long long)(item + 1) * sc.tpi);
+        const int g = sc.group_of(item), mt = sc.mtile_of(item);
+        if (seg > 0) ptx::mbar_wait(&bar->q_empty, (seg - 1) & 1);
+        ptx::mbar_expect_tx(&bar->q_full, C::TILE_BYTES);
+        for (int b = 0; b < C::NBOX; ++b)
+          ptx::tma_load_3d(smem + C::OFF_Q + b * C::BOX_BYTES, &tm_q, &bar->q_full, b * BOX_COLS,
+                           mt * BM, g, keep);
+        for (; t < seg_end; ++t, ++j) {
+          const int s = j % C::STAGES;
+          const int lt = (int)(t - (long long)item * sc.tpi);
+          const bool ext = lt < ext_tiles;
+          int row = ext ? lt * BN : (lt - ext_tiles) * BN;
+          int slab = g;
+          if (ext && pg.table != nullptr) {  // paged cache: the tile's page, row inside it
+            slab = __ldg(pg.table + (long long)g * pg.max_pages + row / pg.page_rows);
+            row %= pg.page_rows;
+          }
+          ptx::mbar_wait(&bar->k_empty[s], ((j / C::STAGES) & 1) ^ 1);
+          ptx::mbar_expect_tx(&bar->k_full[s], C::TILE_BYTES);
+          for (int b = 0; b < C::NBOX; ++b)
+            ptx::tma_load_3d(smem + C::OFF_K + s * C::TILE_BYTES + b * C::BOX_BYTES,
+                             ext ? &tm_k : &tm_ki, &bar->k_full[s], b * BOX_COLS, row, slab, stream);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, BN, false);
+      const uint32_t q_base = ptx::smem_u32(smem + C::OFF_Q);
+      int j = 0, seg = 0;
+      for (long long t0 = t_begin; t0 < t_end; ++seg) {
+        const int item = (int)(t0 / sc.tpi);
+        const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+        ptx::mbar_wait(&bar->q_full, seg & 1);
+        ptx::tc_fence_after();
+        for (int t = 0; t < n; ++t, ++j) {
+          const int s = j % C::STAGES;
+          ptx::mbar_wait(&bar->k_full[s], (j / C::STAGES) & 1);
+          if (j >= 2) ptx::mbar_wait(&bar->s_free[j & 1], ((j >> 1) - 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K + s * C::TILE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * C::BOX_BYTES + (kk % 4) * 32;
+            ptx::mma_ss(tmem + (j & 1) * 128, ptx::sdesc_sw128(q_base + off, 16, 1024),
+                        ptx::sdesc_sw128(k_base + off, 16, 1024), IDESC_S, kk > 0);
+          }
+          ptx::tc_commit(&bar->k_empty[s]);
+          ptx::tc_commit(&bar->s_full[j & 1]);
+          if (t == n - 1) ptx::tc_commit(&bar->q_empty);
+        }
+        t0 += n;
+      }
+    }
+  } else if (warp >= 4) {
+    // warpgroup w (warps 4+4w .. 7+4w): columns [32w, 32w+32) of every S tile
+    const int wq = warp & 3;
+    const int w = (warp - 4) >> 2;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const int row = wq * 32 + lane;
+    float s[QC];
+    int j = 0, seg = 0;
+    const uint64_t c2 = ptx::f2_pack(scale_log2, scale_log2);
+    for (long long t0 = t_begin; t0 < t_end; ++seg) {
+      const int item = (int)(t0 / sc.tpi);
+      const int lt0 = (int)(t0 - (long long)item * sc.tpi);
+      const int n = (int)(min(t_end, (long long)(item + 1) * sc.tpi) - t0);
+      const int g = sc.group_of(item), mt = sc.mtile_of(item);
+      const int grow = mt * BM + row;
+      const long long orow = (long long)g * q_rows + grow;
+      float m = -INFINITY, l = 0.f;
+      for (int t = 0; t < n; ++t, ++j) {
+        const int lt = lt0 + t;
+        ptx::mbar_wait(&bar->s_full[j & 1], (j >> 1) & 1);
+        ptx::tc_fence_after();
+        ptx::tmem_ld32(tmem + lane_off + (j & 1) * 128 + w * QC, reinterpret_cast<uint32_t*>(s));
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&bar->s_free[j & 1]);
+        const bool ext = lt < ext_tiles;
+        const int valid = (ext ? n_ext - lt * BN : n_in - (lt - ext_tiles) * BN) - w * QC;
+        float a[QC / 16];
+        float tmax;
+        if constexpr (POLY == -1) {  // diagnostics: the TMA + MMA pipeline alone (no score math)
+          continue;
+        }
+        constexpr int NP = POLY < 0 ? 0 : POLY;  // -2: diagnostics, the math without the A / mt stores
+        if (valid >= QC) {
+          // full quarter tile (warp-uniform): no masking; per 16-key block,
+          // pairs [0, 8 - POLY) on MUFU.EX2 and the rest on the FMA pipes
+          float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+          for (int i = 4; i < QC; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+          tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+          const uint64_t n2 = ptx::f2_pack(-tmax, -tmax);
+#pragma unroll
+          for (int bi = 0; bi < QC / 16; ++bi) {
+            uint64_t acc0 = ptx::f2_pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+            for (int pi = 0; pi < 8; ++pi) {
+              const uint64_t x = ptx::f2_fma(ptx::f2_pack(s[bi * 16 + 2 * pi], s[bi * 16 + 2 * pi + 1]), c2, n2);
+              uint64_t e;
+              if (pi >= 8 - NP) {
+                e = ptx::ex2_poly5x2(x);
+              } else {
+                float x0, x1;
+                ptx::f2_unpack(x, x0, x1);
+                e = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+              }
+              if (pi & 1) acc1 = ptx::f2_add(acc1, e); else acc0 = ptx::f2_add(acc0, e);
+            }
+            float u0, u1, u2, u3;
+            ptx::f2_unpack(acc0, u0, u1);
+            ptx::f2_unpack(acc1, u2, u3);
+            a[bi] = (u0 + u1) + (u2 + u3);
+          }
+        } else {
+          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int i = 0; i < QC; ++i) {
+            if (i >= valid) s[i] = -INFINITY;
+            mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+          }
+          tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+#pragma unroll
+          for (int bi = 0; bi < QC / 16; ++bi) {
+            float p4[4] = {0.f, 0.f, 0.f, 0.f};
+            if (tmax != -INFINITY) {  // a quarter tile may be fully masked
+#pragma unroll
+              for (int i = 0; i < 16; ++i) p4[i & 3] += ptx::ex2(fmaf(s[bi * 16 + i], scale_log2, -tmax));
+            }
+            a[bi] = (p4[0] + p4[1]) + (p4[2] + p4[3]);
+          }
+        }
+        if (tmax != -INFINITY) {
+          const float m_new = fmaxf(m, tmax);
+          l = l * ptx::ex2(m - m_new) + (a[0] + a[1]) * ptx::ex2(tmax - m_new);
+          m = m_new;
+        }
+        if (ext && POLY != -2) {  // A [group][ext tile][8 blocks][128 rows], mt [group][ext tile][4 quarters][128 rows]
+          const long long tb = (long long)g * ext_tiles + lt;
+#pragma unroll
+          for (int bi = 0; bi < QC / 16; ++bi) ws_a[(tb * 8 + w * (QC / 16) + bi) * BM + row] = a[bi];
+          ws_m[(tb * 4 + w) * BM + row] = tmax;
+        }
+      }
+      t0 += n;
+      // combine the four column quarters of each row, then the split partials
+      if (w > 0) {
+        xch[((w - 1) * 2 + 0) * BM + row] = m;
+        xch[((w - 1) * 2 + 1) * BM + row] = l;
+      }
+      asm volatile("bar.sync 1, 512;" ::: "memory");
+      if (w == 0) {
+        float mm = m;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) mm = fmaxf(mm, xch[(k * 2) * BM + row]);
+        float lt = mm == -INFINITY ? 0.f : l * ptx::ex2(m - mm);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const float mk = xch[(k * 2) * BM + row];
+          if (mk != -INFINITY) lt += xch[(k * 2 + 1) * BM + row] * ptx::ex2(mk - mm);
+        }
+        const bool whole = sc.item_begin(item) >= t_begin && sc.item_end(item) <= t_end;
+        const float lse = mm + log2f(lt);
+        if (whole) {
+          if (grow < q_rows) lse2_out[orow] = lse;
+        } else {
+          ws_l[sc.slot(blockIdx.x, item) * BM + row] = lse;
+        }
+      }
+      asm volatile("bar.sync 1, 512;" ::: "memory");
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 256);
+  }
+}
+
 __global__ void score_lse_merge_kernel(Sched sc, int q_rows, const float* __restrict__ ws_l,
                                        float* __restrict__ lse2_out) {
   ptx::pdl_wait();
@@ -1474,6 +1737,105 @@ __global__ void score_lse_merge_kernel(Sched sc, int q_rows, const float* __rest
   float z = 0.f;
   for (int c = c_first; c <= c_last; ++c) z += exp2f(ws_l[sc.slot(c, item) * BM + row] - mx);
   lse2_out[(long long)g * q_rows + grow] = mx + log2f(z);
+}
+
+// Fused K5, second half: mass[g][blk] = sum over the group's rows of
+// A[g][tile][blk % 8][row] * exp2(mt[g][tile][quarter][row] - lse2[row]).  One
+// CTA per (group, tiles_per_cta external tiles); the group's final row LSEs
+// (the stream-K split partials merged here, as score_lse_merge_kernel does)
+// sit in shared memory; a warp takes every 8th tile (its first tile's loads
+// issued before the LSE merge), 4 CTAs per SM, lane = 4 rows, then a fixed-order double transpose-reduce over the
+// lanes (equal inputs -> bit-equal masses).
+__device__ __forceinline__ void mass_tile_reduce(const float4 (&mq)[4], const float4 (&a)[8], float4 ls,
+                                                 int lane, int lt, int nb, double* __restrict__ mrow) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double v[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float w0 = ptx::ex2(mq[q].x - ls.x), w1 = ptx::ex2(mq[q].y - ls.y);
+    const float w2 = ptx::ex2(mq[q].z - ls.z), w3 = ptx::ex2(mq[q].w - ls.w);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 x = a[2 * q + h];
+      v[2 * q + h] = (double)(((x.x * w0) + (x.y * w1)) + ((x.z * w2) + (x.w * w3)));
+    }
+  }
+  // transpose-reduce: 8 -> 4 -> 2 -> 1 values per lane, then the last two levels
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double r = __shfl_xor_sync(0xffffffffu, b4 ? v[k] : v[k + 4], 16);
+    v[k] = (b4 ? v[k + 4] : v[k]) + r;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double r = __shfl_xor_sync(0xffffffffu, b3 ? v[k] : v[k + 2], 8);
+    v[k] = (b3 ? v[k + 2] : v[k]) + r;
+  }
+  {
+    const double r = __shfl_xor_sync(0xffffffffu, b2 ? v[0] : v[1], 4);
+    v[0] = (b2 ? v[1] : v[0]) + r;
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  if ((lane & 3) == 0) {
+    const int blk = lt * 8 + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+    if (blk < nb) mrow[blk] = v[0];
+  }
+}
+
+__global__ void __launch_bounds__(256, 4)
+score_mass_kernel(Sched sc, int q_rows, int ext_tiles, int nb, int tiles_per_cta,
+                  const float* __restrict__ lse2_whole, const float* __restrict__ ws_l,
+                  const float* __restrict__ ws_a, const float* __restrict__ ws_m, double* __restrict__ mass) {
+  __shared__ __align__(16) float lse2[BM];
+  const int g = blockIdx.y;  // q_rows <= BM: item == group
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lt_end = min(ext_tiles, (int)(blockIdx.x + 1) * tiles_per_cta);
+  double* mrow = mass + (long long)g * nb;
+  float4 mq[1][4], a[1][8];  // one tile in flight per warp: 4 CTAs (32 warps) per SM
+  auto load = [&](int u, int lt) {
+    const long long tb = (long long)g * ext_tiles + lt;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mq[u][q] = __ldcg(reinterpret_cast<const float4*>(ws_m + (tb * 4 + q) * BM) + lane);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) a[u][b] = __ldcg(reinterpret_cast<const float4*>(ws_a + (tb * 8 + b) * BM) + lane);
+  };
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
+  int lt = blockIdx.x * tiles_per_cta + warp;
+  if (lt < lt_end) load(0, lt);  // in flight while the row LSEs are merged
+  if (threadIdx.x < BM) {
+    const int row = threadIdx.x;
+    float v = INFINITY;  // rows past q_rows weigh 0
+    if (row < q_rows) {
+      const int c_first = sc.cta_of(sc.item_begin(g));
+      const int c_last = sc.cta_of(sc.item_end(g) - 1);
+      if (c_first == c_last) {
+        v = lse2_whole[(long long)g * q_rows + row];
+      } else {
+        float x[8];
+        const int nc = min(c_last - c_first + 1, 8);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = c < nc ? __ldcg(ws_l + sc.slot(c_first + c, g) * BM + row) : -INFINITY;
+        float mx = -INFINITY;
+        for (int c = c_first + 8; c <= c_last; ++c) mx = fmaxf(mx, __ldcg(ws_l + sc.slot(c, g) * BM + row));
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mx = fmaxf(mx, x[c]);
+        float z = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) z += c < nc ? exp2f(x[c] - mx) : 0.f;
+        for (int c = c_first + 8; c <= c_last; ++c) z += exp2f(__ldcg(ws_l + sc.slot(c, g) * BM + row) - mx);
+        v = mx + log2f(z);
+      }
+    }
+    lse2[row] = v;
+  }
+  __syncthreads();
+  const float4 ls = *reinterpret_cast<const float4*>(lse2 + 4 * lane);
+  for (; lt < lt_end; lt += 8) {
+    mass_tile_reduce(mq[0], a[0], ls, lane, lt, nb, mrow);
+    if (lt + 8 < lt_end) load(0, lt + 8);
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -2478,10 +2840,37 @@ bool score_sm100_supported(int64_t head_dim, int64_t q_rows, int64_t kbs) {
   return (head_dim == 64 || head_dim == 128) && q_rows <= 128 && kbs == 16;
 }
 
-size_t score_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
+// FB_K5_TWO_PASS=1 / fb_debug_set_k5_mode(1): the LSE + MASS two-pass scoring
+// (diagnostics / A-B); fb_debug_set_k5_mode(-1) returns to the environment
+static int g_k5_mode = -1;
+static long long g_k5_fused_launches = 0;
+void set_k5_mode(int m) { g_k5_mode = m; }
+long long k5_fused_launches() { return g_k5_fused_launches; }
+static bool k5_two_pass() {
+  if (g_k5_mode >= 0) return g_k5_mode == 1;
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_K5_TWO_PASS");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v != 0;
+}
+
+// two-pass workspace: row LSEs + split partials; the fused pass adds the
+// per-(row, 16-key block) sums A and the per-(row, half tile) maxima
+static size_t score_two_pass_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
   const int64_t tiles = (n_ext + 127) / 128 + (n_in + 127) / 128;
   const RefreshPlan p = plan_refresh(groups, q_rows, 0, tiles * 128);
-  return align_up((size_t)groups * q_rows * sizeof(float), 256) + p.ws_bytes;
+  return align_up((size_t)groups * q_rows * sizeof(float), 256) + align_up(p.ws_bytes, 256);
+}
+static size_t score_fused_extra_bytes(int64_t groups, int64_t n_ext) {
+  return (size_t)groups * ((n_ext + 127) / 128) * 12 * sm100::BM * sizeof(float);  // A: 8, mt: 4 per row
+}
+size_t score_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
+  return score_two_pass_bytes(groups, q_rows, n_ext, n_in) + score_fused_extra_bytes(groups, n_ext);
+}
+size_t score_sm100_min_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
+  return score_two_pass_bytes(groups, q_rows, n_ext, n_in);
 }
 
 template <int D>
@@ -2509,8 +2898,8 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sm100::score_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    cudaFuncSetAttribute(sm100::score_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(sm100::score_kernel<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(sm100::score_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
   const int ext_tiles = (int)((n_ext + 127) / 128);
@@ -2520,11 +2909,48 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   float* lse2 = reinterpret_cast<float*>(ws);
   const size_t lse_bytes = align_up((size_t)groups * q_rows * sizeof(float), 256);
   float* ws_l = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + lse_bytes);
-  // LSE pass over ext + internal keys
+  // LSE (or fused) pass over ext + internal keys
   RefreshPlan p = plan_refresh(groups, q_rows, 0, (int64_t)(ext_tiles + in_tiles) * 128);
-  if (ws_bytes < lse_bytes + p.ws_bytes) return fail(FB_ERR_VALUE, "score workspace too small");
+  const size_t two = score_two_pass_bytes(groups, q_rows, n_ext, n_in);
+  if (ws_bytes < two) return fail(FB_ERR_VALUE, "score workspace too small");
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};
-  launch_pdl(sm100::score_kernel<D, false>, dim3((unsigned)p.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
+  if (!k5_two_pass() && ws_bytes >= two + score_fused_extra_bytes(groups, n_ext)) {
+    float* ws_a = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + two);
+    float* ws_m = ws_a + (size_t)groups * ext_tiles * 8 * sm100::BM;
+    using CF = sm100::ScoreFusedCfg<D>;
+    auto kern = sm100::score_fused_kernel<D, sm100::K5_POLY_DEFAULT>;
+    static int poly = -3;
+    if (poly < -2) {  // diagnostics: FB_K5_POLY = 0 / 2 / 4 exp2 pairs of 8 on the FMA pipes;
+                      // -1 the TMA + MMA pipeline alone, -2 the math without the A / mt stores
+      const char* e = getenv("FB_K5_POLY");
+      poly = e ? atoi(e) : sm100::K5_POLY_DEFAULT;
+      cudaFuncSetAttribute(sm100::score_fused_kernel<D, sm100::K5_POLY_DEFAULT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+      cudaFuncSetAttribute(sm100::score_fused_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+      cudaFuncSetAttribute(sm100::score_fused_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+      cudaFuncSetAttribute(sm100::score_fused_kernel<D, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+      cudaFuncSetAttribute(sm100::score_fused_kernel<D, -2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+    }
+    if (poly == -1) kern = sm100::score_fused_kernel<D, -1>;
+    if (poly == -2) kern = sm100::score_fused_kernel<D, -2>;
+    if (poly == 2) kern = sm100::score_fused_kernel<D, 2>;
+    if (poly == 4) kern = sm100::score_fused_kernel<D, 4>;
+    launch_pdl(kern, dim3((unsigned)p.ctas), dim3(sm100::SCORE_FUSED_THREADS), CF::SMEM,
+               st, mq, mk, mki, pgv, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
+               lse2, ws_l, ws_a, ws_m);
+    count_launch();
+    ++g_k5_fused_launches;
+    if ((rc = check_launch("score_kernel<fused>"))) return rc;
+    // ~4 CTAs per SM in one wave, at least 8 tiles (one per warp) each
+    const int64_t want = std::max<int64_t>(1, 4 * num_sms() / std::max<int64_t>(groups, 1));
+    const int tpc = (int)std::max<int64_t>(8, (ext_tiles + want - 1) / want);
+    const dim3 grid((unsigned)((ext_tiles + tpc - 1) / tpc), (unsigned)groups);
+    launch_pdl(sm100::score_mass_kernel, grid, dim3(256), 0, st, sc, (int)q_rows, ext_tiles, (int)nb, tpc,
+               (const float*)lse2, (const float*)ws_l, (const float*)ws_a, (const float*)ws_m, mass);
+    count_launch();
+    return check_launch("score_mass_kernel");
+  }
+  launch_pdl(sm100::score_kernel<D, 0>, dim3((unsigned)p.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
              st, mq, mk, mki, pgv, sc, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
              (const float*)nullptr, lse2, ws_l, (double*)nullptr, (int)nb);
   count_launch();
@@ -2539,7 +2965,7 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   // MASS pass over the external keys
   RefreshPlan pm = plan_refresh(groups, q_rows, 0, (int64_t)ext_tiles * 128);
   sm100::Sched sm{pm.T, pm.tpi, pm.m_tiles, pm.items, pm.ctas, nullptr};
-  launch_pdl(sm100::score_kernel<D, true>, dim3((unsigned)pm.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
+  launch_pdl(sm100::score_kernel<D, 1>, dim3((unsigned)pm.ctas), dim3(sm100::SCORE_THREADS), C::SMEM,
              st, mq, mk, mki, pgv, sm, (int)q_rows, (int)n_ext, (int)n_in, ext_tiles, scale_log2,
              (const float*)lse2, (float*)nullptr, (float*)nullptr, mass, (int)nb);
   count_launch();

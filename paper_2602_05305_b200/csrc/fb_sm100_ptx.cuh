@@ -389,6 +389,32 @@ __device__ __forceinline__ void ex2_poly2(uint64_t x2, float& p0, float& p1) {
   p1 = x1 > -127.f ? r1 : 0.f;
 }
 
+// 2^x for a packed pair on the FMA pipes with fp32-level accuracy (K5 block
+// masses are summed in fp32, not rounded to bf16 like P): the same range
+// reduction as ex2_poly2 and a degree-5 minimax polynomial on [-0.5, 0.5]
+// (max rel. error 2.3e-7 evaluated in fp32 -- MUFU.EX2's own is ~1.7e-7).
+// x is clamped to >= -126 (finite inputs only: the caller keeps masked keys
+// on the MUFU path), so far-below-max keys give ~1e-38 instead of 0.
+__device__ __forceinline__ uint64_t ex2_poly5x2(uint64_t x2) {
+  float x0, x1;
+  f2_unpack(x2, x0, x1);
+  const uint64_t xc = f2_pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t t = f2_add(xc, f2_pack(12582912.f, 12582912.f));  // rint in the low mantissa
+  const uint64_t j = f2_add(t, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = f2_fma(j, f2_pack(-1.f, -1.f), xc);            // f = x - rint(x)
+  uint64_t p = f2_fma(f2_pack(0.001327644451521337f, 0.001327644451521337f), f,
+                      f2_pack(0.00967553723603487f, 0.00967553723603487f));
+  p = f2_fma(p, f, f2_pack(0.05550713464617729f, 0.05550713464617729f));
+  p = f2_fma(p, f, f2_pack(0.24022120237350464f, 0.24022120237350464f));
+  p = f2_fma(p, f, f2_pack(0.6931469440460205f, 0.6931469440460205f));
+  p = f2_fma(p, f, f2_pack(1.0000001192092896f, 1.0000001192092896f));
+  float pa, pb, ta, tb;
+  f2_unpack(p, pa, pb);
+  f2_unpack(t, ta, tb);
+  return f2_pack(__int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23)),
+                 __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23)));
+}
+
 // 256-bit global store (STG.E.ENL2.256): a full 32-byte sector per request,
 // half the requests of float4 stores.  p must be 32-byte aligned.
 __device__ __forceinline__ void st_v8(float* p, float a0, float a1, float a2, float a3, float a4, float a5,
