@@ -320,6 +320,22 @@ FB_API int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, cons
  * (one fused tcgen05 kernel); large blocks (video chunks) run the stream-K
  * tensor-core partial over the block's keys plus a K3 merge and need this
  * much (without it they fall back to the SIMT kernel). */
+/* Host-buffer cached step: attention_with_reuse (attention.py:295-321) for
+ * the reference's synchronous numpy signature in ONE call.  q [groups,
+ * q_rows, d], k_in / v_in [groups, n_in, d] and the outputs are HOST arrays
+ * in the mode's element type (FB_F64: double, FB_F32: float; lognorms are
+ * double in both); o_ext / lse_ext are the DEVICE cached external partial
+ * (the partial types of the mode).  The inputs are packed into a per-thread
+ * pinned staging buffer and uploaded with one copy, the cached step runs on
+ * `stream`, and out / o_int / lse_int (o_int, lse_int optional: NULL skips)
+ * come back with one copy and one stream synchronisation.  *empty_rows (may
+ * be NULL) receives the number of rows with no keys on either side; the
+ * caller raises DegenerateInputError if it is > 0, as the reference does.
+ * Only FB_F64 / FB_F32 (numpy has no bf16). */
+FB_API int fb_internal_merge_host(int dtype, const void* q, const void* k_in, const void* v_in,
+                                  int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_in,
+                                  double scale, const void* o_ext, const void* lse_ext, void* out,
+                                  void* o_int, double* lse_int, int64_t* empty_rows, void* stream);
 FB_API size_t fb_internal_merge_workspace_bytes(int dtype, int64_t groups, int64_t q_rows,
                                                 int64_t head_dim, int64_t n_in);
 

@@ -28,6 +28,8 @@ vp, i64, i32, dbl, sz = C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_size_t
 # name -> (restype, argtypes); mirrors include/flashblock_b200.h
 SIGNATURES = {
     "fb_last_error": (C.c_char_p, []),
+    "fb_internal_merge_host": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, vp, vp,
+                                     vp, vp]),
     "fb_version": (C.c_char_p, []),
     "fb_launch_count": (i64, []),
     "fb_partial_workspace_bytes": (sz, [i32, i64, i64, i64, i64]),

@@ -15,7 +15,9 @@ rounding (tests/test_attention.py:128-134 there).
 
 from __future__ import annotations
 
+import ctypes
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -61,6 +63,97 @@ def _to_dev(x, dtype=None) -> torch.Tensor:
         a = a.astype(np.float64)
     t = torch.from_numpy(a).to(_device(), non_blocking=False)
     return t if dtype is None else t.to(dtype)
+
+
+class _Staging:
+    """Pinned host staging for the numpy drop-in path: a call's numpy inputs
+    are packed into one pinned buffer and uploaded with ONE host->device copy;
+    its results come back by async device->host copies into pinned memory and
+    ONE stream synchronisation (the reference API is synchronous numpy, so a
+    call must return host arrays).  Buffers are reused across calls: every
+    call ends with that synchronisation, so no copy is in flight when the next
+    call overwrites them.  Not shared between threads (see _ThreadStaging)."""
+
+    def __init__(self):
+        self._up: torch.Tensor | None = None
+        self._down: torch.Tensor | None = None
+        self._up_done: torch.cuda.Event | None = None  # the last upload's copy
+
+    @staticmethod
+    def _grow(buf, nbytes):
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 16) * 2, dtype=torch.uint8, pin_memory=True)
+        return buf
+
+    def upload(self, dt: torch.dtype, arrays) -> list[torch.Tensor]:
+        np_dt = np.float64 if dt == torch.float64 else np.float32
+        item = np.dtype(np_dt).itemsize
+        sizes = [int(np.prod(a.shape)) for a in arrays]
+        total = sum(sizes)
+        if self._up_done is not None:  # a call that raised before its download never synchronised
+            self._up_done.synchronize()
+        self._up = self._grow(self._up, total * item)
+        host = self._up[:total * item].numpy().view(np_dt)
+        off = 0
+        for a, n in zip(arrays, sizes):
+            host[off:off + n] = np.asarray(a).reshape(-1)
+            off += n
+        dev = torch.empty(total, dtype=dt, device=_device())
+        dev.copy_(self._up[:total * item].view(dt), non_blocking=True)
+        if self._up_done is None:
+            self._up_done = torch.cuda.Event()
+        self._up_done.record()
+        out, off = [], 0
+        for a, n in zip(arrays, sizes):
+            out.append(dev[off:off + n].view(a.shape))
+            off += n
+        return out
+
+    def download(self, tensors) -> list[np.ndarray]:
+        """Host copies (own memory) of device tensors, one synchronisation."""
+        offs, total = [], 0
+        for t in tensors:
+            total = (total + 7) // 8 * 8
+            offs.append(total)
+            total += t.numel() * t.element_size()
+        self._down = self._grow(self._down, total)
+        views = []
+        for t, o in zip(tensors, offs):
+            nb = t.numel() * t.element_size()
+            hv = self._down[o:o + nb].view(t.dtype)
+            hv.copy_(t.reshape(-1), non_blocking=True)
+            views.append(hv)
+        torch.cuda.current_stream(_device()).synchronize()
+        return [v.numpy().reshape(tuple(t.shape)).copy() for v, t in zip(views, tensors)]
+
+
+class _ThreadStaging(threading.local):
+    """One staging area per host thread: the reference calls its attention
+    functions from worker threads (bench.sweep_density's thread_map)."""
+
+    def __init__(self):
+        self.stage = _Staging()
+
+    def upload(self, dt, arrays):
+        return self.stage.upload(dt, arrays)
+
+    def download(self, tensors):
+        return self.stage.download(tensors)
+
+
+_STAGE = _ThreadStaging()
+
+
+def _np_mode_dtype(*arrs) -> torch.dtype:
+    """Device dtype for numpy inputs: float64 if any input is float64 (numpy
+    promotion in the reference), float32 if all are float32, else float64."""
+    if all(isinstance(a, np.ndarray) and a.dtype == np.float32 for a in arrs):
+        return torch.float32
+    return torch.float64
+
+
+def _all_np(*arrs) -> bool:
+    return all(isinstance(a, np.ndarray) for a in arrs)
 
 
 def _common_dtype(*arrs) -> torch.dtype:
@@ -117,6 +210,25 @@ class AttnPartial:
     out: np.ndarray | torch.Tensor
     lognorm: np.ndarray | torch.Tensor
 
+    # numpy partials made by this module keep the device tensors they were
+    # read back from (and host snapshots to detect in-place edits), so a later
+    # cached step / merge does not upload them again
+    def _set_mirror(self, o_dev: torch.Tensor, l_dev: torch.Tensor) -> "AttnPartial":
+        self.__dict__["_mirror"] = (o_dev, l_dev, self.out, self.lognorm, self.out.copy(),
+                                    self.lognorm.copy())
+        return self
+
+    def _device_mirror(self):
+        m = self.__dict__.get("_mirror")
+        if m is None:
+            return None
+        o_dev, l_dev, out_obj, ln_obj, out_snap, ln_snap = m
+        if self.out is not out_obj or self.lognorm is not ln_obj \
+                or not np.array_equal(self.out, out_snap) or not np.array_equal(self.lognorm, ln_snap):
+            self.__dict__.pop("_mirror", None)
+            return None
+        return o_dev, l_dev
+
     @classmethod
     def empty(cls, num_queries: int, head_dim: int, dtype=np.float64) -> "AttnPartial":
         return cls(out=np.zeros((num_queries, head_dim), dtype=dtype),
@@ -147,22 +259,46 @@ class AttnPartial:
                            self.lognorm.copy() if _is_np(self.lognorm) else self.lognorm.clone())
 
 
+def _upload_qkv(q, keys, values):
+    """(q, keys, values) on the device in the call's precision mode; numpy
+    inputs go up in one pinned host->device copy."""
+    dt = _common_dtype(q, keys, values)
+    if _all_np(q, keys, values):
+        return _STAGE.upload(dt, [q, keys, values])
+    return [_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt)]
+
+
 def _partial_dev(q, keys, values, scale, begin=0, end=None):
     """Device partial of keys[begin:end] for the 2-D reference signature."""
-    dt = _common_dtype(q, keys, values)
-    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
+    qt, kt, vt, dv = _widen(*_upload_qkv(q, keys, values))
     o, l = K.attention_partial(qt, kt, vt, begin, end, scale)
     return o[..., :dv], l
 
 
-def _wrap(o3, l3, as_numpy: bool, out_np_dtype=None) -> AttnPartial:
-    o, l = o3[0], l3[0]
-    if as_numpy:
-        o_np = o.cpu().numpy()
+def _wrap_many(parts, as_numpy: bool, out_np_dtype=None) -> list[AttnPartial]:
+    """AttnPartials from device (o3, l3) pairs; numpy results come back with
+    one synchronisation and keep their device tensors as a mirror when no
+    dtype cast was applied (the mirror then equals an upload of the arrays)."""
+    devs = [(o3[0], l3[0]) for o3, l3 in parts]
+    if not as_numpy:
+        return [AttnPartial(o, l) for o, l in devs]
+    hosts = _STAGE.download([t for pair in devs for t in pair])
+    res = []
+    for i, (o, l) in enumerate(devs):
+        o_np, l_np = hosts[2 * i], hosts[2 * i + 1]
+        exact = out_np_dtype is None or np.dtype(out_np_dtype) == o_np.dtype
         if out_np_dtype is not None:
             o_np = o_np.astype(out_np_dtype, copy=False)
-        return AttnPartial(o_np, l.cpu().numpy().astype(np.float64, copy=False))
-    return AttnPartial(o, l)
+        exact = exact and l_np.dtype == np.float64
+        p = AttnPartial(o_np, l_np.astype(np.float64, copy=False))
+        if exact and o.is_contiguous() and l.is_contiguous():
+            p._set_mirror(o, l)
+        res.append(p)
+    return res
+
+
+def _wrap(o3, l3, as_numpy: bool, out_np_dtype=None) -> AttnPartial:
+    return _wrap_many([(o3, l3)], as_numpy, out_np_dtype)[0]
 
 
 def attention_dense(q, keys, values, scale: float | None = None):
@@ -181,11 +317,14 @@ def attention_dense(q, keys, values, scale: float | None = None):
     dt = _common_dtype(q, keys, values)
     if dt != torch.bfloat16:
         dt = torch.float64
-    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
+    if _all_np(q, keys, values):
+        qt, kt, vt, dv = _widen(*_STAGE.upload(dt, [q, keys, values]))
+    else:
+        qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
     o, _ = K.attention_partial(qt, kt, vt, 0, None, scale)
     o = o[..., :dv]
     if _is_np(q):
-        return o[0].cpu().numpy().astype(np.float64, copy=False)
+        return _STAGE.download([o[0].contiguous()])[0].astype(np.float64, copy=False)
     return o[0]
 
 
@@ -199,7 +338,7 @@ def attention_partial(q, keys, values, scale: float | None = None,
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[1])
     o, l = _partial_dev(q, keys, values, scale)
-    return _wrap(o, l, _is_np(q), q.dtype if _is_np(q) else None)
+    return _wrap(o.contiguous(), l, _is_np(q), q.dtype if _is_np(q) else None)
 
 
 def attention_streamed(q, keys, values, boundary: int, scale: float | None = None,
@@ -213,19 +352,23 @@ def attention_streamed(q, keys, values, boundary: int, scale: float | None = Non
         raise ValueError("tile_size must be >= 1")
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[1])
-    dt = _common_dtype(q, keys, values)
-    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(keys, dt), _to_dev(values, dt))
+    qt, kt, vt, dv = _widen(*_upload_qkv(q, keys, values))
     n = kt.shape[0]
     eo, el = K.attention_partial(qt, kt, vt, 0, boundary, scale)
     io, il = K.attention_partial(qt, kt, vt, boundary, n, scale)
-    eo, io = eo[..., :dv], io[..., :dv]
+    if dv != eo.shape[-1]:
+        eo, io = eo[..., :dv].contiguous(), io[..., :dv].contiguous()
     np_out = q.dtype if _is_np(q) else None
-    return _wrap(eo, el, _is_np(q), np_out), _wrap(io, il, _is_np(q), np_out)
+    ext, inn = _wrap_many([(eo, el), (io, il)], _is_np(q), np_out)
+    return ext, inn
 
 
 def _partial_to_dev(p: AttnPartial):
     if isinstance(p.out, torch.Tensor):
         return p.out, p.lognorm
+    m = p._device_mirror()
+    if m is not None:
+        return m
     out = np.ascontiguousarray(p.out)
     if out.dtype not in (np.float32, np.float64):
         out = out.astype(np.float64)
@@ -250,8 +393,7 @@ def combine_partials(a: AttnPartial, b: AttnPartial) -> AttnPartial:
     else:
         out = K.combine([(ao, al), (bo, bl)], out_dtype=ao.dtype)
     if _is_np(a.out):
-        return AttnPartial(out[0].cpu().numpy().astype(a.out.dtype, copy=False),
-                           out[1].cpu().numpy().astype(np.float64, copy=False))
+        return _wrap(out[0][None], out[1][None], True, a.out.dtype)
     return AttnPartial(out[0], out[1])
 
 
@@ -301,6 +443,38 @@ class ExternalAttnCache:
         return sum(e.partial.nbytes for e in self._entries.values() if e.valid)
 
 
+def _reuse_host(q, partial: AttnPartial, k_in, v_in, scale: float):
+    """The numpy cached step in ONE C-ABI call (fb_internal_merge_host: pinned
+    staging, one upload, the cached step, one read-back) when the cached
+    external partial is already on the device in the call's precision mode
+    (a partial this module returned).  None: take the general path."""
+    if not (_all_np(q, k_in, v_in) and q.shape[1] == k_in.shape[1] == v_in.shape[1]):
+        return None
+    m = partial._device_mirror() if isinstance(partial.out, np.ndarray) else None
+    if m is None:
+        return None
+    dt = _np_mode_dtype(q, k_in, v_in)
+    o_ext, l_ext = m
+    if o_ext.dtype != dt or l_ext.dtype != torch.float64 or o_ext.shape != tuple(q.shape) \
+            or o_ext.device != _device():
+        return None
+    np_dt = np.float64 if dt == torch.float64 else np.float32
+    qa = np.ascontiguousarray(q, dtype=np_dt)
+    ka = np.ascontiguousarray(k_in, dtype=np_dt)
+    va = np.ascontiguousarray(v_in, dtype=np_dt)
+    out = np.empty(q.shape, dtype=np_dt)
+    o_int = np.empty(q.shape, dtype=np_dt)
+    l_int = np.empty(q.shape[0], dtype=np.float64)
+    empty = ctypes.c_int64(0)
+    K._lib.call("fb_internal_merge_host", K._lib.FB_F64 if dt == torch.float64 else K._lib.FB_F32,
+                qa.ctypes.data, ka.ctypes.data, va.ctypes.data, 1, q.shape[0], q.shape[1], k_in.shape[0],
+                float(scale), o_ext.data_ptr(), l_ext.data_ptr(), out.ctypes.data, o_int.ctypes.data,
+                l_int.ctypes.data, ctypes.addressof(empty), torch.cuda.current_stream(_device()).cuda_stream)
+    if empty.value > 0:
+        raise DegenerateInputError("some query rows have no keys on either side")
+    return out.astype(q.dtype, copy=False), AttnPartial(o_int.astype(q.dtype, copy=False), l_int)
+
+
 def attention_with_reuse(q, entry: CacheEntry | None, internal_keys, internal_values,
                          scale: float | None = None, tile_size: int = DEFAULT_TILE):
     """Cached step (attention.py:295-321): fresh internal partial fused with the
@@ -316,8 +490,10 @@ def attention_with_reuse(q, entry: CacheEntry | None, internal_keys, internal_va
         raise ValueError("tile_size must be >= 1")
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[1])
-    dt = _common_dtype(q, internal_keys, internal_values)
-    qt, kt, vt, dv = _widen(_to_dev(q, dt), _to_dev(internal_keys, dt), _to_dev(internal_values, dt))
+    fast = _reuse_host(q, entry.partial, internal_keys, internal_values, scale)
+    if fast is not None:
+        return fast
+    qt, kt, vt, dv = _widen(*_upload_qkv(q, internal_keys, internal_values))
     eo, el = _partial_to_dev(entry.partial)
     if eo.shape[-1] != dv:
         raise ShapeError(f"cached partial has {eo.shape[-1]} value columns, internal values {dv}")
@@ -327,11 +503,18 @@ def attention_with_reuse(q, entry: CacheEntry | None, internal_keys, internal_va
         eo = torch.cat([eo, eo.new_zeros(eo.shape[:-1] + (qt.shape[-1] - dv,))], dim=-1)
     out, lse_m, (io, il) = K.internal_merge(qt, kt, vt, eo, el, scale, want_lse=True,
                                             want_internal=True)
-    out, io = out[..., :dv], io[..., :dv]
+    if dv != out.shape[-1]:
+        out, io = out[..., :dv].contiguous(), io[..., :dv].contiguous()
+    if _is_np(q):
+        # one synchronisation for the merged output, its lognorm (the empty
+        # row check) and the internal partial
+        o_np, lse_np, io_np, il_np = _STAGE.download([out[0], lse_m[0], io[0], il[0]])
+        if np.isneginf(lse_np).any():
+            raise DegenerateInputError("some query rows have no keys on either side")
+        internal = AttnPartial(io_np.astype(q.dtype, copy=False), il_np.astype(np.float64, copy=False))
+        if io_np.dtype == q.dtype and il_np.dtype == np.float64:
+            internal._set_mirror(io[0], il[0])
+        return o_np.astype(q.dtype, copy=False), internal
     if bool(torch.isneginf(lse_m).any()):
         raise DegenerateInputError("some query rows have no keys on either side")
-    if _is_np(q):
-        return (out[0].cpu().numpy().astype(q.dtype, copy=False),
-                AttnPartial(io[0].cpu().numpy().astype(q.dtype, copy=False),
-                            il[0].cpu().numpy().astype(np.float64, copy=False)))
     return out[0], AttnPartial(io[0], il[0])

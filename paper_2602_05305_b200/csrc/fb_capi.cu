@@ -967,6 +967,108 @@ int fb_internal_merge(int dtype, const void* q, const void* k_in, const void* v_
                               workspace, workspace_bytes, 0, stream);
 }
 
+// Per-thread (and per-device) staging for the host-buffer entries: a pinned
+// host buffer and a device buffer, grown on demand.  Each call ends with a
+// stream synchronisation, so the next call of the same thread may reuse both.
+namespace {
+struct HostStage {
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* dbuf = nullptr;
+  size_t dbuf_bytes = 0;
+};
+constexpr int kMaxStageDevices = 16;
+thread_local HostStage t_stage[kMaxStageDevices];
+
+int stage_reserve(size_t host_bytes, size_t dev_bytes, HostStage*& out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxStageDevices)
+    return fail(FB_ERR_CUDA, "no current CUDA device for the host staging");
+  HostStage& s = t_stage[dev];
+  if (s.pinned_bytes < host_bytes) {
+    if (s.pinned) cudaFreeHost(s.pinned);
+    s.pinned = nullptr;
+    s.pinned_bytes = 0;
+    const size_t want = std::max<size_t>(host_bytes * 2, 1 << 16);
+    if (cudaMallocHost(&s.pinned, want) != cudaSuccess) return fail(FB_ERR_CUDA, "cudaMallocHost failed");
+    s.pinned_bytes = want;
+  }
+  if (s.dbuf_bytes < dev_bytes) {
+    if (s.dbuf) cudaFree(s.dbuf);
+    s.dbuf = nullptr;
+    s.dbuf_bytes = 0;
+    const size_t want = std::max<size_t>(dev_bytes * 2, 1 << 16);
+    if (cudaMalloc(&s.dbuf, want) != cudaSuccess) return fail(FB_ERR_CUDA, "cudaMalloc failed");
+    s.dbuf_bytes = want;
+  }
+  out = &s;
+  return FB_OK;
+}
+}  // namespace
+
+int fb_internal_merge_host(int dtype, const void* q, const void* k_in, const void* v_in, int64_t groups,
+                           int64_t q_rows, int64_t head_dim, int64_t n_in, double scale, const void* o_ext,
+                           const void* lse_ext, void* out, void* o_int, double* lse_int,
+                           int64_t* empty_rows, void* stream) {
+  if (dtype != FB_F64 && dtype != FB_F32)
+    return fail(FB_ERR_UNSUPPORTED, "fb_internal_merge_host: FB_F64 or FB_F32 host arrays");
+  if (groups < 0 || q_rows < 0 || head_dim < 1 || n_in < 0)
+    return fail(FB_ERR_SHAPE, "negative extent or head_dim < 1");
+  if (empty_rows) *empty_rows = 0;
+  if (groups == 0 || q_rows == 0) return FB_OK;
+  if (q == nullptr || out == nullptr || o_ext == nullptr || lse_ext == nullptr ||
+      (n_in > 0 && (k_in == nullptr || v_in == nullptr)))
+    return fail(FB_ERR_VALUE, "fb_internal_merge_host: null pointer");
+  const size_t E = dtype == FB_F64 ? sizeof(double) : sizeof(float);
+  const size_t rows = (size_t)(groups * q_rows);
+  const size_t qb = rows * head_dim * E, kb = (size_t)(groups * n_in) * head_dim * E;
+  const size_t in_bytes = align_up(qb + 2 * kb, 256);
+  // device / pinned layout: [q | k_in | v_in] [out | o_int | lse_int | empty counter]
+  const size_t ob = align_up(rows * head_dim * E, 256), lb = align_up(rows * sizeof(double), 256);
+  const size_t out_bytes = 2 * ob + lb + 256;
+  HostStage* s = nullptr;
+  if (int rc = stage_reserve(in_bytes + out_bytes, in_bytes + out_bytes, s)) return rc;
+  cudaStream_t st = as_stream(stream);
+  char* hp = reinterpret_cast<char*>(s->pinned);
+  char* dp = reinterpret_cast<char*>(s->dbuf);
+  std::memcpy(hp, q, qb);
+  if (kb) {
+    std::memcpy(hp + qb, k_in, kb);
+    std::memcpy(hp + qb + kb, v_in, kb);
+  }
+  char* d_out = dp + in_bytes;
+  char* d_oi = d_out + ob;
+  char* d_li = d_oi + ob;
+  int32_t* d_cnt = reinterpret_cast<int32_t*>(d_li + lb);
+  if (cudaMemcpyAsync(dp, hp, qb + 2 * kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemsetAsync(d_cnt, 0, sizeof(int32_t), st) != cudaSuccess)
+    return fail(FB_ERR_CUDA, "fb_internal_merge_host: staging copy failed");
+  const bool want_int = o_int != nullptr || lse_int != nullptr;
+  if (int rc = fb_internal_merge_ex(dtype, dp, dp + qb, dp + qb + kb, groups, q_rows, head_dim, n_in, scale,
+                                    o_ext, lse_ext, d_out, dtype, nullptr, want_int ? d_oi : nullptr,
+                                    want_int ? d_li : nullptr, d_cnt, nullptr, 0, FB_EXT_STABLE, stream))
+    return rc;
+  // one read-back: out, then (if wanted) o_int and lse_int, then the counter
+  char* h_out = hp + in_bytes;
+  cudaError_t e;
+  if (want_int) {
+    e = cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
+  } else {
+    e = cudaMemcpyAsync(h_out, d_out, ob, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_out + 2 * ob + lb, d_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(FB_ERR_CUDA, cudaGetErrorString(e));
+  std::memcpy(out, h_out, rows * head_dim * E);
+  if (o_int) std::memcpy(o_int, h_out + ob, rows * head_dim * E);
+  if (lse_int) std::memcpy(lse_int, h_out + 2 * ob, rows * sizeof(double));
+  int32_t cnt = 0;
+  std::memcpy(&cnt, h_out + 2 * ob + lb, sizeof(int32_t));
+  if (empty_rows) *empty_rows = cnt;
+  return FB_OK;
+}
+
 int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void* v_in,
                          int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_in,
                          double scale, const void* o_ext, const void* lse_ext, void* out,

@@ -359,8 +359,10 @@ def c1(out):
                    "final_ids_equal": bool((gpu.final_ids == base.final_ids).all()),
                    "max_checksum_rel_diff": max(abs(a.checksum - b.checksum) / max(1.0, abs(b.checksum))
                                                 for a, b in zip(gpu.traces, base.traces)),
-                   "note": "steps only (wall_ns of denoise_step); GPU replay pays a host<->device "
-                           "round trip per (layer, head) call, as the reference API is synchronous numpy"})
+                   "note": "steps only (wall_ns of denoise_step); the reference API is synchronous "
+                           "numpy, so every (layer, head) call is one host<->device round trip: cached "
+                           "steps go through fb_internal_merge_host (pinned staging, one upload, one "
+                           "read-back) against the device-resident cached partial"})
 
 
 # ---------------------------------------------------------------- CPU reference at C3 / C4
