@@ -2289,15 +2289,27 @@ static int launch_quad_128(const __nv_bfloat16* k, const CUtensorMap& mq, const 
       ws_l = ws_o + (size_t)2 * sc.ctas * PM * D;
     }
   }
-  auto kern = sm100::quad::quad_kernel<D>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
-    attr = true;
+  auto kern = sm100::quad::quad_kernel<D, 0>;
+  static int qpoly = -1;  // FB_QUAD_POLY=2 / 3 / 4: every n-th exp2 pair on the FMA pipes (diagnostics)
+  if (qpoly < 0) {
+    const char* e = getenv("FB_QUAD_POLY");
+    qpoly = e ? atoi(e) : 0;
+    cudaFuncSetAttribute(sm100::quad::quad_kernel<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
+    cudaFuncSetAttribute(sm100::quad::quad_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
+    cudaFuncSetAttribute(sm100::quad::quad_kernel<D, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
+    cudaFuncSetAttribute(sm100::quad::quad_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
   }
+  if (qpoly == 2) kern = sm100::quad::quad_kernel<D, 2>;
+  if (qpoly == 3) kern = sm100::quad::quad_kernel<D, 3>;
+  if (qpoly == 4) kern = sm100::quad::quad_kernel<D, 4>;
+  if (qpoly == 9) {  // diagnostics: no softmax (TMA + MMA pipeline only)
+    kern = sm100::quad::quad_kernel<D, -1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM);
+  }
+  const int threads = sm100::THREADS;
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   int rc;
-  launch_pdl(kern, dim3((unsigned)sc.ctas), dim3(sm100::THREADS), Q::SMEM, st, mq, mk, mv, pgv, cz, sc,
+  launch_pdl(kern, dim3((unsigned)sc.ctas), dim3(threads), Q::SMEM, st, mq, mk, mv, pgv, cz, sc,
              (int)q_rows, (int)key_begin, (int)key_end, scale_log2, o_out, lse_out, ws_o, ws_l);
   count_launch();
   ++g_quad_launches;

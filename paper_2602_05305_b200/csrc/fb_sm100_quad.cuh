@@ -31,6 +31,7 @@ struct QCfg {
   static constexpr uint32_t OFF_BAR = OFF_V + STAGES * TILE_BYTES;
   static constexpr uint32_t SMEM = OFF_BAR + 512 + 1024;
 };
+static_assert(QCfg<128>::SMEM <= 232448, "quad kernel shared memory exceeds 227 KB");
 
 struct QBars {
   uint64_t q_full, q_empty;
@@ -40,7 +41,7 @@ struct QBars {
   uint32_t tmem_base;
 };
 
-template <int D>
+template <int D, int POLY = 0>
 __global__ void __launch_bounds__(THREADS, 1)
 quad_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
             const __grid_constant__ CUtensorMap tm_v, Paged pg, Causal cz, Sched sc, int q_rows, int key_begin,
@@ -72,10 +73,10 @@ quad_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&bar->s_full[x], 1);
-      ptx::mbar_init(&bar->p_ready[x], 4);  // the warpgroup's 4 warps
+      ptx::mbar_init(&bar->p_ready[x], 4);  // the tile's softmax warps
     }
     ptx::mbar_init(&bar->o_full, 1);
-    ptx::mbar_init(&bar->o_empty, 8);       // 8 softmax warps
+    ptx::mbar_init(&bar->o_empty, 8);  // every softmax warp
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(&bar->tmem_base, TMEM_COLS);
@@ -207,6 +208,14 @@ quad_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         const int j = jg + t;
         ptx::mbar_wait(&bar->s_full[x], j & 1);
         ptx::tc_fence_after();
+        if constexpr (POLY < 0) {  // diagnostics: the TMA + MMA pipeline without the softmax
+          m_used = 0.f;
+          l = 1.f;
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&bar->p_ready[x]);
+          continue;
+        }
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c)
           ptx::tmem_ld32(tmem + lane_off + s_col + c * 32, reinterpret_cast<uint32_t*>(s) + c * 32);
@@ -231,7 +240,13 @@ quad_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
               const uint64_t x2 = ptx::f2_fma(ptx::f2_pack(s[c * 64 + 2 * i], s[c * 64 + 2 * i + 1]), sc2, ng2);
               float x0, x1;
               ptx::f2_unpack(x2, x0, x1);
-              const float p0 = ptx::ex2(x0), p1 = ptx::ex2(x1);
+              float p0, p1;
+              if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
+                ptx::ex2_poly2(x2, p0, p1);  // every POLY-th pair on the FMA pipes (MUFU offload)
+              } else {
+                p0 = ptx::ex2(x0);
+                p1 = ptx::ex2(x1);
+              }
               ls4[i & 3] = ptx::f2_add(ls4[i & 3], ptx::f2_pack(p0, p1));
               r[i] = ptx::pack_bf16(p0, p1);
             }
