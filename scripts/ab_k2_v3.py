@@ -1,4 +1,5 @@
-"""Interleaved A/B of the cached step (K2, bf16 cached partial, FB_EXT_STABLE)
+"""(Experiment record: needs the removed internal_merge_v3_kernel / fb_debug_set_k2_v3 build.)
+Interleaved A/B of the cached step (K2, bf16 cached partial, FB_EXT_STABLE)
 on v2 (two lock-step CTAs per SM) vs v3 (one CTA per SM, two pipelined query
 tiles): graph of 36 layers x 31 cached steps at the C2 shapes; outputs
 compared bitwise.   python scripts/ab_k2_v3.py [batch ...]"""
