@@ -2648,6 +2648,10 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
       for (int k = 16; k >= 2; k >>= 1) {
         if ((long long)p.items * k > num_sms() || p.tpi < 2 * k) continue;
         if (!need_merge && (p.tpi + k - 1) / k > per_streamk + per_streamk / 5) break;  // owner path: <= +20 % tiles
+        // large items (C3 b >= 4, C2 b >= 4): the SMs a power-of-two CTA group
+        // leaves idle cost more than the split-merge kernel (C3 b=4 P=1: 256 vs
+        // 222 tiles per CTA, 0.81 vs 0.9 of peak) -- stay on stream-K
+        if (need_merge && (p.tpi + k - 1) / k > per_streamk + 4) break;
         if (ws == nullptr || ws_bytes < (size_t)p.items * k * sm100::BM * (D + 1) * sizeof(float)) break;
         sc.clus = k;
         sc.gbar = 1;
