@@ -203,3 +203,25 @@ def test_grid_barrier_split_k(lib, groups, n):
     for gi in (0, groups - 1):
         ref = orc.partial(q[gi].double().cpu().numpy(), k[gi].double().cpu().numpy(), v[gi].double().cpu().numpy())
         assert np.max(np.abs(o_a[gi].double().cpu().numpy() - ref.out)) <= 1e-2 * np.max(np.abs(ref.out))
+
+
+@pytest.mark.parametrize("groups,n,expect_split_k", [
+    (8, 16384, True),     # C3 b=1 P=8 shard: 8 items x 128 tiles -> 16-CTA groups (grid barrier)
+    (32, 131072, False),  # C3 b=4 P=1: 32 items x 1024 tiles; a 4-CTA group would hold 256 tiles
+                          # vs 222 on 148-CTA stream-K
+])
+def test_split_k_plan_keeps_stream_k_for_large_items(lib, groups, n, expect_split_k):
+    """The per-item split-K plans (clusters / grid barrier) only for items
+    whose power-of-two CTA group stays near the stream-K share of tiles; large
+    items stay on 148-CTA stream-K + the split-merge kernel (the 128-CTA plan
+    had cost C3 b=8 P=1 12 %).  Both plans agree with the whole-range oracle."""
+    from paper_2602_05305_b200 import kernels as K
+    from oracle import flashblock_oracle as orc
+
+    g = torch.Generator(device="cuda").manual_seed(groups + n)
+    q, k, v = _r(g, groups, 128, 128), _r(g, groups, n, 128), _r(g, groups, n, 128)
+    (o, l), launches = _run(lib, -1, lambda: K.attention_partial(q, k, v))
+    assert (launches > 0) == expect_split_k
+    ref = orc.partial(q[0].double().cpu().numpy(), k[0].double().cpu().numpy(), v[0].double().cpu().numpy())
+    assert np.max(np.abs(o[0].cpu().numpy() - ref.out)) <= 1e-2 * np.max(np.abs(ref.out))
+    assert np.max(np.abs(l[0].cpu().numpy() - ref.lognorm)) <= 1e-3
