@@ -629,9 +629,10 @@ def run_e2e(args, eng, kc, vc, dev, sched, world):
     return {"value": world * b * BLK * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b,
             "h2d_gbs": h2d_b * steps / dt / 1e9, "d2h_gbs": d2h_b * steps / dt / 1e9,
-            "note": "public engine API, eager launches; per diffusion step: H2D of Q/K_in/V_in (all "
+            "note": "public engine API, eager launches; every diffusion step: H2D of Q/K_in/V_in (all "
                     "layers) and D2H of the attention outputs (all layers, bf16) from/to pinned host "
-                    "memory on two copy streams overlapping the attention; host wall clock; PCIe-bound"}
+                    "memory on two copy streams overlapping the attention; the *_bytes_per_step count "
+                    "one bench step = one 32-step block; host wall clock; PCIe-bound"}
 
 
 C3_CTX = 131072
