@@ -683,11 +683,13 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     o_ext = [torch.empty((per, rows, D), device=dev, dtype=torch.bfloat16) for _ in range(L)]
     l_ext = [torch.empty((per, rows), device=dev, dtype=torch.float32) for _ in range(L)]
     out = [torch.empty((per, rows, D), device=dev, dtype=torch.bfloat16) for _ in range(L)]
-    refresh = SplitKVRefresh(layout="all_to_all")
+    layouts = {"nccl": "all_to_all", "p2p": "p2p"}
+    refresh = SplitKVRefresh(layout=layouts[args.exchange] if world > 1 else "all_to_all")
 
-    def refresh_step():
+    def refresh_step(rf=None):
+        rf = rf or refresh
         for l in range(L):
-            refresh(q[l], kc[l], vc[l], n_loc, None, out=o_ext[l], lse=l_ext[l])
+            rf(q[l], kc[l], vc[l], n_loc, None, out=o_ext[l], lse=l_ext[l])
             K.internal_merge(q[l][g0:g1], ki[l][g0:g1], vi[l][g0:g1], o_ext[l], l_ext[l],
                              out_dtype=torch.bfloat16, out=out[l])
 
@@ -747,6 +749,13 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     # layers) and the cached steps
     ms_ref = timed(refresh_step, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
     ms_cached = timed(g_cached.replay, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
+    # the other exchange for comparison: peer-memory (CUDA IPC mapped partials,
+    # device flags, K3 reading in place) vs the NCCL grouped send / recv
+    other = {"nccl": "p2p", "p2p": "nccl"}[args.exchange]
+    ms_ref_other = None
+    if world > 1:
+        alt = SplitKVRefresh(layout=layouts[other])
+        ms_ref_other = timed(lambda: refresh_step(alt), max(2, args.steps // 2), 2) / max(2, args.steps // 2)
 
     # K1 on the local shard alone (roofline of the dominant kernel at this P)
     o_dt = torch.bfloat16 if world == 1 else torch.float32  # N=1 writes the cached partial directly
@@ -774,11 +783,16 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
                        "layers": L, "batch": b, "ctx": N, "shard_rows": n_loc, "q_heads": HQ,
                        "kv_heads": HKV, "head_dim": D, "block": BLK, "steps_per_block": STEPS_PER_BLOCK,
                        "kv_groups_per_rank": per,
-                       "exchange": "packed fp32 (O, LSE) partials, one grouped send/recv per layer "
-                                   "per block (all_to_all by kv-group chunk); cached steps exchange nothing",
+                       "exchange": ("packed fp32 (O, LSE) partials, one grouped send/recv per layer "
+                                    "per block (all_to_all by kv-group chunk); cached steps exchange nothing"
+                                    if args.exchange == "nccl" or world == 1 else
+                                    "peer memory: CUDA-IPC-mapped packed fp32 (O, LSE) partials, device "
+                                    "flag handshake, K3 merging the rank's kv-group chunk in place; no "
+                                    "collective; cached steps exchange nothing"),
                        "parallelism": f"split-KV x{world} (refresh) + kv-head shards (cached steps)",
                        "l2": "inputs larger than L2 (distinct KV shard per layer)"},
             "refresh_step_ms": ms_ref, "refresh_ms_per_layer": ms_ref / L,
+            "refresh_step_ms_other_exchange": ({other: ms_ref_other} if ms_ref_other is not None else None),
             "cached_steps_ms": ms_cached,
             "exchange_bytes_sent_per_layer_per_rank": exch,
             "roofline": {"bound": "hbm", "kernel": "K1 on the local KV shard",
@@ -822,6 +836,9 @@ def main():
     ap.add_argument("--ctx", type=int, default=C3_CTX, help="context for C3")
     ap.add_argument("--layers", type=int, default=LAYERS, help="layers for C3")
     ap.add_argument("--c3-batch", type=int, default=4, help="sequences for C3 (whole job)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="C3 split-KV exchange at N > 1: NCCL grouped send/recv (default) or peer memory "
+                         "(CUDA IPC, device flags, K3 in place); the other one is timed alongside")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -873,7 +890,8 @@ def main():
                 if line is not None and c3 is not None:
                     line["c3_split_kv"] = {k: c3[k] for k in (
                         "metric", "value", "unit", "ms_per_step", "scaling", "config", "refresh_step_ms",
-                        "refresh_ms_per_layer", "cached_steps_ms", "exchange_bytes_sent_per_layer_per_rank",
+                        "refresh_ms_per_layer", "refresh_step_ms_other_exchange", "cached_steps_ms",
+                        "exchange_bytes_sent_per_layer_per_rank",
                         "roofline", "gpu_launches")}
         if line is not None:
             print(json.dumps(line), flush=True)

@@ -432,6 +432,29 @@ FB_API size_t fb_sparse_workspace_bytes(int dtype, int64_t groups, int64_t q_row
 /* Count of kernel launches issued by this library since load (for bench). */
 FB_API int64_t fb_launch_count(void);
 
+/* ---------------------------------------------------------------- peer memory
+ * Split-KV exchange over peer memory: the ranks of one node map
+ * each other's packed partial buffers with CUDA IPC; a refresh then signals
+ * its peers after K1, waits for theirs, and runs the K3 merge (fb_combine)
+ * straight on the peers' mapped partials -- no collective, no staging copy.
+ * Replaces the NCCL exchange of the reference-side split (there is none in
+ * the single-process reference: simulator.py runs one sequence on one CPU;
+ * the merge itself is combine_partials, attention.py:207-233). */
+#define FB_P2P_HANDLE_BYTES 64
+/* cudaMalloc'ed, zeroed device memory and its 64-byte IPC handle. */
+FB_API int fb_p2p_alloc(size_t bytes, void** ptr, void* handle);
+FB_API int fb_p2p_free(void* ptr);
+/* Map a peer process's buffer (its fb_p2p_alloc handle) into this process. */
+FB_API int fb_p2p_open(const void* handle, void** ptr);
+FB_API int fb_p2p_close(void* ptr);
+/* On `stream`, after everything queued before it: a system-scope fence, then
+ * flags[p][slot] = value (release) for each of the n DEVICE pointers in the
+ * DEVICE array peer_flags (typically every rank's flag array, own included). */
+FB_API int fb_p2p_signal(uint64_t* const* peer_flags, int n, int slot, uint64_t value, void* stream);
+/* On `stream`: block until flags[i] >= value for every i < n (n <= 32;
+ * acquire, system scope).  Watchdog: traps after ~4 s without progress. */
+FB_API int fb_p2p_wait(const uint64_t* flags, int n, uint64_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,12 @@ vp, i64, i32, dbl, sz = C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_size_t
 # name -> (restype, argtypes); mirrors include/flashblock_b200.h
 SIGNATURES = {
     "fb_last_error": (C.c_char_p, []),
+    "fb_p2p_alloc": (i32, [sz, vp, vp]),
+    "fb_p2p_free": (i32, [vp]),
+    "fb_p2p_open": (i32, [vp, vp]),
+    "fb_p2p_close": (i32, [vp]),
+    "fb_p2p_signal": (i32, [vp, i32, i32, C.c_uint64, vp]),
+    "fb_p2p_wait": (i32, [vp, i32, C.c_uint64, vp]),
     "fb_internal_merge_host": (i32, [i32, vp, vp, vp, i64, i64, i64, i64, dbl, vp, vp, vp, vp, vp,
                                      vp, vp]),
     "fb_version": (C.c_char_p, []),

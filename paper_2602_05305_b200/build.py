@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "fb200")
 LIB = os.path.join(PKG, "libfb200.so")
 SOURCES = ["fb_capi.cu", "fb_simt.cu", "fb_sm100.cu", "fb_sm100_k2.cu", "fb_sparse.cu",
-           "fb_similarity.cu"]
+           "fb_similarity.cu", "fb_p2p.cu"]
 GENCODE = "arch=compute_100a,code=sm_100a"
 
 

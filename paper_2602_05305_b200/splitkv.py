@@ -20,6 +20,15 @@ LSE (groups, rows)]`` so the exchange is a single operation:
     exchange (``batch_isend_irecv``: with NCCL one ncclGroupStart/End, one
     kernel launch); the local chunk never leaves the device.
 
+  * ``p2p``         -- the same group-chunk result with no collective on the
+    data path: every rank's packed partial lives in device memory the other
+    ranks have mapped through CUDA IPC (``P2PExchange``); after K1 a rank
+    signals a flag in every peer's flag array, waits until all P flags of
+    this refresh are set (device-side, system-scope acquire), and K3 merges
+    its group chunk reading the P partials in place over NVLink.  Partial
+    buffers are double-buffered by refresh parity, so a rank's next K1 never
+    overwrites a partial a peer is still merging.
+
 The local partial and the merge default to the CUDA kernels (K1, K3); the
 hooks exist so the collective choreography can be tested with world-size-2
 ``gloo`` process groups on CPU, where tests pass oracle-backed callables.
@@ -112,8 +121,9 @@ class SplitKVRefresh:
     host_staged: bool = field(default=False, init=False)
 
     def __post_init__(self):
-        if self.layout not in ("all_gather", "all_to_all"):
+        if self.layout not in ("all_gather", "all_to_all", "p2p"):
             raise ValueError(f"unknown layout {self.layout!r}")
+        self._p2p: dict = {}
 
     def _stage(self, t: torch.Tensor) -> bool:
         return t.is_cuda and dist.get_backend(self.group) == "gloo"
@@ -129,6 +139,14 @@ class SplitKVRefresh:
         groups, rows, d = q.shape
         if world == 1:  # nothing to exchange: K1 straight into the destination
             return self.local_partial(q, k_shard, v_shard, n_local, scale, out, lse)
+        if self.layout == "p2p":
+            key = (groups, rows, d, q.dtype, q.device)
+            ex = self._p2p.get(key)
+            if ex is None:
+                ex = self._p2p[key] = P2PExchange(groups, rows, d, q.dtype, q.device, self.group)
+            self.host_staged = False
+            return ex.refresh(lambda o, l: self.local_partial(q, k_shard, v_shard, n_local, scale, o, l),
+                              out, lse)
         pk = PackedPartial(groups, rows, d, q.dtype, q.device)
         o, l = pk.views(pk.buf)
         self.local_partial(q, k_shard, v_shard, n_local, scale, o, l)
@@ -188,3 +206,134 @@ class SplitKVRefresh:
             if last:
                 return res
             parts = [res] + parts
+
+
+class _CudaMem:
+    """__cuda_array_interface__ of raw device bytes (a P2P allocation), so
+    torch can wrap it without a copy."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class P2PExchange:
+    """Peer-memory split-KV exchange of one partial shape.
+
+    Collective at construction (every rank of ``group``): each rank allocates
+    a double-buffered packed-partial region and a flag array [world] of
+    uint64 (``fb_p2p_alloc``), the 64-byte IPC handles are all-gathered, and
+    every peer's region / flags are mapped (``fb_p2p_open``).  ``refresh``
+    then runs with no collective:
+
+      1. K1 writes this rank's partial into its region's slot (epoch % 2);
+      2. ``fb_p2p_signal`` stores epoch + 1 into slot `rank` of every rank's
+         flag array (system-scope fence + release store);
+      3. ``fb_p2p_wait`` blocks the stream until all `world` flags of this
+         rank reach epoch + 1 (every peer's K1 of this refresh is done);
+      4. K3 (``fb_combine``) merges this rank's group chunk straight out of
+         the `world` mapped partials.
+
+    A rank's K1 of refresh e + 2 is stream-ordered after its wait of refresh
+    e + 1, which saw every peer's signal e + 1, itself ordered after that
+    peer's merge of refresh e -- so slot e % 2 is free again (no second
+    handshake).  Requires groups divisible by the world size and <= 32 ranks.
+    """
+
+    def __init__(self, groups: int, rows: int, d: int, in_dtype: torch.dtype, device, group=None):
+        from . import _lib
+
+        self.lib = _lib.load()
+        self._lib = _lib
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 32:
+            raise ValueError("p2p exchange: at most 32 ranks")
+        chunks = group_chunks(groups, self.world)
+        if any(hi - lo != chunks[0][1] - chunks[0][0] for lo, hi in chunks):
+            raise ShapeError(f"p2p exchange needs groups ({groups}) divisible by world ({self.world})")
+        self.chunks = chunks
+        self.device = torch.device(device)
+        self.pk = PackedPartial(groups, rows, d, in_dtype, "meta")
+        self.rows, self.d = rows, d
+        self.nbytes = self.pk.nbytes
+        self._opened: list[int] = []
+        self._owned: list[int] = []
+        region, h_region = self._alloc(2 * self.nbytes)
+        flags, h_flags = self._alloc(8 * self.world)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, (h_region, h_flags), group=group)
+        self.regions, flag_ptrs = [], []
+        for p, (hr, hf) in enumerate(handles):
+            if p == self.rank:
+                self.regions.append(region)
+                flag_ptrs.append(flags)
+            else:
+                self.regions.append(self._open(hr))
+                flag_ptrs.append(self._open(hf))
+        self.my_flags = flags
+        self.flag_ptrs = torch.tensor(flag_ptrs, dtype=torch.int64, device=self.device)
+        local = torch.as_tensor(_CudaMem(region, 2 * self.nbytes), device=self.device)
+        self.local = [local[i * self.nbytes:(i + 1) * self.nbytes] for i in range(2)]
+        self.epoch = 0
+
+    def _alloc(self, nbytes: int):
+        import ctypes
+
+        ptr = ctypes.c_void_p()
+        h = (ctypes.c_ubyte * 64)()
+        with torch.cuda.device(self.device):
+            self._lib.call("fb_p2p_alloc", nbytes, ctypes.addressof(ptr), ctypes.addressof(h))
+        self._owned.append(ptr.value)
+        return ptr.value, bytes(h)
+
+    def _open(self, handle: bytes) -> int:
+        import ctypes
+
+        ptr = ctypes.c_void_p()
+        h = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+        with torch.cuda.device(self.device):
+            self._lib.call("fb_p2p_open", ctypes.addressof(h), ctypes.addressof(ptr))
+        self._opened.append(ptr.value)
+        return ptr.value
+
+    def close(self) -> None:
+        """Unmap the peers and free this rank's buffers (call on every rank
+        once no refresh is in flight)."""
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            self.lib.fb_p2p_close(p)
+        for p in self._owned:
+            self.lib.fb_p2p_free(p)
+        self._opened, self._owned = [], []
+
+    def refresh(self, local_partial, out=None, lse=None):
+        from . import kernels as K
+
+        slot = self.epoch % 2
+        o, l = self.pk.views(self.local[slot])
+        local_partial(o, l)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        value = self.epoch + 1
+        self._lib.call("fb_p2p_signal", self.flag_ptrs.data_ptr(), self.world, self.rank, value, stream)
+        self._lib.call("fb_p2p_wait", self.my_flags, self.world, value, stream)
+        lo, hi = self.chunks[self.rank]
+        osz, lsz = o.element_size(), l.element_size()
+        o_parts = [r + slot * self.nbytes + lo * self.rows * self.d * osz for r in self.regions]
+        l_parts = [r + slot * self.nbytes + self.pk.l_off + lo * self.rows * lsz for r in self.regions]
+        code = K.mode_of_partial(o, l)
+        shape = (hi - lo, self.rows, self.d)
+        if out is None:
+            out = torch.empty(shape, dtype=o.dtype, device=self.device)
+        if lse is None:
+            lse = torch.empty(shape[:2], dtype=l.dtype, device=self.device)
+        if tuple(out.shape) != shape or tuple(lse.shape) != shape[:2] or not (out.is_contiguous()
+                                                                           and lse.is_contiguous()):
+            raise ShapeError(f"p2p exchange: out / lse must be contiguous {shape} / {shape[:2]}")
+        K._check_partial_out(code, out, lse)
+        self._lib.call("fb_combine", code, self.world, self._lib.ptr_array(o_parts), self._lib.ptr_array(l_parts),
+                       (hi - lo) * self.rows, self.d, out.data_ptr(), K._OUT_CODE[out.dtype], lse.data_ptr(),
+                       None, stream)
+        self.epoch += 1
+        return out, lse
