@@ -1203,7 +1203,9 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
 
 // ---------------------------------------------------------------- K5 scoring
 //
-// Sparse block selection scores (sparse.py:117-125) on the tensor cores:
+// Sparse block selection scores (sparse.py:117-125) on the tensor cores.
+// Two-pass form (score_kernel<D, MODE>, MODE 0 / 1; kept for A/B behind
+// fb_debug_set_k5_mode(1) / FB_K5_TWO_PASS=1):
 //   LSE pass  : per query row, log2-domain log-sum-exp of the scaled scores over
 //               ALL keys (committed [0,n_ext) + current block [0,n_in)), as
 //               stream-K split partials merged by score_lse_merge_kernel;
@@ -1215,8 +1217,9 @@ refresh_merge_kernel(Sched sc, int q_rows, int D, const float* __restrict__ ws_o
 //   FUSED pass (score_fused_kernel, the default): ONE read of K.  Four
 //               score warpgroups take 32 columns (two 16-key blocks) of every
 //               S tile each; a thread takes its row's quarter-tile max mt,
-//               sums p = exp2(s*c - mt) per block (A) -- part of the exp2 pairs
-//               on the FMA pipes -- and over the quarter (the row's running
+//               sums p = exp2(s*c - mt) per block (A; optionally part of the
+//               exp2 pairs on the FMA pipes, off by default) and over the
+//               quarter (the row's running
 //               LSE, rescaled by two exp2 per tile), and stores A and mt for
 //               the external tiles; score_mass_kernel weights A by
 //               exp2(mt - lse2_row) once the row LSE is final and sums the
