@@ -102,3 +102,26 @@ def test_host_cached_step_raises_on_degenerate_rows(lib):
     assert ext._device_mirror() is not None
     with pytest.raises(DegenerateInputError):
         A.attention_with_reuse(q, A.CacheEntry(ext, 0), k, k)
+
+
+@pytest.mark.gpu
+def test_host_cached_step_mixed_dtypes_and_value_width(lib):
+    """Mixed numpy dtypes promote like the reference (float64 wins); a value
+    width != key width takes the general device path; both equal the oracle."""
+    from oracle import flashblock_oracle as orc
+    from paper_2602_05305_b200 import attention as A
+
+    rng = np.random.default_rng(7)
+    q = rng.standard_normal((12, 16)).astype(np.float32)
+    k = rng.standard_normal((200, 16))           # float64
+    v = rng.standard_normal((200, 16)).astype(np.float32)
+    ext, _ = A.attention_streamed(q, k, v, 180)
+    out, internal = A.attention_with_reuse(q, A.CacheEntry(ext, 0), k[180:], v[180:])
+    ref = orc.dense(q.astype(np.float64), k, v.astype(np.float64))
+    assert out.dtype == np.float32 and internal.lognorm.dtype == np.float64
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-5 * np.abs(ref).max())
+    # value width 12 != key width 16
+    v12 = rng.standard_normal((200, 12))
+    ext12, _ = A.attention_streamed(q.astype(np.float64), k, v12, 180)
+    out12, _ = A.attention_with_reuse(q.astype(np.float64), A.CacheEntry(ext12, 0), k[180:], v12[180:])
+    np.testing.assert_allclose(out12, orc.dense(q.astype(np.float64), k, v12), rtol=0, atol=1e-10)

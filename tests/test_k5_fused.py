@@ -54,6 +54,8 @@ def _mass(lib, mode, q, k, kin, n_ext, page_table=None):
     (5, 128, 128, 300, 200),      # current block spanning two tiles
     (2, 128, 64, 3000, 32),       # head_dim 64
     (40, 128, 128, 16384, 32),    # items split over several CTAs (stream-K LSE partials)
+    (3, 1, 128, 17, 1),           # one query row, a 1-key tail block, a 1-key current block
+    (2, 33, 64, 16, 5),           # a single external block, odd row count
 ])
 def test_fused_mass_equals_two_pass_and_oracle(lib, groups, q_rows, d, n_ext, n_in):
     from paper_2602_05305_b200 import kernels as K
