@@ -2885,8 +2885,13 @@ static size_t score_two_pass_bytes(int64_t groups, int64_t q_rows, int64_t n_ext
 static size_t score_fused_extra_bytes(int64_t groups, int64_t n_ext) {
   return (size_t)groups * ((n_ext + 127) / 128) * 12 * sm100::BM * sizeof(float);  // A: 8, mt: 4 per row
 }
+// the fused pass's per-(row, block) sums are ~19 % of the K bytes; past 256 MB
+// of them the workspace query reports the two-pass size instead (the launcher
+// then takes the two-pass kernels: 2 x K bytes, no proportional scratch)
+constexpr size_t SCORE_FUSED_MAX_EXTRA = size_t(256) << 20;
 size_t score_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
-  return score_two_pass_bytes(groups, q_rows, n_ext, n_in) + score_fused_extra_bytes(groups, n_ext);
+  const size_t extra = score_fused_extra_bytes(groups, n_ext);
+  return score_two_pass_bytes(groups, q_rows, n_ext, n_in) + (extra <= SCORE_FUSED_MAX_EXTRA ? extra : 0);
 }
 size_t score_sm100_min_workspace_bytes(int64_t groups, int64_t q_rows, int64_t n_ext, int64_t n_in) {
   return score_two_pass_bytes(groups, q_rows, n_ext, n_in);
@@ -2933,7 +2938,8 @@ static int launch_score_d(const __nv_bfloat16* q, const __nv_bfloat16* k, const 
   const size_t two = score_two_pass_bytes(groups, q_rows, n_ext, n_in);
   if (ws_bytes < two) return fail(FB_ERR_VALUE, "score workspace too small");
   sm100::Sched sc{p.T, p.tpi, p.m_tiles, p.items, p.ctas, nullptr};
-  if (!k5_two_pass() && ws_bytes >= two + score_fused_extra_bytes(groups, n_ext)) {
+  if (!k5_two_pass() && score_fused_extra_bytes(groups, n_ext) <= SCORE_FUSED_MAX_EXTRA &&
+      ws_bytes >= two + score_fused_extra_bytes(groups, n_ext)) {
     float* ws_a = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + two);
     float* ws_m = ws_a + (size_t)groups * ext_tiles * 8 * sm100::BM;
     using CF = sm100::ScoreFusedCfg<D>;

@@ -125,6 +125,13 @@ class SplitKVRefresh:
             raise ValueError(f"unknown layout {self.layout!r}")
         self._p2p: dict = {}
 
+    def close(self) -> None:
+        """Release the peer-memory exchanges (layout "p2p"): collective, call on
+        every rank once no refresh is in flight."""
+        for ex in self._p2p.values():
+            ex.close()
+        self._p2p.clear()
+
     def _stage(self, t: torch.Tensor) -> bool:
         return t.is_cuda and dist.get_backend(self.group) == "gloo"
 
