@@ -754,8 +754,12 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     other = {"nccl": "p2p", "p2p": "nccl"}[args.exchange]
     ms_ref_other = None
     if world > 1:
-        alt = SplitKVRefresh(layout=layouts[other])
-        ms_ref_other = timed(lambda: refresh_step(alt), max(2, args.steps // 2), 2) / max(2, args.steps // 2)
+        try:  # a set-up failure of the comparison (e.g. no CUDA IPC) must not cost the line
+            alt = SplitKVRefresh(layout=layouts[other])
+            ms_ref_other = timed(lambda: refresh_step(alt), max(2, args.steps // 2), 2) / max(2, args.steps // 2)
+            alt.close()
+        except Exception as e:  # noqa: BLE001
+            ms_ref_other = f"unavailable: {type(e).__name__}: {e}"[:200]
 
     # K1 on the local shard alone (roofline of the dominant kernel at this P)
     o_dt = torch.bfloat16 if world == 1 else torch.float32  # N=1 writes the cached partial directly
@@ -793,6 +797,7 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
                        "l2": "inputs larger than L2 (distinct KV shard per layer)"},
             "refresh_step_ms": ms_ref, "refresh_ms_per_layer": ms_ref / L,
             "refresh_step_ms_other_exchange": ({other: ms_ref_other} if ms_ref_other is not None else None),
+            "exchange_used": args.exchange if world > 1 else None,
             "cached_steps_ms": ms_cached,
             "exchange_bytes_sent_per_layer_per_rank": exch,
             "roofline": {"bound": "hbm", "kernel": "K1 on the local KV shard",
