@@ -1110,8 +1110,9 @@ int fb_internal_merge_ex(int dtype, const void* q, const void* k_in, const void*
         // without an lse_merged output the K3 merge with the cached external
         // partial runs inside K1's split-merge kernel (MergeFinal): one launch
         // and one pass over the internal partial fewer
+        // (the internal partial is scratch unless the caller asked for it)
         const MergeFinal fin{o_ext, reinterpret_cast<const float*>(lse_ext), out, out_dtype == FB_BF16 ? 1 : 0,
-                             empty_rows, extb ? 1 : 0};
+                             empty_rows, extb ? 1 : 0, (o_int == nullptr && lse_int == nullptr) ? 1 : 0};
         const bool fuse = lse_merged == nullptr;
         if (extb && !fuse)
           return fail(FB_ERR_UNSUPPORTED, "FB_PARTIAL_BF16 large-block cached step: lse_merged not supported");

@@ -100,6 +100,8 @@ struct Sched {
   int gbar;                // ... with the item's CTAs meeting at a counter in global memory
                            // instead of a cluster barrier (any co-resident CTAs, no GPC placement)
   int rot;                 // two-query-tile kernel: rotate each segment's key tiles (Seg::shift)
+  int fin_whole;           // refresh kernel: items one CTA finishes apply the MergeFinal in its
+                           // epilogue; the merge kernel then finishes split items only
   __device__ __forceinline__ void resolve() {
     if (prefix != nullptr) T = prefix[items];
   }
@@ -936,6 +938,20 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         c1 *= w_own * inv_z;
         lse = mmax + logf(z);
       }
+      // whole item with a fused final merge (fin_whole): this row's partial
+      // (v below, lse) is merged with (o2, l2) here and written as the output,
+      // the same arithmetic as final_merge_row
+      const bool fw = !CL && sc.fin_whole && whole && live;
+      float f_wp = 0.f, f_w2 = 0.f, f_iz = 0.f;
+      if (fw) {
+        const float l2 = fin.l2 ? fin.l2[orow] : -INFINITY;
+        const float m = fmaxf(lse, l2);
+        const bool flive = m != -INFINITY;
+        f_wp = (flive && lse != -INFINITY) ? __expf(lse - m) : 0.f;
+        f_w2 = (flive && l2 != -INFINITY) ? __expf(l2 - m) : 0.f;
+        f_iz = flive ? 1.f / (f_wp + f_w2) : 0.f;
+        if (!flive && wg == 1 && fin.empty_rows) atomicAdd(fin.empty_rows, 1);
+      }
       ptx::mbar_wait(&bar->o_full, seg & 1);
       ptx::tc_fence_after();
       if (row == 0 && wg == 0 && seg == 0) stamp(5);
@@ -970,6 +986,42 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(brow + ((j ^ (row & 7)) << 4)) =
                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else if (fw) {
+            if (!fin.skip_partial) ptx::st_row32(dst + c * 32, v);
+            float o2[32];
+            if (f_w2 != 0.f) {
+              if (fin.o2_bf16) {
+                const uint4* src = reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const __nv_bfloat16*>(fin.o2) + orow * D + c * 32);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const uint4 u = __ldg(src + j);
+                  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    o2[8 * j + 2 * k] = ptx::bf16_lo(w[k]);
+                    o2[8 * j + 2 * k + 1] = ptx::bf16_hi(w[k]);
+                  }
+                }
+              } else {
+                const float4* src = reinterpret_cast<const float4*>(
+                    reinterpret_cast<const float*>(fin.o2) + orow * D + c * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float4 x = __ldg(src + j);
+                  o2[4 * j] = x.x; o2[4 * j + 1] = x.y; o2[4 * j + 2] = x.z; o2[4 * j + 3] = x.w;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o2[i] = 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = (__fmul_rn(f_wp, v[i]) + __fmul_rn(f_w2, o2[i])) * f_iz;
+            if (fin.out_bf16)
+              ptx::st_row32_bf16(reinterpret_cast<__nv_bfloat16*>(fin.out) + orow * D + c * 32, v);
+            else
+              ptx::st_row32(reinterpret_cast<float*>(fin.out) + orow * D + c * 32, v);
           } else if (sc.o_bf16 && (whole || owner)) {  // final row into a bf16 partial
             ptx::st_row32_bf16(reinterpret_cast<__nv_bfloat16*>(o_out) + orow * D + c * 32, v);
           } else {
@@ -985,7 +1037,7 @@ refresh_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (wg == 0 && row == 0) flag_signal(flags + blockIdx.x, 1ull);
       }
-      if (!CL && (whole || owner) && live && wg == 1) lse_out[orow] = lse;
+      if (!CL && (whole || owner) && live && wg == 1 && !(fw && fin.skip_partial)) lse_out[orow] = lse;
       if (row == 0 && wg == 0) stamp(2 + 2 * (seg & 1));
     }
     if constexpr (CL) {
@@ -1089,6 +1141,7 @@ __device__ __forceinline__ void final_merge_row(const Sched& sc, int item, int r
   const int c_first = ib < ie ? sc.cta_of(ib) : 0;
   const int c_last = ib < ie ? sc.cta_of(ie - 1) : 0;
   const bool split = ib < ie && c_last > c_first;
+  if (sc.fin_whole && ib < ie && !split) return;  // finished by its CTA's epilogue
   const int c = lane * 4;  // this lane's 4 columns (D <= 128)
   const bool col = c < D;
   float lp;
@@ -2342,6 +2395,14 @@ static int k1_cluster_mode() {
   }
   return m;
 }
+static bool k1_fin_whole_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_K1_FIN_WHOLE");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
 // grid-barrier split-K: 0 off, 1 instead of the split-merge kernel (default),
 // 2 also instead of the in-kernel owner merge (FB_K1_GBAR / fb_debug_set_k1_gbar)
 static int g_gbar_override = -1;
@@ -2612,6 +2673,13 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
     if (fin != nullptr) {
       need_merge = true;
       flags = nullptr;
+      // items one CTA finishes apply the final merge in their epilogue (the
+      // merge kernel then only finishes split items): the C5 large-block
+      // cached step wrote / re-read every row's fp32 partial (FB_K1_FIN_WHOLE=0: off)
+      if (k1_fin_whole_enabled()) {
+        sc.fin_whole = 1;
+        kfin = *fin;
+      }
     }
     // cluster split-K instead of the merge kernel: the largest cluster that
     // gives every item its own cluster in one wave, >= 2 tiles per CTA.  Auto
