@@ -527,6 +527,7 @@ FB_API int64_t fb_debug_pair_launches(void) { return (int64_t)pair_launches(); }
 FB_API void fb_debug_set_quad(int m) { set_quad_mode(m); }
 FB_API int64_t fb_debug_quad_launches(void) { return (int64_t)quad_launches(); }
 FB_API void fb_debug_set_k1_cluster(int m) { set_k1_cluster_mode(m); }
+FB_API void fb_debug_set_k1_fin_whole(int m) { set_k1_fin_whole(m); }
 FB_API void fb_debug_set_gather_atoms(int m) { set_gather_atoms(m); }
 FB_API void fb_debug_set_k1_gbar(int m) { set_k1_gbar_mode(m); }
 FB_API int64_t fb_debug_k1_cluster_launches(void) { return (int64_t)k1_cluster_launches(); }

@@ -85,6 +85,7 @@ long long pair_launches();       // CTA-pair K1 launches so far (diagnostics)
 void set_quad_mode(int m);        // two-query-tile K1: -1 default (causal), 0 off, 1 all shapes
 long long quad_launches();
 void set_k1_cluster_mode(int m);  // cluster split-K K1: -1 default (auto), 0 off, 1 whenever feasible
+void set_k1_fin_whole(int m);    // K1 epilogue final merge for whole items: -1 environment (default on), 0 off, 1 on
 long long k1_cluster_launches();
 void set_gather_atoms(int m);     // K7 / K8 atom layout: -1 default (on), 0 off, 1 on
 void set_k1_gbar_mode(int m);     // grid-barrier split-K: -1 default, 0 off, 1 vs merge kernel, 2 also vs owner merge

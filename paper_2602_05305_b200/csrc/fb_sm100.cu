@@ -2395,7 +2395,10 @@ static int k1_cluster_mode() {
   }
   return m;
 }
+static int g_fin_whole_override = -1;
+void set_k1_fin_whole(int m) { g_fin_whole_override = m; }
 static bool k1_fin_whole_enabled() {
+  if (g_fin_whole_override >= 0) return g_fin_whole_override == 1;
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("FB_K1_FIN_WHOLE");

@@ -118,3 +118,31 @@ def test_quad_large_block_cached_step_and_determinism(lib):
     x2, y2 = K.attention_partial(q, k, v)
     lib.fb_debug_set_quad(-1)
     assert torch.equal(x1, x2) and torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("out_bf16", [True, False])
+def test_large_block_final_merge_in_epilogue_is_bitwise_equal(out_bf16):
+    """C5-style large-block cached step: items one CTA finishes apply the final
+    merge with the cached partial in K1's epilogue (fin_whole) -- bitwise the
+    same result as the split-merge kernel doing it for every item."""
+    import ctypes
+
+    from paper_2602_05305_b200 import _lib
+    from paper_2602_05305_b200 import kernels as K
+
+    lib = _lib.load()
+    lib.fb_debug_set_k1_fin_whole.argtypes = [ctypes.c_int]
+    g = torch.Generator(device="cuda").manual_seed(77)
+    H, B, D = 12, 2048, 128  # 192 items of 16 tiles over 148 CTAs: two thirds whole, one third split
+    r = lambda *s: torch.randn(s, device="cuda", generator=g).to(torch.bfloat16)
+    q, ki, vi, oe = r(H, B, D), r(H, B, D), r(H, B, D), r(H, B, D)
+    le = torch.randn((H, B), device="cuda", generator=g)
+    odt = torch.bfloat16 if out_bf16 else torch.float32
+    res = []
+    try:
+        for mode in (0, 1):
+            lib.fb_debug_set_k1_fin_whole(mode)
+            res.append(K.internal_merge(q, ki, vi, oe, le, out_dtype=odt, ext_stable=True))
+    finally:
+        lib.fb_debug_set_k1_fin_whole(-1)
+    assert torch.equal(res[0], res[1])
