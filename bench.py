@@ -895,7 +895,7 @@ def main():
                 if line is not None and c3 is not None:
                     line["c3_split_kv"] = {k: c3[k] for k in (
                         "metric", "value", "unit", "ms_per_step", "scaling", "config", "refresh_step_ms",
-                        "refresh_ms_per_layer", "refresh_step_ms_other_exchange", "cached_steps_ms",
+                        "refresh_ms_per_layer", "refresh_step_ms_other_exchange", "exchange_used", "cached_steps_ms",
                         "exchange_bytes_sent_per_layer_per_rank",
                         "roofline", "gpu_launches")}
         if line is not None:
