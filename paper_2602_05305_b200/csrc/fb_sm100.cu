@@ -2682,6 +2682,9 @@ static int launch_refresh_d(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
       if (k1_fin_whole_enabled()) {
         sc.fin_whole = 1;
         kfin = *fin;
+        // every item whole (C5: 444 items of 37 tiles = 3 per CTA): nothing left
+        // for the merge kernel -- no launch
+        if (p.T % p.ctas == 0 && (p.T / p.ctas) % p.tpi == 0) need_merge = false;
       }
     }
     // cluster split-K instead of the merge kernel: the largest cluster that
