@@ -48,10 +48,30 @@ def _is_np(x) -> bool:
     return isinstance(x, np.ndarray)
 
 
+_CUDA_OK = None
+_DEVICES: dict[int, torch.device] = {}
+
+
 def _device():
-    if not torch.cuda.is_available():
+    global _CUDA_OK
+    if _CUDA_OK is None:
+        _CUDA_OK = torch.cuda.is_available()
+    if not _CUDA_OK:
         raise RuntimeError("paper_2602_05305_b200 needs a CUDA device (no CPU fallback)")
-    return torch.device("cuda", torch.cuda.current_device())
+    idx = torch.cuda.current_device()
+    dev = _DEVICES.get(idx)
+    if dev is None:
+        dev = _DEVICES[idx] = torch.device("cuda", idx)
+    return dev
+
+
+def _raw_stream(dev: torch.device) -> int:
+    """cudaStream_t of the current torch stream on `dev` (the cheap internal
+    query when this torch build has it)."""
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return get(dev.index)
+    return torch.cuda.current_stream(dev).cuda_stream
 
 
 def _to_dev(x, dtype=None) -> torch.Tensor:
@@ -214,8 +234,8 @@ class AttnPartial:
     # read back from (and host snapshots to detect in-place edits), so a later
     # cached step / merge does not upload them again
     def _set_mirror(self, o_dev: torch.Tensor, l_dev: torch.Tensor) -> "AttnPartial":
-        self.__dict__["_mirror"] = (o_dev, l_dev, self.out, self.lognorm, self.out.copy(),
-                                    self.lognorm.copy())
+        self.__dict__["_mirror"] = (o_dev, l_dev, self.out, self.lognorm, self.out.tobytes(),
+                                    self.lognorm.tobytes())
         return self
 
     def _device_mirror(self):
@@ -223,8 +243,9 @@ class AttnPartial:
         if m is None:
             return None
         o_dev, l_dev, out_obj, ln_obj, out_snap, ln_snap = m
+        # byte snapshots: an in-place edit (even one that keeps NaN != NaN) drops the mirror
         if self.out is not out_obj or self.lognorm is not ln_obj \
-                or not np.array_equal(self.out, out_snap) or not np.array_equal(self.lognorm, ln_snap):
+                or self.out.tobytes() != out_snap or self.lognorm.tobytes() != ln_snap:
             self.__dict__.pop("_mirror", None)
             return None
         return o_dev, l_dev
@@ -469,7 +490,7 @@ def _reuse_host(q, partial: AttnPartial, k_in, v_in, scale: float):
     K._lib.call("fb_internal_merge_host", K._lib.FB_F64 if dt == torch.float64 else K._lib.FB_F32,
                 qa.ctypes.data, ka.ctypes.data, va.ctypes.data, 1, q.shape[0], q.shape[1], k_in.shape[0],
                 float(scale), o_ext.data_ptr(), l_ext.data_ptr(), out.ctypes.data, o_int.ctypes.data,
-                l_int.ctypes.data, ctypes.addressof(empty), torch.cuda.current_stream(_device()).cuda_stream)
+                l_int.ctypes.data, ctypes.addressof(empty), _raw_stream(o_ext.device))
     if empty.value > 0:
         raise DegenerateInputError("some query rows have no keys on either side")
     return out.astype(q.dtype, copy=False), AttnPartial(o_int.astype(q.dtype, copy=False), l_int)

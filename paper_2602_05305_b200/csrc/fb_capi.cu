@@ -1023,10 +1023,10 @@ int fb_internal_merge_host(int dtype, const void* q, const void* k_in, const voi
   const size_t E = dtype == FB_F64 ? sizeof(double) : sizeof(float);
   const size_t rows = (size_t)(groups * q_rows);
   const size_t qb = rows * head_dim * E, kb = (size_t)(groups * n_in) * head_dim * E;
-  const size_t in_bytes = align_up(qb + 2 * kb, 256);
-  // device / pinned layout: [q | k_in | v_in] [out | o_int | lse_int | empty counter]
+  const size_t in_bytes = align_up(align_up(qb + 2 * kb, 16) + sizeof(int32_t), 256);
+  // device / pinned layout: [q | k_in | v_in | empty counter] [out | o_int | lse_int]
   const size_t ob = align_up(rows * head_dim * E, 256), lb = align_up(rows * sizeof(double), 256);
-  const size_t out_bytes = 2 * ob + lb + 256;
+  const size_t out_bytes = 2 * ob + lb;
   HostStage* s = nullptr;
   if (int rc = stage_reserve(in_bytes + out_bytes, in_bytes + out_bytes, s)) return rc;
   cudaStream_t st = as_stream(stream);
@@ -1037,35 +1037,34 @@ int fb_internal_merge_host(int dtype, const void* q, const void* k_in, const voi
     std::memcpy(hp + qb, k_in, kb);
     std::memcpy(hp + qb + kb, v_in, kb);
   }
+  // the empty-row counter travels with the inputs (zeroed in the same copy,
+  // no memset launch): [q | k_in | v_in | counter]
+  const size_t cnt_off = align_up(qb + 2 * kb, 16);
+  std::memset(hp + cnt_off, 0, sizeof(int32_t));
   char* d_out = dp + in_bytes;
   char* d_oi = d_out + ob;
   char* d_li = d_oi + ob;
-  int32_t* d_cnt = reinterpret_cast<int32_t*>(d_li + lb);
-  if (cudaMemcpyAsync(dp, hp, qb + 2 * kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemsetAsync(d_cnt, 0, sizeof(int32_t), st) != cudaSuccess)
+  int32_t* d_cnt = reinterpret_cast<int32_t*>(dp + cnt_off);
+  if (cudaMemcpyAsync(dp, hp, cnt_off + sizeof(int32_t), cudaMemcpyHostToDevice, st) != cudaSuccess)
     return fail(FB_ERR_CUDA, "fb_internal_merge_host: staging copy failed");
   const bool want_int = o_int != nullptr || lse_int != nullptr;
   if (int rc = fb_internal_merge_ex(dtype, dp, dp + qb, dp + qb + kb, groups, q_rows, head_dim, n_in, scale,
                                     o_ext, lse_ext, d_out, dtype, nullptr, want_int ? d_oi : nullptr,
                                     want_int ? d_li : nullptr, d_cnt, nullptr, 0, FB_EXT_STABLE, stream))
     return rc;
-  // one read-back: out, then (if wanted) o_int and lse_int, then the counter
+  // one read-back: the counter and the outputs are contiguous from cnt_off
+  // ([counter | pad | out | o_int | lse_int]); without the internal partial
+  // only [counter .. out] is copied
   char* h_out = hp + in_bytes;
-  cudaError_t e;
-  if (want_int) {
-    e = cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
-  } else {
-    e = cudaMemcpyAsync(h_out, d_out, ob, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(h_out + 2 * ob + lb, d_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-  }
+  const size_t back = (size_t)(d_out - (dp + cnt_off)) + (want_int ? 2 * ob + lb : ob);
+  cudaError_t e = cudaMemcpyAsync(hp + cnt_off, dp + cnt_off, back, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail(FB_ERR_CUDA, cudaGetErrorString(e));
   std::memcpy(out, h_out, rows * head_dim * E);
   if (o_int) std::memcpy(o_int, h_out + ob, rows * head_dim * E);
   if (lse_int) std::memcpy(lse_int, h_out + 2 * ob, rows * sizeof(double));
   int32_t cnt = 0;
-  std::memcpy(&cnt, h_out + 2 * ob + lb, sizeof(int32_t));
+  std::memcpy(&cnt, hp + cnt_off, sizeof(int32_t));
   if (empty_rows) *empty_rows = cnt;
   return FB_OK;
 }
