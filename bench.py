@@ -749,18 +749,6 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
     # layers) and the cached steps
     ms_ref = timed(refresh_step, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
     ms_cached = timed(g_cached.replay, max(2, args.steps // 2), 2) / max(2, args.steps // 2)
-    # the other exchange for comparison: peer-memory (CUDA IPC mapped partials,
-    # device flags, K3 reading in place) vs the NCCL grouped send / recv
-    other = {"nccl": "p2p", "p2p": "nccl"}[args.exchange]
-    ms_ref_other = None
-    if world > 1:
-        try:  # a set-up failure of the comparison (e.g. no CUDA IPC) must not cost the line
-            alt = SplitKVRefresh(layout=layouts[other])
-            ms_ref_other = timed(lambda: refresh_step(alt), max(2, args.steps // 2), 2) / max(2, args.steps // 2)
-            alt.close()
-        except Exception as e:  # noqa: BLE001
-            ms_ref_other = f"unavailable: {type(e).__name__}: {e}"[:200]
-
     # K1 on the local shard alone (roofline of the dominant kernel at this P)
     o_dt = torch.bfloat16 if world == 1 else torch.float32  # N=1 writes the cached partial directly
     o_s = torch.empty((groups, rows, D), device=dev, dtype=o_dt)
@@ -771,6 +759,19 @@ def run_splitkv(args, rank: int, world: int, local_rank: int):
             K.attention_partial(q[l], kc[l], vc[l], 0, n_loc, None, out=o_s, lse=l_s)
 
     ms_k1 = timed(k1_only, 2, 1) / 2 / L
+
+    # the other exchange for comparison (last: a peer-memory set-up that fails
+    # leaves every number above already measured): peer-memory (CUDA IPC mapped partials,
+    # device flags, K3 reading in place) vs the NCCL grouped send / recv
+    other = {"nccl": "p2p", "p2p": "nccl"}[args.exchange]
+    ms_ref_other = None
+    if world > 1:
+        try:  # a set-up failure of the comparison (e.g. no CUDA IPC) must not cost the line
+            alt = SplitKVRefresh(layout=layouts[other])
+            ms_ref_other = timed(lambda: refresh_step(alt), max(2, args.steps // 2), 2) / max(2, args.steps // 2)
+            alt.close()
+        except Exception as e:  # noqa: BLE001
+            ms_ref_other = f"unavailable: {type(e).__name__}: {e}"[:200]
     k1_bytes = 2 * groups * n_loc * D * 2 + groups * rows * D * 2 + groups * rows * (D * o_s.element_size() + 4)
     peak, peak_kind = _peaks()
     if rank == 0:

@@ -442,10 +442,12 @@ template <int NT, bool EXTB = false>
 __global__ void __launch_bounds__(V2_THREADS, 2)
 internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_e,
+                         const __grid_constant__ CUtensorMap tm_o,
                          const float* __restrict__ lse_ext, int q_rows, int m_tiles, int n_in,
                          float scale_log2, void* __restrict__ out, int out_bf16,
                          float* __restrict__ lse_merged, float* __restrict__ o_int,
-                         float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early) {
+                         float* __restrict__ lse_int, int* __restrict__ empty_rows, int ext_early,
+                         int tma_out) {
   using C = CfgV2<NT, EXTB>;
   constexpr int D = C::D;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -627,7 +629,17 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         val[i] = live ? (__fmul_rn(we, oc[i]) + __fmul_rn(wi, oi)) * iz : 0.f;
         r[i] = __float_as_uint(oi);
       }
-      if (live_row) {
+      if (tma_out) {
+        // bf16 row -> the dead Q tile (box wg, 128B-swizzled like the TMA
+        // load that filled it; MMA 1 finished reading it before o_full), one
+        // bulk tensor store per warpgroup below; rows past q_rows are clipped
+        unsigned char* orow = smem + C::OFF_Q + wg * C::QBOX + row * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(orow + (((cc * 4 + j) ^ (row & 7)) << 4)) =
+              make_uint4(ptx::pack_bf16(val[8 * j], val[8 * j + 1]), ptx::pack_bf16(val[8 * j + 2], val[8 * j + 3]),
+                         ptx::pack_bf16(val[8 * j + 4], val[8 * j + 5]), ptx::pack_bf16(val[8 * j + 6], val[8 * j + 7]));
+      } else if (live_row) {
         if (out_bf16) {
           __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(out) + rr * D + c * 32;
           uint32_t pk[16];
@@ -644,13 +656,22 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         } else {
           ptx::st_row32(reinterpret_cast<float*>(out) + rr * D + c * 32, val);
         }
-        if (o_int) {
-          float4* di = reinterpret_cast<float4*>(o_int + rr * D + c * 32);
+      }
+      if (live_row && o_int) {
+        float4* di = reinterpret_cast<float4*>(o_int + rr * D + c * 32);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            di[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-        }
+        for (int j = 0; j < 8; ++j)
+          di[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                              __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+      }
+    }
+    if (tma_out) {
+      ptx::fence_proxy_async_smem();
+      asm volatile("bar.sync %0, 128;" ::"r"(3 + wg) : "memory");
+      if (row == 0) {
+        ptx::tma_store_3d(&tm_o, smem + C::OFF_Q + wg * C::QBOX, wg * 64, mt * BM, g);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read();  // the tile must outlive the CTA's shared memory
       }
     }
     if (live_row && wg == 0) {
@@ -675,6 +696,11 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int dtype_bytes, int64_t in
 
 static int g_k2_v2_override = -1;
 void set_k2_v2(int v) { g_k2_v2_override = v; }
+// v2 output stores: -1 (default) / 1 one bulk tensor store per (CTA, column
+// half) from shared memory, 0 row-per-thread 256-bit global stores.  C2 b=32
+// cached step 8.62 -> 8.42 us, b=64 16.36 -> 16.21 (scripts/ab_k2_store.py)
+static int g_k2_store = -1;
+void set_k2_store(int v) { g_k2_store = v; }
 // diagnostics: FB_K2_PDL_LATE=1 signals the dependent launch after the Q/K/V loads landed
 static int k2_pdl_late() {
   static int v = -1;
@@ -747,6 +773,10 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   if ((rc = make_tmap_3d(&mk, k_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&me, o_ext, EXTB ? 2 : 4, D, q_rows, q_rows, groups, C::ECOLS, sm100k2::BM))) return rc;
+  // bf16 output through one bulk tensor store per (CTA, column half)
+  const bool tma_out = out_bf16 && g_k2_store != 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  CUtensorMap mo = me;  // unused unless tma_out
+  if (tma_out && (rc = make_tmap_3d(&mo, out, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
   auto kern = sm100k2::internal_merge_v2_kernel<NT, EXTB>;
   static bool attr = false;
   if (!attr) {
@@ -756,8 +786,9 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   const int m_tiles = (int)((q_rows + sm100k2::BM - 1) / sm100k2::BM);
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles)), dim3(sm100k2::V2_THREADS), C::SMEM, st, mq, mk,
-             mv, me, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
-             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0));
+             mv, me, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
+             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0),
+             tma_out ? 1 : 0);
   count_launch();
   return check_launch("internal_merge_v2_kernel(sm100)");
 }
