@@ -533,6 +533,7 @@ FB_API void fb_debug_set_k1_gbar(int m) { set_k1_gbar_mode(m); }
 FB_API int64_t fb_debug_k1_cluster_launches(void) { return (int64_t)k1_cluster_launches(); }
 FB_API void fb_debug_set_k2_variant(int v) { set_k2_v2(v); }
 FB_API void fb_debug_set_k2_store(int v) { set_k2_store(v); }
+FB_API void fb_debug_set_k2_vsplit(int v) { set_k2_vsplit(v); }
 FB_API void fb_debug_set_k5_mode(int m) { set_k5_mode(m); }
 FB_API int64_t fb_debug_k5_fused_launches(void) { return (int64_t)k5_fused_launches(); }
 FB_API void fb_debug_set_k2_trace(void* p, int launches) { set_k2_trace(p, launches); }

@@ -92,6 +92,7 @@ void set_k1_gbar_mode(int m);     // grid-barrier split-K: -1 default, 0 off, 1 
 void set_k2_trace(void* p, int launches);  // diagnostics: K2 v1 per-CTA stamps
 void set_k5_mode(int m);         // K5 scoring: -1 environment (default fused), 0 fused, 1 two-pass
 long long k5_fused_launches();
+void set_k2_vsplit(int v);       // K2 v2: -1 default / 1 V_in on its own barrier, 0 one Q/K/V barrier
 void set_k2_store(int v);        // K2 v2 output: -1 default (TMA store), 0 per-thread stores, 1 TMA store (diagnostics)
 void set_k2_v2(int v);           // K2 variant: -1 by size (default), 0 v1, 1 v2 (diagnostics)
 size_t refresh_sm100_workspace_bytes(int64_t groups, int64_t q_rows, int64_t head_dim, int64_t n_keys);

@@ -430,11 +430,12 @@ struct CfgV2 {
   static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;
   static constexpr uint32_t TMEM_COLS = (COL_O + D) <= 256 ? 256 : 512;
   static constexpr uint32_t TX_QKV = 2 * (QBOX + 2 * KBOX);
+  static constexpr uint32_t TX_QK = 2 * (QBOX + KBOX), TX_V = 2 * KBOX;
   static constexpr uint32_t TX_E = NE * EBOX;
 };
 
 struct BarsV2 {
-  uint64_t load_qkv, load_e, s_full, p_ready, o_full;
+  uint64_t load_qkv, load_e, s_full, p_ready, o_full, load_v;
   uint32_t tmem_base;
 };
 
@@ -469,6 +470,8 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
   // CTA's Q / K / V have landed, so the next launch's O_ext prefetch does not
   // compete with this launch's post-wait loads
   const bool pdl_late = (ext_early & 2) != 0;
+  // bit 2: V_in on its own barrier, so S = Q K^T starts once Q and K landed
+  const bool vsplit = (ext_early & 4) != 0;
   ext_early &= 1;
   float le = -INFINITY;
   if (ext_early && live_row) le = __ldg(lse_ext + rr);
@@ -482,6 +485,7 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     ptx::mbar_init(&bar->s_full, 1);
     ptx::mbar_init(&bar->p_ready, 128);
     ptx::mbar_init(&bar->o_full, 1);
+    ptx::mbar_init(&bar->load_v, 1);
     ptx::fence_barrier_init();
     if (ext_early) {  // the cached partial is final before this launch: fetch it now
       const uint64_t pol = ptx::policy_evict_first();
@@ -506,12 +510,15 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         for (int b = 0; b < C::NE; ++b)
           ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * C::ECOLS, mt * BM, g, pol);
       }
-      ptx::mbar_expect_tx(&bar->load_qkv, C::TX_QKV);
+      uint64_t* bar_v = vsplit ? &bar->load_v : &bar->load_qkv;
+      ptx::mbar_expect_tx(&bar->load_qkv, vsplit ? C::TX_QK : C::TX_QKV);
+      if (vsplit) ptx::mbar_expect_tx(bar_v, C::TX_V);
       for (int b = 0; b < 2; ++b) {
         ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
         ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
-        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, b * BOX, 0, g, pol);
       }
+      for (int b = 0; b < 2; ++b)
+        ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, bar_v, b * BOX, 0, g, pol);
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
       constexpr uint32_t IDESC_O = ptx::idesc_bf16_f32(BM, D, true);
       ptx::mbar_wait(&bar->load_qkv, 0);
@@ -527,6 +534,7 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     ptx::sdesc_sw128(k_base + (kk / 4) * C::KBOX + (kk % 4) * 32, 16, 1024),
                     IDESC_S, kk > 0);
       ptx::tc_commit(&bar->s_full);
+      if (vsplit) ptx::mbar_wait(&bar->load_v, 0);
       ptx::mbar_wait(&bar->p_ready, 0);
       ptx::tc_fence_after();
 #pragma unroll
@@ -701,6 +709,17 @@ void set_k2_v2(int v) { g_k2_v2_override = v; }
 // cached step 8.62 -> 8.42 us, b=64 16.36 -> 16.21 (scripts/ab_k2_store.py)
 static int g_k2_store = -1;
 void set_k2_store(int v) { g_k2_store = v; }
+// v2 V_in on its own load barrier (S = Q K^T issued once Q and K landed):
+// -1 (default) / 1 on, 0 one barrier for Q, K and V
+static int g_k2_vsplit = -1;
+void set_k2_vsplit(int v) { g_k2_vsplit = v; }
+// the defaults above can be overridden from the environment (A/B inside whole
+// programs such as bench.py): FB_K2_STORE=0/1, FB_K2_VSPLIT=0/1
+static int k2_env(const char* name, int v) {
+  if (v != -1) return v;
+  const char* e = getenv(name);
+  return (e != nullptr && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
+}
 // diagnostics: FB_K2_PDL_LATE=1 signals the dependent launch after the Q/K/V loads landed
 static int k2_pdl_late() {
   static int v = -1;
@@ -774,7 +793,7 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&me, o_ext, EXTB ? 2 : 4, D, q_rows, q_rows, groups, C::ECOLS, sm100k2::BM))) return rc;
   // bf16 output through one bulk tensor store per (CTA, column half)
-  const bool tma_out = out_bf16 && g_k2_store != 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const bool tma_out = out_bf16 && k2_env("FB_K2_STORE", g_k2_store) != 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   CUtensorMap mo = me;  // unused unless tma_out
   if (tma_out && (rc = make_tmap_3d(&mo, out, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
   auto kern = sm100k2::internal_merge_v2_kernel<NT, EXTB>;
@@ -787,8 +806,8 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles)), dim3(sm100k2::V2_THREADS), C::SMEM, st, mq, mk,
              mv, me, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
-             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty), (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0),
-             tma_out ? 1 : 0);
+             lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
+             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0) | (k2_env("FB_K2_VSPLIT", g_k2_vsplit) != 0 ? 4 : 0), tma_out ? 1 : 0);
   count_launch();
   return check_launch("internal_merge_v2_kernel(sm100)");
 }

@@ -1,6 +1,7 @@
 """Interleaved A/B of the cached step (K2 v2, bf16 O_ext) with the output
 written by row-per-thread 256-bit global stores (A) vs one bulk tensor store
-per (CTA, column half) from the dead Q tile (B, fb_debug_set_k2_store(1)):
+per (CTA, column half) from the dead Q tile (B, fb_debug_set_k2_store(1)),
+and with V_in on its own load barrier as well (C, fb_debug_set_k2_vsplit(1)):
 graph of 36 layers x 31 cached steps at the C2 shapes.
     python scripts/ab_k2_store.py [batch ...]"""
 import ctypes as C, math, os, sys, torch
@@ -22,13 +23,15 @@ for b in [int(x) for x in sys.argv[1:]] or [32]:
     vs = [r(groups, BLK, D) for _ in range(L)]
     oeb = [r(groups, rows, D) for _ in range(L)]
     le = [torch.randn((groups, rows), device="cuda", generator=g) for _ in range(L)]
-    VARS = {"A": 0, "B": 1}
+    # (store, vsplit): A the previous kernel, B TMA store, C TMA store + V on its own barrier
+    VARS = {"A": (0, 0), "B": (1, 0), "C": (1, 1)}
     out = {n: [torch.empty((groups, rows, D), device="cuda", dtype=torch.bfloat16) for _ in range(L)] for n in VARS}
     s = torch.cuda.Stream()
     graphs = {}
     lib.fb_debug_set_k2_variant(1)
     for n in VARS:
-        lib.fb_debug_set_k2_store(VARS[n])
+        lib.fb_debug_set_k2_store(VARS[n][0])
+        lib.fb_debug_set_k2_vsplit(VARS[n][1])
         def fn(n=n):
             for _ in range(31):
                 for i in range(L):
@@ -43,6 +46,7 @@ for b in [int(x) for x in sys.argv[1:]] or [32]:
                 fn()
         graphs[n] = gr
     lib.fb_debug_set_k2_store(-1)
+    lib.fb_debug_set_k2_vsplit(-1)
     lib.fb_debug_set_k2_variant(-1)
     res = {}
     for rnd in range(10):
@@ -51,10 +55,10 @@ for b in [int(x) for x in sys.argv[1:]] or [32]:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); graphs[n].replay(); e1.record(); torch.cuda.synchronize()
             res.setdefault(n, []).append(e0.elapsed_time(e1) / (31 * L) * 1000)
-    eq = all(torch.equal(out["A"][i], out["B"][i]) for i in range(L))
+    eq = all(torch.equal(out["A"][i], out[n][i]) for n in VARS for i in range(L))
     byts = L and (groups * rows * D * 2 * 3 + 2 * groups * BLK * D * 2 + groups * rows * 4)
     for n in VARS:
         v = sorted(res[n])
-        print(f"b={b} store={'tma' if VARS[n] else 'per-thread'}: K2 per launch us min {v[0]:.2f} med {v[len(v)//2]:.2f}"
+        print(f"b={b} store={'tma' if VARS[n][0] else 'per-thread'} vsplit={VARS[n][1]}: K2 per launch us min {v[0]:.2f} med {v[len(v)//2]:.2f}"
               f"  ({byts / (v[len(v)//2] * 1e-6) / 1e9:.0f} GB/s)")
     print(f"b={b} outputs bitwise equal: {eq}")

@@ -1,7 +1,8 @@
 """K2 v2 (cached step, attention_with_reuse: attention.py:295-321) with the bf16
 output written by one bulk tensor store per (CTA, column half) from the dead Q
 tile (fb_debug_set_k2_store(1)) is bitwise equal to the row-per-thread global
-stores -- same arithmetic, only the store path differs -- including query
+stores -- same arithmetic, only the store path differs -- and so is issuing
+S = Q K^T before V_in landed (fb_debug_set_k2_vsplit(1)); including query
 tiles clipped at q_rows, rows with an empty external partial, and the fp32
 and bf16 cached-partial layouts."""
 import math
@@ -33,8 +34,9 @@ def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb):
     outs, lses = {}, {}
     lib.fb_debug_set_k2_variant(1)
     try:
-        for mode in (0, 1):
-            lib.fb_debug_set_k2_store(mode)
+        for mode in (0, 1, 2):  # per-thread stores / TMA store / TMA store + V on its own barrier
+            lib.fb_debug_set_k2_store(min(mode, 1))
+            lib.fb_debug_set_k2_vsplit(1 if mode == 2 else 0)
             o = torch.full((groups, q_rows, 128), 3.0, device="cuda", dtype=torch.bfloat16)
             K.internal_merge(q, ki, vi, oe, le, out_dtype=torch.bfloat16, out=o, ext_stable=True)
             outs[mode] = o
@@ -43,7 +45,9 @@ def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb):
         torch.cuda.synchronize()
     finally:
         lib.fb_debug_set_k2_store(-1)
+        lib.fb_debug_set_k2_vsplit(-1)
         lib.fb_debug_set_k2_variant(-1)
-    assert torch.equal(outs[0], outs[1])
-    a, b = outs[0, "lse"], outs[1, "lse"]
-    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    for mode in (1, 2):
+        assert torch.equal(outs[0], outs[mode])
+        a, b = outs[0, "lse"], outs[mode, "lse"]
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
