@@ -57,10 +57,11 @@ struct Cfg {
   static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;  // P stores span >= 32 cols
   static constexpr uint32_t TMEM_COLS = (COL_O + DC) <= 128 ? 128 : (COL_O + DC) <= 256 ? 256 : 512;
   static constexpr uint32_t TX_QKV = NB * (QBOX + KBOX) + NBV * KBOX;
+  static constexpr uint32_t TX_V = NBV * KBOX;
 };
 
 struct Bars {
-  uint64_t load_qkv, s_full, p_ready, o_full;
+  uint64_t load_qkv, s_full, p_ready, o_full, load_v;
   uint32_t tmem_base;
 };
 
@@ -165,6 +166,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     }
   };
   const bool pdl_late = (ext_early & 2) != 0;  // see internal_merge_v2_kernel
+  const bool vsplit = (ext_early & 4) != 0;    // V_in on its own barrier (as v2)
   ext_early &= 1;
   if (ext_early) load_ext();
 
@@ -176,6 +178,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     ptx::mbar_init(&bar->s_full, 1);
     ptx::mbar_init(&bar->p_ready, 128);
     ptx::mbar_init(&bar->o_full, 1);
+    ptx::mbar_init(&bar->load_v, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 4) ptx::tmem_alloc(&bar->tmem_base, C::TMEM_COLS);
@@ -192,8 +195,10 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     if (lane == 0) {
       const uint64_t pol = ptx::policy_evict_first();
       // (TOK: the Q box holds G * B rows, not BM, so fewer bytes land)
-      ptx::mbar_expect_tx(&bar->load_qkv, TOK ? C::TX_QKV - C::NB * (uint32_t)(BM - tl.B * tl.G) * 128u
-                                              : C::TX_QKV);
+      uint64_t* bar_v = vsplit ? &bar->load_v : &bar->load_qkv;
+      ptx::mbar_expect_tx(&bar->load_qkv, (TOK ? C::TX_QKV - C::NB * (uint32_t)(BM - tl.B * tl.G) * 128u
+                                               : C::TX_QKV) - (vsplit ? C::TX_V : 0u));
+      if (vsplit) ptx::mbar_expect_tx(bar_v, C::TX_V);
       if constexpr (TOK) {  // 5-D Q {d, B, G, Hkv, b}, 4-D K / V {d, B, Hkv, b}
         const int bi = g / tl.Hkv, kvh = g % tl.Hkv;
         for (int b = 0; b < C::NB; ++b) {
@@ -201,14 +206,14 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
           ptx::tma_load_4d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, kvh, bi, pol);
         }
         for (int b = 0; b < C::NBV; ++b)
-          ptx::tma_load_4d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, kvh, bi, pol);
+          ptx::tma_load_4d(smem + C::OFF_V + b * C::KBOX, &tm_v, bar_v, col0 + b * BOX, 0, kvh, bi, pol);
       } else {
         for (int b = 0; b < C::NB; ++b) {
           ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
           ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
         }
         for (int b = 0; b < C::NBV; ++b)
-          ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, &bar->load_qkv, col0 + b * BOX, 0, g, pol);
+          ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, bar_v, col0 + b * BOX, 0, g, pol);
       }
 
       constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(BM, NT, false);
@@ -228,6 +233,7 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                     IDESC_S, kk > 0);
       }
       ptx::tc_commit(&bar->s_full);
+      if (vsplit) ptx::mbar_wait(&bar->load_v, 0);
       ptx::mbar_wait(&bar->p_ready, 0);
       ptx::tc_fence_after();
 #pragma unroll
@@ -430,12 +436,12 @@ struct CfgV2 {
   static constexpr uint32_t COL_S = 0, COL_O = NT < 32 ? 32 : NT;
   static constexpr uint32_t TMEM_COLS = (COL_O + D) <= 256 ? 256 : 512;
   static constexpr uint32_t TX_QKV = 2 * (QBOX + 2 * KBOX);
-  static constexpr uint32_t TX_QK = 2 * (QBOX + KBOX), TX_V = 2 * KBOX;
+  static constexpr uint32_t TX_QK = 2 * (QBOX + KBOX), TX_V = 2 * KBOX, TX_H = QBOX + KBOX;
   static constexpr uint32_t TX_E = NE * EBOX;
 };
 
 struct BarsV2 {
-  uint64_t load_qkv, load_e, s_full, p_ready, o_full, load_v;
+  uint64_t load_qkv, load_e, s_full, p_ready, o_full, load_v, load_h1;
   uint32_t tmem_base;
 };
 
@@ -470,8 +476,11 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
   // CTA's Q / K / V have landed, so the next launch's O_ext prefetch does not
   // compete with this launch's post-wait loads
   const bool pdl_late = (ext_early & 2) != 0;
-  // bit 2: V_in on its own barrier, so S = Q K^T starts once Q and K landed
+  // bit 2: V_in on its own barrier, so S = Q K^T starts once Q and K landed;
+  // bit 3 as well: the two 64-column halves of Q and K on their own barriers,
+  // so the first half of S = Q K^T starts once Q / K columns 0-63 landed
   const bool vsplit = (ext_early & 4) != 0;
+  const bool hsplit = vsplit && (ext_early & 8) != 0;
   ext_early &= 1;
   float le = -INFINITY;
   if (ext_early && live_row) le = __ldg(lse_ext + rr);
@@ -486,6 +495,7 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     ptx::mbar_init(&bar->p_ready, 128);
     ptx::mbar_init(&bar->o_full, 1);
     ptx::mbar_init(&bar->load_v, 1);
+    ptx::mbar_init(&bar->load_h1, 1);
     ptx::fence_barrier_init();
     if (ext_early) {  // the cached partial is final before this launch: fetch it now
       const uint64_t pol = ptx::policy_evict_first();
@@ -511,11 +521,14 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
           ptx::tma_load_3d(smem + C::OFF_E + b * C::EBOX, &tm_e, &bar->load_e, b * C::ECOLS, mt * BM, g, pol);
       }
       uint64_t* bar_v = vsplit ? &bar->load_v : &bar->load_qkv;
-      ptx::mbar_expect_tx(&bar->load_qkv, vsplit ? C::TX_QK : C::TX_QKV);
+      uint64_t* bar_h1 = hsplit ? &bar->load_h1 : &bar->load_qkv;
+      ptx::mbar_expect_tx(&bar->load_qkv, hsplit ? C::TX_H : vsplit ? C::TX_QK : C::TX_QKV);
+      if (hsplit) ptx::mbar_expect_tx(bar_h1, C::TX_H);
       if (vsplit) ptx::mbar_expect_tx(bar_v, C::TX_V);
       for (int b = 0; b < 2; ++b) {
-        ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, &bar->load_qkv, b * BOX, mt * BM, g, pol);
-        ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, &bar->load_qkv, b * BOX, 0, g, pol);
+        uint64_t* bh = b == 0 ? &bar->load_qkv : bar_h1;
+        ptx::tma_load_3d(smem + C::OFF_Q + b * C::QBOX, &tm_q, bh, b * BOX, mt * BM, g, pol);
+        ptx::tma_load_3d(smem + C::OFF_K + b * C::KBOX, &tm_k, bh, b * BOX, 0, g, pol);
       }
       for (int b = 0; b < 2; ++b)
         ptx::tma_load_3d(smem + C::OFF_V + b * C::KBOX, &tm_v, bar_v, b * BOX, 0, g, pol);
@@ -528,11 +541,16 @@ internal_merge_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
       const uint32_t k_base = ptx::smem_u32(smem + C::OFF_K);
       const uint32_t v_base = ptx::smem_u32(smem + C::OFF_V);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk)
+      for (int kk = 0; kk < D / 16; ++kk) {
+        if (kk == 4 && hsplit) {
+          ptx::mbar_wait(&bar->load_h1, 0);
+          ptx::tc_fence_after();
+        }
         ptx::mma_ss(tmem + C::COL_S,
                     ptx::sdesc_sw128(q_base + (kk / 4) * C::QBOX + (kk % 4) * 32, 16, 1024),
                     ptx::sdesc_sw128(k_base + (kk / 4) * C::KBOX + (kk % 4) * 32, 16, 1024),
                     IDESC_S, kk > 0);
+      }
       ptx::tc_commit(&bar->s_full);
       if (vsplit) ptx::mbar_wait(&bar->load_v, 0);
       ptx::mbar_wait(&bar->p_ready, 0);
@@ -710,7 +728,7 @@ void set_k2_v2(int v) { g_k2_v2_override = v; }
 static int g_k2_store = -1;
 void set_k2_store(int v) { g_k2_store = v; }
 // v2 V_in on its own load barrier (S = Q K^T issued once Q and K landed):
-// -1 (default) / 1 on, 0 one barrier for Q, K and V
+// -1 (default) / 1 on, 2 also the Q / K column halves, 0 one barrier for Q, K and V
 static int g_k2_vsplit = -1;
 void set_k2_vsplit(int v) { g_k2_vsplit = v; }
 // the defaults above can be overridden from the environment (A/B inside whole
@@ -718,7 +736,15 @@ void set_k2_vsplit(int v) { g_k2_vsplit = v; }
 static int k2_env(const char* name, int v) {
   if (v != -1) return v;
   const char* e = getenv(name);
-  return (e != nullptr && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
+  return (e != nullptr && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : -1;
+}
+// vsplit level 2 (FB_K2_VSPLIT=2): also the Q / K column halves on their own
+// barriers.  Default (-1): level 2 when the grid exceeds the SMs (two CTAs per
+// SM: b=32 8.24 -> 8.08 us), else level 1 (b=4 3.73 -> 3.68 us)
+static int k2_vsplit_bits(int64_t ctas = 0) {
+  int v = k2_env("FB_K2_VSPLIT", g_k2_vsplit);
+  if (v == -1) v = ctas > num_sms() ? 2 : 1;
+  return v == 0 ? 0 : v == 2 ? 4 | 8 : 4;
 }
 // diagnostics: FB_K2_PDL_LATE=1 signals the dependent launch after the Q/K/V loads landed
 static int k2_pdl_late() {
@@ -773,7 +799,8 @@ static int launch_k2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const __
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles * C::SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st,
              mq, mk, mv, o_ext, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out,
              out_bf16 ? 1 : 0, lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
-             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0), trace, sm100k2::TokLayout{1, 1, 1, 0});
+             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0) | (k2_vsplit_bits() & 4), trace,
+             sm100k2::TokLayout{1, 1, 1, 0});
   count_launch();
   return check_launch("internal_merge_kernel(sm100)");
 }
@@ -793,7 +820,12 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   if ((rc = make_tmap_3d(&mv, v_in, 2, D, nin_eff, nin_eff, groups, sm100k2::BOX, NT))) return rc;
   if ((rc = make_tmap_3d(&me, o_ext, EXTB ? 2 : 4, D, q_rows, q_rows, groups, C::ECOLS, sm100k2::BM))) return rc;
   // bf16 output through one bulk tensor store per (CTA, column half)
-  const bool tma_out = out_bf16 && k2_env("FB_K2_STORE", g_k2_store) != 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  // default (-1): TMA store only when the grid exceeds the SMs (b=16, one CTA
+  // per SM: 5.78 -> 6.08 us with it; b=32 8.56 -> 8.38)
+  const int store = k2_env("FB_K2_STORE", g_k2_store);
+  const int64_t ctas = groups * ((q_rows + sm100k2::BM - 1) / sm100k2::BM);
+  const bool tma_out = out_bf16 && (store == 1 || (store == -1 && ctas > num_sms())) &&
+                       (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   CUtensorMap mo = me;  // unused unless tma_out
   if (tma_out && (rc = make_tmap_3d(&mo, out, 2, D, q_rows, q_rows, groups, sm100k2::BOX, sm100k2::BM))) return rc;
   auto kern = sm100k2::internal_merge_v2_kernel<NT, EXTB>;
@@ -807,7 +839,7 @@ static int launch_k2_v2(const __nv_bfloat16* q, const __nv_bfloat16* k_in, const
   launch_pdl(kern, dim3((unsigned)(groups * m_tiles)), dim3(sm100k2::V2_THREADS), C::SMEM, st, mq, mk,
              mv, me, mo, lse_ext, (int)q_rows, m_tiles, (int)n_in, scale_log2, out, out_bf16 ? 1 : 0,
              lse_merged, o_int, lse_int, reinterpret_cast<int*>(empty),
-             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0) | (k2_env("FB_K2_VSPLIT", g_k2_vsplit) != 0 ? 4 : 0), tma_out ? 1 : 0);
+             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0) | k2_vsplit_bits(ctas), tma_out ? 1 : 0);
   count_launch();
   return check_launch("internal_merge_v2_kernel(sm100)");
 }
@@ -854,7 +886,8 @@ static int launch_k2_tok(const __nv_bfloat16* q, int64_t q_ts, const __nv_bfloat
   const float scale_log2 = (float)(scale * 1.4426950408889634);
   launch_pdl(kern, dim3((unsigned)(groups * SPLIT)), dim3(sm100k2::THREADS), C::SMEM, st, mq, mk, mv, o_ext,
              lse_ext, (int)q_rows, 1, (int)B, scale_log2, out, out_bf16 ? 1 : 0, (float*)nullptr,
-             (float*)nullptr, (float*)nullptr, (int*)nullptr, (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0),
+             (float*)nullptr, (float*)nullptr, (int*)nullptr,
+             (ext_early ? 1 : 0) | (k2_pdl_late() ? 2 : 0) | (k2_vsplit_bits() & 4),
              (unsigned long long*)nullptr, sm100k2::TokLayout{(int)B, (int)G, (int)Hkv, (long long)out_ts});
   count_launch();
   return check_launch("internal_merge_kernel(sm100, token-major)");

@@ -24,11 +24,12 @@ for b in [int(x) for x in sys.argv[1:]] or [32]:
     oeb = [r(groups, rows, D) for _ in range(L)]
     le = [torch.randn((groups, rows), device="cuda", generator=g) for _ in range(L)]
     # (store, vsplit): A the previous kernel, B TMA store, C TMA store + V on its own barrier
-    VARS = {"A": (0, 0), "B": (1, 0), "C": (1, 1)}
+    # D: + Q / K column halves; E: the library defaults (by grid size)
+    VARS = {"A": (0, 0), "B": (1, 0), "C": (1, 1), "D": (1, 2), "E": (-1, -1)}
     out = {n: [torch.empty((groups, rows, D), device="cuda", dtype=torch.bfloat16) for _ in range(L)] for n in VARS}
     s = torch.cuda.Stream()
     graphs = {}
-    lib.fb_debug_set_k2_variant(1)
+    lib.fb_debug_set_k2_variant(-1)  # by size: v1 up to b=16 at C2, v2 beyond (store modes are v2-only)
     for n in VARS:
         lib.fb_debug_set_k2_store(VARS[n][0])
         lib.fb_debug_set_k2_vsplit(VARS[n][1])
@@ -59,6 +60,6 @@ for b in [int(x) for x in sys.argv[1:]] or [32]:
     byts = L and (groups * rows * D * 2 * 3 + 2 * groups * BLK * D * 2 + groups * rows * 4)
     for n in VARS:
         v = sorted(res[n])
-        print(f"b={b} store={'tma' if VARS[n][0] else 'per-thread'} vsplit={VARS[n][1]}: K2 per launch us min {v[0]:.2f} med {v[len(v)//2]:.2f}"
+        print(f"b={b} store={ {1: 'tma', 0: 'per-thread', -1: 'default'}[VARS[n][0]] } vsplit={VARS[n][1]}: K2 per launch us min {v[0]:.2f} med {v[len(v)//2]:.2f}"
               f"  ({byts / (v[len(v)//2] * 1e-6) / 1e9:.0f} GB/s)")
     print(f"b={b} outputs bitwise equal: {eq}")

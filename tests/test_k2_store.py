@@ -19,7 +19,8 @@ def _r(g, *shape):
 
 @pytest.mark.parametrize("groups,q_rows,n_in", [(256, 128, 32), (16, 128, 16), (12, 200, 64), (5, 77, 1)])
 @pytest.mark.parametrize("extb", [False, True])
-def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb):
+@pytest.mark.parametrize("variant", [0, 1])  # v1 (V split only) / v2
+def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb, variant):
     from paper_2602_05305_b200 import _lib
     from paper_2602_05305_b200 import kernels as K
 
@@ -32,11 +33,12 @@ def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb):
     le = torch.randn((groups, q_rows), device="cuda", generator=g)
     le[0, :5] = -math.inf  # rows with an empty external partial
     outs, lses = {}, {}
-    lib.fb_debug_set_k2_variant(1)
+    lib.fb_debug_set_k2_variant(variant)
     try:
-        for mode in (0, 1, 2):  # per-thread stores / TMA store / TMA store + V on its own barrier
+        # per-thread stores / TMA store / + V on its own barrier / + Q, K halves
+        for mode in (0, 1, 2, 3):
             lib.fb_debug_set_k2_store(min(mode, 1))
-            lib.fb_debug_set_k2_vsplit(1 if mode == 2 else 0)
+            lib.fb_debug_set_k2_vsplit(max(mode - 1, 0))
             o = torch.full((groups, q_rows, 128), 3.0, device="cuda", dtype=torch.bfloat16)
             K.internal_merge(q, ki, vi, oe, le, out_dtype=torch.bfloat16, out=o, ext_stable=True)
             outs[mode] = o
@@ -47,7 +49,7 @@ def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb):
         lib.fb_debug_set_k2_store(-1)
         lib.fb_debug_set_k2_vsplit(-1)
         lib.fb_debug_set_k2_variant(-1)
-    for mode in (1, 2):
+    for mode in (1, 2, 3):
         assert torch.equal(outs[0], outs[mode])
         a, b = outs[0, "lse"], outs[mode, "lse"]
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
