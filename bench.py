@@ -268,12 +268,33 @@ def _sched_names(per_step: int = UNMASK_PER_STEP, tau: int = TAU):
     return [d.value for d in refresh_schedule(ReuseConfig(tau=tau), BLK, STEPS_PER_BLOCK, per_step)]
 
 
-def _cpu_sample_text(kind, t, sched, reps):
+_BLAS_LIMITS = None
+
+
+def _blas_threads() -> int:
+    """Give the host BLAS every core (torchrun sets OMP_NUM_THREADS=1 per rank,
+    and numpy may already be loaded, so the environment alone is not enough)
+    and return the thread count its pool actually uses -- the `cores` the CPU
+    legs report."""
+    global _BLAS_LIMITS
+    import numpy  # noqa: F401  (loads the BLAS whose pool is set below)
+
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+
+        _BLAS_LIMITS = threadpool_limits(limits=os.cpu_count(), user_api="blas")
+        n = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:  # noqa: BLE001 (threadpoolctl missing: report what was asked for)
+        return os.cpu_count() or 1
+
+
+def _cpu_sample_text(kind, t, sched, reps, cores=None):
     n_ref = sum(1 for d in sched if d == "Recompute")
     return (f"1 layer x {HKV} kv-heads (G={HQ // HKV} stacked -> {(HQ // HKV) * BLK} fp32 rows, d={D}) "
             f"x one {STEPS_PER_BLOCK}-step block ({n_ref} refresh over {CTX} keys via attention_streamed + "
             f"merge_partials, {STEPS_PER_BLOCK - n_ref} attention_with_reuse), b=1, tile 512, best of {reps}: "
-            f"{t:.3f} s; extrapolated x{LAYERS} layers (batch cancels); {kind} on {os.cpu_count()} host "
+            f"{t:.3f} s; extrapolated x{LAYERS} layers (batch cancels); {kind} on {cores or os.cpu_count()} host "
             f"threads ({cpu_model()})")
 
 
@@ -283,6 +304,7 @@ def run_reference_arm(args, rank: int, world: int):
     threads = str(os.cpu_count())
     for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ.setdefault(var, threads)
+    cores = _blas_threads()
     sched = _sched_names()
     for _ in range(args.warmup):
         cpu_layer_block(CTX, sched, reps=1)
@@ -303,9 +325,9 @@ def run_reference_arm(args, rank: int, world: int):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
         "data": "synthetic N(0,1), seeded",
         "config": _config(args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "cpu_model": cpu_model(),
-                         "sample": _cpu_sample_text(kind, statistics.median(times), sched, 1),
+                         "sample": _cpu_sample_text(kind, statistics.median(times), sched, 1, cores),
                          "extrapolation": f"x{LAYERS} layers (measured: a whole layer-block at b=1)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "measured_s_per_step": statistics.median(times),
@@ -523,10 +545,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and world == 1 and not args.no_cpu:
         for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
             os.environ.setdefault(var, str(os.cpu_count()))
+        cores = _blas_threads()
         names = _sched_names()
         kind, t_lb = cpu_layer_block(CTX, names, reps=2)
-        cpu = {"value": cpu_tokens_per_s(t_lb), "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
-               "cpu_model": cpu_model(), "sample": _cpu_sample_text(kind, t_lb, names, 2),
+        cpu = {"value": cpu_tokens_per_s(t_lb), "unit": UNIT, "cores": cores, "kind": kind,
+               "cpu_model": cpu_model(), "sample": _cpu_sample_text(kind, t_lb, names, 2, cores),
                "extrapolation": f"x{LAYERS} layers (measured: a whole layer-block at b=1)"}
 
     if rank == 0:

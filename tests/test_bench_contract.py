@@ -30,3 +30,22 @@ def test_reference_arm_line_contract():
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0 \
         and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("C2")
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "flashblock")),
+                    reason="reference not installed at baseline/_ref")
+def test_reference_arm_under_torchrun_prints_one_line_with_all_blas_threads():
+    """The driver launches the reference arm like ours (torchrun for N > 1):
+    rank 0 alone runs and prints, the other rank exits 0 without work, and the
+    BLAS pool gets every core although torchrun sets OMP_NUM_THREADS=1."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29517",
+                        os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["cores"] == os.cpu_count()
