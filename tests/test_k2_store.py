@@ -53,3 +53,34 @@ def test_k2_tma_store_is_bitwise_equal(groups, q_rows, n_in, extb, variant):
         assert torch.equal(outs[0], outs[mode])
         a, b = outs[0, "lse"], outs[mode, "lse"]
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("groups,q_rows", [(160, 77), (150, 200)])
+def test_k2_tma_store_writes_nothing_past_the_output(groups, q_rows):
+    """The bulk tensor store clips query tiles at q_rows: a sentinel tail right
+    after the output (same allocation) stays untouched, and so do the rows of
+    other groups (every row is written exactly once with its own value)."""
+    from paper_2602_05305_b200 import _lib
+    from paper_2602_05305_b200 import kernels as K
+
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(groups + q_rows)
+    n_in = 32
+    q, ki, vi = _r(g, groups, q_rows, 128), _r(g, groups, n_in, 128), _r(g, groups, n_in, 128)
+    oe = _r(g, groups, q_rows, 128)
+    le = torch.randn((groups, q_rows), device="cuda", generator=g)
+    n = groups * q_rows * 128
+    lib.fb_debug_set_k2_variant(1)
+    try:
+        lib.fb_debug_set_k2_store(0)  # reference: row-per-thread stores
+        ref = K.internal_merge(q, ki, vi, oe, le, out_dtype=torch.bfloat16, ext_stable=True)
+        lib.fb_debug_set_k2_store(1)
+        buf = torch.full((n + 64 * 128,), 7.0, device="cuda", dtype=torch.bfloat16)
+        K.internal_merge(q, ki, vi, oe, le, out_dtype=torch.bfloat16, out=buf[:n].view(groups, q_rows, 128),
+                         ext_stable=True)
+        torch.cuda.synchronize()
+    finally:
+        lib.fb_debug_set_k2_store(-1)
+        lib.fb_debug_set_k2_variant(-1)
+    assert bool((buf[n:] == 7.0).all())
+    assert torch.equal(buf[:n].view(groups, q_rows, 128), ref)
