@@ -412,7 +412,11 @@ internal_merge_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 // prefetching while this one computes.  288 threads: warps 0-3 and 4-7 run the
 // merge epilogue on output columns 0-63 / 64-127 of the same rows (TMEM lane
 // quarter = warp % 4); warps 0-3 also run the softmax; warp 8 allocates TMEM,
-// issues the TMA loads and the two MMAs.
+// issues the TMA loads and the two MMAs.  Loads land on up to three
+// barriers (Q / K columns 0-63, columns 64-127, V_in), so S = Q K^T starts on
+// the first half while the rest is in flight; when the grid exceeds the SMs
+// the bf16 output goes out as one bulk tensor store per (CTA, column half)
+// from the Q tile, which is dead once o_full has fired.
 constexpr int V2_THREADS = 288;
 
 template <int NT, bool EXTB = false>
